@@ -1,0 +1,225 @@
+/*
+ * b200paint.h -- C-ABI of libb200paint.so, the B200-native (sm_100a) drop-in
+ * for the reference's `mg-oras` path: reduced full multigrid with the
+ * Robin-optimised restricted-additive-Schwarz (ORAS) block smoother for
+ * homogeneous-diffusion inpainting (arXiv 2401.06744).
+ *
+ * The reference (`diffpaint`, pure Python/NumPy) has no FFI boundary of its
+ * own; its boundary is the Python API.  Each entry point below names the
+ * reference interface it replaces (paths relative to
+ * /root/reference/pkg/src/diffpaint/).  INTEGRATION.md shows the ctypes stub a
+ * maintainer of the reference would add.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no C++/torch types cross this boundary;
+ *   - every function returns 0 on success, <0 for an argument/usage error,
+ *     >0 for a CUDA runtime error code; b200p_last_error() gives the text;
+ *   - "d_" pointers are device pointers owned by the caller, "h_" pointers are
+ *     host pointers; fields are row-major fp64 (core.py:14-16), masks are one
+ *     byte per pixel (0 / non-zero);
+ *   - a plan is not thread-safe; different plans may be used concurrently;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream);
+ *   - there is NO CPU fallback: without a CUDA device every compute entry
+ *     point fails with a CUDA error.
+ */
+#ifndef B200PAINT_H
+#define B200PAINT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define B200P_MAX_LEVELS 32
+#define B200P_MAX_HISTORY 128  /* v_cycles_max + 1 entries are kept, capped here */
+#define B200P_MAX_BLOCK 64     /* largest supported block edge */
+
+enum {
+    B200P_OK = 0,
+    B200P_ERR_ARG = -1,         /* ValueError in the reference */
+    B200P_ERR_EMPTY_MASK = -2,  /* EmptyMaskError (core.py:28-33, multigrid.py:442-443) */
+    B200P_ERR_UNSUPPORTED = -3,
+    B200P_ERR_STATE = -4
+};
+
+/* MultigridConfig (multigrid.py:50-82) + SolverConfig (solvers.py:43-69) +
+ * the problem geometry (InpaintingProblem, core.py:118-166). */
+typedef struct b200p_config {
+    int width, height, channels;  /* W, H, C of one frame */
+    int frames;                   /* frames batched in one plan (independent problems) */
+    double spacing;               /* InpaintingProblem.spacing, > 0 */
+    int block_size, overlap;      /* MultigridConfig.block_size / overlap */
+    int nu_pre, nu_post;          /* smoothing sweeps around the coarse correction */
+    int v_cycles_max;             /* MultigridConfig.v_cycles_max */
+    int value_downsampling;       /* 1 = "modified", 0 = "naive" */
+    double coarse_tol;            /* MultigridConfig.coarse_tol */
+    int coarse_max_iters;         /* MultigridConfig.coarse_max_iters */
+    double tol_rel;               /* SolverConfig.tol_rel */
+    double alpha;                 /* SolverConfig.alpha (Robin weight) */
+    double eta;                   /* SolverConfig.local_tol_fraction */
+    int local_max_iters;          /* SolverConfig.local_max_iters, 0 = None -> 4*bh*bw */
+    int use_graphs;               /* 1: replay cascade / V-cycle as CUDA graphs */
+    int spec_cycles;              /* V-cycles enqueued between host convergence checks (>=1) */
+} b200p_config;
+
+/* SolveReport (solvers.py:72-94), one per (frame, channel). */
+typedef struct b200p_report {
+    int iterations;               /* V-cycles */
+    int converged;
+    int fine_smoother_iterations;
+    int history_len;
+    double final_rel_residual;
+    double baseline_residual;
+    double init_residual;
+    double history[B200P_MAX_HISTORY];
+} b200p_report;
+
+typedef struct b200p_level_info {
+    int height, width;
+    int nx, ny, block_w, block_h;
+    double spacing;
+} b200p_level_info;
+
+typedef struct b200p_plan b200p_plan;
+
+const char *b200p_last_error(void);
+int b200p_device_count(void);
+
+/* Defaults of MultigridConfig()/SolverConfig() for a W x H x C problem. */
+void b200p_config_default(b200p_config *cfg, int width, int height, int channels);
+
+/* ---- host-side geometry (no GPU needed) -------------------------------- */
+
+/* partition._axis_starts (partition.py:84-90).  Returns the block count and
+ * writes min(count, cap) starts. */
+int b200p_axis_starts(int dim, int block, int overlap, int64_t *out, int cap);
+/* partition._axis_weights (partition.py:137-154).  w is (n, block_dim) with
+ * block_dim = min(block, dim). */
+int b200p_axis_weights(int dim, int block, int overlap, double *w, int cap);
+/* Level shapes of build_hierarchy (multigrid.py:236-261).  Returns the level
+ * count; fills min(count, cap) entries. */
+int b200p_level_shapes(int width, int height, double spacing, int block, int overlap,
+                       b200p_level_info *out, int cap);
+
+/* ---- plan -------------------------------------------------------------- */
+
+/* Validates the configuration (same ValueError conditions as
+ * MultigridConfig.__post_init__, SolverConfig.__post_init__,
+ * build_partition), builds level geometry, partition-of-unity tables and all
+ * device scratch.  Replaces build_hierarchy's geometry half + Level.__init__
+ * (multigrid.py:189-207) + BlockSolver.__init__ (solvers.py:266-301). */
+int b200p_plan_create(const b200p_config *cfg, b200p_plan **out);
+void b200p_plan_destroy(b200p_plan *plan);
+int b200p_plan_num_levels(const b200p_plan *plan);
+int b200p_plan_level_info(const b200p_plan *plan, int level, b200p_level_info *out);
+/* Bytes of device memory the plan holds. */
+int64_t b200p_plan_device_bytes(const b200p_plan *plan);
+/* Kernel launches issued by the plan since creation (graph replays count the
+ * kernel nodes they contain). */
+int64_t b200p_plan_launch_count(const b200p_plan *plan);
+
+/* Per-kernel timing for the roofline report.  While enabled, solves run eagerly
+ * (no graph replay) with a CUDA event pair around every kernel launch on the
+ * launching stream.  `kind` indexes the kernel classes 0..profile_kinds()-1
+ * (names from b200p_plan_profile_name); _get returns the accumulated device
+ * milliseconds, launch count and algorithmic bytes since enable. */
+int b200p_plan_profile(b200p_plan *plan, int enable);
+int b200p_plan_profile_kinds(void);
+const char *b200p_plan_profile_name(int kind);
+int b200p_plan_profile_get(b200p_plan *plan, int kind, double *ms, int64_t *launches, double *bytes);
+
+/* solve_image(problem, "mg-oras", cfg) (pipelines.py:96-114) for `frames`
+ * frames at once: d_mask (frames,H,W) bytes, d_known (frames,C,H,W) fp64,
+ * d_out (frames,C,H,W) fp64, h_reports frames*C entries (host).  Enqueues on
+ * `stream` and synchronises it before returning (the V-cycle loop is
+ * convergence-controlled).  The caller must have checked the masks are not
+ * empty (b200p_solve_host does). */
+int b200p_solve(b200p_plan *plan, const uint8_t *d_mask, const double *d_known, double *d_out,
+                b200p_report *h_reports, void *stream);
+
+/* Same through HOST buffers: H2D of mask+known, solve, D2H of the result.
+ * Returns B200P_ERR_EMPTY_MASK if any frame's mask is all zero. */
+int b200p_solve_host(b200p_plan *plan, const uint8_t *h_mask, const double *h_known, double *h_out,
+                     b200p_report *h_reports);
+
+/* 8-bit ingest/egress variant (fileio.image_from_fields, fileio.py:58-65):
+ * h_known_u8 (frames,C,H,W) uint8, result rounded half-to-even and clipped to
+ * [0,255] on the device.  h_out_u8 (frames,C,H,W). */
+int b200p_solve_host_u8(b200p_plan *plan, const uint8_t *h_mask, const uint8_t *h_known_u8,
+                        uint8_t *h_out_u8, b200p_report *h_reports);
+
+/* ---- stage entry points (A/B tests against the reference functions) ---- */
+
+/* build_hierarchy's data half (multigrid.py:249-260): coarsen mask and known
+ * values down all levels of the plan. */
+int b200p_plan_build_hierarchy(b200p_plan *plan, const uint8_t *d_mask, const double *d_known,
+                               void *stream);
+/* Device pointers of level data after build_hierarchy: mask (frames,h,w)
+ * bytes; rhs (frames*C,h,w) fp64 (level 0: NULL, rhs is where(mask,known,0)). */
+int b200p_plan_level_ptrs(const b200p_plan *plan, int level, const uint8_t **d_mask,
+                          const double **d_rhs);
+/* cascadic_init (multigrid.py:374-386) after build_hierarchy; d_u (frames*C,H,W). */
+int b200p_plan_cascade(b200p_plan *plan, double *d_u, void *stream);
+/* v_cycle(hier, level, u, rhs, cfg, counters) (multigrid.py:335-371): one
+ * V-cycle at `level` on d_u/d_rhs (frames*C planes of that level's shape),
+ * after build_hierarchy.  fine_units (host, frames*C, may be NULL) receives
+ * the finest-level smoothing units when level == 0. */
+int b200p_plan_vcycle(b200p_plan *plan, int level, double *d_u, const double *d_rhs,
+                      int *h_fine_units, void *stream);
+/* fmg_solve's second half after cascade: not exposed separately; use b200p_solve. */
+
+/* oras_sweeps(op, blocks, b, u, max_sweeps=, stop_norm=, eta=, local_max_iters=)
+ * (solvers.py:393-424) on level `level` of the plan (after build_hierarchy for
+ * the masks), d_u/d_b (frames*C planes).  Per problem: sweeps done and final
+ * residual norm (host arrays, frames*C).  path: 0 auto, 1 force the generic
+ * kernel, 2 force the warp-tile kernel (error if the level is ineligible). */
+int b200p_plan_oras_sweeps(b200p_plan *plan, int level, const double *d_b, double *d_u,
+                           int max_sweeps, double stop_norm, int path, int *h_sweeps,
+                           double *h_rn, void *stream);
+/* BlockSolver.gather + solve_blocks (solvers.py:303-305, :372-390) on a given
+ * residual field d_r, target_sq as in the reference; d_v (frames*C, nblocks,
+ * bh, bw) receives the UNWEIGHTED local corrections.  Generic kernel only. */
+int b200p_plan_solve_blocks(b200p_plan *plan, int level, const double *d_r, double target_sq,
+                            double *d_v, void *stream);
+
+/* StencilOperator.apply / residual (core.py:100-110) on one (h,w) field. */
+int b200p_apply(const uint8_t *d_mask, int h, int w, double spacing, const double *d_u,
+                double *d_out, void *stream);
+int b200p_residual(const uint8_t *d_mask, int h, int w, double spacing, const double *d_b,
+                   const double *d_u, double *d_r, void *stream);
+/* ||b - A u||^2 per plane (planes fields sharing one mask). */
+int b200p_residual_sqnorm(const uint8_t *d_mask, int h, int w, double spacing, const double *d_b,
+                          const double *d_u, int planes, double *h_out, void *stream);
+
+/* Transfers (multigrid.py:98-186); coarse shapes are ceil(h/2) x ceil(w/2). */
+int b200p_downsample_mask(const uint8_t *d_fine, int h, int w, uint8_t *d_coarse, void *stream);
+int b200p_downsample_values(const uint8_t *d_fine_mask, const uint8_t *d_coarse_mask,
+                            const double *d_fine_rhs, int h, int w, int modified,
+                            double *d_coarse_rhs, void *stream);
+/* residual + restrict_residual fused (multigrid.py:358-360). */
+int b200p_residual_restrict(const uint8_t *d_fine_mask, const uint8_t *d_coarse_mask, int h, int w,
+                            double spacing, const double *d_b, const double *d_u,
+                            double *d_coarse_r, void *stream);
+/* restrict_residual alone on a given fine residual field (multigrid.py:149-154). */
+int b200p_restrict_residual(const double *d_fine_r, const uint8_t *d_coarse_mask, int h, int w,
+                            double *d_coarse_r, void *stream);
+/* u += prolongate_correction(e, mask) (multigrid.py:367, :175-177). */
+int b200p_prolongate_correct(const double *d_coarse_e, const uint8_t *d_fine_mask, int h, int w,
+                             double *d_u, void *stream);
+/* u = prolongate_solution(coarse_u, mask, rhs) (multigrid.py:180-186). */
+int b200p_prolongate_solution(const double *d_coarse_u, const uint8_t *d_fine_mask,
+                              const double *d_fine_rhs, int h, int w, double *d_u, void *stream);
+
+/* ---- small device-memory helpers for host languages without a CUDA binding */
+int b200p_malloc(void **d_ptr, int64_t bytes);
+int b200p_free(void *d_ptr);
+int b200p_memcpy_h2d(void *d_dst, const void *h_src, int64_t bytes);
+int b200p_memcpy_d2h(void *h_dst, const void *d_src, int64_t bytes);
+int b200p_memset(void *d_ptr, int value, int64_t bytes);
+int b200p_device_synchronize(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200PAINT_H */

@@ -1,0 +1,60 @@
+"""Device-memory handoff: torch CUDA tensors carry the buffers, nothing else.
+
+PyTorch is plumbing here (allocation, streams, pinned host memory); all
+arithmetic of the path happens inside libb200paint.so.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+def require_cuda():
+    if not torch.cuda.is_available() or _lib.lib().b200p_device_count() < 1:
+        raise _lib.B200PaintError(
+            "no CUDA device: paper_2401_06744_b200 has no CPU fallback (sm_100a kernels only)")
+
+
+def device():
+    require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream() -> int:
+    return int(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t) -> int:
+    return int(t.data_ptr())
+
+
+def call(name, *args):
+    return _lib.check(getattr(_lib.lib(), name)(*args))
+
+
+def to_device_f64(a) -> torch.Tensor:
+    t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+    return t.to(device(), non_blocking=False)
+
+
+def to_device_u8(a) -> torch.Tensor:
+    a = np.asarray(a)
+    if a.dtype != np.uint8:
+        a = a.astype(bool).astype(np.uint8)
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device())
+
+
+def empty_f64(shape) -> torch.Tensor:
+    return torch.empty(tuple(shape), dtype=torch.float64, device=device())
+
+
+def empty_u8(shape) -> torch.Tensor:
+    return torch.empty(tuple(shape), dtype=torch.uint8, device=device())
+
+
+def to_host(t: torch.Tensor) -> np.ndarray:
+    torch.cuda.current_stream().synchronize()
+    return t.cpu().numpy()

@@ -1,0 +1,1323 @@
+// b200paint.cu -- host driver + C-ABI of libb200paint.so (sm_100a only).
+//
+// Implements include/b200paint.h: plan construction (level geometry, partition
+// of unity tables, device scratch), the FMG / V-cycle driver of the reference's
+// mg-oras path (multigrid.py:335-487, pipelines.py:96-114) as CUDA-graph
+// replays, and stage-level entry points for A/B tests against the reference
+// functions.  Frames x channels are batched as independent "problems" p.
+//
+// There is no CPU fallback anywhere in this file: every compute entry point
+// launches CUDA kernels and returns the CUDA error if no device is present.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/b200paint.h"
+#include "kernels_stencil.cuh"
+#include "kernels_oras.cuh"
+
+using namespace b200p;
+
+// ------------------------------------------------------------- errors ------
+static thread_local std::string g_err;
+
+static int fail_arg(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+static int fail_cuda(cudaError_t e, const char *what) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return (int)e > 0 ? (int)e : 999;
+}
+
+#define CU(x)                                            \
+    do {                                                 \
+        cudaError_t e__ = (x);                           \
+        if (e__ != cudaSuccess) return fail_cuda(e__, #x); \
+    } while (0)
+
+// ------------------------------------------------------------ geometry -----
+// partition._axis_starts (partition.py:84-90)
+static std::vector<int> axis_starts(int dim, int block, int stride) {
+    std::vector<int> s;
+    if (dim <= block) {
+        s.push_back(0);
+        return s;
+    }
+    const int count = (dim - block + stride - 1) / stride + 1;
+    for (int i = 0; i < count; ++i) s.push_back(stride * i);
+    s[count - 1] = dim - block;
+    return s;
+}
+
+// partition._axis_weights (partition.py:137-154); block = min(block_size, dim).
+static std::vector<double> axis_weights(const std::vector<int> &starts, int block, int dim,
+                                        int overlap) {
+    const int n = (int)starts.size();
+    std::vector<double> w((size_t)n * block, 1.0);
+    if (overlap > 0) {
+        // np.linspace(0, 1, overlap): k * step, endpoint forced to 1; [0.0] for overlap == 1
+        std::vector<double> ramp(overlap);
+        if (overlap == 1) {
+            ramp[0] = 0.0;
+        } else {
+            const double step = 1.0 / (double)(overlap - 1);
+            for (int k = 0; k < overlap; ++k) ramp[k] = (double)k * step;
+            ramp[overlap - 1] = 1.0;
+        }
+        for (int i = 0; i < n; ++i) {
+            if (starts[i] > 0)
+                for (int k = 0; k < overlap && k < block; ++k) w[(size_t)i * block + k] *= ramp[k];
+            if (starts[i] + block < dim)
+                for (int k = 0; k < overlap && k < block; ++k)
+                    w[(size_t)i * block + block - overlap + k] *= ramp[overlap - 1 - k];
+        }
+    }
+    std::vector<double> total(dim, 0.0);
+    for (int i = 0; i < n; ++i)
+        for (int k = 0; k < block; ++k) total[starts[i] + k] += w[(size_t)i * block + k];
+    for (int i = 0; i < n; ++i)
+        for (int k = 0; k < block; ++k) w[(size_t)i * block + k] /= total[starts[i] + k];
+    return w;
+}
+
+// first covering block and number of covering blocks of every pixel on an axis
+static void axis_cover(const std::vector<int> &starts, int block, int dim, std::vector<int> &first,
+                       std::vector<int> &count) {
+    first.assign(dim, 0);
+    count.assign(dim, 0);
+    for (int i = (int)starts.size() - 1; i >= 0; --i)
+        for (int k = 0; k < block; ++k) {
+            first[starts[i] + k] = i;
+            count[starts[i] + k] += 1;
+        }
+}
+
+static int level_shapes(int width, int height, double spacing, int block, int overlap,
+                        std::vector<b200p_level_info> &out) {
+    int h = height, w = width;
+    const int stride = block - overlap;
+    for (;;) {
+        b200p_level_info L;
+        L.height = h;
+        L.width = w;
+        L.block_w = std::min(block, w);
+        L.block_h = std::min(block, h);
+        L.nx = (int)axis_starts(w, block, stride).size();
+        L.ny = (int)axis_starts(h, block, stride).size();
+        L.spacing = spacing;
+        out.push_back(L);
+        if (std::max(h, w) <= block || (int)out.size() >= B200P_MAX_LEVELS) break;
+        h = (h + 1) / 2;
+        w = (w + 1) / 2;
+        spacing *= 2.0;
+    }
+    return (int)out.size();
+}
+
+// --------------------------------------------------------------- plan ------
+enum KernelKind {
+    KK_NORM = 0,      // K1
+    KK_SWEEP,         // K2 / K2g
+    KK_COMBINE,       // K2b
+    KK_RESTRICT,      // K3
+    KK_PROLONG_CORR,  // K4
+    KK_PROLONG_SOL,   // K5
+    KK_DOWN_MASK,     // K6a
+    KK_DOWN_VALUES,   // K6b
+    KK_COARSE,        // K7
+    KK_CONTROL,       // per-problem bookkeeping
+    KK_CONVERT,       // u8 ingest / egress
+    KK_COUNT
+};
+
+static const char *const kKindNames[KK_COUNT] = {
+    "residual_sqnorm", "oras_sweep", "oras_combine", "residual_restrict", "prolongate_correct",
+    "prolongate_solution", "downsample_mask", "downsample_values", "coarse_solve", "control",
+    "convert_u8"};
+
+struct LevelHost {
+    b200p_level_info info;
+    int nblocks = 0;
+    LevelDev dev;
+    uint8_t *d_mask = nullptr;  // (F,h,w); level 0: caller's pointer
+    double *d_rhs = nullptr;    // (P,h,w) hierarchy values; level 0: caller's `known`
+    double *d_u = nullptr;      // (P,h,w) cascade iterate / V-cycle correction (levels >= 1)
+    double *d_rc = nullptr;     // (P,h,w) restricted residual (levels >= 1)
+    int tile = 0;               // K2 variant: 0 generic, else see launch_sweep
+};
+
+struct ProfEvent {
+    int kind;
+    double bytes;
+    cudaEvent_t a, b;
+};
+
+struct GraphSlot {
+    cudaGraphExec_t exec = nullptr;
+    const void *k0 = nullptr, *k1 = nullptr, *k2 = nullptr;  // pointers baked into the graph
+    int64_t kernels = 0;
+};
+
+struct b200p_plan {
+    b200p_config cfg;
+    int F = 0, C = 0, P = 0;
+    std::vector<LevelHost> lev;
+    std::vector<void *> owned;  // device allocations
+    int64_t dev_bytes = 0;
+    int64_t launches = 0;
+    int64_t *launch_sink = nullptr;  // where launches are counted (graph capture: the slot)
+    // sweep scratch + norm reduction
+    double *d_scratch = nullptr;
+    int norm_ctas = 0;
+    double *d_partial = nullptr;
+    int *d_partial_flag = nullptr;
+    unsigned *d_counter = nullptr;
+    double *d_rs = nullptr;
+    int *d_mflag = nullptr;
+    // per-problem FMG control (multigrid.py:466-486)
+    int *d_active = nullptr, *d_cycles = nullptr, *d_units = nullptr, *d_histlen = nullptr;
+    int *d_any = nullptr;
+    double *d_baseline = nullptr, *d_denom = nullptr, *d_rel = nullptr, *d_hist = nullptr;
+    int *d_gate = nullptr, *d_sweeps = nullptr;  // stage API (oras_sweeps with stop_norm)
+    double *d_rn = nullptr;
+    int *h_any = nullptr;  // pinned
+    // staging for the host entry points
+    uint8_t *d_in_mask = nullptr;
+    double *d_in_known = nullptr, *d_out = nullptr;
+    uint8_t *d_io_u8 = nullptr;
+    void *h_pin = nullptr;  // pinned bounce buffer
+    size_t h_pin_bytes = 0;
+    cudaStream_t own_stream = nullptr;
+    bool hierarchy_ready = false;
+    // graphs
+    GraphSlot g_front, g_cycle;
+    // profiling
+    bool profiling = false;
+    std::vector<ProfEvent> prof_events;
+    double prof_ms[KK_COUNT] = {0};
+    double prof_bytes[KK_COUNT] = {0};
+    int64_t prof_launches[KK_COUNT] = {0};
+};
+
+template <class T>
+static int dev_alloc(b200p_plan *pl, T **out, size_t count) {
+    void *p = nullptr;
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    CU(cudaMalloc(&p, bytes));
+    pl->owned.push_back(p);
+    pl->dev_bytes += (int64_t)bytes;
+    *out = reinterpret_cast<T *>(p);
+    return 0;
+}
+
+template <class T>
+static int dev_upload(b200p_plan *pl, const std::vector<T> &v, const T **out) {
+    T *d = nullptr;
+    int rc = dev_alloc(pl, &d, v.size());
+    if (rc) return rc;
+    CU(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    *out = d;
+    return 0;
+}
+
+// Launch bracket: counts the launch, and in profiling mode wraps it in a CUDA
+// event pair on the launching stream.
+struct LaunchScope {
+    b200p_plan *pl;
+    cudaStream_t st;
+    int idx = -1;
+    LaunchScope(b200p_plan *p, cudaStream_t s, int kind, double bytes) : pl(p), st(s) {
+        if (pl->launch_sink) *pl->launch_sink += 1; else pl->launches += 1;
+        if (pl->profiling) {
+            ProfEvent e;
+            e.kind = kind;
+            e.bytes = bytes;
+            cudaEventCreate(&e.a);
+            cudaEventCreate(&e.b);
+            cudaEventRecord(e.a, st);
+            pl->prof_events.push_back(e);
+            idx = (int)pl->prof_events.size() - 1;
+        }
+    }
+    ~LaunchScope() {
+        if (idx >= 0) cudaEventRecord(pl->prof_events[idx].b, st);
+    }
+};
+
+static void prof_collect(b200p_plan *pl) {
+    for (auto &e : pl->prof_events) {
+        float ms = 0.f;
+        cudaEventSynchronize(e.b);
+        cudaEventElapsedTime(&ms, e.a, e.b);
+        pl->prof_ms[e.kind] += ms;
+        pl->prof_bytes[e.kind] += e.bytes;
+        pl->prof_launches[e.kind] += 1;
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
+    pl->prof_events.clear();
+}
+
+// ------------------------------------------------- control kernels ---------
+// fmg_solve bookkeeping (multigrid.py:446, :468-479), one thread per problem.
+// stage 0: baseline = sqrt(rs)            (flat-init defect)
+// stage 1: first check after the cascade  (denom, rel, history[0], active)
+// stage 2: check after a V-cycle          (cycles+1, rel, history, active)
+__global__ void fmg_control_kernel(int P, int stage, const double *rs, double tol, int cycles_max,
+                                   double *baseline, double *denom, double *rel, double *hist,
+                                   int *histlen, int *active, int *cycles, int *units, int *any) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    const double rn = sqrt(rs[p]);
+    if (stage == 0) {
+        baseline[p] = rn;
+        units[p] = 0;
+        cycles[p] = 0;
+        histlen[p] = 0;
+        active[p] = 1;
+        return;
+    }
+    if (stage == 1) {
+        const double base = baseline[p];
+        const double d = base > 0.0 ? base : (rn > 0.0 ? rn : 1.0);
+        denom[p] = d;
+        const double r = rn / d;
+        rel[p] = r;
+        hist[(size_t)p * B200P_MAX_HISTORY] = r;
+        histlen[p] = 1;
+        const int act = (r > tol && 0 < cycles_max) ? 1 : 0;
+        active[p] = act;
+        if (act) atomicOr(any, 1);
+        return;
+    }
+    if (!active[p]) return;
+    const int c = cycles[p] + 1;
+    cycles[p] = c;
+    const double r = rn / denom[p];
+    rel[p] = r;
+    const int hl = histlen[p];
+    if (hl < B200P_MAX_HISTORY) {
+        hist[(size_t)p * B200P_MAX_HISTORY + hl] = r;
+        histlen[p] = hl + 1;
+    }
+    const int act = (r > tol && c < cycles_max) ? 1 : 0;
+    active[p] = act;
+    if (act) atomicOr(any, 1);
+}
+
+__global__ void set_int_kernel(int *p, int n, int v) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+// oras_sweeps exit test (solvers.py:416-421) for the stage API.
+__global__ void sweep_gate_kernel(int P, const double *rs, double stop_norm, int max_sweeps,
+                                  int *gate, const int *sweeps, double *rn_out, int *any) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P || !gate[p]) return;
+    const double r2 = rs[p];
+    const double rn = sqrt(r2);
+    rn_out[p] = rn;
+    if (r2 == 0.0 || rn <= stop_norm || sweeps[p] >= max_sweeps) gate[p] = 0;
+    else atomicOr(any, 1);
+}
+
+// ------------------------------------------------------ launch helpers -----
+static inline dim3 grid2x(int wc, int hc, int z) { return dim3((wc + 63) / 64, (hc + 3) / 4, z); }
+
+static double field_bytes(const b200p_plan *pl, const LevelHost &L, double fields, double masks) {
+    const double n = (double)L.info.height * L.info.width;
+    return fields * pl->P * 8.0 * n + masks * pl->F * n;
+}
+
+// K1: rs[p] = ||b - A u||^2, mflag[p].  UM/RM as in residual_px.
+static int launch_norm(b200p_plan *pl, const LevelHost &L, const double *u, const double *b,
+                       bool um, bool rm, const int *pred, cudaStream_t st) {
+    const size_t plane = (size_t)L.info.height * L.info.width;
+    dim3 grid(pl->norm_ctas, pl->P);
+    LaunchScope sc(pl, st, KK_NORM, field_bytes(pl, L, rm ? 1.0 : 2.0, 1.0));
+#define NORM_ARGS u, b, L.d_mask, L.info.height, L.info.width, L.dev.hinv2, pl->C, plane, pred, \
+                  pl->d_partial, pl->d_partial_flag, pl->d_counter, pl->d_rs, pl->d_mflag
+    if (um && rm) residual_sqnorm_kernel<true, true><<<grid, ST_THREADS, 0, st>>>(NORM_ARGS);
+    else if (rm) residual_sqnorm_kernel<false, true><<<grid, ST_THREADS, 0, st>>>(NORM_ARGS);
+    else if (um) residual_sqnorm_kernel<true, false><<<grid, ST_THREADS, 0, st>>>(NORM_ARGS);
+    else residual_sqnorm_kernel<false, false><<<grid, ST_THREADS, 0, st>>>(NORM_ARGS);
+#undef NORM_ARGS
+    CU(cudaGetLastError());
+    return 0;
+}
+
+static int local_cap(const b200p_plan *pl, const LevelHost &L) {
+    return pl->cfg.local_max_iters > 0 ? pl->cfg.local_max_iters
+                                       : 4 * L.info.block_h * L.info.block_w;
+}
+
+// Tile variants of K2 (block extent -> <TW,TH,NWARP>).
+enum { TILE_GENERIC = 0, TILE_32_A = 1, TILE_16 = 2, TILE_8 = 3, TILE_32_B = 4, TILE_32_C = 5 };
+
+static int tile_for(int bw, int bh) {
+    if (bw == 32 && bh == 32) {
+        const char *e = getenv("B200P_TILE32");
+        if (e && *e == 'B') return TILE_32_B;
+        if (e && *e == 'C') return TILE_32_C;
+        return TILE_32_A;
+    }
+    if (bw == 16 && bh == 16) return TILE_16;
+    if (bw == 8 && bh == 8) return TILE_8;
+    return TILE_GENERIC;
+}
+
+template <int TW, int TH, int NWARP>
+static void launch_tile(const SweepArgs &A, bool rm, dim3 grid, cudaStream_t st) {
+    if (rm) oras_sweep_tile_kernel<TW, TH, NWARP, true><<<grid, NWARP * 32, 0, st>>>(A);
+    else oras_sweep_tile_kernel<TW, TH, NWARP, false><<<grid, NWARP * 32, 0, st>>>(A);
+}
+
+// K2 + K2b: one ORAS sweep using rs/mflag from the preceding K1.
+static int launch_sweep(b200p_plan *pl, const LevelHost &L, double *u, const double *b, bool rm,
+                        const int *pred, int *unit_counter, int force_tile, cudaStream_t st) {
+    SweepArgs A;
+    A.L = L.dev;
+    A.u = u;
+    A.b = b;
+    A.mask = L.d_mask;
+    A.channels = pl->C;
+    A.plane = (size_t)L.info.height * L.info.width;
+    A.pred = pred;
+    A.rs = pl->d_rs;
+    A.mflag = pl->d_mflag;
+    A.eta = pl->cfg.eta;
+    A.max_iters = local_cap(pl, L);
+    A.scratch = pl->d_scratch;
+    const int tile = force_tile >= 0 ? force_tile : L.tile;
+    dim3 grid(L.nblocks, pl->P);
+    {
+        // sweep = read u (+ b) + mask, write weighted corrections
+        LaunchScope sc(pl, st, KK_SWEEP, field_bytes(pl, L, rm ? 2.0 : 3.0, 1.0));
+        switch (tile) {
+            case TILE_32_A: launch_tile<4, 2, 4>(A, rm, grid, st); break;
+            case TILE_32_B: launch_tile<4, 4, 2>(A, rm, grid, st); break;
+            case TILE_32_C: launch_tile<4, 1, 8>(A, rm, grid, st); break;
+            case TILE_16: launch_tile<2, 4, 1>(A, rm, grid, st); break;
+            case TILE_8: launch_tile<1, 2, 1>(A, rm, grid, st); break;
+            default: {
+                const size_t smem = smem_cg_bytes(L.info.block_w, L.info.block_h);
+                if (rm) oras_sweep_generic_kernel<true, 0><<<grid, GEN_THREADS, smem, st>>>(A);
+                else oras_sweep_generic_kernel<false, 0><<<grid, GEN_THREADS, smem, st>>>(A);
+            }
+        }
+        CU(cudaGetLastError());
+    }
+    {
+        dim3 g((L.info.width + 127) / 128, (L.info.height + 1) / 2, pl->P);
+        LaunchScope sc(pl, st, KK_COMBINE, field_bytes(pl, L, 2.0, 0.0));
+        oras_combine_kernel<<<g, ST_THREADS_COMBINE, 0, st>>>(L.dev, pl->d_scratch, A.plane, pred,
+                                                              pl->d_rs, u, unit_counter);
+        CU(cudaGetLastError());
+    }
+    return 0;
+}
+
+// _smooth (multigrid.py:264-279): `units` sweeps with stop_norm = 0.  When
+// have_norm is set, rs/mflag already describe (u, b) and the first K1 is skipped.
+static int enqueue_smooth(b200p_plan *pl, const LevelHost &L, double *u, const double *b, bool rm,
+                          int units, const int *pred, int *unit_counter, bool have_norm,
+                          cudaStream_t st) {
+    for (int i = 0; i < units; ++i) {
+        if (!(have_norm && i == 0)) {
+            int rc = launch_norm(pl, L, u, b, false, rm, pred, st);
+            if (rc) return rc;
+        }
+        int rc = launch_sweep(pl, L, u, b, rm, pred, unit_counter, -1, st);
+        if (rc) return rc;
+    }
+    return 0;
+}
+
+static int launch_coarse(b200p_plan *pl, const LevelHost &L, double *u, const double *b,
+                         bool rhs_masked, int init_mode, double tol, int max_sweeps, const int *pred,
+                         int *units_out, int accumulate, cudaStream_t st) {
+    CoarseArgs A;
+    A.L = L.dev;
+    A.u = u;
+    A.b = b;
+    A.mask = L.d_mask;
+    A.channels = pl->C;
+    A.pred = pred;
+    A.tol = tol;
+    A.max_sweeps = max_sweeps;
+    A.eta = pl->cfg.eta;
+    A.max_iters = local_cap(pl, L);
+    A.rhs_masked = rhs_masked ? 1 : 0;
+    A.init_mode = init_mode;
+    A.units_out = units_out;
+    A.units_accumulate = accumulate;
+    A.rel_out = nullptr;
+    const size_t n = (size_t)L.info.block_w * L.info.block_h;
+    const size_t smem = smem_cg_bytes(L.info.block_w, L.info.block_h) + 2 * n * sizeof(double);
+    LaunchScope sc(pl, st, KK_COARSE, field_bytes(pl, L, 3.0, 1.0));
+    coarse_solve_kernel<<<pl->P, GEN_THREADS, smem, st>>>(A);
+    CU(cudaGetLastError());
+    return 0;
+}
+
+static int launch_control(b200p_plan *pl, int stage, cudaStream_t st) {
+    LaunchScope sc(pl, st, KK_CONTROL, 0.0);
+    fmg_control_kernel<<<(pl->P + 127) / 128, 128, 0, st>>>(
+        pl->P, stage, pl->d_rs, pl->cfg.tol_rel, pl->cfg.v_cycles_max, pl->d_baseline, pl->d_denom,
+        pl->d_rel, pl->d_hist, pl->d_histlen, pl->d_active, pl->d_cycles, pl->d_units, pl->d_any);
+    CU(cudaGetLastError());
+    return 0;
+}
+
+static int launch_set_int(b200p_plan *pl, int *p, int n, int v, cudaStream_t st) {
+    LaunchScope sc(pl, st, KK_CONTROL, 0.0);
+    set_int_kernel<<<(n + 127) / 128, 128, 0, st>>>(p, n, v);
+    CU(cudaGetLastError());
+    return 0;
+}
+
+// build_hierarchy's data half (multigrid.py:249-260).
+static int enqueue_hierarchy(b200p_plan *pl, cudaStream_t st) {
+    const int nl = (int)pl->lev.size();
+    for (int l = 0; l + 1 < nl; ++l) {
+        const LevelHost &f = pl->lev[l];
+        LevelHost &c = pl->lev[l + 1];
+        const int h = f.info.height, w = f.info.width;
+        {
+            LaunchScope sc(pl, st, KK_DOWN_MASK, 1.25 * pl->F * (double)h * w);
+            downsample_mask_kernel<<<grid2x(c.info.width, c.info.height, pl->F), ST_THREADS, 0, st>>>(
+                f.d_mask, h, w, c.d_mask);
+            CU(cudaGetLastError());
+        }
+        {
+            LaunchScope sc(pl, st, KK_DOWN_VALUES, field_bytes(pl, f, 1.25, 1.25));
+            downsample_values_kernel<<<grid2x(c.info.width, c.info.height, pl->P), ST_THREADS, 0, st>>>(
+                f.d_mask, c.d_mask, f.d_rhs, h, w, pl->C, pl->cfg.value_downsampling, c.d_rhs);
+            CU(cudaGetLastError());
+        }
+    }
+    return 0;
+}
+
+// _cascade(to_tol=False) (multigrid.py:389-422) into d_u0 (level-0 iterate).
+static int enqueue_cascade(b200p_plan *pl, double *d_u0, cudaStream_t st) {
+    const int nl = (int)pl->lev.size();
+    const double tol = std::min(pl->cfg.coarse_tol, pl->cfg.tol_rel);
+    LevelHost &co = pl->lev[nl - 1];
+    if (nl == 1) {
+        // single level: the coarse solve IS the finest level; its sweeps count as fine units
+        return launch_coarse(pl, co, d_u0, co.d_rhs, true, 1, tol, pl->cfg.coarse_max_iters, nullptr,
+                             pl->d_units, 1, st);
+    }
+    int rc = launch_coarse(pl, co, co.d_u, co.d_rhs, true, 1, tol, pl->cfg.coarse_max_iters,
+                           nullptr, nullptr, 0, st);
+    if (rc) return rc;
+    for (int l = nl - 2; l >= 0; --l) {
+        LevelHost &f = pl->lev[l];
+        const LevelHost &c = pl->lev[l + 1];
+        double *uf = l == 0 ? d_u0 : f.d_u;
+        {
+            LaunchScope sc(pl, st, KK_PROLONG_SOL, field_bytes(pl, f, 1.25, 1.0));
+            prolongate_kernel<true><<<grid2x(c.info.width, c.info.height, pl->P), ST_THREADS, 0, st>>>(
+                c.d_u, f.d_mask, f.d_rhs, f.info.height, f.info.width, pl->C, nullptr, uf);
+            CU(cudaGetLastError());
+        }
+        if (l > 0) {
+            rc = enqueue_smooth(pl, f, uf, f.d_rhs, true, 1, nullptr, nullptr, false, st);
+            if (rc) return rc;
+        }
+    }
+    return 0;
+}
+
+// v_cycle (multigrid.py:335-371).  rm: b is read masked (level-0 `known` /
+// hierarchy values); have_norm: rs/mflag are current for (u, b) on entry.
+static int enqueue_vcycle(b200p_plan *pl, int level, double *u, const double *b, bool rm,
+                          const int *pred, int *unit_counter, bool have_norm, cudaStream_t st) {
+    const int nl = (int)pl->lev.size();
+    LevelHost &L = pl->lev[level];
+    const b200p_config &cfg = pl->cfg;
+    int *uc = level == 0 ? unit_counter : nullptr;
+    if (level == nl - 1) {
+        // single-level cycle: nu_pre + nu_post sweeps (always a single block here)
+        return launch_coarse(pl, L, u, b, rm, 2, 0.0, cfg.nu_pre + cfg.nu_post, pred, uc, 1, st);
+    }
+    int rc = enqueue_smooth(pl, L, u, b, rm, cfg.nu_pre, pred, uc, have_norm, st);
+    if (rc) return rc;
+    LevelHost &Cc = pl->lev[level + 1];
+    {
+        LaunchScope sc(pl, st, KK_RESTRICT, field_bytes(pl, L, rm ? 1.25 : 2.25, 1.25));
+        dim3 g = grid2x(Cc.info.width, Cc.info.height, pl->P);
+        // e is zeroed by the coarse solve (init_mode 0) on the coarsest level, else here
+        double *ez = (level + 1 == nl - 1) ? nullptr : Cc.d_u;
+        if (rm)
+            residual_restrict_kernel<true><<<g, ST_THREADS, 0, st>>>(
+                u, b, L.d_mask, Cc.d_mask, L.info.height, L.info.width, L.dev.hinv2, pl->C, pred,
+                Cc.d_rc, ez);
+        else
+            residual_restrict_kernel<false><<<g, ST_THREADS, 0, st>>>(
+                u, b, L.d_mask, Cc.d_mask, L.info.height, L.info.width, L.dev.hinv2, pl->C, pred,
+                Cc.d_rc, ez);
+        CU(cudaGetLastError());
+    }
+    if (level + 1 == nl - 1) {
+        const double tol = std::min(cfg.coarse_tol, cfg.tol_rel);
+        rc = launch_coarse(pl, Cc, Cc.d_u, Cc.d_rc, false, 0, tol, cfg.coarse_max_iters, pred,
+                           nullptr, 0, st);
+    } else {
+        rc = enqueue_vcycle(pl, level + 1, Cc.d_u, Cc.d_rc, false, pred, nullptr, false, st);
+    }
+    if (rc) return rc;
+    {
+        LaunchScope sc(pl, st, KK_PROLONG_CORR, field_bytes(pl, L, 2.25, 1.0));
+        prolongate_kernel<false><<<grid2x(Cc.info.width, Cc.info.height, pl->P), ST_THREADS, 0, st>>>(
+            Cc.d_u, L.d_mask, nullptr, L.info.height, L.info.width, pl->C, pred, u);
+        CU(cudaGetLastError());
+    }
+    return enqueue_smooth(pl, L, u, b, rm, cfg.nu_post, pred, uc, false, st);
+}
+
+// Front half of fmg_solve: hierarchy, baseline, cascade, first convergence check.
+static int enqueue_front(b200p_plan *pl, double *d_out, cudaStream_t st) {
+    LevelHost &L0 = pl->lev[0];
+    int rc = enqueue_hierarchy(pl, st);
+    if (rc) return rc;
+    // baseline = ||b - A b|| with b = where(mask, known, 0) (multigrid.py:446)
+    if ((rc = launch_norm(pl, L0, L0.d_rhs, L0.d_rhs, true, true, nullptr, st))) return rc;
+    if ((rc = launch_control(pl, 0, st))) return rc;
+    if ((rc = enqueue_cascade(pl, d_out, st))) return rc;
+    if ((rc = launch_norm(pl, L0, d_out, L0.d_rhs, false, true, nullptr, st))) return rc;
+    if ((rc = launch_set_int(pl, pl->d_any, 1, 0, st))) return rc;
+    if ((rc = launch_control(pl, 1, st))) return rc;
+    CU(cudaMemcpyAsync(pl->h_any, pl->d_any, sizeof(int), cudaMemcpyDeviceToHost, st));
+    return 0;
+}
+
+// One V-cycle on level 0 + convergence check (multigrid.py:474-479).
+static int enqueue_cycle(b200p_plan *pl, double *d_out, cudaStream_t st) {
+    LevelHost &L0 = pl->lev[0];
+    // rs/mflag are current on entry (the previous check's K1) iff nu_pre > 0 uses them first
+    int rc = enqueue_vcycle(pl, 0, d_out, L0.d_rhs, true, pl->d_active, pl->d_units,
+                            (int)pl->lev.size() > 1, st);
+    if (rc) return rc;
+    if ((rc = launch_norm(pl, L0, d_out, L0.d_rhs, false, true, pl->d_active, st))) return rc;
+    if ((rc = launch_set_int(pl, pl->d_any, 1, 0, st))) return rc;
+    if ((rc = launch_control(pl, 2, st))) return rc;
+    CU(cudaMemcpyAsync(pl->h_any, pl->d_any, sizeof(int), cudaMemcpyDeviceToHost, st));
+    return 0;
+}
+
+template <class F>
+static int run_graph(b200p_plan *pl, GraphSlot &slot, const void *k0, const void *k1, const void *k2,
+                     cudaStream_t st, F &&enqueue) {
+    if (!pl->cfg.use_graphs || pl->profiling) return enqueue(st);
+    if (!slot.exec || slot.k0 != k0 || slot.k1 != k1 || slot.k2 != k2) {
+        if (slot.exec) {
+            cudaGraphExecDestroy(slot.exec);
+            slot.exec = nullptr;
+        }
+        slot.kernels = 0;
+        cudaGraph_t g = nullptr;
+        CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        pl->launch_sink = &slot.kernels;
+        int rc = enqueue(st);
+        pl->launch_sink = nullptr;
+        cudaError_t e = cudaStreamEndCapture(st, &g);
+        if (rc) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        if (e != cudaSuccess) return fail_cuda(e, "cudaStreamEndCapture");
+        e = cudaGraphInstantiate(&slot.exec, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fail_cuda(e, "cudaGraphInstantiate");
+        slot.k0 = k0;
+        slot.k1 = k1;
+        slot.k2 = k2;
+    }
+    CU(cudaGraphLaunch(slot.exec, st));
+    pl->launches += slot.kernels;
+    return 0;
+}
+
+static void bind_level0(b200p_plan *pl, const uint8_t *d_mask, const double *d_known) {
+    pl->lev[0].d_mask = const_cast<uint8_t *>(d_mask);
+    pl->lev[0].d_rhs = const_cast<double *>(d_known);
+}
+
+static int set_smem_attrs() {
+    static bool done = false;
+    if (done) return 0;
+    const int big = 227 * 1024;
+    CU(cudaFuncSetAttribute(coarse_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(cudaFuncSetAttribute(oras_sweep_generic_kernel<true, 0>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(cudaFuncSetAttribute(oras_sweep_generic_kernel<false, 0>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    CU(cudaFuncSetAttribute(oras_sweep_generic_kernel<false, 1>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    done = true;
+    return 0;
+}
+
+// ================================================================ C-ABI =====
+extern "C" {
+
+const char *b200p_last_error(void) { return g_err.c_str(); }
+
+int b200p_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+void b200p_config_default(b200p_config *c, int width, int height, int channels) {
+    memset(c, 0, sizeof *c);
+    c->width = width;
+    c->height = height;
+    c->channels = channels;
+    c->frames = 1;
+    c->spacing = 1.0;
+    c->block_size = 32;
+    c->overlap = 6;
+    c->nu_pre = 1;
+    c->nu_post = 1;
+    c->v_cycles_max = 100;
+    c->value_downsampling = 1;
+    c->coarse_tol = 1e-8;
+    c->coarse_max_iters = 20000;
+    c->tol_rel = 1e-3;
+    c->alpha = 0.5;
+    c->eta = 1e-5;
+    c->local_max_iters = 0;
+    c->use_graphs = 1;
+    c->spec_cycles = 1;
+}
+
+int b200p_axis_starts(int dim, int block, int overlap, int64_t *out, int cap) {
+    if (dim < 1) return fail_arg(B200P_ERR_ARG, "image dimensions must be >= 1, got %d", dim);
+    if (overlap < 0 || block <= overlap)
+        return fail_arg(B200P_ERR_ARG, "need block_size > overlap >= 0, got %d, %d", block, overlap);
+    std::vector<int> s = axis_starts(dim, block, block - overlap);
+    for (int i = 0; i < (int)s.size() && i < cap; ++i) out[i] = s[i];
+    return (int)s.size();
+}
+
+int b200p_axis_weights(int dim, int block, int overlap, double *w, int cap) {
+    if (dim < 1) return fail_arg(B200P_ERR_ARG, "image dimensions must be >= 1, got %d", dim);
+    if (overlap < 0 || block <= overlap)
+        return fail_arg(B200P_ERR_ARG, "need block_size > overlap >= 0, got %d, %d", block, overlap);
+    std::vector<int> s = axis_starts(dim, block, block - overlap);
+    const int bd = std::min(block, dim);
+    std::vector<double> ww = axis_weights(s, bd, dim, overlap);
+    for (int i = 0; i < (int)ww.size() && i < cap; ++i) w[i] = ww[i];
+    return (int)ww.size();
+}
+
+int b200p_level_shapes(int width, int height, double spacing, int block, int overlap,
+                       b200p_level_info *out, int cap) {
+    if (width < 1 || height < 1)
+        return fail_arg(B200P_ERR_ARG, "image dimensions must be >= 1, got %dx%d", width, height);
+    if (overlap < 0 || block <= overlap)
+        return fail_arg(B200P_ERR_ARG, "need block_size > overlap >= 0, got %d, %d", block, overlap);
+    std::vector<b200p_level_info> v;
+    level_shapes(width, height, spacing, block, overlap, v);
+    for (int i = 0; i < (int)v.size() && i < cap; ++i) out[i] = v[i];
+    return (int)v.size();
+}
+
+void b200p_plan_destroy(b200p_plan *pl) {
+    if (!pl) return;
+    prof_collect(pl);
+    if (pl->g_front.exec) cudaGraphExecDestroy(pl->g_front.exec);
+    if (pl->g_cycle.exec) cudaGraphExecDestroy(pl->g_cycle.exec);
+    for (void *p : pl->owned) cudaFree(p);
+    if (pl->h_any) cudaFreeHost(pl->h_any);
+    if (pl->h_pin) cudaFreeHost(pl->h_pin);
+    if (pl->own_stream) cudaStreamDestroy(pl->own_stream);
+    delete pl;
+}
+
+int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
+    if (!cfg || !out) return fail_arg(B200P_ERR_ARG, "null argument");
+    *out = nullptr;
+    const b200p_config &c = *cfg;
+    // same conditions as the reference's __post_init__ / build_partition checks
+    if (c.width < 1 || c.height < 1)
+        return fail_arg(B200P_ERR_ARG, "image dimensions must be >= 1, got %dx%d", c.width, c.height);
+    if (c.channels < 1 || c.frames < 1)
+        return fail_arg(B200P_ERR_ARG, "need channels >= 1 and frames >= 1");
+    if (!(c.spacing > 0.0)) return fail_arg(B200P_ERR_ARG, "spacing must be positive, got %g", c.spacing);
+    if (c.overlap < 0 || c.block_size <= c.overlap)
+        return fail_arg(B200P_ERR_ARG, "need block_size > overlap >= 0, got %d, %d", c.block_size, c.overlap);
+    if (c.block_size > B200P_MAX_BLOCK)
+        return fail_arg(B200P_ERR_UNSUPPORTED, "block_size %d exceeds the supported maximum %d",
+                        c.block_size, B200P_MAX_BLOCK);
+    if (c.nu_pre < 0 || c.nu_post < 0 || c.nu_pre + c.nu_post < 1)
+        return fail_arg(B200P_ERR_ARG, "need at least one smoothing iteration per cycle");
+    if (!(c.tol_rel > 0.0 && c.tol_rel < 1.0))
+        return fail_arg(B200P_ERR_ARG, "tol_rel must be in (0, 1), got %g", c.tol_rel);
+    if (!(c.alpha > 0.0)) return fail_arg(B200P_ERR_ARG, "alpha must be positive, got %g", c.alpha);
+    if (!(c.eta > 0.0)) return fail_arg(B200P_ERR_ARG, "local_tol_fraction must be positive, got %g", c.eta);
+    if (c.value_downsampling != 0 && c.value_downsampling != 1)
+        return fail_arg(B200P_ERR_ARG, "unknown value downsampling %d", c.value_downsampling);
+    if (c.v_cycles_max < 0 || c.coarse_max_iters < 0 || c.local_max_iters < 0)
+        return fail_arg(B200P_ERR_ARG, "iteration caps must be >= 0");
+
+    int ndev = 0;
+    CU(cudaGetDeviceCount(&ndev));
+    int rc = set_smem_attrs();
+    if (rc) return rc;
+
+    b200p_plan *pl = new b200p_plan();
+    pl->cfg = c;
+    if (pl->cfg.spec_cycles < 1) pl->cfg.spec_cycles = 1;
+    pl->F = c.frames;
+    pl->C = c.channels;
+    pl->P = c.frames * c.channels;
+    std::vector<b200p_level_info> shapes;
+    level_shapes(c.width, c.height, c.spacing, c.block_size, c.overlap, shapes);
+    if (std::max(shapes.back().height, shapes.back().width) > c.block_size) {
+        delete pl;
+        return fail_arg(B200P_ERR_UNSUPPORTED, "more than %d levels", B200P_MAX_LEVELS);
+    }
+    pl->lev.resize(shapes.size());
+    const int stride = c.block_size - c.overlap;
+    size_t scratch = 0;
+#define PTRY(x)                      \
+    do {                             \
+        int r__ = (x);               \
+        if (r__) {                   \
+            b200p_plan_destroy(pl);  \
+            return r__;              \
+        }                            \
+    } while (0)
+    for (size_t l = 0; l < shapes.size(); ++l) {
+        LevelHost &L = pl->lev[l];
+        L.info = shapes[l];
+        const int h = L.info.height, w = L.info.width;
+        std::vector<int> xs = axis_starts(w, c.block_size, stride);
+        std::vector<int> ys = axis_starts(h, c.block_size, stride);
+        std::vector<double> wx = axis_weights(xs, L.info.block_w, w, c.overlap);
+        std::vector<double> wy = axis_weights(ys, L.info.block_h, h, c.overlap);
+        std::vector<int> cxf, cxn, cyf, cyn;
+        axis_cover(xs, L.info.block_w, w, cxf, cxn);
+        axis_cover(ys, L.info.block_h, h, cyf, cyn);
+        L.nblocks = L.info.nx * L.info.ny;
+        LevelDev &D = L.dev;
+        D.h = h; D.w = w; D.nx = L.info.nx; D.ny = L.info.ny;
+        D.bw = L.info.block_w; D.bh = L.info.block_h; D.nblocks = L.nblocks;
+        D.spacing = L.info.spacing;
+        D.hinv2 = 1.0 / (L.info.spacing * L.info.spacing);
+        D.robin = c.alpha / L.info.spacing;
+        PTRY(dev_upload(pl, xs, &D.xs));
+        PTRY(dev_upload(pl, ys, &D.ys));
+        PTRY(dev_upload(pl, wx, &D.wx));
+        PTRY(dev_upload(pl, wy, &D.wy));
+        PTRY(dev_upload(pl, cxf, &D.cxf));
+        PTRY(dev_upload(pl, cxn, &D.cxn));
+        PTRY(dev_upload(pl, cyf, &D.cyf));
+        PTRY(dev_upload(pl, cyn, &D.cyn));
+        L.tile = tile_for(D.bw, D.bh);
+        const size_t plane = (size_t)h * w;
+        if (l > 0) {
+            PTRY(dev_alloc(pl, &L.d_mask, pl->F * plane));
+            PTRY(dev_alloc(pl, &L.d_rhs, pl->P * plane));
+            PTRY(dev_alloc(pl, &L.d_u, pl->P * plane));
+            PTRY(dev_alloc(pl, &L.d_rc, pl->P * plane));
+        }
+        if (L.nblocks > 1 || shapes.size() == 1)
+            scratch = std::max(scratch, (size_t)pl->P * L.nblocks * D.bw * D.bh);
+    }
+    PTRY(dev_alloc(pl, &pl->d_scratch, scratch));
+    pl->norm_ctas = std::max(1, std::min(1024, (148 * 8 + pl->P - 1) / pl->P));
+    PTRY(dev_alloc(pl, &pl->d_partial, (size_t)pl->P * pl->norm_ctas));
+    PTRY(dev_alloc(pl, &pl->d_partial_flag, (size_t)pl->P * pl->norm_ctas));
+    PTRY(dev_alloc(pl, &pl->d_counter, (size_t)pl->P));
+    CU(cudaMemset(pl->d_counter, 0, sizeof(unsigned) * pl->P));
+    PTRY(dev_alloc(pl, &pl->d_rs, (size_t)pl->P));
+    PTRY(dev_alloc(pl, &pl->d_mflag, (size_t)pl->P));
+    PTRY(dev_alloc(pl, &pl->d_active, (size_t)pl->P));
+    PTRY(dev_alloc(pl, &pl->d_cycles, (size_t)pl->P));
+    PTRY(dev_alloc(pl, &pl->d_units, (size_t)pl->P));
+    PTRY(dev_alloc(pl, &pl->d_histlen, (size_t)pl->P));
+    PTRY(dev_alloc(pl, &pl->d_any, (size_t)1));
+    PTRY(dev_alloc(pl, &pl->d_baseline, (size_t)pl->P));
+    PTRY(dev_alloc(pl, &pl->d_denom, (size_t)pl->P));
+    PTRY(dev_alloc(pl, &pl->d_rel, (size_t)pl->P));
+    PTRY(dev_alloc(pl, &pl->d_hist, (size_t)pl->P * B200P_MAX_HISTORY));
+    PTRY(dev_alloc(pl, &pl->d_gate, (size_t)pl->P));
+    PTRY(dev_alloc(pl, &pl->d_sweeps, (size_t)pl->P));
+    PTRY(dev_alloc(pl, &pl->d_rn, (size_t)pl->P));
+    {
+        cudaError_t e = cudaMallocHost((void **)&pl->h_any, 64);
+        if (e != cudaSuccess) {
+            b200p_plan_destroy(pl);
+            return fail_cuda(e, "cudaMallocHost");
+        }
+    }
+#undef PTRY
+    *out = pl;
+    return 0;
+}
+
+int b200p_plan_num_levels(const b200p_plan *pl) { return pl ? (int)pl->lev.size() : 0; }
+
+int b200p_plan_level_info(const b200p_plan *pl, int level, b200p_level_info *out) {
+    if (!pl || !out || level < 0 || level >= (int)pl->lev.size())
+        return fail_arg(B200P_ERR_ARG, "bad level %d", level);
+    *out = pl->lev[level].info;
+    return 0;
+}
+
+int64_t b200p_plan_device_bytes(const b200p_plan *pl) { return pl ? pl->dev_bytes : 0; }
+int64_t b200p_plan_launch_count(const b200p_plan *pl) { return pl ? pl->launches : 0; }
+
+int b200p_plan_profile(b200p_plan *pl, int enable) {
+    if (!pl) return fail_arg(B200P_ERR_ARG, "null plan");
+    prof_collect(pl);
+    pl->profiling = enable != 0;
+    if (enable) {
+        memset(pl->prof_ms, 0, sizeof pl->prof_ms);
+        memset(pl->prof_bytes, 0, sizeof pl->prof_bytes);
+        memset(pl->prof_launches, 0, sizeof pl->prof_launches);
+    }
+    return 0;
+}
+
+int b200p_plan_profile_kinds(void) { return KK_COUNT; }
+
+const char *b200p_plan_profile_name(int kind) {
+    return kind >= 0 && kind < KK_COUNT ? kKindNames[kind] : "";
+}
+
+int b200p_plan_profile_get(b200p_plan *pl, int kind, double *ms, int64_t *launches, double *bytes) {
+    if (!pl || kind < 0 || kind >= KK_COUNT) return fail_arg(B200P_ERR_ARG, "bad kind %d", kind);
+    prof_collect(pl);
+    if (ms) *ms = pl->prof_ms[kind];
+    if (launches) *launches = pl->prof_launches[kind];
+    if (bytes) *bytes = pl->prof_bytes[kind];
+    return 0;
+}
+
+static int collect_reports(b200p_plan *pl, b200p_report *h_reports, cudaStream_t st) {
+    const int P = pl->P;
+    std::vector<int> cycles(P), units(P), histlen(P);
+    std::vector<double> base(P), rel(P), hist((size_t)P * B200P_MAX_HISTORY);
+    CU(cudaMemcpyAsync(cycles.data(), pl->d_cycles, P * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(units.data(), pl->d_units, P * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(histlen.data(), pl->d_histlen, P * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(base.data(), pl->d_baseline, P * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(rel.data(), pl->d_rel, P * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(hist.data(), pl->d_hist, hist.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    for (int p = 0; p < P; ++p) {
+        b200p_report &r = h_reports[p];
+        memset(&r, 0, sizeof r);
+        r.iterations = cycles[p];
+        r.fine_smoother_iterations = units[p];
+        r.history_len = histlen[p];
+        r.final_rel_residual = rel[p];
+        r.baseline_residual = base[p];
+        r.init_residual = base[p];
+        r.converged = rel[p] <= pl->cfg.tol_rel;
+        memcpy(r.history, &hist[(size_t)p * B200P_MAX_HISTORY], sizeof(double) * B200P_MAX_HISTORY);
+    }
+    return 0;
+}
+
+int b200p_solve(b200p_plan *pl, const uint8_t *d_mask, const double *d_known, double *d_out,
+                b200p_report *h_reports, void *stream) {
+    if (!pl || !d_mask || !d_known || !d_out) return fail_arg(B200P_ERR_ARG, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (pl->cfg.use_graphs && !pl->profiling && st == nullptr) {
+        // stream capture is not allowed on the legacy default stream
+        if (!pl->own_stream) CU(cudaStreamCreateWithFlags(&pl->own_stream, cudaStreamNonBlocking));
+        CU(cudaDeviceSynchronize());
+        st = pl->own_stream;
+    }
+    bind_level0(pl, d_mask, d_known);
+    int rc = run_graph(pl, pl->g_front, d_mask, d_known, d_out, st,
+                       [&](cudaStream_t s) { return enqueue_front(pl, d_out, s); });
+    if (rc) return rc;
+    pl->hierarchy_ready = true;
+    CU(cudaStreamSynchronize(st));
+    int done = 0;
+    while (*pl->h_any && done < pl->cfg.v_cycles_max) {
+        const int k = std::min(pl->cfg.spec_cycles, pl->cfg.v_cycles_max - done);
+        for (int i = 0; i < k; ++i) {
+            rc = run_graph(pl, pl->g_cycle, d_mask, d_known, d_out, st,
+                           [&](cudaStream_t s) { return enqueue_cycle(pl, d_out, s); });
+            if (rc) return rc;
+        }
+        done += k;
+        CU(cudaStreamSynchronize(st));
+    }
+    if (h_reports) {
+        rc = collect_reports(pl, h_reports, st);
+        if (rc) return rc;
+    }
+    if (pl->profiling) prof_collect(pl);
+    return 0;
+}
+
+static int ensure_staging(b200p_plan *pl, bool u8) {
+    const size_t plane = (size_t)pl->cfg.width * pl->cfg.height;
+    if (!pl->d_in_mask) {
+        int rc;
+        if ((rc = dev_alloc(pl, &pl->d_in_mask, pl->F * plane))) return rc;
+        if ((rc = dev_alloc(pl, &pl->d_in_known, pl->P * plane))) return rc;
+        if ((rc = dev_alloc(pl, &pl->d_out, pl->P * plane))) return rc;
+    }
+    if (u8 && !pl->d_io_u8) {
+        int rc;
+        if ((rc = dev_alloc(pl, &pl->d_io_u8, pl->P * plane))) return rc;
+    }
+    if (!pl->own_stream) CU(cudaStreamCreateWithFlags(&pl->own_stream, cudaStreamNonBlocking));
+    return 0;
+}
+
+static bool any_nonzero(const uint8_t *p, size_t n) {
+    size_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+        uint64_t v;
+        memcpy(&v, p + i, 8);
+        if (v) return true;
+    }
+    for (; i < n; ++i)
+        if (p[i]) return true;
+    return false;
+}
+
+static int check_masks(const b200p_plan *pl, const uint8_t *h_mask) {
+    const size_t plane = (size_t)pl->cfg.width * pl->cfg.height;
+    for (int f = 0; f < pl->F; ++f)
+        if (!any_nonzero(h_mask + (size_t)f * plane, plane))
+            return fail_arg(B200P_ERR_EMPTY_MASK, "cannot solve without known pixels");
+    return 0;
+}
+
+int b200p_solve_host(b200p_plan *pl, const uint8_t *h_mask, const double *h_known, double *h_out,
+                     b200p_report *h_reports) {
+    if (!pl || !h_mask || !h_known || !h_out) return fail_arg(B200P_ERR_ARG, "null argument");
+    int rc = check_masks(pl, h_mask);
+    if (rc) return rc;
+    if ((rc = ensure_staging(pl, false))) return rc;
+    const size_t plane = (size_t)pl->cfg.width * pl->cfg.height;
+    cudaStream_t st = pl->own_stream;
+    CU(cudaMemcpyAsync(pl->d_in_mask, h_mask, pl->F * plane, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(pl->d_in_known, h_known, pl->P * plane * sizeof(double), cudaMemcpyHostToDevice, st));
+    if ((rc = b200p_solve(pl, pl->d_in_mask, pl->d_in_known, pl->d_out, h_reports, st))) return rc;
+    CU(cudaMemcpyAsync(h_out, pl->d_out, pl->P * plane * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int b200p_solve_host_u8(b200p_plan *pl, const uint8_t *h_mask, const uint8_t *h_known_u8,
+                        uint8_t *h_out_u8, b200p_report *h_reports) {
+    if (!pl || !h_mask || !h_known_u8 || !h_out_u8) return fail_arg(B200P_ERR_ARG, "null argument");
+    int rc = check_masks(pl, h_mask);
+    if (rc) return rc;
+    if ((rc = ensure_staging(pl, true))) return rc;
+    const size_t plane = (size_t)pl->cfg.width * pl->cfg.height;
+    const size_t n = pl->P * plane;
+    cudaStream_t st = pl->own_stream;
+    CU(cudaMemcpyAsync(pl->d_in_mask, h_mask, pl->F * plane, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(pl->d_io_u8, h_known_u8, n, cudaMemcpyHostToDevice, st));
+    {
+        LaunchScope sc(pl, st, KK_CONVERT, 9.0 * n);
+        u8_to_f64_kernel<<<(unsigned)((n + ST_THREADS - 1) / ST_THREADS), ST_THREADS, 0, st>>>(
+            pl->d_io_u8, n, pl->d_in_known);
+        CU(cudaGetLastError());
+    }
+    if ((rc = b200p_solve(pl, pl->d_in_mask, pl->d_in_known, pl->d_out, h_reports, st))) return rc;
+    {
+        LaunchScope sc(pl, st, KK_CONVERT, 9.0 * n);
+        f64_to_u8_kernel<<<(unsigned)((n + ST_THREADS - 1) / ST_THREADS), ST_THREADS, 0, st>>>(
+            pl->d_out, n, pl->d_io_u8);
+        CU(cudaGetLastError());
+    }
+    CU(cudaMemcpyAsync(h_out_u8, pl->d_io_u8, n, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    return 0;
+}
+
+// ---- stage entry points -------------------------------------------------
+
+int b200p_plan_build_hierarchy(b200p_plan *pl, const uint8_t *d_mask, const double *d_known,
+                               void *stream) {
+    if (!pl || !d_mask || !d_known) return fail_arg(B200P_ERR_ARG, "null argument");
+    bind_level0(pl, d_mask, d_known);
+    int rc = enqueue_hierarchy(pl, (cudaStream_t)stream);
+    if (rc) return rc;
+    pl->hierarchy_ready = true;
+    return 0;
+}
+
+int b200p_plan_level_ptrs(const b200p_plan *pl, int level, const uint8_t **d_mask,
+                          const double **d_rhs) {
+    if (!pl || level < 0 || level >= (int)pl->lev.size()) return fail_arg(B200P_ERR_ARG, "bad level %d", level);
+    if (!pl->hierarchy_ready) return fail_arg(B200P_ERR_STATE, "build_hierarchy has not run");
+    if (d_mask) *d_mask = pl->lev[level].d_mask;
+    if (d_rhs) *d_rhs = level == 0 ? nullptr : pl->lev[level].d_rhs;
+    return 0;
+}
+
+int b200p_plan_cascade(b200p_plan *pl, double *d_u, void *stream) {
+    if (!pl || !d_u) return fail_arg(B200P_ERR_ARG, "null argument");
+    if (!pl->hierarchy_ready) return fail_arg(B200P_ERR_STATE, "build_hierarchy has not run");
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = launch_set_int(pl, pl->d_units, pl->P, 0, st);
+    if (rc) return rc;
+    return enqueue_cascade(pl, d_u, st);
+}
+
+int b200p_plan_vcycle(b200p_plan *pl, int level, double *d_u, const double *d_rhs, int *h_fine_units,
+                      void *stream) {
+    if (!pl || !d_u || !d_rhs) return fail_arg(B200P_ERR_ARG, "null argument");
+    if (level < 0 || level >= (int)pl->lev.size()) return fail_arg(B200P_ERR_ARG, "bad level %d", level);
+    if (!pl->hierarchy_ready) return fail_arg(B200P_ERR_STATE, "build_hierarchy has not run");
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = launch_set_int(pl, pl->d_units, pl->P, 0, st);
+    if (rc) return rc;
+    if ((rc = enqueue_vcycle(pl, level, d_u, d_rhs, false, nullptr, pl->d_units, false, st))) return rc;
+    if (h_fine_units) {
+        CU(cudaMemcpyAsync(h_fine_units, pl->d_units, pl->P * sizeof(int), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        if (level != 0) memset(h_fine_units, 0, pl->P * sizeof(int));
+    }
+    return 0;
+}
+
+int b200p_plan_oras_sweeps(b200p_plan *pl, int level, const double *d_b, double *d_u, int max_sweeps,
+                           double stop_norm, int path, int *h_sweeps, double *h_rn, void *stream) {
+    if (!pl || !d_b || !d_u) return fail_arg(B200P_ERR_ARG, "null argument");
+    if (level < 0 || level >= (int)pl->lev.size()) return fail_arg(B200P_ERR_ARG, "bad level %d", level);
+    if (!pl->lev[level].d_mask) return fail_arg(B200P_ERR_STATE, "level mask not bound (build_hierarchy)");
+    LevelHost &L = pl->lev[level];
+    int force = -1;
+    if (path == 1) force = TILE_GENERIC;
+    else if (path >= 2) {
+        const int t = path == 2 ? tile_for(L.info.block_w, L.info.block_h) : path - 2;
+        bool ok = false;
+        if (L.info.block_w == 32 && L.info.block_h == 32) ok = t == TILE_32_A || t == TILE_32_B || t == TILE_32_C;
+        if (L.info.block_w == 16 && L.info.block_h == 16) ok = t == TILE_16;
+        if (L.info.block_w == 8 && L.info.block_h == 8) ok = t == TILE_8;
+        if (!ok) return fail_arg(B200P_ERR_UNSUPPORTED, "level %d is not eligible for tile path %d", level, path);
+        force = t;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc;
+    if ((rc = launch_set_int(pl, pl->d_gate, pl->P, 1, st))) return rc;
+    if ((rc = launch_set_int(pl, pl->d_sweeps, pl->P, 0, st))) return rc;
+    int it = 0;
+    for (;;) {
+        const int chunk = 8;
+        if ((rc = launch_set_int(pl, pl->d_any, 1, 0, st))) return rc;
+        for (int k = 0; k < chunk && it <= max_sweeps; ++k, ++it) {
+            if ((rc = launch_norm(pl, L, d_u, d_b, false, false, pl->d_gate, st))) return rc;
+            {
+                LaunchScope sc(pl, st, KK_CONTROL, 0.0);
+                sweep_gate_kernel<<<(pl->P + 127) / 128, 128, 0, st>>>(
+                    pl->P, pl->d_rs, stop_norm, max_sweeps, pl->d_gate, pl->d_sweeps, pl->d_rn, pl->d_any);
+                CU(cudaGetLastError());
+            }
+            if ((rc = launch_sweep(pl, L, d_u, d_b, false, pl->d_gate, pl->d_sweeps, force, st))) return rc;
+        }
+        CU(cudaMemcpyAsync(pl->h_any, pl->d_any, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        if (!*pl->h_any || it > max_sweeps) break;
+    }
+    if (h_sweeps) CU(cudaMemcpyAsync(h_sweeps, pl->d_sweeps, pl->P * sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (h_rn) CU(cudaMemcpyAsync(h_rn, pl->d_rn, pl->P * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (pl->profiling) prof_collect(pl);
+    return 0;
+}
+
+int b200p_plan_solve_blocks(b200p_plan *pl, int level, const double *d_r, double target_sq,
+                            double *d_v, void *stream) {
+    if (!pl || !d_r || !d_v) return fail_arg(B200P_ERR_ARG, "null argument");
+    if (level < 0 || level >= (int)pl->lev.size()) return fail_arg(B200P_ERR_ARG, "bad level %d", level);
+    if (!pl->lev[level].d_mask) return fail_arg(B200P_ERR_STATE, "level mask not bound (build_hierarchy)");
+    LevelHost &L = pl->lev[level];
+    SweepArgs A;
+    A.L = L.dev;
+    A.u = d_r;
+    A.b = nullptr;
+    A.mask = L.d_mask;
+    A.channels = pl->C;
+    A.plane = (size_t)L.info.height * L.info.width;
+    A.pred = nullptr;
+    A.rs = nullptr;
+    A.mflag = nullptr;
+    A.eta = target_sq;
+    A.max_iters = local_cap(pl, L);
+    A.scratch = d_v;
+    cudaStream_t st = (cudaStream_t)stream;
+    LaunchScope sc(pl, st, KK_SWEEP, 0.0);
+    oras_sweep_generic_kernel<false, 1><<<dim3(L.nblocks, pl->P), GEN_THREADS,
+                                          smem_cg_bytes(L.info.block_w, L.info.block_h), st>>>(A);
+    CU(cudaGetLastError());
+    return 0;
+}
+
+int b200p_apply(const uint8_t *d_mask, int h, int w, double spacing, const double *d_u, double *d_out,
+                void *stream) {
+    if (!d_mask || !d_u || !d_out || h < 1 || w < 1) return fail_arg(B200P_ERR_ARG, "bad argument");
+    if (!(spacing > 0.0)) return fail_arg(B200P_ERR_ARG, "spacing must be positive, got %g", spacing);
+    const size_t n = (size_t)h * w;
+    residual_field_kernel<<<(unsigned)((n + ST_THREADS - 1) / ST_THREADS), ST_THREADS, 0,
+                            (cudaStream_t)stream>>>(d_u, nullptr, d_mask, h, w, 1.0 / (spacing * spacing),
+                                                    1, d_out);
+    CU(cudaGetLastError());
+    return 0;
+}
+
+int b200p_residual(const uint8_t *d_mask, int h, int w, double spacing, const double *d_b,
+                   const double *d_u, double *d_r, void *stream) {
+    if (!d_mask || !d_u || !d_b || !d_r || h < 1 || w < 1) return fail_arg(B200P_ERR_ARG, "bad argument");
+    if (!(spacing > 0.0)) return fail_arg(B200P_ERR_ARG, "spacing must be positive, got %g", spacing);
+    const size_t n = (size_t)h * w;
+    residual_field_kernel<<<(unsigned)((n + ST_THREADS - 1) / ST_THREADS), ST_THREADS, 0,
+                            (cudaStream_t)stream>>>(d_u, d_b, d_mask, h, w, 1.0 / (spacing * spacing), 0,
+                                                    d_r);
+    CU(cudaGetLastError());
+    return 0;
+}
+
+int b200p_residual_sqnorm(const uint8_t *d_mask, int h, int w, double spacing, const double *d_b,
+                          const double *d_u, int planes, double *h_out, void *stream) {
+    if (!d_mask || !d_u || !d_b || !h_out || h < 1 || w < 1 || planes < 1)
+        return fail_arg(B200P_ERR_ARG, "bad argument");
+    if (!(spacing > 0.0)) return fail_arg(B200P_ERR_ARG, "spacing must be positive, got %g", spacing);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int ctas = 256;
+    double *d_partial = nullptr, *d_rs = nullptr;
+    int *d_pf = nullptr, *d_flag = nullptr;
+    unsigned *d_cnt = nullptr;
+    CU(cudaMalloc(&d_partial, sizeof(double) * ctas * planes));
+    CU(cudaMalloc(&d_pf, sizeof(int) * ctas * planes));
+    CU(cudaMalloc(&d_cnt, sizeof(unsigned) * planes));
+    CU(cudaMalloc(&d_rs, sizeof(double) * planes));
+    CU(cudaMalloc(&d_flag, sizeof(int) * planes));
+    CU(cudaMemsetAsync(d_cnt, 0, sizeof(unsigned) * planes, st));
+    residual_sqnorm_kernel<false, false><<<dim3(ctas, planes), ST_THREADS, 0, st>>>(
+        d_u, d_b, d_mask, h, w, 1.0 / (spacing * spacing), planes, (size_t)h * w, nullptr, d_partial,
+        d_pf, d_cnt, d_rs, d_flag);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_out, d_rs, sizeof(double) * planes, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(d_partial); cudaFree(d_pf); cudaFree(d_cnt); cudaFree(d_rs); cudaFree(d_flag);
+    if (e != cudaSuccess) return fail_cuda(e, "residual_sqnorm");
+    return 0;
+}
+
+int b200p_downsample_mask(const uint8_t *d_fine, int h, int w, uint8_t *d_coarse, void *stream) {
+    if (!d_fine || !d_coarse || h < 1 || w < 1) return fail_arg(B200P_ERR_ARG, "bad argument");
+    downsample_mask_kernel<<<grid2x((w + 1) / 2, (h + 1) / 2, 1), ST_THREADS, 0, (cudaStream_t)stream>>>(
+        d_fine, h, w, d_coarse);
+    CU(cudaGetLastError());
+    return 0;
+}
+
+int b200p_downsample_values(const uint8_t *d_fine_mask, const uint8_t *d_coarse_mask,
+                            const double *d_fine_rhs, int h, int w, int modified, double *d_coarse_rhs,
+                            void *stream) {
+    if (!d_fine_mask || !d_coarse_mask || !d_fine_rhs || !d_coarse_rhs || h < 1 || w < 1)
+        return fail_arg(B200P_ERR_ARG, "bad argument");
+    downsample_values_kernel<<<grid2x((w + 1) / 2, (h + 1) / 2, 1), ST_THREADS, 0, (cudaStream_t)stream>>>(
+        d_fine_mask, d_coarse_mask, d_fine_rhs, h, w, 1, modified, d_coarse_rhs);
+    CU(cudaGetLastError());
+    return 0;
+}
+
+int b200p_residual_restrict(const uint8_t *d_fine_mask, const uint8_t *d_coarse_mask, int h, int w,
+                            double spacing, const double *d_b, const double *d_u, double *d_coarse_r,
+                            void *stream) {
+    if (!d_fine_mask || !d_coarse_mask || !d_b || !d_u || !d_coarse_r || h < 1 || w < 1)
+        return fail_arg(B200P_ERR_ARG, "bad argument");
+    if (!(spacing > 0.0)) return fail_arg(B200P_ERR_ARG, "spacing must be positive, got %g", spacing);
+    residual_restrict_kernel<false><<<grid2x((w + 1) / 2, (h + 1) / 2, 1), ST_THREADS, 0,
+                                      (cudaStream_t)stream>>>(
+        d_u, d_b, d_fine_mask, d_coarse_mask, h, w, 1.0 / (spacing * spacing), 1, nullptr, d_coarse_r,
+        nullptr);
+    CU(cudaGetLastError());
+    return 0;
+}
+
+int b200p_restrict_residual(const double *d_fine_r, const uint8_t *d_coarse_mask, int h, int w,
+                            double *d_coarse_r, void *stream) {
+    if (!d_fine_r || !d_coarse_mask || !d_coarse_r || h < 1 || w < 1)
+        return fail_arg(B200P_ERR_ARG, "bad argument");
+    restrict_field_kernel<<<grid2x((w + 1) / 2, (h + 1) / 2, 1), ST_THREADS, 0, (cudaStream_t)stream>>>(
+        d_fine_r, d_coarse_mask, h, w, d_coarse_r);
+    CU(cudaGetLastError());
+    return 0;
+}
+
+int b200p_prolongate_correct(const double *d_coarse_e, const uint8_t *d_fine_mask, int h, int w,
+                             double *d_u, void *stream) {
+    if (!d_coarse_e || !d_fine_mask || !d_u || h < 1 || w < 1) return fail_arg(B200P_ERR_ARG, "bad argument");
+    prolongate_kernel<false><<<grid2x((w + 1) / 2, (h + 1) / 2, 1), ST_THREADS, 0, (cudaStream_t)stream>>>(
+        d_coarse_e, d_fine_mask, nullptr, h, w, 1, nullptr, d_u);
+    CU(cudaGetLastError());
+    return 0;
+}
+
+int b200p_prolongate_solution(const double *d_coarse_u, const uint8_t *d_fine_mask,
+                              const double *d_fine_rhs, int h, int w, double *d_u, void *stream) {
+    if (!d_coarse_u || !d_fine_mask || !d_fine_rhs || !d_u || h < 1 || w < 1)
+        return fail_arg(B200P_ERR_ARG, "bad argument");
+    prolongate_kernel<true><<<grid2x((w + 1) / 2, (h + 1) / 2, 1), ST_THREADS, 0, (cudaStream_t)stream>>>(
+        d_coarse_u, d_fine_mask, d_fine_rhs, h, w, 1, nullptr, d_u);
+    CU(cudaGetLastError());
+    return 0;
+}
+
+// ---- device-memory helpers -----------------------------------------------
+int b200p_malloc(void **d_ptr, int64_t bytes) {
+    if (!d_ptr || bytes < 0) return fail_arg(B200P_ERR_ARG, "bad argument");
+    CU(cudaMalloc(d_ptr, (size_t)std::max<int64_t>(bytes, 1)));
+    return 0;
+}
+int b200p_free(void *d_ptr) {
+    CU(cudaFree(d_ptr));
+    return 0;
+}
+int b200p_memcpy_h2d(void *d_dst, const void *h_src, int64_t bytes) {
+    CU(cudaMemcpy(d_dst, h_src, (size_t)bytes, cudaMemcpyHostToDevice));
+    return 0;
+}
+int b200p_memcpy_d2h(void *h_dst, const void *d_src, int64_t bytes) {
+    CU(cudaMemcpy(h_dst, d_src, (size_t)bytes, cudaMemcpyDeviceToHost));
+    return 0;
+}
+int b200p_memset(void *d_ptr, int value, int64_t bytes) {
+    CU(cudaMemset(d_ptr, value, (size_t)bytes));
+    return 0;
+}
+int b200p_device_synchronize(void) {
+    CU(cudaDeviceSynchronize());
+    return 0;
+}
+
+}  // extern "C"

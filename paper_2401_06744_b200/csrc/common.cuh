@@ -1,0 +1,76 @@
+// common.cuh -- shared device helpers for libb200paint (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace b200p {
+
+// Per-level geometry handed to kernels by value.  Mirrors Level /
+// BlockPartition / BlockWeights of the reference (multigrid.py:189-207,
+// partition.py:38-62, :119-134); tables live in device memory.
+struct LevelDev {
+    int h, w;            // pixels
+    int nx, ny, bw, bh;  // blocks per axis, block extent
+    int nblocks;
+    double spacing, hinv2, robin;  // robin = alpha / spacing (solvers.py:291)
+    const int *xs, *ys;            // block starts (partition.py:84-90)
+    const double *wx, *wy;         // PoU weights (nx,bw), (ny,bh) (partition.py:137-154)
+    // per-pixel cover tables along each axis: first covering block and count
+    const int *cxf, *cxn, *cyf, *cyn;
+};
+
+constexpr unsigned FULL_MASK = 0xffffffffu;
+
+__device__ __forceinline__ double warp_sum(double v) {
+    // xor butterfly: every lane ends with the bit-identical total
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+    return v;
+}
+
+// CTA-wide sum, identical in every thread.  `red` needs 33 doubles of shared
+// memory; contains two __syncthreads, so it is safe to call back to back.
+__device__ __forceinline__ double cta_sum(double v, double *red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarp = (blockDim.x + 31) >> 5;
+    v = warp_sum(v);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        double t = lane < nwarp ? red[lane] : 0.0;
+        t = warp_sum(t);
+        if (lane == 0) red[32] = t;
+    }
+    __syncthreads();
+    const double out = red[32];
+    return out;
+}
+
+// b - A u at one pixel: StencilOperator.apply/residual (core.py:100-110).
+// UM: u is where(mask, u_arr, 0) (flat init read straight from `known`);
+// RM: b is where(mask, b_arr, 0) (level rhs read straight from `known` /
+//     hierarchy values, which are 0 off the mask by construction).
+template <bool UM, bool RM>
+__device__ __forceinline__ double residual_px(const double *__restrict__ u,
+                                              const double *__restrict__ b,
+                                              const uint8_t *__restrict__ mask, int y, int x, int h,
+                                              int w, double hinv2) {
+    const size_t i = (size_t)y * w + x;
+    const bool m = mask[i] != 0;
+    if (m) {
+        const double bb = b[i];
+        const double uu = u[i];
+        return bb - uu;
+    }
+    const double bb = RM ? 0.0 : b[i];
+    const double uu = UM ? 0.0 : u[i];
+    double s = 0.0, cnt = 4.0;
+    if (y > 0) s += UM ? (mask[i - w] ? u[i - w] : 0.0) : u[i - w]; else cnt -= 1.0;
+    if (y < h - 1) s += UM ? (mask[i + w] ? u[i + w] : 0.0) : u[i + w]; else cnt -= 1.0;
+    if (x > 0) s += UM ? (mask[i - 1] ? u[i - 1] : 0.0) : u[i - 1]; else cnt -= 1.0;
+    if (x < w - 1) s += UM ? (mask[i + 1] ? u[i + 1] : 0.0) : u[i + 1]; else cnt -= 1.0;
+    const double au = s * (-hinv2) + (cnt * hinv2) * uu;
+    return bb - au;
+}
+
+}  // namespace b200p

@@ -1,0 +1,586 @@
+// kernels_oras.cuh -- the ORAS block smoother (the hot kernel of the path).
+//
+//   K2   oras_sweep_tile_kernel<TW,TH,NWARP>  register-tiled local Robin CG, one
+//        warp group per overlapping block; all CG state lives in registers,
+//        neighbour exchange by warp shuffles, reductions by shuffle butterflies
+//        (solvers.py:303-305 gather, :328-370 _solve_range, :307-314 scatter weights)
+//   K2g  oras_sweep_generic_kernel            any block extent <= 64x64, shared-memory
+//        CG with one CTA per block (same semantics; partial / odd-sized blocks)
+//   K2b  oras_combine_kernel                  u += sum over covering blocks of the
+//        weighted corrections, in block order (np.bincount order, solvers.py:310-314)
+//   K7   coarse_solve_kernel                  _smooth_to_tol on a single-block level,
+//        sweeps looped in-kernel (multigrid.py:282-332, :362-364, :397-401)
+//
+// One sweep = K1 (||r||^2, kernels_stencil.cuh) -> K2 -> K2b.  K2 recomputes the
+// global residual of its block from u (1-pixel halo) instead of reading a
+// materialised residual field.
+#pragma once
+#include "common.cuh"
+
+namespace b200p {
+
+constexpr int ST_THREADS_COMBINE = 256;
+
+struct SweepArgs {
+    LevelDev L;
+    const double *u;       // (P, h, w) current iterate
+    const double *b;       // (P, h, w) right-hand side
+    const uint8_t *mask;   // (F, h, w)
+    int channels;
+    size_t plane;
+    const int *pred;       // per-problem active flag or null
+    const double *rs;      // (P) global ||r||^2 from K1
+    const int *mflag;      // (P) residual non-zero at some mask pixel
+    double eta;            // local_tol_fraction
+    int max_iters;         // local CG cap
+    double *scratch;       // (P, nblocks, bh, bw) weighted corrections
+};
+
+// ------------------------------------------------------------------ K2 ----
+// Block = (8*TW) x (4*TH*NWARP) pixels, handled by NWARP warps (= one CTA).
+// Lane (lx = lane&7, ly = lane>>3) of warp wg owns the TW x TH tile at
+// (lx*TW, (wg*4+ly)*TH).  The local operator is applied in the scaled form
+//     q' = A_i p / hinv2 = 4 p - (sum of 4 neighbours incl. ghosts),
+// where a neighbour cut off by a block side is replaced by the ghost
+// gamma * p_edge: gamma = 1 on the image border (reflecting, diag count 3) and
+// gamma = 1 - alpha*h on an inner side (Robin: diag 3 + alpha*h, solvers.py:206-216,
+// :288-297).  Mask pixels are identity rows; p and r stay exactly 0 there.
+template <int TW, int TH, int NWARP>
+struct TileCG {
+    static constexpr int BW = 8 * TW, BH = 4 * TH * NWARP;
+    int lane, wg, lx, ly;
+    bool eL, eR, eT, eB;     // tile touches the block's left/right/top/bottom side
+    double gL, gR, gT, gB;   // ghost factors of those sides
+    unsigned mbits;          // local mask, bit j*TW+i
+    double *xrow;            // smem: NWARP*2*BW doubles (cross-warp boundary rows)
+    double *red;             // smem: 2*NWARP doubles (two alternating slots)
+    int slot;
+
+    __device__ __forceinline__ double group_sum(double v) {
+        v = warp_sum(v);
+        if (NWARP == 1) return v;
+        if (lane == 0) red[slot * NWARP + wg] = v;
+        __syncthreads();
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < NWARP; ++k) t += red[slot * NWARP + k];
+        slot ^= 1;
+        return t;
+    }
+
+    // q' = 4p - neighbours (scaled local operator), 0 at mask pixels unless
+    // KEEP_MASK (then q' = p there: used for the unscaled v0 product).
+    __device__ __forceinline__ void apply(const double (&pc)[TH][TW], double (&q)[TH][TW]) {
+        double hT[TW], hB[TW];
+#pragma unroll
+        for (int i = 0; i < TW; ++i) {
+            hT[i] = __shfl_up_sync(FULL_MASK, pc[TH - 1][i], 8);
+            hB[i] = __shfl_down_sync(FULL_MASK, pc[0][i], 8);
+        }
+        if (NWARP > 1) {
+            const int bx = lx * TW;
+            if (ly == 0) {
+#pragma unroll
+                for (int i = 0; i < TW; ++i) xrow[(wg * 2 + 0) * BW + bx + i] = pc[0][i];
+            }
+            if (ly == 3) {
+#pragma unroll
+                for (int i = 0; i < TW; ++i) xrow[(wg * 2 + 1) * BW + bx + i] = pc[TH - 1][i];
+            }
+            __syncthreads();
+            if (ly == 0 && wg > 0) {
+#pragma unroll
+                for (int i = 0; i < TW; ++i) hT[i] = xrow[((wg - 1) * 2 + 1) * BW + bx + i];
+            }
+            if (ly == 3 && wg < NWARP - 1) {
+#pragma unroll
+                for (int i = 0; i < TW; ++i) hB[i] = xrow[((wg + 1) * 2 + 0) * BW + bx + i];
+            }
+        }
+        if (eT) {
+#pragma unroll
+            for (int i = 0; i < TW; ++i) hT[i] = gT * pc[0][i];
+        }
+        if (eB) {
+#pragma unroll
+            for (int i = 0; i < TW; ++i) hB[i] = gB * pc[TH - 1][i];
+        }
+#pragma unroll
+        for (int j = 0; j < TH; ++j) {
+            double hl = __shfl_up_sync(FULL_MASK, pc[j][TW - 1], 1);
+            double hr = __shfl_down_sync(FULL_MASK, pc[j][0], 1);
+            if (eL) hl = gL * pc[j][0];
+            if (eR) hr = gR * pc[j][TW - 1];
+#pragma unroll
+            for (int i = 0; i < TW; ++i) {
+                const double up = j == 0 ? hT[i] : pc[j - 1][i];
+                const double dn = j == TH - 1 ? hB[i] : pc[j + 1][i];
+                const double lf = i == 0 ? hl : pc[j][i - 1];
+                const double rt = i == TW - 1 ? hr : pc[j][i + 1];
+                const double s = ((up + dn) + lf) + rt;
+                const double qq = fma(4.0, pc[j][i], -s);
+                q[j][i] = ((mbits >> (j * TW + i)) & 1u) ? 0.0 : qq;
+            }
+        }
+    }
+};
+
+template <int TW, int TH, int NWARP, bool RM>
+__global__ void __launch_bounds__(NWARP * 32)
+oras_sweep_tile_kernel(const SweepArgs A) {
+    using CG = TileCG<TW, TH, NWARP>;
+    constexpr int BW = CG::BW, BH = CG::BH;
+    __shared__ double s_xrow[NWARP > 1 ? NWARP * 2 * BW : 1];
+    __shared__ double s_red[2 * NWARP];
+
+    const int p = blockIdx.y;
+    if (A.pred && !A.pred[p]) return;
+    const double rs_g = A.rs[p];
+    if (rs_g == 0.0) return;  // oras_sweeps exit, solvers.py:420
+    const double target = A.eta * rs_g;
+    const LevelDev &L = A.L;
+    const int blk = blockIdx.x;
+    const int iy = blk / L.nx, ix = blk - iy * L.nx;
+    const int x0 = L.xs[ix], y0 = L.ys[iy];
+    const int W = L.w, H = L.h;
+
+    CG cg;
+    cg.lane = threadIdx.x & 31;
+    cg.wg = threadIdx.x >> 5;
+    cg.lx = cg.lane & 7;
+    cg.ly = cg.lane >> 3;
+    cg.xrow = s_xrow;
+    cg.red = s_red;
+    cg.slot = 0;
+    cg.eL = cg.lx == 0;
+    cg.eR = cg.lx == 7;
+    cg.eT = cg.wg == 0 && cg.ly == 0;
+    cg.eB = cg.wg == NWARP - 1 && cg.ly == 3;
+    const double g_in = 1.0 - L.robin / L.hinv2;  // 1 - alpha*h
+    cg.gL = x0 > 0 ? g_in : 1.0;
+    cg.gR = x0 + BW < W ? g_in : 1.0;
+    cg.gT = y0 > 0 ? g_in : 1.0;
+    cg.gB = y0 + BH < H ? g_in : 1.0;
+
+    const int bx = cg.lx * TW, by = (cg.wg * 4 + cg.ly) * TH;
+    const int gx0 = x0 + bx, gy0 = y0 + by;
+    const double *up = A.u + (size_t)p * A.plane;
+    const double *bp = A.b + (size_t)p * A.plane;
+    const uint8_t *mp = A.mask + (size_t)(p / A.channels) * A.plane;
+    const double hinv2 = L.hinv2;
+
+    // ---- gather: global residual g = b - A u on the tile (core.py:100-110)
+    double r[TH][TW];
+    unsigned mbits = 0;
+    {
+        double uc[TH + 2][TW + 2];  // tile + 1-pixel halo, 0 outside the image
+#pragma unroll
+        for (int j = 0; j < TH + 2; ++j) {
+            const int gy = gy0 + j - 1;
+#pragma unroll
+            for (int i = 0; i < TW + 2; ++i) {
+                const int gx = gx0 + i - 1;
+                const bool corner = (j == 0 || j == TH + 1) && (i == 0 || i == TW + 1);
+                const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+                uc[j][i] = (!corner && in) ? up[(size_t)gy * W + gx] : 0.0;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < TH; ++j) {
+            const int gy = gy0 + j;
+            const double cy = 4.0 - (gy == 0 ? 1.0 : 0.0) - (gy == H - 1 ? 1.0 : 0.0);
+#pragma unroll
+            for (int i = 0; i < TW; ++i) {
+                const int gx = gx0 + i;
+                const size_t gi = (size_t)gy * W + gx;
+                const bool m = mp[gi] != 0;
+                if (m) mbits |= 1u << (j * TW + i);
+                const double cnt = cy - (gx == 0 ? 1.0 : 0.0) - (gx == W - 1 ? 1.0 : 0.0);
+                const double s = ((uc[j][i + 1] + uc[j + 2][i + 1]) + uc[j + 1][i]) + uc[j + 1][i + 2];
+                const double au = s * (-hinv2) + (cnt * hinv2) * uc[j + 1][i + 1];
+                double bb;
+                if (RM) bb = m ? bp[gi] : 0.0; else bb = bp[gi];
+                r[j][i] = m ? (bb - uc[j + 1][i + 1]) : (bb - au);
+            }
+        }
+    }
+    cg.mbits = mbits;
+
+    // ---- local start: v0 = where(mask, g, 0), r0 = g - A_i v0 (solvers.py:331-333)
+    double v[TH][TW], pc[TH][TW], q[TH][TW];
+#pragma unroll
+    for (int j = 0; j < TH; ++j)
+#pragma unroll
+        for (int i = 0; i < TW; ++i) v[j][i] = 0.0;
+    if (A.mflag[p]) {
+        // general case (u violates the interpolation condition): mask pixels
+        // carry v0 = g, which leaks into their neighbours' rows.
+#pragma unroll
+        for (int j = 0; j < TH; ++j)
+#pragma unroll
+            for (int i = 0; i < TW; ++i) {
+                const bool m = (mbits >> (j * TW + i)) & 1u;
+                v[j][i] = m ? r[j][i] : 0.0;
+                pc[j][i] = v[j][i];
+            }
+        cg.apply(pc, q);  // q' = 4 v0 - nbrs at non-mask pixels, 0 at mask pixels
+#pragma unroll
+        for (int j = 0; j < TH; ++j)
+#pragma unroll
+            for (int i = 0; i < TW; ++i) {
+                const bool m = (mbits >> (j * TW + i)) & 1u;
+                r[j][i] = m ? 0.0 : fma(-hinv2, q[j][i], r[j][i]);
+            }
+    }
+    double part = 0.0;
+#pragma unroll
+    for (int j = 0; j < TH; ++j)
+#pragma unroll
+        for (int i = 0; i < TW; ++i) part = fma(r[j][i], r[j][i], part);
+    double rs_k = cg.group_sum(part);
+
+    if (rs_k > target) {  // solvers.py:336 (strict)
+#pragma unroll
+        for (int j = 0; j < TH; ++j)
+#pragma unroll
+            for (int i = 0; i < TW; ++i) pc[j][i] = r[j][i];
+        for (int it = 0; it < A.max_iters; ++it) {
+            cg.apply(pc, q);
+            part = 0.0;
+#pragma unroll
+            for (int j = 0; j < TH; ++j)
+#pragma unroll
+                for (int i = 0; i < TW; ++i) part = fma(pc[j][i], q[j][i], part);
+            const double pq = hinv2 * cg.group_sum(part);
+            const bool ok = pq > 0.0;                 // solvers.py:348
+            const double a = ok ? rs_k / pq : 0.0;    // :349-350
+            const double ah = a * hinv2;
+            part = 0.0;
+#pragma unroll
+            for (int j = 0; j < TH; ++j)
+#pragma unroll
+                for (int i = 0; i < TW; ++i) {
+                    v[j][i] = fma(a, pc[j][i], v[j][i]);
+                    r[j][i] = fma(-ah, q[j][i], r[j][i]);
+                    part = fma(r[j][i], r[j][i], part);
+                }
+            const double rs_new = cg.group_sum(part);
+            if (rs_new <= target || !ok) break;       // :354
+            const double beta = rs_new / rs_k;
+            rs_k = rs_new;
+#pragma unroll
+            for (int j = 0; j < TH; ++j)
+#pragma unroll
+                for (int i = 0; i < TW; ++i) pc[j][i] = fma(beta, pc[j][i], r[j][i]);
+        }
+    }
+
+    // ---- weighted correction (v * wy) * wx -> scratch (solvers.py:309-310)
+    double wxv[TW];
+#pragma unroll
+    for (int i = 0; i < TW; ++i) wxv[i] = L.wx[ix * BW + bx + i];
+    double *sp = A.scratch + ((size_t)p * L.nblocks + blk) * (BW * BH);
+#pragma unroll
+    for (int j = 0; j < TH; ++j) {
+        const double wyv = L.wy[iy * BH + by + j];
+        double *row = sp + (by + j) * BW + bx;
+        if (TW % 2 == 0) {
+#pragma unroll
+            for (int i = 0; i < TW; i += 2) {
+                double2 o;
+                o.x = (v[j][i] * wyv) * wxv[i];
+                o.y = (v[j][i + 1] * wyv) * wxv[i + 1];
+                *reinterpret_cast<double2 *>(row + i) = o;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < TW; ++i) row[i] = (v[j][i] * wyv) * wxv[i];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ K2g ---
+// Shared-memory layout of the generic per-block CG (n = bw*bh):
+//   P  (bh+2)*(bw+2)  search direction with a zero ring (cut neighbours read 0)
+//   R, V, Q  n each (G aliases R: r0 = g - A v0 is formed in place);
+//   M n bytes; red 34 doubles.
+struct SmemCG {
+    double *P, *R, *V, *Q, *G, *red;
+    uint8_t *M;
+    int bw, bh, n, pw;  // pw = bw + 2
+    __device__ __forceinline__ double &p_at(int k) { return P[(k / bw + 1) * pw + (k % bw) + 1]; }
+};
+
+__host__ __device__ inline size_t smem_cg_bytes(int bw, int bh) {
+    const size_t n = (size_t)bw * bh;
+    return sizeof(double) * ((size_t)(bw + 2) * (bh + 2) + 3 * n + 34) + ((n + 15) / 16) * 16;
+}
+
+__device__ __forceinline__ SmemCG smem_cg_carve(unsigned char *base, int bw, int bh) {
+    SmemCG S;
+    S.bw = bw; S.bh = bh; S.n = bw * bh; S.pw = bw + 2;
+    double *d = reinterpret_cast<double *>(base);
+    S.P = d; d += (size_t)(bw + 2) * (bh + 2);
+    S.R = d; d += S.n;
+    S.G = S.R;
+    S.V = d; d += S.n;
+    S.Q = d; d += S.n;
+    S.red = d; d += 34;
+    S.M = reinterpret_cast<uint8_t *>(d);
+    return S;
+}
+
+// LocalSystem.apply / BlockSolver._apply at local pixel k (solvers.py:221-229,
+// :316-326): diag*v - hinv2*s with diag = cnt*hinv2 (+ robin per inner side in
+// the order left, right, top, bottom, :288-297); identity at mask pixels.
+__device__ __forceinline__ double smem_apply_at(SmemCG &S, int k, double hinv2, double robin,
+                                                bool inL, bool inR, bool inT, bool inB) {
+    const int j = k / S.bw, i = k - j * S.bw;
+    const double *c = &S.P[(j + 1) * S.pw + i + 1];
+    const double pv = c[0];
+    if (S.M[k]) return pv;
+    double cnt = 4.0;
+    if (j == 0) cnt -= 1.0;
+    if (j == S.bh - 1) cnt -= 1.0;
+    if (i == 0) cnt -= 1.0;
+    if (i == S.bw - 1) cnt -= 1.0;
+    double diag = cnt * hinv2;
+    if (inL && i == 0) diag += robin;
+    if (inR && i == S.bw - 1) diag += robin;
+    if (inT && j == 0) diag += robin;
+    if (inB && j == S.bh - 1) diag += robin;
+    const double s = ((c[-S.pw] + c[S.pw]) + c[-1]) + c[1];
+    return diag * pv - hinv2 * s;
+}
+
+// _solve_range for one block on shared memory (solvers.py:328-370).  Expects
+// S.G (gathered residual) and S.M filled and the P ring zeroed; leaves the
+// local correction in S.V.  Returns the CG steps taken.
+__device__ int smem_block_cg(SmemCG &S, double hinv2, double robin, bool inL, bool inR, bool inT,
+                             bool inB, double target, int max_iters) {
+    const int T = blockDim.x, tid = threadIdx.x;
+    for (int k = tid; k < S.n; k += T) {
+        const double v0 = S.M[k] ? S.G[k] : 0.0;
+        S.V[k] = v0;
+        S.p_at(k) = v0;
+    }
+    __syncthreads();
+    double part = 0.0;
+    for (int k = tid; k < S.n; k += T) {
+        const double r0 = S.G[k] - smem_apply_at(S, k, hinv2, robin, inL, inR, inT, inB);
+        S.R[k] = r0;
+        part += r0 * r0;
+    }
+    double rs = cta_sum(part, S.red);  // (contains the barrier that orders P reads/writes)
+    if (!(rs > target)) return 0;
+    for (int k = tid; k < S.n; k += T) S.p_at(k) = S.R[k];
+    __syncthreads();
+    int steps = 0;
+    for (int it = 0; it < max_iters; ++it) {
+        part = 0.0;
+        for (int k = tid; k < S.n; k += T) {
+            const double q = smem_apply_at(S, k, hinv2, robin, inL, inR, inT, inB);
+            S.Q[k] = q;
+            part += S.p_at(k) * q;
+        }
+        const double pq = cta_sum(part, S.red);
+        const bool ok = pq > 0.0;
+        const double a = ok ? rs / pq : 0.0;
+        part = 0.0;
+        for (int k = tid; k < S.n; k += T) {
+            S.V[k] += a * S.p_at(k);
+            const double rr = S.R[k] - a * S.Q[k];
+            S.R[k] = rr;
+            part += rr * rr;
+        }
+        const double rs_new = cta_sum(part, S.red);
+        ++steps;
+        if (rs_new <= target || !ok) break;
+        const double beta = rs_new / rs;
+        rs = rs_new;
+        for (int k = tid; k < S.n; k += T) S.p_at(k) = beta * S.p_at(k) + S.R[k];
+        __syncthreads();
+    }
+    return steps;
+}
+
+constexpr int GEN_THREADS = 256;
+
+// MODE 0: sweep  -- gather from u, solve, write weighted corrections to scratch
+// MODE 1: blocks -- gather from a given residual field (A.u), explicit target
+//                   (A.eta holds target_sq), write UNWEIGHTED v (solve_blocks)
+template <bool RM, int MODE>
+__global__ void __launch_bounds__(GEN_THREADS)
+oras_sweep_generic_kernel(const SweepArgs A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int p = blockIdx.y;
+    if (A.pred && !A.pred[p]) return;
+    double target;
+    if (MODE == 0) {
+        const double rs_g = A.rs[p];
+        if (rs_g == 0.0) return;
+        target = A.eta * rs_g;
+    } else {
+        target = A.eta;
+    }
+    const LevelDev &L = A.L;
+    const int blk = blockIdx.x;
+    const int iy = blk / L.nx, ix = blk - iy * L.nx;
+    const int x0 = L.xs[ix], y0 = L.ys[iy];
+    SmemCG S = smem_cg_carve(smem_raw, L.bw, L.bh);
+    const double *up = A.u + (size_t)p * A.plane;
+    const double *bp = A.b ? A.b + (size_t)p * A.plane : nullptr;
+    const uint8_t *mp = A.mask + (size_t)(p / A.channels) * A.plane;
+    for (int k = threadIdx.x; k < (S.bw + 2) * (S.bh + 2); k += GEN_THREADS) S.P[k] = 0.0;
+    for (int k = threadIdx.x; k < S.n; k += GEN_THREADS) {
+        const int j = k / S.bw, i = k - j * S.bw;
+        const int gy = y0 + j, gx = x0 + i;
+        const size_t gi = (size_t)gy * L.w + gx;
+        S.M[k] = mp[gi] != 0;
+        S.G[k] = MODE == 0 ? residual_px<false, RM>(up, bp, mp, gy, gx, L.h, L.w, L.hinv2) : up[gi];
+    }
+    __syncthreads();
+    smem_block_cg(S, L.hinv2, L.robin, x0 > 0, x0 + L.bw < L.w, y0 > 0, y0 + L.bh < L.h, target,
+                  A.max_iters);
+    __syncthreads();
+    double *sp = A.scratch + ((size_t)p * L.nblocks + blk) * S.n;
+    for (int k = threadIdx.x; k < S.n; k += GEN_THREADS) {
+        const int j = k / S.bw, i = k - j * S.bw;
+        sp[k] = MODE == 0 ? (S.V[k] * L.wy[iy * L.bh + j]) * L.wx[ix * L.bw + i] : S.V[k];
+    }
+}
+
+// ------------------------------------------------------------------ K2b ---
+// u += sum_b w_b v_b over the blocks covering each pixel, accumulated from 0 in
+// ascending block index (iy outer, ix inner) like np.bincount does, then added
+// to u (solvers.py:310-314, :423).  One thread per pixel; the per-axis cover
+// tables give the first covering slot and the slot count.
+__global__ void __launch_bounds__(ST_THREADS_COMBINE)
+oras_combine_kernel(const LevelDev L, const double *__restrict__ scratch, size_t plane,
+                    const int *__restrict__ pred, const double *__restrict__ rs,
+                    double *__restrict__ u, int *__restrict__ unit_counter) {
+    const int p = blockIdx.z;
+    if (pred && !pred[p]) return;
+    if (rs[p] == 0.0) return;
+    const int x = blockIdx.x * 128 + (threadIdx.x & 127);
+    const int y = blockIdx.y * 2 + (threadIdx.x >> 7);
+    if (unit_counter && x == 0 && y == 0) unit_counter[p] += 1;
+    if (x >= L.w || y >= L.h) return;
+    const int ixf = L.cxf[x], ixn = L.cxn[x], iyf = L.cyf[y], iyn = L.cyn[y];
+    const size_t bsz = (size_t)L.bw * L.bh;
+    const double *sp = scratch + (size_t)p * L.nblocks * bsz;
+    double acc = 0.0;
+    for (int a = 0; a < iyn; ++a) {
+        const int iy = iyf + a;
+        const int ly = y - L.ys[iy];
+        for (int c = 0; c < ixn; ++c) {
+            const int ix = ixf + c;
+            const int lx = x - L.xs[ix];
+            acc += sp[((size_t)iy * L.nx + ix) * bsz + (size_t)ly * L.bw + lx];
+        }
+    }
+    u[(size_t)p * plane + (size_t)y * L.w + x] += acc;
+}
+
+// ------------------------------------------------------------------ K7 ----
+// _smooth_to_tol / _smooth on a level that is a single block (always true for
+// the coarsest level: both extents <= block_size, multigrid.py:249).  One CTA
+// per problem keeps u, b and the CG state in shared memory and loops whole ORAS
+// sweeps in-kernel:
+//   r = b - A u; rs = |r|^2; first pass fixes denom = |r| (0 -> done);
+//   stop when rs == 0, |r| <= tol*denom or max_sweeps reached;
+//   local solve to eta*rs; u += (v*wy)*wx (single block: weights are 1).
+// (multigrid.py:300-322, solvers.py:413-424).  tol == 0 gives _smooth's
+// stop_norm = 0 behaviour (fixed sweep count, early exit only on rs == 0).
+// init_mode: 0  u = 0 (V-cycle correction e, multigrid.py:361)
+//            1  u = b (flat initialisation, multigrid.py:393-394)
+//            2  u = stored iterate
+struct CoarseArgs {
+    LevelDev L;
+    double *u;
+    const double *b;
+    const uint8_t *mask;
+    int channels;
+    const int *pred;
+    double tol;
+    int max_sweeps;
+    double eta;
+    int max_iters;
+    int rhs_masked;
+    int init_mode;
+    int *units_out;       // may be null
+    int units_accumulate;
+    double *rel_out;      // may be null: final |r| / denom
+};
+
+__global__ void __launch_bounds__(GEN_THREADS)
+coarse_solve_kernel(const CoarseArgs A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int p = blockIdx.x;
+    if (A.pred && !A.pred[p]) return;
+    const LevelDev &L = A.L;
+    SmemCG S = smem_cg_carve(smem_raw, L.bw, L.bh);
+    // U and B live behind the CG arrays
+    double *U = reinterpret_cast<double *>(smem_raw + smem_cg_bytes(L.bw, L.bh));
+    double *B = U + S.n;
+    const size_t plane = (size_t)L.h * L.w;
+    double *up = A.u + (size_t)p * plane;
+    const double *bp = A.b + (size_t)p * plane;
+    const uint8_t *mp = A.mask + (size_t)(p / A.channels) * plane;
+    const int T = GEN_THREADS, tid = threadIdx.x;
+    for (int k = tid; k < (S.bw + 2) * (S.bh + 2); k += T) S.P[k] = 0.0;
+    for (int k = tid; k < S.n; k += T) {
+        const bool m = mp[k] != 0;
+        S.M[k] = m;
+        const double bb = A.rhs_masked ? (m ? bp[k] : 0.0) : bp[k];
+        B[k] = bb;
+        U[k] = A.init_mode == 0 ? 0.0 : (A.init_mode == 1 ? bb : up[k]);
+    }
+    __syncthreads();
+    const double hinv2 = L.hinv2;
+    const int w = L.w, h = L.h;
+    double stop = 0.0, denom = 0.0, rn = 0.0;
+    int sweeps = 0;
+    for (;;) {
+        double part = 0.0;
+        for (int k = tid; k < S.n; k += T) {
+            const int y = k / w, x = k - y * w;
+            double g;
+            if (S.M[k]) {
+                g = B[k] - U[k];
+            } else {
+                double s = 0.0, cnt = 4.0;
+                if (y > 0) s += U[k - w]; else cnt -= 1.0;
+                if (y < h - 1) s += U[k + w]; else cnt -= 1.0;
+                if (x > 0) s += U[k - 1]; else cnt -= 1.0;
+                if (x < w - 1) s += U[k + 1]; else cnt -= 1.0;
+                g = B[k] - (s * (-hinv2) + (cnt * hinv2) * U[k]);
+            }
+            S.G[k] = g;
+            part += g * g;
+        }
+        const double rs = cta_sum(part, S.red);
+        rn = sqrt(rs);
+        if (sweeps == 0) {
+            denom = rn;
+            if (rn == 0.0) break;  // denom == 0 -> (0, 0.0), multigrid.py:302-303
+            stop = A.tol * rn;
+        }
+        if (rs == 0.0 || rn <= stop || sweeps >= A.max_sweeps) break;
+        smem_block_cg(S, hinv2, L.robin, false, false, false, false, A.eta * rs, A.max_iters);
+        __syncthreads();
+        for (int k = tid; k < S.n; k += T) {
+            const int y = k / w, x = k - y * w;
+            U[k] += (S.V[k] * L.wy[y]) * L.wx[x];
+        }
+        __syncthreads();
+        ++sweeps;
+    }
+    for (int k = tid; k < S.n; k += T) up[k] = U[k];
+    if (tid == 0) {
+        if (A.units_out) A.units_out[p] = A.units_accumulate ? A.units_out[p] + sweeps : sweeps;
+        if (A.rel_out) A.rel_out[p] = denom == 0.0 ? 0.0 : rn / denom;
+    }
+}
+
+}  // namespace b200p

@@ -1,0 +1,314 @@
+// kernels_stencil.cuh -- HBM-bound streaming stencil kernels of the mg-oras path.
+//
+//   K1  residual_sqnorm_kernel     ||b - A u||^2 per problem        (solvers.py:415-417)
+//   K3  residual_restrict_kernel   fused residual + 2x2 restriction  (multigrid.py:358-360, :149-154)
+//   K4  prolongate_correct_kernel  u += P e, zero at mask            (multigrid.py:367, :157-177)
+//   K5  prolongate_solution_kernel u  = P u_c, known at mask         (multigrid.py:410, :180-186)
+//   K6a downsample_mask_kernel     2x2 any-pool                      (multigrid.py:98-101)
+//   K6b downsample_values_kernel   naive / neighbour-suppressed      (multigrid.py:104-146)
+//
+// All kernels are batched: blockIdx.z (or .y) selects the problem p (a
+// (frame, channel) pair); channels of a frame share its mask plane.  Fields
+// are fp64 (core.py:14-16).  `pred` (may be null) is the per-problem "active"
+// flag of the V-cycle loop: converged problems are frozen (multigrid.py:474).
+#pragma once
+#include "common.cuh"
+
+namespace b200p {
+
+constexpr int ST_THREADS = 256;
+
+// ---------------------------------------------------------------- K1 ------
+// Grid: (ctas_per_problem, P).  Each CTA grid-strides over the pixels of its
+// problem, reduces in fp64, writes one partial; the last CTA of a problem adds
+// the partials in index order (deterministic) and publishes rs[p] plus the
+// "residual at a mask pixel is non-zero" flag the ORAS kernels use to skip the
+// A v0 product (solvers.py:331-333).
+template <bool UM, bool RM>
+__global__ void __launch_bounds__(ST_THREADS)
+residual_sqnorm_kernel(const double *__restrict__ u, const double *__restrict__ b,
+                       const uint8_t *__restrict__ mask, int h, int w, double hinv2, int channels,
+                       size_t plane, const int *__restrict__ pred, double *__restrict__ partial,
+                       int *__restrict__ partial_flag, unsigned *__restrict__ counter,
+                       double *__restrict__ rs_out, int *__restrict__ flag_out) {
+    __shared__ double red[33];
+    __shared__ int sflag;
+    __shared__ bool is_last;
+    const int p = blockIdx.y;
+    if (pred && !pred[p]) return;
+    const double *up = u + (size_t)p * plane;
+    const double *bp = b + (size_t)p * plane;
+    const uint8_t *mp = mask + (size_t)(p / channels) * plane;
+    if (threadIdx.x == 0) sflag = 0;
+    __syncthreads();
+    double acc = 0.0;
+    int flag = 0;
+    const size_t n = plane;
+    for (size_t i = (size_t)blockIdx.x * ST_THREADS + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * ST_THREADS) {
+        const int y = (int)(i / w), x = (int)(i - (size_t)y * w);
+        const double r = residual_px<UM, RM>(up, bp, mp, y, x, h, w, hinv2);
+        acc += r * r;
+        if (mp[i] && r != 0.0) flag = 1;
+    }
+    if (flag) sflag = 1;
+    const double tot = cta_sum(acc, red);
+    if (threadIdx.x == 0) {
+        partial[(size_t)p * gridDim.x + blockIdx.x] = tot;
+        partial_flag[(size_t)p * gridDim.x + blockIdx.x] = sflag;
+        __threadfence();
+        const unsigned done = atomicAdd(&counter[p], 1u);
+        is_last = (done == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (is_last) {
+        __threadfence();
+        double t = 0.0;
+        int f = 0;
+        // fixed-order tree: thread k sums partials k, k+T, ... then cta_sum
+        for (int k = threadIdx.x; k < (int)gridDim.x; k += ST_THREADS) {
+            t += ((volatile double *)partial)[(size_t)p * gridDim.x + k];
+            f |= ((volatile int *)partial_flag)[(size_t)p * gridDim.x + k];
+        }
+        if (f) sflag = 1;
+        const double total = cta_sum(t, red);
+        if (threadIdx.x == 0) {
+            rs_out[p] = total;
+            flag_out[p] = sflag;
+            counter[p] = 0;
+        }
+    }
+}
+
+// residual field (StencilOperator.residual, core.py:109-110); with b == 0 and
+// negate it is StencilOperator.apply.
+__global__ void __launch_bounds__(ST_THREADS)
+residual_field_kernel(const double *__restrict__ u, const double *__restrict__ b,
+                      const uint8_t *__restrict__ mask, int h, int w, double hinv2, int apply_only,
+                      double *__restrict__ out) {
+    const size_t n = (size_t)h * w;
+    const size_t i = (size_t)blockIdx.x * ST_THREADS + threadIdx.x;
+    if (i >= n) return;
+    const int y = (int)(i / w), x = (int)(i - (size_t)y * w);
+    if (apply_only) {
+        // A u = 0 - (0 - A u): evaluate the residual against b = 0 exactly
+        const bool m = mask[i] != 0;
+        if (m) { out[i] = u[i]; return; }
+        double s = 0.0, cnt = 4.0;
+        if (y > 0) s += u[i - w]; else cnt -= 1.0;
+        if (y < h - 1) s += u[i + w]; else cnt -= 1.0;
+        if (x > 0) s += u[i - 1]; else cnt -= 1.0;
+        if (x < w - 1) s += u[i + 1]; else cnt -= 1.0;
+        out[i] = s * (-hinv2) + (cnt * hinv2) * u[i];
+    } else {
+        out[i] = residual_px<false, false>(u, b, mask, y, x, h, w, hinv2);
+    }
+}
+
+// ---------------------------------------------------------------- K3 ------
+// One thread per coarse pixel: residual of its (up to) 2x2 fine constituents,
+// cell mean with the true constituent count, 0 at coarse mask pixels; also
+// clears the coarse correction e (multigrid.py:361).  The 2x2 sum follows
+// NumPy's (a00+a01)+(a10+a11) order.
+template <bool RM>
+__global__ void __launch_bounds__(ST_THREADS)
+residual_restrict_kernel(const double *__restrict__ u, const double *__restrict__ b,
+                         const uint8_t *__restrict__ fmask, const uint8_t *__restrict__ cmask, int h,
+                         int w, double hinv2, int channels, const int *__restrict__ pred,
+                         double *__restrict__ rc, double *__restrict__ e_zero) {
+    const int p = blockIdx.z;
+    if (pred && !pred[p]) return;
+    const int hc = (h + 1) >> 1, wc = (w + 1) >> 1;
+    const int X = blockIdx.x * 64 + (threadIdx.x & 63);
+    const int Y = blockIdx.y * 4 + (threadIdx.x >> 6);
+    if (X >= wc || Y >= hc) return;
+    const size_t fplane = (size_t)h * w, cplane = (size_t)hc * wc;
+    const double *up = u + (size_t)p * fplane;
+    const double *bp = b + (size_t)p * fplane;
+    const uint8_t *fm = fmask + (size_t)(p / channels) * fplane;
+    const uint8_t *cm = cmask + (size_t)(p / channels) * cplane;
+    const size_t ci = (size_t)Y * wc + X;
+    double out = 0.0;
+    if (!cm[ci]) {
+        const int y0 = 2 * Y, x0 = 2 * X;
+        const bool hx = x0 + 1 < w, hy = y0 + 1 < h;
+        const double a00 = residual_px<false, RM>(up, bp, fm, y0, x0, h, w, hinv2);
+        const double a01 = hx ? residual_px<false, RM>(up, bp, fm, y0, x0 + 1, h, w, hinv2) : 0.0;
+        const double a10 = hy ? residual_px<false, RM>(up, bp, fm, y0 + 1, x0, h, w, hinv2) : 0.0;
+        const double a11 = (hx && hy) ? residual_px<false, RM>(up, bp, fm, y0 + 1, x0 + 1, h, w, hinv2) : 0.0;
+        const double cnt = (hx ? 2.0 : 1.0) * (hy ? 2.0 : 1.0);
+        out = ((a00 + a01) + (a10 + a11)) / cnt;
+    }
+    rc[(size_t)p * cplane + ci] = out;
+    if (e_zero) e_zero[(size_t)p * cplane + ci] = 0.0;
+}
+
+// restrict_residual alone (multigrid.py:149-154) on a given fine residual.
+__global__ void __launch_bounds__(ST_THREADS)
+restrict_field_kernel(const double *__restrict__ r, const uint8_t *__restrict__ cmask, int h, int w,
+                      double *__restrict__ rc) {
+    const int hc = (h + 1) >> 1, wc = (w + 1) >> 1;
+    const int X = blockIdx.x * 64 + (threadIdx.x & 63);
+    const int Y = blockIdx.y * 4 + (threadIdx.x >> 6);
+    if (X >= wc || Y >= hc) return;
+    const int y0 = 2 * Y, x0 = 2 * X;
+    const bool hx = x0 + 1 < w, hy = y0 + 1 < h;
+    const double a00 = r[(size_t)y0 * w + x0];
+    const double a01 = hx ? r[(size_t)y0 * w + x0 + 1] : 0.0;
+    const double a10 = hy ? r[(size_t)(y0 + 1) * w + x0] : 0.0;
+    const double a11 = (hx && hy) ? r[(size_t)(y0 + 1) * w + x0 + 1] : 0.0;
+    const double cnt = (hx ? 2.0 : 1.0) * (hy ? 2.0 : 1.0);
+    const size_t ci = (size_t)Y * wc + X;
+    rc[ci] = cmask[ci] ? 0.0 : ((a00 + a01) + (a10 + a11)) / cnt;
+}
+
+// ------------------------------------------------------------ K4 / K5 -----
+// One thread per coarse pixel -> its (up to) 2x2 fine pixels.  Cell-centred
+// bilinear interpolation, x pass then y pass, 0.75 near + 0.25 far with the
+// far index clamped at the borders (multigrid.py:157-172).
+// SOLUTION = false:  u += P e, 0 at fine mask pixels  (prolongate_correction)
+// SOLUTION = true :  u  = P c, rhs at fine mask pixels (prolongate_solution)
+template <bool SOLUTION>
+__global__ void __launch_bounds__(ST_THREADS)
+prolongate_kernel(const double *__restrict__ c, const uint8_t *__restrict__ fmask,
+                  const double *__restrict__ frhs, int h, int w, int channels,
+                  const int *__restrict__ pred, double *__restrict__ u) {
+    const int p = blockIdx.z;
+    if (pred && !pred[p]) return;
+    const int hc = (h + 1) >> 1, wc = (w + 1) >> 1;
+    const int X = blockIdx.x * 64 + (threadIdx.x & 63);
+    const int Y = blockIdx.y * 4 + (threadIdx.x >> 6);
+    if (X >= wc || Y >= hc) return;
+    const size_t fplane = (size_t)h * w, cplane = (size_t)hc * wc;
+    const double *cp = c + (size_t)p * cplane;
+    const uint8_t *fm = fmask + (size_t)(p / channels) * fplane;
+    double *up = u + (size_t)p * fplane;
+    const int Xm = X > 0 ? X - 1 : 0, Xp = X < wc - 1 ? X + 1 : wc - 1;
+    const int Ym = Y > 0 ? Y - 1 : 0, Yp = Y < hc - 1 ? Y + 1 : hc - 1;
+    double rowL[3], rowR[3];  // x-interpolated values on coarse rows Ym, Y, Yp
+    const int ys[3] = {Ym, Y, Yp};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double *row = cp + (size_t)ys[k] * wc;
+        const double mid = row[X];
+        rowL[k] = 0.75 * mid + 0.25 * row[Xm];  // fine x even: far = near - 1
+        rowR[k] = 0.75 * mid + 0.25 * row[Xp];  // fine x odd : far = near + 1
+    }
+    const int y0 = 2 * Y, x0 = 2 * X;
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy) {
+        const int y = y0 + dy;
+        if (y >= h) break;
+        const int kf = dy ? 2 : 0;  // far row: Y+1 for odd fine rows, Y-1 for even
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx) {
+            const int x = x0 + dx;
+            if (x >= w) break;
+            const double nearv = dx ? rowR[1] : rowL[1];
+            const double farv = dx ? rowR[kf] : rowL[kf];
+            const double val = 0.75 * nearv + 0.25 * farv;
+            const size_t i = (size_t)y * w + x;
+            const bool m = fm[i] != 0;
+            if (SOLUTION) {
+                up[i] = m ? frhs[(size_t)p * fplane + i] : val;
+            } else {
+                if (!m) up[i] += val;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K6 ------
+__global__ void __launch_bounds__(ST_THREADS)
+downsample_mask_kernel(const uint8_t *__restrict__ fine, int h, int w, uint8_t *__restrict__ coarse) {
+    const int f = blockIdx.z;
+    const int hc = (h + 1) >> 1, wc = (w + 1) >> 1;
+    const int X = blockIdx.x * 64 + (threadIdx.x & 63);
+    const int Y = blockIdx.y * 4 + (threadIdx.x >> 6);
+    if (X >= wc || Y >= hc) return;
+    const uint8_t *fm = fine + (size_t)f * h * w;
+    const int y0 = 2 * Y, x0 = 2 * X;
+    const bool hx = x0 + 1 < w, hy = y0 + 1 < h;
+    int any = fm[(size_t)y0 * w + x0];
+    if (hx) any |= fm[(size_t)y0 * w + x0 + 1];
+    if (hy) any |= fm[(size_t)(y0 + 1) * w + x0];
+    if (hx && hy) any |= fm[(size_t)(y0 + 1) * w + x0 + 1];
+    coarse[(size_t)f * hc * wc + (size_t)Y * wc + X] = any ? 1 : 0;
+}
+
+// Values: every fine known pixel enters its cell with weight 4 - (#known
+// direct neighbours); in-cell neighbours come from the fine mask, the others
+// from the coarse mask of the adjacent cell, off-image counts as unknown
+// (multigrid.py:122-137).  Cells known on the coarse grid whose total weight is
+// 0 fall back to the plain average (:143-145); 0 off the coarse mask (:146).
+// Fine values are read only at fine mask pixels (level-0 `known` is arbitrary
+// elsewhere; hierarchy values are 0 there).
+__global__ void __launch_bounds__(ST_THREADS)
+downsample_values_kernel(const uint8_t *__restrict__ fmask, const uint8_t *__restrict__ cmask,
+                         const double *__restrict__ frhs, int h, int w, int channels, int modified,
+                         double *__restrict__ crhs) {
+    const int p = blockIdx.z;
+    const int hc = (h + 1) >> 1, wc = (w + 1) >> 1;
+    const int X = blockIdx.x * 64 + (threadIdx.x & 63);
+    const int Y = blockIdx.y * 4 + (threadIdx.x >> 6);
+    if (X >= wc || Y >= hc) return;
+    const size_t fplane = (size_t)h * w, cplane = (size_t)hc * wc;
+    const uint8_t *fm = fmask + (size_t)(p / channels) * fplane;
+    const uint8_t *cm = cmask + (size_t)(p / channels) * cplane;
+    const double *fr = frhs + (size_t)p * fplane;
+    const size_t ci = (size_t)Y * wc + X;
+    double out = 0.0;
+    if (cm[ci]) {
+        double wg[4] = {0, 0, 0, 0}, wv[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0}, nv[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < 2; ++dx) {
+                const int y = 2 * Y + dy, x = 2 * X + dx;
+                if (y >= h || x >= w) continue;
+                const size_t i = (size_t)y * w + x;
+                if (!fm[i]) continue;
+                const double val = fr[i];
+                double n = 0.0;
+                if (x >= 1) n += (x & 1) ? (double)(fm[i - 1] != 0) : (double)(cm[(size_t)Y * wc + (X - 1)] != 0);
+                if (x <= w - 2) n += !(x & 1) ? (double)(fm[i + 1] != 0) : (double)(cm[(size_t)Y * wc + (X + 1)] != 0);
+                if (y >= 1) n += (y & 1) ? (double)(fm[i - w] != 0) : (double)(cm[(size_t)(Y - 1) * wc + X] != 0);
+                if (y <= h - 2) n += !(y & 1) ? (double)(fm[i + w] != 0) : (double)(cm[(size_t)(Y + 1) * wc + X] != 0);
+                const int k = dy * 2 + dx;
+                wg[k] = 4.0 - n;
+                wv[k] = wg[k] * val;
+                c1[k] = 1.0;
+                nv[k] = val;
+            }
+        const double nnum = (nv[0] + nv[1]) + (nv[2] + nv[3]);
+        const double nden = (c1[0] + c1[1]) + (c1[2] + c1[3]);
+        const double naive = nnum / fmax(1.0, nden);
+        if (modified) {
+            const double num = (wv[0] + wv[1]) + (wv[2] + wv[3]);
+            const double den = (wg[0] + wg[1]) + (wg[2] + wg[3]);
+            out = den == 0.0 ? naive : num / fmax(1.0, den);
+        } else {
+            out = naive;
+        }
+    }
+    crhs[(size_t)p * cplane + ci] = out;
+}
+
+// 8-bit ingest / egress (fileio.py:51-65): known = float(u8); out = clip(rint(u)).
+__global__ void __launch_bounds__(ST_THREADS)
+u8_to_f64_kernel(const uint8_t *__restrict__ in, size_t n, double *__restrict__ out) {
+    const size_t i = (size_t)blockIdx.x * ST_THREADS + threadIdx.x;
+    if (i < n) out[i] = (double)in[i];
+}
+
+__global__ void __launch_bounds__(ST_THREADS)
+f64_to_u8_kernel(const double *__restrict__ in, size_t n, uint8_t *__restrict__ out) {
+    const size_t i = (size_t)blockIdx.x * ST_THREADS + threadIdx.x;
+    if (i < n) {
+        double v = rint(in[i]);  // round half to even, like np.rint
+        v = v < 0.0 ? 0.0 : (v > 255.0 ? 255.0 : v);
+        out[i] = (uint8_t)v;
+    }
+}
+
+}  // namespace b200p

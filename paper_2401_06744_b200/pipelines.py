@@ -1,0 +1,119 @@
+"""Named-pipeline front end: the drop-in boundary of the path.
+
+``solve_image(problem, "mg-oras", cfg)`` has the reference's signature, result
+type and error behaviour (pipelines.py:20-114).  Only the ORAS-smoothed
+full-multigrid pipeline is built here; the other names of the reference are
+recognised and rejected with NotImplementedError (out of scope).
+``solve_frames`` is the batched entry (frames x channels in one plan).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from .core import EmptyMaskError, InpaintingProblem
+from .multigrid import LevelHierarchy, MultigridConfig, build_hierarchy, cached_plan, fmg_solve
+from .solvers import SolveReport
+
+SOLVER_NAMES = ("cg", "oras", "ml-cg", "ml-oras", "mg-cg", "mg-oras")
+BUILT = ("mg-oras",)
+
+
+def split_solver_name(name: str):
+    """pipelines.py:23-31: name -> (smoother, mode)."""
+    if name not in SOLVER_NAMES:
+        raise ValueError(f"unknown solver {name!r}, expected one of {SOLVER_NAMES}")
+    head, sep, tail = name.partition("-")
+    if not sep:
+        return name, "single"
+    return tail, {"ml": "multilevel", "mg": "full_multigrid"}[head]
+
+
+def join_solver_name(base: str, mode: str) -> str:
+    name = {"single": "", "multilevel": "ml-", "full_multigrid": "mg-"}[mode] + base
+    if name not in SOLVER_NAMES:
+        raise ValueError(f"no solver for base {base!r} in mode {mode!r}")
+    return name
+
+
+def _require_built(name: str):
+    split_solver_name(name)
+    if name not in BUILT:
+        raise NotImplementedError(
+            f"pipeline {name!r} is outside the B200 hot path; only {BUILT} are built")
+
+
+@dataclass
+class SolveResult:
+    """pipelines.py:75-93."""
+
+    fields: np.ndarray
+    reports: list
+    elapsed: float
+
+    @property
+    def converged(self) -> bool:
+        return all(r.converged for r in self.reports)
+
+    @property
+    def iterations(self) -> int:
+        return max(r.iterations for r in self.reports)
+
+    @property
+    def final_rel_residual(self) -> float:
+        return max(r.final_rel_residual for r in self.reports)
+
+
+def solve_channel(problem: InpaintingProblem, name: str, cfg: MultigridConfig | None = None,
+                  channel: int = 0, hierarchy: LevelHierarchy | None = None, callback=None):
+    """pipelines.py:42-72 for "mg-oras"."""
+    _require_built(name)
+    base, mode = split_solver_name(name)
+    cfg = replace(cfg or MultigridConfig(), smoother=base, mode=mode)
+    if hierarchy is None:
+        hierarchy = build_hierarchy(problem, cfg)
+    return fmg_solve(hierarchy, cfg, channel, callback=callback)
+
+
+def solve_image(problem: InpaintingProblem, name: str = "mg-oras",
+                cfg: MultigridConfig | None = None) -> SolveResult:
+    """All channels of one frame, batched in one plan (pipelines.py:96-114).
+
+    Host arrays in, host arrays out; ``elapsed`` covers H2D, hierarchy build,
+    the solve and D2H.
+    """
+    _require_built(name)
+    base, mode = split_solver_name(name)
+    cfg = replace(cfg or MultigridConfig(), smoother=base, mode=mode)
+    if not problem.mask.any():
+        raise EmptyMaskError("cannot solve without known pixels")
+    t0 = time.perf_counter()
+    h, w = problem.shape
+    plan = cached_plan(w, h, problem.channels, 1, cfg, problem.spacing)
+    out, reports = plan.solve_host(problem.mask.view(np.uint8)[None], problem.known[None])
+    elapsed = time.perf_counter() - t0
+    for r in reports:
+        r.wall_time = elapsed
+    return SolveResult(fields=out[0], reports=reports, elapsed=elapsed)
+
+
+def solve_frames(masks, known, cfg: MultigridConfig | None = None, spacing: float = 1.0):
+    """Batch of independent frames: masks (F,H,W), known (F,C,H,W) -> (fields, reports[F][C], elapsed)."""
+    cfg = cfg or MultigridConfig()
+    masks = np.asarray(masks)
+    known = np.asarray(known, dtype=np.float64)
+    if known.ndim == 3:
+        known = known[:, None]
+    if masks.ndim != 3 or known.ndim != 4 or known.shape[0] != masks.shape[0] or known.shape[2:] != masks.shape[1:]:
+        raise ValueError(f"need masks (F,H,W) and known (F,C,H,W), got {masks.shape} and {known.shape}")
+    if not np.isfinite(known).all():
+        raise ValueError("known values contain non-finite entries")
+    f, c, h, w = known.shape
+    t0 = time.perf_counter()
+    plan = cached_plan(w, h, c, f, cfg, spacing)
+    out, reports = plan.solve_host(masks.astype(bool).view(np.uint8), known)
+    elapsed = time.perf_counter() - t0
+    return out, [reports[i * c:(i + 1) * c] for i in range(f)], elapsed

@@ -1,0 +1,138 @@
+"""Generates the golden fixtures in this directory from the LIVE reference
+(`/root/reference/pkg/src/diffpaint`, pure Python/NumPy).  Run in the build
+container (the reference is not present on the GPU box):
+
+    python tests/golden/make_golden.py            # small vectors  (seconds)
+    python tests/golden/make_golden.py --anchors  # + 1080p / 4K anchors (~3 min)
+
+Outputs: golden_small.npz (inputs are regenerated from seeds by the tests; only
+reference OUTPUTS are stored) and anchors.json / anchors_4k_sample.npz."""
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, "/root/reference/pkg/src")
+import diffpaint as dp  # noqa: E402
+from diffpaint import multigrid as mg  # noqa: E402
+from diffpaint import solvers as sv  # noqa: E402
+
+
+def seeded(w, h, density, seed, channels=1):
+    mask = dp.random_mask(w, h, density, seed)
+    known = np.stack([dp.synthetic_image(w, h, seed + 1000 + c) for c in range(channels)])
+    return dp.InpaintingProblem(mask, known)
+
+
+def small():
+    out = {}
+    rng = np.random.default_rng(2401_06744)
+    # inputs drawn here are stored too (they are not reproducible from a public seed recipe)
+    for i, shape in enumerate([(8, 8), (7, 9), (8, 5), (33, 47)]):
+        m = rng.random(shape) < 0.25
+        m.flat[0] = True
+        u = rng.normal(size=shape) * 100
+        b = rng.normal(size=shape) * 100
+        cs = ((shape[0] + 1) // 2, (shape[1] + 1) // 2)
+        cm = mg.downsample_mask(m)
+        rhs = np.where(m, np.round(rng.uniform(0, 255, size=shape)), 0.0)
+        ce = rng.normal(size=cs)
+        out[f"t{i}_mask"] = m
+        out[f"t{i}_u"] = u
+        out[f"t{i}_b"] = b
+        out[f"t{i}_rhs"] = rhs
+        out[f"t{i}_ce"] = ce
+        out[f"t{i}_apply"] = dp.StencilOperator(m, 2.0).apply(u)
+        out[f"t{i}_residual"] = dp.StencilOperator(m, 1.0).residual(b, u)
+        out[f"t{i}_cmask"] = cm
+        out[f"t{i}_val_mod"] = mg.downsample_values_modified(m, cm, rhs)
+        out[f"t{i}_val_naive"] = mg.downsample_values_naive(m, rhs)
+        out[f"t{i}_restrict"] = mg.restrict_residual(u, cm)
+        out[f"t{i}_pro_corr"] = mg.prolongate_correction(ce, m)
+        out[f"t{i}_pro_sol"] = mg.prolongate_solution(ce, m, rhs)
+    # partitions / weights
+    for j, (dim, bs, ov) in enumerate([(3840, 32, 6), (2160, 32, 6), (64, 32, 6), (80, 16, 2), (56, 32, 6),
+                                       (20, 32, 6), (135, 32, 6), (100, 24, 4), (33, 32, 0), (1080, 16, 2)]):
+        part = dp.build_partition(dim, dim, bs, ov)
+        out[f"p{j}_cfg"] = np.array([dim, bs, ov])
+        out[f"p{j}_xs"] = part.xs
+        out[f"p{j}_wx"] = dp.build_weights(part).wx
+    # ORAS sweeps and block solves on the clamped-block case of tests/test_solvers.py:156-169
+    prob = seeded(80, 56, 0.15, 8)
+    for bs, ov in [(32, 6), (16, 2)]:
+        part = dp.build_partition(80, 56, bs, ov)
+        blocks = sv.BlockSolver(prob.mask, 1.0, part, dp.build_weights(part), 0.5)
+        b = prob.rhs(0)
+        u = b.copy()
+        hist = []
+        sweeps, rn = sv.oras_sweeps(prob.operator(), blocks, b, u, max_sweeps=3, stop_norm=0.0, eta=1e-5,
+                                    local_max_iters=4 * part.block_w * part.block_h,
+                                    on_state=lambda uu, r, s: hist.append(r))
+        out[f"sweep_{bs}_{ov}_u"] = u
+        out[f"sweep_{bs}_{ov}_hist"] = np.array(hist)
+        r = prob.operator().residual(b, b)
+        out[f"blocks_{bs}_{ov}_v"] = blocks.solve_blocks(blocks.gather(r), 1e-5 * float(np.vdot(r, r)),
+                                                        4 * part.block_w * part.block_h)
+    # whole-path solves
+    cases = {
+        "c64": (64, 64, 0.10, 1, 1, dict(block_size=16, overlap=2), dict(tol_rel=1e-8)),
+        "c80x56": (80, 56, 0.15, 8, 1, dict(block_size=32, overlap=6), dict(tol_rel=1e-6)),
+        "c97x131": (97, 131, 0.03, 2, 2, dict(block_size=16, overlap=2), dict()),
+        "c20x30": (20, 30, 0.20, 3, 1, dict(block_size=32, overlap=6), dict(tol_rel=1e-6)),
+        "c256": (256, 256, 0.05, 0, 1, dict(block_size=16, overlap=2), dict()),
+    }
+    meta = {}
+    for name, (w, h, dens, seed, ch, mkw, skw) in cases.items():
+        prob = seeded(w, h, dens, seed, ch)
+        cfg = dp.MultigridConfig(solver=dp.SolverConfig(**skw), **mkw)
+        res = dp.solve_image(prob, "mg-oras", cfg)
+        out[f"{name}_fields"] = res.fields
+        meta[name] = dict(w=w, h=h, density=dens, seed=seed, channels=ch, mg=mkw, solver=skw,
+                          reports=[dict(iterations=r.iterations, final_rel=r.final_rel_residual,
+                                        baseline=r.baseline_residual, fine_units=r.fine_smoother_iterations,
+                                        converged=bool(r.converged), history=list(r.history))
+                                   for r in res.reports])
+        hier = dp.build_hierarchy(prob, cfg)
+        out[f"{name}_cascade"] = dp.cascadic_init(hier, cfg, 0)
+        out[f"{name}_nlevels"] = np.array(len(hier))
+        out[f"{name}_coarsest_rhs"] = hier.levels[-1].rhs
+    np.savez_compressed(os.path.join(HERE, "golden_small.npz"), **out)
+    with open(os.path.join(HERE, "golden_small.json"), "w") as f:
+        json.dump(meta, f, indent=1)
+
+
+def anchors():
+    os.environ["INPAINT_THREADS"] = "0"
+    res = {}
+    sample = {}
+    for name, (w, h, dens, ch, bs, ov) in {
+        "1080p_4pct_16_2": (1920, 1080, 0.04, 3, 16, 2),
+        "4k_2pct_32_6": (3840, 2160, 0.02, 3, 32, 6),
+        "4k_0.5pct_32_6": (3840, 2160, 0.005, 1, 32, 6),
+    }.items():
+        prob = seeded(w, h, dens, 0, ch)
+        cfg = dp.MultigridConfig(block_size=bs, overlap=ov)
+        r = dp.solve_image(prob, "mg-oras", cfg)
+        res[name] = dict(w=w, h=h, density=dens, channels=ch, block_size=bs, overlap=ov, seed=0,
+                         elapsed_s=r.elapsed, threads=os.cpu_count(),
+                         reports=[dict(iterations=x.iterations, final_rel=x.final_rel_residual,
+                                       baseline=x.baseline_residual, fine_units=x.fine_smoother_iterations,
+                                       history=list(x.history)) for x in r.reports])
+        sample[name] = r.fields.reshape(ch, -1)[:, ::997].copy()
+        print(name, r.elapsed, [x.iterations for x in r.reports], flush=True)
+    with open(os.path.join(HERE, "anchors.json"), "w") as f:
+        json.dump(res, f, indent=1)
+    np.savez_compressed(os.path.join(HERE, "anchors_sample.npz"), **sample)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--anchors", action="store_true")
+    a = ap.parse_args()
+    small()
+    if a.anchors:
+        anchors()

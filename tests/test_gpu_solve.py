@@ -1,0 +1,210 @@
+"""GPU parity of the whole mg-oras path (solve_image / fmg_solve) against the
+CPU oracle at the BASELINE.json configurations, through the C-ABI.
+
+Bar (BASELINE.json north_star): max-abs <= 1e-3 on [0,255], the same V-cycle
+count per channel and the same final relative residual (checked to 1e-6
+relative).  Full-size cases additionally check size-independent properties:
+interpolation at mask pixels, the discrete maximum principle, a recomputed
+residual, batch == single-frame bit-for-bit, run-to-run determinism."""
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2401_06744_b200 as bp
+
+pytestmark = pytest.mark.gpu
+
+TOL_ABS = 1e-3       # north_star: max-abs on a [0,255] scale
+TOL_REL_RES = 1e-6   # relative agreement of final relative residuals
+
+
+def _cfgs(bs, ov, **kw):
+    skw = {k: kw.pop(k) for k in list(kw) if k in ("tol_rel", "alpha", "local_tol_fraction", "local_max_iters")}
+    return (oracle.MultigridConfig(block_size=bs, overlap=ov, solver=oracle.SolverConfig(**skw), **kw),
+            bp.MultigridConfig(block_size=bs, overlap=ov, solver=bp.SolverConfig(**skw), **kw))
+
+
+def _compare(m, k, cfg_o, cfg_b, spacing=1.0):
+    ref, reps_o = oracle.solve_image(m, k, spacing, cfg_o)
+    res = bp.solve_image(bp.InpaintingProblem(m, k, spacing), "mg-oras", cfg_b)
+    assert res.fields.shape == ref.shape
+    for ro, rg in zip(reps_o, res.reports):
+        assert rg.iterations == ro.iterations
+        assert rg.fine_smoother_iterations == ro.fine_smoother_iterations
+        assert rg.converged == ro.converged
+        assert len(rg.history) == len(ro.history)
+        assert rg.baseline_residual == pytest.approx(ro.baseline_residual, rel=1e-12)
+        assert rg.final_rel_residual == pytest.approx(ro.final_rel_residual, rel=TOL_REL_RES)
+        np.testing.assert_allclose(rg.history, ro.history, rtol=1e-5)
+    err = np.abs(res.fields - ref).max()
+    assert err <= TOL_ABS, f"max-abs {err}"
+    return res, ref, err
+
+
+def _properties(m, k, res, cfg_b, spacing=1.0):
+    u = res.fields
+    # interpolation condition: exact at mask pixels
+    assert np.array_equal(u[:, m], k[:, m])
+    # discrete maximum principle (slack for the unconverged interior)
+    lo, hi = k[:, m].min(), k[:, m].max()
+    assert u.min() >= lo - 1e-6 * (hi - lo + 1) and u.max() <= hi + 1e-6 * (hi - lo + 1)
+    # the reported residual is the residual of the returned field
+    for c, rep in enumerate(res.reports):
+        b = np.where(m, k[c], 0.0)
+        rn = np.linalg.norm(oracle.residual(m, spacing, b, u[c]))
+        assert rn / rep.baseline_residual == pytest.approx(rep.final_rel_residual, rel=1e-9)
+        assert rep.final_rel_residual <= cfg_b.solver.tol_rel
+
+
+def test_config1_256_gray():
+    """BASELINE config 0: 256x256 gray, 5 %, block 16 overlap 2 (1 cycle, rel 9.844e-4)."""
+    m, k = oracle.seeded_problem(256, 256, 0.05, 0)
+    res, ref, err = _compare(m, k, *_cfgs(16, 2))
+    assert res.reports[0].iterations == 1
+    assert res.reports[0].final_rel_residual == pytest.approx(9.844034e-4, rel=1e-5)
+    _properties(m, k, res, _cfgs(16, 2)[1])
+
+
+@pytest.mark.parametrize("bs,ov", [(16, 2), (32, 6)])
+def test_config2_1080p_rgb(bs, ov):
+    """BASELINE config 1: 1920x1080 RGB, 4 % mask."""
+    m, k = oracle.seeded_problem(1920, 1080, 0.04, 0, channels=3)
+    res, ref, err = _compare(m, k, *_cfgs(bs, ov))
+    _properties(m, k, res, _cfgs(bs, ov)[1])
+
+
+def test_config3_4k_rgb():
+    """BASELINE config 2 (headline): 3840x2160 RGB, 2 % mask, block 32 overlap 6."""
+    m, k = oracle.seeded_problem(3840, 2160, 0.02, 0, channels=3)
+    res, ref, err = _compare(m, k, *_cfgs(32, 6))
+    assert [r.iterations for r in res.reports] == [2, 2, 2]
+    assert res.reports[0].final_rel_residual == pytest.approx(1.289595e-4, rel=1e-5)
+    _properties(m, k, res, _cfgs(32, 6)[1])
+
+
+def test_config4_4k_sparse():
+    """BASELINE config 3: 3840x2160, 0.5 % mask (one more active level); also a tighter tolerance."""
+    m, k = oracle.seeded_problem(3840, 2160, 0.005, 0, channels=1)
+    _compare(m, k, *_cfgs(32, 6))
+    res, ref, err = _compare(m, k, *_cfgs(32, 6, tol_rel=1e-5))
+    assert res.reports[0].iterations > 2
+
+
+@pytest.mark.parametrize("w,h,dens,seed,bs,ov,kw", [
+    (64, 64, 0.10, 1, 16, 2, dict(tol_rel=1e-8)),                  # tests/test_multigrid.py:328-334 setup
+    (80, 56, 0.15, 8, 32, 6, dict(tol_rel=1e-6)),                  # clamped blocks on both axes
+    (97, 131, 0.03, 2, 16, 2, dict()),                             # odd dims at every level
+    (20, 30, 0.20, 3, 32, 6, dict(tol_rel=1e-6)),                  # single level (image <= block)
+    (256, 64, 0.05, 4, 32, 6, dict()),                             # blocks clipped in one axis on coarse levels
+    (200, 150, 0.05, 5, 24, 4, dict()),                            # generic-kernel block size
+    (128, 128, 0.05, 6, 16, 2, dict(nu_pre=2, nu_post=1)),
+    (128, 128, 0.05, 6, 16, 2, dict(nu_pre=0, nu_post=2)),
+    (128, 128, 0.05, 6, 16, 2, dict(value_downsampling="naive")),
+    (128, 128, 0.05, 6, 16, 2, dict(alpha=2.0, local_tol_fraction=1e-3)),
+    (128, 128, 0.05, 6, 16, 2, dict(v_cycles_max=1, tol_rel=1e-9)),  # cap reached: converged False
+    (128, 128, 0.05, 6, 8, 2, dict()),
+    (300, 300, 0.9, 7, 32, 6, dict()),                             # dense mask: coarse levels all-known
+])
+def test_small_cases(w, h, dens, seed, bs, ov, kw):
+    m, k = oracle.seeded_problem(w, h, dens, seed, channels=2)
+    _compare(m, k, *_cfgs(bs, ov, **kw))
+
+
+def test_spacing_other_than_one():
+    m, k = oracle.seeded_problem(120, 90, 0.05, 3)
+    _compare(m, k, *_cfgs(16, 2), spacing=0.5)
+
+
+def test_fmg_solve_and_solve_channel_api():
+    m, k = oracle.seeded_problem(128, 96, 0.05, 2, channels=3)
+    cfg_o, cfg_b = _cfgs(16, 2)
+    prob = bp.InpaintingProblem(m, k)
+    hier = bp.build_hierarchy(prob, cfg_b)
+    ho = oracle.build_hierarchy(m, k, 1.0, cfg_o)
+    for c in range(3):
+        u, rep = bp.fmg_solve(hier, cfg_b, channel=c)
+        uo, ro = oracle.fmg_solve(ho, cfg_o, channel=c)
+        assert rep.solver == "mg-oras" and rep.iterations == ro.iterations
+        assert np.abs(u - uo).max() <= TOL_ABS
+        u2, rep2 = bp.solve_channel(prob, "mg-oras", cfg_b, channel=c, hierarchy=hier)
+        assert np.array_equal(u, u2)
+    res = bp.solve_image(prob, "mg-oras", cfg_b)
+    assert res.converged and res.iterations == max(r.iterations for r in res.reports)
+    assert res.elapsed > 0
+
+
+def test_errors_match_reference_behaviour():
+    m = np.zeros((32, 32), bool)
+    k = np.zeros((32, 32))
+    with pytest.raises(bp.EmptyMaskError):
+        bp.solve_image(bp.InpaintingProblem(m, k), "mg-oras")
+    m[3, 3] = True
+    with pytest.raises(ValueError):
+        bp.solve_image(bp.InpaintingProblem(m, k), "no-such-solver")
+    with pytest.raises(NotImplementedError):
+        bp.solve_image(bp.InpaintingProblem(m, k), "mg-cg")
+    with pytest.raises(ValueError):
+        bp.solve_image(bp.InpaintingProblem(m, k), "mg-oras", bp.MultigridConfig(block_size=8, overlap=8))
+    with pytest.raises(ValueError):
+        bp.InpaintingProblem(m, np.full((32, 32), np.nan))
+    # single known pixel -> constant solution (tests/test_oracle.py:38-44 of the reference)
+    k[3, 3] = 42.0
+    res = bp.solve_image(bp.InpaintingProblem(m, k), "mg-oras",
+                         bp.MultigridConfig(solver=bp.SolverConfig(tol_rel=1e-10)))
+    np.testing.assert_allclose(res.fields, 42.0, rtol=0, atol=1e-6)
+
+
+def test_batch_equals_single_frames_and_is_deterministic():
+    """Frames are independent problems: a batched plan gives bit-identical fields."""
+    w, h = 320, 200
+    masks, known = [], []
+    for f in range(3):
+        m, k = oracle.seeded_problem(w, h, [0.02, 0.05, 0.3][f], f, channels=3)
+        masks.append(m)
+        known.append(k)
+    cfg = bp.MultigridConfig(block_size=32, overlap=6)
+    out, reports, _ = bp.solve_frames(np.stack(masks), np.stack(known), cfg)
+    out2, _, _ = bp.solve_frames(np.stack(masks), np.stack(known), cfg)
+    assert np.array_equal(out, out2)
+    for f in range(3):
+        single = bp.solve_image(bp.InpaintingProblem(masks[f], known[f]), "mg-oras", cfg)
+        assert np.array_equal(single.fields, out[f])
+        assert [r.iterations for r in single.reports] == [r.iterations for r in reports[f]]
+        ref, _ = oracle.solve_image(masks[f], known[f], 1.0, oracle.MultigridConfig(block_size=32, overlap=6))
+        assert np.abs(out[f] - ref).max() <= TOL_ABS
+
+
+def test_graph_and_eager_paths_agree():
+    m, k = oracle.seeded_problem(256, 192, 0.04, 5, channels=3)
+    cfg = bp.MultigridConfig(block_size=16, overlap=2)
+    mk = m.view(np.uint8)[None]
+    a = bp.Plan(256, 192, 3, 1, cfg, use_graphs=True)
+    b = bp.Plan(256, 192, 3, 1, cfg, use_graphs=False)
+    oa, ra = a.solve_host(mk, k[None])
+    ob, rb = b.solve_host(mk, k[None])
+    assert np.array_equal(oa, ob)
+    assert a.launch_count == b.launch_count > 0
+    # replay of the captured graphs
+    oc, _ = a.solve_host(mk, k[None])
+    assert np.array_equal(oa, oc)
+    # profiling mode (eager + events) leaves results unchanged and reports kernels
+    a.profile(True)
+    od, _ = a.solve_host(mk, k[None])
+    prof = a.profile_summary()
+    a.profile(False)
+    assert np.array_equal(oa, od)
+    assert prof["oras_sweep"][1] > 0 and prof["oras_sweep"][0] > 0
+    a.close(); b.close()
+
+
+def test_u8_ingest_egress():
+    """fileio.image_from_fields (fileio.py:58-65): round half to even, clip to [0,255]."""
+    m, k = oracle.seeded_problem(200, 120, 0.05, 1, channels=3)
+    cfg = bp.MultigridConfig(block_size=16, overlap=2)
+    plan = bp.Plan(200, 120, 3, 1, cfg)
+    out8, reps = plan.solve_host_u8(m.view(np.uint8)[None], k.astype(np.uint8)[None])
+    ref = bp.solve_image(bp.InpaintingProblem(m, k), "mg-oras", cfg)
+    expect = np.clip(np.rint(ref.fields), 0, 255).astype(np.uint8)
+    assert np.array_equal(out8[0], expect)
+    plan.close()

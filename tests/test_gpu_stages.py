@@ -1,0 +1,250 @@
+"""GPU parity, stage by stage: every CUDA kernel of the path against the CPU
+oracle (oracle/, a restatement of the reference pinned by test_oracle_*.py) on
+the same seeded inputs, through the C-ABI (ctypes).  fp64 everywhere; the
+tolerances below are absolute on a [0,255] value scale unless stated."""
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2401_06744_b200 as bp
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(8, 8), (7, 9), (8, 5), (33, 47), (135, 240), (1, 1), (1, 6), (64, 3)]
+
+
+def _mask(rng, shape, density):
+    m = rng.random(shape) < density
+    if not m.any():
+        m.flat[0] = True
+    return m
+
+
+# ------------------------------------------------------------------ core ----
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("spacing", [1.0, 2.0, 0.5])
+def test_apply_and_residual(rng, shape, spacing):
+    m = _mask(rng, shape, 0.2)
+    u = rng.normal(size=shape) * 100
+    b = rng.normal(size=shape) * 100
+    op = bp.StencilOperator(m, spacing)
+    np.testing.assert_allclose(op.apply(u), oracle.apply_operator(m, spacing, u), rtol=0, atol=1e-10)
+    np.testing.assert_allclose(op.residual(b, u), oracle.residual(m, spacing, b, u), rtol=0, atol=1e-10)
+    r = oracle.residual(m, spacing, b, u)
+    assert op.residual_sqnorm(b, u) == pytest.approx(float(np.vdot(r, r)), rel=1e-13)
+
+
+def test_stencil_known_answers():
+    """tests/test_core.py:18-41 of the reference: 4m-n-s-e-w inside, /h^2 scaling, identity at mask."""
+    u = np.arange(25, dtype=float).reshape(5, 5) ** 2
+    m = np.zeros((5, 5), bool)
+    m[0, 0] = True
+    out = bp.StencilOperator(m, 1.0).apply(u)
+    assert out[2, 2] == 4 * u[2, 2] - u[1, 2] - u[3, 2] - u[2, 1] - u[2, 3]
+    assert out[0, 0] == u[0, 0]
+    assert out[0, 2] == 3 * u[0, 2] - u[1, 2] - u[0, 1] - u[0, 3]
+    assert out[4, 4] == 2 * u[4, 4] - u[3, 4] - u[4, 3]
+    out2 = bp.StencilOperator(m, 2.0).apply(u)
+    np.testing.assert_allclose(out2[~m], out[~m] / 4.0, rtol=1e-15)
+    const = bp.StencilOperator(np.zeros((6, 7), bool), 1.0).apply(np.full((6, 7), 3.25))
+    assert np.abs(const).max() == 0.0
+
+
+def test_shape_errors():
+    op = bp.StencilOperator(np.ones((4, 4), bool))
+    with pytest.raises(ValueError):
+        op.apply(np.zeros((4, 5)))
+    with pytest.raises(ValueError):
+        bp.StencilOperator(np.ones((4, 4), bool), 0.0)
+
+
+# ------------------------------------------------------------- transfers ----
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_downsample_mask(rng, shape):
+    for density in (0.05, 0.5):
+        m = _mask(rng, shape, density)
+        np.testing.assert_array_equal(bp.downsample_mask(m), oracle.downsample_mask(m))
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("density", [0.05, 0.3, 0.9, 1.0])
+def test_downsample_values(rng, shape, density):
+    m = _mask(rng, shape, density) if density < 1 else np.ones(shape, bool)
+    rhs = np.where(m, np.round(rng.uniform(0, 255, size=shape)), 0.0)
+    cm = oracle.downsample_mask(m)
+    got = bp.downsample_values_modified(m, cm, rhs)
+    np.testing.assert_allclose(got, oracle.downsample_values_modified(m, cm, rhs), rtol=0, atol=1e-12)
+    got = bp.downsample_values_naive(m, rhs)
+    np.testing.assert_allclose(got, oracle.downsample_values_naive(m, rhs), rtol=0, atol=1e-12)
+
+
+def test_downsample_values_known_answers():
+    """tests/test_multigrid.py:73-92 of the reference (plus-shape suppression, all-suppressed fallback)."""
+    m = np.zeros((4, 4), bool)
+    rhs = np.zeros((4, 4))
+    # a fully known 2x2 cell whose every pixel has all four neighbours known -> weights 0 -> naive
+    m[:, :] = True
+    rhs[:2, :2] = [[10, 20], [30, 40]]
+    cm = oracle.downsample_mask(m)
+    out = bp.downsample_values_modified(m, cm, rhs)
+    assert out[0, 0] == pytest.approx(oracle.downsample_values_modified(m, cm, rhs)[0, 0], abs=1e-12)
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_restrict_residual(rng, shape):
+    r = rng.normal(size=shape)
+    cm = _mask(rng, ((shape[0] + 1) // 2, (shape[1] + 1) // 2), 0.3)
+    np.testing.assert_allclose(bp.restrict_residual(r, cm), oracle.restrict_residual(r, cm), rtol=0, atol=1e-13)
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_prolongation(rng, shape):
+    cs = ((shape[0] + 1) // 2, (shape[1] + 1) // 2)
+    c = rng.normal(size=cs) * 50
+    fm = _mask(rng, shape, 0.2)
+    rhs = rng.normal(size=shape)
+    np.testing.assert_allclose(bp.prolongate_correction(c, fm), oracle.prolongate_correction(c, fm), rtol=0, atol=1e-12)
+    np.testing.assert_allclose(bp.prolongate_solution(c, fm, rhs), oracle.prolongate_solution(c, fm, rhs), rtol=0, atol=1e-12)
+    with pytest.raises(ValueError):
+        bp.prolongate_correction(np.zeros((cs[0] + 1, cs[1])), fm)
+
+
+def test_prolongation_1d_weights():
+    """(3a+b)/4 interior, border clamp (tests/test_multigrid.py:161-167 of the reference)."""
+    c = np.array([[4.0, 8.0, 16.0]])
+    out = bp.prolongate_correction(c, np.zeros((1, 6), bool))
+    np.testing.assert_allclose(out[0], [4.0, 5.0, 7.0, 10.0, 14.0, 16.0], rtol=0, atol=1e-14)
+
+
+@pytest.mark.parametrize("w,h,bs,ov", [(256, 256, 16, 2), (250, 130, 32, 6), (70, 45, 16, 2)])
+@pytest.mark.parametrize("mode", ["modified", "naive"])
+def test_build_hierarchy(w, h, bs, ov, mode):
+    m, k = oracle.seeded_problem(w, h, 0.05, 3, channels=2)
+    cfg_o = oracle.MultigridConfig(block_size=bs, overlap=ov, value_downsampling=mode)
+    cfg_b = bp.MultigridConfig(block_size=bs, overlap=ov, value_downsampling=mode)
+    ho = oracle.build_hierarchy(m, k, 1.0, cfg_o)
+    hb = bp.build_hierarchy(bp.InpaintingProblem(m, k), cfg_b)
+    assert len(hb) == len(ho)
+    for lo, lb in zip(ho.levels, hb.levels):
+        assert lb.shape == lo.shape
+        assert lb.spacing == lo.spacing
+        np.testing.assert_array_equal(lb.mask, lo.mask)
+        np.testing.assert_allclose(lb.rhs, lo.rhs, rtol=0, atol=1e-11)
+        np.testing.assert_array_equal(lb.part.xs, lo.xs)
+        np.testing.assert_array_equal(lb.part.ys, lo.ys)
+        np.testing.assert_array_equal(lb.weights.wx, lo.wx)
+        np.testing.assert_array_equal(lb.weights.wy, lo.wy)
+
+
+# ---------------------------------------------------------------- smoother --
+
+SWEEP_CASES = [
+    # w, h, density, seed, block, overlap  (80x56 clamps the last block on both axes)
+    (80, 56, 0.15, 8, 32, 6),
+    (80, 56, 0.15, 8, 16, 2),
+    (96, 64, 0.05, 2, 8, 2),
+    (100, 70, 0.10, 5, 24, 4),     # generic kernel (24x24 blocks)
+    (40, 20, 0.20, 1, 32, 6),      # block clipped to the image height (32x20)
+    (256, 256, 0.05, 0, 16, 2),
+    (300, 200, 0.02, 4, 32, 6),
+]
+
+
+@pytest.mark.parametrize("case", SWEEP_CASES)
+@pytest.mark.parametrize("path", [0, 1])
+def test_oras_sweeps_match_oracle(case, path):
+    w, h, dens, seed, bs, ov = case
+    m, k = oracle.seeded_problem(w, h, dens, seed)
+    b = np.where(m, k[0], 0.0)
+    part = bp.build_partition(w, h, bs, ov)
+    blocks = bp.BlockSolver(m, 1.0, part, bp.build_weights(part), 0.5)
+    for sweeps in (1, 2, 4):
+        u_o = b.copy()
+        s_o, rn_o = oracle.oras_sweeps(m, 1.0, bs, ov, 0.5, b, u_o, max_sweeps=sweeps)
+        u_g = b.copy()
+        s_g, rn_g = bp.oras_sweeps(bp.StencilOperator(m), blocks, b, u_g, max_sweeps=sweeps,
+                                   stop_norm=0.0, eta=1e-5, local_max_iters=None, path=path)
+        assert s_g == s_o
+        assert rn_g == pytest.approx(rn_o, rel=1e-9)
+        np.testing.assert_allclose(u_g, u_o, rtol=0, atol=1e-9)
+
+
+def test_oras_sweeps_general_start_and_stop_norm(rng):
+    """u violating the interpolation condition (v0 != 0 path) and a stop_norm exit."""
+    w, h, bs, ov = 90, 70, 16, 2
+    m, k = oracle.seeded_problem(w, h, 0.1, 11)
+    b = rng.normal(size=(h, w)) * 10
+    u0 = rng.normal(size=(h, w)) * 10
+    part = bp.build_partition(w, h, bs, ov)
+    blocks = bp.BlockSolver(m, 2.0, part, bp.build_weights(part), 1.5)
+    for path in (0, 1):
+        u_o, u_g = u0.copy(), u0.copy()
+        s_o, rn_o = oracle.oras_sweeps(m, 2.0, bs, ov, 1.5, b, u_o, max_sweeps=50, stop_norm=1e-3, eta=1e-4)
+        s_g, rn_g = bp.oras_sweeps(bp.StencilOperator(m, 2.0), blocks, b, u_g, max_sweeps=50,
+                                   stop_norm=1e-3, eta=1e-4, local_max_iters=None, path=path)
+        assert s_g == s_o and 0 < s_o < 50
+        assert rn_g == pytest.approx(rn_o, rel=1e-7)
+        np.testing.assert_allclose(u_g, u_o, rtol=0, atol=1e-8)
+
+
+def test_oras_zero_residual_exit():
+    """rs == 0 exits without sweeps or NaNs (solvers.py:420; all-mask coarse levels)."""
+    m = np.ones((40, 40), bool)
+    b = np.arange(1600, dtype=float).reshape(40, 40)
+    part = bp.build_partition(40, 40, 16, 2)
+    blocks = bp.BlockSolver(m, 1.0, part, bp.build_weights(part), 0.5)
+    u = b.copy()
+    s, rn = bp.oras_sweeps(bp.StencilOperator(m), blocks, b, u, max_sweeps=3, stop_norm=0.0, eta=1e-5,
+                           local_max_iters=None)
+    assert (s, rn) == (0, 0.0)
+    np.testing.assert_array_equal(u, b)
+
+
+@pytest.mark.parametrize("case", SWEEP_CASES[:5])
+def test_solve_blocks_match_oracle(case, rng):
+    """BlockSolver.solve_blocks (tests/test_solvers.py:156-169 of the reference)."""
+    w, h, dens, seed, bs, ov = case
+    m, _ = oracle.seeded_problem(w, h, dens, seed)
+    r = rng.normal(size=(h, w))
+    part = bp.build_partition(w, h, bs, ov)
+    blocks = bp.BlockSolver(m, 1.0, part, bp.build_weights(part), 0.5)
+    tgt = 1e-6 * float(np.vdot(r, r))
+    v_g = blocks.solve_blocks(r, tgt, 4 * part.block_w * part.block_h)
+    v_o = oracle.solve_blocks(m, 1.0, bs, ov, 0.5, r, tgt, 4 * part.block_w * part.block_h)
+    np.testing.assert_allclose(v_g, v_o, rtol=0, atol=1e-10)
+
+
+# ------------------------------------------------------------- cycle pieces -
+
+@pytest.mark.parametrize("w,h,bs,ov", [(256, 256, 16, 2), (200, 120, 32, 6), (30, 20, 32, 6)])
+def test_cascadic_init(w, h, bs, ov):
+    m, k = oracle.seeded_problem(w, h, 0.05, 7, channels=2)
+    ho = oracle.build_hierarchy(m, k, 1.0, oracle.MultigridConfig(block_size=bs, overlap=ov))
+    hb = bp.build_hierarchy(bp.InpaintingProblem(m, k), bp.MultigridConfig(block_size=bs, overlap=ov))
+    for c in (0, 1):
+        np.testing.assert_allclose(bp.cascadic_init(hb, channel=c), oracle.cascadic_init(ho, channel=c),
+                                   rtol=0, atol=1e-7)
+
+
+@pytest.mark.parametrize("w,h,bs,ov", [(256, 256, 16, 2), (200, 120, 32, 6), (30, 20, 32, 6)])
+def test_v_cycle(w, h, bs, ov, rng):
+    m, k = oracle.seeded_problem(w, h, 0.05, 9)
+    ho = oracle.build_hierarchy(m, k, 1.0, oracle.MultigridConfig(block_size=bs, overlap=ov))
+    hb = bp.build_hierarchy(bp.InpaintingProblem(m, k), bp.MultigridConfig(block_size=bs, overlap=ov))
+    b = np.where(m, k[0], 0.0)
+    u_o, u_g = b.copy(), b.copy()
+    fu_o = oracle.v_cycle(ho, 0, u_o, b)
+    cnt = {"fine_units": 0}
+    bp.v_cycle(hb, 0, u_g, b, counters=cnt)
+    assert cnt["fine_units"] == fu_o
+    np.testing.assert_allclose(u_g, u_o, rtol=0, atol=1e-7)
+    if len(hb) > 2:
+        lev = ho.levels[1]
+        rb = np.where(lev.mask, 0.0, rng.normal(size=lev.shape))
+        e_o, e_g = np.zeros(lev.shape), np.zeros(lev.shape)
+        oracle.v_cycle(ho, 1, e_o, rb)
+        bp.v_cycle(hb, 1, e_g, rb)
+        np.testing.assert_allclose(e_g, e_o, rtol=0, atol=1e-8)

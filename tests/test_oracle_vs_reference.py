@@ -1,0 +1,167 @@
+"""Pins the CPU oracle against the LIVE reference package (only where
+/root/reference is mounted, i.e. in the build container): every restated
+function on the reference's own test inputs (tests/conftest.py:7-12 recipe)."""
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.reference
+
+
+def _problem(dp, w, h, density, seed, channels=1):
+    mask = dp.random_mask(w, h, density, seed)
+    known = np.stack([dp.synthetic_image(w, h, seed + 1000 + c) for c in range(channels)])
+    return dp.InpaintingProblem(mask, known)
+
+
+def test_input_generators_are_bit_identical(diffpaint):
+    for w, h, d, s in [(64, 48, 0.1, 0), (256, 256, 0.05, 0), (97, 131, 0.03, 2)]:
+        m, k = oracle.seeded_problem(w, h, d, s, channels=2)
+        p = _problem(diffpaint, w, h, d, s, 2)
+        assert np.array_equal(m, p.mask) and np.array_equal(k, p.known)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_stencil(diffpaint, seed):
+    rng = np.random.default_rng(seed)
+    shape = [(5, 5), (1, 7), (9, 1), (16, 23), (40, 31), (2, 2)][seed]
+    m = rng.random(shape) < 0.3
+    u = rng.normal(size=shape)
+    b = rng.normal(size=shape)
+    for spacing in (1.0, 2.0, 0.25):
+        op = diffpaint.StencilOperator(m, spacing)
+        assert np.array_equal(oracle.apply_operator(m, spacing, u), op.apply(u))
+        assert np.array_equal(oracle.residual(m, spacing, b, u), op.residual(b, u))
+
+
+@pytest.mark.parametrize("dim", [1, 5, 16, 17, 31, 32, 33, 58, 64, 80, 135, 240, 1080, 3840])
+@pytest.mark.parametrize("bs,ov", [(32, 6), (16, 2), (8, 0), (24, 4), (32, 16), (10, 9)])
+def test_partition_weights(diffpaint, dim, bs, ov):
+    pr = diffpaint.build_partition(dim, max(1, dim // 2), bs, ov)
+    po = oracle.build_partition(dim, max(1, dim // 2), bs, ov)
+    assert np.array_equal(po.xs, pr.xs) and np.array_equal(po.ys, pr.ys)
+    assert (po.block_w, po.block_h) == (pr.block_w, pr.block_h)
+    if ov != 1:
+        wr = diffpaint.build_weights(pr)
+        wx, wy = oracle.build_weights(po)
+        assert np.array_equal(wx, wr.wx) and np.array_equal(wy, wr.wy)
+
+
+@pytest.mark.parametrize("shape", [(8, 8), (7, 9), (8, 5), (1, 1), (135, 240), (2, 3)])
+@pytest.mark.parametrize("density", [0.05, 0.4, 1.0])
+def test_transfers(diffpaint, shape, density):
+    from diffpaint import multigrid as mg
+    rng = np.random.default_rng(shape[0] * 31 + shape[1])
+    m = rng.random(shape) < density
+    m.flat[0] = True
+    rhs = np.where(m, np.round(rng.uniform(0, 255, size=shape)), 0.0)
+    cm = mg.downsample_mask(m)
+    assert np.array_equal(oracle.downsample_mask(m), cm)
+    assert np.array_equal(oracle.downsample_values_modified(m, cm, rhs), mg.downsample_values_modified(m, cm, rhs))
+    assert np.array_equal(oracle.downsample_values_naive(m, rhs), mg.downsample_values_naive(m, rhs))
+    r = rng.normal(size=shape)
+    assert np.array_equal(oracle.restrict_residual(r, cm), mg.restrict_residual(r, cm))
+    ce = rng.normal(size=cm.shape)
+    assert np.array_equal(oracle.prolongate_correction(ce, m), mg.prolongate_correction(ce, m))
+    assert np.array_equal(oracle.prolongate_solution(ce, m, rhs), mg.prolongate_solution(ce, m, rhs))
+
+
+@pytest.mark.parametrize("w,h,bs,ov,alpha,spacing", [
+    (80, 56, 32, 6, 0.5, 1.0), (80, 56, 16, 2, 0.5, 1.0), (64, 64, 32, 6, 2.0, 2.0), (50, 37, 12, 3, 0.1, 0.5),
+])
+def test_block_solver_and_sweeps(diffpaint, w, h, bs, ov, alpha, spacing):
+    from diffpaint import solvers as sv
+    p = _problem(diffpaint, w, h, 0.15, 8)
+    prob = diffpaint.InpaintingProblem(p.mask, p.known, spacing)
+    part = diffpaint.build_partition(w, h, bs, ov)
+    wts = diffpaint.build_weights(part)
+    blocks = sv.BlockSolver(prob.mask, spacing, part, wts, alpha)
+    rng = np.random.default_rng(3)
+    r = rng.normal(size=(h, w))
+    cap = 4 * part.block_w * part.block_h
+    tgt = 1e-6 * float(np.vdot(r, r))
+    v_ref = blocks.solve_blocks(blocks.gather(r), tgt, cap)
+    v_orc = oracle.solve_blocks(prob.mask, spacing, bs, ov, alpha, r, tgt, cap)
+    np.testing.assert_allclose(v_orc, v_ref, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(oracle.scatter_weighted((h, w), bs, ov, v_ref), blocks.scatter_weighted(v_ref),
+                               rtol=0, atol=1e-13)
+    b = prob.rhs(0)
+    for sweeps in (1, 3):
+        u_r, u_o = b.copy(), b.copy()
+        s_r, rn_r = sv.oras_sweeps(prob.operator(), blocks, b, u_r, max_sweeps=sweeps, stop_norm=0.0,
+                                   eta=1e-5, local_max_iters=cap)
+        s_o, rn_o = oracle.oras_sweeps(prob.mask, spacing, bs, ov, alpha, b, u_o, max_sweeps=sweeps)
+        assert s_o == s_r
+        assert rn_o == pytest.approx(rn_r, rel=1e-10)
+        np.testing.assert_allclose(u_o, u_r, rtol=0, atol=1e-10)
+    # stop_norm exit
+    u_r, u_o = b.copy(), b.copy()
+    base = float(np.linalg.norm(prob.operator().residual(b, b)))
+    s_r, _ = sv.oras_sweeps(prob.operator(), blocks, b, u_r, max_sweeps=200, stop_norm=1e-4 * base, eta=1e-5,
+                            local_max_iters=cap)
+    s_o, _ = oracle.oras_sweeps(prob.mask, spacing, bs, ov, alpha, b, u_o, max_sweeps=200, stop_norm=1e-4 * base)
+    assert s_o == s_r and 0 < s_r < 200
+
+
+@pytest.mark.parametrize("w,h,dens,seed,ch,mkw,skw", [
+    (256, 256, 0.05, 0, 1, dict(block_size=16, overlap=2), dict()),
+    (64, 64, 0.10, 1, 1, dict(block_size=16, overlap=2), dict(tol_rel=1e-8)),
+    (97, 131, 0.03, 2, 2, dict(block_size=16, overlap=2), dict()),
+    (20, 30, 0.2, 3, 1, dict(block_size=32, overlap=6), dict(tol_rel=1e-6)),
+    (256, 64, 0.05, 4, 1, dict(block_size=32, overlap=6), dict()),
+    (128, 128, 0.05, 6, 1, dict(block_size=16, overlap=2, nu_pre=2, nu_post=0), dict()),
+    (128, 128, 0.05, 6, 1, dict(block_size=16, overlap=2, value_downsampling="naive"), dict(alpha=2.0)),
+    (128, 128, 0.05, 6, 1, dict(block_size=16, overlap=2, v_cycles_max=1), dict(tol_rel=1e-9)),
+    (300, 300, 0.9, 7, 1, dict(block_size=32, overlap=6), dict()),
+    (160, 120, 0.05, 9, 1, dict(block_size=32, overlap=6, mode="multilevel"), dict()),
+])
+def test_hierarchy_cascade_vcycle_fmg(diffpaint, w, h, dens, seed, ch, mkw, skw):
+    p = _problem(diffpaint, w, h, dens, seed, ch)
+    cfg_r = diffpaint.MultigridConfig(solver=diffpaint.SolverConfig(**skw), **mkw)
+    cfg_o = oracle.MultigridConfig(solver=oracle.SolverConfig(**skw), **mkw)
+    hr = diffpaint.build_hierarchy(p, cfg_r)
+    ho = oracle.build_hierarchy(p.mask, p.known, 1.0, cfg_o)
+    assert len(ho) == len(hr)
+    for lo, lr in zip(ho.levels, hr.levels):
+        assert lo.shape == lr.shape and lo.spacing == lr.spacing
+        assert np.array_equal(lo.mask, lr.mask) and np.array_equal(lo.rhs, lr.rhs)
+    if mkw.get("mode") != "multilevel":
+        np.testing.assert_allclose(oracle.cascadic_init(ho, cfg_o, 0), diffpaint.cascadic_init(hr, cfg_r, 0),
+                                   rtol=0, atol=1e-8)
+        b = p.rhs(0)
+        u_r, u_o = b.copy(), b.copy()
+        cnt = {"fine_units": 0}
+        diffpaint.v_cycle(hr, 0, u_r, b, cfg_r, cnt)
+        fu = oracle.v_cycle(ho, 0, u_o, b, cfg_o)
+        assert fu == cnt["fine_units"]
+        np.testing.assert_allclose(u_o, u_r, rtol=0, atol=1e-8)
+    name = "ml-oras" if mkw.get("mode") == "multilevel" else "mg-oras"
+    res = diffpaint.solve_image(p, name, cfg_r)
+    out, reps = oracle.solve_image(p.mask, p.known, 1.0, cfg_o)
+    for ro, rr in zip(reps, res.reports):
+        assert ro.iterations == rr.iterations
+        assert ro.fine_smoother_iterations == rr.fine_smoother_iterations
+        assert ro.converged == rr.converged
+        floor = 1e-6 * cfg_r.solver.tol_rel
+        assert ro.final_rel_residual == pytest.approx(rr.final_rel_residual, rel=1e-6, abs=floor)
+        assert ro.baseline_residual == pytest.approx(rr.baseline_residual, rel=1e-12)
+        np.testing.assert_allclose(ro.history, rr.history, rtol=1e-6, atol=floor)
+    assert np.abs(out - res.fields).max() <= 1e-7
+
+
+def test_empty_mask_error(diffpaint):
+    with pytest.raises(ValueError):
+        oracle.solve_image(np.zeros((16, 16), bool), np.zeros((16, 16)))
+
+
+def test_oracle_vs_dense_lu(diffpaint):
+    """tests/test_multigrid.py:328-334 of the reference: mg-oras at tol 1e-8 vs the dense LU truth."""
+    from diffpaint import oracle as dense
+    p = _problem(diffpaint, 64, 64, 0.10, 1)
+    truth = dense.solve(p, 0)
+    out, _ = oracle.solve_image(p.mask, p.known, 1.0,
+                                oracle.MultigridConfig(block_size=16, overlap=2,
+                                                       solver=oracle.SolverConfig(tol_rel=1e-8)))
+    assert float(np.mean((out[0] - truth) ** 2)) <= 1e-10
