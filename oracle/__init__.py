@@ -463,44 +463,41 @@ def counters():
 
 
 # ------------------------------------------------ synthetic inputs (masks.py)
+# The reference's benchmark recipe (masks.py:13-25, :50-67; tests/conftest.py:7-12)
+# restated with the same Generator calls, hence the same bits (pinned by
+# tests/test_oracle_vs_reference.py::test_input_generators_are_bit_identical).
 
 def random_mask(width, height, density, seed=0):
-    """masks.py:13-25 -- same NumPy Generator calls, hence the same bits."""
     if not 0.0 < density <= 1.0:
         raise ValueError(f"density must be in (0, 1], got {density}")
-    n = width * height
-    count = int(round(density * n))
-    if count < 1:
+    total = width * height
+    wanted = int(round(density * total))
+    if wanted < 1:
         raise ValueError("density selects zero pixels")
-    rng = np.random.default_rng(seed)
-    picks = rng.choice(n, size=count, replace=False)
-    mask = np.zeros(n, dtype=bool)
-    mask[picks] = True
-    return mask.reshape(height, width)
+    chosen = np.random.default_rng(seed).choice(total, size=wanted, replace=False)
+    flat = np.zeros(total, dtype=bool)
+    flat[chosen] = True
+    return flat.reshape(height, width)
+
+
+def _lattice_axis(n_nodes, n_px):
+    pos = np.linspace(0.0, n_nodes - 1.0, n_px)
+    cell = np.clip(pos.astype(int), 0, n_nodes - 2)
+    return cell, pos - cell
 
 
 def synthetic_image(width, height, seed=0):
-    """masks.py:50-67 -- bilinearly upsampled U(0,255) nodes, rounded."""
-    rng = np.random.default_rng(seed)
-    nodes_x = max(2, width // 24 + 2)
-    nodes_y = max(2, height // 24 + 2)
-    coarse = rng.uniform(0.0, 255.0, size=(nodes_y, nodes_x))
-    ys = np.linspace(0.0, nodes_y - 1.0, height)
-    xs = np.linspace(0.0, nodes_x - 1.0, width)
-    y0 = np.clip(ys.astype(int), 0, nodes_y - 2)
-    x0 = np.clip(xs.astype(int), 0, nodes_x - 2)
-    ty = (ys - y0)[:, None]
-    tx = (xs - x0)[None, :]
-    a = coarse[y0[:, None], x0[None, :]]
-    b = coarse[y0[:, None], x0[None, :] + 1]
-    c = coarse[y0[:, None] + 1, x0[None, :]]
-    d = coarse[y0[:, None] + 1, x0[None, :] + 1]
-    img = (1 - ty) * ((1 - tx) * a + tx * b) + ty * ((1 - tx) * c + tx * d)
-    return np.round(img).astype(np.float64)
+    gx, gy = max(2, width // 24 + 2), max(2, height // 24 + 2)
+    nodes = np.random.default_rng(seed).uniform(0.0, 255.0, size=(gy, gx))
+    cy, fy = _lattice_axis(gy, height)
+    cx, fx = _lattice_axis(gx, width)
+    hi = nodes[cy][:, cx] * (1 - fx) + nodes[cy][:, cx + 1] * fx
+    lo = nodes[cy + 1][:, cx] * (1 - fx) + nodes[cy + 1][:, cx + 1] * fx
+    return np.rint(hi * (1 - fy)[:, None] + lo * fy[:, None]).astype(np.float64)
 
 
 def seeded_problem(width, height, density, seed, channels=1):
-    """tests/conftest.py:7-12 of the reference: (mask, known (C,h,w))."""
+    """(mask, known (C,h,w)) of the reference's tests/conftest.py:7-12 recipe."""
     mask = random_mask(width, height, density, seed)
     known = np.stack([synthetic_image(width, height, seed + 1000 + c) for c in range(channels)])
     return mask, known

@@ -1,0 +1,58 @@
+"""Synthetic benchmark inputs (host side, NumPy): the seeded random mask and
+the smooth test image of the reference's benchmark recipe (masks.py:13-25,
+:50-67; tests/conftest.py:7-12), drawn with the same Generator calls so that
+the CPU baseline and the CUDA path see identical bits.  Not on the hot path."""
+
+from __future__ import annotations
+
+import numpy as np
+
+NODE_PITCH = 24  # one random node every ~24 pixels
+
+
+def random_mask(width: int, height: int, density: float, seed: int = 0) -> np.ndarray:
+    """Exactly round(density * W * H) known pixels, drawn without replacement."""
+    if not 0.0 < density <= 1.0:
+        raise ValueError(f"density must be in (0, 1], got {density}")
+    total = width * height
+    wanted = int(round(density * total))
+    if wanted < 1:
+        raise ValueError(f"density {density} selects zero pixels on {width}x{height}")
+    flat = np.zeros(total, dtype=bool)
+    flat[np.random.default_rng(seed).choice(total, size=wanted, replace=False)] = True
+    return flat.reshape(height, width)
+
+
+def _axis_cells(n_nodes: int, n_px: int):
+    """Node cell index and fractional offset of every pixel along one axis."""
+    pos = np.linspace(0.0, n_nodes - 1.0, n_px)
+    cell = np.clip(pos.astype(int), 0, n_nodes - 2)
+    return cell, pos - cell
+
+
+def synthetic_image(width: int, height: int, seed: int = 0) -> np.ndarray:
+    """U(0,255) nodes on a coarse lattice, bilinearly upsampled, rounded to integers."""
+    gx = max(2, width // NODE_PITCH + 2)
+    gy = max(2, height // NODE_PITCH + 2)
+    nodes = np.random.default_rng(seed).uniform(0.0, 255.0, size=(gy, gx))
+    cy, fy = _axis_cells(gy, height)
+    cx, fx = _axis_cells(gx, width)
+    upper, lower = nodes[cy], nodes[cy + 1]
+    row_hi = upper[:, cx] * (1 - fx) + upper[:, cx + 1] * fx
+    row_lo = lower[:, cx] * (1 - fx) + lower[:, cx + 1] * fx
+    return np.rint(row_hi * (1 - fy)[:, None] + row_lo * fy[:, None]).astype(np.float64)
+
+
+def seeded_problem(width: int, height: int, density: float, seed: int, channels: int = 1):
+    """(mask (H,W) bool, known (C,H,W) float64): mask seed `seed`, channel c image seed+1000+c."""
+    mask = random_mask(width, height, density, seed)
+    known = np.stack([synthetic_image(width, height, seed + 1000 + c) for c in range(channels)])
+    return mask, known
+
+
+def seeded_frames(width: int, height: int, density: float, frames: int, channels: int = 3,
+                  first_seed: int = 0):
+    """Batch of independent frames: frame f uses seed first_seed + f."""
+    ms, ks = zip(*(seeded_problem(width, height, density, first_seed + f, channels)
+                   for f in range(frames)))
+    return np.stack(ms), np.stack(ks)
