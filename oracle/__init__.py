@@ -493,7 +493,7 @@ def synthetic_image(width, height, seed=0):
     cx, fx = _lattice_axis(gx, width)
     hi = nodes[cy][:, cx] * (1 - fx) + nodes[cy][:, cx + 1] * fx
     lo = nodes[cy + 1][:, cx] * (1 - fx) + nodes[cy + 1][:, cx + 1] * fx
-    return np.rint(hi * (1 - fy)[:, None] + lo * fy[:, None]).astype(np.float64)
+    return np.ascontiguousarray(np.rint(hi * (1 - fy)[:, None] + lo * fy[:, None]), dtype=np.float64)
 
 
 def seeded_problem(width, height, density, seed, channels=1):

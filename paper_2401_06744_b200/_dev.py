@@ -58,3 +58,15 @@ def empty_u8(shape) -> torch.Tensor:
 def to_host(t: torch.Tensor) -> np.ndarray:
     torch.cuda.current_stream().synchronize()
     return t.cpu().numpy()
+
+
+def check_tensor(t, name: str, dtype: str, numel: int):
+    """Device buffers cross the C-ABI as raw pointers: insist on the exact layout."""
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != getattr(torch, dtype):
+        raise ValueError(f"{name} must have dtype {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be C-contiguous (row-major), got strides {tuple(t.stride())}")
+    if t.numel() != numel:
+        raise ValueError(f"{name} has {t.numel()} elements, expected {numel}")

@@ -145,6 +145,10 @@ class Plan:
         """Device-resident solve: mask (F,H,W) uint8, known (F,C,H,W) float64 CUDA tensors."""
         if d_out is None:
             d_out = _dev.empty_f64((self.frames, self.channels, self.height, self.width))
+        n = self.height * self.width
+        _dev.check_tensor(d_mask, "mask", "uint8", self.frames * n)
+        _dev.check_tensor(d_known, "known", "float64", self.problems * n)
+        _dev.check_tensor(d_out, "out", "float64", self.problems * n)
         raw = (_lib.Report * self.problems)() if want_reports else None
         t0 = time.perf_counter()
         _dev.call("b200p_solve", self.handle, _dev.ptr(d_mask), _dev.ptr(d_known), _dev.ptr(d_out),

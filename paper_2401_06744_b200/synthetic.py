@@ -40,7 +40,8 @@ def synthetic_image(width: int, height: int, seed: int = 0) -> np.ndarray:
     upper, lower = nodes[cy], nodes[cy + 1]
     row_hi = upper[:, cx] * (1 - fx) + upper[:, cx + 1] * fx
     row_lo = lower[:, cx] * (1 - fx) + lower[:, cx + 1] * fx
-    return np.rint(row_hi * (1 - fy)[:, None] + row_lo * fy[:, None]).astype(np.float64)
+    img = np.rint(row_hi * (1 - fy)[:, None] + row_lo * fy[:, None])
+    return np.ascontiguousarray(img, dtype=np.float64)  # fancy indexing above yields F-ordered data
 
 
 def seeded_problem(width: int, height: int, density: float, seed: int, channels: int = 1):
