@@ -172,8 +172,10 @@ int b200p_plan_vcycle(b200p_plan *plan, int level, double *d_u, const double *d_
 /* oras_sweeps(op, blocks, b, u, max_sweeps=, stop_norm=, eta=, local_max_iters=)
  * (solvers.py:393-424) on level `level` of the plan (after build_hierarchy for
  * the masks), d_u/d_b (frames*C planes).  Per problem: sweeps done and final
- * residual norm (host arrays, frames*C).  path: 0 auto, 1 force the generic
- * kernel, 2 force the warp-tile kernel (error if the level is ineligible). */
+ * residual norm (host arrays, frames*C).  path: 0 plan default (fused sweep
+ * where the level is eligible), 1 generic shared-memory kernel + combine,
+ * 2 register-tile kernel + combine, 3 fused persistent sweep, 10+t tile
+ * variant t (split); an ineligible level gives B200P_ERR_UNSUPPORTED. */
 int b200p_plan_oras_sweeps(b200p_plan *plan, int level, const double *d_b, double *d_u,
                            int max_sweeps, double stop_norm, int path, int *h_sweeps,
                            double *h_rn, void *stream);

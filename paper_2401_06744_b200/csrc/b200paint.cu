@@ -131,7 +131,8 @@ static int level_shapes(int width, int height, double spacing, int block, int ov
 // --------------------------------------------------------------- plan ------
 enum KernelKind {
     KK_NORM = 0,      // K1
-    KK_SWEEP,         // K2 / K2g
+    KK_SWEEP,         // K2F fused sweep
+    KK_SWEEP_SPLIT,   // K2 / K2g (split path)
     KK_COMBINE,       // K2b
     KK_RESTRICT,      // K3
     KK_PROLONG_CORR,  // K4
@@ -145,7 +146,7 @@ enum KernelKind {
 };
 
 static const char *const kKindNames[KK_COUNT] = {
-    "residual_sqnorm", "oras_sweep", "oras_combine", "residual_restrict", "prolongate_correct",
+    "residual_sqnorm", "oras_sweep", "oras_sweep_split", "oras_combine", "residual_restrict", "prolongate_correct",
     "prolongate_solution", "downsample_mask", "downsample_values", "coarse_solve", "control",
     "convert_u8"};
 
@@ -158,6 +159,17 @@ struct LevelHost {
     double *d_u = nullptr;      // (P,h,w) cascade iterate / V-cycle correction (levels >= 1)
     double *d_rc = nullptr;     // (P,h,w) restricted residual (levels >= 1)
     int tile = 0;               // K2 variant: 0 generic, else see launch_sweep
+    // fused sweep (K2F): ping-pong partner of the iterate, L2-resident ring, schedule tables
+    bool fused = false;
+    double *d_u_alt = nullptr;  // (P,h,w)
+    double *d_ring = nullptr;   // (R, nx, bh*bw)
+    int R = 0, lag = 0, nsx = 0, nc = 0, cw = 0, fused_grid = 0;
+    const int *d_band_first_row = nullptr, *d_row_last_band = nullptr;
+};
+
+// current iterate of a level + its ping-pong partner (fused sweeps swap them)
+struct UBuf {
+    double *cur, *alt;
 };
 
 struct ProfEvent {
@@ -192,6 +204,8 @@ struct b200p_plan {
     int *d_active = nullptr, *d_cycles = nullptr, *d_units = nullptr, *d_histlen = nullptr;
     int *d_any = nullptr;
     double *d_baseline = nullptr, *d_denom = nullptr, *d_rel = nullptr, *d_hist = nullptr;
+    unsigned *d_sched = nullptr;  // K2F counters: [work | row_done P*ny | band_done P*ny]
+    size_t sched_words = 0;
     int *d_gate = nullptr, *d_sweeps = nullptr;  // stage API (oras_sweeps with stop_norm)
     double *d_rn = nullptr;
     int *h_any = nullptr;  // pinned
@@ -387,10 +401,14 @@ static void launch_tile(const SweepArgs &A, bool rm, dim3 grid, cudaStream_t st)
     else oras_sweep_tile_kernel<TW, TH, NWARP, false><<<grid, NWARP * 32, 0, st>>>(A);
 }
 
-// K2 + K2b: one ORAS sweep using rs/mflag from the preceding K1.
-static int launch_sweep(b200p_plan *pl, const LevelHost &L, double *u, const double *b, bool rm,
-                        const int *pred, int *unit_counter, int force_tile, cudaStream_t st) {
-    SweepArgs A;
+template <int TW, int TH, int NWARP>
+static void launch_fused(const FusedArgs &A, bool rm, int grid, cudaStream_t st) {
+    if (rm) oras_fused_sweep_kernel<TW, TH, NWARP, true><<<grid, FUSED_THREADS, 0, st>>>(A);
+    else oras_fused_sweep_kernel<TW, TH, NWARP, false><<<grid, FUSED_THREADS, 0, st>>>(A);
+}
+
+static void fill_sweep_args(b200p_plan *pl, const LevelHost &L, const double *u, const double *b,
+                            const int *pred, SweepArgs &A) {
     A.L = L.dev;
     A.u = u;
     A.b = b;
@@ -403,11 +421,54 @@ static int launch_sweep(b200p_plan *pl, const LevelHost &L, double *u, const dou
     A.eta = pl->cfg.eta;
     A.max_iters = local_cap(pl, L);
     A.scratch = pl->d_scratch;
-    const int tile = force_tile >= 0 ? force_tile : L.tile;
+}
+
+// K2F: fused solve + combine, u.cur -> u.alt, then swap.
+static int launch_sweep_fused(b200p_plan *pl, const LevelHost &L, UBuf &u, const double *b, bool rm,
+                              const int *pred, int *unit_counter, cudaStream_t st) {
+    FusedArgs A;
+    fill_sweep_args(pl, L, u.cur, b, pred, A.S);
+    A.S.scratch = L.d_ring;
+    A.u_new = u.alt;
+    A.R = L.R;
+    A.lag = L.lag;
+    A.nsx = L.nsx;
+    A.nc = L.nc;
+    A.cw = L.cw;
+    A.P = pl->P;
+    A.items_per_problem = L.info.ny * (L.nsx + L.nc);
+    const size_t rows = (size_t)pl->P * L.info.ny;
+    A.work = pl->d_sched;
+    A.row_done = pl->d_sched + 1;
+    A.band_done = pl->d_sched + 1 + rows;
+    A.band_first_row = L.d_band_first_row;
+    A.row_last_band = L.d_row_last_band;
+    A.unit_counter = unit_counter;
+    CU(cudaMemsetAsync(pl->d_sched, 0, sizeof(unsigned) * (1 + 2 * rows), st));
+    const long long total = (long long)pl->P * A.items_per_problem;
+    const int grid = (int)std::min<long long>(total, L.fused_grid);
+    // sweep = read u_old (+ b) + mask, write u_new; the corrections stay in L2
+    LaunchScope sc(pl, st, KK_SWEEP, field_bytes(pl, L, rm ? 2.0 : 3.0, 1.0));
+    switch (L.tile) {
+        case TILE_32_A: launch_fused<4, 2, 4>(A, rm, grid, st); break;
+        case TILE_32_B: launch_fused<4, 4, 2>(A, rm, grid, st); break;
+        case TILE_16: launch_fused<2, 4, 1>(A, rm, grid, st); break;
+        default: return fail_arg(B200P_ERR_STATE, "level is not eligible for the fused sweep");
+    }
+    CU(cudaGetLastError());
+    std::swap(u.cur, u.alt);
+    return 0;
+}
+
+// K2 + K2b: one ORAS sweep (in place on u.cur) using rs/mflag from the preceding K1.
+static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, double *u, const double *b, bool rm,
+                              const int *pred, int *unit_counter, int tile, cudaStream_t st) {
+    SweepArgs A;
+    fill_sweep_args(pl, L, u, b, pred, A);
     dim3 grid(L.nblocks, pl->P);
     {
-        // sweep = read u (+ b) + mask, write weighted corrections
-        LaunchScope sc(pl, st, KK_SWEEP, field_bytes(pl, L, rm ? 2.0 : 3.0, 1.0));
+        // read u (+ b) + mask, write the weighted correction tiles
+        LaunchScope sc(pl, st, KK_SWEEP_SPLIT, field_bytes(pl, L, rm ? 2.0 : 3.0, 1.0));
         switch (tile) {
             case TILE_32_A: launch_tile<4, 2, 4>(A, rm, grid, st); break;
             case TILE_32_B: launch_tile<4, 4, 2>(A, rm, grid, st); break;
@@ -432,14 +493,22 @@ static int launch_sweep(b200p_plan *pl, const LevelHost &L, double *u, const dou
     return 0;
 }
 
+// path: -1 plan default; 0 generic split; >0 a tile id (split); -2 fused
+static int launch_sweep(b200p_plan *pl, const LevelHost &L, UBuf &u, const double *b, bool rm,
+                        const int *pred, int *unit_counter, int path, cudaStream_t st) {
+    if ((path == -1 && L.fused) || path == -2)
+        return launch_sweep_fused(pl, L, u, b, rm, pred, unit_counter, st);
+    return launch_sweep_split(pl, L, u.cur, b, rm, pred, unit_counter, path >= 0 ? path : L.tile, st);
+}
+
 // _smooth (multigrid.py:264-279): `units` sweeps with stop_norm = 0.  When
 // have_norm is set, rs/mflag already describe (u, b) and the first K1 is skipped.
-static int enqueue_smooth(b200p_plan *pl, const LevelHost &L, double *u, const double *b, bool rm,
+static int enqueue_smooth(b200p_plan *pl, const LevelHost &L, UBuf &u, const double *b, bool rm,
                           int units, const int *pred, int *unit_counter, bool have_norm,
                           cudaStream_t st) {
     for (int i = 0; i < units; ++i) {
         if (!(have_norm && i == 0)) {
-            int rc = launch_norm(pl, L, u, b, false, rm, pred, st);
+            int rc = launch_norm(pl, L, u.cur, b, false, rm, pred, st);
             if (rc) return rc;
         }
         int rc = launch_sweep(pl, L, u, b, rm, pred, unit_counter, -1, st);
@@ -514,6 +583,23 @@ static int enqueue_hierarchy(b200p_plan *pl, cudaStream_t st) {
     return 0;
 }
 
+static UBuf level_ubuf(b200p_plan *pl, int level, double *d_u0) {
+    LevelHost &L = pl->lev[level];
+    UBuf u;
+    u.cur = level == 0 ? d_u0 : L.d_u;
+    u.alt = L.d_u_alt;
+    return u;
+}
+
+// Brings the iterate back into `home` if an odd number of fused sweeps left it in the partner.
+static int settle(b200p_plan *pl, const LevelHost &L, UBuf &u, double *home, cudaStream_t st) {
+    if (u.cur == home) return 0;
+    const size_t bytes = sizeof(double) * (size_t)pl->P * L.info.height * L.info.width;
+    CU(cudaMemcpyAsync(home, u.cur, bytes, cudaMemcpyDeviceToDevice, st));
+    std::swap(u.cur, u.alt);
+    return 0;
+}
+
 // _cascade(to_tol=False) (multigrid.py:389-422) into d_u0 (level-0 iterate).
 static int enqueue_cascade(b200p_plan *pl, double *d_u0, cudaStream_t st) {
     const int nl = (int)pl->lev.size();
@@ -527,69 +613,78 @@ static int enqueue_cascade(b200p_plan *pl, double *d_u0, cudaStream_t st) {
     int rc = launch_coarse(pl, co, co.d_u, co.d_rhs, true, 1, tol, pl->cfg.coarse_max_iters,
                            nullptr, nullptr, 0, st);
     if (rc) return rc;
+    const double *coarse_u = co.d_u;
     for (int l = nl - 2; l >= 0; --l) {
         LevelHost &f = pl->lev[l];
         const LevelHost &c = pl->lev[l + 1];
-        double *uf = l == 0 ? d_u0 : f.d_u;
+        UBuf uf = level_ubuf(pl, l, d_u0);
         {
             LaunchScope sc(pl, st, KK_PROLONG_SOL, field_bytes(pl, f, 1.25, 1.0));
             prolongate_kernel<true><<<grid2x(c.info.width, c.info.height, pl->P), ST_THREADS, 0, st>>>(
-                c.d_u, f.d_mask, f.d_rhs, f.info.height, f.info.width, pl->C, nullptr, uf);
+                coarse_u, f.d_mask, f.d_rhs, f.info.height, f.info.width, pl->C, nullptr, uf.cur);
             CU(cudaGetLastError());
         }
         if (l > 0) {
             rc = enqueue_smooth(pl, f, uf, f.d_rhs, true, 1, nullptr, nullptr, false, st);
             if (rc) return rc;
         }
+        coarse_u = uf.cur;
     }
     return 0;
 }
 
 // v_cycle (multigrid.py:335-371).  rm: b is read masked (level-0 `known` /
 // hierarchy values); have_norm: rs/mflag are current for (u, b) on entry.
-static int enqueue_vcycle(b200p_plan *pl, int level, double *u, const double *b, bool rm,
-                          const int *pred, int *unit_counter, bool have_norm, cudaStream_t st) {
+// The iterate enters and leaves in u.cur == its home buffer.
+static int enqueue_vcycle(b200p_plan *pl, int level, UBuf &u, const double *b, bool rm,
+                          const int *pred, int *unit_counter, bool have_norm, cudaStream_t st,
+                          bool settle_home = true) {
     const int nl = (int)pl->lev.size();
     LevelHost &L = pl->lev[level];
     const b200p_config &cfg = pl->cfg;
     int *uc = level == 0 ? unit_counter : nullptr;
+    double *home = u.cur;
     if (level == nl - 1) {
         // single-level cycle: nu_pre + nu_post sweeps (always a single block here)
-        return launch_coarse(pl, L, u, b, rm, 2, 0.0, cfg.nu_pre + cfg.nu_post, pred, uc, 1, st);
+        return launch_coarse(pl, L, u.cur, b, rm, 2, 0.0, cfg.nu_pre + cfg.nu_post, pred, uc, 1, st);
     }
     int rc = enqueue_smooth(pl, L, u, b, rm, cfg.nu_pre, pred, uc, have_norm, st);
     if (rc) return rc;
     LevelHost &Cc = pl->lev[level + 1];
+    UBuf e = level_ubuf(pl, level + 1, nullptr);
     {
         LaunchScope sc(pl, st, KK_RESTRICT, field_bytes(pl, L, rm ? 1.25 : 2.25, 1.25));
         dim3 g = grid2x(Cc.info.width, Cc.info.height, pl->P);
         // e is zeroed by the coarse solve (init_mode 0) on the coarsest level, else here
-        double *ez = (level + 1 == nl - 1) ? nullptr : Cc.d_u;
+        double *ez = (level + 1 == nl - 1) ? nullptr : e.cur;
         if (rm)
             residual_restrict_kernel<true><<<g, ST_THREADS, 0, st>>>(
-                u, b, L.d_mask, Cc.d_mask, L.info.height, L.info.width, L.dev.hinv2, pl->C, pred,
+                u.cur, b, L.d_mask, Cc.d_mask, L.info.height, L.info.width, L.dev.hinv2, pl->C, pred,
                 Cc.d_rc, ez);
         else
             residual_restrict_kernel<false><<<g, ST_THREADS, 0, st>>>(
-                u, b, L.d_mask, Cc.d_mask, L.info.height, L.info.width, L.dev.hinv2, pl->C, pred,
+                u.cur, b, L.d_mask, Cc.d_mask, L.info.height, L.info.width, L.dev.hinv2, pl->C, pred,
                 Cc.d_rc, ez);
         CU(cudaGetLastError());
     }
     if (level + 1 == nl - 1) {
         const double tol = std::min(cfg.coarse_tol, cfg.tol_rel);
-        rc = launch_coarse(pl, Cc, Cc.d_u, Cc.d_rc, false, 0, tol, cfg.coarse_max_iters, pred,
+        rc = launch_coarse(pl, Cc, e.cur, Cc.d_rc, false, 0, tol, cfg.coarse_max_iters, pred,
                            nullptr, 0, st);
     } else {
-        rc = enqueue_vcycle(pl, level + 1, Cc.d_u, Cc.d_rc, false, pred, nullptr, false, st);
+        rc = enqueue_vcycle(pl, level + 1, e, Cc.d_rc, false, pred, nullptr, false, st, false);
     }
     if (rc) return rc;
     {
         LaunchScope sc(pl, st, KK_PROLONG_CORR, field_bytes(pl, L, 2.25, 1.0));
         prolongate_kernel<false><<<grid2x(Cc.info.width, Cc.info.height, pl->P), ST_THREADS, 0, st>>>(
-            Cc.d_u, L.d_mask, nullptr, L.info.height, L.info.width, pl->C, pred, u);
+            e.cur, L.d_mask, nullptr, L.info.height, L.info.width, pl->C, pred, u.cur);
         CU(cudaGetLastError());
     }
-    return enqueue_smooth(pl, L, u, b, rm, cfg.nu_post, pred, uc, false, st);
+    if ((rc = enqueue_smooth(pl, L, u, b, rm, cfg.nu_post, pred, uc, false, st))) return rc;
+    // inner levels may end in the partner buffer (the caller prolongates from e.cur); the level
+    // handed in from outside must end where it started
+    return settle_home ? settle(pl, L, u, home, st) : 0;
 }
 
 // Front half of fmg_solve: hierarchy, baseline, cascade, first convergence check.
@@ -612,7 +707,8 @@ static int enqueue_front(b200p_plan *pl, double *d_out, cudaStream_t st) {
 static int enqueue_cycle(b200p_plan *pl, double *d_out, cudaStream_t st) {
     LevelHost &L0 = pl->lev[0];
     // rs/mflag are current on entry (the previous check's K1) iff nu_pre > 0 uses them first
-    int rc = enqueue_vcycle(pl, 0, d_out, L0.d_rhs, true, pl->d_active, pl->d_units,
+    UBuf u = level_ubuf(pl, 0, d_out);
+    int rc = enqueue_vcycle(pl, 0, u, L0.d_rhs, true, pl->d_active, pl->d_units,
                             (int)pl->lev.size() > 1, st);
     if (rc) return rc;
     if ((rc = launch_norm(pl, L0, d_out, L0.d_rhs, false, true, pl->d_active, st))) return rc;
@@ -838,6 +934,44 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
         PTRY(dev_upload(pl, cyn, &D.cyn));
         L.tile = tile_for(D.bw, D.bh);
         const size_t plane = (size_t)h * w;
+        {
+            const char *e = getenv("B200P_FUSED");
+            const bool want = !(e && *e == '0');
+            const int bpc = L.tile == TILE_32_A ? 1 : (L.tile == TILE_32_B ? 2 : (L.tile == TILE_16 ? 4 : 0));
+            if (want && bpc > 0 && L.nblocks > 1) {
+                L.fused = true;
+                std::vector<int> first(L.info.ny), last(L.info.ny);
+                int span = 0;
+                for (int j = 0; j < L.info.ny; ++j) {
+                    first[j] = cyf[ys[j]];
+                    const int yl = ys[j] + D.bh - 1;
+                    last[j] = cyf[yl] + cyn[yl] - 1;
+                    span = std::max(span, last[j] - j);
+                }
+                const char *le = getenv("B200P_LAG");
+                L.lag = le ? std::max(0, atoi(le)) : 4;
+                L.R = L.lag + span + 4;
+                L.nsx = (L.info.nx + bpc - 1) / bpc;
+                L.cw = FUSED_THREADS;
+                L.nc = (w + L.cw - 1) / L.cw;
+                PTRY(dev_upload(pl, first, &L.d_band_first_row));
+                PTRY(dev_upload(pl, last, &L.d_row_last_band));
+                PTRY(dev_alloc(pl, &L.d_ring, (size_t)L.R * L.info.nx * D.bw * D.bh));
+                PTRY(dev_alloc(pl, &L.d_u_alt, pl->P * plane));
+                pl->sched_words = std::max(pl->sched_words, (size_t)1 + 2 * (size_t)pl->P * L.info.ny);
+                int occ = 0, sms = 148;
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+                cudaError_t oe = cudaSuccess;
+                if (L.tile == TILE_32_A)
+                    oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, oras_fused_sweep_kernel<4, 2, 4, true>, FUSED_THREADS, 0);
+                else if (L.tile == TILE_32_B)
+                    oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, oras_fused_sweep_kernel<4, 4, 2, true>, FUSED_THREADS, 0);
+                else
+                    oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, oras_fused_sweep_kernel<2, 4, 1, true>, FUSED_THREADS, 0);
+                if (oe != cudaSuccess || occ < 1) occ = 4;
+                L.fused_grid = sms * occ;
+            }
+        }
         if (l > 0) {
             PTRY(dev_alloc(pl, &L.d_mask, pl->F * plane));
             PTRY(dev_alloc(pl, &L.d_rhs, pl->P * plane));
@@ -848,6 +982,7 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
             scratch = std::max(scratch, (size_t)pl->P * L.nblocks * D.bw * D.bh);
     }
     PTRY(dev_alloc(pl, &pl->d_scratch, scratch));
+    PTRY(dev_alloc(pl, &pl->d_sched, std::max<size_t>(pl->sched_words, 4)));
     pl->norm_ctas = std::max(1, std::min(1024, (148 * 8 + pl->P - 1) / pl->P));
     PTRY(dev_alloc(pl, &pl->d_partial, (size_t)pl->P * pl->norm_ctas));
     PTRY(dev_alloc(pl, &pl->d_partial_flag, (size_t)pl->P * pl->norm_ctas));
@@ -1098,7 +1233,10 @@ int b200p_plan_vcycle(b200p_plan *pl, int level, double *d_u, const double *d_rh
     cudaStream_t st = (cudaStream_t)stream;
     int rc = launch_set_int(pl, pl->d_units, pl->P, 0, st);
     if (rc) return rc;
-    if ((rc = enqueue_vcycle(pl, level, d_u, d_rhs, false, nullptr, pl->d_units, false, st))) return rc;
+    UBuf u;
+    u.cur = d_u;
+    u.alt = pl->lev[level].d_u_alt;
+    if ((rc = enqueue_vcycle(pl, level, u, d_rhs, false, nullptr, pl->d_units, false, st))) return rc;
     if (h_fine_units) {
         CU(cudaMemcpyAsync(h_fine_units, pl->d_units, pl->P * sizeof(int), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
@@ -1113,17 +1251,30 @@ int b200p_plan_oras_sweeps(b200p_plan *pl, int level, const double *d_b, double 
     if (level < 0 || level >= (int)pl->lev.size()) return fail_arg(B200P_ERR_ARG, "bad level %d", level);
     if (!pl->lev[level].d_mask) return fail_arg(B200P_ERR_STATE, "level mask not bound (build_hierarchy)");
     LevelHost &L = pl->lev[level];
-    int force = -1;
+    int force = -1;  // plan default
+    const bool is32 = L.info.block_w == 32 && L.info.block_h == 32;
+    const bool is16 = L.info.block_w == 16 && L.info.block_h == 16;
+    const bool is8 = L.info.block_w == 8 && L.info.block_h == 8;
     if (path == 1) force = TILE_GENERIC;
-    else if (path >= 2) {
-        const int t = path == 2 ? tile_for(L.info.block_w, L.info.block_h) : path - 2;
-        bool ok = false;
-        if (L.info.block_w == 32 && L.info.block_h == 32) ok = t == TILE_32_A || t == TILE_32_B || t == TILE_32_C;
-        if (L.info.block_w == 16 && L.info.block_h == 16) ok = t == TILE_16;
-        if (L.info.block_w == 8 && L.info.block_h == 8) ok = t == TILE_8;
-        if (!ok) return fail_arg(B200P_ERR_UNSUPPORTED, "level %d is not eligible for tile path %d", level, path);
+    else if (path == 2) {
+        force = tile_for(L.info.block_w, L.info.block_h);
+        if (force == TILE_GENERIC)
+            return fail_arg(B200P_ERR_UNSUPPORTED, "level %d has no register-tile kernel", level);
+    } else if (path == 3) {
+        if (!L.fused) return fail_arg(B200P_ERR_UNSUPPORTED, "level %d is not eligible for the fused sweep", level);
+        force = -2;
+    } else if (path >= 10) {
+        const int t = path - 10;
+        const bool ok = (is32 && (t == TILE_32_A || t == TILE_32_B || t == TILE_32_C)) ||
+                        (is16 && t == TILE_16) || (is8 && t == TILE_8);
+        if (!ok) return fail_arg(B200P_ERR_UNSUPPORTED, "level %d is not eligible for tile variant %d", level, t);
         force = t;
+    } else if (path != 0) {
+        return fail_arg(B200P_ERR_ARG, "unknown path %d", path);
     }
+    UBuf ub;
+    ub.cur = d_u;
+    ub.alt = L.d_u_alt;
     cudaStream_t st = (cudaStream_t)stream;
     int rc;
     if ((rc = launch_set_int(pl, pl->d_gate, pl->P, 1, st))) return rc;
@@ -1133,19 +1284,20 @@ int b200p_plan_oras_sweeps(b200p_plan *pl, int level, const double *d_b, double 
         const int chunk = 8;
         if ((rc = launch_set_int(pl, pl->d_any, 1, 0, st))) return rc;
         for (int k = 0; k < chunk && it <= max_sweeps; ++k, ++it) {
-            if ((rc = launch_norm(pl, L, d_u, d_b, false, false, pl->d_gate, st))) return rc;
+            if ((rc = launch_norm(pl, L, ub.cur, d_b, false, false, pl->d_gate, st))) return rc;
             {
                 LaunchScope sc(pl, st, KK_CONTROL, 0.0);
                 sweep_gate_kernel<<<(pl->P + 127) / 128, 128, 0, st>>>(
                     pl->P, pl->d_rs, stop_norm, max_sweeps, pl->d_gate, pl->d_sweeps, pl->d_rn, pl->d_any);
                 CU(cudaGetLastError());
             }
-            if ((rc = launch_sweep(pl, L, d_u, d_b, false, pl->d_gate, pl->d_sweeps, force, st))) return rc;
+            if ((rc = launch_sweep(pl, L, ub, d_b, false, pl->d_gate, pl->d_sweeps, force, st))) return rc;
         }
         CU(cudaMemcpyAsync(pl->h_any, pl->d_any, sizeof(int), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
         if (!*pl->h_any || it > max_sweeps) break;
     }
+    if ((rc = settle(pl, L, ub, d_u, st))) return rc;
     if (h_sweeps) CU(cudaMemcpyAsync(h_sweeps, pl->d_sweeps, pl->P * sizeof(int), cudaMemcpyDeviceToHost, st));
     if (h_rn) CU(cudaMemcpyAsync(h_rn, pl->d_rn, pl->P * sizeof(double), cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));

@@ -37,18 +37,20 @@ struct SweepArgs {
 };
 
 // ------------------------------------------------------------------ K2 ----
-// Block = (8*TW) x (4*TH*NWARP) pixels, handled by NWARP warps (= one CTA).
-// Lane (lx = lane&7, ly = lane>>3) of warp wg owns the TW x TH tile at
+// Block = (8*TW) x (4*TH*NWARP) pixels, handled by a group of NWARP warps.
+// Lane (lx = lane&7, ly = lane>>3) of group warp wg owns the TW x TH tile at
 // (lx*TW, (wg*4+ly)*TH).  The local operator is applied in the scaled form
 //     q' = A_i p / hinv2 = 4 p - (sum of 4 neighbours incl. ghosts),
 // where a neighbour cut off by a block side is replaced by the ghost
 // gamma * p_edge: gamma = 1 on the image border (reflecting, diag count 3) and
 // gamma = 1 - alpha*h on an inner side (Robin: diag 3 + alpha*h, solvers.py:206-216,
 // :288-297).  Mask pixels are identity rows; p and r stay exactly 0 there.
+// A CTA may hold several groups (one block each); groups synchronise on their
+// own named barrier (id 1 + group), never on the CTA barrier.
 template <int TW, int TH, int NWARP>
 struct TileCG {
     static constexpr int BW = 8 * TW, BH = 4 * TH * NWARP;
-    int lane, wg, lx, ly;
+    int lane, wg, lx, ly, bar_id;
     bool eL, eR, eT, eB;     // tile touches the block's left/right/top/bottom side
     double gL, gR, gT, gB;   // ghost factors of those sides
     unsigned mbits;          // local mask, bit j*TW+i
@@ -56,11 +58,15 @@ struct TileCG {
     double *red;             // smem: 2*NWARP doubles (two alternating slots)
     int slot;
 
+    __device__ __forceinline__ void group_bar() {
+        if (NWARP > 1) asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(NWARP * 32) : "memory");
+    }
+
     __device__ __forceinline__ double group_sum(double v) {
         v = warp_sum(v);
         if (NWARP == 1) return v;
         if (lane == 0) red[slot * NWARP + wg] = v;
-        __syncthreads();
+        group_bar();
         double t = 0.0;
 #pragma unroll
         for (int k = 0; k < NWARP; ++k) t += red[slot * NWARP + k];
@@ -68,8 +74,7 @@ struct TileCG {
         return t;
     }
 
-    // q' = 4p - neighbours (scaled local operator), 0 at mask pixels unless
-    // KEEP_MASK (then q' = p there: used for the unscaled v0 product).
+    // q' = 4p - neighbours (scaled local operator), 0 at mask pixels.
     __device__ __forceinline__ void apply(const double (&pc)[TH][TW], double (&q)[TH][TW]) {
         double hT[TW], hB[TW];
 #pragma unroll
@@ -87,7 +92,7 @@ struct TileCG {
 #pragma unroll
                 for (int i = 0; i < TW; ++i) xrow[(wg * 2 + 1) * BW + bx + i] = pc[TH - 1][i];
             }
-            __syncthreads();
+            group_bar();
             if (ly == 0 && wg > 0) {
 #pragma unroll
                 for (int i = 0; i < TW; ++i) hT[i] = xrow[((wg - 1) * 2 + 1) * BW + bx + i];
@@ -125,32 +130,36 @@ struct TileCG {
     }
 };
 
-template <int TW, int TH, int NWARP, bool RM>
-__global__ void __launch_bounds__(NWARP * 32)
-oras_sweep_tile_kernel(const SweepArgs A) {
+template <int TW, int TH, int NWARP>
+struct TileSmem {
+    double xrow[NWARP > 1 ? NWARP * 2 * 8 * TW : 1];
+    double red[2 * NWARP];
+};
+
+// One block's sweep work for the NWARP warps of group `grp`: gather the global
+// residual from u (1-pixel halo), run the local Robin CG to eta*rs, and store
+// the PoU-weighted correction (v*wy)*wx as a (BH,BW) tile at `out`
+// (solvers.py:303-305, :328-370, :309-310).  STCG: store with st.global.cg
+// (L2 only) -- used when another CTA of the same kernel reads the tile.
+template <int TW, int TH, int NWARP, bool RM, bool STCG>
+__device__ __forceinline__ void tile_block_solve(const SweepArgs &A, int p, int blk, int grp, int wg,
+                                                 TileSmem<TW, TH, NWARP> &sm, double target,
+                                                 double *__restrict__ out) {
     using CG = TileCG<TW, TH, NWARP>;
     constexpr int BW = CG::BW, BH = CG::BH;
-    __shared__ double s_xrow[NWARP > 1 ? NWARP * 2 * BW : 1];
-    __shared__ double s_red[2 * NWARP];
-
-    const int p = blockIdx.y;
-    if (A.pred && !A.pred[p]) return;
-    const double rs_g = A.rs[p];
-    if (rs_g == 0.0) return;  // oras_sweeps exit, solvers.py:420
-    const double target = A.eta * rs_g;
     const LevelDev &L = A.L;
-    const int blk = blockIdx.x;
     const int iy = blk / L.nx, ix = blk - iy * L.nx;
     const int x0 = L.xs[ix], y0 = L.ys[iy];
     const int W = L.w, H = L.h;
 
     CG cg;
     cg.lane = threadIdx.x & 31;
-    cg.wg = threadIdx.x >> 5;
+    cg.wg = wg;
+    cg.bar_id = 1 + grp;
     cg.lx = cg.lane & 7;
     cg.ly = cg.lane >> 3;
-    cg.xrow = s_xrow;
-    cg.red = s_red;
+    cg.xrow = sm.xrow;
+    cg.red = sm.red;
     cg.slot = 0;
     cg.eL = cg.lx == 0;
     cg.eR = cg.lx == 7;
@@ -275,26 +284,215 @@ oras_sweep_tile_kernel(const SweepArgs A) {
         }
     }
 
-    // ---- weighted correction (v * wy) * wx -> scratch (solvers.py:309-310)
+    // ---- weighted correction (v * wy) * wx (solvers.py:309-310)
     double wxv[TW];
 #pragma unroll
     for (int i = 0; i < TW; ++i) wxv[i] = L.wx[ix * BW + bx + i];
-    double *sp = A.scratch + ((size_t)p * L.nblocks + blk) * (BW * BH);
 #pragma unroll
     for (int j = 0; j < TH; ++j) {
         const double wyv = L.wy[iy * BH + by + j];
-        double *row = sp + (by + j) * BW + bx;
+        double *row = out + (by + j) * BW + bx;
         if (TW % 2 == 0) {
 #pragma unroll
             for (int i = 0; i < TW; i += 2) {
                 double2 o;
                 o.x = (v[j][i] * wyv) * wxv[i];
                 o.y = (v[j][i + 1] * wyv) * wxv[i + 1];
-                *reinterpret_cast<double2 *>(row + i) = o;
+                if (STCG) __stcg(reinterpret_cast<double2 *>(row + i), o);
+                else *reinterpret_cast<double2 *>(row + i) = o;
             }
         } else {
 #pragma unroll
-            for (int i = 0; i < TW; ++i) row[i] = (v[j][i] * wyv) * wxv[i];
+            for (int i = 0; i < TW; ++i) {
+                const double o = (v[j][i] * wyv) * wxv[i];
+                if (STCG) __stcg(row + i, o); else row[i] = o;
+            }
+        }
+    }
+}
+
+template <int TW, int TH, int NWARP, bool RM>
+__global__ void __launch_bounds__(NWARP * 32)
+oras_sweep_tile_kernel(const SweepArgs A) {
+    __shared__ TileSmem<TW, TH, NWARP> sm;
+    const int p = blockIdx.y;
+    if (A.pred && !A.pred[p]) return;
+    const double rs_g = A.rs[p];
+    if (rs_g == 0.0) return;  // oras_sweeps exit, solvers.py:420
+    const int blk = blockIdx.x;
+    double *out = A.scratch + ((size_t)p * A.L.nblocks + blk) * (8 * TW * 4 * TH * NWARP);
+    tile_block_solve<TW, TH, NWARP, RM, false>(A, p, blk, 0, threadIdx.x >> 5, sm, A.eta * rs_g, out);
+}
+
+// ------------------------------------------------------------------ K2F ---
+// Fused sweep: solve + deterministic combine in ONE persistent kernel.
+//
+// Work items are claimed from an atomic counter in a fixed order.  Per problem
+// the order is, block-row by block-row: the solve items of block row t, then the
+// combine items of pixel band t - lag.  Band j is the set of pixel rows whose
+// LAST covering block row is j (rows [ys[j], ys[j+1]), the last band runs to the
+// image bottom); its u_new = u_old + sum of covering blocks' weighted
+// corrections needs block rows <= j only.  Solve items write their weighted
+// correction tile into a RING of R block rows (slot = global row index mod R),
+// signal `row_done`; combine items wait for the rows they read, sum the
+// contributions in ascending block order (np.bincount order, solvers.py:310-314)
+// and write u_new.  A solve item that re-uses a ring slot first waits for the
+// bands that read the slot's previous occupant (`band_done`).  Every wait points
+// to an item EARLIER in the claim order, so the earliest unfinished item never
+// blocks: no deadlock for any number of resident CTAs.
+//
+// The ring (R * nx tiles, a few MB) stays resident in L2, so the corrections
+// never travel to HBM: the sweep's DRAM traffic is read u_old + write u_new
+// (+ mask, rhs).  u is ping-ponged (u_old -> u_new); skipped problems (frozen
+// by `pred`, or rs == 0) are copied through so that every problem's current
+// iterate lives in the same buffer.
+struct FusedArgs {
+    SweepArgs S;          // S.u = u_old, S.scratch = ring
+    double *u_new;
+    int R, lag;           // ring depth in block rows; combine lag in block rows
+    int nsx;              // solve items per block row (ceil(nx / blocks per CTA))
+    int nc, cw;           // combine chunks per band, chunk width in pixels
+    int P, items_per_problem;
+    unsigned *work;       // [1] claim counter (zeroed before launch)
+    unsigned *row_done;   // [P*ny] solve items finished per block row
+    unsigned *band_done;  // [P*ny] combine items finished per band
+    const int *band_first_row;  // [ny] first block row a band reads
+    const int *row_last_band;   // [ny] last band that reads a block row
+    int *unit_counter;    // per-problem sweep counter (may be null)
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void spin_until(const unsigned *ctr, unsigned target) {
+    while (ld_acquire_u32(ctr) < target) __nanosleep(40);
+}
+
+constexpr int FUSED_THREADS = 128;
+
+template <int TW, int TH, int NWARP, bool RM>
+__global__ void __launch_bounds__(FUSED_THREADS)
+oras_fused_sweep_kernel(const FusedArgs A) {
+    constexpr int BW = 8 * TW, BH = 4 * TH * NWARP;
+    constexpr int BPC = FUSED_THREADS / (NWARP * 32);  // blocks per solve item
+    __shared__ TileSmem<TW, TH, NWARP> sm[BPC];
+    __shared__ unsigned s_item;
+    const LevelDev &L = A.S.L;
+    const int tid = threadIdx.x;
+    const int ny = L.ny, nx = L.nx;
+    const unsigned total = (unsigned)A.P * (unsigned)A.items_per_problem;
+    const int lag = A.lag < ny ? A.lag : ny;
+    const int per_slot = A.nsx + A.nc;
+
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) s_item = atomicAdd(A.work, 1u);
+        __syncthreads();
+        const unsigned item = s_item;
+        if (item >= total) break;
+        const int p = (int)(item / (unsigned)A.items_per_problem);
+        int q = (int)(item - (unsigned)p * (unsigned)A.items_per_problem);
+        // ---- decode (see the order described above)
+        bool solve;
+        int row, sub;
+        if (q < lag * A.nsx) {
+            solve = true; row = q / A.nsx; sub = q - row * A.nsx;
+        } else {
+            q -= lag * A.nsx;
+            const int mid = (ny - lag) * per_slot;
+            if (q < mid) {
+                const int t = q / per_slot, r = q - t * per_slot;
+                if (r < A.nsx) { solve = true; row = lag + t; sub = r; }
+                else { solve = false; row = t; sub = r - A.nsx; }
+            } else {
+                q -= mid;
+                solve = false; row = (ny - lag) + q / A.nc; sub = q % A.nc;
+            }
+        }
+        const bool skip = (A.S.pred && !A.S.pred[p]) || A.S.rs[p] == 0.0;
+        const int grow = p * ny + row;  // global block row / band index
+
+        if (solve) {
+            if (!skip) {
+                // ring slot re-use: the bands that read the previous occupant must be done
+                const int old = grow - A.R;
+                if (old >= 0 && tid == 0) {
+                    const int op = old / ny, orow = old - op * ny;
+                    for (int b = orow; b <= A.row_last_band[orow]; ++b)
+                        spin_until(&A.band_done[op * ny + b], (unsigned)A.nc);
+                    __threadfence();
+                }
+                __syncthreads();
+                const int warp = tid >> 5;
+                const int grp = warp / NWARP, wg = warp - grp * NWARP;
+                const int ix = sub * BPC + grp;
+                if (ix < nx) {
+                    double *out = A.S.scratch + ((size_t)(grow % A.R) * nx + ix) * (BW * BH);
+                    tile_block_solve<TW, TH, NWARP, RM, true>(A.S, p, row * nx + ix, grp, wg, sm[grp],
+                                                              A.S.eta * A.S.rs[p], out);
+                }
+            }
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                atomicAdd(&A.row_done[grow], 1u);
+            }
+        } else {
+            // ---- combine band `row`, columns [sub*cw, sub*cw + cw)
+            const int y0 = L.ys[row];
+            const int y1 = row + 1 < ny ? L.ys[row + 1] : L.h;
+            const int x0 = sub * A.cw;
+            const int x1 = x0 + A.cw < L.w ? x0 + A.cw : L.w;
+            const double *uo = A.S.u + (size_t)p * A.S.plane;
+            double *un = A.u_new + (size_t)p * A.S.plane;
+            if (skip) {
+                for (int y = y0 + (tid / A.cw); y < y1; y += FUSED_THREADS / A.cw)
+                    for (int x = x0 + (tid % A.cw); x < x1; x += A.cw)
+                        un[(size_t)y * L.w + x] = uo[(size_t)y * L.w + x];
+            } else {
+                if (tid == 0) {
+                    for (int r = A.band_first_row[row]; r <= row; ++r)
+                        spin_until(&A.row_done[p * ny + r], (unsigned)A.nsx);
+                    __threadfence();
+                }
+                __syncthreads();
+                if (A.unit_counter && row == 0 && sub == 0 && tid == 0) A.unit_counter[p] += 1;
+                const size_t bsz = (size_t)BW * BH;
+                // thread -> one column, FUSED_THREADS / cw row phases
+                const int tx = tid % A.cw, ty = tid / A.cw;
+                const int x = x0 + tx;
+                if (x < x1) {
+                    const int ixf = L.cxf[x], ixn = L.cxn[x];
+                    const int lx0 = x - L.xs[ixf];
+                    const int lx1 = ixn > 1 ? x - L.xs[ixf + 1] : 0;
+                    const int lx2 = ixn > 2 ? x - L.xs[ixf + 2] : 0;
+                    for (int y = y0 + ty; y < y1; y += FUSED_THREADS / A.cw) {
+                        const int iyf = L.cyf[y], iyn = L.cyn[y];
+                        double acc = 0.0;
+                        for (int a = 0; a < iyn; ++a) {
+                            const int iy = iyf + a;
+                            const int ly = y - L.ys[iy];
+                            const double *tile = A.S.scratch +
+                                ((size_t)((p * ny + iy) % A.R) * nx + ixf) * bsz + (size_t)ly * BW;
+                            acc += __ldcg(tile + lx0);
+                            if (ixn > 1) acc += __ldcg(tile + bsz + lx1);
+                            if (ixn > 2) acc += __ldcg(tile + 2 * bsz + lx2);
+                            for (int c = 3; c < ixn; ++c)
+                                acc += __ldcg(tile + (size_t)c * bsz + (x - L.xs[ixf + c]));
+                        }
+                        const size_t gi = (size_t)y * L.w + x;
+                        un[gi] = uo[gi] + acc;
+                    }
+                }
+            }
+            __syncthreads();
+            if (tid == 0) {
+                __threadfence();
+                atomicAdd(&A.band_done[grow], 1u);
+            }
         }
     }
 }

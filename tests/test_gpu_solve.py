@@ -198,6 +198,51 @@ def test_graph_and_eager_paths_agree():
     a.close(); b.close()
 
 
+def test_device_resident_solve_and_layout_checks():
+    """Plan.solve_device (b200p_solve on caller-owned device buffers) == host path bit-for-bit;
+    non-contiguous / mistyped tensors are rejected instead of being read with the wrong strides."""
+    import torch
+    m, k = oracle.seeded_problem(384, 256, 0.03, 4, channels=3)
+    cfg = bp.MultigridConfig(block_size=32, overlap=6)
+    plan = bp.Plan(384, 256, 3, 1, cfg)
+    d_mask = torch.from_numpy(m.view(np.uint8)[None].copy()).cuda()
+    d_known = torch.from_numpy(k[None].copy()).cuda()
+    d_out, reps = plan.solve_device(d_mask, d_known)
+    host = bp.solve_image(bp.InpaintingProblem(m, k), "mg-oras", cfg)
+    assert np.array_equal(d_out.cpu().numpy()[0], host.fields)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        d_out2, _ = plan.solve_device(d_mask, d_known)
+    torch.cuda.synchronize()
+    assert torch.equal(d_out, d_out2)
+    with pytest.raises(ValueError):
+        plan.solve_device(d_mask, d_known.transpose(2, 3))
+    with pytest.raises(ValueError):
+        plan.solve_device(d_mask, d_known.float())
+    with pytest.raises(ValueError):
+        plan.solve_device(d_mask[:, :100], d_known)
+    plan.close()
+
+
+def test_fused_and_split_sweeps_agree():
+    """B200P_FUSED=0 (K2 + K2b) and the fused persistent sweep give the same fields."""
+    import os
+    m, k = oracle.seeded_problem(640, 400, 0.02, 3, channels=3)
+    cfg = bp.MultigridConfig(block_size=32, overlap=6)
+    mk = m.view(np.uint8)[None]
+    a = bp.Plan(640, 400, 3, 1, cfg)
+    os.environ["B200P_FUSED"] = "0"
+    try:
+        b = bp.Plan(640, 400, 3, 1, cfg)
+    finally:
+        del os.environ["B200P_FUSED"]
+    oa, ra = a.solve_host(mk, k[None])
+    ob, rb = b.solve_host(mk, k[None])
+    assert [r.iterations for r in ra] == [r.iterations for r in rb]
+    assert np.array_equal(oa, ob)
+    a.close(); b.close()
+
+
 def test_u8_ingest_egress():
     """fileio.image_from_fields (fileio.py:58-65): round half to even, clip to [0,255]."""
     m, k = oracle.seeded_problem(200, 120, 0.05, 1, channels=3)
