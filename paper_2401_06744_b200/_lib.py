@@ -12,7 +12,7 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libb200paint.so")
+LIB_PATH = os.environ.get("B200P_LIB") or os.path.join(_HERE, "libb200paint.so")  # override: A/B builds
 CSRC = os.path.join(_HERE, "csrc")
 
 MAX_LEVELS = 32

@@ -204,6 +204,7 @@ struct b200p_plan {
     int *d_active = nullptr, *d_cycles = nullptr, *d_units = nullptr, *d_histlen = nullptr;
     int *d_any = nullptr;
     double *d_baseline = nullptr, *d_denom = nullptr, *d_rel = nullptr, *d_hist = nullptr;
+    unsigned long long *d_stats = nullptr;  // B200P_STATS=1: K2F cycle accounting
     unsigned *d_sched = nullptr;  // K2F counters: [work | row_done P*ny | band_done P*ny]
     size_t sched_words = 0;
     int *d_gate = nullptr, *d_sweeps = nullptr;  // stage API (oras_sweeps with stop_norm)
@@ -366,10 +367,20 @@ static int launch_norm(b200p_plan *pl, const LevelHost &L, const double *u, cons
     LaunchScope sc(pl, st, KK_NORM, field_bytes(pl, L, rm ? 1.0 : 2.0, 1.0));
 #define NORM_ARGS u, b, L.d_mask, L.info.height, L.info.width, L.dev.hinv2, pl->C, plane, pred, \
                   pl->d_partial, pl->d_partial_flag, pl->d_counter, pl->d_rs, pl->d_mflag
-    if (um && rm) residual_sqnorm_kernel<true, true><<<grid, ST_THREADS, 0, st>>>(NORM_ARGS);
-    else if (rm) residual_sqnorm_kernel<false, true><<<grid, ST_THREADS, 0, st>>>(NORM_ARGS);
-    else if (um) residual_sqnorm_kernel<true, false><<<grid, ST_THREADS, 0, st>>>(NORM_ARGS);
-    else residual_sqnorm_kernel<false, false><<<grid, ST_THREADS, 0, st>>>(NORM_ARGS);
+    const bool vec_ok = L.info.width % 2 == 0 && L.info.width >= 4 && ((uintptr_t)u % 16) == 0 &&
+                        ((uintptr_t)L.d_mask % 2) == 0 && (plane % 2) == 0;
+    if (!um && vec_ok) {
+        // vector path: two columns per thread, one partial per (column strip, row chunk)
+        dim3 g((L.info.width / 2 + ST_THREADS - 1) / ST_THREADS, (L.info.height + NORM_ROWS - 1) / NORM_ROWS, pl->P);
+        if (rm) residual_sqnorm_rows2_kernel<true><<<g, ST_THREADS, 0, st>>>(NORM_ARGS);
+        else residual_sqnorm_rows2_kernel<false><<<g, ST_THREADS, 0, st>>>(NORM_ARGS);
+    } else if (!um) {
+        // scalar row-walking kernel (odd widths)
+        dim3 g((L.info.width + ST_THREADS - 1) / ST_THREADS, (L.info.height + NORM_ROWS - 1) / NORM_ROWS, pl->P);
+        if (rm) residual_sqnorm_rows_kernel<true><<<g, ST_THREADS, 0, st>>>(NORM_ARGS);
+        else residual_sqnorm_rows_kernel<false><<<g, ST_THREADS, 0, st>>>(NORM_ARGS);
+    } else if (rm) residual_sqnorm_kernel<true, true><<<grid, ST_THREADS, 0, st>>>(NORM_ARGS);
+    else residual_sqnorm_kernel<true, false><<<grid, ST_THREADS, 0, st>>>(NORM_ARGS);
 #undef NORM_ARGS
     CU(cudaGetLastError());
     return 0;
@@ -444,6 +455,7 @@ static int launch_sweep_fused(b200p_plan *pl, const LevelHost &L, UBuf &u, const
     A.band_first_row = L.d_band_first_row;
     A.row_last_band = L.d_row_last_band;
     A.unit_counter = unit_counter;
+    A.stats = pl->d_stats;
     CU(cudaMemsetAsync(pl->d_sched, 0, sizeof(unsigned) * (1 + 2 * rows), st));
     const long long total = (long long)pl->P * A.items_per_problem;
     const int grid = (int)std::min<long long>(total, L.fused_grid);
@@ -843,6 +855,14 @@ int b200p_level_shapes(int width, int height, double spacing, int block, int ove
 void b200p_plan_destroy(b200p_plan *pl) {
     if (!pl) return;
     prof_collect(pl);
+    if (pl->d_stats) {
+        unsigned long long h[8] = {0};
+        cudaDeviceSynchronize();
+        cudaMemcpy(h, pl->d_stats, 64, cudaMemcpyDeviceToHost);
+        fprintf(stderr, "[b200p stats] solve: %llu items, %.0f cyc/item (+%.0f wait)  combine: %llu items, %.0f cyc/item (+%.0f wait)\n",
+                h[4], h[4] ? (double)h[0] / h[4] : 0.0, h[4] ? (double)h[2] / h[4] : 0.0, h[5],
+                h[5] ? (double)h[1] / h[5] : 0.0, h[5] ? (double)h[3] / h[5] : 0.0);
+    }
     if (pl->g_front.exec) cudaGraphExecDestroy(pl->g_front.exec);
     if (pl->g_cycle.exec) cudaGraphExecDestroy(pl->g_cycle.exec);
     for (void *p : pl->owned) cudaFree(p);
@@ -950,7 +970,8 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
                 }
                 const char *le = getenv("B200P_LAG");
                 L.lag = le ? std::max(0, atoi(le)) : 4;
-                L.R = L.lag + span + 4;
+                const char *re = getenv("B200P_RING");
+                L.R = L.lag + span + 1 + (re ? std::max(0, atoi(re)) : 16);
                 L.nsx = (L.info.nx + bpc - 1) / bpc;
                 L.cw = FUSED_THREADS;
                 L.nc = (w + L.cw - 1) / L.cw;
@@ -983,9 +1004,17 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
     }
     PTRY(dev_alloc(pl, &pl->d_scratch, scratch));
     PTRY(dev_alloc(pl, &pl->d_sched, std::max<size_t>(pl->sched_words, 4)));
+    if (getenv("B200P_STATS")) {
+        PTRY(dev_alloc(pl, &pl->d_stats, (size_t)8));
+        CU(cudaMemset(pl->d_stats, 0, 64));
+    }
     pl->norm_ctas = std::max(1, std::min(1024, (148 * 8 + pl->P - 1) / pl->P));
-    PTRY(dev_alloc(pl, &pl->d_partial, (size_t)pl->P * pl->norm_ctas));
-    PTRY(dev_alloc(pl, &pl->d_partial_flag, (size_t)pl->P * pl->norm_ctas));
+    size_t nparts = pl->norm_ctas;
+    for (const LevelHost &L : pl->lev)
+        nparts = std::max(nparts, (size_t)((L.info.width + ST_THREADS - 1) / ST_THREADS) *
+                                      ((L.info.height + NORM_ROWS - 1) / NORM_ROWS));
+    PTRY(dev_alloc(pl, &pl->d_partial, (size_t)pl->P * nparts));
+    PTRY(dev_alloc(pl, &pl->d_partial_flag, (size_t)pl->P * nparts));
     PTRY(dev_alloc(pl, &pl->d_counter, (size_t)pl->P));
     CU(cudaMemset(pl->d_counter, 0, sizeof(unsigned) * pl->P));
     PTRY(dev_alloc(pl, &pl->d_rs, (size_t)pl->P));

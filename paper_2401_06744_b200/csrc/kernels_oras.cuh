@@ -311,8 +311,11 @@ __device__ __forceinline__ void tile_block_solve(const SweepArgs &A, int p, int 
     }
 }
 
+#ifndef B200P_TILE_MINB
+#define B200P_TILE_MINB 1
+#endif
 template <int TW, int TH, int NWARP, bool RM>
-__global__ void __launch_bounds__(NWARP * 32)
+__global__ void __launch_bounds__(NWARP * 32, B200P_TILE_MINB)
 oras_sweep_tile_kernel(const SweepArgs A) {
     __shared__ TileSmem<TW, TH, NWARP> sm;
     const int p = blockIdx.y;
@@ -359,6 +362,7 @@ struct FusedArgs {
     const int *band_first_row;  // [ny] first block row a band reads
     const int *row_last_band;   // [ny] last band that reads a block row
     int *unit_counter;    // per-problem sweep counter (may be null)
+    unsigned long long *stats;  // debug (may be null): cycles solve, combine, wait-ring, wait-rows; item counts
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
@@ -373,13 +377,22 @@ __device__ __forceinline__ void spin_until(const unsigned *ctr, unsigned target)
 
 constexpr int FUSED_THREADS = 128;
 
+#ifndef B200P_FUSED_MINB
+#define B200P_FUSED_MINB 4
+#endif
+#ifndef B200P_COMBINE_G
+#define B200P_COMBINE_G 4
+#endif
+
 template <int TW, int TH, int NWARP, bool RM>
-__global__ void __launch_bounds__(FUSED_THREADS)
+__global__ void __launch_bounds__(FUSED_THREADS, (TH * TW * NWARP <= 32 ? B200P_FUSED_MINB : 1))
 oras_fused_sweep_kernel(const FusedArgs A) {
     constexpr int BW = 8 * TW, BH = 4 * TH * NWARP;
     constexpr int BPC = FUSED_THREADS / (NWARP * 32);  // blocks per solve item
     __shared__ TileSmem<TW, TH, NWARP> sm[BPC];
     __shared__ unsigned s_item;
+    __shared__ int s_rn[BH], s_rf[BH];
+    __shared__ size_t s_roff[BH][2];
     const LevelDev &L = A.S.L;
     const int tid = threadIdx.x;
     const int ny = L.ny, nx = L.nx;
@@ -415,6 +428,8 @@ oras_fused_sweep_kernel(const FusedArgs A) {
         const bool skip = (A.S.pred && !A.S.pred[p]) || A.S.rs[p] == 0.0;
         const int grow = p * ny + row;  // global block row / band index
 
+        long long t0 = 0, t1 = 0;
+        if (A.stats && tid == 0) t0 = t1 = clock64();
         if (solve) {
             if (!skip) {
                 // ring slot re-use: the bands that read the previous occupant must be done
@@ -425,6 +440,7 @@ oras_fused_sweep_kernel(const FusedArgs A) {
                         spin_until(&A.band_done[op * ny + b], (unsigned)A.nc);
                     __threadfence();
                 }
+                if (A.stats && tid == 0) t1 = clock64();
                 __syncthreads();
                 const int warp = tid >> 5;
                 const int grp = warp / NWARP, wg = warp - grp * NWARP;
@@ -439,6 +455,12 @@ oras_fused_sweep_kernel(const FusedArgs A) {
             if (tid == 0) {
                 __threadfence();
                 atomicAdd(&A.row_done[grow], 1u);
+                if (A.stats) {
+                    const long long t2 = clock64();
+                    atomicAdd(&A.stats[0], (unsigned long long)(t2 - t1));
+                    atomicAdd(&A.stats[2], (unsigned long long)(t1 - t0));
+                    atomicAdd(&A.stats[4], 1ull);
+                }
             }
         } else {
             // ---- combine band `row`, columns [sub*cw, sub*cw + cw)
@@ -457,34 +479,73 @@ oras_fused_sweep_kernel(const FusedArgs A) {
                     for (int r = A.band_first_row[row]; r <= row; ++r)
                         spin_until(&A.row_done[p * ny + r], (unsigned)A.nsx);
                     __threadfence();
+                    if (A.stats) t1 = clock64();
                 }
                 __syncthreads();
                 if (A.unit_counter && row == 0 && sub == 0 && tid == 0) A.unit_counter[p] += 1;
                 const size_t bsz = (size_t)BW * BH;
-                // thread -> one column, FUSED_THREADS / cw row phases
-                const int tx = tid % A.cw, ty = tid / A.cw;
-                const int x = x0 + tx;
+                const int rows = y1 - y0;  // <= BH
+                // per-row covering block rows (uniform over the chunk): count + ring offsets of
+                // the first two tiles' row starts
+                if (tid < rows) {
+                    const int y = y0 + tid;
+                    const int iyf = L.cyf[y], iyn = L.cyn[y];
+                    s_rn[tid] = iyn;
+                    s_rf[tid] = iyf;
+                    for (int a = 0; a < 2; ++a) {
+                        const int iy = iyf + (a < iyn ? a : 0);
+                        s_roff[tid][a] = ((size_t)((p * ny + iy) % A.R) * nx) * bsz + (size_t)(y - L.ys[iy]) * BW;
+                    }
+                }
+                __syncthreads();
+                const int x = x0 + tid;  // cw == FUSED_THREADS: one column per thread
                 if (x < x1) {
                     const int ixf = L.cxf[x], ixn = L.cxn[x];
-                    const int lx0 = x - L.xs[ixf];
-                    const int lx1 = ixn > 1 ? x - L.xs[ixf + 1] : 0;
-                    const int lx2 = ixn > 2 ? x - L.xs[ixf + 2] : 0;
-                    for (int y = y0 + ty; y < y1; y += FUSED_THREADS / A.cw) {
-                        const int iyf = L.cyf[y], iyn = L.cyn[y];
-                        double acc = 0.0;
-                        for (int a = 0; a < iyn; ++a) {
-                            const int iy = iyf + a;
-                            const int ly = y - L.ys[iy];
-                            const double *tile = A.S.scratch +
-                                ((size_t)((p * ny + iy) % A.R) * nx + ixf) * bsz + (size_t)ly * BW;
-                            acc += __ldcg(tile + lx0);
-                            if (ixn > 1) acc += __ldcg(tile + bsz + lx1);
-                            if (ixn > 2) acc += __ldcg(tile + 2 * bsz + lx2);
-                            for (int c = 3; c < ixn; ++c)
-                                acc += __ldcg(tile + (size_t)c * bsz + (x - L.xs[ixf + c]));
+                    const size_t xo0 = (size_t)ixf * bsz + (x - L.xs[ixf]);
+                    const size_t xo1 = ixn > 1 ? (size_t)(ixf + 1) * bsz + (x - L.xs[ixf + 1]) : 0;
+                    const double *ring = A.S.scratch;
+                    constexpr int G = B200P_COMBINE_G;
+                    const bool two_x = ixn > 1;
+                    const bool wide = ixn > 2;  // > 2 covering blocks per axis: heavily overlapped layouts
+                    for (int k0 = 0; k0 < rows; k0 += G) {
+                        double uu[G], cc[G], v00[G], v01[G], v10[G], v11[G];
+                        // all loads first, branch-free (absent contributions re-read tile 0 and are
+                        // discarded), so that ~40 independent loads per thread are in flight
+#pragma unroll
+                        for (int j = 0; j < G; ++j) {
+                            const int k = k0 + j < rows ? k0 + j : rows - 1;
+                            uu[j] = uo[(size_t)(y0 + k) * L.w + x];
+                            const size_t o0 = s_roff[k][0], o1 = s_roff[k][1];
+                            v00[j] = __ldcg(ring + o0 + xo0);
+                            v01[j] = __ldcg(ring + o0 + (two_x ? xo1 : xo0));
+                            v10[j] = __ldcg(ring + o1 + xo0);
+                            v11[j] = __ldcg(ring + o1 + (two_x ? xo1 : xo0));
                         }
-                        const size_t gi = (size_t)y * L.w + x;
-                        un[gi] = uo[gi] + acc;
+#pragma unroll
+                        for (int j = 0; j < G; ++j) {
+                            const int k = k0 + j < rows ? k0 + j : rows - 1;
+                            const int n = s_rn[k];
+                            // ascending block order: (iy0,ix0), (iy0,ix1), (iy1,ix0), (iy1,ix1)
+                            double acc = v00[j];
+                            acc += two_x ? v01[j] : 0.0;
+                            if (wide || n > 2) {
+                                acc = 0.0;
+                                for (int a = 0; a < n; ++a) {
+                                    const int iy = s_rf[k] + a;
+                                    const size_t oa = ((size_t)((p * ny + iy) % A.R) * nx) * bsz +
+                                                      (size_t)(y0 + k - L.ys[iy]) * BW;
+                                    for (int c = 0; c < ixn; ++c)
+                                        acc += __ldcg(ring + oa + (size_t)(ixf + c) * bsz + (x - L.xs[ixf + c]));
+                                }
+                            } else {
+                                acc += n > 1 ? v10[j] : 0.0;
+                                acc += (n > 1 && two_x) ? v11[j] : 0.0;
+                            }
+                            cc[j] = acc;
+                        }
+#pragma unroll
+                        for (int j = 0; j < G; ++j)
+                            if (k0 + j < rows) un[(size_t)(y0 + k0 + j) * L.w + x] = uu[j] + cc[j];
                     }
                 }
             }
@@ -492,6 +553,12 @@ oras_fused_sweep_kernel(const FusedArgs A) {
             if (tid == 0) {
                 __threadfence();
                 atomicAdd(&A.band_done[grow], 1u);
+                if (A.stats) {
+                    const long long t2 = clock64();
+                    atomicAdd(&A.stats[1], (unsigned long long)(t2 - t1));
+                    atomicAdd(&A.stats[3], (unsigned long long)(t1 - t0));
+                    atomicAdd(&A.stats[5], 1ull);
+                }
             }
         }
     }

@@ -80,6 +80,191 @@ residual_sqnorm_kernel(const double *__restrict__ u, const double *__restrict__ 
     }
 }
 
+// K1 (fast path, u given as a field): grid (ceil(w/256), ceil(h/NORM_ROWS), P).
+// Thread x walks NORM_ROWS consecutive rows with a 3-row register window, so
+// every u value is fetched from DRAM once (left/right neighbours are L1 hits of
+// the same coalesced row); no integer division per pixel.  Partials are
+// reduced by the last CTA of a problem in index order (deterministic).
+constexpr int NORM_ROWS = 32;
+
+template <bool RM>
+__global__ void __launch_bounds__(ST_THREADS)
+residual_sqnorm_rows_kernel(const double *__restrict__ u, const double *__restrict__ b,
+                            const uint8_t *__restrict__ mask, int h, int w, double hinv2, int channels,
+                            size_t plane, const int *__restrict__ pred, double *__restrict__ partial,
+                            int *__restrict__ partial_flag, unsigned *__restrict__ counter,
+                            double *__restrict__ rs_out, int *__restrict__ flag_out) {
+    __shared__ double red[34];
+    __shared__ int sflag;
+    __shared__ bool is_last;
+    const int p = blockIdx.z;
+    if (pred && !pred[p]) return;
+    const double *up = u + (size_t)p * plane;
+    const double *bp = b + (size_t)p * plane;
+    const uint8_t *mp = mask + (size_t)(p / channels) * plane;
+    if (threadIdx.x == 0) sflag = 0;
+    __syncthreads();
+    const int x = blockIdx.x * ST_THREADS + threadIdx.x;
+    const int y0 = blockIdx.y * NORM_ROWS;
+    const int y1 = min(h, y0 + NORM_ROWS);
+    double acc = 0.0;
+    int flag = 0;
+    if (x < w) {
+        const double cx = 4.0 - (x == 0 ? 1.0 : 0.0) - (x == w - 1 ? 1.0 : 0.0);
+        const bool hasL = x > 0, hasR = x < w - 1;
+        const double *col = up + x;
+        double above = y0 > 0 ? col[(size_t)(y0 - 1) * w] : 0.0;
+        double centre = col[(size_t)y0 * w];
+#pragma unroll 4
+        for (int y = y0; y < y1; ++y) {
+            const size_t i = (size_t)y * w + x;
+            const double below = y < h - 1 ? col[(size_t)(y + 1) * w] : 0.0;
+            const double left = hasL ? up[i - 1] : 0.0;
+            const double right = hasR ? up[i + 1] : 0.0;
+            const bool m = mp[i] != 0;
+            double r;
+            if (m) {
+                r = bp[i] - centre;
+                if (r != 0.0) flag = 1;
+            } else {
+                const double bb = RM ? 0.0 : bp[i];
+                const double cnt = cx - (y == 0 ? 1.0 : 0.0) - (y == h - 1 ? 1.0 : 0.0);
+                // same operation order as residual_px: ((up + down) + left) + right
+                const double s = ((above + below) + left) + right;
+                r = bb - (s * (-hinv2) + (cnt * hinv2) * centre);
+            }
+            acc += r * r;
+            above = centre;
+            centre = below;
+        }
+    }
+    if (flag) sflag = 1;
+    const double tot = cta_sum(acc, red);
+    const unsigned nparts = gridDim.x * gridDim.y;
+    const unsigned me = blockIdx.y * gridDim.x + blockIdx.x;
+    if (threadIdx.x == 0) {
+        partial[(size_t)p * nparts + me] = tot;
+        partial_flag[(size_t)p * nparts + me] = sflag;
+        __threadfence();
+        const unsigned done = atomicAdd(&counter[p], 1u);
+        is_last = (done == nparts - 1);
+    }
+    __syncthreads();
+    if (is_last) {
+        __threadfence();
+        double t = 0.0;
+        int f = 0;
+        for (unsigned k = threadIdx.x; k < nparts; k += ST_THREADS) {
+            t += ((volatile double *)partial)[(size_t)p * nparts + k];
+            f |= ((volatile int *)partial_flag)[(size_t)p * nparts + k];
+        }
+        if (f) sflag = 1;
+        const double total = cta_sum(t, red);
+        if (threadIdx.x == 0) {
+            rs_out[p] = total;
+            flag_out[p] = sflag;
+            counter[p] = 0;
+        }
+    }
+}
+
+// K1 (vector path): as residual_sqnorm_rows_kernel, but every thread owns TWO
+// adjacent columns (one 16-byte load per row) and takes its left/right
+// neighbours from the adjacent lanes by shuffle; only the warp's edge lanes load
+// an extra element.  Needs an even width (rows stay 16-byte aligned).
+template <bool RM>
+__global__ void __launch_bounds__(ST_THREADS)
+residual_sqnorm_rows2_kernel(const double *__restrict__ u, const double *__restrict__ b,
+                             const uint8_t *__restrict__ mask, int h, int w, double hinv2, int channels,
+                             size_t plane, const int *__restrict__ pred, double *__restrict__ partial,
+                             int *__restrict__ partial_flag, unsigned *__restrict__ counter,
+                             double *__restrict__ rs_out, int *__restrict__ flag_out) {
+    __shared__ double red[34];
+    __shared__ int sflag;
+    __shared__ bool is_last;
+    const int p = blockIdx.z;
+    if (pred && !pred[p]) return;
+    const double *up = u + (size_t)p * plane;
+    const double *bp = b + (size_t)p * plane;
+    const uint8_t *mp = mask + (size_t)(p / channels) * plane;
+    if (threadIdx.x == 0) sflag = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int x = 2 * (blockIdx.x * ST_THREADS + threadIdx.x);  // columns x, x+1
+    const int y0 = blockIdx.y * NORM_ROWS;
+    const int y1 = min(h, y0 + NORM_ROWS);
+    double acc = 0.0;
+    int flag = 0;
+    const bool live = x < w;  // w even: x+1 < w as well
+    // warp-uniform trip count; dead lanes clamp their column so shuffles stay defined
+    const int xc = live ? x : w - 2;
+    const double cx0 = 4.0 - (xc == 0 ? 1.0 : 0.0);
+    const double cx1 = 4.0 - (xc + 1 == w - 1 ? 1.0 : 0.0);
+    const double2 zero2 = make_double2(0.0, 0.0);
+    double2 above = y0 > 0 ? *reinterpret_cast<const double2 *>(up + (size_t)(y0 - 1) * w + xc) : zero2;
+    double2 centre = *reinterpret_cast<const double2 *>(up + (size_t)y0 * w + xc);
+#pragma unroll 4
+    for (int y = y0; y < y1; ++y) {
+        const size_t i = (size_t)y * w + xc;
+        const double2 below = y < h - 1 ? *reinterpret_cast<const double2 *>(up + i + w) : zero2;
+        double left = __shfl_up_sync(FULL_MASK, centre.y, 1);
+        double right = __shfl_down_sync(FULL_MASK, centre.x, 1);
+        if (lane == 0) left = xc > 0 ? up[i - 1] : 0.0;
+        if (lane == 31) right = xc + 2 < w ? up[i + 2] : 0.0;
+        if (xc + 2 >= w) right = 0.0;  // last column pair of the image
+        const uchar2 m2 = *reinterpret_cast<const uchar2 *>(mp + i);
+        const double cy = (y == 0 ? 1.0 : 0.0) + (y == h - 1 ? 1.0 : 0.0);
+        double r0, r1;
+        if (m2.x) {
+            r0 = bp[i] - centre.x;
+            if (r0 != 0.0) flag = 1;
+        } else {
+            const double bb = RM ? 0.0 : bp[i];
+            const double s = ((above.x + below.x) + left) + centre.y;
+            r0 = bb - (s * (-hinv2) + ((cx0 - cy) * hinv2) * centre.x);
+        }
+        if (m2.y) {
+            r1 = bp[i + 1] - centre.y;
+            if (r1 != 0.0) flag = 1;
+        } else {
+            const double bb = RM ? 0.0 : bp[i + 1];
+            const double s = ((above.y + below.y) + centre.x) + right;
+            r1 = bb - (s * (-hinv2) + ((cx1 - cy) * hinv2) * centre.y);
+        }
+        if (live) acc += r0 * r0 + r1 * r1;
+        above = centre;
+        centre = below;
+    }
+    if (flag && live) sflag = 1;
+    const double tot = cta_sum(acc, red);
+    const unsigned nparts = gridDim.x * gridDim.y;
+    const unsigned me = blockIdx.y * gridDim.x + blockIdx.x;
+    if (threadIdx.x == 0) {
+        partial[(size_t)p * nparts + me] = tot;
+        partial_flag[(size_t)p * nparts + me] = sflag;
+        __threadfence();
+        const unsigned done = atomicAdd(&counter[p], 1u);
+        is_last = (done == nparts - 1);
+    }
+    __syncthreads();
+    if (is_last) {
+        __threadfence();
+        double t = 0.0;
+        int f = 0;
+        for (unsigned k = threadIdx.x; k < nparts; k += ST_THREADS) {
+            t += ((volatile double *)partial)[(size_t)p * nparts + k];
+            f |= ((volatile int *)partial_flag)[(size_t)p * nparts + k];
+        }
+        if (f) sflag = 1;
+        const double total = cta_sum(t, red);
+        if (threadIdx.x == 0) {
+            rs_out[p] = total;
+            flag_out[p] = sflag;
+            counter[p] = 0;
+        }
+    }
+}
+
 // residual field (StencilOperator.residual, core.py:109-110); with b == 0 and
 // negate it is StencilOperator.apply.
 __global__ void __launch_bounds__(ST_THREADS)
