@@ -369,11 +369,13 @@ static int launch_norm(b200p_plan *pl, const LevelHost &L, const double *u, cons
                   pl->d_partial, pl->d_partial_flag, pl->d_counter, pl->d_rs, pl->d_mflag
     const bool vec_ok = L.info.width % 2 == 0 && L.info.width >= 4 && ((uintptr_t)u % 16) == 0 &&
                         ((uintptr_t)L.d_mask % 2) == 0 && (plane % 2) == 0;
-    if (!um && vec_ok) {
+    if (vec_ok) {
         // vector path: two columns per thread, one partial per (column strip, row chunk)
         dim3 g((L.info.width / 2 + ST_THREADS - 1) / ST_THREADS, (L.info.height + NORM_ROWS - 1) / NORM_ROWS, pl->P);
-        if (rm) residual_sqnorm_rows2_kernel<true><<<g, ST_THREADS, 0, st>>>(NORM_ARGS);
-        else residual_sqnorm_rows2_kernel<false><<<g, ST_THREADS, 0, st>>>(NORM_ARGS);
+        if (um && rm) residual_sqnorm_rows2_kernel<true, true><<<g, ST_THREADS, 0, st>>>(NORM_ARGS);
+        else if (um) residual_sqnorm_rows2_kernel<true, false><<<g, ST_THREADS, 0, st>>>(NORM_ARGS);
+        else if (rm) residual_sqnorm_rows2_kernel<false, true><<<g, ST_THREADS, 0, st>>>(NORM_ARGS);
+        else residual_sqnorm_rows2_kernel<false, false><<<g, ST_THREADS, 0, st>>>(NORM_ARGS);
     } else if (!um) {
         // scalar row-walking kernel (odd widths)
         dim3 g((L.info.width + ST_THREADS - 1) / ST_THREADS, (L.info.height + NORM_ROWS - 1) / NORM_ROWS, pl->P);
@@ -397,9 +399,9 @@ enum { TILE_GENERIC = 0, TILE_32_A = 1, TILE_16 = 2, TILE_8 = 3, TILE_32_B = 4, 
 static int tile_for(int bw, int bh) {
     if (bw == 32 && bh == 32) {
         const char *e = getenv("B200P_TILE32");
-        if (e && *e == 'B') return TILE_32_B;
+        if (e && *e == 'A') return TILE_32_A;
         if (e && *e == 'C') return TILE_32_C;
-        return TILE_32_A;
+        return TILE_32_B;
     }
     if (bw == 16 && bh == 16) return TILE_16;
     if (bw == 8 && bh == 8) return TILE_8;
@@ -414,8 +416,19 @@ static void launch_tile(const SweepArgs &A, bool rm, dim3 grid, cudaStream_t st)
 
 template <int TW, int TH, int NWARP>
 static void launch_fused(const FusedArgs &A, bool rm, int grid, cudaStream_t st) {
-    if (rm) oras_fused_sweep_kernel<TW, TH, NWARP, true><<<grid, FUSED_THREADS, 0, st>>>(A);
-    else oras_fused_sweep_kernel<TW, TH, NWARP, false><<<grid, FUSED_THREADS, 0, st>>>(A);
+    const size_t smem = sizeof(double) * 4 * TH * NWARP * FUSED_THREADS;  // u_old staging of one band chunk
+    if (rm) oras_fused_sweep_kernel<TW, TH, NWARP, true><<<grid, FUSED_THREADS, smem, st>>>(A);
+    else oras_fused_sweep_kernel<TW, TH, NWARP, false><<<grid, FUSED_THREADS, smem, st>>>(A);
+}
+
+template <int TW, int TH, int NWARP>
+static int fused_occupancy() {
+    int occ = 0;
+    const size_t smem = sizeof(double) * 4 * TH * NWARP * FUSED_THREADS;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, oras_fused_sweep_kernel<TW, TH, NWARP, true>,
+                                                      FUSED_THREADS, smem) != cudaSuccess)
+        occ = 0;
+    return occ;
 }
 
 static void fill_sweep_args(b200p_plan *pl, const LevelHost &L, const double *u, const double *b,
@@ -496,7 +509,8 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, double *u, con
         CU(cudaGetLastError());
     }
     {
-        dim3 g((L.info.width + 127) / 128, (L.info.height + 1) / 2, pl->P);
+        dim3 g((L.info.width + ST_THREADS_COMBINE - 1) / ST_THREADS_COMBINE,
+               (L.info.height + COMBINE_ROWS - 1) / COMBINE_ROWS, pl->P);
         LaunchScope sc(pl, st, KK_COMBINE, field_bytes(pl, L, 2.0, 0.0));
         oras_combine_kernel<<<g, ST_THREADS_COMBINE, 0, st>>>(L.dev, pl->d_scratch, A.plane, pred,
                                                               pl->d_rs, u, unit_counter);
@@ -956,7 +970,7 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
         const size_t plane = (size_t)h * w;
         {
             const char *e = getenv("B200P_FUSED");
-            const bool want = !(e && *e == '0');
+            const bool want = e && *e == '1';  // experimental; the split sweep (K2 + K2b) is faster
             const int bpc = L.tile == TILE_32_A ? 1 : (L.tile == TILE_32_B ? 2 : (L.tile == TILE_16 ? 4 : 0));
             if (want && bpc > 0 && L.nblocks > 1) {
                 L.fused = true;
@@ -969,9 +983,9 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
                     span = std::max(span, last[j] - j);
                 }
                 const char *le = getenv("B200P_LAG");
-                L.lag = le ? std::max(0, atoi(le)) : 4;
+                L.lag = le ? std::max(0, atoi(le)) : 8;
                 const char *re = getenv("B200P_RING");
-                L.R = L.lag + span + 1 + (re ? std::max(0, atoi(re)) : 16);
+                L.R = L.lag + span + 1 + (re ? std::max(0, atoi(re)) : 24);
                 L.nsx = (L.info.nx + bpc - 1) / bpc;
                 L.cw = FUSED_THREADS;
                 L.nc = (w + L.cw - 1) / L.cw;
@@ -982,14 +996,9 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
                 pl->sched_words = std::max(pl->sched_words, (size_t)1 + 2 * (size_t)pl->P * L.info.ny);
                 int occ = 0, sms = 148;
                 cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-                cudaError_t oe = cudaSuccess;
-                if (L.tile == TILE_32_A)
-                    oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, oras_fused_sweep_kernel<4, 2, 4, true>, FUSED_THREADS, 0);
-                else if (L.tile == TILE_32_B)
-                    oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, oras_fused_sweep_kernel<4, 4, 2, true>, FUSED_THREADS, 0);
-                else
-                    oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, oras_fused_sweep_kernel<2, 4, 1, true>, FUSED_THREADS, 0);
-                if (oe != cudaSuccess || occ < 1) occ = 4;
+                occ = L.tile == TILE_32_A ? fused_occupancy<4, 2, 4>()
+                      : (L.tile == TILE_32_B ? fused_occupancy<4, 4, 2>() : fused_occupancy<2, 4, 1>());
+                if (occ < 1) occ = 4;
                 L.fused_grid = sms * occ;
             }
         }

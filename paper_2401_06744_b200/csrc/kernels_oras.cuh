@@ -141,10 +141,14 @@ struct TileSmem {
 // the PoU-weighted correction (v*wy)*wx as a (BH,BW) tile at `out`
 // (solvers.py:303-305, :328-370, :309-310).  STCG: store with st.global.cg
 // (L2 only) -- used when another CTA of the same kernel reads the tile.
-template <int TW, int TH, int NWARP, bool RM, bool STCG>
+struct NoHook {
+    __device__ __forceinline__ void operator()() const {}
+};
+
+template <int TW, int TH, int NWARP, bool RM, bool STCG, class PreStore = NoHook>
 __device__ __forceinline__ void tile_block_solve(const SweepArgs &A, int p, int blk, int grp, int wg,
                                                  TileSmem<TW, TH, NWARP> &sm, double target,
-                                                 double *__restrict__ out) {
+                                                 double *__restrict__ out, PreStore pre_store = PreStore()) {
     using CG = TileCG<TW, TH, NWARP>;
     constexpr int BW = CG::BW, BH = CG::BH;
     const LevelDev &L = A.L;
@@ -285,6 +289,7 @@ __device__ __forceinline__ void tile_block_solve(const SweepArgs &A, int p, int 
     }
 
     // ---- weighted correction (v * wy) * wx (solvers.py:309-310)
+    pre_store();  // fused sweep: the ring slot must be free before the tile is written
     double wxv[TW];
 #pragma unroll
     for (int i = 0; i < TW; ++i) wxv[i] = L.wx[ix * BW + bx + i];
@@ -381,8 +386,16 @@ constexpr int FUSED_THREADS = 128;
 #define B200P_FUSED_MINB 4
 #endif
 #ifndef B200P_COMBINE_G
-#define B200P_COMBINE_G 4
+#define B200P_COMBINE_G 8
 #endif
+
+__device__ __forceinline__ void cp_async8(void *smem_dst, const void *gmem_src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
 
 template <int TW, int TH, int NWARP, bool RM>
 __global__ void __launch_bounds__(FUSED_THREADS, (TH * TW * NWARP <= 32 ? B200P_FUSED_MINB : 1))
@@ -390,9 +403,10 @@ oras_fused_sweep_kernel(const FusedArgs A) {
     constexpr int BW = 8 * TW, BH = 4 * TH * NWARP;
     constexpr int BPC = FUSED_THREADS / (NWARP * 32);  // blocks per solve item
     __shared__ TileSmem<TW, TH, NWARP> sm[BPC];
-    __shared__ unsigned s_item;
+    __shared__ unsigned s_item[2];
     __shared__ int s_rn[BH], s_rf[BH];
     __shared__ size_t s_roff[BH][2];
+    extern __shared__ __align__(16) double s_u[];  // BH x FUSED_THREADS staging of u_old
     const LevelDev &L = A.S.L;
     const int tid = threadIdx.x;
     const int ny = L.ny, nx = L.nx;
@@ -400,12 +414,14 @@ oras_fused_sweep_kernel(const FusedArgs A) {
     const int lag = A.lag < ny ? A.lag : ny;
     const int per_slot = A.nsx + A.nc;
 
-    for (;;) {
-        __syncthreads();
-        if (tid == 0) s_item = atomicAdd(A.work, 1u);
-        __syncthreads();
-        const unsigned item = s_item;
+    // claim-ahead: the next item is requested while the current one is processed.  An item
+    // claimed early still only waits on items earlier in the order, so progress is kept.
+    if (tid == 0) s_item[0] = atomicAdd(A.work, 1u);
+    __syncthreads();
+    for (int it = 0;; ++it) {
+        const unsigned item = s_item[it & 1];
         if (item >= total) break;
+        if (tid == 0) s_item[(it + 1) & 1] = atomicAdd(A.work, 1u);
         const int p = (int)(item / (unsigned)A.items_per_problem);
         int q = (int)(item - (unsigned)p * (unsigned)A.items_per_problem);
         // ---- decode (see the order described above)
@@ -427,28 +443,42 @@ oras_fused_sweep_kernel(const FusedArgs A) {
         }
         const bool skip = (A.S.pred && !A.S.pred[p]) || A.S.rs[p] == 0.0;
         const int grow = p * ny + row;  // global block row / band index
-
         long long t0 = 0, t1 = 0;
         if (A.stats && tid == 0) t0 = t1 = clock64();
+
         if (solve) {
             if (!skip) {
-                // ring slot re-use: the bands that read the previous occupant must be done
+                // Ring slot re-use: the bands that read the slot's previous occupant must be done
+                // before the tile is WRITTEN (end of the item).  Poll the flags now (one lane per
+                // band), re-check just before the stores.
                 const int old = grow - A.R;
-                if (old >= 0 && tid == 0) {
+                const unsigned *flag = nullptr;
+                bool ok = true;
+                if (old >= 0) {
                     const int op = old / ny, orow = old - op * ny;
-                    for (int b = orow; b <= A.row_last_band[orow]; ++b)
-                        spin_until(&A.band_done[op * ny + b], (unsigned)A.nc);
-                    __threadfence();
+                    if (tid <= A.row_last_band[orow] - orow) {
+                        flag = &A.band_done[op * ny + orow + tid];
+                        ok = ld_acquire_u32(flag) >= (unsigned)A.nc;
+                    }
                 }
-                if (A.stats && tid == 0) t1 = clock64();
-                __syncthreads();
+                auto pre_store = [&]() {
+                    if (!ok) {
+                        long long w0 = 0;
+                        if (A.stats) w0 = clock64();
+                        spin_until(flag, (unsigned)A.nc);
+                        if (A.stats) atomicAdd(&A.stats[2], (unsigned long long)(clock64() - w0));
+                    }
+                    __syncthreads();
+                };
                 const int warp = tid >> 5;
                 const int grp = warp / NWARP, wg = warp - grp * NWARP;
                 const int ix = sub * BPC + grp;
                 if (ix < nx) {
                     double *out = A.S.scratch + ((size_t)(grow % A.R) * nx + ix) * (BW * BH);
                     tile_block_solve<TW, TH, NWARP, RM, true>(A.S, p, row * nx + ix, grp, wg, sm[grp],
-                                                              A.S.eta * A.S.rs[p], out);
+                                                              A.S.eta * A.S.rs[p], out, pre_store);
+                } else {
+                    pre_store();
                 }
             }
             __syncthreads();
@@ -456,35 +486,35 @@ oras_fused_sweep_kernel(const FusedArgs A) {
                 __threadfence();
                 atomicAdd(&A.row_done[grow], 1u);
                 if (A.stats) {
-                    const long long t2 = clock64();
-                    atomicAdd(&A.stats[0], (unsigned long long)(t2 - t1));
-                    atomicAdd(&A.stats[2], (unsigned long long)(t1 - t0));
+                    atomicAdd(&A.stats[0], (unsigned long long)(clock64() - t0));
                     atomicAdd(&A.stats[4], 1ull);
                 }
             }
         } else {
-            // ---- combine band `row`, columns [sub*cw, sub*cw + cw)
+            // ---- combine band `row`, columns [sub*cw, sub*cw + cw); cw == FUSED_THREADS
             const int y0 = L.ys[row];
             const int y1 = row + 1 < ny ? L.ys[row + 1] : L.h;
-            const int x0 = sub * A.cw;
-            const int x1 = x0 + A.cw < L.w ? x0 + A.cw : L.w;
+            const int rows = y1 - y0;  // <= BH
+            const int x = sub * A.cw + tid;
+            const bool inx = x < L.w;
             const double *uo = A.S.u + (size_t)p * A.S.plane;
             double *un = A.u_new + (size_t)p * A.S.plane;
+            // u_old of the whole chunk goes to shared memory asynchronously (no registers held)
+            if (inx)
+                for (int k = 0; k < rows; ++k)
+                    cp_async8(&s_u[k * FUSED_THREADS + tid], uo + (size_t)(y0 + k) * L.w + x);
             if (skip) {
-                for (int y = y0 + (tid / A.cw); y < y1; y += FUSED_THREADS / A.cw)
-                    for (int x = x0 + (tid % A.cw); x < x1; x += A.cw)
-                        un[(size_t)y * L.w + x] = uo[(size_t)y * L.w + x];
+                cp_async_wait_all();
+                if (inx)
+                    for (int k = 0; k < rows; ++k)
+                        un[(size_t)(y0 + k) * L.w + x] = s_u[k * FUSED_THREADS + tid];
             } else {
-                if (tid == 0) {
-                    for (int r = A.band_first_row[row]; r <= row; ++r)
-                        spin_until(&A.row_done[p * ny + r], (unsigned)A.nsx);
-                    __threadfence();
-                    if (A.stats) t1 = clock64();
-                }
-                __syncthreads();
+                // rows this band reads must be complete: one lane per block row polls
+                const int r0 = A.band_first_row[row];
+                if (tid <= row - r0) spin_until(&A.row_done[p * ny + r0 + tid], (unsigned)A.nsx);
+                if (A.stats && tid == 0) t1 = clock64();
                 if (A.unit_counter && row == 0 && sub == 0 && tid == 0) A.unit_counter[p] += 1;
                 const size_t bsz = (size_t)BW * BH;
-                const int rows = y1 - y0;  // <= BH
                 // per-row covering block rows (uniform over the chunk): count + ring offsets of
                 // the first two tiles' row starts
                 if (tid < rows) {
@@ -498,8 +528,7 @@ oras_fused_sweep_kernel(const FusedArgs A) {
                     }
                 }
                 __syncthreads();
-                const int x = x0 + tid;  // cw == FUSED_THREADS: one column per thread
-                if (x < x1) {
+                if (inx) {
                     const int ixf = L.cxf[x], ixn = L.cxn[x];
                     const size_t xo0 = (size_t)ixf * bsz + (x - L.xs[ixf]);
                     const size_t xo1 = ixn > 1 ? (size_t)(ixf + 1) * bsz + (x - L.xs[ixf + 1]) : 0;
@@ -507,14 +536,14 @@ oras_fused_sweep_kernel(const FusedArgs A) {
                     constexpr int G = B200P_COMBINE_G;
                     const bool two_x = ixn > 1;
                     const bool wide = ixn > 2;  // > 2 covering blocks per axis: heavily overlapped layouts
+                    bool landed = false;
                     for (int k0 = 0; k0 < rows; k0 += G) {
-                        double uu[G], cc[G], v00[G], v01[G], v10[G], v11[G];
-                        // all loads first, branch-free (absent contributions re-read tile 0 and are
-                        // discarded), so that ~40 independent loads per thread are in flight
+                        double cc[G], v00[G], v01[G], v10[G], v11[G];
+                        // all ring loads first, branch-free (absent contributions re-read tile 0 and
+                        // are discarded), so that 4*G independent loads per thread are in flight
 #pragma unroll
                         for (int j = 0; j < G; ++j) {
                             const int k = k0 + j < rows ? k0 + j : rows - 1;
-                            uu[j] = uo[(size_t)(y0 + k) * L.w + x];
                             const size_t o0 = s_roff[k][0], o1 = s_roff[k][1];
                             v00[j] = __ldcg(ring + o0 + xo0);
                             v01[j] = __ldcg(ring + o0 + (two_x ? xo1 : xo0));
@@ -543,9 +572,14 @@ oras_fused_sweep_kernel(const FusedArgs A) {
                             }
                             cc[j] = acc;
                         }
+                        if (!landed) {
+                            cp_async_wait_all();  // own copies only: each thread reads back what it issued
+                            landed = true;
+                        }
 #pragma unroll
                         for (int j = 0; j < G; ++j)
-                            if (k0 + j < rows) un[(size_t)(y0 + k0 + j) * L.w + x] = uu[j] + cc[j];
+                            if (k0 + j < rows)
+                                un[(size_t)(y0 + k0 + j) * L.w + x] = s_u[(k0 + j) * FUSED_THREADS + tid] + cc[j];
                     }
                 }
             }
@@ -561,6 +595,7 @@ oras_fused_sweep_kernel(const FusedArgs A) {
                 }
             }
         }
+        __syncthreads();  // s_item[(it+1)&1] visible; shared staging free for the next item
     }
 }
 
@@ -718,33 +753,85 @@ oras_sweep_generic_kernel(const SweepArgs A) {
 // ------------------------------------------------------------------ K2b ---
 // u += sum_b w_b v_b over the blocks covering each pixel, accumulated from 0 in
 // ascending block index (iy outer, ix inner) like np.bincount does, then added
-// to u (solvers.py:310-314, :423).  One thread per pixel; the per-axis cover
-// tables give the first covering slot and the slot count.
+// to u (solvers.py:310-314, :423).  Grid (ceil(w/256), ceil(h/COMBINE_ROWS), P):
+// a thread owns one column of a COMBINE_ROWS-row chunk.  The covering block rows
+// of each pixel row (uniform over the chunk) are staged in shared memory, the
+// covering block columns are per-thread constants, and the (up to) four tile
+// reads per pixel are issued branch-free, COMBINE_G rows at a time, so that
+// ~40 independent loads per thread are in flight (HBM-bound streaming pass).
+constexpr int COMBINE_ROWS = 32;
+constexpr int COMBINE_G = 8;
+
 __global__ void __launch_bounds__(ST_THREADS_COMBINE)
 oras_combine_kernel(const LevelDev L, const double *__restrict__ scratch, size_t plane,
                     const int *__restrict__ pred, const double *__restrict__ rs,
                     double *__restrict__ u, int *__restrict__ unit_counter) {
+    __shared__ int s_rn[COMBINE_ROWS], s_rf[COMBINE_ROWS];
+    __shared__ size_t s_roff[COMBINE_ROWS][2];
     const int p = blockIdx.z;
     if (pred && !pred[p]) return;
     if (rs[p] == 0.0) return;
-    const int x = blockIdx.x * 128 + (threadIdx.x & 127);
-    const int y = blockIdx.y * 2 + (threadIdx.x >> 7);
-    if (unit_counter && x == 0 && y == 0) unit_counter[p] += 1;
-    if (x >= L.w || y >= L.h) return;
-    const int ixf = L.cxf[x], ixn = L.cxn[x], iyf = L.cyf[y], iyn = L.cyn[y];
+    const int tid = threadIdx.x;
+    const int x = blockIdx.x * ST_THREADS_COMBINE + tid;
+    const int y0 = blockIdx.y * COMBINE_ROWS;
+    const int rows = min(COMBINE_ROWS, L.h - y0);
+    if (unit_counter && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) unit_counter[p] += 1;
     const size_t bsz = (size_t)L.bw * L.bh;
-    const double *sp = scratch + (size_t)p * L.nblocks * bsz;
-    double acc = 0.0;
-    for (int a = 0; a < iyn; ++a) {
-        const int iy = iyf + a;
-        const int ly = y - L.ys[iy];
-        for (int c = 0; c < ixn; ++c) {
-            const int ix = ixf + c;
-            const int lx = x - L.xs[ix];
-            acc += sp[((size_t)iy * L.nx + ix) * bsz + (size_t)ly * L.bw + lx];
+    if (tid < rows) {
+        const int y = y0 + tid;
+        const int iyf = L.cyf[y], iyn = L.cyn[y];
+        s_rn[tid] = iyn;
+        s_rf[tid] = iyf;
+        for (int a = 0; a < 2; ++a) {
+            const int iy = iyf + (a < iyn ? a : 0);
+            s_roff[tid][a] = (size_t)iy * L.nx * bsz + (size_t)(y - L.ys[iy]) * L.bw;
         }
     }
-    u[(size_t)p * plane + (size_t)y * L.w + x] += acc;
+    __syncthreads();
+    if (x >= L.w) return;
+    const int ixf = L.cxf[x], ixn = L.cxn[x];
+    const size_t xo0 = (size_t)ixf * bsz + (x - L.xs[ixf]);
+    const size_t xo1 = ixn > 1 ? (size_t)(ixf + 1) * bsz + (x - L.xs[ixf + 1]) : 0;
+    const bool two_x = ixn > 1;
+    const bool wide = ixn > 2;  // > 2 covering blocks per axis: heavily overlapped layouts
+    const double *sp = scratch + (size_t)p * L.nblocks * bsz;
+    double *up = u + (size_t)p * plane;
+    constexpr int G = COMBINE_G;
+    for (int k0 = 0; k0 < rows; k0 += G) {
+        double uu[G], v00[G], v01[G], v10[G], v11[G];
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+            const int k = k0 + j < rows ? k0 + j : rows - 1;
+            const size_t o0 = s_roff[k][0], o1 = s_roff[k][1];
+            uu[j] = up[(size_t)(y0 + k) * L.w + x];
+            v00[j] = sp[o0 + xo0];
+            v01[j] = sp[o0 + (two_x ? xo1 : xo0)];
+            v10[j] = sp[o1 + xo0];
+            v11[j] = sp[o1 + (two_x ? xo1 : xo0)];
+        }
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+            const int k = k0 + j;
+            if (k >= rows) break;
+            const int n = s_rn[k];
+            // ascending block order: (iy0,ix0), (iy0,ix1), (iy1,ix0), (iy1,ix1)
+            double acc = v00[j];
+            acc += two_x ? v01[j] : 0.0;
+            if (wide || n > 2) {
+                acc = 0.0;
+                for (int a = 0; a < n; ++a) {
+                    const int iy = s_rf[k] + a;
+                    const size_t oa = (size_t)iy * L.nx * bsz + (size_t)(y0 + k - L.ys[iy]) * L.bw;
+                    for (int c = 0; c < ixn; ++c)
+                        acc += sp[oa + (size_t)(ixf + c) * bsz + (x - L.xs[ixf + c])];
+                }
+            } else {
+                acc += n > 1 ? v10[j] : 0.0;
+                acc += (n > 1 && two_x) ? v11[j] : 0.0;
+            }
+            up[(size_t)(y0 + k) * L.w + x] = uu[j] + acc;
+        }
+    }
 }
 
 // ------------------------------------------------------------------ K7 ----

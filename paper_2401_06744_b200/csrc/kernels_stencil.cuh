@@ -172,7 +172,7 @@ residual_sqnorm_rows_kernel(const double *__restrict__ u, const double *__restri
 // adjacent columns (one 16-byte load per row) and takes its left/right
 // neighbours from the adjacent lanes by shuffle; only the warp's edge lanes load
 // an extra element.  Needs an even width (rows stay 16-byte aligned).
-template <bool RM>
+template <bool UM, bool RM>
 __global__ void __launch_bounds__(ST_THREADS)
 residual_sqnorm_rows2_kernel(const double *__restrict__ u, const double *__restrict__ b,
                              const uint8_t *__restrict__ mask, int h, int w, double hinv2, int channels,
@@ -201,16 +201,30 @@ residual_sqnorm_rows2_kernel(const double *__restrict__ u, const double *__restr
     const double cx0 = 4.0 - (xc == 0 ? 1.0 : 0.0);
     const double cx1 = 4.0 - (xc + 1 == w - 1 ? 1.0 : 0.0);
     const double2 zero2 = make_double2(0.0, 0.0);
-    double2 above = y0 > 0 ? *reinterpret_cast<const double2 *>(up + (size_t)(y0 - 1) * w + xc) : zero2;
-    double2 centre = *reinterpret_cast<const double2 *>(up + (size_t)y0 * w + xc);
+    // UM: the iterate is where(mask, u, 0) (flat initialisation read straight from `known`)
+    auto row2 = [&](size_t i) {
+        double2 v = *reinterpret_cast<const double2 *>(up + i);
+        if (UM) {
+            const uchar2 mm = *reinterpret_cast<const uchar2 *>(mp + i);
+            v.x = mm.x ? v.x : 0.0;
+            v.y = mm.y ? v.y : 0.0;
+        }
+        return v;
+    };
+    auto one = [&](size_t i) {
+        const double v = up[i];
+        return UM ? (mp[i] ? v : 0.0) : v;
+    };
+    double2 above = y0 > 0 ? row2((size_t)(y0 - 1) * w + xc) : zero2;
+    double2 centre = row2((size_t)y0 * w + xc);
 #pragma unroll 4
     for (int y = y0; y < y1; ++y) {
         const size_t i = (size_t)y * w + xc;
-        const double2 below = y < h - 1 ? *reinterpret_cast<const double2 *>(up + i + w) : zero2;
+        const double2 below = y < h - 1 ? row2(i + w) : zero2;
         double left = __shfl_up_sync(FULL_MASK, centre.y, 1);
         double right = __shfl_down_sync(FULL_MASK, centre.x, 1);
-        if (lane == 0) left = xc > 0 ? up[i - 1] : 0.0;
-        if (lane == 31) right = xc + 2 < w ? up[i + 2] : 0.0;
+        if (lane == 0) left = xc > 0 ? one(i - 1) : 0.0;
+        if (lane == 31) right = xc + 2 < w ? one(i + 2) : 0.0;
         if (xc + 2 >= w) right = 0.0;  // last column pair of the image
         const uchar2 m2 = *reinterpret_cast<const uchar2 *>(mp + i);
         const double cy = (y == 0 ? 1.0 : 0.0) + (y == h - 1 ? 1.0 : 0.0);

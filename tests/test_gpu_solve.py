@@ -194,7 +194,7 @@ def test_graph_and_eager_paths_agree():
     prof = a.profile_summary()
     a.profile(False)
     assert np.array_equal(oa, od)
-    assert prof["oras_sweep"][1] > 0 and prof["oras_sweep"][0] > 0
+    assert prof["oras_sweep_split"][1] > 0 and prof["oras_sweep_split"][0] > 0
     a.close(); b.close()
 
 
@@ -225,13 +225,14 @@ def test_device_resident_solve_and_layout_checks():
 
 
 def test_fused_and_split_sweeps_agree():
-    """B200P_FUSED=0 (K2 + K2b) and the fused persistent sweep give the same fields."""
+    """The default split sweep (K2 + K2b) and the experimental fused persistent sweep
+    (B200P_FUSED=1) give the same fields."""
     import os
     m, k = oracle.seeded_problem(640, 400, 0.02, 3, channels=3)
     cfg = bp.MultigridConfig(block_size=32, overlap=6)
     mk = m.view(np.uint8)[None]
     a = bp.Plan(640, 400, 3, 1, cfg)
-    os.environ["B200P_FUSED"] = "0"
+    os.environ["B200P_FUSED"] = "1"
     try:
         b = bp.Plan(640, 400, 3, 1, cfg)
     finally:
