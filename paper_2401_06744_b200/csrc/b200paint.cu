@@ -21,6 +21,7 @@
 
 #include "../../include/b200paint.h"
 #include "kernels_stencil.cuh"
+#include "kernels_rows.cuh"
 #include "kernels_oras.cuh"
 
 using namespace b200p;
@@ -359,6 +360,35 @@ static double field_bytes(const b200p_plan *pl, const LevelHost &L, double field
     return fields * pl->P * 8.0 * n + masks * pl->F * n;
 }
 
+static int rows_chunk(int h) { return h >= 1024 ? 32 : (h >= 256 ? 16 : 8); }
+
+static bool rows4_ok(const LevelHost &L, const double *u, const double *b) {
+    const size_t plane = (size_t)L.info.height * L.info.width;
+    return L.info.width % 4 == 0 && L.info.width >= 8 && plane % 4 == 0 && ((uintptr_t)u % 16) == 0 &&
+           ((uintptr_t)b % 16) == 0 && ((uintptr_t)L.d_mask % 4) == 0;
+}
+
+static RowsArgs rows_args(b200p_plan *pl, const LevelHost &L, const double *u, const double *b,
+                          const int *pred) {
+    RowsArgs R;
+    R.u = u;
+    R.b = b;
+    R.mask = L.d_mask;
+    R.h = L.info.height;
+    R.w = L.info.width;
+    R.hinv2 = L.dev.hinv2;
+    R.channels = pl->C;
+    R.plane = (size_t)L.info.height * L.info.width;
+    R.pred = pred;
+    R.rows_per_cta = rows_chunk(L.info.height);
+    R.partial = pl->d_partial;
+    R.partial_flag = pl->d_partial_flag;
+    R.counter = pl->d_counter;
+    R.rs_out = pl->d_rs;
+    R.flag_out = pl->d_mflag;
+    return R;
+}
+
 // K1: rs[p] = ||b - A u||^2, mflag[p].  UM/RM as in residual_px.
 static int launch_norm(b200p_plan *pl, const LevelHost &L, const double *u, const double *b,
                        bool um, bool rm, const int *pred, cudaStream_t st) {
@@ -367,6 +397,18 @@ static int launch_norm(b200p_plan *pl, const LevelHost &L, const double *u, cons
     LaunchScope sc(pl, st, KK_NORM, field_bytes(pl, L, rm ? 1.0 : 2.0, 1.0));
 #define NORM_ARGS u, b, L.d_mask, L.info.height, L.info.width, L.dev.hinv2, pl->C, plane, pred, \
                   pl->d_partial, pl->d_partial_flag, pl->d_counter, pl->d_rs, pl->d_mflag
+    if (rows4_ok(L, u, b)) {
+        // four columns per thread, 16-byte loads (kernels_rows.cuh)
+        RowsArgs R = rows_args(pl, L, u, b, pred);
+        dim3 g4((L.info.width / 4 + ROWS4_THREADS - 1) / ROWS4_THREADS,
+                (L.info.height + R.rows_per_cta - 1) / R.rows_per_cta, pl->P);
+        if (um && rm) residual_sqnorm_rows4_kernel<true, true><<<g4, ROWS4_THREADS, 0, st>>>(R);
+        else if (um) residual_sqnorm_rows4_kernel<true, false><<<g4, ROWS4_THREADS, 0, st>>>(R);
+        else if (rm) residual_sqnorm_rows4_kernel<false, true><<<g4, ROWS4_THREADS, 0, st>>>(R);
+        else residual_sqnorm_rows4_kernel<false, false><<<g4, ROWS4_THREADS, 0, st>>>(R);
+        CU(cudaGetLastError());
+        return 0;
+    }
     const bool vec_ok = L.info.width % 2 == 0 && L.info.width >= 4 && ((uintptr_t)u % 16) == 0 &&
                         ((uintptr_t)L.d_mask % 2) == 0 && (plane % 2) == 0;
     if (vec_ok) {
@@ -678,19 +720,33 @@ static int enqueue_vcycle(b200p_plan *pl, int level, UBuf &u, const double *b, b
     if (rc) return rc;
     LevelHost &Cc = pl->lev[level + 1];
     UBuf e = level_ubuf(pl, level + 1, nullptr);
+    bool coarse_norm = false;  // K3 also produced ||r_c||^2 = residual norm^2 of the coarse system at e = 0
     {
         LaunchScope sc(pl, st, KK_RESTRICT, field_bytes(pl, L, rm ? 1.25 : 2.25, 1.25));
-        dim3 g = grid2x(Cc.info.width, Cc.info.height, pl->P);
         // e is zeroed by the coarse solve (init_mode 0) on the coarsest level, else here
         double *ez = (level + 1 == nl - 1) ? nullptr : e.cur;
-        if (rm)
-            residual_restrict_kernel<true><<<g, ST_THREADS, 0, st>>>(
-                u.cur, b, L.d_mask, Cc.d_mask, L.info.height, L.info.width, L.dev.hinv2, pl->C, pred,
-                Cc.d_rc, ez);
-        else
-            residual_restrict_kernel<false><<<g, ST_THREADS, 0, st>>>(
-                u.cur, b, L.d_mask, Cc.d_mask, L.info.height, L.info.width, L.dev.hinv2, pl->C, pred,
-                Cc.d_rc, ez);
+        if (rows4_ok(L, u.cur, b) && ((uintptr_t)Cc.d_rc % 16) == 0 && ((uintptr_t)Cc.d_mask % 2) == 0) {
+            RestrictArgs RA;
+            RA.R = rows_args(pl, L, u.cur, b, pred);
+            RA.cmask = Cc.d_mask;
+            RA.rc = Cc.d_rc;
+            RA.e_zero = ez;
+            dim3 g4((L.info.width / 4 + ROWS4_THREADS - 1) / ROWS4_THREADS,
+                    (L.info.height + RA.R.rows_per_cta - 1) / RA.R.rows_per_cta, pl->P);
+            if (rm) residual_restrict_rows4_kernel<true><<<g4, ROWS4_THREADS, 0, st>>>(RA);
+            else residual_restrict_rows4_kernel<false><<<g4, ROWS4_THREADS, 0, st>>>(RA);
+            coarse_norm = true;
+        } else {
+            dim3 g = grid2x(Cc.info.width, Cc.info.height, pl->P);
+            if (rm)
+                residual_restrict_kernel<true><<<g, ST_THREADS, 0, st>>>(
+                    u.cur, b, L.d_mask, Cc.d_mask, L.info.height, L.info.width, L.dev.hinv2, pl->C, pred,
+                    Cc.d_rc, ez);
+            else
+                residual_restrict_kernel<false><<<g, ST_THREADS, 0, st>>>(
+                    u.cur, b, L.d_mask, Cc.d_mask, L.info.height, L.info.width, L.dev.hinv2, pl->C, pred,
+                    Cc.d_rc, ez);
+        }
         CU(cudaGetLastError());
     }
     if (level + 1 == nl - 1) {
@@ -698,7 +754,7 @@ static int enqueue_vcycle(b200p_plan *pl, int level, UBuf &u, const double *b, b
         rc = launch_coarse(pl, Cc, e.cur, Cc.d_rc, false, 0, tol, cfg.coarse_max_iters, pred,
                            nullptr, 0, st);
     } else {
-        rc = enqueue_vcycle(pl, level + 1, e, Cc.d_rc, false, pred, nullptr, false, st, false);
+        rc = enqueue_vcycle(pl, level + 1, e, Cc.d_rc, false, pred, nullptr, coarse_norm, st, false);
     }
     if (rc) return rc;
     {
@@ -1020,8 +1076,12 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
     pl->norm_ctas = std::max(1, std::min(1024, (148 * 8 + pl->P - 1) / pl->P));
     size_t nparts = pl->norm_ctas;
     for (const LevelHost &L : pl->lev)
+    {
         nparts = std::max(nparts, (size_t)((L.info.width + ST_THREADS - 1) / ST_THREADS) *
                                       ((L.info.height + NORM_ROWS - 1) / NORM_ROWS));
+        nparts = std::max(nparts, (size_t)((L.info.width / 4 + ROWS4_THREADS - 1) / ROWS4_THREADS + 1) *
+                                      ((L.info.height + 7) / 8));
+    }
     PTRY(dev_alloc(pl, &pl->d_partial, (size_t)pl->P * nparts));
     PTRY(dev_alloc(pl, &pl->d_partial_flag, (size_t)pl->P * nparts));
     PTRY(dev_alloc(pl, &pl->d_counter, (size_t)pl->P));

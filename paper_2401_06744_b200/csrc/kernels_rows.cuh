@@ -1,0 +1,253 @@
+// kernels_rows.cuh -- row-walking residual kernels (HBM-bound passes over a level).
+//
+// A thread owns FOUR adjacent columns and walks a chunk of rows with a 3-row
+// register window: every u value is fetched once with 16-byte loads, vertical
+// neighbours come from the window, horizontal ones from the thread's own
+// registers or the adjacent lane (shuffle); only a warp's two edge lanes load one
+// extra element per row.  No integer division, no per-pixel bounds tests.
+//
+//   K1  residual_sqnorm_rows4_kernel    ||b - A u||^2 per problem       (solvers.py:415-417)
+//   K3  residual_restrict_rows4_kernel  r = b - A u restricted 2x2, plus ||r_c||^2 of
+//                                       the coarse system with e = 0    (multigrid.py:358-361)
+//
+// Both need w % 4 == 0 and 16-byte aligned planes; other shapes use the scalar
+// kernels of kernels_stencil.cuh.
+#pragma once
+#include "common.cuh"
+
+namespace b200p {
+
+constexpr int ROWS4_THREADS = 128;  // 512 columns per CTA
+#ifndef B200P_ROWS_UNROLL
+#define B200P_ROWS_UNROLL 1
+#endif
+
+struct RowsArgs {
+    const double *u, *b;
+    const uint8_t *mask;
+    int h, w;
+    double hinv2;
+    int channels;
+    size_t plane;
+    const int *pred;
+    int rows_per_cta;  // even
+    // reduction of the per-CTA partials (last CTA of a problem sums them in index order)
+    double *partial;
+    int *partial_flag;
+    unsigned *counter;
+    double *rs_out;
+    int *flag_out;
+};
+
+// Deterministic two-stage reduction: every CTA stores its partial, the last one to
+// arrive (per problem) adds all partials in index order and publishes the total.
+__device__ __forceinline__ void publish_partial(double acc, int flag, int p, const RowsArgs &A,
+                                                double *red, int *sflag, bool *is_last) {
+    const int T = blockDim.x;
+    if (flag) *sflag = 1;
+    const double tot = cta_sum(acc, red);
+    const unsigned nparts = gridDim.x * gridDim.y;
+    const unsigned me = blockIdx.y * gridDim.x + blockIdx.x;
+    if (threadIdx.x == 0) {
+        A.partial[(size_t)p * nparts + me] = tot;
+        A.partial_flag[(size_t)p * nparts + me] = *sflag;
+        __threadfence();
+        const unsigned done = atomicAdd(&A.counter[p], 1u);
+        *is_last = (done == nparts - 1);
+    }
+    __syncthreads();
+    if (*is_last) {
+        __threadfence();
+        double t = 0.0;
+        int f = 0;
+        for (unsigned k = threadIdx.x; k < nparts; k += T) {
+            t += ((volatile double *)A.partial)[(size_t)p * nparts + k];
+            f |= ((volatile int *)A.partial_flag)[(size_t)p * nparts + k];
+        }
+        if (f) *sflag = 1;
+        const double total = cta_sum(t, red);
+        if (threadIdx.x == 0) {
+            A.rs_out[p] = total;
+            A.flag_out[p] = *sflag;
+            A.counter[p] = 0;
+        }
+    }
+}
+
+struct Row4 {
+    double v[4];
+};
+
+// Walks rows [y0, y1) of the thread's four columns xc..xc+3 and hands the
+// residual of each row to `consume(y, r[4], m[4])`.  UM: the iterate is
+// where(mask, u, 0); RM: the right-hand side is where(mask, b, 0).
+// The arithmetic of a pixel follows residual_px (common.cuh) operation by operation.
+template <bool UM, bool RM, class Consumer>
+__device__ __forceinline__ void walk_rows4(const double *__restrict__ up, const double *__restrict__ bp,
+                                           const uint8_t *__restrict__ mp, int h, int w, double hinv2,
+                                           int xc, int y0, int y1, Consumer &consume) {
+    const int lane = threadIdx.x & 31;
+    const bool hasL = xc > 0, hasR = xc + 4 < w;
+    const double cxL = 4.0 - (xc == 0 ? 1.0 : 0.0);
+    const double cxR = 4.0 - (xc + 4 == w ? 1.0 : 0.0);
+    auto load_mask = [&](size_t i) { return *reinterpret_cast<const uchar4 *>(mp + i); };
+    auto load_row = [&](size_t i, uchar4 m) {
+        const double2 a = *reinterpret_cast<const double2 *>(up + i);
+        const double2 c = *reinterpret_cast<const double2 *>(up + i + 2);
+        Row4 r;
+        r.v[0] = a.x; r.v[1] = a.y; r.v[2] = c.x; r.v[3] = c.y;
+        if (UM) {
+            r.v[0] = m.x ? r.v[0] : 0.0;
+            r.v[1] = m.y ? r.v[1] : 0.0;
+            r.v[2] = m.z ? r.v[2] : 0.0;
+            r.v[3] = m.w ? r.v[3] : 0.0;
+        }
+        return r;
+    };
+    auto load_one = [&](size_t i) {
+        const double v = up[i];
+        return UM ? (mp[i] ? v : 0.0) : v;
+    };
+    Row4 above, centre, below;
+    const Row4 zero = {{0.0, 0.0, 0.0, 0.0}};
+    uchar4 mc = load_mask((size_t)y0 * w + xc), mn = mc;
+    above = zero;
+    if (y0 > 0) {
+        const size_t ia = (size_t)(y0 - 1) * w + xc;
+        above = load_row(ia, UM ? load_mask(ia) : mc);
+    }
+    centre = load_row((size_t)y0 * w + xc, mc);
+    // (unrolling or prefetching a further row ahead measured slower: the pass is bound by
+    // occupancy x bytes in flight, and both cost registers)
+    constexpr int kUnroll = B200P_ROWS_UNROLL;
+#pragma unroll kUnroll
+    for (int y = y0; y < y1; ++y) {
+        const size_t i = (size_t)y * w + xc;
+        below = zero;
+        if (y < h - 1) {
+            mn = load_mask(i + w);
+            below = load_row(i + w, mn);
+        }
+        double left = __shfl_up_sync(FULL_MASK, centre.v[3], 1);
+        double right = __shfl_down_sync(FULL_MASK, centre.v[0], 1);
+        if (lane == 0) left = hasL ? load_one(i - 1) : 0.0;
+        if (lane == 31) right = hasR ? load_one(i + 4) : 0.0;
+        if (!hasR) right = 0.0;  // last columns of the image (any lane)
+        const double cy = (y == 0 ? 1.0 : 0.0) + (y == h - 1 ? 1.0 : 0.0);
+        const uint8_t m[4] = {mc.x, mc.y, mc.z, mc.w};
+        double r[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            // branch-free: the stencil value is always formed, mask pixels select b - u
+            const double c = centre.v[k];
+            const double bb = RM ? (m[k] ? bp[i + k] : 0.0) : bp[i + k];
+            const double lf = k == 0 ? left : centre.v[k - 1];
+            const double rt = k == 3 ? right : centre.v[k + 1];
+            const double s = ((above.v[k] + below.v[k]) + lf) + rt;
+            const double cnt = (k == 0 ? cxL : (k == 3 ? cxR : 4.0)) - cy;
+            const double au = s * (-hinv2) + (cnt * hinv2) * c;
+            r[k] = bb - (m[k] ? c : au);
+        }
+        consume(y, r, m);
+        above = centre;
+        centre = below;
+        mc = mn;
+    }
+}
+
+// ---------------------------------------------------------------- K1 ------
+template <bool UM, bool RM>
+__global__ void __launch_bounds__(ROWS4_THREADS)
+residual_sqnorm_rows4_kernel(const RowsArgs A) {
+    __shared__ double red[34];
+    __shared__ int sflag;
+    __shared__ bool is_last;
+    const int p = blockIdx.z;
+    if (A.pred && !A.pred[p]) return;
+    if (threadIdx.x == 0) sflag = 0;
+    __syncthreads();
+    const int x = 4 * (blockIdx.x * ROWS4_THREADS + threadIdx.x);
+    const bool live = x < A.w;
+    const int xc = live ? x : A.w - 4;  // dead lanes shadow the last column group (shuffles stay defined)
+    const int y0 = blockIdx.y * A.rows_per_cta;
+    const int y1 = min(A.h, y0 + A.rows_per_cta);
+    double acc = 0.0;
+    int flag = 0;
+    auto consume = [&](int, const double (&r)[4], const uint8_t (&m)[4]) {
+        acc += (r[0] * r[0] + r[1] * r[1]) + (r[2] * r[2] + r[3] * r[3]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (m[k] && r[k] != 0.0) flag = 1;
+    };
+    walk_rows4<UM, RM>(A.u + (size_t)p * A.plane, A.b + (size_t)p * A.plane,
+                       A.mask + (size_t)(p / A.channels) * A.plane, A.h, A.w, A.hinv2, xc, y0, y1, consume);
+    if (!live) { acc = 0.0; flag = 0; }
+    publish_partial(acc, flag, p, A, red, &sflag, &is_last);
+}
+
+// ---------------------------------------------------------------- K3 ------
+// Fine rows come in pairs (2Y, 2Y+1); the thread's four fine columns make two
+// coarse columns.  Cell mean with the true constituent count (w % 4 == 0, so only
+// the last coarse row of an odd-height level is partial), 0 at coarse mask pixels;
+// NumPy's 2x2 order (a00 + a01) + (a10 + a11) (multigrid.py:91-95, :149-154).
+// Also zeroes the coarse correction e (multigrid.py:361) and accumulates
+// ||r_c||^2, which IS the residual norm^2 of the coarse system at e = 0, so the
+// next level's pre-smoothing needs no separate K1 pass.
+struct RestrictArgs {
+    RowsArgs R;
+    const uint8_t *cmask;  // (F, hc, wc)
+    double *rc;            // (P, hc, wc)
+    double *e_zero;        // (P, hc, wc) or null
+};
+
+template <bool RM>
+__global__ void __launch_bounds__(ROWS4_THREADS)
+residual_restrict_rows4_kernel(const RestrictArgs A) {
+    __shared__ double red[34];
+    __shared__ int sflag;
+    __shared__ bool is_last;
+    const RowsArgs &R = A.R;
+    const int p = blockIdx.z;
+    if (R.pred && !R.pred[p]) return;
+    if (threadIdx.x == 0) sflag = 0;
+    __syncthreads();
+    const int h = R.h, w = R.w;
+    const int hc = (h + 1) >> 1, wc = w >> 1;
+    const int x = 4 * (blockIdx.x * ROWS4_THREADS + threadIdx.x);
+    const bool live = x < w;
+    const int xc = live ? x : w - 4;
+    const int y0 = blockIdx.y * R.rows_per_cta;  // even
+    const int y1 = min(h, y0 + R.rows_per_cta);
+    const size_t cplane = (size_t)hc * wc;
+    const uint8_t *cm = A.cmask + (size_t)(p / R.channels) * cplane;
+    double *rc = A.rc + (size_t)p * cplane;
+    double *ez = A.e_zero ? A.e_zero + (size_t)p * cplane : nullptr;
+    double acc = 0.0;
+    double top0 = 0.0, top1 = 0.0;
+    auto emit = [&](int Y, double s0, double s1, double cnt) {
+        const size_t ci = (size_t)Y * wc + (xc >> 1);
+        const uchar2 m = *reinterpret_cast<const uchar2 *>(cm + ci);
+        double2 o;
+        o.x = m.x ? 0.0 : s0 / cnt;
+        o.y = m.y ? 0.0 : s1 / cnt;
+        if (live) {
+            *reinterpret_cast<double2 *>(rc + ci) = o;
+            if (ez) *reinterpret_cast<double2 *>(ez + ci) = make_double2(0.0, 0.0);
+            acc += o.x * o.x + o.y * o.y;
+        }
+    };
+    auto consume = [&](int y, const double (&r)[4], const uint8_t (&)[4]) {
+        if ((y & 1) == 0) {
+            top0 = r[0] + r[1];
+            top1 = r[2] + r[3];
+            if (y == h - 1) emit(y >> 1, top0 + 0.0, top1 + 0.0, 2.0);  // odd height: single-row cell
+        } else {
+            emit(y >> 1, top0 + (r[0] + r[1]), top1 + (r[2] + r[3]), 4.0);
+        }
+    };
+    walk_rows4<false, RM>(R.u + (size_t)p * R.plane, R.b + (size_t)p * R.plane,
+                          R.mask + (size_t)(p / R.channels) * R.plane, h, w, R.hinv2, xc, y0, y1, consume);
+    publish_partial(acc, 0, p, R, red, &sflag, &is_last);
+}
+
+}  // namespace b200p
