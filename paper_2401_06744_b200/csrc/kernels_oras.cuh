@@ -141,6 +141,21 @@ struct TileSmem {
 // the PoU-weighted correction (v*wy)*wx as a (BH,BW) tile at `out`
 // (solvers.py:303-305, :328-370, :309-310).  STCG: store with st.global.cg
 // (L2 only) -- used when another CTA of the same kernel reads the tile.
+// Dot product of two register tiles with four independent accumulation chains (the single
+// chain of TH*TW dependent DFMAs was on the critical path of every CG step).
+template <int TW, int TH>
+__device__ __forceinline__ double tile_dot(const double (&a)[TH][TW], const double (&b)[TH][TW]) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < TH; ++j)
+#pragma unroll
+        for (int i = 0; i < TW; ++i) {
+            const int k = (j * TW + i) & 3;
+            acc[k] = fma(a[j][i], b[j][i], acc[k]);
+        }
+    return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
 struct NoHook {
     __device__ __forceinline__ void operator()() const {}
 };
@@ -245,12 +260,7 @@ __device__ __forceinline__ void tile_block_solve(const SweepArgs &A, int p, int 
                 r[j][i] = m ? 0.0 : fma(-hinv2, q[j][i], r[j][i]);
             }
     }
-    double part = 0.0;
-#pragma unroll
-    for (int j = 0; j < TH; ++j)
-#pragma unroll
-        for (int i = 0; i < TW; ++i) part = fma(r[j][i], r[j][i], part);
-    double rs_k = cg.group_sum(part);
+    double rs_k = cg.group_sum(tile_dot<TW, TH>(r, r));
 
     if (rs_k > target) {  // solvers.py:336 (strict)
 #pragma unroll
@@ -259,25 +269,18 @@ __device__ __forceinline__ void tile_block_solve(const SweepArgs &A, int p, int 
             for (int i = 0; i < TW; ++i) pc[j][i] = r[j][i];
         for (int it = 0; it < A.max_iters; ++it) {
             cg.apply(pc, q);
-            part = 0.0;
-#pragma unroll
-            for (int j = 0; j < TH; ++j)
-#pragma unroll
-                for (int i = 0; i < TW; ++i) part = fma(pc[j][i], q[j][i], part);
-            const double pq = hinv2 * cg.group_sum(part);
+            const double pq = hinv2 * cg.group_sum(tile_dot<TW, TH>(pc, q));
             const bool ok = pq > 0.0;                 // solvers.py:348
             const double a = ok ? rs_k / pq : 0.0;    // :349-350
             const double ah = a * hinv2;
-            part = 0.0;
 #pragma unroll
             for (int j = 0; j < TH; ++j)
 #pragma unroll
                 for (int i = 0; i < TW; ++i) {
                     v[j][i] = fma(a, pc[j][i], v[j][i]);
                     r[j][i] = fma(-ah, q[j][i], r[j][i]);
-                    part = fma(r[j][i], r[j][i], part);
                 }
-            const double rs_new = cg.group_sum(part);
+            const double rs_new = cg.group_sum(tile_dot<TW, TH>(r, r));
             if (rs_new <= target || !ok) break;       // :354
             const double beta = rs_new / rs_k;
             rs_k = rs_new;
