@@ -55,7 +55,7 @@ struct TileCG {
     double gL, gR, gT, gB;   // ghost factors of those sides
     unsigned mbits;          // local mask, bit j*TW+i
     double *xrow;            // smem: NWARP*2*BW doubles (cross-warp boundary rows)
-    double *red;             // smem: 2*NWARP doubles (two alternating slots)
+    double *red;             // smem: 2*NWARP*3 doubles (two alternating slots of up to 3 values)
     int slot;
 
     __device__ __forceinline__ void group_bar() {
@@ -65,13 +65,40 @@ struct TileCG {
     __device__ __forceinline__ double group_sum(double v) {
         v = warp_sum(v);
         if (NWARP == 1) return v;
-        if (lane == 0) red[slot * NWARP + wg] = v;
+        double *s = red + slot * NWARP * 3;
+        if (lane == 0) s[wg] = v;
         group_bar();
         double t = 0.0;
 #pragma unroll
-        for (int k = 0; k < NWARP; ++k) t += red[slot * NWARP + k];
+        for (int k = 0; k < NWARP; ++k) t += s[k];
         slot ^= 1;
         return t;
+    }
+
+    // Three sums in ONE butterfly / one cross-warp exchange (a single latency chain).
+    __device__ __forceinline__ void group_sum3(double &a, double &b, double &c) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(FULL_MASK, a, o);
+            b += __shfl_xor_sync(FULL_MASK, b, o);
+            c += __shfl_xor_sync(FULL_MASK, c, o);
+        }
+        if (NWARP == 1) return;
+        double *s = red + slot * NWARP * 3;
+        if (lane == 0) {
+            s[wg * 3 + 0] = a;
+            s[wg * 3 + 1] = b;
+            s[wg * 3 + 2] = c;
+        }
+        group_bar();
+        a = b = c = 0.0;
+#pragma unroll
+        for (int k = 0; k < NWARP; ++k) {
+            a += s[k * 3 + 0];
+            b += s[k * 3 + 1];
+            c += s[k * 3 + 2];
+        }
+        slot ^= 1;
     }
 
     // q' = 4p - neighbours (scaled local operator), 0 at mask pixels.
@@ -133,7 +160,7 @@ struct TileCG {
 template <int TW, int TH, int NWARP>
 struct TileSmem {
     double xrow[NWARP > 1 ? NWARP * 2 * 8 * TW : 1];
-    double red[2 * NWARP];
+    double red[2 * NWARP * 3];
 };
 
 // One block's sweep work for the NWARP warps of group `grp`: gather the global
@@ -267,12 +294,22 @@ __device__ __forceinline__ void tile_block_solve(const SweepArgs &A, int p, int 
         for (int j = 0; j < TH; ++j)
 #pragma unroll
             for (int i = 0; i < TW; ++i) pc[j][i] = r[j][i];
+        // CG with ONE reduction per step: (p.q), (r.q) and (q.q) are summed together and the
+        // new squared residual follows from the identity |r - a q|^2 = |r|^2 - 2a (r.q) + a^2 (q.q).
+        // Same iterates as the textbook recurrence (solvers.py:345-369) up to rounding; the step is
+        // latency-bound, so one butterfly + one cross-warp exchange instead of two is what counts.
+        double inv_rs = 1.0 / rs_k;  // for beta; off the critical path
         for (int it = 0; it < A.max_iters; ++it) {
             cg.apply(pc, q);
-            const double pq = hinv2 * cg.group_sum(tile_dot<TW, TH>(pc, q));
+            double d_pq = tile_dot<TW, TH>(pc, q);
+            double d_rq = tile_dot<TW, TH>(r, q);
+            double d_qq = tile_dot<TW, TH>(q, q);
+            cg.group_sum3(d_pq, d_rq, d_qq);
+            const double pq = hinv2 * d_pq;
             const bool ok = pq > 0.0;                 // solvers.py:348
             const double a = ok ? rs_k / pq : 0.0;    // :349-350
             const double ah = a * hinv2;
+            const double rs_new = fma(ah * ah, d_qq, fma(-2.0 * ah, d_rq, rs_k));
 #pragma unroll
             for (int j = 0; j < TH; ++j)
 #pragma unroll
@@ -280,10 +317,10 @@ __device__ __forceinline__ void tile_block_solve(const SweepArgs &A, int p, int 
                     v[j][i] = fma(a, pc[j][i], v[j][i]);
                     r[j][i] = fma(-ah, q[j][i], r[j][i]);
                 }
-            const double rs_new = cg.group_sum(tile_dot<TW, TH>(r, r));
             if (rs_new <= target || !ok) break;       // :354
-            const double beta = rs_new / rs_k;
+            const double beta = rs_new * inv_rs;
             rs_k = rs_new;
+            inv_rs = 1.0 / rs_k;
 #pragma unroll
             for (int j = 0; j < TH; ++j)
 #pragma unroll
