@@ -85,6 +85,10 @@ typedef struct b200p_plan b200p_plan;
 
 const char *b200p_last_error(void);
 int b200p_device_count(void);
+/* CUDA's current device is per host thread: worker threads that drive their own plan
+ * (pipeline lanes) select the device of their process first. */
+int b200p_set_device(int device);
+int b200p_get_device(int *device);
 
 /* Defaults of MultigridConfig()/SolverConfig() for a W x H x C problem. */
 void b200p_config_default(b200p_config *cfg, int width, int height, int channels);

@@ -16,6 +16,7 @@ from .multigrid import (Level, LevelHierarchy, MultigridConfig, Plan, build_hier
                         prolongate_solution, restrict_residual, v_cycle)
 from .partition import (BlockPartition, BlockRect, BlockWeights, build_partition, build_weights,
                         extend_add_weighted, restrict_to_block)
+from .pipeline import FramePipeline
 from .pipelines import (SOLVER_NAMES, SolveResult, join_solver_name, solve_channel, solve_frames,
                         solve_image, split_solver_name)
 from .solvers import BlockSolver, SolveReport, SolverConfig, oras_sweeps
@@ -35,5 +36,5 @@ __all__ = [
     "extend_add_weighted", "restrict_to_block",
     "SOLVER_NAMES", "SolveResult", "join_solver_name", "solve_channel", "solve_frames", "solve_image",
     "split_solver_name",
-    "BlockSolver", "SolveReport", "SolverConfig", "oras_sweeps",
+    "BlockSolver", "SolveReport", "SolverConfig", "oras_sweeps", "FramePipeline",
 ]

@@ -85,6 +85,8 @@ _VP, _I, _D, _I64 = C.c_void_p, C.c_int, C.c_double, C.c_int64
 SIGNATURES = {
     "b200p_last_error": (C.c_char_p, []),
     "b200p_device_count": (_I, []),
+    "b200p_set_device": (_I, [_I]),
+    "b200p_get_device": (_I, [C.POINTER(_I)]),
     "b200p_config_default": (None, [C.POINTER(Config), _I, _I, _I]),
     "b200p_axis_starts": (_I, [_I, _I, _I, _VP, _I]),
     "b200p_axis_weights": (_I, [_I, _I, _I, _VP, _I]),

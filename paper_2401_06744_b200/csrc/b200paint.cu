@@ -553,7 +553,8 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, double *u, con
     {
         dim3 g((L.info.width + ST_THREADS_COMBINE - 1) / ST_THREADS_COMBINE,
                (L.info.height + COMBINE_ROWS - 1) / COMBINE_ROWS, pl->P);
-        LaunchScope sc(pl, st, KK_COMBINE, field_bytes(pl, L, 2.0, 0.0));
+        // read corrections + u, write u
+        LaunchScope sc(pl, st, KK_COMBINE, field_bytes(pl, L, 3.0, 0.0));
         oras_combine_kernel<<<g, ST_THREADS_COMBINE, 0, st>>>(L.dev, pl->d_scratch, A.plane, pred,
                                                               pl->d_rs, u, unit_counter);
         CU(cudaGetLastError());
@@ -865,6 +866,17 @@ int b200p_device_count(void) {
         return 0;
     }
     return n;
+}
+
+int b200p_set_device(int device) {
+    CU(cudaSetDevice(device));
+    return 0;
+}
+
+int b200p_get_device(int *device) {
+    if (!device) return fail_arg(B200P_ERR_ARG, "null argument");
+    CU(cudaGetDevice(device));
+    return 0;
 }
 
 void b200p_config_default(b200p_config *c, int width, int height, int channels) {

@@ -254,3 +254,27 @@ def test_u8_ingest_egress():
     expect = np.clip(np.rint(ref.fields), 0, 255).astype(np.uint8)
     assert np.array_equal(out8[0], expect)
     plan.close()
+
+
+def test_frame_pipeline_matches_batched_plan():
+    """FramePipeline (threads x plans, PCIe overlapped) is bit-identical to one batched plan."""
+    w, h, f, c = 256, 160, 5, 3
+    ms, ks = zip(*(oracle.seeded_problem(w, h, 0.03, s, c) for s in range(f)))
+    masks, known = np.stack(ms), np.stack(ks)
+    cfg = bp.MultigridConfig(block_size=32, overlap=6)
+    ref, ref_reports, _ = bp.solve_frames(masks, known, cfg)
+    pipe = bp.FramePipeline(w, h, c, cfg, lanes=3, frames_per_lane=1)
+    out, reports = pipe.run(masks, known)
+    assert np.array_equal(out, ref)
+    assert [[r.iterations for r in fr] for fr in reports] == [[r.iterations for r in fr] for fr in ref_reports]
+    out8, _ = pipe.run(masks, known.astype(np.uint8), u8=True)
+    assert np.array_equal(out8, np.clip(np.rint(ref), 0, 255).astype(np.uint8))
+    with pytest.raises(ValueError):
+        pipe.run(masks, known.astype(np.float32))
+    pipe.close()
+    bad = masks.copy()
+    bad[2] = False
+    pipe2 = bp.FramePipeline(w, h, c, cfg, lanes=2, frames_per_lane=1)
+    with pytest.raises(bp.EmptyMaskError):
+        pipe2.run(bad, known)
+    pipe2.close()
