@@ -23,6 +23,7 @@
 #include "kernels_stencil.cuh"
 #include "kernels_rows.cuh"
 #include "kernels_oras.cuh"
+#include "kernels_oras_tma.cuh"
 
 using namespace b200p;
 
@@ -160,6 +161,7 @@ struct LevelHost {
     double *d_u = nullptr;      // (P,h,w) cascade iterate / V-cycle correction (levels >= 1)
     double *d_rc = nullptr;     // (P,h,w) restricted residual (levels >= 1)
     int tile = 0;               // K2 variant: 0 generic, else see launch_sweep
+    unsigned *d_mtab = nullptr; // K2T: packed block-local masks (F, nblocks, 64); null = level not eligible
     // fused sweep (K2F): ping-pong partner of the iterate, L2-resident ring, schedule tables
     bool fused = false;
     double *d_u_alt = nullptr;  // (P,h,w)
@@ -436,13 +438,18 @@ static int local_cap(const b200p_plan *pl, const LevelHost &L) {
 }
 
 // Tile variants of K2 (block extent -> <TW,TH,NWARP>).
-enum { TILE_GENERIC = 0, TILE_32_A = 1, TILE_16 = 2, TILE_8 = 3, TILE_32_B = 4, TILE_32_C = 5 };
+enum { TILE_GENERIC = 0, TILE_32_A = 1, TILE_16 = 2, TILE_8 = 3, TILE_32_B = 4, TILE_32_C = 5,
+       TILE_32_S = 6, TILE_32_T = 7, TILE_32_U = 8, TILE_32_TMA = 9 };
 
 static int tile_for(int bw, int bh) {
     if (bw == 32 && bh == 32) {
         const char *e = getenv("B200P_TILE32");
         if (e && *e == 'A') return TILE_32_A;
         if (e && *e == 'C') return TILE_32_C;
+        if (e && *e == 'S') return TILE_32_S;
+        if (e && *e == 'T') return TILE_32_T;
+        if (e && *e == 'U') return TILE_32_U;
+        if (e && *e == 'M') return TILE_32_TMA;
         return TILE_32_B;
     }
     if (bw == 16 && bh == 16) return TILE_16;
@@ -450,10 +457,16 @@ static int tile_for(int bw, int bh) {
     return TILE_GENERIC;
 }
 
-template <int TW, int TH, int NWARP>
+template <int TW, int TH, int NWARP, int REGCAP = 255>
 static void launch_tile(const SweepArgs &A, bool rm, dim3 grid, cudaStream_t st) {
-    if (rm) oras_sweep_tile_kernel<TW, TH, NWARP, true><<<grid, NWARP * 32, 0, st>>>(A);
-    else oras_sweep_tile_kernel<TW, TH, NWARP, false><<<grid, NWARP * 32, 0, st>>>(A);
+    if (rm) oras_sweep_tile_kernel<TW, TH, NWARP, true, REGCAP><<<grid, NWARP * 32, 0, st>>>(A);
+    else oras_sweep_tile_kernel<TW, TH, NWARP, false, REGCAP><<<grid, NWARP * 32, 0, st>>>(A);
+}
+
+template <int TW, int TH, int NWARP, bool SR>
+static void launch_tile_s(const SweepArgs &A, bool rm, dim3 grid, cudaStream_t st) {
+    if (rm) oras_sweep_tile_s_kernel<TW, TH, NWARP, true, SR><<<grid, NWARP * 32, 0, st>>>(A);
+    else oras_sweep_tile_s_kernel<TW, TH, NWARP, false, SR><<<grid, NWARP * 32, 0, st>>>(A);
 }
 
 template <int TW, int TH, int NWARP>
@@ -527,6 +540,95 @@ static int launch_sweep_fused(b200p_plan *pl, const LevelHost &L, UBuf &u, const
     return 0;
 }
 
+// ---- K2T: TMA-fed persistent sweep kernel (kernels_oras_tma.cuh)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn tensor_map_encoder() {
+    static EncodeTiledFn fn = []() -> EncodeTiledFn {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return nullptr;
+        return (EncodeTiledFn)p;
+    }();
+    return fn;
+}
+
+// (P, h, w) fp64 planes as a 3-D tensor; box = bw x bh x 1 elements.
+static int encode_field_map(CUtensorMap *tm, const double *base, int w, int h, int planes, int box_w, int box_h) {
+    EncodeTiledFn enc = tensor_map_encoder();
+    if (!enc) return fail_arg(B200P_ERR_STATE, "cuTensorMapEncodeTiled is not available in this driver");
+    cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)planes};
+    cuuint64_t strides[2] = {(cuuint64_t)w * 8, (cuuint64_t)w * h * 8};
+    cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(base), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail_arg(B200P_ERR_STATE, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return 0;
+}
+
+static int tma_regcap() {
+    static const int cap = getenv("B200P_TMA_REGCAP") ? atoi(getenv("B200P_TMA_REGCAP")) : 168;
+    return cap;
+}
+
+template <bool RM, int REGCAP>
+static int tma_grid() {
+    static int grid = 0;
+    if (!grid) {
+        int occ = 0, sms = 148, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaFuncSetAttribute(oras_sweep_tma_kernel<RM, REGCAP>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, oras_sweep_tma_kernel<RM, REGCAP>, KT_THREADS, 0) !=
+                cudaSuccess || occ < 1)
+            occ = 4;
+        grid = sms * occ;
+    }
+    return grid;
+}
+
+template <bool RM, int REGCAP>
+static void launch_tma_t(const SweepTmaArgs &A, const CUtensorMap &tu, const CUtensorMap &tb, cudaStream_t st) {
+    const int grid = std::min(A.total_items, tma_grid<RM, REGCAP>());
+    oras_sweep_tma_kernel<RM, REGCAP><<<grid, KT_THREADS, 0, st>>>(A, tu, tb);
+}
+
+static bool tma_eligible(const LevelHost &L, const double *u, const double *b, bool rm) {
+    return L.d_mtab && L.info.width % 2 == 0 && ((uintptr_t)u % 16) == 0 && (rm || ((uintptr_t)b % 16) == 0);
+}
+
+static int launch_sweep_tma(b200p_plan *pl, const LevelHost &L, const SweepArgs &S, bool rm, cudaStream_t st) {
+    SweepTmaArgs A;
+    A.S = S;
+    A.mtab = L.d_mtab;
+    A.total_items = pl->P * L.nblocks;
+    CUtensorMap tu, tb;
+    int rc = encode_field_map(&tu, S.u, L.info.width, L.info.height, pl->P, KT_WIN_W, KT_WIN_H);
+    if (rc) return rc;
+    if (rm) tb = tu;
+    else if ((rc = encode_field_map(&tb, S.b, L.info.width, L.info.height, pl->P, 32, 32))) return rc;
+    const int cap = tma_regcap();
+#define KT_LAUNCH(CAP)                                      \
+    do {                                                    \
+        if (rm) launch_tma_t<true, CAP>(A, tu, tb, st);     \
+        else launch_tma_t<false, CAP>(A, tu, tb, st);       \
+    } while (0)
+    if (cap == 255) KT_LAUNCH(255);
+    else if (cap == 160) KT_LAUNCH(160);
+    else if (cap == 128) KT_LAUNCH(128);
+    else KT_LAUNCH(168);
+#undef KT_LAUNCH
+    return 0;
+}
+
 // K2 + K2b: one ORAS sweep (in place on u.cur) using rs/mflag from the preceding K1.
 static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, double *u, const double *b, bool rm,
                               const int *pred, int *unit_counter, int tile, cudaStream_t st) {
@@ -536,10 +638,27 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, double *u, con
     {
         // read u (+ b) + mask, write the weighted correction tiles
         LaunchScope sc(pl, st, KK_SWEEP_SPLIT, field_bytes(pl, L, rm ? 2.0 : 3.0, 1.0));
+        if (tile == TILE_32_TMA && !tma_eligible(L, u, b, rm)) tile = TILE_32_B;
         switch (tile) {
+            case TILE_32_TMA: {
+                int rc = launch_sweep_tma(pl, L, A, rm, st);
+                if (rc) return rc;
+                break;
+            }
             case TILE_32_A: launch_tile<4, 2, 4>(A, rm, grid, st); break;
-            case TILE_32_B: launch_tile<4, 4, 2>(A, rm, grid, st); break;
+            case TILE_32_B: {
+                static const int cap = getenv("B200P_REGCAP") ? atoi(getenv("B200P_REGCAP")) : 168;
+                if (cap == 168) launch_tile<4, 4, 2, 168>(A, rm, grid, st);
+                else if (cap == 160) launch_tile<4, 4, 2, 160>(A, rm, grid, st);
+                else if (cap == 144) launch_tile<4, 4, 2, 144>(A, rm, grid, st);
+                else if (cap == 128) launch_tile<4, 4, 2, 128>(A, rm, grid, st);
+                else launch_tile<4, 4, 2>(A, rm, grid, st);
+                break;
+            }
             case TILE_32_C: launch_tile<4, 1, 8>(A, rm, grid, st); break;
+            case TILE_32_S: launch_tile_s<4, 4, 2, false>(A, rm, grid, st); break;
+            case TILE_32_T: launch_tile_s<4, 4, 2, true>(A, rm, grid, st); break;
+            case TILE_32_U: launch_tile_s<4, 2, 4, false>(A, rm, grid, st); break;
             case TILE_16: launch_tile<2, 4, 1>(A, rm, grid, st); break;
             case TILE_8: launch_tile<1, 2, 1>(A, rm, grid, st); break;
             default: {
@@ -630,8 +749,21 @@ static int launch_set_int(b200p_plan *pl, int *p, int n, int v, cudaStream_t st)
 }
 
 // build_hierarchy's data half (multigrid.py:249-260).
+static int pack_masks(b200p_plan *pl, const LevelHost &L, cudaStream_t st) {
+    if (!L.d_mtab) return 0;
+    LaunchScope sc(pl, st, KK_DOWN_MASK, (double)pl->F * L.nblocks * (32.0 * 32.0 + 4.0 * KT_THREADS));
+    pack_block_masks_kernel<<<dim3(L.nblocks, pl->F), KT_THREADS, 0, st>>>(
+        L.dev, L.d_mask, (size_t)L.info.height * L.info.width, L.d_mtab);
+    CU(cudaGetLastError());
+    return 0;
+}
+
 static int enqueue_hierarchy(b200p_plan *pl, cudaStream_t st) {
     const int nl = (int)pl->lev.size();
+    {
+        int rc = pack_masks(pl, pl->lev[0], st);
+        if (rc) return rc;
+    }
     for (int l = 0; l + 1 < nl; ++l) {
         const LevelHost &f = pl->lev[l];
         LevelHost &c = pl->lev[l + 1];
@@ -641,6 +773,10 @@ static int enqueue_hierarchy(b200p_plan *pl, cudaStream_t st) {
             downsample_mask_kernel<<<grid2x(c.info.width, c.info.height, pl->F), ST_THREADS, 0, st>>>(
                 f.d_mask, h, w, c.d_mask);
             CU(cudaGetLastError());
+        }
+        {
+            int rc = pack_masks(pl, c, st);
+            if (rc) return rc;
         }
         {
             LaunchScope sc(pl, st, KK_DOWN_VALUES, field_bytes(pl, f, 1.25, 1.25));
@@ -850,6 +986,15 @@ static int set_smem_attrs() {
                             cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(cudaFuncSetAttribute(oras_sweep_generic_kernel<false, 1>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+    // K2S keeps CG state in static shared memory: ask for the large carve-out so that
+    // 8 blocks per SM are resident
+    const int carve = cudaSharedmemCarveoutMaxShared;
+    CU(cudaFuncSetAttribute(oras_sweep_tile_s_kernel<4, 4, 2, true, false>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+    CU(cudaFuncSetAttribute(oras_sweep_tile_s_kernel<4, 4, 2, false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+    CU(cudaFuncSetAttribute(oras_sweep_tile_s_kernel<4, 4, 2, true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+    CU(cudaFuncSetAttribute(oras_sweep_tile_s_kernel<4, 4, 2, false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+    CU(cudaFuncSetAttribute(oras_sweep_tile_s_kernel<4, 2, 4, true, false>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+    CU(cudaFuncSetAttribute(oras_sweep_tile_s_kernel<4, 2, 4, false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     done = true;
     return 0;
 }
@@ -1070,6 +1215,11 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
                 L.fused_grid = sms * occ;
             }
         }
+        // K2T: the TMA box starts at x0 - 2 and needs a 16-byte aligned start: even block starts
+        bool xs_even = true;
+        for (int x : xs) xs_even = xs_even && (x % 2 == 0);
+        if (D.bw == 32 && D.bh == 32 && w % 2 == 0 && xs_even)
+            PTRY(dev_alloc(pl, &L.d_mtab, (size_t)pl->F * L.nblocks * KT_THREADS));
         if (l > 0) {
             PTRY(dev_alloc(pl, &L.d_mask, pl->F * plane));
             PTRY(dev_alloc(pl, &L.d_rhs, pl->P * plane));
@@ -1375,7 +1525,8 @@ int b200p_plan_oras_sweeps(b200p_plan *pl, int level, const double *d_b, double 
         force = -2;
     } else if (path >= 10) {
         const int t = path - 10;
-        const bool ok = (is32 && (t == TILE_32_A || t == TILE_32_B || t == TILE_32_C)) ||
+        const bool ok = (is32 && (t == TILE_32_A || t == TILE_32_B || t == TILE_32_C || t == TILE_32_S ||
+                                 t == TILE_32_T || t == TILE_32_U || t == TILE_32_TMA)) ||
                         (is16 && t == TILE_16) || (is8 && t == TILE_8);
         if (!ok) return fail_arg(B200P_ERR_UNSUPPORTED, "level %d is not eligible for tile variant %d", level, t);
         force = t;

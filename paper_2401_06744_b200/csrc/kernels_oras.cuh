@@ -21,6 +21,10 @@ namespace b200p {
 
 constexpr int ST_THREADS_COMBINE = 256;
 
+#ifndef B200P_PACKED_RED
+#define B200P_PACKED_RED 0
+#endif
+
 struct SweepArgs {
     LevelDev L;
     const double *u;       // (P, h, w) current iterate
@@ -77,6 +81,37 @@ struct TileCG {
 
     // Three sums in ONE butterfly / one cross-warp exchange (a single latency chain).
     __device__ __forceinline__ void group_sum3(double &a, double &b, double &c) {
+#if B200P_PACKED_RED
+        // Packed butterfly: shuffles go through the LSU data pipe, which this kernel loads
+        // heavily (ncu: l1tex__data_pipe_lsu_wavefronts), so the three sums share one
+        // butterfly instead of running three.  Stage 16 folds a and b into one register
+        // (lower half-warp keeps a, upper keeps b), stage 8 folds c in (lanes with bit 3 keep
+        // c), stages 4,2,1 finish: 6 exchanges instead of 15.  Lane 0 ends with a, lane 16 with
+        // b, lane 8 with c; summation order is fixed, results are deterministic.
+        {
+            const bool hi = lane & 16;
+            const double send = hi ? a : b;
+            double keep = hi ? b : a;
+            keep += __shfl_xor_sync(FULL_MASK, send, 16);
+            c += __shfl_xor_sync(FULL_MASK, c, 16);
+            const bool h8 = lane & 8;
+            const double send2 = h8 ? keep : c;
+            double w = h8 ? c : keep;
+            w += __shfl_xor_sync(FULL_MASK, send2, 8);
+            w += __shfl_xor_sync(FULL_MASK, w, 4);
+            w += __shfl_xor_sync(FULL_MASK, w, 2);
+            w += __shfl_xor_sync(FULL_MASK, w, 1);
+            if (NWARP == 1) {
+                a = __shfl_sync(FULL_MASK, w, 0);
+                b = __shfl_sync(FULL_MASK, w, 16);
+                c = __shfl_sync(FULL_MASK, w, 8);
+                return;
+            }
+            if ((lane & 7) == 0 && lane < 24)
+                red[slot * NWARP * 3 + wg * 3 + (lane == 0 ? 0 : (lane == 16 ? 1 : 2))] = w;
+        }
+        double *s = red + slot * NWARP * 3;
+#else
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             a += __shfl_xor_sync(FULL_MASK, a, o);
@@ -90,6 +125,7 @@ struct TileCG {
             s[wg * 3 + 1] = b;
             s[wg * 3 + 2] = c;
         }
+#endif
         group_bar();
         a = b = c = 0.0;
 #pragma unroll
@@ -356,11 +392,11 @@ __device__ __forceinline__ void tile_block_solve(const SweepArgs &A, int p, int 
     }
 }
 
-#ifndef B200P_TILE_MINB
-#define B200P_TILE_MINB 1
-#endif
-template <int TW, int TH, int NWARP, bool RM>
-__global__ void __launch_bounds__(NWARP * 32, B200P_TILE_MINB)
+// REGCAP: register cap per thread.  The 32x32 tile needs 194 registers uncapped, which the
+// allocation granularity (512 per warp) turns into 4 resident blocks per SM; 168 gives 5,
+// 160 gives 6 at the price of a few spilled words.
+template <int TW, int TH, int NWARP, bool RM, int REGCAP = 255>
+__global__ void __launch_bounds__(NWARP * 32) __maxnreg__(REGCAP)
 oras_sweep_tile_kernel(const SweepArgs A) {
     __shared__ TileSmem<TW, TH, NWARP> sm;
     const int p = blockIdx.y;
@@ -370,6 +406,254 @@ oras_sweep_tile_kernel(const SweepArgs A) {
     const int blk = blockIdx.x;
     double *out = A.scratch + ((size_t)p * A.L.nblocks + blk) * (8 * TW * 4 * TH * NWARP);
     tile_block_solve<TW, TH, NWARP, RM, false>(A, p, blk, 0, threadIdx.x >> 5, sm, A.eta * rs_g, out);
+}
+
+// ------------------------------------------------------------------ K2S ---
+// Same block solve with the CG state split between registers and shared memory:
+// the search direction p (needed by the neighbours through shuffles) and, unless
+// SR, the residual r stay in registers; the iterate v and the operator image q
+// = A_i p (both touched once per CG step, never exchanged) live in shared memory.
+// The register tile of K2 holds 4 arrays x 16 px x 2 regs = 128 registers of
+// pure state, which caps residency at 4 blocks per SM and leaves the FP64 pipe
+// waiting on the latency of the reductions; K2S fits 8 blocks per SM.
+// Thread t owns double2 slot [k][t] (k = 2*row + half): 16-byte accesses, a
+// warp reads 512 contiguous bytes, no bank conflicts, no hazards between threads.
+template <int TW, int TH, int NWARP, bool SR>
+struct TileSmemS {
+    static constexpr int NT = NWARP * 32, K = TH * TW / 2;
+    double2 v[K][NT];
+    double2 q[K][NT];
+    double2 r[SR ? K : 1][SR ? NT : 1];
+    double xrow[NWARP > 1 ? NWARP * 2 * 8 * TW : 1];
+    double red[2 * NWARP * 3];
+};
+
+template <int TW, int TH, int NWARP, bool RM, bool SR>
+__device__ __forceinline__ void tile_block_solve_s(const SweepArgs &A, int p, int blk,
+                                                   TileSmemS<TW, TH, NWARP, SR> &sm, double target,
+                                                   double *__restrict__ out) {
+    static_assert(TW == 4, "K2S stores rows as two double2");
+    using CG = TileCG<TW, TH, NWARP>;
+    constexpr int BW = CG::BW, BH = CG::BH;
+    const LevelDev &L = A.L;
+    const int iy = blk / L.nx, ix = blk - iy * L.nx;
+    const int x0 = L.xs[ix], y0 = L.ys[iy];
+    const int W = L.w, H = L.h;
+    const int tid = threadIdx.x;
+
+    CG cg;
+    cg.lane = tid & 31;
+    cg.wg = tid >> 5;
+    cg.bar_id = 1;
+    cg.lx = cg.lane & 7;
+    cg.ly = cg.lane >> 3;
+    cg.xrow = sm.xrow;
+    cg.red = sm.red;
+    cg.slot = 0;
+    cg.eL = cg.lx == 0;
+    cg.eR = cg.lx == 7;
+    cg.eT = cg.wg == 0 && cg.ly == 0;
+    cg.eB = cg.wg == NWARP - 1 && cg.ly == 3;
+    const double g_in = 1.0 - L.robin / L.hinv2;  // 1 - alpha*h
+    cg.gL = x0 > 0 ? g_in : 1.0;
+    cg.gR = x0 + BW < W ? g_in : 1.0;
+    cg.gT = y0 > 0 ? g_in : 1.0;
+    cg.gB = y0 + BH < H ? g_in : 1.0;
+
+    const int bx = cg.lx * TW, by = (cg.wg * 4 + cg.ly) * TH;
+    const int gx0 = x0 + bx, gy0 = y0 + by;
+    const double *up = A.u + (size_t)p * A.plane;
+    const double *bp = A.b + (size_t)p * A.plane;
+    const uint8_t *mp = A.mask + (size_t)(p / A.channels) * A.plane;
+    const double hinv2 = L.hinv2;
+
+    // ---- gather: global residual g = b - A u on the tile (core.py:100-110)
+    double r[TH][TW];
+    unsigned mbits = 0;
+    {
+        double uc[TH + 2][TW + 2];
+#pragma unroll
+        for (int j = 0; j < TH + 2; ++j) {
+            const int gy = gy0 + j - 1;
+#pragma unroll
+            for (int i = 0; i < TW + 2; ++i) {
+                const int gx = gx0 + i - 1;
+                const bool corner = (j == 0 || j == TH + 1) && (i == 0 || i == TW + 1);
+                const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+                uc[j][i] = (!corner && in) ? up[(size_t)gy * W + gx] : 0.0;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < TH; ++j) {
+            const int gy = gy0 + j;
+            const double cy = 4.0 - (gy == 0 ? 1.0 : 0.0) - (gy == H - 1 ? 1.0 : 0.0);
+#pragma unroll
+            for (int i = 0; i < TW; ++i) {
+                const int gx = gx0 + i;
+                const size_t gi = (size_t)gy * W + gx;
+                const bool m = mp[gi] != 0;
+                if (m) mbits |= 1u << (j * TW + i);
+                const double cnt = cy - (gx == 0 ? 1.0 : 0.0) - (gx == W - 1 ? 1.0 : 0.0);
+                const double s = ((uc[j][i + 1] + uc[j + 2][i + 1]) + uc[j + 1][i]) + uc[j + 1][i + 2];
+                const double au = s * (-hinv2) + (cnt * hinv2) * uc[j + 1][i + 1];
+                double bb;
+                if (RM) bb = m ? bp[gi] : 0.0; else bb = bp[gi];
+                r[j][i] = m ? (bb - uc[j + 1][i + 1]) : (bb - au);
+            }
+        }
+    }
+    cg.mbits = mbits;
+
+    // ---- local start: v0 = where(mask, g, 0), r0 = g - A_i v0 (solvers.py:331-333)
+    double pc[TH][TW];
+    const bool general = A.mflag[p] != 0;
+    if (general) {
+        double q[TH][TW];
+#pragma unroll
+        for (int j = 0; j < TH; ++j)
+#pragma unroll
+            for (int i = 0; i < TW; ++i) {
+                const bool m = (mbits >> (j * TW + i)) & 1u;
+                pc[j][i] = m ? r[j][i] : 0.0;
+            }
+#pragma unroll
+        for (int j = 0; j < TH; ++j) {
+            sm.v[2 * j][tid] = make_double2(pc[j][0], pc[j][1]);
+            sm.v[2 * j + 1][tid] = make_double2(pc[j][2], pc[j][3]);
+        }
+        cg.apply(pc, q);
+#pragma unroll
+        for (int j = 0; j < TH; ++j)
+#pragma unroll
+            for (int i = 0; i < TW; ++i) {
+                const bool m = (mbits >> (j * TW + i)) & 1u;
+                r[j][i] = m ? 0.0 : fma(-hinv2, q[j][i], r[j][i]);
+            }
+    }
+    double rs_k = cg.group_sum(tile_dot<TW, TH>(r, r));
+    bool have_v = general;  // v == 0 is not materialised before the first CG step
+
+    if (rs_k > target) {  // solvers.py:336 (strict)
+#pragma unroll
+        for (int j = 0; j < TH; ++j)
+#pragma unroll
+            for (int i = 0; i < TW; ++i) pc[j][i] = r[j][i];
+        if (SR) {
+#pragma unroll
+            for (int j = 0; j < TH; ++j) {
+                sm.r[2 * j][tid] = make_double2(r[j][0], r[j][1]);
+                sm.r[2 * j + 1][tid] = make_double2(r[j][2], r[j][3]);
+            }
+        }
+        double inv_rs = 1.0 / rs_k;
+        for (int it = 0; it < A.max_iters; ++it) {
+            double d_pq, d_rq, d_qq;
+            {
+                double q[TH][TW];
+                cg.apply(pc, q);
+                if (SR) {
+#pragma unroll
+                    for (int j = 0; j < TH; ++j) {
+                        const double2 a0 = sm.r[2 * j][tid], a1 = sm.r[2 * j + 1][tid];
+                        r[j][0] = a0.x; r[j][1] = a0.y; r[j][2] = a1.x; r[j][3] = a1.y;
+                    }
+                }
+                d_pq = tile_dot<TW, TH>(pc, q);
+                d_rq = tile_dot<TW, TH>(r, q);
+                d_qq = tile_dot<TW, TH>(q, q);
+#pragma unroll
+                for (int j = 0; j < TH; ++j) {
+                    sm.q[2 * j][tid] = make_double2(q[j][0], q[j][1]);
+                    sm.q[2 * j + 1][tid] = make_double2(q[j][2], q[j][3]);
+                }
+            }
+            cg.group_sum3(d_pq, d_rq, d_qq);
+            const double pq = hinv2 * d_pq;
+            const bool ok = pq > 0.0;                 // solvers.py:348
+            const double a = ok ? rs_k / pq : 0.0;    // :349-350
+            const double ah = a * hinv2;
+            const double rs_new = fma(ah * ah, d_qq, fma(-2.0 * ah, d_rq, rs_k));
+            const bool last = rs_new <= target || !ok;  // :354
+            const double beta = rs_new * inv_rs;
+#pragma unroll
+            for (int j = 0; j < TH; ++j) {
+                // v += a p
+                double2 v0 = make_double2(0.0, 0.0), v1 = v0;
+                if (have_v) {
+                    v0 = sm.v[2 * j][tid];
+                    v1 = sm.v[2 * j + 1][tid];
+                }
+                v0.x = fma(a, pc[j][0], v0.x); v0.y = fma(a, pc[j][1], v0.y);
+                v1.x = fma(a, pc[j][2], v1.x); v1.y = fma(a, pc[j][3], v1.y);
+                sm.v[2 * j][tid] = v0;
+                sm.v[2 * j + 1][tid] = v1;
+                if (!last) {
+                    // r -= a q ; p = beta p + r
+                    const double2 q0 = sm.q[2 * j][tid], q1 = sm.q[2 * j + 1][tid];
+                    double2 r0, r1;
+                    if (SR) {
+                        r0 = sm.r[2 * j][tid];
+                        r1 = sm.r[2 * j + 1][tid];
+                    } else {
+                        r0 = make_double2(r[j][0], r[j][1]);
+                        r1 = make_double2(r[j][2], r[j][3]);
+                    }
+                    r0.x = fma(-ah, q0.x, r0.x); r0.y = fma(-ah, q0.y, r0.y);
+                    r1.x = fma(-ah, q1.x, r1.x); r1.y = fma(-ah, q1.y, r1.y);
+                    if (SR) {
+                        sm.r[2 * j][tid] = r0;
+                        sm.r[2 * j + 1][tid] = r1;
+                    } else {
+                        r[j][0] = r0.x; r[j][1] = r0.y; r[j][2] = r1.x; r[j][3] = r1.y;
+                    }
+                    pc[j][0] = fma(beta, pc[j][0], r0.x); pc[j][1] = fma(beta, pc[j][1], r0.y);
+                    pc[j][2] = fma(beta, pc[j][2], r1.x); pc[j][3] = fma(beta, pc[j][3], r1.y);
+                }
+            }
+            have_v = true;
+            if (last) break;
+            rs_k = rs_new;
+            inv_rs = 1.0 / rs_k;
+        }
+    }
+
+    // ---- weighted correction (v * wy) * wx (solvers.py:309-310)
+    double wxv[TW];
+#pragma unroll
+    for (int i = 0; i < TW; ++i) wxv[i] = L.wx[ix * BW + bx + i];
+#pragma unroll
+    for (int j = 0; j < TH; ++j) {
+        const double wyv = L.wy[iy * BH + by + j];
+        double *row = out + (by + j) * BW + bx;
+        double2 v0 = make_double2(0.0, 0.0), v1 = v0;
+        if (have_v) {
+            v0 = sm.v[2 * j][tid];
+            v1 = sm.v[2 * j + 1][tid];
+        }
+        double2 o0, o1;
+        o0.x = (v0.x * wyv) * wxv[0];
+        o0.y = (v0.y * wyv) * wxv[1];
+        o1.x = (v1.x * wyv) * wxv[2];
+        o1.y = (v1.y * wyv) * wxv[3];
+        *reinterpret_cast<double2 *>(row) = o0;
+        *reinterpret_cast<double2 *>(row + 2) = o1;
+    }
+}
+
+#ifndef B200P_TILES_MINB
+#define B200P_TILES_MINB 8
+#endif
+template <int TW, int TH, int NWARP, bool RM, bool SR>
+__global__ void __launch_bounds__(NWARP * 32, B200P_TILES_MINB)
+oras_sweep_tile_s_kernel(const SweepArgs A) {
+    __shared__ __align__(16) TileSmemS<TW, TH, NWARP, SR> sm;
+    const int p = blockIdx.y;
+    if (A.pred && !A.pred[p]) return;
+    const double rs_g = A.rs[p];
+    if (rs_g == 0.0) return;  // oras_sweeps exit, solvers.py:420
+    const int blk = blockIdx.x;
+    double *out = A.scratch + ((size_t)p * A.L.nblocks + blk) * (8 * TW * 4 * TH * NWARP);
+    tile_block_solve_s<TW, TH, NWARP, RM, SR>(A, p, blk, sm, A.eta * rs_g, out);
 }
 
 // ------------------------------------------------------------------ K2F ---

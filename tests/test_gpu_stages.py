@@ -194,6 +194,25 @@ def test_oras_sweeps_general_start_and_stop_norm(rng):
         np.testing.assert_allclose(u_g, u_o, rtol=0, atol=1e-8)
 
 
+@pytest.mark.parametrize("variant", [1, 4, 5, 6, 7, 8, 9])
+def test_tile32_variants_match_oracle(variant, rng):
+    """Every 32x32 register/shared-memory tile variant of K2 (path 10 + id), regular start and
+    the general start (u violating the interpolation condition)."""
+    w, h, bs, ov = 150, 100, 32, 6
+    m, k = oracle.seeded_problem(w, h, 0.05, 21)
+    part = bp.build_partition(w, h, bs, ov)
+    blocks = bp.BlockSolver(m, 1.0, part, bp.build_weights(part), 0.5)
+    b = np.where(m, k[0], 0.0)
+    for b_, u0 in ((b, b.copy()), (rng.normal(size=(h, w)) * 10, rng.normal(size=(h, w)) * 10)):
+        u_o, u_g = u0.copy(), u0.copy()
+        s_o, rn_o = oracle.oras_sweeps(m, 1.0, bs, ov, 0.5, b_, u_o, max_sweeps=3)
+        s_g, rn_g = bp.oras_sweeps(bp.StencilOperator(m), blocks, b_, u_g, max_sweeps=3,
+                                   stop_norm=0.0, eta=1e-5, local_max_iters=None, path=10 + variant)
+        assert s_g == s_o
+        assert rn_g == pytest.approx(rn_o, rel=1e-8)
+        np.testing.assert_allclose(u_g, u_o, rtol=0, atol=1e-8)
+
+
 def test_oras_zero_residual_exit():
     """rs == 0 exits without sweeps or NaNs (solvers.py:420; all-mask coarse levels)."""
     m = np.ones((40, 40), bool)
