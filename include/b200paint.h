@@ -142,6 +142,16 @@ int b200p_plan_profile_get(b200p_plan *plan, int kind, double *ms, int64_t *laun
 int b200p_solve(b200p_plan *plan, const uint8_t *d_mask, const double *d_known, double *d_out,
                 b200p_report *h_reports, void *stream);
 
+/* The same solve without the host in the loop: the whole of fmg_solve is ONE CUDA graph
+ * (front half -> WHILE node whose body is a V-cycle + convergence check,
+ * multigrid.py:474-479, the loop condition is set on the device -> report gather into a
+ * pinned host record).  b200p_solve_async only enqueues on `stream`; b200p_solve_wait
+ * synchronises that stream and fills h_reports (may be NULL).  One solve may be pending
+ * per plan.  b200p_solve == b200p_solve_async + b200p_solve_wait. */
+int b200p_solve_async(b200p_plan *plan, const uint8_t *d_mask, const double *d_known, double *d_out,
+                      void *stream);
+int b200p_solve_wait(b200p_plan *plan, b200p_report *h_reports);
+
 /* Same through HOST buffers: H2D of mask+known, solve, D2H of the result.
  * Returns B200P_ERR_EMPTY_MASK if any frame's mask is all zero. */
 int b200p_solve_host(b200p_plan *plan, const uint8_t *h_mask, const double *h_known, double *h_out,
@@ -152,6 +162,14 @@ int b200p_solve_host(b200p_plan *plan, const uint8_t *h_mask, const double *h_kn
  * [0,255] on the device.  h_out_u8 (frames,C,H,W). */
 int b200p_solve_host_u8(b200p_plan *plan, const uint8_t *h_mask, const uint8_t *h_known_u8,
                         uint8_t *h_out_u8, b200p_report *h_reports);
+
+/* Asynchronous forms of the two host entry points: copies and solve are enqueued on the
+ * plan's own stream and the call returns; b200p_solve_wait completes them.  The host buffers
+ * must stay valid (and should be pinned for the copies to overlap other plans' kernels)
+ * until the wait returns.  This is what the frame pipeline drives, one plan per lane. */
+int b200p_solve_host_async(b200p_plan *plan, const uint8_t *h_mask, const double *h_known, double *h_out);
+int b200p_solve_host_u8_async(b200p_plan *plan, const uint8_t *h_mask, const uint8_t *h_known_u8,
+                              uint8_t *h_out_u8);
 
 /* ---- stage entry points (A/B tests against the reference functions) ---- */
 

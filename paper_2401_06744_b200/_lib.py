@@ -102,7 +102,11 @@ SIGNATURES = {
     "b200p_plan_profile_name": (C.c_char_p, [_I]),
     "b200p_plan_profile_get": (_I, [_VP, _I, C.POINTER(_D), C.POINTER(_I64), C.POINTER(_D)]),
     "b200p_solve": (_I, [_VP, _VP, _VP, _VP, _VP, _VP]),
+    "b200p_solve_async": (_I, [_VP, _VP, _VP, _VP, _VP]),
+    "b200p_solve_wait": (_I, [_VP, _VP]),
     "b200p_solve_host": (_I, [_VP, _VP, _VP, _VP, _VP]),
+    "b200p_solve_host_async": (_I, [_VP, _VP, _VP, _VP]),
+    "b200p_solve_host_u8_async": (_I, [_VP, _VP, _VP, _VP]),
     "b200p_solve_host_u8": (_I, [_VP, _VP, _VP, _VP, _VP]),
     "b200p_plan_build_hierarchy": (_I, [_VP, _VP, _VP, _VP]),
     "b200p_plan_level_ptrs": (_I, [_VP, _I, C.POINTER(_VP), C.POINTER(_VP)]),

@@ -181,6 +181,12 @@ struct ProfEvent {
     cudaEvent_t a, b;
 };
 
+// SolveReport fields of all problems into one (mapped, pinned) host record.
+struct ReportPack {
+    int *cycles, *units, *histlen;
+    double *baseline, *rel, *hist;
+};
+
 struct GraphSlot {
     cudaGraphExec_t exec = nullptr;
     const void *k0 = nullptr, *k1 = nullptr, *k2 = nullptr;  // pointers baked into the graph
@@ -213,6 +219,16 @@ struct b200p_plan {
     int *d_gate = nullptr, *d_sweeps = nullptr;  // stage API (oras_sweeps with stop_norm)
     double *d_rn = nullptr;
     int *h_any = nullptr;  // pinned
+    // single-graph solve: WHILE node handle, pinned report record, pending state
+    cudaGraphConditionalHandle cond = 0;
+    bool cond_capture = false;   // control kernels drive the WHILE node (set during capture)
+    void *h_rep = nullptr;       // mapped pinned host block behind `rep`
+    ReportPack rep = {};
+    cudaStream_t aux_stream = nullptr;  // captures the WHILE body
+    cudaStream_t pending_stream = nullptr;
+    bool pending = false;
+    GraphSlot g_solve;
+    int64_t cycle_kernels = 0;   // kernel nodes of one WHILE body pass
     // staging for the host entry points
     uint8_t *d_in_mask = nullptr;
     double *d_in_known = nullptr, *d_out = nullptr;
@@ -297,44 +313,69 @@ static void prof_collect(b200p_plan *pl) {
 // stage 2: check after a V-cycle          (cycles+1, rel, history, active)
 __global__ void fmg_control_kernel(int P, int stage, const double *rs, double tol, int cycles_max,
                                    double *baseline, double *denom, double *rel, double *hist,
-                                   int *histlen, int *active, int *cycles, int *units, int *any) {
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= P) return;
-    const double rn = sqrt(rs[p]);
-    if (stage == 0) {
-        baseline[p] = rn;
-        units[p] = 0;
-        cycles[p] = 0;
-        histlen[p] = 0;
-        active[p] = 1;
-        return;
-    }
-    if (stage == 1) {
-        const double base = baseline[p];
-        const double d = base > 0.0 ? base : (rn > 0.0 ? rn : 1.0);
-        denom[p] = d;
-        const double r = rn / d;
+                                   int *histlen, int *active, int *cycles, int *units, int *any,
+                                   int use_cond, cudaGraphConditionalHandle cond) {
+    // one CTA, problems strided over its threads: the "is any problem still active" verdict is
+    // a CTA-wide OR, written to `any` (eager host loop) or to the WHILE node of the solve graph
+    int mine = 0;
+    for (int p = threadIdx.x; p < P; p += blockDim.x) {
+        const double rn = sqrt(rs[p]);
+        if (stage == 0) {
+            baseline[p] = rn;
+            units[p] = 0;
+            cycles[p] = 0;
+            histlen[p] = 0;
+            active[p] = 1;
+            continue;
+        }
+        if (stage == 1) {
+            const double base = baseline[p];
+            const double d = base > 0.0 ? base : (rn > 0.0 ? rn : 1.0);
+            denom[p] = d;
+            const double r = rn / d;
+            rel[p] = r;
+            hist[(size_t)p * B200P_MAX_HISTORY] = r;
+            histlen[p] = 1;
+            const int act = (r > tol && 0 < cycles_max) ? 1 : 0;
+            active[p] = act;
+            mine |= act;
+            continue;
+        }
+        if (!active[p]) continue;
+        const int c = cycles[p] + 1;
+        cycles[p] = c;
+        const double r = rn / denom[p];
         rel[p] = r;
-        hist[(size_t)p * B200P_MAX_HISTORY] = r;
-        histlen[p] = 1;
-        const int act = (r > tol && 0 < cycles_max) ? 1 : 0;
+        const int hl = histlen[p];
+        if (hl < B200P_MAX_HISTORY) {
+            hist[(size_t)p * B200P_MAX_HISTORY + hl] = r;
+            histlen[p] = hl + 1;
+        }
+        const int act = (r > tol && c < cycles_max) ? 1 : 0;
         active[p] = act;
-        if (act) atomicOr(any, 1);
-        return;
+        mine |= act;
     }
-    if (!active[p]) return;
-    const int c = cycles[p] + 1;
-    cycles[p] = c;
-    const double r = rn / denom[p];
-    rel[p] = r;
-    const int hl = histlen[p];
-    if (hl < B200P_MAX_HISTORY) {
-        hist[(size_t)p * B200P_MAX_HISTORY + hl] = r;
-        histlen[p] = hl + 1;
+    if (stage == 0) return;
+    const int all = __syncthreads_or(mine);
+    if (threadIdx.x == 0) {
+        *any = all;
+        if (use_cond) cudaGraphSetConditional(cond, all ? 1u : 0u);
     }
-    const int act = (r > tol && c < cycles_max) ? 1 : 0;
-    active[p] = act;
-    if (act) atomicOr(any, 1);
+}
+
+// SolveReport fields of all problems into one (mapped, pinned) host record.
+__global__ void pack_reports_kernel(int P, const int *cycles, const int *units, const int *histlen,
+                                    const double *baseline, const double *rel, const double *hist,
+                                    ReportPack out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < P) {
+        out.cycles[i] = cycles[i];
+        out.units[i] = units[i];
+        out.histlen[i] = histlen[i];
+        out.baseline[i] = baseline[i];
+        out.rel[i] = rel[i];
+    }
+    if (i < P * B200P_MAX_HISTORY) out.hist[i] = hist[i];
 }
 
 __global__ void set_int_kernel(int *p, int n, int v) {
@@ -734,9 +775,10 @@ static int launch_coarse(b200p_plan *pl, const LevelHost &L, double *u, const do
 
 static int launch_control(b200p_plan *pl, int stage, cudaStream_t st) {
     LaunchScope sc(pl, st, KK_CONTROL, 0.0);
-    fmg_control_kernel<<<(pl->P + 127) / 128, 128, 0, st>>>(
+    fmg_control_kernel<<<1, 128, 0, st>>>(
         pl->P, stage, pl->d_rs, pl->cfg.tol_rel, pl->cfg.v_cycles_max, pl->d_baseline, pl->d_denom,
-        pl->d_rel, pl->d_hist, pl->d_histlen, pl->d_active, pl->d_cycles, pl->d_units, pl->d_any);
+        pl->d_rel, pl->d_hist, pl->d_histlen, pl->d_active, pl->d_cycles, pl->d_units, pl->d_any,
+        pl->cond_capture ? 1 : 0, pl->cond);
     CU(cudaGetLastError());
     return 0;
 }
@@ -916,9 +958,8 @@ static int enqueue_front(b200p_plan *pl, double *d_out, cudaStream_t st) {
     if ((rc = launch_control(pl, 0, st))) return rc;
     if ((rc = enqueue_cascade(pl, d_out, st))) return rc;
     if ((rc = launch_norm(pl, L0, d_out, L0.d_rhs, false, true, nullptr, st))) return rc;
-    if ((rc = launch_set_int(pl, pl->d_any, 1, 0, st))) return rc;
     if ((rc = launch_control(pl, 1, st))) return rc;
-    CU(cudaMemcpyAsync(pl->h_any, pl->d_any, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (!pl->cond_capture) CU(cudaMemcpyAsync(pl->h_any, pl->d_any, sizeof(int), cudaMemcpyDeviceToHost, st));
     return 0;
 }
 
@@ -931,9 +972,8 @@ static int enqueue_cycle(b200p_plan *pl, double *d_out, cudaStream_t st) {
                             (int)pl->lev.size() > 1, st);
     if (rc) return rc;
     if ((rc = launch_norm(pl, L0, d_out, L0.d_rhs, false, true, pl->d_active, st))) return rc;
-    if ((rc = launch_set_int(pl, pl->d_any, 1, 0, st))) return rc;
     if ((rc = launch_control(pl, 2, st))) return rc;
-    CU(cudaMemcpyAsync(pl->h_any, pl->d_any, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (!pl->cond_capture) CU(cudaMemcpyAsync(pl->h_any, pl->d_any, sizeof(int), cudaMemcpyDeviceToHost, st));
     return 0;
 }
 
@@ -1092,6 +1132,9 @@ void b200p_plan_destroy(b200p_plan *pl) {
     }
     if (pl->g_front.exec) cudaGraphExecDestroy(pl->g_front.exec);
     if (pl->g_cycle.exec) cudaGraphExecDestroy(pl->g_cycle.exec);
+    if (pl->g_solve.exec) cudaGraphExecDestroy(pl->g_solve.exec);
+    if (pl->h_rep) cudaFreeHost(pl->h_rep);
+    if (pl->aux_stream) cudaStreamDestroy(pl->aux_stream);
     for (void *p : pl->owned) cudaFree(p);
     if (pl->h_any) cudaFreeHost(pl->h_any);
     if (pl->h_pin) cudaFreeHost(pl->h_pin);
@@ -1313,65 +1356,185 @@ int b200p_plan_profile_get(b200p_plan *pl, int kind, double *ms, int64_t *launch
     return 0;
 }
 
-static int collect_reports(b200p_plan *pl, b200p_report *h_reports, cudaStream_t st) {
-    const int P = pl->P;
-    std::vector<int> cycles(P), units(P), histlen(P);
-    std::vector<double> base(P), rel(P), hist((size_t)P * B200P_MAX_HISTORY);
-    CU(cudaMemcpyAsync(cycles.data(), pl->d_cycles, P * sizeof(int), cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(units.data(), pl->d_units, P * sizeof(int), cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(histlen.data(), pl->d_histlen, P * sizeof(int), cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(base.data(), pl->d_baseline, P * sizeof(double), cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(rel.data(), pl->d_rel, P * sizeof(double), cudaMemcpyDeviceToHost, st));
-    CU(cudaMemcpyAsync(hist.data(), pl->d_hist, hist.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    for (int p = 0; p < P; ++p) {
-        b200p_report &r = h_reports[p];
-        memset(&r, 0, sizeof r);
-        r.iterations = cycles[p];
-        r.fine_smoother_iterations = units[p];
-        r.history_len = histlen[p];
-        r.final_rel_residual = rel[p];
-        r.baseline_residual = base[p];
-        r.init_residual = base[p];
-        r.converged = rel[p] <= pl->cfg.tol_rel;
-        memcpy(r.history, &hist[(size_t)p * B200P_MAX_HISTORY], sizeof(double) * B200P_MAX_HISTORY);
-    }
+static int ensure_report_block(b200p_plan *pl) {
+    if (pl->h_rep) return 0;
+    const size_t P = pl->P;
+    const size_t bytes = P * (3 * sizeof(int) + 2 * sizeof(double)) + P * B200P_MAX_HISTORY * sizeof(double) + 64;
+    CU(cudaHostAlloc(&pl->h_rep, bytes, cudaHostAllocMapped));
+    memset(pl->h_rep, 0, bytes);
+    // doubles first (alignment), then the ints
+    double *d = reinterpret_cast<double *>(pl->h_rep);
+    pl->rep.hist = d;
+    pl->rep.baseline = d + P * B200P_MAX_HISTORY;
+    pl->rep.rel = pl->rep.baseline + P;
+    int *i = reinterpret_cast<int *>(pl->rep.rel + P);
+    pl->rep.cycles = i;
+    pl->rep.units = i + P;
+    pl->rep.histlen = i + 2 * P;
     return 0;
 }
 
-int b200p_solve(b200p_plan *pl, const uint8_t *d_mask, const double *d_known, double *d_out,
-                b200p_report *h_reports, void *stream) {
+// Device-side gather of the report fields into the mapped host record (no copy engine involved,
+// so a lane's reports never queue behind another lane's bulk transfers).
+static int enqueue_reports(b200p_plan *pl, cudaStream_t st) {
+    int rc = ensure_report_block(pl);
+    if (rc) return rc;
+    LaunchScope sc(pl, st, KK_CONTROL, 0.0);
+    const int n = pl->P * B200P_MAX_HISTORY;
+    pack_reports_kernel<<<(n + 255) / 256, 256, 0, st>>>(pl->P, pl->d_cycles, pl->d_units, pl->d_histlen,
+                                                        pl->d_baseline, pl->d_rel, pl->d_hist, pl->rep);
+    CU(cudaGetLastError());
+    return 0;
+}
+
+static void read_reports(b200p_plan *pl, b200p_report *h_reports) {
+    for (int p = 0; p < pl->P; ++p) {
+        b200p_report &r = h_reports[p];
+        memset(&r, 0, sizeof r);
+        r.iterations = pl->rep.cycles[p];
+        r.fine_smoother_iterations = pl->rep.units[p];
+        r.history_len = pl->rep.histlen[p];
+        r.final_rel_residual = pl->rep.rel[p];
+        r.baseline_residual = pl->rep.baseline[p];
+        r.init_residual = pl->rep.baseline[p];
+        r.converged = pl->rep.rel[p] <= pl->cfg.tol_rel;
+        memcpy(r.history, &pl->rep.hist[(size_t)p * B200P_MAX_HISTORY], sizeof(double) * B200P_MAX_HISTORY);
+    }
+}
+
+// The whole of fmg_solve as ONE graph: front (hierarchy, baseline, cascade, first check) ->
+// WHILE node whose body is one V-cycle + check (multigrid.py:474-479; the control kernel sets
+// the loop condition on the device) -> report gather.  No host round trip inside a solve.
+static int launch_solve_graph(b200p_plan *pl, const uint8_t *d_mask, const double *d_known, double *d_out,
+                              cudaStream_t st) {
+    GraphSlot &slot = pl->g_solve;
+    if (!slot.exec || slot.k0 != d_mask || slot.k1 != d_known || slot.k2 != d_out) {
+        if (slot.exec) {
+            cudaGraphExecDestroy(slot.exec);
+            slot.exec = nullptr;
+        }
+        int rc = ensure_report_block(pl);
+        if (rc) return rc;
+        if (!pl->aux_stream) CU(cudaStreamCreateWithFlags(&pl->aux_stream, cudaStreamNonBlocking));
+        slot.kernels = 0;
+        pl->cycle_kernels = 0;
+        cudaGraph_t g = nullptr, body = nullptr, tmp = nullptr;
+        cudaStreamCaptureStatus cs;
+        const cudaGraphNode_t *deps = nullptr;
+        size_t ndeps = 0;
+        CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        pl->cond_capture = true;
+        rc = 0;
+        cudaError_t e = cudaStreamGetCaptureInfo_v2(st, &cs, nullptr, &g, &deps, &ndeps);
+        if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&pl->cond, g, 0, cudaGraphCondAssignDefault);
+        if (e == cudaSuccess) {
+            pl->launch_sink = &slot.kernels;
+            rc = enqueue_front(pl, d_out, st);
+        }
+        cudaGraphNode_t node = nullptr;
+        if (e == cudaSuccess && !rc) e = cudaStreamGetCaptureInfo_v2(st, &cs, nullptr, &g, &deps, &ndeps);
+        if (e == cudaSuccess && !rc) {
+            cudaGraphNodeParams np = {};
+            np.type = cudaGraphNodeTypeConditional;
+            np.conditional.handle = pl->cond;
+            np.conditional.type = cudaGraphCondTypeWhile;
+            np.conditional.size = 1;
+            e = cudaGraphAddNode(&node, g, deps, ndeps, &np);
+            if (e == cudaSuccess) body = np.conditional.phGraph_out[0];
+        }
+        if (e == cudaSuccess && !rc)
+            e = cudaStreamBeginCaptureToGraph(pl->aux_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+        if (e == cudaSuccess && !rc) {
+            pl->launch_sink = &pl->cycle_kernels;
+            rc = enqueue_cycle(pl, d_out, pl->aux_stream);
+            cudaError_t e2 = cudaStreamEndCapture(pl->aux_stream, &tmp);
+            if (e == cudaSuccess) e = e2;
+        }
+        if (e == cudaSuccess && !rc) e = cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies);
+        if (e == cudaSuccess && !rc) {
+            pl->launch_sink = &slot.kernels;
+            rc = enqueue_reports(pl, st);
+        }
+        pl->launch_sink = nullptr;
+        pl->cond_capture = false;
+        cudaGraph_t full = nullptr;
+        cudaError_t e3 = cudaStreamEndCapture(st, &full);
+        if (rc) {
+            if (full) cudaGraphDestroy(full);
+            return rc;
+        }
+        if (e != cudaSuccess) {
+            if (full) cudaGraphDestroy(full);
+            return fail_cuda(e, "capture of the solve graph");
+        }
+        if (e3 != cudaSuccess) return fail_cuda(e3, "cudaStreamEndCapture");
+        e = cudaGraphInstantiate(&slot.exec, full, 0);
+        cudaGraphDestroy(full);
+        if (e != cudaSuccess) return fail_cuda(e, "cudaGraphInstantiate");
+        slot.k0 = d_mask;
+        slot.k1 = d_known;
+        slot.k2 = d_out;
+    }
+    CU(cudaGraphLaunch(slot.exec, st));
+    return 0;
+}
+
+int b200p_solve_async(b200p_plan *pl, const uint8_t *d_mask, const double *d_known, double *d_out,
+                      void *stream) {
     if (!pl || !d_mask || !d_known || !d_out) return fail_arg(B200P_ERR_ARG, "null argument");
+    if (pl->pending) return fail_arg(B200P_ERR_STATE, "a solve is pending on this plan: call b200p_solve_wait first");
     cudaStream_t st = (cudaStream_t)stream;
-    if (pl->cfg.use_graphs && !pl->profiling && st == nullptr) {
+    const bool graphs = pl->cfg.use_graphs && !pl->profiling;
+    if (graphs && st == nullptr) {
         // stream capture is not allowed on the legacy default stream
         if (!pl->own_stream) CU(cudaStreamCreateWithFlags(&pl->own_stream, cudaStreamNonBlocking));
         CU(cudaDeviceSynchronize());
         st = pl->own_stream;
     }
     bind_level0(pl, d_mask, d_known);
-    int rc = run_graph(pl, pl->g_front, d_mask, d_known, d_out, st,
-                       [&](cudaStream_t s) { return enqueue_front(pl, d_out, s); });
-    if (rc) return rc;
-    pl->hierarchy_ready = true;
-    CU(cudaStreamSynchronize(st));
-    int done = 0;
-    while (*pl->h_any && done < pl->cfg.v_cycles_max) {
-        const int k = std::min(pl->cfg.spec_cycles, pl->cfg.v_cycles_max - done);
-        for (int i = 0; i < k; ++i) {
-            rc = run_graph(pl, pl->g_cycle, d_mask, d_known, d_out, st,
-                           [&](cudaStream_t s) { return enqueue_cycle(pl, d_out, s); });
-            if (rc) return rc;
-        }
-        done += k;
+    int rc;
+    if (graphs) {
+        if ((rc = launch_solve_graph(pl, d_mask, d_known, d_out, st))) return rc;
+        pl->hierarchy_ready = true;
+    } else {
+        // eager: the host reads the loop condition after every cycle
+        if ((rc = enqueue_front(pl, d_out, st))) return rc;
+        pl->hierarchy_ready = true;
         CU(cudaStreamSynchronize(st));
+        int done = 0;
+        while (*pl->h_any && done < pl->cfg.v_cycles_max) {
+            if ((rc = enqueue_cycle(pl, d_out, st))) return rc;
+            ++done;
+            CU(cudaStreamSynchronize(st));
+        }
+        if ((rc = enqueue_reports(pl, st))) return rc;
     }
-    if (h_reports) {
-        rc = collect_reports(pl, h_reports, st);
-        if (rc) return rc;
+    pl->pending = true;
+    pl->pending_stream = st;
+    return 0;
+}
+
+int b200p_solve_wait(b200p_plan *pl, b200p_report *h_reports) {
+    if (!pl) return fail_arg(B200P_ERR_ARG, "null plan");
+    if (!pl->pending) return fail_arg(B200P_ERR_STATE, "no solve is pending on this plan");
+    pl->pending = false;
+    CU(cudaStreamSynchronize(pl->pending_stream));
+    if (pl->cfg.use_graphs && !pl->profiling) {
+        // kernels launched = front + report gather + one body pass per V-cycle that ran
+        int cyc = 0;
+        for (int p = 0; p < pl->P; ++p) cyc = std::max(cyc, pl->rep.cycles[p]);
+        pl->launches += pl->g_solve.kernels + (int64_t)cyc * pl->cycle_kernels;
     }
+    if (h_reports) read_reports(pl, h_reports);
     if (pl->profiling) prof_collect(pl);
     return 0;
+}
+
+int b200p_solve(b200p_plan *pl, const uint8_t *d_mask, const double *d_known, double *d_out,
+                b200p_report *h_reports, void *stream) {
+    int rc = b200p_solve_async(pl, d_mask, d_known, d_out, stream);
+    if (rc) return rc;
+    return b200p_solve_wait(pl, h_reports);
 }
 
 static int ensure_staging(b200p_plan *pl, bool u8) {
@@ -1410,8 +1573,7 @@ static int check_masks(const b200p_plan *pl, const uint8_t *h_mask) {
     return 0;
 }
 
-int b200p_solve_host(b200p_plan *pl, const uint8_t *h_mask, const double *h_known, double *h_out,
-                     b200p_report *h_reports) {
+int b200p_solve_host_async(b200p_plan *pl, const uint8_t *h_mask, const double *h_known, double *h_out) {
     if (!pl || !h_mask || !h_known || !h_out) return fail_arg(B200P_ERR_ARG, "null argument");
     int rc = check_masks(pl, h_mask);
     if (rc) return rc;
@@ -1420,14 +1582,20 @@ int b200p_solve_host(b200p_plan *pl, const uint8_t *h_mask, const double *h_know
     cudaStream_t st = pl->own_stream;
     CU(cudaMemcpyAsync(pl->d_in_mask, h_mask, pl->F * plane, cudaMemcpyHostToDevice, st));
     CU(cudaMemcpyAsync(pl->d_in_known, h_known, pl->P * plane * sizeof(double), cudaMemcpyHostToDevice, st));
-    if ((rc = b200p_solve(pl, pl->d_in_mask, pl->d_in_known, pl->d_out, h_reports, st))) return rc;
+    if ((rc = b200p_solve_async(pl, pl->d_in_mask, pl->d_in_known, pl->d_out, st))) return rc;
     CU(cudaMemcpyAsync(h_out, pl->d_out, pl->P * plane * sizeof(double), cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
     return 0;
 }
 
-int b200p_solve_host_u8(b200p_plan *pl, const uint8_t *h_mask, const uint8_t *h_known_u8,
-                        uint8_t *h_out_u8, b200p_report *h_reports) {
+int b200p_solve_host(b200p_plan *pl, const uint8_t *h_mask, const double *h_known, double *h_out,
+                     b200p_report *h_reports) {
+    int rc = b200p_solve_host_async(pl, h_mask, h_known, h_out);
+    if (rc) return rc;
+    return b200p_solve_wait(pl, h_reports);
+}
+
+int b200p_solve_host_u8_async(b200p_plan *pl, const uint8_t *h_mask, const uint8_t *h_known_u8,
+                              uint8_t *h_out_u8) {
     if (!pl || !h_mask || !h_known_u8 || !h_out_u8) return fail_arg(B200P_ERR_ARG, "null argument");
     int rc = check_masks(pl, h_mask);
     if (rc) return rc;
@@ -1443,7 +1611,7 @@ int b200p_solve_host_u8(b200p_plan *pl, const uint8_t *h_mask, const uint8_t *h_
             pl->d_io_u8, n, pl->d_in_known);
         CU(cudaGetLastError());
     }
-    if ((rc = b200p_solve(pl, pl->d_in_mask, pl->d_in_known, pl->d_out, h_reports, st))) return rc;
+    if ((rc = b200p_solve_async(pl, pl->d_in_mask, pl->d_in_known, pl->d_out, st))) return rc;
     {
         LaunchScope sc(pl, st, KK_CONVERT, 9.0 * n);
         f64_to_u8_kernel<<<(unsigned)((n + ST_THREADS - 1) / ST_THREADS), ST_THREADS, 0, st>>>(
@@ -1451,8 +1619,14 @@ int b200p_solve_host_u8(b200p_plan *pl, const uint8_t *h_mask, const uint8_t *h_
         CU(cudaGetLastError());
     }
     CU(cudaMemcpyAsync(h_out_u8, pl->d_io_u8, n, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
     return 0;
+}
+
+int b200p_solve_host_u8(b200p_plan *pl, const uint8_t *h_mask, const uint8_t *h_known_u8,
+                        uint8_t *h_out_u8, b200p_report *h_reports) {
+    int rc = b200p_solve_host_u8_async(pl, h_mask, h_known_u8, h_out_u8);
+    if (rc) return rc;
+    return b200p_solve_wait(pl, h_reports);
 }
 
 // ---- stage entry points -------------------------------------------------

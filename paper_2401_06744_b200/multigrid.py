@@ -169,6 +169,25 @@ class Plan:
         wall = time.perf_counter() - t0
         return out, self._reports(raw, wall)
 
+    def solve_host_async(self, mask, known, out, u8: bool = False):
+        """Enqueue H2D + solve + D2H on the plan's stream and return; `wait()` completes it.
+        The arrays must be C-contiguous, of the exact dtypes, and stay alive until `wait()`."""
+        want = np.uint8 if u8 else np.float64
+        for a, n, dt in ((mask, "mask", np.uint8), (known, "known", want), (out, "out", want)):
+            if not isinstance(a, np.ndarray) or a.dtype != dt or not a.flags.c_contiguous:
+                raise ValueError(f"{n} must be a C-contiguous {np.dtype(dt)} array")
+        self._t0 = time.perf_counter()
+        _dev.call("b200p_solve_host_u8_async" if u8 else "b200p_solve_host_async", self.handle,
+                  mask.ctypes.data, known.ctypes.data, out.ctypes.data)
+        self._keep = (mask, known, out)
+
+    def wait(self):
+        """Complete the pending asynchronous solve; returns its SolveReports."""
+        raw = (_lib.Report * self.problems)()
+        _dev.call("b200p_solve_wait", self.handle, C.cast(raw, C.c_void_p))
+        self._keep = None
+        return self._reports(raw, time.perf_counter() - self._t0)
+
     def solve_host_u8(self, mask, known_u8, out=None):
         mask = np.ascontiguousarray(mask, dtype=np.uint8)
         known_u8 = np.ascontiguousarray(known_u8, dtype=np.uint8)

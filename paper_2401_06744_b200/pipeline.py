@@ -1,20 +1,21 @@
 """Host-side frame pipeline: overlaps PCIe with compute for batches of frames.
 
 Frames are independent problems, so a batch that arrives in HOST memory is cut
-into chunks of `frames_per_lane` frames and fed to `lanes` worker threads.  Each
-lane owns a plan (its own CUDA stream, staging buffers and graphs) and runs
-``b200p_solve_host`` on its chunk: H2D, solve, D2H.  With two or more lanes the
-copies of one chunk overlap the kernels of another (PCIe is full duplex), which
-is what the end-to-end frames/s of a decoder fed from host memory depends on.
-Results do not depend on the chunking (bit-identical to a single batched plan).
-
-ctypes releases the GIL during the C call, so plain threads suffice."""
+into chunks of `frames_per_lane` frames that rotate over `lanes` plans.  Each
+lane owns a plan (its own CUDA stream, staging buffers and solve graph).  A
+chunk is ENQUEUED with ``b200p_solve_host_async`` -- H2D of mask + known, the
+whole FMG solve as one CUDA graph (the V-cycle loop is a WHILE node, so no host
+round trip), D2H of the result -- and the call returns at once; the lane is
+waited for (``b200p_solve_wait``) only when it is needed for the next chunk.
+One host thread therefore keeps `lanes` chunks in flight and the copy engines
+run under the kernels of the other lanes (PCIe is full duplex), which is what
+the end-to-end frames/s of a decoder fed from host memory depends on.  Pass
+pinned arrays: pageable memory makes the copies synchronous.
+Results do not depend on the chunking (bit-identical to a single batched plan)."""
 
 from __future__ import annotations
 
 import ctypes as C
-import queue
-import threading
 
 import numpy as np
 
@@ -24,7 +25,7 @@ from .multigrid import MultigridConfig, Plan
 
 class FramePipeline:
     def __init__(self, width, height, channels, cfg: MultigridConfig | None = None, spacing=1.0,
-                 lanes: int = 3, frames_per_lane: int = 1):
+                 lanes: int = 4, frames_per_lane: int = 1):
         if lanes < 1 or frames_per_lane < 1:
             raise ValueError("need lanes >= 1 and frames_per_lane >= 1")
         _dev.require_cuda()
@@ -35,8 +36,11 @@ class FramePipeline:
         _lib.check(_lib.lib().b200p_get_device(C.byref(dev)))
         self.device = dev.value
         self.plans = [Plan(width, height, channels, frames_per_lane, self.cfg, spacing) for _ in range(lanes)]
+        self._inflight = [None] * lanes  # (job, chunk index) pending on each lane
+        self._next = 0
 
     def close(self):
+        self._drain_quietly()
         for p in self.plans:
             p.close()
         self.plans = []
@@ -56,11 +60,14 @@ class FramePipeline:
             raise ValueError(f"frame count {masks.shape[0]} is not a multiple of frames_per_lane "
                              f"{self.frames_per_lane}")
 
-    def run(self, masks, known, out=None, u8: bool = False):
-        """masks (F,H,W) bool/uint8, known (F,C,H,W) float64 (or uint8 with u8=True) -> (out, reports).
+    def submit(self, masks, known, out=None, u8: bool = False):
+        """Enqueue a batch: masks (F,H,W) bool/uint8, known (F,C,H,W) float64 (uint8 with u8=True).
 
-        `out` may be a preallocated (pinned) array of known's shape and dtype.  reports[f] is the
-        list of per-channel SolveReports of frame f."""
+        Returns a job dict {"out", "reports"}; its arrays are complete after `flush()` (or once
+        later submits have recycled all of its lanes).  Batches submitted back to back keep the
+        lanes busy across batch boundaries: only `flush()` drains the pipeline.  `out` may be a
+        preallocated (pinned) array of known's shape and dtype.  reports[f] is the list of
+        per-channel SolveReports of frame f."""
         masks = np.asarray(masks)
         known = np.asarray(known)
         want = np.uint8 if u8 else np.float64
@@ -73,35 +80,49 @@ class FramePipeline:
         self._check(masks, known, out)
         m8 = masks.view(np.uint8)
         k = self.frames_per_lane
-        nchunks = masks.shape[0] // k
-        work: queue.SimpleQueue = queue.SimpleQueue()
-        for i in range(nchunks):
-            work.put(i)
-        reports = [None] * masks.shape[0]
-        errors = []
+        job = {"out": out, "reports": [None] * masks.shape[0]}
+        try:
+            for i in range(masks.shape[0] // k):
+                li = self._next % len(self.plans)
+                self._next += 1
+                self._retire(li)
+                sl = slice(i * k, (i + 1) * k)
+                self.plans[li].solve_host_async(m8[sl], known[sl], out[sl], u8=u8)
+                self._inflight[li] = (job, i)
+        except BaseException:
+            self._drain_quietly()
+            raise
+        return job
 
-        def lane(plan):
+    def _retire(self, li):
+        ent = self._inflight[li]
+        if ent is None:
+            return
+        self._inflight[li] = None
+        job, i = ent
+        reps = self.plans[li].wait()
+        k, c = self.frames_per_lane, self.shape[0]
+        for j in range(k):
+            job["reports"][i * k + j] = reps[j * c:(j + 1) * c]
+
+    def _drain_quietly(self):
+        for li in range(len(self.plans)):  # leave no solve pending on a plan
             try:
-                _lib.check(_lib.lib().b200p_set_device(self.device))
-                while True:
-                    try:
-                        i = work.get_nowait()
-                    except queue.Empty:
-                        return
-                    sl = slice(i * k, (i + 1) * k)
-                    fn = plan.solve_host_u8 if u8 else plan.solve_host
-                    _, reps = fn(m8[sl], known[sl], out[sl])
-                    c = self.shape[0]
-                    for j in range(k):
-                        reports[i * k + j] = reps[j * c:(j + 1) * c]
-            except BaseException as e:  # surfaced in the caller's thread
-                errors.append(e)
+                self._retire(li)
+            except Exception:
+                pass
 
-        threads = [threading.Thread(target=lane, args=(p,), daemon=True) for p in self.plans[:nchunks]]
-        for t in threads:
-            t.start()
-        for t in threads:
-            t.join()
-        if errors:
-            raise errors[0]
-        return out, reports
+    def flush(self):
+        """Wait for everything submitted so far."""
+        try:
+            for li in range(len(self.plans)):
+                self._retire(li)
+        except BaseException:
+            self._drain_quietly()
+            raise
+
+    def run(self, masks, known, out=None, u8: bool = False):
+        """submit + flush: returns (out, reports)."""
+        job = self.submit(masks, known, out, u8=u8)
+        self.flush()
+        return job["out"], job["reports"]
