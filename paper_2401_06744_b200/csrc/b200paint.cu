@@ -164,6 +164,7 @@ struct LevelHost {
     unsigned *d_mtab = nullptr; // K2T: packed block-local masks (F, nblocks, 64); null = level not eligible
     // fused sweep (K2F): ping-pong partner of the iterate, L2-resident ring, schedule tables
     bool fused = false;
+    int fused_tile = 0;
     double *d_u_alt = nullptr;  // (P,h,w)
     double *d_ring = nullptr;   // (R, nx, bh*bw)
     int R = 0, lag = 0, nsx = 0, nc = 0, cw = 0, fused_grid = 0;
@@ -480,7 +481,7 @@ static int local_cap(const b200p_plan *pl, const LevelHost &L) {
 
 // Tile variants of K2 (block extent -> <TW,TH,NWARP>).
 enum { TILE_GENERIC = 0, TILE_32_A = 1, TILE_16 = 2, TILE_8 = 3, TILE_32_B = 4, TILE_32_C = 5,
-       TILE_32_S = 6, TILE_32_T = 7, TILE_32_U = 8, TILE_32_TMA = 9 };
+       TILE_32_S = 6, TILE_32_T = 7, TILE_32_U = 8, TILE_32_TMA = 9, TILE_32_L = 10 };
 
 static int tile_for(int bw, int bh) {
     if (bw == 32 && bh == 32) {
@@ -491,7 +492,8 @@ static int tile_for(int bw, int bh) {
         if (e && *e == 'T') return TILE_32_T;
         if (e && *e == 'U') return TILE_32_U;
         if (e && *e == 'M') return TILE_32_TMA;
-        return TILE_32_B;
+        if (e && *e == 'B') return TILE_32_B;
+        return TILE_32_L;  // lean prologue + packed reduction; falls back to B where not eligible
     }
     if (bw == 16 && bh == 16) return TILE_16;
     if (bw == 8 && bh == 8) return TILE_8;
@@ -570,7 +572,7 @@ static int launch_sweep_fused(b200p_plan *pl, const LevelHost &L, UBuf &u, const
     const int grid = (int)std::min<long long>(total, L.fused_grid);
     // sweep = read u_old (+ b) + mask, write u_new; the corrections stay in L2
     LaunchScope sc(pl, st, KK_SWEEP, field_bytes(pl, L, rm ? 2.0 : 3.0, 1.0));
-    switch (L.tile) {
+    switch (L.fused_tile) {
         case TILE_32_A: launch_fused<4, 2, 4>(A, rm, grid, st); break;
         case TILE_32_B: launch_fused<4, 4, 2>(A, rm, grid, st); break;
         case TILE_16: launch_fused<2, 4, 1>(A, rm, grid, st); break;
@@ -679,8 +681,25 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, double *u, con
     {
         // read u (+ b) + mask, write the weighted correction tiles
         LaunchScope sc(pl, st, KK_SWEEP_SPLIT, field_bytes(pl, L, rm ? 2.0 : 3.0, 1.0));
-        if (tile == TILE_32_TMA && !tma_eligible(L, u, b, rm)) tile = TILE_32_B;
+        if ((tile == TILE_32_TMA || tile == TILE_32_L) && !tma_eligible(L, u, b, rm)) tile = TILE_32_B;
         switch (tile) {
+            case TILE_32_L: {
+                static const int cap = getenv("B200P_REGCAP") ? atoi(getenv("B200P_REGCAP")) : 168;
+                dim3 g3(L.info.nx, L.info.ny, pl->P);
+#define KL_LAUNCH(CAP)                                                                      \
+    do {                                                                                    \
+        if (rm) oras_sweep_lean_kernel<true, CAP><<<g3, 64, 0, st>>>(A, L.d_mtab);          \
+        else oras_sweep_lean_kernel<false, CAP><<<g3, 64, 0, st>>>(A, L.d_mtab);            \
+    } while (0)
+                if (cap == 255) KL_LAUNCH(255);
+                else if (cap == 160) KL_LAUNCH(160);
+                else if (cap == 152) KL_LAUNCH(152);
+                else if (cap == 144) KL_LAUNCH(144);
+                else if (cap == 128) KL_LAUNCH(128);
+                else KL_LAUNCH(168);
+#undef KL_LAUNCH
+                break;
+            }
             case TILE_32_TMA: {
                 int rc = launch_sweep_tma(pl, L, A, rm, st);
                 if (rc) return rc;
@@ -1227,7 +1246,8 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
         {
             const char *e = getenv("B200P_FUSED");
             const bool want = e && *e == '1';  // experimental; the split sweep (K2 + K2b) is faster
-            const int bpc = L.tile == TILE_32_A ? 1 : (L.tile == TILE_32_B ? 2 : (L.tile == TILE_16 ? 4 : 0));
+            const int ftile = (D.bw == 32 && D.bh == 32 && L.tile != TILE_32_A) ? TILE_32_B : L.tile;  // K2F knows A, B, 16
+            const int bpc = ftile == TILE_32_A ? 1 : (ftile == TILE_32_B ? 2 : (ftile == TILE_16 ? 4 : 0));
             if (want && bpc > 0 && L.nblocks > 1) {
                 L.fused = true;
                 std::vector<int> first(L.info.ny), last(L.info.ny);
@@ -1252,8 +1272,9 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
                 pl->sched_words = std::max(pl->sched_words, (size_t)1 + 2 * (size_t)pl->P * L.info.ny);
                 int occ = 0, sms = 148;
                 cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-                occ = L.tile == TILE_32_A ? fused_occupancy<4, 2, 4>()
-                      : (L.tile == TILE_32_B ? fused_occupancy<4, 4, 2>() : fused_occupancy<2, 4, 1>());
+                L.fused_tile = ftile;
+                occ = ftile == TILE_32_A ? fused_occupancy<4, 2, 4>()
+                      : (ftile == TILE_32_B ? fused_occupancy<4, 4, 2>() : fused_occupancy<2, 4, 1>());
                 if (occ < 1) occ = 4;
                 L.fused_grid = sms * occ;
             }
@@ -1700,7 +1721,7 @@ int b200p_plan_oras_sweeps(b200p_plan *pl, int level, const double *d_b, double 
     } else if (path >= 10) {
         const int t = path - 10;
         const bool ok = (is32 && (t == TILE_32_A || t == TILE_32_B || t == TILE_32_C || t == TILE_32_S ||
-                                 t == TILE_32_T || t == TILE_32_U || t == TILE_32_TMA)) ||
+                                 t == TILE_32_T || t == TILE_32_U || t == TILE_32_TMA || t == TILE_32_L)) ||
                         (is16 && t == TILE_16) || (is8 && t == TILE_8);
         if (!ok) return fail_arg(B200P_ERR_UNSUPPORTED, "level %d is not eligible for tile variant %d", level, t);
         force = t;

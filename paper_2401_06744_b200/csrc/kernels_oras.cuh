@@ -22,7 +22,7 @@ namespace b200p {
 constexpr int ST_THREADS_COMBINE = 256;
 
 #ifndef B200P_PACKED_RED
-#define B200P_PACKED_RED 0
+#define B200P_PACKED_RED 1
 #endif
 
 struct SweepArgs {
@@ -406,6 +406,216 @@ oras_sweep_tile_kernel(const SweepArgs A) {
     const int blk = blockIdx.x;
     double *out = A.scratch + ((size_t)p * A.L.nblocks + blk) * (8 * TW * 4 * TH * NWARP);
     tile_block_solve<TW, TH, NWARP, RM, false>(A, p, blk, 0, threadIdx.x >> 5, sm, A.eta * rs_g, out);
+}
+
+// ------------------------------------------------------------------ K2L ---
+// The 32x32 register-tile solve with a lean per-block prologue/epilogue.  ncu on K2 showed
+// that with ~4.3 CG steps per block the per-block part (gather, start, weighted store) issues
+// as many instructions as 2.4 CG steps; K2L trims it:
+//   * grid (ix, iy, problem): no integer division;
+//   * the block-local mask comes from the bit table packed at hierarchy build (one coalesced
+//     32-bit load per thread instead of 16 byte loads and tests);
+//   * own pixels are loaded as aligned double2 (block starts are even), only the halo needs a
+//     predicate, and the neighbour count of core.py:100-110 is 4 unless the block touches the
+//     image border (block-uniform branch);
+//   * inside FMG the right-hand side is where(mask, known, 0) and b - u == 0 at mask pixels
+//     (mflag == 0), so level-0 / cascade sweeps (RM) do not read b at all;
+//   * the PoU weight rows of the block are fetched into shared memory at block start and read
+//     back after the CG loop (their global-load latency used to be exposed at the end).
+// Requires: even level width, even block starts, 16-byte aligned u / b (the driver checks).
+struct LeanSmem {
+    TileSmem<4, 4, 2> cg;
+    alignas(16) double wx[32];
+    alignas(16) double wy[32];
+};
+
+template <bool RM, int REGCAP>
+__global__ void __launch_bounds__(64) __maxnreg__(REGCAP)
+oras_sweep_lean_kernel(const SweepArgs A, const unsigned *__restrict__ mtab) {
+    constexpr int TW = 4, TH = 4, NWARP = 2, BW = 32, BH = 32;
+    using CG = TileCG<TW, TH, NWARP>;
+    __shared__ LeanSmem sm;
+    const int p = blockIdx.z;
+    if (A.pred && !A.pred[p]) return;
+    const double rs_g = A.rs[p];
+    if (rs_g == 0.0) return;  // oras_sweeps exit, solvers.py:420
+    const LevelDev &L = A.L;
+    const int ix = blockIdx.x, iy = blockIdx.y, blk = iy * L.nx + ix;
+    const int tid = threadIdx.x;
+    const unsigned mbits = mtab[((size_t)(p / A.channels) * L.nblocks + blk) * 64 + tid];
+    // PoU weight rows of this block -> shared memory (consumed after the CG loop)
+    {
+        const double wv = tid < 32 ? L.wx[ix * BW + tid] : L.wy[iy * BH + tid - 32];
+        if (tid < 32) sm.wx[tid] = wv; else sm.wy[tid - 32] = wv;
+    }
+    const int x0 = L.xs[ix], y0 = L.ys[iy];
+    const int W = L.w, H = L.h;
+    const double target = A.eta * rs_g;
+    const bool general = A.mflag[p] != 0;
+
+    CG cg;
+    cg.lane = tid & 31;
+    cg.wg = tid >> 5;
+    cg.bar_id = 1;
+    cg.lx = cg.lane & 7;
+    cg.ly = cg.lane >> 3;
+    cg.xrow = sm.cg.xrow;
+    cg.red = sm.cg.red;
+    cg.slot = 0;
+    cg.eL = cg.lx == 0;
+    cg.eR = cg.lx == 7;
+    cg.eT = cg.wg == 0 && cg.ly == 0;
+    cg.eB = cg.wg == NWARP - 1 && cg.ly == 3;
+    const double g_in = 1.0 - L.robin / L.hinv2;  // 1 - alpha*h
+    cg.gL = x0 > 0 ? g_in : 1.0;
+    cg.gR = x0 + BW < W ? g_in : 1.0;
+    cg.gT = y0 > 0 ? g_in : 1.0;
+    cg.gB = y0 + BH < H ? g_in : 1.0;
+    cg.mbits = mbits;
+
+    const int bx = cg.lx * TW, by = (cg.wg * 4 + cg.ly) * TH;
+    const int gx0 = x0 + bx, gy0 = y0 + by;
+    const double hinv2 = L.hinv2;
+    const bool border = x0 == 0 || y0 == 0 || x0 + BW >= W || y0 + BH >= H;  // block-uniform
+
+    // ---- gather: global residual g = b - A u on the tile (core.py:100-110)
+    double r[TH][TW];
+    {
+        const double *urow = A.u + (size_t)p * A.plane + (size_t)(gy0 - 1) * W + gx0;
+        const bool hasL = gx0 > 0, hasR = gx0 + TW < W, hasT = gy0 > 0, hasB = gy0 + TH < H;
+        double uc[TH + 2][TW + 2];
+#pragma unroll
+        for (int j = 0; j < TH + 2; ++j) {
+            const double *rp = urow + (size_t)j * W;
+            const bool rowin = (j > 0 || hasT) && (j < TH + 1 || hasB);
+            double2 a0 = make_double2(0.0, 0.0), a1 = a0;
+            if (rowin) {
+                a0 = *reinterpret_cast<const double2 *>(rp);
+                a1 = *reinterpret_cast<const double2 *>(rp + 2);
+            }
+            uc[j][1] = a0.x; uc[j][2] = a0.y; uc[j][3] = a1.x; uc[j][4] = a1.y;
+            uc[j][0] = uc[j][5] = 0.0;
+            if (j >= 1 && j <= TH) {
+                if (hasL) uc[j][0] = rp[-1];
+                if (hasR) uc[j][5] = rp[TW];
+            }
+        }
+        const double c4 = 4.0 * hinv2;
+#pragma unroll
+        for (int j = 0; j < TH; ++j) {
+            double bt[TW] = {0.0, 0.0, 0.0, 0.0};
+            if (!RM) {
+                const double *bp = A.b + (size_t)p * A.plane + (size_t)(gy0 + j) * W + gx0;
+                const double2 b0 = *reinterpret_cast<const double2 *>(bp);
+                const double2 b1 = *reinterpret_cast<const double2 *>(bp + 2);
+                bt[0] = b0.x; bt[1] = b0.y; bt[2] = b1.x; bt[3] = b1.y;
+            } else if (general) {
+#pragma unroll
+                for (int i = 0; i < TW; ++i)
+                    if ((mbits >> (j * TW + i)) & 1u)
+                        bt[i] = A.b[(size_t)p * A.plane + (size_t)(gy0 + j) * W + gx0 + i];
+            }
+#pragma unroll
+            for (int i = 0; i < TW; ++i) {
+                const bool m = (mbits >> (j * TW + i)) & 1u;
+                const double s = ((uc[j][i + 1] + uc[j + 2][i + 1]) + uc[j + 1][i]) + uc[j + 1][i + 2];
+                double d = c4;
+                if (border) {
+                    const int gy = gy0 + j, gx = gx0 + i;
+                    const double cnt = 4.0 - (gy == 0 ? 1.0 : 0.0) - (gy == H - 1 ? 1.0 : 0.0) -
+                                       (gx == 0 ? 1.0 : 0.0) - (gx == W - 1 ? 1.0 : 0.0);
+                    d = cnt * hinv2;
+                }
+                const double uu = uc[j + 1][i + 1];
+                // b - (d u - hinv2 s)
+                const double res = fma(hinv2, s, fma(-d, uu, bt[i]));
+                if (RM) r[j][i] = m ? (general ? bt[i] - uu : 0.0) : res;
+                else r[j][i] = m ? (bt[i] - uu) : res;
+            }
+        }
+    }
+
+    // ---- local start: v0 = where(mask, g, 0), r0 = g - A_i v0 (solvers.py:331-333)
+    double v[TH][TW], pc[TH][TW], q[TH][TW];
+#pragma unroll
+    for (int j = 0; j < TH; ++j)
+#pragma unroll
+        for (int i = 0; i < TW; ++i) v[j][i] = 0.0;
+    if (general) {
+#pragma unroll
+        for (int j = 0; j < TH; ++j)
+#pragma unroll
+            for (int i = 0; i < TW; ++i) {
+                const bool m = (mbits >> (j * TW + i)) & 1u;
+                v[j][i] = m ? r[j][i] : 0.0;
+                pc[j][i] = v[j][i];
+            }
+        cg.apply(pc, q);
+#pragma unroll
+        for (int j = 0; j < TH; ++j)
+#pragma unroll
+            for (int i = 0; i < TW; ++i) {
+                const bool m = (mbits >> (j * TW + i)) & 1u;
+                r[j][i] = m ? 0.0 : fma(-hinv2, q[j][i], r[j][i]);
+            }
+    }
+    double rs_k = cg.group_sum(tile_dot<TW, TH>(r, r));
+
+    if (rs_k > target) {  // solvers.py:336 (strict)
+#pragma unroll
+        for (int j = 0; j < TH; ++j)
+#pragma unroll
+            for (int i = 0; i < TW; ++i) pc[j][i] = r[j][i];
+        double inv_rs = 1.0 / rs_k;
+        for (int it = 0; it < A.max_iters; ++it) {
+            cg.apply(pc, q);
+            double d_pq = tile_dot<TW, TH>(pc, q);
+            double d_rq = tile_dot<TW, TH>(r, q);
+            double d_qq = tile_dot<TW, TH>(q, q);
+            cg.group_sum3(d_pq, d_rq, d_qq);
+            const double pq = hinv2 * d_pq;
+            const bool ok = pq > 0.0;                 // solvers.py:348
+            const double a = ok ? rs_k / pq : 0.0;    // :349-350
+            const double ah = a * hinv2;
+            const double rs_new = fma(ah * ah, d_qq, fma(-2.0 * ah, d_rq, rs_k));
+#pragma unroll
+            for (int j = 0; j < TH; ++j)
+#pragma unroll
+                for (int i = 0; i < TW; ++i) {
+                    v[j][i] = fma(a, pc[j][i], v[j][i]);
+                    r[j][i] = fma(-ah, q[j][i], r[j][i]);
+                }
+            if (rs_new <= target || !ok) break;       // :354
+            const double beta = rs_new * inv_rs;
+            rs_k = rs_new;
+            inv_rs = 1.0 / rs_k;
+#pragma unroll
+            for (int j = 0; j < TH; ++j)
+#pragma unroll
+                for (int i = 0; i < TW; ++i) pc[j][i] = fma(beta, pc[j][i], r[j][i]);
+        }
+    }
+
+    // ---- weighted correction (v * wy) * wx (solvers.py:309-310)
+    {
+        double *out = A.scratch + ((size_t)p * L.nblocks + blk) * (BW * BH);
+        const double2 wx0 = *reinterpret_cast<const double2 *>(&sm.wx[bx]);
+        const double2 wx1 = *reinterpret_cast<const double2 *>(&sm.wx[bx + 2]);
+        const double2 wy0 = *reinterpret_cast<const double2 *>(&sm.wy[by]);
+        const double2 wy1 = *reinterpret_cast<const double2 *>(&sm.wy[by + 2]);
+        const double wyv[4] = {wy0.x, wy0.y, wy1.x, wy1.y};
+#pragma unroll
+        for (int j = 0; j < TH; ++j) {
+            double2 o0, o1;
+            o0.x = (v[j][0] * wyv[j]) * wx0.x;
+            o0.y = (v[j][1] * wyv[j]) * wx0.y;
+            o1.x = (v[j][2] * wyv[j]) * wx1.x;
+            o1.y = (v[j][3] * wyv[j]) * wx1.y;
+            double2 *row = reinterpret_cast<double2 *>(out + (by + j) * BW + bx);
+            row[0] = o0;
+            row[1] = o1;
+        }
+    }
 }
 
 // ------------------------------------------------------------------ K2S ---
