@@ -241,7 +241,8 @@ def test_fused_and_split_sweeps_agree():
     oa, ra = a.solve_host(mk, k[None])
     ob, rb = b.solve_host(mk, k[None])
     assert [r.iterations for r in ra] == [r.iterations for r in rb]
-    assert np.array_equal(oa, ob)
+    # the two paths gather the block residual with differently ordered fp64 operations
+    np.testing.assert_allclose(oa, ob, rtol=0, atol=1e-9)
     a.close(); b.close()
 
 
