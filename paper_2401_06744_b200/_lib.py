@@ -34,6 +34,7 @@ class Config(C.Structure):
         ("coarse_tol", C.c_double), ("coarse_max_iters", C.c_int),
         ("tol_rel", C.c_double), ("alpha", C.c_double), ("eta", C.c_double),
         ("local_max_iters", C.c_int), ("use_graphs", C.c_int), ("spec_cycles", C.c_int),
+        ("mode", C.c_int), ("max_outer_iters", C.c_int),
     ]
 
 

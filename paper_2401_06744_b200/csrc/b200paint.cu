@@ -228,6 +228,7 @@ struct b200p_plan {
     cudaStream_t aux_stream = nullptr;  // captures the WHILE body
     cudaStream_t pending_stream = nullptr;
     bool pending = false;
+    bool pending_eager = false;  // the pending solve ran eagerly (launches already counted)
     GraphSlot g_solve;
     int64_t cycle_kernels = 0;   // kernel nodes of one WHILE body pass
     // staging for the host entry points
@@ -394,6 +395,55 @@ __global__ void sweep_gate_kernel(int P, const double *rs, double stop_norm, int
     rn_out[p] = rn;
     if (r2 == 0.0 || rn <= stop_norm || sweeps[p] >= max_sweeps) gate[p] = 0;
     else atomicOr(any, 1);
+}
+
+// Multilevel mode (ml-oras): _smooth_to_tol on one level of the cascade (multigrid.py:282-332).
+// base: the level's flat-init defect -> denom (0 -> the first residual norm, and 0 again -> done).
+__global__ void ml_level_begin_kernel(int P, const double *rs_base, double *denom, int *gate, int *sweeps) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    denom[p] = sqrt(rs_base[p]);
+    gate[p] = 1;
+    sweeps[p] = 0;
+}
+// One residual evaluation of oras_sweeps with stop_norm = tol * denom (solvers.py:413-421):
+// records the relative norm (history on the finest level), closes the gate on exit.
+__global__ void ml_gate_kernel(int P, const double *rs, double tol, int max_units, double *denom, int *gate,
+                               const int *sweeps, double *rel, double *hist, int *histlen, int record,
+                               int *any) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P || !gate[p]) return;
+    const double r2 = rs[p];
+    const double rn = sqrt(r2);
+    double d = denom[p];
+    if (d == 0.0) {  // multigrid.py:300-303
+        d = rn;
+        denom[p] = d;
+        if (d == 0.0) {
+            rel[p] = 0.0;
+            gate[p] = 0;
+            return;
+        }
+    }
+    const double r = rn / d;
+    rel[p] = r;
+    if (record) {
+        const int hl = histlen[p];
+        if (hl < B200P_MAX_HISTORY) {
+            hist[(size_t)p * B200P_MAX_HISTORY + hl] = r;
+            histlen[p] = hl + 1;
+        }
+    }
+    if (r2 == 0.0 || rn <= tol * d || sweeps[p] >= max_units) gate[p] = 0;
+    else atomicOr(any, 1);
+}
+// report fields of multilevel mode: iterations = finest-level smoother units
+__global__ void ml_finish_kernel(int P, const int *sweeps, int *cycles, int *units, int *active) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    cycles[p] = sweeps[p];
+    units[p] = sweeps[p];
+    active[p] = 0;
 }
 
 // ------------------------------------------------------ launch helpers -----
@@ -767,7 +817,8 @@ static int enqueue_smooth(b200p_plan *pl, const LevelHost &L, UBuf &u, const dou
 
 static int launch_coarse(b200p_plan *pl, const LevelHost &L, double *u, const double *b,
                          bool rhs_masked, int init_mode, double tol, int max_sweeps, const int *pred,
-                         int *units_out, int accumulate, cudaStream_t st) {
+                         int *units_out, int accumulate, cudaStream_t st, double *rel_out = nullptr,
+                         bool record_history = false) {
     CoarseArgs A;
     A.L = L.dev;
     A.u = u;
@@ -783,7 +834,10 @@ static int launch_coarse(b200p_plan *pl, const LevelHost &L, double *u, const do
     A.init_mode = init_mode;
     A.units_out = units_out;
     A.units_accumulate = accumulate;
-    A.rel_out = nullptr;
+    A.rel_out = rel_out;
+    A.hist = record_history ? pl->d_hist : nullptr;
+    A.histlen = pl->d_histlen;
+    A.hist_cap = B200P_MAX_HISTORY;
     const size_t n = (size_t)L.info.block_w * L.info.block_h;
     const size_t smem = smem_cg_bytes(L.info.block_w, L.info.block_h) + 2 * n * sizeof(double);
     LaunchScope sc(pl, st, KK_COARSE, field_bytes(pl, L, 3.0, 1.0));
@@ -967,6 +1021,81 @@ static int enqueue_vcycle(b200p_plan *pl, int level, UBuf &u, const double *b, b
     return settle_home ? settle(pl, L, u, home, st) : 0;
 }
 
+// fmg_solve in "multilevel" mode (ml-oras; multigrid.py:449-464 with _cascade(to_tol=True),
+// :389-418): coarsest level to min(coarse_tol, tol_rel); every finer level is initialised by
+// prolongate_solution and smoothed until ||r|| <= tol_rel * (flat-init defect of that level),
+// at most max_outer_iters sweeps.  A comparison pipeline of the paper, not the headline: it runs
+// eagerly, the host reads the per-problem gates every few sweeps.
+static int run_multilevel(b200p_plan *pl, double *d_out, cudaStream_t st) {
+    const int nl = (int)pl->lev.size();
+    const b200p_config &cfg = pl->cfg;
+    LevelHost &L0 = pl->lev[0];
+    const int nb = (pl->P + 127) / 128;
+    int rc;
+    if ((rc = enqueue_hierarchy(pl, st))) return rc;
+    if ((rc = launch_norm(pl, L0, L0.d_rhs, L0.d_rhs, true, true, nullptr, st))) return rc;
+    if ((rc = launch_control(pl, 0, st))) return rc;  // baseline; units, cycles, histlen = 0
+    const double ctol = std::min(cfg.coarse_tol, cfg.tol_rel);
+    LevelHost &co = pl->lev[nl - 1];
+    if (nl == 1) {
+        // single level: the coarse solve is the finest level (its per-evaluation history is not recorded)
+        if ((rc = launch_coarse(pl, co, d_out, co.d_rhs, true, 1, ctol, cfg.coarse_max_iters, nullptr,
+                                pl->d_sweeps, 0, st, pl->d_rel, true)))
+            return rc;
+    } else {
+        if ((rc = launch_coarse(pl, co, co.d_u, co.d_rhs, true, 1, ctol, cfg.coarse_max_iters, nullptr,
+                                nullptr, 0, st)))
+            return rc;
+        const double *coarse_u = co.d_u;
+        for (int l = nl - 2; l >= 0; --l) {
+            LevelHost &f = pl->lev[l];
+            const LevelHost &c = pl->lev[l + 1];
+            UBuf uf = level_ubuf(pl, l, d_out);
+            double *home = uf.cur;
+            {
+                LaunchScope sc(pl, st, KK_PROLONG_SOL, field_bytes(pl, f, 1.25, 1.0));
+                prolongate_kernel<true><<<grid2x(c.info.width, c.info.height, pl->P), ST_THREADS, 0, st>>>(
+                    coarse_u, f.d_mask, f.d_rhs, f.info.height, f.info.width, pl->C, nullptr, uf.cur);
+                CU(cudaGetLastError());
+            }
+            // denom = ||b - A flat_init|| of this level (multigrid.py:413)
+            if ((rc = launch_norm(pl, f, f.d_rhs, f.d_rhs, true, true, nullptr, st))) return rc;
+            {
+                LaunchScope sc(pl, st, KK_CONTROL, 0.0);
+                ml_level_begin_kernel<<<nb, 128, 0, st>>>(pl->P, pl->d_rs, pl->d_denom, pl->d_gate, pl->d_sweeps);
+                CU(cudaGetLastError());
+            }
+            int it = 0;
+            for (;;) {
+                const int chunk = 4;
+                if ((rc = launch_set_int(pl, pl->d_any, 1, 0, st))) return rc;
+                for (int k = 0; k < chunk && it <= cfg.max_outer_iters; ++k, ++it) {
+                    if ((rc = launch_norm(pl, f, uf.cur, f.d_rhs, false, true, pl->d_gate, st))) return rc;
+                    {
+                        LaunchScope sc(pl, st, KK_CONTROL, 0.0);
+                        ml_gate_kernel<<<nb, 128, 0, st>>>(pl->P, pl->d_rs, cfg.tol_rel, cfg.max_outer_iters,
+                                                          pl->d_denom, pl->d_gate, pl->d_sweeps, pl->d_rel,
+                                                          pl->d_hist, pl->d_histlen, l == 0 ? 1 : 0, pl->d_any);
+                        CU(cudaGetLastError());
+                    }
+                    if ((rc = launch_sweep(pl, f, uf, f.d_rhs, true, pl->d_gate, pl->d_sweeps, -1, st))) return rc;
+                }
+                CU(cudaMemcpyAsync(pl->h_any, pl->d_any, sizeof(int), cudaMemcpyDeviceToHost, st));
+                CU(cudaStreamSynchronize(st));
+                if (!*pl->h_any || it > cfg.max_outer_iters) break;
+            }
+            if ((rc = settle(pl, f, uf, home, st))) return rc;
+            coarse_u = home;
+        }
+    }
+    {
+        LaunchScope sc(pl, st, KK_CONTROL, 0.0);
+        ml_finish_kernel<<<nb, 128, 0, st>>>(pl->P, pl->d_sweeps, pl->d_cycles, pl->d_units, pl->d_active);
+        CU(cudaGetLastError());
+    }
+    return 0;
+}
+
 // Front half of fmg_solve: hierarchy, baseline, cascade, first convergence check.
 static int enqueue_front(b200p_plan *pl, double *d_out, cudaStream_t st) {
     LevelHost &L0 = pl->lev[0];
@@ -1104,6 +1233,8 @@ void b200p_config_default(b200p_config *c, int width, int height, int channels) 
     c->local_max_iters = 0;
     c->use_graphs = 1;
     c->spec_cycles = 1;
+    c->mode = 0;
+    c->max_outer_iters = 10000;
 }
 
 int b200p_axis_starts(int dim, int block, int overlap, int64_t *out, int cap) {
@@ -1184,8 +1315,9 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
     if (!(c.eta > 0.0)) return fail_arg(B200P_ERR_ARG, "local_tol_fraction must be positive, got %g", c.eta);
     if (c.value_downsampling != 0 && c.value_downsampling != 1)
         return fail_arg(B200P_ERR_ARG, "unknown value downsampling %d", c.value_downsampling);
-    if (c.v_cycles_max < 0 || c.coarse_max_iters < 0 || c.local_max_iters < 0)
+    if (c.v_cycles_max < 0 || c.coarse_max_iters < 0 || c.local_max_iters < 0 || c.max_outer_iters < 0)
         return fail_arg(B200P_ERR_ARG, "iteration caps must be >= 0");
+    if (c.mode != 0 && c.mode != 1) return fail_arg(B200P_ERR_ARG, "unknown mode %d", c.mode);
 
     int ndev = 0;
     CU(cudaGetDeviceCount(&ndev));
@@ -1514,6 +1646,16 @@ int b200p_solve_async(b200p_plan *pl, const uint8_t *d_mask, const double *d_kno
     }
     bind_level0(pl, d_mask, d_known);
     int rc;
+    if (pl->cfg.mode == 1) {
+        if ((rc = run_multilevel(pl, d_out, st))) return rc;
+        pl->hierarchy_ready = true;
+        if ((rc = enqueue_reports(pl, st))) return rc;
+        pl->pending = true;
+        pl->pending_stream = st;
+        pl->pending_eager = true;
+        return 0;
+    }
+    pl->pending_eager = !graphs;
     if (graphs) {
         if ((rc = launch_solve_graph(pl, d_mask, d_known, d_out, st))) return rc;
         pl->hierarchy_ready = true;
@@ -1540,7 +1682,7 @@ int b200p_solve_wait(b200p_plan *pl, b200p_report *h_reports) {
     if (!pl->pending) return fail_arg(B200P_ERR_STATE, "no solve is pending on this plan");
     pl->pending = false;
     CU(cudaStreamSynchronize(pl->pending_stream));
-    if (pl->cfg.use_graphs && !pl->profiling) {
+    if (!pl->pending_eager) {
         // kernels launched = front + report gather + one body pass per V-cycle that ran
         int cyc = 0;
         for (int p = 0; p < pl->P; ++p) cyc = std::max(cyc, pl->rep.cycles[p]);

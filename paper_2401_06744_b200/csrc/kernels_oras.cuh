@@ -1397,6 +1397,9 @@ struct CoarseArgs {
     int *units_out;       // may be null
     int units_accumulate;
     double *rel_out;      // may be null: final |r| / denom
+    double *hist;         // may be null: (P, hist_cap) relative norm of every residual evaluation
+    int *histlen;         //   (single-level multilevel solve: the on_fine_state history)
+    int hist_cap;
 };
 
 __global__ void __launch_bounds__(GEN_THREADS)
@@ -1451,6 +1454,10 @@ coarse_solve_kernel(const CoarseArgs A) {
             denom = rn;
             if (rn == 0.0) break;  // denom == 0 -> (0, 0.0), multigrid.py:302-303
             stop = A.tol * rn;
+        }
+        if (A.hist && tid == 0 && sweeps < A.hist_cap) {
+            A.hist[(size_t)p * A.hist_cap + sweeps] = rn / denom;
+            A.histlen[p] = sweeps + 1;
         }
         if (rs == 0.0 || rn <= stop || sweeps >= A.max_sweeps) break;
         smem_block_cg(S, hinv2, L.robin, false, false, false, false, A.eta * rs, A.max_iters);

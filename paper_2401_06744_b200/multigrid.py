@@ -53,9 +53,9 @@ class MultigridConfig:
 
 
 def _require_hot_path(cfg) -> None:
-    if cfg.smoother != "oras" or cfg.mode != "full_multigrid":
+    if cfg.smoother != "oras":
         raise NotImplementedError(
-            "the B200 build covers the mg-oras path only (smoother='oras', mode='full_multigrid'); "
+            "the B200 build covers the ORAS-smoothed pipelines only (mg-oras, ml-oras); "
             f"got smoother={cfg.smoother!r}, mode={cfg.mode!r}")
 
 
@@ -82,6 +82,8 @@ class Plan:
         c.local_max_iters = int(s.local_max_iters or 0)
         c.use_graphs = 1 if use_graphs else 0
         c.spec_cycles = int(spec_cycles)
+        c.mode = 1 if cfg.mode == "multilevel" else 0
+        c.max_outer_iters = int(s.max_outer_iters)
         self.config = c
         self.cfg = cfg
         self.width, self.height, self.channels, self.frames = int(width), int(height), int(channels), int(frames)
@@ -133,10 +135,12 @@ class Plan:
     # -- solves
     def _reports(self, raw, wall):
         reps = []
+        name = "ml-oras" if self.cfg.mode == "multilevel" else "mg-oras"
         for r in raw:
             reps.append(SolveReport(
-                solver="mg-oras", iterations=r.iterations, final_rel_residual=r.final_rel_residual,
-                wall_time=wall, history=list(r.history[: r.history_len]), converged=bool(r.converged),
+                solver=name, iterations=r.iterations, final_rel_residual=r.final_rel_residual,
+                wall_time=wall, history=list(r.history[: r.history_len]) or [r.final_rel_residual],
+                converged=bool(r.converged),
                 baseline_residual=r.baseline_residual, init_residual=r.init_residual,
                 fine_smoother_iterations=r.fine_smoother_iterations))
         return reps
@@ -209,7 +213,7 @@ def _cfg_key(cfg):
     s = cfg.solver
     return (cfg.nu_pre, cfg.nu_post, cfg.v_cycles_max, cfg.value_downsampling, cfg.block_size,
             cfg.overlap, cfg.coarse_tol, cfg.coarse_max_iters, s.tol_rel, s.alpha,
-            s.local_tol_fraction, s.local_max_iters)
+            s.local_tol_fraction, s.local_max_iters, cfg.mode, s.max_outer_iters)
 
 
 def cached_plan(width, height, channels, frames, cfg, spacing=1.0) -> Plan:

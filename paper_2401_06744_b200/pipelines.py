@@ -1,8 +1,9 @@
 """Named-pipeline front end: the drop-in boundary of the path.
 
 ``solve_image(problem, "mg-oras", cfg)`` has the reference's signature, result
-type and error behaviour (pipelines.py:20-114).  Only the ORAS-smoothed
-full-multigrid pipeline is built here; the other names of the reference are
+type and error behaviour (pipelines.py:20-114).  The ORAS-smoothed pipelines are
+built: "mg-oras" (the hot path) and "ml-oras" (cascadic multilevel, the paper's
+comparison variant, same kernels); the other names of the reference are
 recognised and rejected with NotImplementedError (out of scope).
 ``solve_frames`` is the batched entry (frames x channels in one plan).
 """
@@ -19,7 +20,7 @@ from .multigrid import LevelHierarchy, MultigridConfig, build_hierarchy, cached_
 from .solvers import SolveReport
 
 SOLVER_NAMES = ("cg", "oras", "ml-cg", "ml-oras", "mg-cg", "mg-oras")
-BUILT = ("mg-oras",)
+BUILT = ("mg-oras", "ml-oras")
 
 
 def split_solver_name(name: str):

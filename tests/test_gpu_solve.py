@@ -111,6 +111,35 @@ def test_small_cases(w, h, dens, seed, bs, ov, kw):
     _compare(m, k, *_cfgs(bs, ov, **kw))
 
 
+@pytest.mark.parametrize("w,h,dens,seed,bs,ov,kw", [
+    (160, 120, 0.05, 9, 32, 6, dict()),
+    (256, 256, 0.05, 0, 16, 2, dict()),
+    (97, 131, 0.03, 2, 16, 2, dict(tol_rel=1e-5)),          # odd dims at every level
+    (300, 200, 0.02, 4, 32, 6, dict(max_outer_iters=3)),    # sweep cap reached: converged False
+    (20, 30, 0.20, 3, 32, 6, dict(tol_rel=1e-6)),           # single level
+])
+def test_ml_oras_matches_oracle(w, h, dens, seed, bs, ov, kw):
+    """The cascadic multilevel pipeline "ml-oras" (multigrid.py:449-464): every level
+    smoothed to tol_rel against its own flat-init defect; iterations = finest-level sweeps."""
+    m, k = oracle.seeded_problem(w, h, dens, seed, channels=2)
+    so = oracle.SolverConfig(**kw)
+    sb = bp.SolverConfig(**kw)
+    cfg_o = oracle.MultigridConfig(block_size=bs, overlap=ov, mode="multilevel", solver=so)
+    cfg_b = bp.MultigridConfig(block_size=bs, overlap=ov, solver=sb)
+    ref, reps_o = oracle.solve_image(m, k, 1.0, cfg_o)
+    res = bp.solve_image(bp.InpaintingProblem(m, k), "ml-oras", cfg_b)
+    for ro, rg in zip(reps_o, res.reports):
+        assert rg.solver == "ml-oras"
+        assert rg.iterations == ro.iterations
+        assert rg.fine_smoother_iterations == ro.fine_smoother_iterations
+        assert rg.converged == ro.converged
+        assert rg.final_rel_residual == pytest.approx(ro.final_rel_residual, rel=TOL_REL_RES)
+        if ro.iterations > 0 or len(ro.history) > 1:
+            np.testing.assert_allclose(rg.history, ro.history[: len(rg.history)], rtol=1e-5)
+            assert len(rg.history) == len(ro.history)
+    assert np.abs(res.fields - ref).max() <= TOL_ABS
+
+
 def test_spacing_other_than_one():
     m, k = oracle.seeded_problem(120, 90, 0.05, 3)
     _compare(m, k, *_cfgs(16, 2), spacing=0.5)
