@@ -1365,6 +1365,7 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
         D.spacing = L.info.spacing;
         D.hinv2 = 1.0 / (L.info.spacing * L.info.spacing);
         D.robin = c.alpha / L.info.spacing;
+        D.g_in = 1.0 - D.robin / D.hinv2;
         PTRY(dev_upload(pl, xs, &D.xs));
         PTRY(dev_upload(pl, ys, &D.ys));
         PTRY(dev_upload(pl, wx, &D.wx));

@@ -13,6 +13,7 @@ struct LevelDev {
     int nx, ny, bw, bh;  // blocks per axis, block extent
     int nblocks;
     double spacing, hinv2, robin;  // robin = alpha / spacing (solvers.py:291)
+    double g_in;                   // ghost factor of an inner block side: 1 - robin / hinv2 = 1 - alpha * h
     const int *xs, *ys;            // block starts (partition.py:84-90)
     const double *wx, *wy;         // PoU weights (nx,bw), (ny,bh) (partition.py:137-154)
     // per-pixel cover tables along each axis: first covering block and count

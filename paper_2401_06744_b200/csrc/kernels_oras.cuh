@@ -442,7 +442,9 @@ oras_sweep_lean_kernel(const SweepArgs A, const unsigned *__restrict__ mtab) {
     const LevelDev &L = A.L;
     const int ix = blockIdx.x, iy = blockIdx.y, blk = iy * L.nx + ix;
     const int tid = threadIdx.x;
-    const unsigned mbits = mtab[((size_t)(p / A.channels) * L.nblocks + blk) * 64 + tid];
+    // frame of the problem (channels share the mask): constant divisors for gray / RGB
+    const int frame = A.channels == 3 ? p / 3 : (A.channels == 1 ? p : p / A.channels);
+    const unsigned mbits = mtab[((size_t)frame * L.nblocks + blk) * 64 + tid];
     // PoU weight rows of this block -> shared memory (consumed after the CG loop)
     {
         const double wv = tid < 32 ? L.wx[ix * BW + tid] : L.wy[iy * BH + tid - 32];
@@ -466,7 +468,7 @@ oras_sweep_lean_kernel(const SweepArgs A, const unsigned *__restrict__ mtab) {
     cg.eR = cg.lx == 7;
     cg.eT = cg.wg == 0 && cg.ly == 0;
     cg.eB = cg.wg == NWARP - 1 && cg.ly == 3;
-    const double g_in = 1.0 - L.robin / L.hinv2;  // 1 - alpha*h
+    const double g_in = L.g_in;  // 1 - alpha*h
     cg.gL = x0 > 0 ? g_in : 1.0;
     cg.gR = x0 + BW < W ? g_in : 1.0;
     cg.gT = y0 > 0 ? g_in : 1.0;
@@ -482,56 +484,87 @@ oras_sweep_lean_kernel(const SweepArgs A, const unsigned *__restrict__ mtab) {
     double r[TH][TW];
     {
         const double *urow = A.u + (size_t)p * A.plane + (size_t)(gy0 - 1) * W + gx0;
-        const bool hasL = gx0 > 0, hasR = gx0 + TW < W, hasT = gy0 > 0, hasB = gy0 + TH < H;
         double uc[TH + 2][TW + 2];
+        if (!border) {
+            // interior block: every halo element is inside the image
 #pragma unroll
-        for (int j = 0; j < TH + 2; ++j) {
-            const double *rp = urow + (size_t)j * W;
-            const bool rowin = (j > 0 || hasT) && (j < TH + 1 || hasB);
-            double2 a0 = make_double2(0.0, 0.0), a1 = a0;
-            if (rowin) {
-                a0 = *reinterpret_cast<const double2 *>(rp);
-                a1 = *reinterpret_cast<const double2 *>(rp + 2);
+            for (int j = 0; j < TH + 2; ++j) {
+                const double *rp = urow + (size_t)j * W;
+                const double2 a0 = *reinterpret_cast<const double2 *>(rp);
+                const double2 a1 = *reinterpret_cast<const double2 *>(rp + 2);
+                uc[j][1] = a0.x; uc[j][2] = a0.y; uc[j][3] = a1.x; uc[j][4] = a1.y;
+                if (j >= 1 && j <= TH) {
+                    uc[j][0] = rp[-1];
+                    uc[j][5] = rp[TW];
+                } else {
+                    uc[j][0] = uc[j][5] = 0.0;
+                }
             }
-            uc[j][1] = a0.x; uc[j][2] = a0.y; uc[j][3] = a1.x; uc[j][4] = a1.y;
-            uc[j][0] = uc[j][5] = 0.0;
-            if (j >= 1 && j <= TH) {
-                if (hasL) uc[j][0] = rp[-1];
-                if (hasR) uc[j][5] = rp[TW];
+        } else {
+            const bool hasL = gx0 > 0, hasR = gx0 + TW < W, hasT = gy0 > 0, hasB = gy0 + TH < H;
+#pragma unroll
+            for (int j = 0; j < TH + 2; ++j) {
+                const double *rp = urow + (size_t)j * W;
+                const bool rowin = (j > 0 || hasT) && (j < TH + 1 || hasB);
+                double2 a0 = make_double2(0.0, 0.0), a1 = a0;
+                if (rowin) {
+                    a0 = *reinterpret_cast<const double2 *>(rp);
+                    a1 = *reinterpret_cast<const double2 *>(rp + 2);
+                }
+                uc[j][1] = a0.x; uc[j][2] = a0.y; uc[j][3] = a1.x; uc[j][4] = a1.y;
+                uc[j][0] = uc[j][5] = 0.0;
+                if (j >= 1 && j <= TH) {
+                    if (hasL) uc[j][0] = rp[-1];
+                    if (hasR) uc[j][5] = rp[TW];
+                }
             }
         }
-        const double c4 = 4.0 * hinv2;
+        double bt[TH][TW];
 #pragma unroll
         for (int j = 0; j < TH; ++j) {
-            double bt[TW] = {0.0, 0.0, 0.0, 0.0};
             if (!RM) {
                 const double *bp = A.b + (size_t)p * A.plane + (size_t)(gy0 + j) * W + gx0;
                 const double2 b0 = *reinterpret_cast<const double2 *>(bp);
                 const double2 b1 = *reinterpret_cast<const double2 *>(bp + 2);
-                bt[0] = b0.x; bt[1] = b0.y; bt[2] = b1.x; bt[3] = b1.y;
-            } else if (general) {
+                bt[j][0] = b0.x; bt[j][1] = b0.y; bt[j][2] = b1.x; bt[j][3] = b1.y;
+            } else {
+                bt[j][0] = bt[j][1] = bt[j][2] = bt[j][3] = 0.0;
+            }
+        }
+        const double nc4 = -4.0 * hinv2;
+        // b - (d u - hinv2 s), d = (number of in-image neighbours) / h^2
+#pragma unroll
+        for (int j = 0; j < TH; ++j)
+#pragma unroll
+            for (int i = 0; i < TW; ++i) {
+                const double s = ((uc[j][i + 1] + uc[j + 2][i + 1]) + uc[j + 1][i]) + uc[j + 1][i + 2];
+                const double uu = uc[j + 1][i + 1];
+                const double res = fma(hinv2, s, RM ? nc4 * uu : fma(nc4, uu, bt[j][i]));
+                const bool m = (mbits >> (j * TW + i)) & 1u;
+                // RM: the right-hand side is where(mask, known, 0) and b - u == 0 at mask pixels
+                // unless `general` (fixed up below)
+                r[j][i] = m ? (RM ? 0.0 : bt[j][i] - uu) : res;
+            }
+        if (border) {
+            // image border: fewer in-image neighbours (reflecting boundary, core.py:59-67)
+#pragma unroll
+            for (int j = 0; j < TH; ++j)
+#pragma unroll
+                for (int i = 0; i < TW; ++i) {
+                    const int gy = gy0 + j, gx = gx0 + i;
+                    const double miss = (gy == 0 ? 1.0 : 0.0) + (gy == H - 1 ? 1.0 : 0.0) +
+                                        (gx == 0 ? 1.0 : 0.0) + (gx == W - 1 ? 1.0 : 0.0);
+                    const bool m = (mbits >> (j * TW + i)) & 1u;
+                    if (!m && miss != 0.0) r[j][i] = fma(miss * hinv2, uc[j + 1][i + 1], r[j][i]);
+                }
+        }
+        if (RM && general) {
+#pragma unroll
+            for (int j = 0; j < TH; ++j)
 #pragma unroll
                 for (int i = 0; i < TW; ++i)
                     if ((mbits >> (j * TW + i)) & 1u)
-                        bt[i] = A.b[(size_t)p * A.plane + (size_t)(gy0 + j) * W + gx0 + i];
-            }
-#pragma unroll
-            for (int i = 0; i < TW; ++i) {
-                const bool m = (mbits >> (j * TW + i)) & 1u;
-                const double s = ((uc[j][i + 1] + uc[j + 2][i + 1]) + uc[j + 1][i]) + uc[j + 1][i + 2];
-                double d = c4;
-                if (border) {
-                    const int gy = gy0 + j, gx = gx0 + i;
-                    const double cnt = 4.0 - (gy == 0 ? 1.0 : 0.0) - (gy == H - 1 ? 1.0 : 0.0) -
-                                       (gx == 0 ? 1.0 : 0.0) - (gx == W - 1 ? 1.0 : 0.0);
-                    d = cnt * hinv2;
-                }
-                const double uu = uc[j + 1][i + 1];
-                // b - (d u - hinv2 s)
-                const double res = fma(hinv2, s, fma(-d, uu, bt[i]));
-                if (RM) r[j][i] = m ? (general ? bt[i] - uu : 0.0) : res;
-                else r[j][i] = m ? (bt[i] - uu) : res;
-            }
+                        r[j][i] = A.b[(size_t)p * A.plane + (size_t)(gy0 + j) * W + gx0 + i] - uc[j + 1][i + 1];
         }
     }
 
