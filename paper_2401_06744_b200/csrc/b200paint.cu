@@ -895,7 +895,7 @@ static int enqueue_hierarchy(b200p_plan *pl, cudaStream_t st) {
         }
         {
             LaunchScope sc(pl, st, KK_DOWN_VALUES, field_bytes(pl, f, 1.25, 1.25));
-            downsample_values_kernel<<<grid2x(c.info.width, c.info.height, pl->P), ST_THREADS, 0, st>>>(
+            downsample_values_kernel<<<grid2x(c.info.width, c.info.height, pl->F), ST_THREADS, 0, st>>>(
                 f.d_mask, c.d_mask, f.d_rhs, h, w, pl->C, pl->cfg.value_downsampling, c.d_rhs);
             CU(cudaGetLastError());
         }

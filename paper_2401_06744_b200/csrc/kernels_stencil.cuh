@@ -442,23 +442,25 @@ downsample_mask_kernel(const uint8_t *__restrict__ fine, int h, int w, uint8_t *
 // 0 fall back to the plain average (:143-145); 0 off the coarse mask (:146).
 // Fine values are read only at fine mask pixels (level-0 `known` is arbitrary
 // elsewhere; hierarchy values are 0 there).
+// One thread per coarse pixel of a FRAME: the neighbour-suppression weights depend on the masks
+// only, so they are formed once and applied to all channels of the frame (grid z = frame).
 __global__ void __launch_bounds__(ST_THREADS)
 downsample_values_kernel(const uint8_t *__restrict__ fmask, const uint8_t *__restrict__ cmask,
                          const double *__restrict__ frhs, int h, int w, int channels, int modified,
                          double *__restrict__ crhs) {
-    const int p = blockIdx.z;
+    const int f = blockIdx.z;
     const int hc = (h + 1) >> 1, wc = (w + 1) >> 1;
     const int X = blockIdx.x * 64 + (threadIdx.x & 63);
     const int Y = blockIdx.y * 4 + (threadIdx.x >> 6);
     if (X >= wc || Y >= hc) return;
     const size_t fplane = (size_t)h * w, cplane = (size_t)hc * wc;
-    const uint8_t *fm = fmask + (size_t)(p / channels) * fplane;
-    const uint8_t *cm = cmask + (size_t)(p / channels) * cplane;
-    const double *fr = frhs + (size_t)p * fplane;
+    const uint8_t *fm = fmask + (size_t)f * fplane;
+    const uint8_t *cm = cmask + (size_t)f * cplane;
     const size_t ci = (size_t)Y * wc + X;
-    double out = 0.0;
-    if (cm[ci]) {
-        double wg[4] = {0, 0, 0, 0}, wv[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0}, nv[4] = {0, 0, 0, 0};
+    double wg[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
+    bool has[4] = {false, false, false, false};
+    const bool known = cm[ci] != 0;
+    if (known) {
 #pragma unroll
         for (int dy = 0; dy < 2; ++dy)
 #pragma unroll
@@ -467,7 +469,6 @@ downsample_values_kernel(const uint8_t *__restrict__ fmask, const uint8_t *__res
                 if (y >= h || x >= w) continue;
                 const size_t i = (size_t)y * w + x;
                 if (!fm[i]) continue;
-                const double val = fr[i];
                 double n = 0.0;
                 if (x >= 1) n += (x & 1) ? (double)(fm[i - 1] != 0) : (double)(cm[(size_t)Y * wc + (X - 1)] != 0);
                 if (x <= w - 2) n += !(x & 1) ? (double)(fm[i + 1] != 0) : (double)(cm[(size_t)Y * wc + (X + 1)] != 0);
@@ -475,22 +476,36 @@ downsample_values_kernel(const uint8_t *__restrict__ fmask, const uint8_t *__res
                 if (y <= h - 2) n += !(y & 1) ? (double)(fm[i + w] != 0) : (double)(cm[(size_t)(Y + 1) * wc + X] != 0);
                 const int k = dy * 2 + dx;
                 wg[k] = 4.0 - n;
-                wv[k] = wg[k] * val;
                 c1[k] = 1.0;
-                nv[k] = val;
+                has[k] = true;
             }
-        const double nnum = (nv[0] + nv[1]) + (nv[2] + nv[3]);
-        const double nden = (c1[0] + c1[1]) + (c1[2] + c1[3]);
-        const double naive = nnum / fmax(1.0, nden);
-        if (modified) {
-            const double num = (wv[0] + wv[1]) + (wv[2] + wv[3]);
-            const double den = (wg[0] + wg[1]) + (wg[2] + wg[3]);
-            out = den == 0.0 ? naive : num / fmax(1.0, den);
-        } else {
-            out = naive;
-        }
     }
-    crhs[(size_t)p * cplane + ci] = out;
+    const double nden = (c1[0] + c1[1]) + (c1[2] + c1[3]);
+    const double den = (wg[0] + wg[1]) + (wg[2] + wg[3]);
+    for (int c = 0; c < channels; ++c) {
+        const size_t p = (size_t)f * channels + c;
+        double out = 0.0;
+        if (known) {
+            const double *fr = frhs + p * fplane;
+            double nv[4] = {0, 0, 0, 0}, wv[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (has[k]) {
+                    const double val = fr[(size_t)(2 * Y + (k >> 1)) * w + 2 * X + (k & 1)];
+                    nv[k] = val;
+                    wv[k] = wg[k] * val;
+                }
+            const double nnum = (nv[0] + nv[1]) + (nv[2] + nv[3]);
+            const double naive = nnum / fmax(1.0, nden);
+            if (modified) {
+                const double num = (wv[0] + wv[1]) + (wv[2] + wv[3]);
+                out = den == 0.0 ? naive : num / fmax(1.0, den);
+            } else {
+                out = naive;
+            }
+        }
+        crhs[p * cplane + ci] = out;
+    }
 }
 
 // 8-bit ingest / egress (fileio.py:51-65): known = float(u8); out = clip(rint(u)).
