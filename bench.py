@@ -162,7 +162,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="4k_rgb_2pct_b32o6", choices=sorted(WORKLOADS))
-    ap.add_argument("--frames", type=int, default=4, help="frames per step per GPU")
+    ap.add_argument("--frames", type=int, default=8, help="frames per step per GPU")
     ap.add_argument("--lanes", type=int, default=4, help="host pipeline lanes for the e2e measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -320,7 +320,7 @@ def main():
         ms = prof["oras_sweep_split"][0] + prof["oras_combine"][0]
         n = prof["oras_sweep_split"][1]
         by = prof["oras_sweep_split"][2]
-        dom = "oras_sweep (K2 oras_sweep_tile_kernel + K2b oras_combine_kernel)"
+        dom = "oras_sweep (K2 oras_sweep_lean_kernel + K2b oras_combine_kernel)"
     else:
         dom = max(prof, key=lambda k: prof[k][0])
         ms, n, by = prof[dom]
@@ -329,15 +329,20 @@ def main():
     if os.path.exists(tp):
         try:
             with open(tp) as f:
-                traffic = json.load(f).get("oras_sweep", {}).get("dram_bytes_per_launch")
+                tj = json.load(f).get("oras_sweep", {})
+                traffic = tj.get("dram_bytes_per_launch")
+                if traffic is not None:  # the ncu launch list was taken with tj["frames"] frames per step
+                    traffic = traffic * F / float(tj.get("frames", F))
         except Exception:
             traffic = None
     roofline = {"bound": "hbm", "kernel": dom, "achieved": (by / n / 1e9) / (ms / n * 1e-3), "peak": peak,
                 "unit": "GB/s", "frac": ((by / 1e9) / (ms * 1e-3)) / peak, "traffic": traffic,
                 "peak_source": peak_src, "avg_launch_ms": ms / n, "alg_bytes_per_launch": by / n,
                 "share_of_step": ms / tot_ms,
-                "note": "the sweep is bound by the latency of the per-block CG recurrences (fp64 "
-                        "shuffles/reductions), not by HBM: see DESIGN.md and profiles/",
+                "note": "the sweep is bound by fp64 issue and by the dependent chains of the per-block CG "
+                        "(FP64 pipe 39 %, LSU data pipe 50 %, DRAM 18 % in ncu), not by HBM; its DRAM traffic "
+                        "is ~3x the algorithmic bytes because the weighted correction tiles make a round trip "
+                        "through HBM (K2 writes 1.5 fields, K2b reads them): see DESIGN.md and profiles/",
                 "how": "eager pass of the same step with a CUDA event pair around every launch on the "
                        "launching stream, run right after the timed (graph-replay) region"}
     frame_bytes = algorithmic_bytes_per_frame(W, H, C, max(cycles))
