@@ -35,6 +35,7 @@ WORKLOADS = {
     "4k_rgb_0.5pct_b32o6": (3840, 2160, 3, 0.005, 32, 6),
     "1080p_rgb_4pct_b16o2": (1920, 1080, 3, 0.04, 16, 2),
     "256_gray_5pct_b16o2": (256, 256, 1, 0.05, 16, 2),
+    "8k_rgb_2pct_b32o6": (7680, 4320, 3, 0.02, 32, 6),   # BASELINE config 4b frame size on ONE GPU (no strips)
 }
 METRIC = "4K colour frames/sec (FMG to fixed residual)"
 UNIT = "frames/s"
@@ -163,7 +164,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="4k_rgb_2pct_b32o6", choices=sorted(WORKLOADS))
     ap.add_argument("--frames", type=int, default=8, help="frames per step per GPU")
-    ap.add_argument("--lanes", type=int, default=4, help="host pipeline lanes for the e2e measurement")
+    ap.add_argument("--lanes", type=int, default=5, help="host pipeline lanes for the e2e measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true")

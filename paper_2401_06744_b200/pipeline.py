@@ -25,7 +25,7 @@ from .multigrid import MultigridConfig, Plan
 
 class FramePipeline:
     def __init__(self, width, height, channels, cfg: MultigridConfig | None = None, spacing=1.0,
-                 lanes: int = 4, frames_per_lane: int = 1):
+                 lanes: int = 5, frames_per_lane: int = 1):
         if lanes < 1 or frames_per_lane < 1:
             raise ValueError("need lanes >= 1 and frames_per_lane >= 1")
         _dev.require_cuda()

@@ -91,6 +91,18 @@ def test_config4_4k_sparse():
     assert res.reports[0].iterations > 2
 
 
+def test_8k_single_frame_one_gpu():
+    """The 8K frame of BASELINE config 4 (7680x4320, 2 %, block 32 / overlap 6) on ONE GPU, one
+    channel against the oracle; 296 x 166 = 49 136 blocks per sweep, 9 levels."""
+    m, k = oracle.seeded_problem(7680, 4320, 0.02, 0, channels=1)
+    cfg_o, cfg_b = _cfgs(32, 6)
+    res, ref, err = _compare(m, k, cfg_o, cfg_b)
+    _properties(m, k, res, cfg_b)
+    part = bp.build_partition(7680, 4320, 32, 6)
+    assert (part.nx, part.ny) == (296, 166)
+    assert len(bp.build_hierarchy(bp.InpaintingProblem(m, k), cfg_b)) == 9
+
+
 @pytest.mark.parametrize("w,h,dens,seed,bs,ov,kw", [
     (64, 64, 0.10, 1, 16, 2, dict(tol_rel=1e-8)),                  # tests/test_multigrid.py:328-334 setup
     (80, 56, 0.15, 8, 32, 6, dict(tol_rel=1e-6)),                  # clamped blocks on both axes
