@@ -44,6 +44,22 @@ def synthetic_image(width: int, height: int, seed: int = 0) -> np.ndarray:
     return np.ascontiguousarray(img, dtype=np.float64)  # fancy indexing above yields F-ordered data
 
 
+def step_edge_image(width: int, height: int, edge_x: int) -> np.ndarray:
+    """0 left of column edge_x, 255 from edge_x on (masks.py:70-74)."""
+    img = np.full((height, width), 255.0)
+    img[:, :edge_x] = 0.0
+    return img
+
+
+def edge_concentrated_mask(width: int, height: int, edge_x: int, background_density: float = 0.01,
+                           seed: int = 0) -> np.ndarray:
+    """Sparse background samples plus the three full columns edge_x-2 .. edge_x (masks.py:77-89):
+    the geometry in which plain 2x2 value averaging leaks across the edge."""
+    mask = np.random.default_rng(seed).random((height, width)) < background_density
+    mask[:, max(0, edge_x - 2):edge_x + 1] = True
+    return mask
+
+
 def seeded_problem(width: int, height: int, density: float, seed: int, channels: int = 1):
     """(mask (H,W) bool, known (C,H,W) float64): mask seed `seed`, channel c image seed+1000+c."""
     mask = random_mask(width, height, density, seed)

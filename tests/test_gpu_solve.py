@@ -321,3 +321,32 @@ def test_frame_pipeline_matches_batched_plan():
     with pytest.raises(bp.EmptyMaskError):
         pipe2.run(bad, known)
     pipe2.close()
+
+
+def test_bench_suites_on_the_cuda_path():
+    """the reference's bench suites (bench.py:60-175) on the CUDA path: row schema of
+    fileio.py:233-247, convergence at every density, modified value coarsening leaks less than naive
+    across a step edge (tests/test_multigrid.py:344-354), runtime grows with the pixel count."""
+    from paper_2401_06744_b200 import suites, synthetic
+    cfg = bp.MultigridConfig(block_size=16, overlap=2)
+    img = synthetic.synthetic_image(192, 128, 7)[None]
+    rows = suites.density_suite([img], cfg, densities=(0.02, 0.10), seeds=(0,))
+    assert len(rows) == 4 and all(tuple(r) == suites.ROW_FIELDS for r in rows)
+    assert {r["solver"] for r in rows} == {"mg-oras", "ml-oras"}
+    for r in rows:
+        assert r["rel_residual"] <= cfg.solver.tol_rel and r["mse_vs_reference"] < 1.0 and r["wall_time_s"] > 0
+    # ml-oras smooths every level to tolerance: more finest-level sweeps than mg-oras needs V-cycles
+    by = {(r["solver"], r["density"]): r for r in rows}
+    assert by[("ml-oras", 0.02)]["iterations"] > by[("mg-oras", 0.02)]["iterations"]
+    leak = {r["solver"]: r["mse_vs_reference"] for r in suites.downsampling_suite(cfg)}
+    assert leak["ml-oras+modified"] < leak["ml-oras+naive"]
+    arows = suites.alpha_suite(img, cfg, alphas=(0.1, 0.5, 5.0))
+    assert [r["alpha"] for r in arows] == [0.1, 0.5, 5.0] and all(r["rel_residual"] <= 1e-3 for r in arows)
+    sizes = ((240, 135), (960, 540), (1920, 1080))
+    rrows = [r for r in suites.resolution_suite(bp.MultigridConfig(), sizes=sizes, solvers=("mg-oras",))]
+    t = [r["wall_time_s"] for r in rrows]
+    assert t[0] < t[2]
+    slope = suites.loglog_slope([w * h for w, h in sizes], t)
+    assert 0.0 < slope < 1.5  # sub-linear while the small sizes are launch-latency bound
+    ranked = suites.compare_rows(bp.InpaintingProblem(synthetic.random_mask(192, 128, 0.05, 1), img), cfg)
+    assert ranked[0]["mse_vs_reference"] <= ranked[-1]["mse_vs_reference"]

@@ -23,6 +23,19 @@ def test_input_generators_are_bit_identical(diffpaint):
         assert np.array_equal(m, p.mask) and np.array_equal(k, p.known)
 
 
+def test_product_side_generators_match_reference(diffpaint):
+    """paper_2401_06744_b200.synthetic (benchmark inputs of bench.py and the suites) draws the same bits
+    as the reference's masks.py; importing it needs the built library, not a GPU."""
+    from paper_2401_06744_b200 import synthetic
+    for w, h, d, s in [(64, 48, 0.1, 0), (97, 131, 0.03, 2)]:
+        assert np.array_equal(synthetic.random_mask(w, h, d, s), diffpaint.random_mask(w, h, d, s))
+        assert np.array_equal(synthetic.synthetic_image(w, h, s), diffpaint.synthetic_image(w, h, s))
+    assert np.array_equal(synthetic.step_edge_image(40, 30, 13), diffpaint.masks.step_edge_image(40, 30, 13))
+    for ex in (0, 1, 13, 39):
+        assert np.array_equal(synthetic.edge_concentrated_mask(40, 30, ex, 0.05, 3),
+                              diffpaint.masks.edge_concentrated_mask(40, 30, ex, 0.05, 3))
+
+
 @pytest.mark.parametrize("seed", range(6))
 def test_stencil(diffpaint, seed):
     rng = np.random.default_rng(seed)
