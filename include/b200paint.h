@@ -62,7 +62,8 @@ typedef struct b200p_config {
     int use_graphs;               /* 1: replay cascade / V-cycle as CUDA graphs */
     int spec_cycles;              /* V-cycles enqueued between host convergence checks (>=1) */
     int mode;                     /* MultigridConfig.mode: 0 "full_multigrid" (mg-oras), 1 "multilevel" (ml-oras,
-                                     cascade with every level smoothed to tol_rel, multigrid.py:412-418, :449-464) */
+                                     cascade with every level smoothed to tol_rel, multigrid.py:412-418, :449-464),
+                                     2 "single": oras_solve on the finest level only (solvers.py:427-485) */
     int max_outer_iters;          /* SolverConfig.max_outer_iters (sweep cap per level in multilevel mode) */
 } b200p_config;
 

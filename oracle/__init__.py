@@ -281,6 +281,35 @@ def oras_sweeps(mask, spacing, block, overlap, alpha, b, u, *, max_sweeps, stop_
     return int(s), float(rn.value)
 
 
+def oras_solve(mask, known, spacing=1.0, block=32, overlap=6, cfg=None):
+    """oras_solve (solvers.py:427-485) from the flat initialisation, one channel: `known` (h,w).
+    Built from orc_oras_sweeps one sweep per call (each call ends with the residual evaluation
+    whose norm is the next history entry), so the iterates are those of one long call.
+    Returns (u, report dict with the SolveReport fields)."""
+    cfg = cfg or SolverConfig()
+    m = np.asarray(mask, dtype=bool)
+    b = np.where(m, np.asarray(known, dtype=np.float64), 0.0)
+    u = b.copy()
+    r0 = float(np.linalg.norm(residual(m, spacing, b, u)))
+    rep = dict(solver="oras", iterations=0, final_rel_residual=0.0, history=[0.0], converged=True,
+               baseline_residual=r0, init_residual=r0, fine_smoother_iterations=0)
+    if r0 == 0.0:
+        return u, rep
+    stop = cfg.tol_rel * r0
+    history, sweeps, rn = [1.0], 0, r0
+    while not (rn <= stop or sweeps >= cfg.max_outer_iters):
+        done, rn = oras_sweeps(m, spacing, block, overlap, cfg.alpha, b, u, max_sweeps=1, stop_norm=0.0,
+                               eta=cfg.local_tol_fraction, local_max_iters=cfg.local_max_iters)
+        if done == 0:  # rs == 0
+            break
+        sweeps += done
+        history.append(rn / r0)
+    rel = rn / r0
+    rep.update(iterations=sweeps, final_rel_residual=rel, history=history, converged=rel <= cfg.tol_rel,
+               fine_smoother_iterations=sweeps)
+    return u, rep
+
+
 # --------------------------------------------------------------- multigrid
 
 def downsample_mask(fine):

@@ -1021,6 +1021,83 @@ static int enqueue_vcycle(b200p_plan *pl, int level, UBuf &u, const double *b, b
     return settle_home ? settle(pl, L, u, home, st) : 0;
 }
 
+// _smooth_to_tol with the ORAS smoother on a multi-block level (multigrid.py:282-322): sweeps until
+// ||r|| <= tol_rel * denom per problem, denom = the level's flat-init defect, at most max_outer_iters.
+static int smooth_level_to_tol(b200p_plan *pl, LevelHost &f, UBuf &uf, bool record, cudaStream_t st) {
+    const b200p_config &cfg = pl->cfg;
+    const int nb = (pl->P + 127) / 128;
+    int rc;
+    // denom = ||b - A flat_init|| of this level (multigrid.py:413)
+    if ((rc = launch_norm(pl, f, f.d_rhs, f.d_rhs, true, true, nullptr, st))) return rc;
+    {
+        LaunchScope sc(pl, st, KK_CONTROL, 0.0);
+        ml_level_begin_kernel<<<nb, 128, 0, st>>>(pl->P, pl->d_rs, pl->d_denom, pl->d_gate, pl->d_sweeps);
+        CU(cudaGetLastError());
+    }
+    int it = 0;
+    for (;;) {
+        const int chunk = 4;
+        if ((rc = launch_set_int(pl, pl->d_any, 1, 0, st))) return rc;
+        for (int k = 0; k < chunk && it <= cfg.max_outer_iters; ++k, ++it) {
+            if ((rc = launch_norm(pl, f, uf.cur, f.d_rhs, false, true, pl->d_gate, st))) return rc;
+            {
+                LaunchScope sc(pl, st, KK_CONTROL, 0.0);
+                ml_gate_kernel<<<nb, 128, 0, st>>>(pl->P, pl->d_rs, cfg.tol_rel, cfg.max_outer_iters,
+                                                  pl->d_denom, pl->d_gate, pl->d_sweeps, pl->d_rel,
+                                                  pl->d_hist, pl->d_histlen, record ? 1 : 0, pl->d_any);
+                CU(cudaGetLastError());
+            }
+            if ((rc = launch_sweep(pl, f, uf, f.d_rhs, true, pl->d_gate, pl->d_sweeps, -1, st))) return rc;
+        }
+        CU(cudaMemcpyAsync(pl->h_any, pl->d_any, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        if (!*pl->h_any || it > cfg.max_outer_iters) break;
+    }
+    return 0;
+}
+
+// oras_solve (solvers.py:427-485), the single-level "oras" pipeline: ORAS sweeps on the finest
+// level from the flat initialisation until ||r|| <= tol_rel * ||r0||, at most max_outer_iters.
+__global__ void flat_init_kernel(const uint8_t *__restrict__ mask, const double *__restrict__ known,
+                                 size_t plane, int channels, size_t n, double *__restrict__ out) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const size_t p = i / plane, px = i - p * plane;
+    out[i] = mask[(p / channels) * plane + px] ? known[i] : 0.0;
+}
+
+static int run_single_level(b200p_plan *pl, double *d_out, cudaStream_t st) {
+    const int nl = (int)pl->lev.size();
+    const b200p_config &cfg = pl->cfg;
+    LevelHost &L0 = pl->lev[0];
+    const int nb = (pl->P + 127) / 128;
+    int rc;
+    if ((rc = pack_masks(pl, L0, st))) return rc;
+    if ((rc = launch_norm(pl, L0, L0.d_rhs, L0.d_rhs, true, true, nullptr, st))) return rc;
+    if ((rc = launch_control(pl, 0, st))) return rc;  // baseline = ||b - A flat_init||
+    if (nl == 1) {
+        if ((rc = launch_coarse(pl, L0, d_out, L0.d_rhs, true, 1, cfg.tol_rel, cfg.max_outer_iters, nullptr,
+                                pl->d_sweeps, 0, st, pl->d_rel, true)))
+            return rc;
+    } else {
+        const size_t plane = (size_t)L0.info.height * L0.info.width, n = plane * pl->P;
+        {
+            LaunchScope sc(pl, st, KK_CONVERT, 17.0 * n);
+            flat_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(L0.d_mask, L0.d_rhs, plane, pl->C, n, d_out);
+            CU(cudaGetLastError());
+        }
+        UBuf uf = level_ubuf(pl, 0, d_out);
+        if ((rc = smooth_level_to_tol(pl, L0, uf, true, st))) return rc;
+        if ((rc = settle(pl, L0, uf, d_out, st))) return rc;
+    }
+    {
+        LaunchScope sc(pl, st, KK_CONTROL, 0.0);
+        ml_finish_kernel<<<nb, 128, 0, st>>>(pl->P, pl->d_sweeps, pl->d_cycles, pl->d_units, pl->d_active);
+        CU(cudaGetLastError());
+    }
+    return 0;
+}
+
 // fmg_solve in "multilevel" mode (ml-oras; multigrid.py:449-464 with _cascade(to_tol=True),
 // :389-418): coarsest level to min(coarse_tol, tol_rel); every finer level is initialised by
 // prolongate_solution and smoothed until ||r|| <= tol_rel * (flat-init defect of that level),
@@ -1058,32 +1135,7 @@ static int run_multilevel(b200p_plan *pl, double *d_out, cudaStream_t st) {
                     coarse_u, f.d_mask, f.d_rhs, f.info.height, f.info.width, pl->C, nullptr, uf.cur);
                 CU(cudaGetLastError());
             }
-            // denom = ||b - A flat_init|| of this level (multigrid.py:413)
-            if ((rc = launch_norm(pl, f, f.d_rhs, f.d_rhs, true, true, nullptr, st))) return rc;
-            {
-                LaunchScope sc(pl, st, KK_CONTROL, 0.0);
-                ml_level_begin_kernel<<<nb, 128, 0, st>>>(pl->P, pl->d_rs, pl->d_denom, pl->d_gate, pl->d_sweeps);
-                CU(cudaGetLastError());
-            }
-            int it = 0;
-            for (;;) {
-                const int chunk = 4;
-                if ((rc = launch_set_int(pl, pl->d_any, 1, 0, st))) return rc;
-                for (int k = 0; k < chunk && it <= cfg.max_outer_iters; ++k, ++it) {
-                    if ((rc = launch_norm(pl, f, uf.cur, f.d_rhs, false, true, pl->d_gate, st))) return rc;
-                    {
-                        LaunchScope sc(pl, st, KK_CONTROL, 0.0);
-                        ml_gate_kernel<<<nb, 128, 0, st>>>(pl->P, pl->d_rs, cfg.tol_rel, cfg.max_outer_iters,
-                                                          pl->d_denom, pl->d_gate, pl->d_sweeps, pl->d_rel,
-                                                          pl->d_hist, pl->d_histlen, l == 0 ? 1 : 0, pl->d_any);
-                        CU(cudaGetLastError());
-                    }
-                    if ((rc = launch_sweep(pl, f, uf, f.d_rhs, true, pl->d_gate, pl->d_sweeps, -1, st))) return rc;
-                }
-                CU(cudaMemcpyAsync(pl->h_any, pl->d_any, sizeof(int), cudaMemcpyDeviceToHost, st));
-                CU(cudaStreamSynchronize(st));
-                if (!*pl->h_any || it > cfg.max_outer_iters) break;
-            }
+            if ((rc = smooth_level_to_tol(pl, f, uf, l == 0, st))) return rc;
             if ((rc = settle(pl, f, uf, home, st))) return rc;
             coarse_u = home;
         }
@@ -1317,7 +1369,7 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
         return fail_arg(B200P_ERR_ARG, "unknown value downsampling %d", c.value_downsampling);
     if (c.v_cycles_max < 0 || c.coarse_max_iters < 0 || c.local_max_iters < 0 || c.max_outer_iters < 0)
         return fail_arg(B200P_ERR_ARG, "iteration caps must be >= 0");
-    if (c.mode != 0 && c.mode != 1) return fail_arg(B200P_ERR_ARG, "unknown mode %d", c.mode);
+    if (c.mode < 0 || c.mode > 2) return fail_arg(B200P_ERR_ARG, "unknown mode %d", c.mode);
 
     int ndev = 0;
     CU(cudaGetDeviceCount(&ndev));
@@ -1647,8 +1699,8 @@ int b200p_solve_async(b200p_plan *pl, const uint8_t *d_mask, const double *d_kno
     }
     bind_level0(pl, d_mask, d_known);
     int rc;
-    if (pl->cfg.mode == 1) {
-        if ((rc = run_multilevel(pl, d_out, st))) return rc;
+    if (pl->cfg.mode != 0) {
+        if ((rc = pl->cfg.mode == 1 ? run_multilevel(pl, d_out, st) : run_single_level(pl, d_out, st))) return rc;
         pl->hierarchy_ready = true;
         if ((rc = enqueue_reports(pl, st))) return rc;
         pl->pending = true;

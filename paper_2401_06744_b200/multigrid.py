@@ -65,7 +65,7 @@ class Plan:
     """RAII wrapper of a ``b200p_plan`` (geometry, scratch, CUDA graphs)."""
 
     def __init__(self, width, height, channels=1, frames=1, cfg=None, spacing=1.0,
-                 use_graphs=True, spec_cycles=1):
+                 use_graphs=True, spec_cycles=1, single_level=False):
         cfg = cfg or MultigridConfig()
         _require_hot_path(cfg)
         _dev.require_cuda()
@@ -82,7 +82,9 @@ class Plan:
         c.local_max_iters = int(s.local_max_iters or 0)
         c.use_graphs = 1 if use_graphs else 0
         c.spec_cycles = int(spec_cycles)
-        c.mode = 1 if cfg.mode == "multilevel" else 0
+        # single_level: oras_solve on the finest level only (the "oras" pipeline, solvers.py:427-485)
+        c.mode = 2 if single_level else (1 if cfg.mode == "multilevel" else 0)
+        self.single_level = bool(single_level)
         c.max_outer_iters = int(s.max_outer_iters)
         self.config = c
         self.cfg = cfg
@@ -135,7 +137,7 @@ class Plan:
     # -- solves
     def _reports(self, raw, wall):
         reps = []
-        name = "ml-oras" if self.cfg.mode == "multilevel" else "mg-oras"
+        name = "oras" if self.single_level else ("ml-oras" if self.cfg.mode == "multilevel" else "mg-oras")
         for r in raw:
             reps.append(SolveReport(
                 solver=name, iterations=r.iterations, final_rel_residual=r.final_rel_residual,
@@ -216,14 +218,14 @@ def _cfg_key(cfg):
             s.local_tol_fraction, s.local_max_iters, cfg.mode, s.max_outer_iters)
 
 
-def cached_plan(width, height, channels, frames, cfg, spacing=1.0) -> Plan:
+def cached_plan(width, height, channels, frames, cfg, spacing=1.0, single_level=False) -> Plan:
     """Plans are expensive (device scratch + graph capture); reuse by configuration."""
-    key = (width, height, channels, frames, float(spacing), _cfg_key(cfg))
+    key = (width, height, channels, frames, float(spacing), _cfg_key(cfg), bool(single_level))
     plan = _PLAN_CACHE.pop(key, None)
     if plan is None:
         while len(_PLAN_CACHE) >= _PLAN_CACHE_MAX:
             _PLAN_CACHE.pop(next(iter(_PLAN_CACHE))).close()
-        plan = Plan(width, height, channels, frames, cfg, spacing)
+        plan = Plan(width, height, channels, frames, cfg, spacing, single_level=single_level)
     _PLAN_CACHE[key] = plan
     return plan
 

@@ -2,8 +2,8 @@
 
 ``solve_image(problem, "mg-oras", cfg)`` has the reference's signature, result
 type and error behaviour (pipelines.py:20-114).  The ORAS-smoothed pipelines are
-built: "mg-oras" (the hot path) and "ml-oras" (cascadic multilevel, the paper's
-comparison variant, same kernels); the other names of the reference are
+built: "mg-oras" (the hot path), "ml-oras" (cascadic multilevel) and "oras"
+(single-level Schwarz iteration), the paper's comparison variants on the same kernels; the other names of the reference are
 recognised and rejected with NotImplementedError (out of scope).
 ``solve_frames`` is the batched entry (frames x channels in one plan).
 """
@@ -20,7 +20,7 @@ from .multigrid import LevelHierarchy, MultigridConfig, build_hierarchy, cached_
 from .solvers import SolveReport
 
 SOLVER_NAMES = ("cg", "oras", "ml-cg", "ml-oras", "mg-cg", "mg-oras")
-BUILT = ("mg-oras", "ml-oras")
+BUILT = ("mg-oras", "ml-oras", "oras")
 
 
 def split_solver_name(name: str):
@@ -73,6 +73,12 @@ def solve_channel(problem: InpaintingProblem, name: str, cfg: MultigridConfig | 
     """pipelines.py:42-72 for "mg-oras"."""
     _require_built(name)
     base, mode = split_solver_name(name)
+    if mode == "single":
+        if callback is not None:
+            raise NotImplementedError("per-sweep callbacks are not available on the CUDA path")
+        sub = InpaintingProblem(problem.mask, problem.known[channel], problem.spacing)
+        res = solve_image(sub, name, cfg)
+        return res.fields[0], res.reports[0]
     cfg = replace(cfg or MultigridConfig(), smoother=base, mode=mode)
     if hierarchy is None:
         hierarchy = build_hierarchy(problem, cfg)
@@ -88,12 +94,14 @@ def solve_image(problem: InpaintingProblem, name: str = "mg-oras",
     """
     _require_built(name)
     base, mode = split_solver_name(name)
-    cfg = replace(cfg or MultigridConfig(), smoother=base, mode=mode)
+    single = mode == "single"  # "oras": oras_solve on the finest level (solvers.py:427-485)
+    cfg = cfg or MultigridConfig()
+    cfg = replace(cfg, smoother=base) if single else replace(cfg, smoother=base, mode=mode)
     if not problem.mask.any():
         raise EmptyMaskError("cannot solve without known pixels")
     t0 = time.perf_counter()
     h, w = problem.shape
-    plan = cached_plan(w, h, problem.channels, 1, cfg, problem.spacing)
+    plan = cached_plan(w, h, problem.channels, 1, cfg, problem.spacing, single_level=single)
     out, reports = plan.solve_host(problem.mask.view(np.uint8)[None], problem.known[None])
     elapsed = time.perf_counter() - t0
     for r in reports:

@@ -152,6 +152,30 @@ def test_ml_oras_matches_oracle(w, h, dens, seed, bs, ov, kw):
     assert np.abs(res.fields - ref).max() <= TOL_ABS
 
 
+@pytest.mark.parametrize("w,h,dens,seed,bs,ov,kw", [
+    (96, 64, 0.10, 1, 16, 2, dict()),
+    (300, 200, 0.02, 4, 32, 6, dict(tol_rel=1e-5)),
+    (97, 131, 0.03, 2, 16, 2, dict(max_outer_iters=3)),     # sweep cap: converged False
+    (24, 20, 0.20, 2, 32, 6, dict(tol_rel=1e-6)),           # one block
+])
+def test_single_level_oras_matches_oracle(w, h, dens, seed, bs, ov, kw):
+    """The single-level Schwarz iteration "oras" (oras_solve, solvers.py:427-485) from the flat init."""
+    m, k = oracle.seeded_problem(w, h, dens, seed, channels=2)
+    cfg_b = bp.MultigridConfig(block_size=bs, overlap=ov, solver=bp.SolverConfig(**kw))
+    res = bp.solve_image(bp.InpaintingProblem(m, k), "oras", cfg_b)
+    for c in range(2):
+        uo, ro = oracle.oras_solve(m, k[c], 1.0, bs, ov, oracle.SolverConfig(**kw))
+        rg = res.reports[c]
+        assert rg.solver == "oras" and rg.iterations == ro["iterations"] == rg.fine_smoother_iterations
+        assert rg.converged == ro["converged"]
+        assert rg.final_rel_residual == pytest.approx(ro["final_rel_residual"], rel=TOL_REL_RES)
+        np.testing.assert_allclose(rg.history, ro["history"], rtol=1e-6)
+        assert rg.baseline_residual == pytest.approx(ro["baseline_residual"], rel=1e-12)
+        assert np.abs(res.fields[c] - uo).max() <= TOL_ABS
+    u1, r1 = bp.solve_channel(bp.InpaintingProblem(m, k), "oras", cfg_b, channel=1)
+    assert np.array_equal(u1, res.fields[1]) and r1.iterations == res.reports[1].iterations
+
+
 def test_spacing_other_than_one():
     m, k = oracle.seeded_problem(120, 90, 0.05, 3)
     _compare(m, k, *_cfgs(16, 2), spacing=0.5)
@@ -331,8 +355,8 @@ def test_bench_suites_on_the_cuda_path():
     cfg = bp.MultigridConfig(block_size=16, overlap=2)
     img = synthetic.synthetic_image(192, 128, 7)[None]
     rows = suites.density_suite([img], cfg, densities=(0.02, 0.10), seeds=(0,))
-    assert len(rows) == 4 and all(tuple(r) == suites.ROW_FIELDS for r in rows)
-    assert {r["solver"] for r in rows} == {"mg-oras", "ml-oras"}
+    assert len(rows) == 6 and all(tuple(r) == suites.ROW_FIELDS for r in rows)
+    assert {r["solver"] for r in rows} == {"mg-oras", "ml-oras", "oras"}
     for r in rows:
         assert r["rel_residual"] <= cfg.solver.tol_rel and r["mse_vs_reference"] < 1.0 and r["wall_time_s"] > 0
     # ml-oras smooths every level to tolerance: more finest-level sweeps than mg-oras needs V-cycles

@@ -178,3 +178,23 @@ def test_oracle_vs_dense_lu(diffpaint):
                                 oracle.MultigridConfig(block_size=16, overlap=2,
                                                        solver=oracle.SolverConfig(tol_rel=1e-8)))
     assert float(np.mean((out[0] - truth) ** 2)) <= 1e-10
+
+
+@pytest.mark.parametrize("w,h,d,s,bs,ov,kw", [
+    (96, 64, 0.10, 1, 16, 2, {}),
+    (120, 90, 0.05, 3, 32, 6, {"tol_rel": 1e-5}),
+    (100, 80, 0.02, 5, 16, 2, {"max_outer_iters": 3}),
+    (24, 20, 0.20, 2, 32, 6, {"tol_rel": 1e-6}),
+])
+def test_oras_solve_single_level(diffpaint, w, h, d, s, bs, ov, kw):
+    """oracle.oras_solve (the single-level "oras" pipeline) == solvers.py:427-485."""
+    m = diffpaint.random_mask(w, h, d, s)
+    k = diffpaint.synthetic_image(w, h, s + 1000)
+    part = diffpaint.build_partition(w, h, bs, ov)
+    u, rep = diffpaint.oras_solve(diffpaint.InpaintingProblem(m, k), 0, part=part,
+                                  weights=diffpaint.build_weights(part), cfg=diffpaint.SolverConfig(**kw))
+    uo, ro = oracle.oras_solve(m, k, 1.0, bs, ov, oracle.SolverConfig(**kw))
+    assert ro["iterations"] == rep.iterations and ro["converged"] == rep.converged
+    assert ro["final_rel_residual"] == pytest.approx(rep.final_rel_residual, rel=1e-9)
+    np.testing.assert_allclose(ro["history"], rep.history, rtol=1e-9)
+    np.testing.assert_allclose(uo, u, rtol=0, atol=1e-10)
