@@ -46,6 +46,7 @@ class _Cfg(C.Structure):
         ("tol_rel", C.c_double), ("max_outer_iters", C.c_int),
         ("alpha", C.c_double), ("eta", C.c_double),
         ("local_max_iters", C.c_int), ("threads", C.c_int),
+        ("smoother", C.c_int), ("smoother_cg_iters", C.c_int),
     ]
 
 
@@ -145,8 +146,8 @@ class SolveReport:
 def _cfg(cfg, threads: int = 0) -> _Cfg:
     """Accepts this module's configs or the reference's own (duck-typed)."""
     cfg = cfg or MultigridConfig()
-    if cfg.smoother != "oras":
-        raise ValueError("the oracle restates the ORAS-smoothed pipelines only")
+    if cfg.smoother not in ("oras", "cg"):
+        raise ValueError(f"unknown smoother {cfg.smoother!r}")
     s = cfg.solver
     return _Cfg(
         cfg.nu_pre, cfg.nu_post, cfg.v_cycles_max,
@@ -155,6 +156,7 @@ def _cfg(cfg, threads: int = 0) -> _Cfg:
         cfg.block_size, cfg.overlap, cfg.coarse_tol, cfg.coarse_max_iters,
         s.tol_rel, s.max_outer_iters, s.alpha, s.local_tol_fraction,
         int(s.local_max_iters or 0), threads,
+        1 if cfg.smoother == "cg" else 0, int(s.smoother_cg_iters),
     )
 
 
@@ -460,7 +462,7 @@ def fmg_solve(hier: Hierarchy, cfg=None, channel=0, threads=0):
     rc = lib().orc_fmg_solve(hier._h, C.byref(c), C.c_int(channel), _p(u), C.byref(rep))
     if rc != 0:
         raise ValueError("cannot solve without known pixels")
-    return u, _report(rep, ("ml-" if cfg.mode == "multilevel" else "mg-") + "oras")
+    return u, _report(rep, ("ml-" if cfg.mode == "multilevel" else "mg-") + cfg.smoother)
 
 
 def solve_image(mask, known, spacing=1.0, cfg=None, threads=0):
@@ -476,8 +478,22 @@ def solve_image(mask, known, spacing=1.0, cfg=None, threads=0):
                                C.c_double(spacing), C.byref(c), _p(out), reps)
     if rc != 0:
         raise ValueError("cannot solve without known pixels")
-    name = ("ml-" if cfg.mode == "multilevel" else "mg-") + "oras"
+    name = ("ml-" if cfg.mode == "multilevel" else "mg-") + cfg.smoother
     return out, [_report(r, name) for r in reps]
+
+
+def cg_solve(mask, known, spacing=1.0, cfg=None):
+    """cg_solve (solvers.py:140-186) from the flat initialisation, one channel: known (h,w).
+    Returns (u, SolveReport)."""
+    cfg = cfg or SolverConfig()
+    m, k = _u8(mask), _f64(known)
+    u = np.empty_like(k)
+    rep = _Report()
+    rc = lib().orc_cg_solve(_p(m), _p(k), C.c_int(m.shape[0]), C.c_int(m.shape[1]), C.c_double(spacing),
+                            C.c_double(cfg.tol_rel), C.c_int(cfg.max_outer_iters), _p(u), C.byref(rep))
+    if rc != 0:
+        raise ValueError("cannot solve without known pixels")
+    return u, _report(rep, "cg")
 
 
 def counters_reset():

@@ -47,6 +47,8 @@ typedef struct {
     double alpha, eta;
     int local_max_iters; /* 0 = None -> 4 * block area */
     int threads;         /* <=0: all cores */
+    int smoother;        /* 0 "oras", 1 "cg" (multigrid.py:66, :278-279, :323-331) */
+    int smoother_cg_iters; /* SolverConfig.smoother_cg_iters: CG steps per smoothing unit */
 } orc_cfg;
 
 typedef struct {
@@ -617,9 +619,46 @@ static int local_cap(const orc_cfg *cfg, const orc_level *L) {
     return cfg->local_max_iters > 0 ? cfg->local_max_iters : 4 * L->bh * L->bw;
 }
 
-/* multigrid.py:264-279 _smooth (ORAS branch). */
+/* solvers.py:97-128 _cg_run with the level operator: plain CG, u in place.  Returns the steps;
+ * *rn_out = final residual norm; history (optional) receives sqrt(rs_new) after every step. */
+static int cg_run(const orc_level *L, const double *b, double *u, int max_steps, double stop_norm,
+                  double *rn_out, double *history, int hist_cap, int *hist_len) {
+    const size_t N = (size_t)L->h * L->w;
+    double *r = (double *)malloc(sizeof(double) * N * 3), *p = r + N, *q = p + N;
+    orc_residual(L->mask, L->h, L->w, L->spacing, b, u, r);
+    double rs = orc_dot(r, r, N);
+    int steps = 0;
+    if (!(rs == 0.0 || sqrt(rs) <= stop_norm)) {
+        memcpy(p, r, sizeof(double) * N);
+        while (steps < max_steps) {
+            orc_apply(L->mask, L->h, L->w, L->spacing, p, q);
+            const double pq = orc_dot(p, q, N);
+            if (pq <= 0.0) break;
+            const double alpha = rs / pq;
+            for (size_t i = 0; i < N; ++i) u[i] += alpha * p[i];
+            for (size_t i = 0; i < N; ++i) r[i] -= alpha * q[i];
+            const double rs_new = orc_dot(r, r, N);
+            ++steps;
+            if (history && hist_len && *hist_len < hist_cap) history[(*hist_len)++] = sqrt(rs_new);
+            if (rs_new == 0.0 || sqrt(rs_new) <= stop_norm) { rs = rs_new; break; }
+            const double beta = rs_new / rs;
+            for (size_t i = 0; i < N; ++i) { p[i] *= beta; p[i] += r[i]; }
+            rs = rs_new;
+        }
+    }
+    if (rn_out) *rn_out = sqrt(rs);
+    free(r);
+    return steps;
+}
+
+/* multigrid.py:264-279 _smooth. */
 static int smooth(const orc_level *L, double *u, const double *rhs, int units, const orc_cfg *cfg) {
     if (units <= 0) return 0;
+    if (cfg->smoother == 1) {
+        const int k = cfg->smoother_cg_iters;
+        const int steps = cg_run(L, rhs, u, units * k, 0.0, NULL, NULL, 0, NULL);
+        return (steps + k - 1) / k;  /* -(-steps // k) */
+    }
     orc_blocks B = level_blocks(L, cfg->alpha);
     return oras_sweeps_impl(&B, rhs, u, units, 0.0, cfg->eta, local_cap(cfg, L), cfg->threads,
                             NULL, NULL, 0, NULL);
@@ -638,6 +677,22 @@ static int smooth_to_tol(const orc_level *L, double *u, const double *rhs, doubl
         free(r);
     }
     if (denom == 0.0) { if (rel_out) *rel_out = 0.0; return 0; }
+    if (cfg->smoother == 1) {
+        /* multigrid.py:318-331: the state before the first step, then one entry per CG step */
+        const int h0 = hist_len ? *hist_len : 0;
+        if (history && hist_len && *hist_len < hist_cap) {
+            double *r = (double *)malloc(sizeof(double) * N);
+            orc_residual(L->mask, L->h, L->w, L->spacing, rhs, u, r);
+            history[(*hist_len)++] = sqrt(orc_dot(r, r, N));
+            free(r);
+        }
+        double rn;
+        const int steps = cg_run(L, rhs, u, max_units, tol * denom, &rn, history, hist_cap, hist_len);
+        if (history && hist_len)
+            for (int i = h0; i < *hist_len; ++i) history[i] /= denom;
+        if (rel_out) *rel_out = rn / denom;
+        return steps;
+    }
     orc_blocks B = level_blocks(L, cfg->alpha);
     const int h0 = hist_len ? *hist_len : 0;
     double rn;
@@ -792,6 +847,39 @@ int orc_solve_image(const uint8_t *mask, const double *known, int h, int w, int 
         rc = orc_fmg_solve(H, cfg, c, out + (size_t)c * h * w, &reports[c]);
     orc_hier_free(H);
     return rc;
+}
+
+/* cg_solve (solvers.py:140-186) from the flat initialisation, one channel: known is (h,w).
+ * history[0] = 1, then rn/r0 per step. */
+int orc_cg_solve(const uint8_t *mask, const double *known, int h, int w, double spacing, double tol_rel,
+                 int max_outer_iters, double *u, orc_report *rep) {
+    const size_t N = (size_t)h * w;
+    orc_level L;
+    memset(&L, 0, sizeof L);
+    L.h = h; L.w = w; L.spacing = spacing; L.mask = (uint8_t *)mask;
+    double *b = (double *)malloc(sizeof(double) * N * 2), *t = b + N;
+    int any = 0;
+    for (size_t i = 0; i < N; ++i) { b[i] = mask[i] ? known[i] : 0.0; any |= mask[i]; u[i] = b[i]; }
+    memset(rep, 0, sizeof *rep);
+    if (!any) { free(b); return -1; }
+    orc_residual(mask, h, w, spacing, b, u, t);
+    const double r0 = sqrt(orc_dot(t, t, N));
+    rep->baseline = r0; rep->init_res = r0;
+    if (r0 == 0.0) {
+        rep->history[0] = 0.0; rep->history_len = 1; rep->converged = 1;
+        free(b);
+        return 0;
+    }
+    rep->history[0] = r0; rep->history_len = 1;
+    double rn;
+    const int steps = cg_run(&L, b, u, max_outer_iters, tol_rel * r0, &rn, rep->history, ORC_MAX_HIST,
+                             &rep->history_len);
+    for (int i = 0; i < rep->history_len; ++i) rep->history[i] /= r0;
+    rep->iterations = steps; rep->fine_units = steps;
+    rep->final_rel = rn / r0;
+    rep->converged = rep->final_rel <= tol_rel;
+    free(b);
+    return 0;
 }
 
 int orc_max_threads(void) { return orc_nthreads(0); }

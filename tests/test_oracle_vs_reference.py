@@ -198,3 +198,36 @@ def test_oras_solve_single_level(diffpaint, w, h, d, s, bs, ov, kw):
     assert ro["final_rel_residual"] == pytest.approx(rep.final_rel_residual, rel=1e-9)
     np.testing.assert_allclose(ro["history"], rep.history, rtol=1e-9)
     np.testing.assert_allclose(uo, u, rtol=0, atol=1e-10)
+
+
+@pytest.mark.parametrize("w,h,d,s,bs,ov,mode,kw", [
+    (96, 64, 0.10, 1, 16, 2, "full_multigrid", {}),
+    (160, 120, 0.05, 3, 32, 6, "multilevel", {}),
+    (97, 131, 0.03, 2, 16, 2, "full_multigrid", {"tol_rel": 1e-6}),
+    (20, 30, 0.20, 3, 32, 6, "full_multigrid", {"tol_rel": 1e-6}),   # single level
+    (128, 128, 0.05, 6, 16, 2, "multilevel", {"max_outer_iters": 4}),
+])
+def test_cg_smoothed_pipelines(diffpaint, w, h, d, s, bs, ov, mode, kw):
+    """The oracle's CG smoother (multigrid.py:278-279, :323-331; _cg_run solvers.py:97-128) and
+    cg_solve (solvers.py:140-186) against the reference: mg-cg, ml-cg, cg."""
+    dp = diffpaint
+    m = dp.random_mask(w, h, d, s)
+    k = np.stack([dp.synthetic_image(w, h, s + 1000 + c) for c in range(2)])
+    name = ("ml-" if mode == "multilevel" else "mg-") + "cg"
+    res = dp.solve_image(dp.InpaintingProblem(m, k), name,
+                         dp.MultigridConfig(block_size=bs, overlap=ov, smoother="cg", mode=mode,
+                                            solver=dp.SolverConfig(**kw)))
+    out, reps = oracle.solve_image(m, k, 1.0, oracle.MultigridConfig(
+        block_size=bs, overlap=ov, smoother="cg", mode=mode, solver=oracle.SolverConfig(**kw)))
+    for c in range(2):
+        a, b = res.reports[c], reps[c]
+        assert (b.solver, b.iterations, b.fine_smoother_iterations, b.converged) == \
+               (a.solver, a.iterations, a.fine_smoother_iterations, a.converged)
+        assert b.final_rel_residual == pytest.approx(a.final_rel_residual, rel=1e-6)
+        np.testing.assert_allclose(b.history, a.history, rtol=1e-6)
+        np.testing.assert_allclose(out[c], res.fields[c], rtol=0, atol=1e-9)
+    u, rep = dp.cg_solve(dp.InpaintingProblem(m, k), 1, cfg=dp.SolverConfig(**kw))
+    uo, ro = oracle.cg_solve(m, k[1], 1.0, oracle.SolverConfig(**kw))
+    assert (ro.iterations, ro.converged) == (rep.iterations, rep.converged)
+    np.testing.assert_allclose(ro.history, rep.history, rtol=1e-6)
+    np.testing.assert_allclose(uo, u, rtol=0, atol=1e-9)
