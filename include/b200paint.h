@@ -65,6 +65,9 @@ typedef struct b200p_config {
                                      cascade with every level smoothed to tol_rel, multigrid.py:412-418, :449-464),
                                      2 "single": oras_solve on the finest level only (solvers.py:427-485) */
     int max_outer_iters;          /* SolverConfig.max_outer_iters (sweep cap per level in multilevel mode) */
+    int smoother;                 /* MultigridConfig.smoother: 0 "oras" (the hot path), 1 "cg" (_cg_run,
+                                     solvers.py:97-128: the comparison pipelines cg / ml-cg / mg-cg) */
+    int smoother_cg_iters;        /* SolverConfig.smoother_cg_iters: CG steps per smoothing unit */
 } b200p_config;
 
 /* SolveReport (solvers.py:72-94), one per (frame, channel). */

@@ -35,6 +35,7 @@ class Config(C.Structure):
         ("tol_rel", C.c_double), ("alpha", C.c_double), ("eta", C.c_double),
         ("local_max_iters", C.c_int), ("use_graphs", C.c_int), ("spec_cycles", C.c_int),
         ("mode", C.c_int), ("max_outer_iters", C.c_int),
+        ("smoother", C.c_int), ("smoother_cg_iters", C.c_int),
     ]
 
 

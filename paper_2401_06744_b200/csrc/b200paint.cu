@@ -24,6 +24,7 @@
 #include "kernels_rows.cuh"
 #include "kernels_oras.cuh"
 #include "kernels_oras_tma.cuh"
+#include "kernels_cg.cuh"
 
 using namespace b200p;
 
@@ -144,13 +145,14 @@ enum KernelKind {
     KK_COARSE,        // K7
     KK_CONTROL,       // per-problem bookkeeping
     KK_CONVERT,       // u8 ingest / egress
+    KK_CG,            // global CG field kernels (comparison pipelines)
     KK_COUNT
 };
 
 static const char *const kKindNames[KK_COUNT] = {
     "residual_sqnorm", "oras_sweep", "oras_sweep_split", "oras_combine", "residual_restrict", "prolongate_correct",
     "prolongate_solution", "downsample_mask", "downsample_values", "coarse_solve", "control",
-    "convert_u8"};
+    "convert_u8", "global_cg"};
 
 struct LevelHost {
     b200p_level_info info;
@@ -229,6 +231,9 @@ struct b200p_plan {
     cudaStream_t pending_stream = nullptr;
     bool pending = false;
     bool pending_eager = false;  // the pending solve ran eagerly (launches already counted)
+    // CG-smoothed pipelines (cg, ml-cg, mg-cg): CG vectors sized for level 0 + per-problem state
+    double *cg_r = nullptr, *cg_p = nullptr, *cg_q = nullptr;
+    CgState cgs = {};
     GraphSlot g_solve;
     int64_t cycle_kernels = 0;   // kernel nodes of one WHILE body pass
     // staging for the host entry points
@@ -1021,6 +1026,251 @@ static int enqueue_vcycle(b200p_plan *pl, int level, UBuf &u, const double *b, b
     return settle_home ? settle(pl, L, u, home, st) : 0;
 }
 
+// ====================================================================== CG pipelines ====
+// The paper's comparison pipelines "cg", "ml-cg", "mg-cg": the same multigrid
+// driver with _cg_run (solvers.py:97-128) as smoother / coarse solver.  Eager launches; the
+// host reads the gates every few CG steps.
+constexpr int CG_CTAS = 592;  // CTAs per problem of the flat CG kernels (4 per SM)
+
+static CgArgs cg_args(b200p_plan *pl, const LevelHost &L, double *u, const double *b) {
+    CgArgs A;
+    A.mask = L.d_mask;
+    A.b = b;
+    A.u = u;
+    A.r = pl->cg_r;
+    A.p = pl->cg_p;
+    A.q = pl->cg_q;
+    A.h = L.info.height;
+    A.w = L.info.width;
+    A.channels = pl->C;
+    A.plane = (size_t)L.info.height * L.info.width;
+    A.hinv2 = L.dev.hinv2;
+    A.gate = pl->cgs.gate;
+    A.alpha = pl->cgs.alpha;
+    A.beta = pl->cgs.beta;
+    A.partial = pl->d_partial;
+    A.counter = pl->d_counter;
+    A.sum_out = pl->cgs.sum;
+    return A;
+}
+
+// _cg_run on level L for the problems selected by `pred`.  denom_mode / tol / stop_abs / record as in
+// cg_after_init_kernel.  Steps per problem end up in cgs.steps, |r| / denom in d_rel.
+static int cg_run(b200p_plan *pl, const LevelHost &L, double *u, const double *b, bool rm, int max_steps,
+                  int denom_mode, double tol, double stop_abs, bool record, const int *pred, cudaStream_t st) {
+    const int nb = (pl->P + 127) / 128;
+    CgArgs A = cg_args(pl, L, u, b);
+    CgState &S = pl->cgs;
+    const int ctas = (int)std::min<size_t>(CG_CTAS, (A.plane + CG_THREADS - 1) / CG_THREADS);
+    dim3 grid(ctas, pl->P);
+    const double fb = 8.0 * pl->P * (double)A.plane;
+    {
+        LaunchScope sc(pl, st, KK_CONTROL, 0.0);
+        cg_begin_kernel<<<nb, 128, 0, st>>>(pl->P, pred, S);
+        CU(cudaGetLastError());
+    }
+    {
+        LaunchScope sc(pl, st, KK_CG, 4.0 * fb);
+        if (rm) cg_field_kernel<0, true><<<grid, CG_THREADS, 0, st>>>(A);
+        else cg_field_kernel<0, false><<<grid, CG_THREADS, 0, st>>>(A);
+        CU(cudaGetLastError());
+    }
+    {
+        LaunchScope sc(pl, st, KK_CONTROL, 0.0);
+        cg_after_init_kernel<<<nb, 128, 0, st>>>(pl->P, S, denom_mode, tol, stop_abs, record ? 1 : 0);
+        CU(cudaGetLastError());
+    }
+    const bool host_checks = max_steps > 16;
+    int done = 0;
+    while (done < max_steps) {
+        const int chunk = std::min(host_checks ? 8 : max_steps, max_steps - done);
+        if (host_checks) {
+            int rc = launch_set_int(pl, pl->d_any, 1, 0, st);
+            if (rc) return rc;
+        }
+        for (int k = 0; k < chunk; ++k) {
+            {
+                LaunchScope sc(pl, st, KK_CG, 2.0 * fb);
+                cg_field_kernel<1, false><<<grid, CG_THREADS, 0, st>>>(A);
+            }
+            {
+                LaunchScope sc(pl, st, KK_CONTROL, 0.0);
+                cg_after_apply_kernel<<<nb, 128, 0, st>>>(pl->P, S);
+            }
+            {
+                LaunchScope sc(pl, st, KK_CG, 5.0 * fb);
+                cg_field_kernel<2, false><<<grid, CG_THREADS, 0, st>>>(A);
+            }
+            {
+                LaunchScope sc(pl, st, KK_CONTROL, 0.0);
+                cg_after_update_kernel<<<nb, 128, 0, st>>>(pl->P, S, max_steps, record ? 1 : 0, denom_mode,
+                                                          host_checks ? pl->d_any : nullptr);
+            }
+            {
+                LaunchScope sc(pl, st, KK_CG, 3.0 * fb);
+                cg_dir_kernel<<<grid, CG_THREADS, 0, st>>>(A);
+            }
+            CU(cudaGetLastError());
+        }
+        done += chunk;
+        if (host_checks) {
+            CU(cudaMemcpyAsync(pl->h_any, pl->d_any, sizeof(int), cudaMemcpyDeviceToHost, st));
+            CU(cudaStreamSynchronize(st));
+            if (!*pl->h_any) break;
+        }
+    }
+    return 0;
+}
+
+// _smooth with the CG smoother (multigrid.py:278-279): units * smoother_cg_iters steps, stop_norm 0
+static int cg_smooth(b200p_plan *pl, const LevelHost &L, double *u, const double *b, bool rm, int units,
+                     const int *pred, int *unit_counter, cudaStream_t st) {
+    if (units <= 0) return 0;
+    const int k = pl->cfg.smoother_cg_iters;
+    int rc = cg_run(pl, L, u, b, rm, units * k, 0, 0.0, 0.0, false, pred, st);
+    if (rc) return rc;
+    if (unit_counter) {
+        LaunchScope sc(pl, st, KK_CONTROL, 0.0);
+        cg_units_kernel<<<(pl->P + 127) / 128, 128, 0, st>>>(pl->P, pred, pl->cgs.steps, k, unit_counter);
+        CU(cudaGetLastError());
+    }
+    return 0;
+}
+
+static int cg_restrict(b200p_plan *pl, const LevelHost &L, const LevelHost &Cc, const double *u, const double *b,
+                       bool rm, const int *pred, double *ez, cudaStream_t st) {
+    LaunchScope sc(pl, st, KK_RESTRICT, field_bytes(pl, L, rm ? 1.25 : 2.25, 1.25));
+    dim3 g = grid2x(Cc.info.width, Cc.info.height, pl->P);
+    if (rm)
+        residual_restrict_kernel<true><<<g, ST_THREADS, 0, st>>>(u, b, L.d_mask, Cc.d_mask, L.info.height,
+                                                                 L.info.width, L.dev.hinv2, pl->C, pred, Cc.d_rc, ez);
+    else
+        residual_restrict_kernel<false><<<g, ST_THREADS, 0, st>>>(u, b, L.d_mask, Cc.d_mask, L.info.height,
+                                                                  L.info.width, L.dev.hinv2, pl->C, pred, Cc.d_rc, ez);
+    CU(cudaGetLastError());
+    return 0;
+}
+
+// v_cycle (multigrid.py:335-371) with the CG smoother, in place on u
+static int cg_vcycle(b200p_plan *pl, int level, double *u, const double *b, bool rm, const int *pred,
+                     int *unit_counter, cudaStream_t st) {
+    const int nl = (int)pl->lev.size();
+    const b200p_config &cfg = pl->cfg;
+    LevelHost &L = pl->lev[level];
+    int *uc = level == 0 ? unit_counter : nullptr;
+    int rc;
+    if (level == nl - 1) return cg_smooth(pl, L, u, b, rm, cfg.nu_pre + cfg.nu_post, pred, uc, st);
+    if ((rc = cg_smooth(pl, L, u, b, rm, cfg.nu_pre, pred, uc, st))) return rc;
+    LevelHost &Cc = pl->lev[level + 1];
+    double *e = Cc.d_u;
+    if ((rc = cg_restrict(pl, L, Cc, u, b, rm, pred, e, st))) return rc;  // also e = 0
+    if (level + 1 == nl - 1) {
+        const double tol = std::min(cfg.coarse_tol, cfg.tol_rel);
+        rc = cg_run(pl, Cc, e, Cc.d_rc, false, cfg.coarse_max_iters, 1, tol, 0.0, false, pred, st);
+    } else {
+        rc = cg_vcycle(pl, level + 1, e, Cc.d_rc, false, pred, nullptr, st);
+    }
+    if (rc) return rc;
+    {
+        LaunchScope sc(pl, st, KK_PROLONG_CORR, field_bytes(pl, L, 2.25, 1.0));
+        prolongate_kernel<false><<<grid2x(Cc.info.width, Cc.info.height, pl->P), ST_THREADS, 0, st>>>(
+            e, L.d_mask, nullptr, L.info.height, L.info.width, pl->C, pred, u);
+        CU(cudaGetLastError());
+    }
+    return cg_smooth(pl, L, u, b, rm, cfg.nu_post, pred, uc, st);
+}
+
+static int launch_flat_init(b200p_plan *pl, const LevelHost &L, double *u, cudaStream_t st);
+
+// fmg_solve / cg_solve with the CG smoother: mode 0 "mg-cg", 1 "ml-cg", 2 "cg" (single level)
+static int run_cg_pipeline(b200p_plan *pl, double *d_out, cudaStream_t st) {
+    const int nl = (int)pl->lev.size();
+    const b200p_config &cfg = pl->cfg;
+    LevelHost &L0 = pl->lev[0];
+    const int nb = (pl->P + 127) / 128;
+    int rc;
+    if (cfg.mode != 2 && (rc = enqueue_hierarchy(pl, st))) return rc;
+    if ((rc = launch_norm(pl, L0, L0.d_rhs, L0.d_rhs, true, true, nullptr, st))) return rc;
+    if ((rc = launch_control(pl, 0, st))) return rc;  // baseline; units, cycles, histlen = 0; active = 1
+    if (cfg.mode == 2) {
+        // cg_solve (solvers.py:140-186): flat init, stop at tol_rel * ||r0||, history [1, rn / r0 ...]
+        if ((rc = launch_flat_init(pl, L0, d_out, st))) return rc;
+        if ((rc = cg_run(pl, L0, d_out, L0.d_rhs, true, cfg.max_outer_iters, 1, cfg.tol_rel, 0.0, true, nullptr, st)))
+            return rc;
+        LaunchScope sc(pl, st, KK_CONTROL, 0.0);
+        ml_finish_kernel<<<nb, 128, 0, st>>>(pl->P, pl->cgs.steps, pl->d_cycles, pl->d_units, pl->d_active);
+        CU(cudaGetLastError());
+        return 0;
+    }
+    // ---- _cascade (multigrid.py:389-422)
+    const double ctol = std::min(cfg.coarse_tol, cfg.tol_rel);
+    LevelHost &co = pl->lev[nl - 1];
+    double *cu = nl == 1 ? d_out : co.d_u;
+    if ((rc = launch_flat_init(pl, co, cu, st))) return rc;
+    if ((rc = cg_run(pl, co, cu, co.d_rhs, true, cfg.coarse_max_iters, 1, ctol, 0.0, nl == 1 && cfg.mode == 1,
+                     nullptr, st)))
+        return rc;
+    if (nl == 1) {
+        // single level: the coarse solve is the finest level; its steps count as fine units
+        LaunchScope sc(pl, st, KK_CONTROL, 0.0);
+        if (cfg.mode == 1) {
+            ml_finish_kernel<<<nb, 128, 0, st>>>(pl->P, pl->cgs.steps, pl->d_cycles, pl->d_units, pl->d_active);
+        } else {
+            cg_units_kernel<<<nb, 128, 0, st>>>(pl->P, nullptr, pl->cgs.steps, 1, pl->d_units);
+        }
+        CU(cudaGetLastError());
+    }
+    const double *coarse_u = cu;
+    for (int l = nl - 2; l >= 0; --l) {
+        LevelHost &f = pl->lev[l];
+        const LevelHost &c = pl->lev[l + 1];
+        double *uf = l == 0 ? d_out : f.d_u;
+        {
+            LaunchScope sc(pl, st, KK_PROLONG_SOL, field_bytes(pl, f, 1.25, 1.0));
+            prolongate_kernel<true><<<grid2x(c.info.width, c.info.height, pl->P), ST_THREADS, 0, st>>>(
+                coarse_u, f.d_mask, f.d_rhs, f.info.height, f.info.width, pl->C, nullptr, uf);
+            CU(cudaGetLastError());
+        }
+        if (cfg.mode == 1) {
+            // to_tol: denom = the level's flat-init defect (multigrid.py:413-417)
+            if ((rc = launch_norm(pl, f, f.d_rhs, f.d_rhs, true, true, nullptr, st))) return rc;
+            {
+                LaunchScope sc(pl, st, KK_CONTROL, 0.0);
+                ml_level_begin_kernel<<<nb, 128, 0, st>>>(pl->P, pl->d_rs, pl->cgs.denom, pl->d_gate, pl->d_sweeps);
+                CU(cudaGetLastError());
+            }
+            if ((rc = cg_run(pl, f, uf, f.d_rhs, true, cfg.max_outer_iters, 2, cfg.tol_rel, 0.0, l == 0, nullptr, st)))
+                return rc;
+        } else if (l > 0) {
+            if ((rc = cg_smooth(pl, f, uf, f.d_rhs, true, 1, nullptr, nullptr, st))) return rc;
+        }
+        coarse_u = uf;
+    }
+    if (cfg.mode == 1) {
+        if (nl > 1) {
+            LaunchScope sc(pl, st, KK_CONTROL, 0.0);
+            ml_finish_kernel<<<nb, 128, 0, st>>>(pl->P, pl->cgs.steps, pl->d_cycles, pl->d_units, pl->d_active);
+            CU(cudaGetLastError());
+        }
+        return 0;
+    }
+    // ---- V-cycles until converged (multigrid.py:466-481)
+    if ((rc = launch_norm(pl, L0, d_out, L0.d_rhs, false, true, nullptr, st))) return rc;
+    if ((rc = launch_control(pl, 1, st))) return rc;
+    CU(cudaMemcpyAsync(pl->h_any, pl->d_any, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    int done = 0;
+    while (*pl->h_any && done < cfg.v_cycles_max) {
+        if ((rc = cg_vcycle(pl, 0, d_out, L0.d_rhs, true, pl->d_active, pl->d_units, st))) return rc;
+        if ((rc = launch_norm(pl, L0, d_out, L0.d_rhs, false, true, pl->d_active, st))) return rc;
+        if ((rc = launch_control(pl, 2, st))) return rc;
+        CU(cudaMemcpyAsync(pl->h_any, pl->d_any, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        ++done;
+    }
+    return 0;
+}
+
 // _smooth_to_tol with the ORAS smoother on a multi-block level (multigrid.py:282-322): sweeps until
 // ||r|| <= tol_rel * denom per problem, denom = the level's flat-init defect, at most max_outer_iters.
 static int smooth_level_to_tol(b200p_plan *pl, LevelHost &f, UBuf &uf, bool record, cudaStream_t st) {
@@ -1064,6 +1314,14 @@ __global__ void flat_init_kernel(const uint8_t *__restrict__ mask, const double 
     if (i >= n) return;
     const size_t p = i / plane, px = i - p * plane;
     out[i] = mask[(p / channels) * plane + px] ? known[i] : 0.0;
+}
+
+static int launch_flat_init(b200p_plan *pl, const LevelHost &L, double *u, cudaStream_t st) {
+    const size_t plane = (size_t)L.info.height * L.info.width, n = plane * pl->P;
+    LaunchScope sc(pl, st, KK_CONVERT, 17.0 * n);
+    flat_init_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(L.d_mask, L.d_rhs, plane, pl->C, n, u);
+    CU(cudaGetLastError());
+    return 0;
 }
 
 static int run_single_level(b200p_plan *pl, double *d_out, cudaStream_t st) {
@@ -1287,6 +1545,8 @@ void b200p_config_default(b200p_config *c, int width, int height, int channels) 
     c->spec_cycles = 1;
     c->mode = 0;
     c->max_outer_iters = 10000;
+    c->smoother = 0;
+    c->smoother_cg_iters = 10;
 }
 
 int b200p_axis_starts(int dim, int block, int overlap, int64_t *out, int cap) {
@@ -1370,6 +1630,9 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
     if (c.v_cycles_max < 0 || c.coarse_max_iters < 0 || c.local_max_iters < 0 || c.max_outer_iters < 0)
         return fail_arg(B200P_ERR_ARG, "iteration caps must be >= 0");
     if (c.mode < 0 || c.mode > 2) return fail_arg(B200P_ERR_ARG, "unknown mode %d", c.mode);
+    if (c.smoother != 0 && c.smoother != 1) return fail_arg(B200P_ERR_ARG, "unknown smoother %d", c.smoother);
+    if (c.smoother == 1 && c.smoother_cg_iters < 1)
+        return fail_arg(B200P_ERR_ARG, "need at least one smoothing iteration per cycle");
 
     int ndev = 0;
     CU(cudaGetDeviceCount(&ndev));
@@ -1493,6 +1756,7 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
         nparts = std::max(nparts, (size_t)((L.info.width / 4 + ROWS4_THREADS - 1) / ROWS4_THREADS + 1) *
                                       ((L.info.height + 7) / 8));
     }
+    if (c.smoother == 1) nparts = std::max(nparts, (size_t)CG_CTAS);
     PTRY(dev_alloc(pl, &pl->d_partial, (size_t)pl->P * nparts));
     PTRY(dev_alloc(pl, &pl->d_partial_flag, (size_t)pl->P * nparts));
     PTRY(dev_alloc(pl, &pl->d_counter, (size_t)pl->P));
@@ -1511,6 +1775,26 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
     PTRY(dev_alloc(pl, &pl->d_gate, (size_t)pl->P));
     PTRY(dev_alloc(pl, &pl->d_sweeps, (size_t)pl->P));
     PTRY(dev_alloc(pl, &pl->d_rn, (size_t)pl->P));
+    if (c.smoother == 1) {
+        const size_t n0 = (size_t)pl->P * c.width * c.height;
+        PTRY(dev_alloc(pl, &pl->cg_r, n0));
+        PTRY(dev_alloc(pl, &pl->cg_p, n0));
+        PTRY(dev_alloc(pl, &pl->cg_q, n0));
+        CgState &S = pl->cgs;
+        PTRY(dev_alloc(pl, &S.rs, (size_t)pl->P));
+        PTRY(dev_alloc(pl, &S.pq, (size_t)pl->P));
+        PTRY(dev_alloc(pl, &S.alpha, (size_t)pl->P));
+        PTRY(dev_alloc(pl, &S.beta, (size_t)pl->P));
+        PTRY(dev_alloc(pl, &S.sum, (size_t)pl->P));
+        PTRY(dev_alloc(pl, &S.stop, (size_t)pl->P));
+        PTRY(dev_alloc(pl, &S.steps, (size_t)pl->P));
+        PTRY(dev_alloc(pl, &S.denom, (size_t)pl->P));  // not d_denom: that is fmg_solve's own denominator
+        S.rel = pl->d_rel;
+        S.gate = pl->d_gate;
+        S.hist = pl->d_hist;
+        S.histlen = pl->d_histlen;
+        S.hist_cap = B200P_MAX_HISTORY;
+    }
     {
         cudaError_t e = cudaMallocHost((void **)&pl->h_any, 64);
         if (e != cudaSuccess) {
@@ -1699,8 +1983,10 @@ int b200p_solve_async(b200p_plan *pl, const uint8_t *d_mask, const double *d_kno
     }
     bind_level0(pl, d_mask, d_known);
     int rc;
-    if (pl->cfg.mode != 0) {
-        if ((rc = pl->cfg.mode == 1 ? run_multilevel(pl, d_out, st) : run_single_level(pl, d_out, st))) return rc;
+    if (pl->cfg.mode != 0 || pl->cfg.smoother == 1) {
+        if (pl->cfg.smoother == 1) rc = run_cg_pipeline(pl, d_out, st);
+        else rc = pl->cfg.mode == 1 ? run_multilevel(pl, d_out, st) : run_single_level(pl, d_out, st);
+        if (rc) return rc;
         pl->hierarchy_ready = true;
         if ((rc = enqueue_reports(pl, st))) return rc;
         pl->pending = true;

@@ -53,10 +53,8 @@ class MultigridConfig:
 
 
 def _require_hot_path(cfg) -> None:
-    if cfg.smoother != "oras":
-        raise NotImplementedError(
-            "the B200 build covers the ORAS-smoothed pipelines only (mg-oras, ml-oras); "
-            f"got smoother={cfg.smoother!r}, mode={cfg.mode!r}")
+    if cfg.smoother not in ("oras", "cg"):
+        raise NotImplementedError(f"unknown smoother {cfg.smoother!r}")
 
 
 # --------------------------------------------------------------------- plan
@@ -85,6 +83,8 @@ class Plan:
         # single_level: oras_solve on the finest level only (the "oras" pipeline, solvers.py:427-485)
         c.mode = 2 if single_level else (1 if cfg.mode == "multilevel" else 0)
         self.single_level = bool(single_level)
+        c.smoother = 1 if cfg.smoother == "cg" else 0
+        c.smoother_cg_iters = int(s.smoother_cg_iters)
         c.max_outer_iters = int(s.max_outer_iters)
         self.config = c
         self.cfg = cfg
@@ -137,7 +137,8 @@ class Plan:
     # -- solves
     def _reports(self, raw, wall):
         reps = []
-        name = "oras" if self.single_level else ("ml-oras" if self.cfg.mode == "multilevel" else "mg-oras")
+        base = self.cfg.smoother
+        name = base if self.single_level else ("ml-" if self.cfg.mode == "multilevel" else "mg-") + base
         for r in raw:
             reps.append(SolveReport(
                 solver=name, iterations=r.iterations, final_rel_residual=r.final_rel_residual,
@@ -215,7 +216,8 @@ def _cfg_key(cfg):
     s = cfg.solver
     return (cfg.nu_pre, cfg.nu_post, cfg.v_cycles_max, cfg.value_downsampling, cfg.block_size,
             cfg.overlap, cfg.coarse_tol, cfg.coarse_max_iters, s.tol_rel, s.alpha,
-            s.local_tol_fraction, s.local_max_iters, cfg.mode, s.max_outer_iters)
+            s.local_tol_fraction, s.local_max_iters, cfg.mode, s.max_outer_iters, cfg.smoother,
+            s.smoother_cg_iters)
 
 
 def cached_plan(width, height, channels, frames, cfg, spacing=1.0, single_level=False) -> Plan:

@@ -1,10 +1,10 @@
 """Named-pipeline front end: the drop-in boundary of the path.
 
 ``solve_image(problem, "mg-oras", cfg)`` has the reference's signature, result
-type and error behaviour (pipelines.py:20-114).  The ORAS-smoothed pipelines are
-built: "mg-oras" (the hot path), "ml-oras" (cascadic multilevel) and "oras"
-(single-level Schwarz iteration), the paper's comparison variants on the same kernels; the other names of the reference are
-recognised and rejected with NotImplementedError (out of scope).
+type and error behaviour (pipelines.py:20-114).  All six names run on the CUDA
+path: "mg-oras" (the hot path), "ml-oras" (cascadic multilevel) and "oras"
+(single-level Schwarz iteration) on the same kernels, and the CG-smoothed
+comparison set "mg-cg", "ml-cg", "cg" on flat global-CG kernels.
 ``solve_frames`` is the batched entry (frames x channels in one plan).
 """
 
@@ -20,7 +20,7 @@ from .multigrid import LevelHierarchy, MultigridConfig, build_hierarchy, cached_
 from .solvers import SolveReport
 
 SOLVER_NAMES = ("cg", "oras", "ml-cg", "ml-oras", "mg-cg", "mg-oras")
-BUILT = ("mg-oras", "ml-oras", "oras")
+BUILT = SOLVER_NAMES  # all six pipelines of the reference run on the CUDA path
 
 
 def split_solver_name(name: str):

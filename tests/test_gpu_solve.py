@@ -176,6 +176,39 @@ def test_single_level_oras_matches_oracle(w, h, dens, seed, bs, ov, kw):
     assert np.array_equal(u1, res.fields[1]) and r1.iterations == res.reports[1].iterations
 
 
+@pytest.mark.parametrize("w,h,dens,seed,bs,ov,name,kw", [
+    (96, 64, 0.10, 1, 16, 2, "mg-cg", dict()),
+    (160, 120, 0.05, 3, 32, 6, "ml-cg", dict()),
+    (97, 131, 0.03, 2, 16, 2, "mg-cg", dict(tol_rel=1e-6)),          # odd dims, several V-cycles
+    (20, 30, 0.20, 3, 32, 6, "mg-cg", dict(tol_rel=1e-6)),           # single level
+    (20, 30, 0.20, 3, 32, 6, "ml-cg", dict(tol_rel=1e-6)),
+    (128, 128, 0.05, 6, 16, 2, "ml-cg", dict(max_outer_iters=4)),    # step cap: converged False
+    (256, 256, 0.05, 0, 16, 2, "mg-cg", dict()),
+    (200, 150, 0.05, 5, 32, 6, "cg", dict()),
+    (200, 150, 0.05, 5, 32, 6, "cg", dict(max_outer_iters=7)),
+])
+def test_cg_pipelines_match_oracle(w, h, dens, seed, bs, ov, name, kw):
+    """The paper's CG comparison set: global CG as smoother / coarse solver
+    (multigrid.py:278-279, :323-331; _cg_run solvers.py:97-128) and cg_solve (solvers.py:140-186)."""
+    m, k = oracle.seeded_problem(w, h, dens, seed, channels=2)
+    cfg_b = bp.MultigridConfig(block_size=bs, overlap=ov, solver=bp.SolverConfig(**kw))
+    res = bp.solve_image(bp.InpaintingProblem(m, k), name, cfg_b)
+    if name == "cg":
+        ref, reps_o = zip(*(oracle.cg_solve(m, k[c], 1.0, oracle.SolverConfig(**kw)) for c in range(2)))
+    else:
+        mode = "multilevel" if name.startswith("ml") else "full_multigrid"
+        ref, reps_o = oracle.solve_image(m, k, 1.0, oracle.MultigridConfig(
+            block_size=bs, overlap=ov, smoother="cg", mode=mode, solver=oracle.SolverConfig(**kw)))
+    for c in range(2):
+        ro, rg = reps_o[c], res.reports[c]
+        assert rg.solver == name
+        assert (rg.iterations, rg.fine_smoother_iterations, rg.converged) == \
+               (ro.iterations, ro.fine_smoother_iterations, ro.converged)
+        assert rg.final_rel_residual == pytest.approx(ro.final_rel_residual, rel=1e-5)
+        np.testing.assert_allclose(rg.history, ro.history, rtol=1e-5)
+        assert np.abs(res.fields[c] - ref[c]).max() <= TOL_ABS
+
+
 def test_spacing_other_than_one():
     m, k = oracle.seeded_problem(120, 90, 0.05, 3)
     _compare(m, k, *_cfgs(16, 2), spacing=0.5)
@@ -207,8 +240,6 @@ def test_errors_match_reference_behaviour():
     m[3, 3] = True
     with pytest.raises(ValueError):
         bp.solve_image(bp.InpaintingProblem(m, k), "no-such-solver")
-    with pytest.raises(NotImplementedError):
-        bp.solve_image(bp.InpaintingProblem(m, k), "mg-cg")
     with pytest.raises(ValueError):
         bp.solve_image(bp.InpaintingProblem(m, k), "mg-oras", bp.MultigridConfig(block_size=8, overlap=8))
     with pytest.raises(ValueError):
@@ -354,9 +385,14 @@ def test_bench_suites_on_the_cuda_path():
     from paper_2401_06744_b200 import suites, synthetic
     cfg = bp.MultigridConfig(block_size=16, overlap=2)
     img = synthetic.synthetic_image(192, 128, 7)[None]
-    rows = suites.density_suite([img], cfg, densities=(0.02, 0.10), seeds=(0,))
+    rows = suites.density_suite([img], cfg, densities=(0.02, 0.10), seeds=(0,),
+                                solvers=("mg-oras", "ml-oras", "oras"))
     assert len(rows) == 6 and all(tuple(r) == suites.ROW_FIELDS for r in rows)
     assert {r["solver"] for r in rows} == {"mg-oras", "ml-oras", "oras"}
+    # default: all six pipelines of the reference (pipelines.py:20)
+    allrows = suites.density_suite([img[:, :64, :96]], cfg, densities=(0.05,), with_reference=False)
+    assert [r["solver"] for r in allrows] == list(bp.SOLVER_NAMES)
+    assert all(r["rel_residual"] <= cfg.solver.tol_rel for r in allrows)
     for r in rows:
         assert r["rel_residual"] <= cfg.solver.tol_rel and r["mse_vs_reference"] < 1.0 and r["wall_time_s"] > 0
     # ml-oras smooths every level to tolerance: more finest-level sweeps than mg-oras needs V-cycles
