@@ -1772,6 +1772,7 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
     PTRY(dev_alloc(pl, &pl->d_denom, (size_t)pl->P));
     PTRY(dev_alloc(pl, &pl->d_rel, (size_t)pl->P));
     PTRY(dev_alloc(pl, &pl->d_hist, (size_t)pl->P * B200P_MAX_HISTORY));
+    CU(cudaMemset(pl->d_hist, 0, sizeof(double) * (size_t)pl->P * B200P_MAX_HISTORY));  // entries past histlen are copied out too
     PTRY(dev_alloc(pl, &pl->d_gate, (size_t)pl->P));
     PTRY(dev_alloc(pl, &pl->d_sweeps, (size_t)pl->P));
     PTRY(dev_alloc(pl, &pl->d_rn, (size_t)pl->P));
