@@ -92,21 +92,24 @@ __device__ __forceinline__ void walk_rows4(const double *__restrict__ up, const 
     const double cxR = 4.0 - (xc + 4 == w ? 1.0 : 0.0);
     auto load_mask = [&](size_t i) { return *reinterpret_cast<const uchar4 *>(mp + i); };
     auto load_row = [&](size_t i, uchar4 m) {
+        Row4 r;
+        if (UM) {
+            // flat initialisation where(mask, known, 0): only the known pixels (a few per cent) are
+            // fetched, so the baseline pass reads the mask plus the touched 32-byte sectors of `known`
+            r.v[0] = m.x ? up[i] : 0.0;
+            r.v[1] = m.y ? up[i + 1] : 0.0;
+            r.v[2] = m.z ? up[i + 2] : 0.0;
+            r.v[3] = m.w ? up[i + 3] : 0.0;
+            return r;
+        }
         const double2 a = *reinterpret_cast<const double2 *>(up + i);
         const double2 c = *reinterpret_cast<const double2 *>(up + i + 2);
-        Row4 r;
         r.v[0] = a.x; r.v[1] = a.y; r.v[2] = c.x; r.v[3] = c.y;
-        if (UM) {
-            r.v[0] = m.x ? r.v[0] : 0.0;
-            r.v[1] = m.y ? r.v[1] : 0.0;
-            r.v[2] = m.z ? r.v[2] : 0.0;
-            r.v[3] = m.w ? r.v[3] : 0.0;
-        }
         return r;
     };
     auto load_one = [&](size_t i) {
-        const double v = up[i];
-        return UM ? (mp[i] ? v : 0.0) : v;
+        if (UM) return mp[i] ? up[i] : 0.0;
+        return up[i];
     };
     Row4 above, centre, below;
     const Row4 zero = {{0.0, 0.0, 0.0, 0.0}};
