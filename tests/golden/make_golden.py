@@ -4,6 +4,7 @@ container (the reference is not present on the GPU box):
 
     python tests/golden/make_golden.py            # small vectors  (seconds)
     python tests/golden/make_golden.py --anchors  # + 1080p / 4K anchors (~3 min)
+    python tests/golden/make_golden.py --pipelines  # only golden_pipelines.* (comparison pipelines)
 
 Outputs: golden_small.npz (inputs are regenerated from seeds by the tests; only
 reference OUTPUTS are stored) and anchors.json / anchors_4k_sample.npz."""
@@ -105,6 +106,31 @@ def small():
         json.dump(meta, f, indent=1)
 
 
+def pipelines():
+    """The five comparison pipelines (pipelines.py:20-39): ml-oras, oras, mg-cg, ml-cg, cg."""
+    out, meta = {}, {}
+    cases = {
+        "q96x64": (96, 64, 0.10, 1, 2, dict(block_size=16, overlap=2), dict()),
+        "q160x120": (160, 120, 0.05, 3, 1, dict(block_size=32, overlap=6), dict(tol_rel=1e-5)),
+        "q20x30": (20, 30, 0.20, 3, 1, dict(block_size=32, overlap=6), dict(tol_rel=1e-6)),
+        "q128cap": (128, 128, 0.05, 6, 1, dict(block_size=16, overlap=2), dict(max_outer_iters=4)),
+    }
+    for name, (w, h, dens, seed, ch, mkw, skw) in cases.items():
+        prob = seeded(w, h, dens, seed, ch)
+        cfg = dp.MultigridConfig(solver=dp.SolverConfig(**skw), **mkw)
+        meta[name] = dict(w=w, h=h, density=dens, seed=seed, channels=ch, mg=mkw, solver=skw, reports={})
+        for solver in ("ml-oras", "oras", "mg-cg", "ml-cg", "cg"):
+            res = dp.solve_image(prob, solver, cfg)
+            out[f"{name}_{solver}_fields"] = res.fields
+            meta[name]["reports"][solver] = [
+                dict(iterations=r.iterations, final_rel=r.final_rel_residual, baseline=r.baseline_residual,
+                     fine_units=r.fine_smoother_iterations, converged=bool(r.converged), history=list(r.history))
+                for r in res.reports]
+    np.savez_compressed(os.path.join(HERE, "golden_pipelines.npz"), **out)
+    with open(os.path.join(HERE, "golden_pipelines.json"), "w") as f:
+        json.dump(meta, f, indent=1)
+
+
 def anchors():
     os.environ["INPAINT_THREADS"] = "0"
     res = {}
@@ -132,7 +158,12 @@ def anchors():
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--anchors", action="store_true")
+    ap.add_argument("--pipelines", action="store_true", help="write only golden_pipelines.*")
     a = ap.parse_args()
-    small()
-    if a.anchors:
-        anchors()
+    if a.pipelines:
+        pipelines()
+    else:
+        small()
+        pipelines()
+        if a.anchors:
+            anchors()

@@ -101,3 +101,57 @@ def test_anchors_if_present():
         assert r.final_rel_residual == pytest.approx(g["final_rel"], rel=1e-6)
     got = out.reshape(a["channels"], -1)[:, ::997]
     assert np.abs(got - sample["1080p_4pct_16_2"]).max() <= 1e-6
+
+
+# ---- the five comparison pipelines (golden_pipelines.*: written by the reference) -------------
+
+@pytest.fixture(scope="module")
+def pgold():
+    return np.load(os.path.join(G, "golden_pipelines.npz"))
+
+
+@pytest.fixture(scope="module")
+def pmeta():
+    with open(os.path.join(G, "golden_pipelines.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("solver", ["ml-oras", "oras", "mg-cg", "ml-cg", "cg"])
+@pytest.mark.parametrize("case", ["q96x64", "q160x120", "q20x30", "q128cap"])
+def test_comparison_pipelines(pgold, pmeta, case, solver):
+    """oracle ml-oras / oras / mg-cg / ml-cg / cg == the reference's own outputs (pipelines.py:20-114)."""
+    c = pmeta[case]
+    m, k = oracle.seeded_problem(c["w"], c["h"], c["density"], c["seed"], channels=c["channels"])
+    scfg = oracle.SolverConfig(**c["solver"])
+    bs, ov = c["mg"]["block_size"], c["mg"]["overlap"]
+    base = solver.split("-")[-1]
+    got = []
+    if "-" in solver:
+        mode = "multilevel" if solver.startswith("ml") else "full_multigrid"
+        fields, reps = oracle.solve_image(m, k, 1.0, oracle.MultigridConfig(
+            block_size=bs, overlap=ov, smoother=base, mode=mode, solver=scfg))
+        got = [(fields[ch], dict(iterations=r.iterations, final_rel=r.final_rel_residual,
+                                 fine_units=r.fine_smoother_iterations, converged=r.converged,
+                                 history=r.history, baseline=r.baseline_residual))
+               for ch, r in enumerate(reps)]
+    else:
+        for ch in range(c["channels"]):
+            if base == "cg":
+                u, r = oracle.cg_solve(m, k[ch], 1.0, scfg)
+                rep = dict(iterations=r.iterations, final_rel=r.final_rel_residual,
+                           fine_units=r.fine_smoother_iterations, converged=r.converged,
+                           history=r.history, baseline=r.baseline_residual)
+            else:
+                u, r = oracle.oras_solve(m, k[ch], 1.0, bs, ov, scfg)
+                rep = dict(iterations=r["iterations"], final_rel=r["final_rel_residual"],
+                           fine_units=r["fine_smoother_iterations"], converged=r["converged"],
+                           history=r["history"], baseline=r["baseline_residual"])
+            got.append((u, rep))
+    for ch, (u, rep) in enumerate(got):
+        want = c["reports"][solver][ch]
+        assert (rep["iterations"], rep["fine_units"], bool(rep["converged"])) == \
+               (want["iterations"], want["fine_units"], want["converged"])
+        assert rep["final_rel"] == pytest.approx(want["final_rel"], rel=1e-6, abs=1e-13)
+        assert rep["baseline"] == pytest.approx(want["baseline"], rel=1e-12)
+        np.testing.assert_allclose(rep["history"], want["history"], rtol=1e-6, atol=1e-13)
+        np.testing.assert_allclose(u, pgold[f"{case}_{solver}_fields"][ch], rtol=0, atol=1e-9)
