@@ -410,3 +410,43 @@ def test_bench_suites_on_the_cuda_path():
     assert 0.0 < slope < 1.5  # sub-linear while the small sizes are launch-latency bound
     ranked = suites.compare_rows(bp.InpaintingProblem(synthetic.random_mask(192, 128, 0.05, 1), img), cfg)
     assert ranked[0]["mse_vs_reference"] <= ranked[-1]["mse_vs_reference"]
+
+
+def test_async_api_state_and_streaming_pipeline():
+    """b200p_solve_host_async / b200p_solve_wait: one solve may be pending per plan; the streaming
+    pipeline (submit / flush) returns the same fields as run()."""
+    w, h, c = 192, 128, 2
+    cfg = bp.MultigridConfig(block_size=16, overlap=2)
+    masks, known = [], []
+    for f in range(5):
+        m, k = oracle.seeded_problem(w, h, 0.05, 30 + f, channels=c)
+        masks.append(m)
+        known.append(k)
+    masks, known = np.stack(masks).view(np.uint8), np.stack(known)
+    plan = bp.Plan(w, h, c, 1, cfg)
+    with pytest.raises(RuntimeError):
+        plan.wait()                                   # nothing pending
+    out = np.empty_like(known[:1])
+    plan.solve_host_async(masks[:1], known[:1], out)
+    with pytest.raises(RuntimeError):
+        plan.solve_host_async(masks[:1], known[:1], out)   # a solve is already pending
+    reps = plan.wait()
+    assert len(reps) == c and all(r.converged for r in reps)
+    with pytest.raises(ValueError):
+        plan.solve_host_async(masks[:1].astype(np.int32), known[:1], out)
+    plan.close()
+    pipe = bp.FramePipeline(w, h, c, cfg, lanes=2)
+    ref_out, ref_reps = pipe.run(masks, known)
+    j1 = pipe.submit(masks[:3], known[:3])
+    j2 = pipe.submit(masks[3:], known[3:])
+    pipe.flush()
+    assert np.array_equal(np.concatenate([j1["out"], j2["out"]]), ref_out)
+    assert [r.iterations for fr in j1["reports"] + j2["reports"] for r in fr] == \
+           [r.iterations for fr in ref_reps for r in fr]
+    np.testing.assert_array_equal(out[0], ref_out[0])
+    with pytest.raises(bp.EmptyMaskError):
+        pipe.run(np.zeros_like(masks), known)
+    # the pipeline stays usable after a rejected batch
+    again, _ = pipe.run(masks[:2], known[:2])
+    assert np.array_equal(again, ref_out[:2])
+    pipe.close()
