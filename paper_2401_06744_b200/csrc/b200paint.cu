@@ -164,6 +164,8 @@ struct LevelHost {
     double *d_rc = nullptr;     // (P,h,w) restricted residual (levels >= 1)
     int tile = 0;               // K2 variant: 0 generic, else see launch_sweep
     unsigned *d_mtab = nullptr; // K2T: packed block-local masks (F, nblocks, 64); null = level not eligible
+    // strip mode (level 0 only): rows this rank owns / keeps valid, block rows it solves (default: all)
+    int own_lo = 0, own_hi = 0, ext_lo = 0, ext_hi = 0, iy_lo = 0, iy_hi = 0;
     // fused sweep (K2F): ping-pong partner of the iterate, L2-resident ring, schedule tables
     bool fused = false;
     int fused_tile = 0;
@@ -231,6 +233,10 @@ struct b200p_plan {
     cudaStream_t pending_stream = nullptr;
     bool pending = false;
     bool pending_eager = false;  // the pending solve ran eagerly (launches already counted)
+    // strip mode: the finest level is cut into horizontal strips over ranks; `exchange` moves data
+    bool strip = false;
+    b200p_exchange_fn exchange = nullptr;
+    void *exchange_user = nullptr;
     // CG-smoothed pipelines (cg, ml-cg, mg-cg): CG vectors sized for level 0 + per-problem state
     double *cg_r = nullptr, *cg_p = nullptr, *cg_q = nullptr;
     CgState cgs = {};
@@ -461,6 +467,16 @@ static double field_bytes(const b200p_plan *pl, const LevelHost &L, double field
 
 static int rows_chunk(int h) { return h >= 1024 ? 32 : (h >= 256 ? 16 : 8); }
 
+// Strip mode: level 0 is cut into horizontal strips over ranks, coarser levels are replicated.
+static bool striped(const b200p_plan *pl, const LevelHost &L) { return pl->strip && &L == &pl->lev[0]; }
+
+static int strip_exchange(b200p_plan *pl, int kind, void *d_ptr, cudaStream_t st) {
+    if (!pl->exchange) return fail_arg(B200P_ERR_STATE, "strip mode needs an exchange callback");
+    const int rc = pl->exchange(pl->exchange_user, kind, d_ptr, (void *)st);
+    if (rc) return fail_arg(B200P_ERR_STATE, "strip exchange %d failed (%d)", kind, rc);
+    return 0;
+}
+
 static bool rows4_ok(const LevelHost &L, const double *u, const double *b) {
     const size_t plane = (size_t)L.info.height * L.info.width;
     return L.info.width % 4 == 0 && L.info.width >= 8 && plane % 4 == 0 && ((uintptr_t)u % 16) == 0 &&
@@ -480,6 +496,8 @@ static RowsArgs rows_args(b200p_plan *pl, const LevelHost &L, const double *u, c
     R.plane = (size_t)L.info.height * L.info.width;
     R.pred = pred;
     R.rows_per_cta = rows_chunk(L.info.height);
+    R.y_lo = L.own_lo;
+    R.y_hi = L.own_hi;
     R.partial = pl->d_partial;
     R.partial_flag = pl->d_partial_flag;
     R.counter = pl->d_counter;
@@ -500,14 +518,21 @@ static int launch_norm(b200p_plan *pl, const LevelHost &L, const double *u, cons
         // four columns per thread, 16-byte loads (kernels_rows.cuh)
         RowsArgs R = rows_args(pl, L, u, b, pred);
         dim3 g4((L.info.width / 4 + ROWS4_THREADS - 1) / ROWS4_THREADS,
-                (L.info.height + R.rows_per_cta - 1) / R.rows_per_cta, pl->P);
+                (R.y_hi - R.y_lo + R.rows_per_cta - 1) / R.rows_per_cta, pl->P);
         if (um && rm) residual_sqnorm_rows4_kernel<true, true><<<g4, ROWS4_THREADS, 0, st>>>(R);
         else if (um) residual_sqnorm_rows4_kernel<true, false><<<g4, ROWS4_THREADS, 0, st>>>(R);
         else if (rm) residual_sqnorm_rows4_kernel<false, true><<<g4, ROWS4_THREADS, 0, st>>>(R);
         else residual_sqnorm_rows4_kernel<false, false><<<g4, ROWS4_THREADS, 0, st>>>(R);
         CU(cudaGetLastError());
+        if (striped(pl, L)) {
+            // the strip's partial sums (and mask-residual flags) -> totals over all ranks
+            int rc = strip_exchange(pl, B200P_XCHG_SUM_RS, pl->d_rs, st);
+            if (!rc) rc = strip_exchange(pl, B200P_XCHG_MAX_FLAGS, pl->d_mflag, st);
+            return rc;
+        }
         return 0;
     }
+    if (striped(pl, L)) return fail_arg(B200P_ERR_UNSUPPORTED, "strip mode needs the row-walker kernels (width % 4 == 0)");
     const bool vec_ok = L.info.width % 2 == 0 && L.info.width >= 4 && ((uintptr_t)u % 16) == 0 &&
                         ((uintptr_t)L.d_mask % 2) == 0 && (plane % 2) == 0;
     if (vec_ok) {
@@ -732,7 +757,10 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, double *u, con
                               const int *pred, int *unit_counter, int tile, cudaStream_t st) {
     SweepArgs A;
     fill_sweep_args(pl, L, u, b, pred, A);
+    A.iy0 = L.iy_lo;
     dim3 grid(L.nblocks, pl->P);
+    if (striped(pl, L) && !(tile == TILE_32_L && tma_eligible(L, u, b, rm)))
+        return fail_arg(B200P_ERR_UNSUPPORTED, "strip mode needs the 32x32 lean block-solve kernel");
     {
         // read u (+ b) + mask, write the weighted correction tiles
         LaunchScope sc(pl, st, KK_SWEEP_SPLIT, field_bytes(pl, L, rm ? 2.0 : 3.0, 1.0));
@@ -740,7 +768,7 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, double *u, con
         switch (tile) {
             case TILE_32_L: {
                 static const int cap = getenv("B200P_REGCAP") ? atoi(getenv("B200P_REGCAP")) : 168;
-                dim3 g3(L.info.nx, L.info.ny, pl->P);
+                dim3 g3(L.info.nx, L.iy_hi - L.iy_lo, pl->P);  // strip mode: only the block rows of this rank
 #define KL_LAUNCH(CAP)                                                                      \
     do {                                                                                    \
         if (rm) oras_sweep_lean_kernel<true, CAP><<<g3, 64, 0, st>>>(A, L.d_mtab);          \
@@ -786,13 +814,15 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, double *u, con
     }
     {
         dim3 g((L.info.width + ST_THREADS_COMBINE - 1) / ST_THREADS_COMBINE,
-               (L.info.height + COMBINE_ROWS - 1) / COMBINE_ROWS, pl->P);
+               (L.own_hi - L.own_lo + COMBINE_ROWS - 1) / COMBINE_ROWS, pl->P);
         // read corrections + u, write u
         LaunchScope sc(pl, st, KK_COMBINE, field_bytes(pl, L, 3.0, 0.0));
         oras_combine_kernel<<<g, ST_THREADS_COMBINE, 0, st>>>(L.dev, pl->d_scratch, A.plane, pred,
-                                                              pl->d_rs, u, unit_counter);
+                                                              pl->d_rs, u, unit_counter, L.own_lo, L.own_hi);
         CU(cudaGetLastError());
     }
+    // strip mode: the rows the neighbours' block solves and stencils read from this strip
+    if (striped(pl, L)) return strip_exchange(pl, B200P_XCHG_HALO_U, u, st);
     return 0;
 }
 
@@ -873,7 +903,7 @@ static int pack_masks(b200p_plan *pl, const LevelHost &L, cudaStream_t st) {
     if (!L.d_mtab) return 0;
     LaunchScope sc(pl, st, KK_DOWN_MASK, (double)pl->F * L.nblocks * (32.0 * 32.0 + 4.0 * KT_THREADS));
     pack_block_masks_kernel<<<dim3(L.nblocks, pl->F), KT_THREADS, 0, st>>>(
-        L.dev, L.d_mask, (size_t)L.info.height * L.info.width, L.d_mtab);
+        L.dev, L.d_mask, (size_t)L.info.height * L.info.width, L.d_mtab, 0);
     CU(cudaGetLastError());
     return 0;
 }
@@ -945,8 +975,11 @@ static int enqueue_cascade(b200p_plan *pl, double *d_u0, cudaStream_t st) {
         UBuf uf = level_ubuf(pl, l, d_u0);
         {
             LaunchScope sc(pl, st, KK_PROLONG_SOL, field_bytes(pl, f, 1.25, 1.0));
-            prolongate_kernel<true><<<grid2x(c.info.width, c.info.height, pl->P), ST_THREADS, 0, st>>>(
-                coarse_u, f.d_mask, f.d_rhs, f.info.height, f.info.width, pl->C, nullptr, uf.cur);
+            // strip mode: the coarse level is replicated, so the strip and its halo rows are
+            // prolongated locally (no exchange)
+            const int Ylo = f.ext_lo >> 1, Yhi = (f.ext_hi + 1) >> 1;
+            prolongate_kernel<true><<<grid2x(c.info.width, Yhi - Ylo, pl->P), ST_THREADS, 0, st>>>(
+                coarse_u, f.d_mask, f.d_rhs, f.info.height, f.info.width, pl->C, nullptr, uf.cur, Ylo, Yhi);
             CU(cudaGetLastError());
         }
         if (l > 0) {
@@ -989,10 +1022,12 @@ static int enqueue_vcycle(b200p_plan *pl, int level, UBuf &u, const double *b, b
             RA.rc = Cc.d_rc;
             RA.e_zero = ez;
             dim3 g4((L.info.width / 4 + ROWS4_THREADS - 1) / ROWS4_THREADS,
-                    (L.info.height + RA.R.rows_per_cta - 1) / RA.R.rows_per_cta, pl->P);
+                    (RA.R.y_hi - RA.R.y_lo + RA.R.rows_per_cta - 1) / RA.R.rows_per_cta, pl->P);
             if (rm) residual_restrict_rows4_kernel<true><<<g4, ROWS4_THREADS, 0, st>>>(RA);
             else residual_restrict_rows4_kernel<false><<<g4, ROWS4_THREADS, 0, st>>>(RA);
-            coarse_norm = true;
+            coarse_norm = !striped(pl, L);  // a strip only has its share of ||r_c||^2: the coarse level takes its own norm
+        } else if (striped(pl, L)) {
+            return fail_arg(B200P_ERR_UNSUPPORTED, "strip mode needs the row-walker kernels (width % 4 == 0)");
         } else {
             dim3 g = grid2x(Cc.info.width, Cc.info.height, pl->P);
             if (rm)
@@ -1006,6 +1041,13 @@ static int enqueue_vcycle(b200p_plan *pl, int level, UBuf &u, const double *b, b
         }
         CU(cudaGetLastError());
     }
+    if (striped(pl, L)) {
+        // every rank restricted its own rows: collect the replicated coarse right-hand side, and zero
+        // the whole coarse correction (K3 only zeroed this strip's rows)
+        if ((rc = strip_exchange(pl, B200P_XCHG_GATHER_RC, Cc.d_rc, st))) return rc;
+        if (level + 1 != nl - 1)
+            CU(cudaMemsetAsync(e.cur, 0, sizeof(double) * (size_t)pl->P * Cc.info.height * Cc.info.width, st));
+    }
     if (level + 1 == nl - 1) {
         const double tol = std::min(cfg.coarse_tol, cfg.tol_rel);
         rc = launch_coarse(pl, Cc, e.cur, Cc.d_rc, false, 0, tol, cfg.coarse_max_iters, pred,
@@ -1016,8 +1058,10 @@ static int enqueue_vcycle(b200p_plan *pl, int level, UBuf &u, const double *b, b
     if (rc) return rc;
     {
         LaunchScope sc(pl, st, KK_PROLONG_CORR, field_bytes(pl, L, 2.25, 1.0));
-        prolongate_kernel<false><<<grid2x(Cc.info.width, Cc.info.height, pl->P), ST_THREADS, 0, st>>>(
-            e.cur, L.d_mask, nullptr, L.info.height, L.info.width, pl->C, pred, u.cur);
+        // strip mode: e is replicated, the strip and its halo rows are corrected locally
+        const int Ylo = L.ext_lo >> 1, Yhi = (L.ext_hi + 1) >> 1;
+        prolongate_kernel<false><<<grid2x(Cc.info.width, Yhi - Ylo, pl->P), ST_THREADS, 0, st>>>(
+            e.cur, L.d_mask, nullptr, L.info.height, L.info.width, pl->C, pred, u.cur, Ylo, Yhi);
         CU(cudaGetLastError());
     }
     if ((rc = enqueue_smooth(pl, L, u, b, rm, cfg.nu_post, pred, uc, false, st))) return rc;
@@ -1690,6 +1734,10 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
         PTRY(dev_upload(pl, cyf, &D.cyf));
         PTRY(dev_upload(pl, cyn, &D.cyn));
         L.tile = tile_for(D.bw, D.bh);
+        L.own_lo = L.ext_lo = 0;
+        L.own_hi = L.ext_hi = h;
+        L.iy_lo = 0;
+        L.iy_hi = L.info.ny;
         const size_t plane = (size_t)h * w;
         {
             const char *e = getenv("B200P_FUSED");
@@ -1809,6 +1857,73 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
 }
 
 int b200p_plan_num_levels(const b200p_plan *pl) { return pl ? (int)pl->lev.size() : 0; }
+
+int b200p_plan_strip_ranges(const b200p_plan *pl, int rank, int nranks, int out[6]) {
+    if (!pl || !out) return fail_arg(B200P_ERR_ARG, "null argument");
+    const LevelHost &L = pl->lev[0];
+    const int ny = L.info.ny, H = L.info.height, bh = L.info.block_h;
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+        return fail_arg(B200P_ERR_ARG, "bad rank %d of %d", rank, nranks);
+    if (nranks > ny) return fail_arg(B200P_ERR_ARG, "%d ranks for %d block rows", nranks, ny);
+    const std::vector<int> ys = axis_starts(H, pl->cfg.block_size, pl->cfg.block_size - pl->cfg.overlap);
+    std::vector<int> cyf, cyn;
+    axis_cover(ys, bh, H, cyf, cyn);
+    // block rows are dealt out evenly; a rank owns the pixel rows from its first block row's start to
+    // the next rank's
+    const int k0 = (int)((long long)rank * ny / nranks), k1 = (int)((long long)(rank + 1) * ny / nranks);
+    const int own_lo = k0 == 0 ? 0 : ys[k0], own_hi = k1 == ny ? H : ys[k1];
+    if (own_hi <= own_lo) return fail_arg(B200P_ERR_ARG, "empty strip for rank %d", rank);
+    if ((own_lo | own_hi) & 1) {
+        if (own_hi != H || (own_lo & 1))
+            return fail_arg(B200P_ERR_UNSUPPORTED, "strip mode needs even block-row starts");
+    }
+    // block rows that cover an owned pixel row are solved here (boundary rows redundantly by both sides)
+    int iy_lo = ny, iy_hi = 0;
+    for (int y = own_lo; y < own_hi; ++y) {
+        iy_lo = std::min(iy_lo, cyf[y]);
+        iy_hi = std::max(iy_hi, cyf[y] + cyn[y]);
+    }
+    // rows those block solves (1-pixel gather halo) and the stencils of the owned rows read
+    int ext_lo = std::max(0, ys[iy_lo] - 1), ext_hi = std::min(H, ys[iy_hi - 1] + bh + 1);
+    ext_lo &= ~1;
+    if (ext_hi < H) ext_hi = std::min(H, (ext_hi + 1) & ~1);
+    out[0] = own_lo; out[1] = own_hi; out[2] = ext_lo; out[3] = ext_hi; out[4] = iy_lo; out[5] = iy_hi;
+    return 0;
+}
+
+int b200p_plan_set_strip(b200p_plan *pl, const int r[6], b200p_exchange_fn exchange, void *user) {
+    if (!pl || !r) return fail_arg(B200P_ERR_ARG, "null argument");
+    LevelHost &L = pl->lev[0];
+    const int H = L.info.height;
+    if (pl->pending) return fail_arg(B200P_ERR_STATE, "a solve is pending on this plan");
+    if (!exchange && r[0] == 0 && r[1] == H) {  // back to the whole image
+        pl->strip = false;
+        pl->exchange = nullptr;
+        L.own_lo = L.ext_lo = 0; L.own_hi = L.ext_hi = H; L.iy_lo = 0; L.iy_hi = L.info.ny;
+        return 0;
+    }
+    if (!exchange) return fail_arg(B200P_ERR_ARG, "strip mode needs an exchange callback");
+    if (pl->cfg.use_graphs) return fail_arg(B200P_ERR_STATE, "strip plans run eagerly: create the plan with use_graphs = 0");
+    if (pl->cfg.mode != 0 || pl->cfg.smoother != 0)
+        return fail_arg(B200P_ERR_UNSUPPORTED, "strip mode covers the mg-oras path only");
+    if (pl->lev.size() < 2) return fail_arg(B200P_ERR_UNSUPPORTED, "strip mode needs at least two levels");
+    if (!L.d_mtab || L.info.width % 4 != 0)
+        return fail_arg(B200P_ERR_UNSUPPORTED, "strip mode needs 32x32 blocks with even starts and width % 4 == 0");
+    if (!(0 <= r[2] && r[2] <= r[0] && r[0] < r[1] && r[1] <= r[3] && r[3] <= H && 0 <= r[4] && r[4] < r[5] &&
+          r[5] <= L.info.ny) || (r[0] & 1) || (r[2] & 1) || ((r[1] & 1) && r[1] != H) || ((r[3] & 1) && r[3] != H))
+        return fail_arg(B200P_ERR_ARG, "inconsistent strip ranges");
+    L.own_lo = r[0]; L.own_hi = r[1]; L.ext_lo = r[2]; L.ext_hi = r[3]; L.iy_lo = r[4]; L.iy_hi = r[5];
+    pl->strip = true;
+    pl->exchange = exchange;
+    pl->exchange_user = user;
+    return 0;
+}
+
+int b200p_plan_level_rc(const b200p_plan *pl, int level, double **d_rc) {
+    if (!pl || !d_rc || level < 1 || level >= (int)pl->lev.size()) return fail_arg(B200P_ERR_ARG, "bad level %d", level);
+    *d_rc = pl->lev[level].d_rc;
+    return 0;
+}
 
 int b200p_plan_level_info(const b200p_plan *pl, int level, b200p_level_info *out) {
     if (!pl || !out || level < 0 || level >= (int)pl->lev.size())

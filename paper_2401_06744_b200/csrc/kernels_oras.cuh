@@ -38,6 +38,7 @@ struct SweepArgs {
     double eta;            // local_tol_fraction
     int max_iters;         // local CG cap
     double *scratch;       // (P, nblocks, bh, bw) weighted corrections
+    int iy0;               // first block row of this launch (strip mode; default 0)
 };
 
 // ------------------------------------------------------------------ K2 ----
@@ -440,7 +441,7 @@ oras_sweep_lean_kernel(const SweepArgs A, const unsigned *__restrict__ mtab) {
     const double rs_g = A.rs[p];
     if (rs_g == 0.0) return;  // oras_sweeps exit, solvers.py:420
     const LevelDev &L = A.L;
-    const int ix = blockIdx.x, iy = blockIdx.y, blk = iy * L.nx + ix;
+    const int ix = blockIdx.x, iy = blockIdx.y + A.iy0, blk = iy * L.nx + ix;
     const int tid = threadIdx.x;
     // frame of the problem (channels share the mask): constant divisors for gray / RGB
     const int frame = A.channels == 3 ? p / 3 : (A.channels == 1 ? p : p / A.channels);
@@ -1332,7 +1333,7 @@ constexpr int COMBINE_G = 8;
 __global__ void __launch_bounds__(ST_THREADS_COMBINE)
 oras_combine_kernel(const LevelDev L, const double *__restrict__ scratch, size_t plane,
                     const int *__restrict__ pred, const double *__restrict__ rs,
-                    double *__restrict__ u, int *__restrict__ unit_counter) {
+                    double *__restrict__ u, int *__restrict__ unit_counter, int y_lo, int y_hi) {
     __shared__ int s_rn[COMBINE_ROWS], s_rf[COMBINE_ROWS];
     __shared__ size_t s_roff[COMBINE_ROWS][2];
     const int p = blockIdx.z;
@@ -1340,8 +1341,8 @@ oras_combine_kernel(const LevelDev L, const double *__restrict__ scratch, size_t
     if (rs[p] == 0.0) return;
     const int tid = threadIdx.x;
     const int x = blockIdx.x * ST_THREADS_COMBINE + tid;
-    const int y0 = blockIdx.y * COMBINE_ROWS;
-    const int rows = min(COMBINE_ROWS, L.h - y0);
+    const int y0 = y_lo + blockIdx.y * COMBINE_ROWS;  // rows [y_lo, y_hi): the whole level, or a strip
+    const int rows = min(COMBINE_ROWS, y_hi - y0);
     if (unit_counter && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) unit_counter[p] += 1;
     const size_t bsz = (size_t)L.bw * L.bh;
     if (tid < rows) {

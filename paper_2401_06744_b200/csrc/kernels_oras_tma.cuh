@@ -89,8 +89,8 @@ struct KtSmem {
 // Packs the block-local masks of a level: grid (nblocks, F), 64 threads.
 __global__ void __launch_bounds__(KT_THREADS)
 pack_block_masks_kernel(const LevelDev L, const uint8_t *__restrict__ mask, size_t plane,
-                        unsigned *__restrict__ mtab) {
-    const int blk = blockIdx.x, f = blockIdx.y, t = threadIdx.x;
+                        unsigned *__restrict__ mtab, int blk0) {
+    const int blk = blockIdx.x + blk0, f = blockIdx.y, t = threadIdx.x;
     const int iy = blk / L.nx, ix = blk - iy * L.nx;
     const int lane = t & 31, wg = t >> 5;
     const int gx0 = L.xs[ix] + (lane & 7) * 4, gy0 = L.ys[iy] + (wg * 4 + (lane >> 3)) * 4;

@@ -31,6 +31,7 @@ struct RowsArgs {
     size_t plane;
     const int *pred;
     int rows_per_cta;  // even
+    int y_lo, y_hi;    // rows handled by this launch (strip mode; default 0 .. h)
     // reduction of the per-CTA partials (last CTA of a problem sums them in index order)
     double *partial;
     int *partial_flag;
@@ -172,8 +173,8 @@ residual_sqnorm_rows4_kernel(const RowsArgs A) {
     const int x = 4 * (blockIdx.x * ROWS4_THREADS + threadIdx.x);
     const bool live = x < A.w;
     const int xc = live ? x : A.w - 4;  // dead lanes shadow the last column group (shuffles stay defined)
-    const int y0 = blockIdx.y * A.rows_per_cta;
-    const int y1 = min(A.h, y0 + A.rows_per_cta);
+    const int y0 = A.y_lo + blockIdx.y * A.rows_per_cta;
+    const int y1 = min(A.y_hi, y0 + A.rows_per_cta);
     double acc = 0.0;
     int flag = 0;
     auto consume = [&](int, const double (&r)[4], const uint8_t (&m)[4]) {
@@ -219,8 +220,8 @@ residual_restrict_rows4_kernel(const RestrictArgs A) {
     const int x = 4 * (blockIdx.x * ROWS4_THREADS + threadIdx.x);
     const bool live = x < w;
     const int xc = live ? x : w - 4;
-    const int y0 = blockIdx.y * R.rows_per_cta;  // even
-    const int y1 = min(h, y0 + R.rows_per_cta);
+    const int y0 = R.y_lo + blockIdx.y * R.rows_per_cta;  // even
+    const int y1 = min(R.y_hi, y0 + R.rows_per_cta);
     const size_t cplane = (size_t)hc * wc;
     const uint8_t *cm = A.cmask + (size_t)(p / R.channels) * cplane;
     double *rc = A.rc + (size_t)p * cplane;

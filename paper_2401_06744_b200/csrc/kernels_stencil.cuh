@@ -371,13 +371,13 @@ template <bool SOLUTION>
 __global__ void __launch_bounds__(ST_THREADS)
 prolongate_kernel(const double *__restrict__ c, const uint8_t *__restrict__ fmask,
                   const double *__restrict__ frhs, int h, int w, int channels,
-                  const int *__restrict__ pred, double *__restrict__ u) {
+                  const int *__restrict__ pred, double *__restrict__ u, int Y_lo = 0, int Y_hi = 1 << 30) {
     const int p = blockIdx.z;
     if (pred && !pred[p]) return;
     const int hc = (h + 1) >> 1, wc = (w + 1) >> 1;
     const int X = blockIdx.x * 64 + (threadIdx.x & 63);
-    const int Y = blockIdx.y * 4 + (threadIdx.x >> 6);
-    if (X >= wc || Y >= hc) return;
+    const int Y = Y_lo + blockIdx.y * 4 + (threadIdx.x >> 6);  // coarse rows [Y_lo, Y_hi): strip mode
+    if (X >= wc || Y >= hc || Y >= Y_hi) return;
     const size_t fplane = (size_t)h * w, cplane = (size_t)hc * wc;
     const double *cp = c + (size_t)p * cplane;
     const uint8_t *fm = fmask + (size_t)(p / channels) * fplane;
