@@ -156,6 +156,68 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_strip(args, rank, world, local):
+    """One frame, strip-decomposed over `world` ranks (strong scaling): every rank holds the full
+    input, owns a horizontal strip of the finest level, and exchanges one-block-deep halos of the
+    iterate per ORAS sweep plus the restricted residual per V-cycle (paper_2401_06744_b200/strip.py)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2401_06744_b200 as bp
+    from paper_2401_06744_b200 import strip, synthetic
+
+    name = args.workload if args.workload != "4k_rgb_2pct_b32o6" else "8k_rgb_2pct_b32o6"
+    W, H, C, density, bs, ov = WORKLOADS[name]
+    cfg = bp.MultigridConfig(block_size=bs, overlap=ov)
+    mask, known = synthetic.seeded_problem(W, H, density, 0, C)
+    if "RANK" in os.environ and not dist.is_initialized():  # torchrun with one rank: still exercise NCCL
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if dist.is_initialized():
+        transport = strip.TorchDistTransport()
+    else:
+        transport = strip.LocalGroup(1).transport(0)
+    solver = strip.StripSolver(W, H, C, cfg, transport)
+    d_mask = torch.from_numpy(mask.view(np.uint8)[None]).cuda()
+    d_known = torch.from_numpy(known[None]).cuda()
+    d_out = torch.zeros_like(d_known)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 1)):
+        _, reports = solver.plan.solve_device(d_mask, d_known, d_out)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        solver.plan.solve_device(d_mask, d_known, d_out, want_reports=False)
+    e1.record()
+    barrier()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    if rank == 0:
+        lo, hi = solver.own
+        print(json.dumps({
+            "metric": "single-frame strip-mode frames/sec (FMG to fixed residual)",
+            "value": args.steps / (ms_total * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 1), "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": name, "width": W, "height": H, "channels": C, "mask_density": density,
+                       "block_size": bs, "overlap": ov, "tol_rel": 1e-3, "frames": 1,
+                       "v_cycles": [r.iterations for r in reports],
+                       "parallelism": f"1 frame in {world} horizontal strip(s); rank 0 owns rows [{lo}, {hi}); "
+                                      "halo exchange per sweep, coarse levels replicated"}}), flush=True)
+    solver.close()
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -168,6 +230,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--strip", action="store_true",
+                    help="single-frame strip mode: ONE frame cut into horizontal strips over the ranks "
+                         "(halo exchange per sweep over NCCL); default workload 8k_rgb_2pct_b32o6")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     # the CPU arm costs seconds per step: bound the run to a few minutes
@@ -194,6 +259,10 @@ def main():
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    if args.strip:
+        run_strip(args, rank, world, local)
+        return
 
     W, H, C, density, bs, ov = WORKLOADS[args.workload]
     F = args.frames

@@ -144,6 +144,8 @@ int b200p_plan_level_info(const b200p_plan *plan, int level, b200p_level_info *o
 /* Strip geometry of rank `rank` of `nranks` for this plan's finest level: block rows are dealt out
  * evenly; out = {own_lo, own_hi, ext_lo, ext_hi, iy_lo, iy_hi}.  Host-only. */
 int b200p_plan_strip_ranges(const b200p_plan *plan, int rank, int nranks, int out[6]);
+/* The same from the geometry alone (image height, block_size, overlap). */
+int b200p_strip_ranges(int height, int block, int overlap, int rank, int nranks, int out[6]);
 /* Puts the plan into strip mode with the given ranges (from b200p_plan_strip_ranges) and callback;
  * rank / nranks themselves are the callback's business.  own range (0, H) + NULL callback leaves it. */
 int b200p_plan_set_strip(b200p_plan *plan, const int ranges[6], b200p_exchange_fn exchange, void *user);

@@ -7,7 +7,7 @@ the arithmetic runs in ``libb200paint.so`` (hand-written CUDA, C-ABI in
 ``include/b200paint.h``).  No CPU fallback.
 """
 
-from . import _lib, suites
+from . import _lib, strip, suites
 from .core import (EmptyMaskError, InpaintingProblem, Metrics, StencilOperator, apply_operator,
                    as_field, as_mask, compute_metrics, mask_density, residual)
 from .multigrid import (Level, LevelHierarchy, MultigridConfig, Plan, build_hierarchy, cached_plan,
@@ -36,5 +36,5 @@ __all__ = [
     "extend_add_weighted", "restrict_to_block",
     "SOLVER_NAMES", "SolveResult", "join_solver_name", "solve_channel", "solve_frames", "solve_image",
     "split_solver_name",
-    "BlockSolver", "SolveReport", "SolverConfig", "oras_sweeps", "FramePipeline", "suites",
+    "BlockSolver", "SolveReport", "SolverConfig", "oras_sweeps", "FramePipeline", "suites", "strip",
 ]

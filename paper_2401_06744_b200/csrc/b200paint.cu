@@ -1860,12 +1860,18 @@ int b200p_plan_num_levels(const b200p_plan *pl) { return pl ? (int)pl->lev.size(
 
 int b200p_plan_strip_ranges(const b200p_plan *pl, int rank, int nranks, int out[6]) {
     if (!pl || !out) return fail_arg(B200P_ERR_ARG, "null argument");
-    const LevelHost &L = pl->lev[0];
-    const int ny = L.info.ny, H = L.info.height, bh = L.info.block_h;
+    return b200p_strip_ranges(pl->cfg.height, pl->cfg.block_size, pl->cfg.overlap, rank, nranks, out);
+}
+
+int b200p_strip_ranges(int H, int block, int overlap, int rank, int nranks, int out[6]) {
+    if (!out) return fail_arg(B200P_ERR_ARG, "null argument");
+    if (H < 1 || block <= overlap || overlap < 0)
+        return fail_arg(B200P_ERR_ARG, "need height >= 1 and block_size > overlap >= 0");
+    const std::vector<int> ys = axis_starts(H, block, block - overlap);
+    const int ny = (int)ys.size(), bh = std::min(block, H);
     if (nranks < 1 || rank < 0 || rank >= nranks)
         return fail_arg(B200P_ERR_ARG, "bad rank %d of %d", rank, nranks);
     if (nranks > ny) return fail_arg(B200P_ERR_ARG, "%d ranks for %d block rows", nranks, ny);
-    const std::vector<int> ys = axis_starts(H, pl->cfg.block_size, pl->cfg.block_size - pl->cfg.overlap);
     std::vector<int> cyf, cyn;
     axis_cover(ys, bh, H, cyf, cyn);
     // block rows are dealt out evenly; a rank owns the pixel rows from its first block row's start to

@@ -1,0 +1,251 @@
+"""Single-frame strip decomposition over several GPUs (BASELINE config 4b).
+
+The finest level is cut into horizontal strips, one per rank (one process per GPU); all coarser
+levels are replicated.  A rank owns the pixel rows ``[own_lo, own_hi)`` (block-row starts), solves
+the block rows that cover them (boundary block rows redundantly on both sides, so the ordered
+combine needs no foreign tiles) and keeps the one-block-deep halo ``[ext_lo, ext_hi)`` of the
+iterate valid.  Per ORAS sweep the ranks exchange
+
+* the strip's partial ``||r||^2`` (all-reduce of P doubles: target = eta * rs and the convergence
+  test use the GLOBAL norm, solvers.py:416-422),
+* the halo rows of the updated iterate (send/recv between neighbouring strips),
+
+and per V-cycle the restricted residual of the finest level (all-gather of the rows each rank
+restricted; the coarse levels are then solved identically on every rank).  Prolongation needs no
+exchange: the coarse correction is replicated, every rank prolongates onto its strip plus halo.
+
+The data movement is behind a small ``Transport``: ``TorchDistTransport`` (torch.distributed:
+NCCL over NVLink on GPUs, gloo in the CPU tests) and ``LocalTransport`` (virtual ranks as threads
+of one process on one device, used to check the decomposition against the single-GPU solve).
+The library side is ``b200p_plan_set_strip`` + the exchange callback (include/b200paint.h).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+
+import numpy as np
+import torch
+
+from . import _dev, _lib
+from .multigrid import MultigridConfig, Plan
+
+XCHG_SUM_RS, XCHG_MAX_FLAGS, XCHG_HALO_U, XCHG_GATHER_RC = 1, 2, 3, 4
+_EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p)
+
+
+class _DeviceArray:
+    """Raw device pointer -> torch tensor view (no copy) through __cuda_array_interface__."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 2}
+
+
+def device_view(ptr, shape, dtype):
+    typestr = {torch.float64: "<f8", torch.int32: "<i4"}[dtype]
+    return torch.as_tensor(_DeviceArray(ptr, shape, typestr), device=_dev.device())
+
+
+def halo_plan(ranges, rank):
+    """Row intervals to move for a halo exchange: [(peer, y0, y1)] to receive into `rank`'s halo and
+    to send from `rank`'s strip.  ranges[q] = (own_lo, own_hi, ext_lo, ext_hi, iy_lo, iy_hi)."""
+    def cut(ext, own_me, own_q):
+        out = []
+        for lo, hi in ((ext[0], own_me[0]), (own_me[1], ext[1])):  # halo above, halo below
+            a, b = max(lo, own_q[0]), min(hi, own_q[1])
+            if a < b:
+                out.append((a, b))
+        return out
+    me = ranges[rank]
+    recv, send = [], []
+    for q, r in enumerate(ranges):
+        if q == rank:
+            continue
+        recv += [(q, a, b) for a, b in cut((me[2], me[3]), (me[0], me[1]), (r[0], r[1]))]
+        send += [(q, a, b) for a, b in cut((r[2], r[3]), (r[0], r[1]), (me[0], me[1]))]
+    return recv, send
+
+
+def strip_ranges(height, block_size, overlap, nranks):
+    """[(own_lo, own_hi, ext_lo, ext_hi, iy_lo, iy_hi)] of all ranks (host-only geometry)."""
+    out = []
+    for q in range(nranks):
+        r = (C.c_int * 6)()
+        _lib.check(_lib.lib().b200p_strip_ranges(int(height), int(block_size), int(overlap), q, nranks, C.byref(r)))
+        out.append(tuple(r))
+    return out
+
+
+def coarse_rows(ranges, h1):
+    """Coarse (level-1) rows every rank restricted: own rows halved; the last strip runs to the end."""
+    out = []
+    for i, r in enumerate(ranges):
+        out.append((r[0] // 2, h1 if i == len(ranges) - 1 else r[1] // 2))
+    return out
+
+
+class Transport:
+    rank = 0
+    nranks = 1
+
+    def sum_(self, t): raise NotImplementedError
+    def max_(self, t): raise NotImplementedError
+    def halo(self, u, ranges): raise NotImplementedError
+    def gather_rows(self, field, rows): raise NotImplementedError
+
+
+class TorchDistTransport(Transport):
+    """torch.distributed (NCCL on CUDA tensors, gloo on CPU tensors)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank, self.nranks = dist.get_rank(group), dist.get_world_size(group)
+
+    def sum_(self, t):
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+
+    def max_(self, t):
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+
+    def halo(self, u, ranges):
+        recv, send = halo_plan(ranges, self.rank)
+        ops, landing = [], []
+        for q, a, b in send:
+            ops.append(self.dist.P2POp(self.dist.isend, u[:, a:b].contiguous(), q, self.group))
+        for q, a, b in recv:
+            buf = torch.empty_like(u[:, a:b])
+            landing.append((buf, a, b))
+            ops.append(self.dist.P2POp(self.dist.irecv, buf, q, self.group))
+        if ops:
+            for w in self.dist.batch_isend_irecv(ops):
+                w.wait()
+        for buf, a, b in landing:
+            u[:, a:b].copy_(buf)
+
+    def gather_rows(self, field, rows):
+        for q, (a, b) in enumerate(rows):
+            chunk = field[:, a:b].contiguous()
+            self.dist.broadcast(chunk, src=q, group=self.group)
+            if q != self.rank:
+                field[:, a:b].copy_(chunk)
+
+
+class LocalGroup:
+    """Virtual ranks inside one process (threads) on one device: the test double of a node."""
+
+    def __init__(self, nranks):
+        self.nranks = nranks
+        self.barrier = threading.Barrier(nranks)
+        self.slots = [None] * nranks
+
+    def transport(self, rank):
+        return LocalTransport(self, rank)
+
+
+class LocalTransport(Transport):
+    def __init__(self, group: LocalGroup, rank: int):
+        self.g, self.rank, self.nranks = group, rank, group.nranks
+
+    def _publish(self, t):
+        torch.cuda.synchronize() if t.is_cuda else None
+        self.g.slots[self.rank] = t
+        self.g.barrier.wait()
+
+    def _done(self):
+        torch.cuda.synchronize() if torch.cuda.is_available() else None
+        self.g.barrier.wait()
+
+    def _reduce(self, t, op):
+        self._publish(t.clone())
+        acc = self.g.slots[0].clone()
+        for q in range(1, self.nranks):  # rank order: every virtual rank forms the same value
+            acc = op(acc, self.g.slots[q])
+        self.g.barrier.wait()
+        t.copy_(acc)
+        self._done()
+
+    def sum_(self, t): self._reduce(t, torch.add)
+    def max_(self, t): self._reduce(t, torch.maximum)
+
+    def halo(self, u, ranges):
+        self._publish(u)
+        recv, _ = halo_plan(ranges, self.rank)
+        for q, a, b in recv:
+            u[:, a:b].copy_(self.g.slots[q][:, a:b])
+        self._done()
+
+    def gather_rows(self, field, rows):
+        self._publish(field)
+        for q, (a, b) in enumerate(rows):
+            if q != self.rank:
+                field[:, a:b].copy_(self.g.slots[q][:, a:b])
+        self._done()
+
+
+class StripSolver:
+    """One rank of a strip-decomposed mg-oras solve of a single frame.
+
+    Every rank passes the FULL mask and known values; `solve` returns this rank's rows of the
+    solution (device tensor (C, own_hi - own_lo, W)), and the reports, identical on all ranks."""
+
+    def __init__(self, width, height, channels, cfg: MultigridConfig | None, transport: Transport,
+                 spacing: float = 1.0):
+        self.t = transport
+        self.cfg = cfg or MultigridConfig()
+        self.plan = Plan(width, height, channels, 1, self.cfg, spacing, use_graphs=False)
+        self.shape = (int(channels), int(height), int(width))
+        L = _lib.lib()
+        self.ranges = strip_ranges(height, self.cfg.block_size, self.cfg.overlap, transport.nranks)
+        info1 = self.plan.level_info(1)
+        self.shape1 = (int(channels), info1.height, info1.width)
+        self.rows1 = coarse_rows(self.ranges, info1.height)
+        self.error = None
+        self._cb = _EXCHANGE_FN(self._exchange)  # keep the callback object alive
+        mine = (C.c_int * 6)(*self.ranges[transport.rank])
+        _lib.check(L.b200p_plan_set_strip(self.plan.handle, C.byref(mine), C.cast(self._cb, C.c_void_p), None))
+
+    @property
+    def own(self):
+        r = self.ranges[self.t.rank]
+        return r[0], r[1]
+
+    def _exchange(self, user, kind, d_ptr, stream):
+        try:
+            P = self.shape[0]
+            ext = torch.cuda.ExternalStream(int(stream or 0)) if stream else torch.cuda.default_stream()
+            with torch.cuda.stream(ext):
+                if kind == XCHG_SUM_RS:
+                    self.t.sum_(device_view(d_ptr, (P,), torch.float64))
+                elif kind == XCHG_MAX_FLAGS:
+                    self.t.max_(device_view(d_ptr, (P,), torch.int32))
+                elif kind == XCHG_HALO_U:
+                    self.t.halo(device_view(d_ptr, self.shape, torch.float64), self.ranges)
+                elif kind == XCHG_GATHER_RC:
+                    self.t.gather_rows(device_view(d_ptr, self.shape1, torch.float64), self.rows1)
+                else:
+                    return 1
+            return 0
+        except BaseException as e:  # never let an exception cross the C boundary
+            self.error = e
+            return 2
+
+    def solve(self, mask, known):
+        c, h, w = self.shape
+        d_mask = _dev.to_device_u8(np.ascontiguousarray(mask).view(np.uint8).reshape(1, h, w))
+        d_known = _dev.to_device_f64(np.ascontiguousarray(known, dtype=np.float64).reshape(1, c, h, w))
+        d_out = _dev.empty_f64((1, c, h, w))
+        d_out.zero_()
+        try:
+            _, reports = self.plan.solve_device(d_mask, d_known, d_out)
+        except Exception:
+            if self.error is not None:
+                raise self.error
+            raise
+        lo, hi = self.own
+        return d_out[0, :, lo:hi], reports
+
+    def close(self):
+        self.plan.close()
