@@ -387,7 +387,7 @@ def main():
     # + K2b ordered combine); SURVEY 8(d) states the sweep's algorithmic bytes as ONE unit
     # (read u + write u' + mask [+ rhs]), so both launches are charged against it.
     if "oras_sweep_split" in prof:
-        ms = prof["oras_sweep_split"][0] + prof["oras_combine"][0]
+        ms = prof["oras_sweep_split"][0] + prof.get("oras_combine", (0.0, 0, 0.0))[0]
         n = prof["oras_sweep_split"][1]
         by = prof["oras_sweep_split"][2]
         dom = "oras_sweep (K2 oras_sweep_lean_kernel + K2b oras_combine_kernel)"

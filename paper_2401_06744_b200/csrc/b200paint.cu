@@ -164,6 +164,9 @@ struct LevelHost {
     double *d_rc = nullptr;     // (P,h,w) restricted residual (levels >= 1)
     int tile = 0;               // K2 variant: 0 generic, else see launch_sweep
     unsigned *d_mtab = nullptr; // K2T: packed block-local masks (F, nblocks, 64); null = level not eligible
+    // combine on arrival (FUSE variant of the lean kernel): cell tables and arrival counters
+    const int *d_cell_need = nullptr, *d_lastx = nullptr, *d_lasty = nullptr;
+    unsigned *d_cell_cnt = nullptr;
     // strip mode (level 0 only): rows this rank owns / keeps valid, block rows it solves (default: all)
     int own_lo = 0, own_hi = 0, ext_lo = 0, ext_hi = 0, iy_lo = 0, iy_hi = 0;
     // fused sweep (K2F): ping-pong partner of the iterate, L2-resident ring, schedule tables
@@ -696,6 +699,15 @@ static int encode_field_map(CUtensorMap *tm, const double *base, int w, int h, i
     return 0;
 }
 
+// Combine on arrival inside K2 (no K2b launch, tiles consumed from L2): opt-in with B200P_ARRIVAL=1.
+// Parity-exact, but measured slower than K2 + K2b (193 vs 243 fps): the fence + arrival atomics + two
+// batches of L2 reads add ~5 k cycles of pure latency to every block in a kernel that is bound by
+// latency at 6 blocks per SM, whereas K2b hides the same reads behind full occupancy.
+static bool arrival_fusion_enabled() {
+    const char *e = getenv("B200P_ARRIVAL");  // read at plan creation (the plan then owns the tables)
+    return e && e[0] == '1';
+}
+
 static int tma_regcap() {
     static const int cap = getenv("B200P_TMA_REGCAP") ? atoi(getenv("B200P_TMA_REGCAP")) : 168;
     return cap;
@@ -753,8 +765,9 @@ static int launch_sweep_tma(b200p_plan *pl, const LevelHost &L, const SweepArgs 
 }
 
 // K2 + K2b: one ORAS sweep (in place on u.cur) using rs/mflag from the preceding K1.
-static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, double *u, const double *b, bool rm,
+static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, UBuf &ub, const double *b, bool rm,
                               const int *pred, int *unit_counter, int tile, cudaStream_t st) {
+    double *u = ub.cur;
     SweepArgs A;
     fill_sweep_args(pl, L, u, b, pred, A);
     A.iy0 = L.iy_lo;
@@ -769,6 +782,22 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, double *u, con
             case TILE_32_L: {
                 static const int cap = getenv("B200P_REGCAP") ? atoi(getenv("B200P_REGCAP")) : 168;
                 dim3 g3(L.info.nx, L.iy_hi - L.iy_lo, pl->P);  // strip mode: only the block rows of this rank
+                if (L.d_cell_cnt && !striped(pl, L) && ub.alt && ub.alt != ub.cur) {
+                    // combine on arrival: u.cur -> u.alt inside K2, no K2b launch
+                    FuseArgs Fz;
+                    Fz.u_out = ub.alt;
+                    Fz.cell_cnt = L.d_cell_cnt;
+                    Fz.cell_need = L.d_cell_need;
+                    Fz.lastx = L.d_lastx;
+                    Fz.lasty = L.d_lasty;
+                    Fz.unit_counter = unit_counter;
+                    CU(cudaMemsetAsync(L.d_cell_cnt, 0, sizeof(unsigned) * (size_t)pl->P * L.nblocks, st));
+                    if (rm) oras_sweep_lean_kernel<true, 168, true><<<g3, 64, 0, st>>>(A, L.d_mtab, Fz);
+                    else oras_sweep_lean_kernel<false, 168, true><<<g3, 64, 0, st>>>(A, L.d_mtab, Fz);
+                    CU(cudaGetLastError());
+                    std::swap(ub.cur, ub.alt);
+                    return 0;
+                }
 #define KL_LAUNCH(CAP)                                                                      \
     do {                                                                                    \
         if (rm) oras_sweep_lean_kernel<true, CAP><<<g3, 64, 0, st>>>(A, L.d_mtab);          \
@@ -831,7 +860,7 @@ static int launch_sweep(b200p_plan *pl, const LevelHost &L, UBuf &u, const doubl
                         const int *pred, int *unit_counter, int path, cudaStream_t st) {
     if ((path == -1 && L.fused) || path == -2)
         return launch_sweep_fused(pl, L, u, b, rm, pred, unit_counter, st);
-    return launch_sweep_split(pl, L, u.cur, b, rm, pred, unit_counter, path >= 0 ? path : L.tile, st);
+    return launch_sweep_split(pl, L, u, b, rm, pred, unit_counter, path >= 0 ? path : L.tile, st);
 }
 
 // _smooth (multigrid.py:264-279): `units` sweeps with stop_norm = 0.  When
@@ -1780,6 +1809,35 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
         for (int x : xs) xs_even = xs_even && (x % 2 == 0);
         if (D.bw == 32 && D.bh == 32 && w % 2 == 0 && xs_even)
             PTRY(dev_alloc(pl, &L.d_mtab, (size_t)pl->F * L.nblocks * KT_THREADS));
+        if (L.d_mtab && L.nblocks > 1 && arrival_fusion_enabled()) {
+            // cells = rectangles between consecutive block starts; a block overlaps the cells from its own
+            // index to the last one starting inside its extent
+            auto last_cell = [](const std::vector<int> &st, int extent) {
+                std::vector<int> last(st.size());
+                for (size_t i = 0; i < st.size(); ++i) {
+                    size_t c = i;
+                    while (c + 1 < st.size() && st[c + 1] < st[i] + extent) ++c;
+                    last[i] = (int)c;
+                }
+                return last;
+            };
+            const std::vector<int> lastx = last_cell(xs, D.bw), lasty = last_cell(ys, D.bh);
+            auto need_axis = [](const std::vector<int> &last) {
+                std::vector<int> need(last.size(), 0);
+                for (size_t i = 0; i < last.size(); ++i)
+                    for (int c = (int)i; c <= last[i]; ++c) need[c] += 1;
+                return need;
+            };
+            const std::vector<int> nxv = need_axis(lastx), nyv = need_axis(lasty);
+            std::vector<int> need((size_t)L.nblocks);
+            for (int cy = 0; cy < L.info.ny; ++cy)
+                for (int cx = 0; cx < L.info.nx; ++cx) need[(size_t)cy * L.info.nx + cx] = nxv[cx] * nyv[cy];
+            PTRY(dev_upload(pl, need, &L.d_cell_need));
+            PTRY(dev_upload(pl, lastx, &L.d_lastx));
+            PTRY(dev_upload(pl, lasty, &L.d_lasty));
+            PTRY(dev_alloc(pl, &L.d_cell_cnt, (size_t)pl->P * L.nblocks));
+            if (!L.d_u_alt) PTRY(dev_alloc(pl, &L.d_u_alt, (size_t)pl->P * h * w));
+        }
         if (l > 0) {
             PTRY(dev_alloc(pl, &L.d_mask, pl->F * plane));
             PTRY(dev_alloc(pl, &L.d_rhs, pl->P * plane));

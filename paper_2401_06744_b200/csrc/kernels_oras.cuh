@@ -430,19 +430,111 @@ struct LeanSmem {
     alignas(16) double wy[32];
 };
 
-template <bool RM, int REGCAP>
+// Combine on arrival (FUSE): the ordered sum of the covering tiles (K2b) is done inside K2 by
+// whichever block finishes LAST among the blocks that cover a cell.  Cells are the rectangles
+// between consecutive block starts, [xs[cx], xs[cx+1]) x [ys[cy], ys[cy+1]); a finished block
+// bumps the arrival counter of every cell it overlaps (after a __threadfence), and the block that
+// completes a cell's count sums the tiles -- just written by its neighbours, still in L2 -- in
+// ascending block order (np.bincount order, solvers.py:310-314) and writes u_out = u + sum.
+// Nobody waits: there is no spinning and no dependence on the scheduling order.  The sweep is out
+// of place (u -> u_out) because other blocks still gather from u.
+struct FuseArgs {
+    double *u_out;          // (P, h, w) or null: split path (tiles only, K2b combines)
+    unsigned *cell_cnt;     // (P, ny, nx) arrival counters, zeroed before the launch
+    const int *cell_need;   // (ny, nx) blocks covering each cell
+    const int *lastx, *lasty;  // per block column / row: last cell index it overlaps
+    int *unit_counter;      // per-problem sweep counter (may be null)
+};
+
+// u_out = u + ordered sum of the weighted tiles on cell (cx, cy).  64 threads: a thread owns one
+// column and every second row of the cell; like K2b the (up to) four tile reads of a pixel are
+// issued branch-free, CELL_G rows at a time, so ~35 independent loads are in flight per thread.
+constexpr int CELL_G = 7;
+
+__device__ __forceinline__ void combine_cell(const LevelDev &L, const double *scratch_p, const double *up,
+                                             double *wp, int cx, int cy, int tid) {
+    const int x0 = L.xs[cx], x1 = cx + 1 < L.nx ? L.xs[cx + 1] : L.w;
+    const int y0 = L.ys[cy], y1 = cy + 1 < L.ny ? L.ys[cy + 1] : L.h;
+    const size_t bsz = (size_t)L.bw * L.bh;
+    const int tx = tid & 31, ty = tid >> 5;
+    for (int xb = x0; xb < x1; xb += 32) {
+        const int x = xb + tx;
+        if (x >= x1) continue;
+        const int ixf = L.cxf[x], ixn = L.cxn[x];
+        const size_t xo0 = (size_t)ixf * bsz + (x - L.xs[ixf]);
+        const bool two_x = ixn > 1;
+        const size_t xo1 = two_x ? (size_t)(ixf + 1) * bsz + (x - L.xs[ixf + 1]) : xo0;
+        const bool wide_x = ixn > 2;
+        for (int yb = y0 + ty; yb < y1; yb += 2 * CELL_G) {
+            double uu[CELL_G], v00[CELL_G], v01[CELL_G], v10[CELL_G], v11[CELL_G];
+            int nn[CELL_G];
+#pragma unroll
+            for (int g = 0; g < CELL_G; ++g) {
+                const int yq = yb + 2 * g;
+                const int y = yq < y1 ? yq : y1 - 1;
+                const int iyf = L.cyf[y], iyn = L.cyn[y];
+                nn[g] = iyn;
+                const int iy1 = iyf + (iyn > 1 ? 1 : 0);
+                const size_t o0 = (size_t)iyf * L.nx * bsz + (size_t)(y - L.ys[iyf]) * L.bw;
+                const size_t o1 = (size_t)iy1 * L.nx * bsz + (size_t)(y - L.ys[iy1]) * L.bw;
+                uu[g] = up[(size_t)y * L.w + x];
+                v00[g] = __ldcg(scratch_p + o0 + xo0);
+                v01[g] = __ldcg(scratch_p + o0 + xo1);
+                v10[g] = __ldcg(scratch_p + o1 + xo0);
+                v11[g] = __ldcg(scratch_p + o1 + xo1);
+            }
+#pragma unroll
+            for (int g = 0; g < CELL_G; ++g) {
+                const int y = yb + 2 * g;
+                if (y >= y1) break;
+                const int n = nn[g];
+                // ascending block order: (iy0,ix0), (iy0,ix1), (iy1,ix0), (iy1,ix1)
+                double acc = v00[g];
+                acc += two_x ? v01[g] : 0.0;
+                if (wide_x || n > 2) {  // > 2 covering blocks per axis: heavily overlapped layouts
+                    acc = 0.0;
+                    const int iyf = L.cyf[y];
+                    for (int a = 0; a < n; ++a) {
+                        const int iy = iyf + a;
+                        const size_t ro = (size_t)iy * L.nx * bsz + (size_t)(y - L.ys[iy]) * L.bw;
+                        for (int c = 0; c < ixn; ++c)
+                            acc += __ldcg(scratch_p + ro + (size_t)(ixf + c) * bsz + (x - L.xs[ixf + c]));
+                    }
+                } else {
+                    acc += n > 1 ? v10[g] : 0.0;
+                    acc += (n > 1 && two_x) ? v11[g] : 0.0;
+                }
+                wp[(size_t)y * L.w + x] = uu[g] + acc;
+            }
+        }
+    }
+}
+
+template <bool RM, int REGCAP, bool FUSE = false>
 __global__ void __launch_bounds__(64) __maxnreg__(REGCAP)
-oras_sweep_lean_kernel(const SweepArgs A, const unsigned *__restrict__ mtab) {
+oras_sweep_lean_kernel(const SweepArgs A, const unsigned *__restrict__ mtab, const FuseArgs Fz = FuseArgs()) {
     constexpr int TW = 4, TH = 4, NWARP = 2, BW = 32, BH = 32;
     using CG = TileCG<TW, TH, NWARP>;
     __shared__ LeanSmem sm;
     const int p = blockIdx.z;
-    if (A.pred && !A.pred[p]) return;
-    const double rs_g = A.rs[p];
-    if (rs_g == 0.0) return;  // oras_sweeps exit, solvers.py:420
     const LevelDev &L = A.L;
     const int ix = blockIdx.x, iy = blockIdx.y + A.iy0, blk = iy * L.nx + ix;
     const int tid = threadIdx.x;
+    const bool frozen = A.pred && !A.pred[p];
+    const double rs_g = frozen ? 0.0 : A.rs[p];
+    if (frozen || rs_g == 0.0) {  // frozen problem, or oras_sweeps' rs == 0 exit (solvers.py:420)
+        if (FUSE) {
+            // the sweep is a no-op, but the iterate moves to the partner buffer with everybody else
+            const int x0 = L.xs[ix], x1 = ix + 1 < L.nx ? L.xs[ix + 1] : L.w;
+            const int y0 = L.ys[iy], y1 = iy + 1 < L.ny ? L.ys[iy + 1] : L.h;
+            const size_t off = (size_t)p * A.plane;
+            for (int y = y0 + (tid >> 5); y < y1; y += 2)
+                for (int x = x0 + (tid & 31); x < x1; x += 32)
+                    Fz.u_out[off + (size_t)y * L.w + x] = A.u[off + (size_t)y * L.w + x];
+        }
+        return;
+    }
+    if (FUSE && Fz.unit_counter && ix == 0 && iy == 0 && tid == 0) Fz.unit_counter[p] += 1;
     // frame of the problem (channels share the mask): constant divisors for gray / RGB
     const int frame = A.channels == 3 ? p / 3 : (A.channels == 1 ? p : p / A.channels);
     const unsigned mbits = mtab[((size_t)frame * L.nblocks + blk) * 64 + tid];
@@ -648,6 +740,27 @@ oras_sweep_lean_kernel(const SweepArgs A, const unsigned *__restrict__ mtab) {
             double2 *row = reinterpret_cast<double2 *>(out + (by + j) * BW + bx);
             row[0] = o0;
             row[1] = o1;
+        }
+    }
+    if (FUSE) {
+        // ---- combine on arrival
+        __shared__ int s_do[16];
+        __threadfence();   // this block's tile is visible device-wide before its arrivals are counted
+        __syncthreads();
+        const int cx1 = Fz.lastx[ix], cy1 = Fz.lasty[iy];
+        const int ncx = cx1 - ix + 1, ncell = ncx * (cy1 - iy + 1);
+        if (tid < ncell && tid < 16) {
+            const int cy = iy + tid / ncx, cx = ix + tid % ncx;
+            const int cell = cy * L.nx + cx;
+            const unsigned old = atomicAdd(&Fz.cell_cnt[(size_t)p * L.nblocks + cell], 1u);
+            s_do[tid] = (old + 1u == (unsigned)Fz.cell_need[cell]) ? 1 : 0;
+        }
+        __syncthreads();
+        for (int k = 0; k < ncell && k < 16; ++k) {
+            if (!s_do[k]) continue;
+            __threadfence();   // the other blocks' tiles (their fences precede their arrivals)
+            combine_cell(L, A.scratch + (size_t)p * L.nblocks * (BW * BH), A.u + (size_t)p * A.plane,
+                         Fz.u_out + (size_t)p * A.plane, ix + k % ncx, iy + k / ncx, tid);
         }
     }
 }

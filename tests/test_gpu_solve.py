@@ -342,6 +342,26 @@ def test_fused_and_split_sweeps_agree():
     a.close(); b.close()
 
 
+def test_combine_on_arrival_variant_agrees():
+    """Opt-in B200P_ARRIVAL=1: the ordered combine done inside K2 by the last block to arrive at a cell
+    (no K2b launch) gives the same fields and reports as the split sweep."""
+    import os
+    m, k = oracle.seeded_problem(640, 400, 0.02, 3, channels=3)
+    cfg = bp.MultigridConfig(block_size=32, overlap=6)
+    mk = m.view(np.uint8)[None]
+    a = bp.Plan(640, 400, 3, 1, cfg)
+    os.environ["B200P_ARRIVAL"] = "1"
+    try:
+        b = bp.Plan(640, 400, 3, 1, cfg)
+    finally:
+        del os.environ["B200P_ARRIVAL"]
+    oa, ra = a.solve_host(mk, k[None])
+    ob, rb = b.solve_host(mk, k[None])
+    assert [(r.iterations, r.fine_smoother_iterations) for r in ra] == [(r.iterations, r.fine_smoother_iterations) for r in rb]
+    np.testing.assert_allclose(oa, ob, rtol=0, atol=1e-12)
+    a.close(); b.close()
+
+
 def test_u8_ingest_egress():
     """fileio.image_from_fields (fileio.py:58-65): round half to even, clip to [0,255]."""
     m, k = oracle.seeded_problem(200, 120, 0.05, 1, channels=3)
