@@ -59,8 +59,9 @@ typedef struct b200p_config {
     double alpha;                 /* SolverConfig.alpha (Robin weight) */
     double eta;                   /* SolverConfig.local_tol_fraction */
     int local_max_iters;          /* SolverConfig.local_max_iters, 0 = None -> 4*bh*bw */
-    int use_graphs;               /* 1: replay cascade / V-cycle as CUDA graphs */
-    int spec_cycles;              /* V-cycles enqueued between host convergence checks (>=1) */
+    int use_graphs;               /* 1: the whole solve is one CUDA graph (WHILE node for the V-cycle loop);
+                                     0: eager launches, the host reads the loop condition after every cycle */
+    int spec_cycles;              /* unused since the single-graph solve (kept for ABI stability) */
     int mode;                     /* MultigridConfig.mode: 0 "full_multigrid" (mg-oras), 1 "multilevel" (ml-oras,
                                      cascade with every level smoothed to tol_rel, multigrid.py:412-418, :449-464),
                                      2 "single": oras_solve on the finest level only (solvers.py:427-485) */
@@ -170,9 +171,10 @@ int b200p_plan_profile_get(b200p_plan *plan, int kind, double *ms, int64_t *laun
 /* solve_image(problem, "mg-oras", cfg) (pipelines.py:96-114) for `frames`
  * frames at once: d_mask (frames,H,W) bytes, d_known (frames,C,H,W) fp64,
  * d_out (frames,C,H,W) fp64, h_reports frames*C entries (host).  Enqueues on
- * `stream` and synchronises it before returning (the V-cycle loop is
- * convergence-controlled).  The caller must have checked the masks are not
- * empty (b200p_solve_host does). */
+ * `stream` and synchronises it before returning.  cfg.mode / cfg.smoother select
+ * the pipeline: mg-oras (default, the tuned hot path), ml-oras, oras, mg-cg,
+ * ml-cg, cg.  The caller must have checked the masks are not empty
+ * (b200p_solve_host does). */
 int b200p_solve(b200p_plan *plan, const uint8_t *d_mask, const double *d_known, double *d_out,
                 b200p_report *h_reports, void *stream);
 
@@ -228,10 +230,11 @@ int b200p_plan_vcycle(b200p_plan *plan, int level, double *d_u, const double *d_
 /* oras_sweeps(op, blocks, b, u, max_sweeps=, stop_norm=, eta=, local_max_iters=)
  * (solvers.py:393-424) on level `level` of the plan (after build_hierarchy for
  * the masks), d_u/d_b (frames*C planes).  Per problem: sweeps done and final
- * residual norm (host arrays, frames*C).  path: 0 plan default (fused sweep
- * where the level is eligible), 1 generic shared-memory kernel + combine,
- * 2 register-tile kernel + combine, 3 fused persistent sweep, 10+t tile
- * variant t (split); an ineligible level gives B200P_ERR_UNSUPPORTED. */
+ * residual norm (host arrays, frames*C).  path: 0 plan default (lean 32x32
+ * kernel + combine where the level is eligible), 1 generic shared-memory
+ * kernel + combine, 2 register-tile kernel + combine, 3 fused persistent sweep
+ * (plans created with B200P_FUSED=1), 10+t tile variant t (DESIGN.md lists
+ * them); an ineligible level gives B200P_ERR_UNSUPPORTED. */
 int b200p_plan_oras_sweeps(b200p_plan *plan, int level, const double *d_b, double *d_u,
                            int max_sweeps, double stop_norm, int path, int *h_sweeps,
                            double *h_rn, void *stream);
