@@ -7,6 +7,10 @@
  * cpu_baseline / --impl reference leg and __graft_entry__.smoke() can check the
  * CUDA path; nothing under paper_2401_06744_b200/ may import, link or call it.
  *
+ * It also restates the paper's comparison pipelines that run on the same driver: the
+ * cascadic multilevel mode (ml-*), the CG smoother (_cg_run: mg-cg, ml-cg) and cg_solve;
+ * oracle/__init__.py builds oras_solve from orc_oras_sweeps.
+ *
  * Every function cites the reference file:line it restates (paths relative to
  * /root/reference/pkg/src/diffpaint/).  The reference is pure Python/NumPy, so
  * there is nothing to compile into oracle/_ref; instead this file is PINNED
