@@ -78,7 +78,9 @@ typedef struct {
 
 /* counters for the work model in DESIGN.md (block-CG iterations etc.) */
 static long long g_cg_iters = 0, g_block_solves = 0, g_sweeps = 0;
-void orc_counters_reset(void) { g_cg_iters = g_block_solves = g_sweeps = 0; }
+static long long g_iter_hist[32];  /* blocks by local CG step count (work model of DESIGN.md) */
+void orc_iter_hist_get(long long *out) { memcpy(out, g_iter_hist, sizeof g_iter_hist); }
+void orc_counters_reset(void) { g_cg_iters = g_block_solves = g_sweeps = 0; memset(g_iter_hist, 0, sizeof g_iter_hist); }
 void orc_counters_get(long long *out) { out[0] = g_cg_iters; out[1] = g_block_solves; out[2] = g_sweeps; }
 
 static int orc_nthreads(int req) {
@@ -285,7 +287,10 @@ static void blocks_solve_all(const orc_blocks *B, const double *r, double target
                     rhs[j * B->bw + i] = r[g];
                     lm[j * B->bw + i] = B->mask[g];
                 }
-            iters += block_solve(B, ix, iy, rhs, lm, target_sq, max_iters, v_out + (size_t)b * n, work);
+            const int it = block_solve(B, ix, iy, rhs, lm, target_sq, max_iters, v_out + (size_t)b * n, work);
+            iters += it;
+#pragma omp atomic
+            g_iter_hist[it < 31 ? it : 31] += 1;
         }
         free(work);
         free(lm);
