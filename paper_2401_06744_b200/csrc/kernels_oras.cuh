@@ -692,7 +692,7 @@ oras_sweep_lean_kernel(const SweepArgs A, const unsigned *__restrict__ mtab, con
         for (int j = 0; j < TH; ++j)
 #pragma unroll
             for (int i = 0; i < TW; ++i) pc[j][i] = r[j][i];
-        double inv_rs = 1.0 / rs_k;
+        double inv_rs = __drcp_rn(rs_k);  // reciprocal: division's slow path is off the chain
         for (int it = 0; it < A.max_iters; ++it) {
             cg.apply(pc, q);
             double d_pq = tile_dot<TW, TH>(pc, q);
@@ -701,7 +701,7 @@ oras_sweep_lean_kernel(const SweepArgs A, const unsigned *__restrict__ mtab, con
             cg.group_sum3(d_pq, d_rq, d_qq);
             const double pq = hinv2 * d_pq;
             const bool ok = pq > 0.0;                 // solvers.py:348
-            const double a = ok ? rs_k / pq : 0.0;    // :349-350
+            const double a = ok ? rs_k * __drcp_rn(pq) : 0.0;    // :349-350 (reciprocal + multiply)
             const double ah = a * hinv2;
             const double rs_new = fma(ah * ah, d_qq, fma(-2.0 * ah, d_rq, rs_k));
 #pragma unroll
@@ -714,7 +714,7 @@ oras_sweep_lean_kernel(const SweepArgs A, const unsigned *__restrict__ mtab, con
             if (rs_new <= target || !ok) break;       // :354
             const double beta = rs_new * inv_rs;
             rs_k = rs_new;
-            inv_rs = 1.0 / rs_k;
+            inv_rs = __drcp_rn(rs_k);
 #pragma unroll
             for (int j = 0; j < TH; ++j)
 #pragma unroll
