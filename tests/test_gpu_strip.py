@@ -43,6 +43,7 @@ def _run_virtual(nranks, w, h, c, cfg, mask, known):
     (640, 400, 0.02, 3, 3),
     (512, 700, 0.05, 5, 4),      # clamped last block row, uneven strips
     (1920, 1080, 0.04, 0, 4),
+    (3840, 2160, 0.02, 0, 8),    # the 8-GPU layout of BASELINE config 4 at 4K
 ])
 def test_strip_solve_matches_single_plan(w, h, dens, seed, nranks):
     c = 2
