@@ -177,7 +177,7 @@ def run_strip(args, rank, world, local):
         transport = strip.TorchDistTransport()
     else:
         transport = strip.LocalGroup(1).transport(0)
-    solver = strip.StripSolver(W, H, C, cfg, transport)
+    solver = strip.StripSolver(W, H, C, cfg, transport, levels=args.strip_levels)
     d_mask = torch.from_numpy(mask.view(np.uint8)[None]).cuda()
     d_known = torch.from_numpy(known[None]).cuda()
     d_out = torch.zeros_like(d_known)
@@ -212,7 +212,7 @@ def run_strip(args, rank, world, local):
                        "block_size": bs, "overlap": ov, "tol_rel": 1e-3, "frames": 1,
                        "v_cycles": [r.iterations for r in reports],
                        "parallelism": f"1 frame in {world} horizontal strip(s); rank 0 owns rows [{lo}, {hi}); "
-                                      "halo exchange per sweep, coarse levels replicated"}}), flush=True)
+                                      f"halo exchange per sweep, {args.strip_levels} striped level(s), coarser levels replicated"}}), flush=True)
     solver.close()
     if dist.is_initialized():
         dist.destroy_process_group()
@@ -233,6 +233,8 @@ def main():
     ap.add_argument("--strip", action="store_true",
                     help="single-frame strip mode: ONE frame cut into horizontal strips over the ranks "
                          "(halo exchange per sweep over NCCL); default workload 8k_rgb_2pct_b32o6")
+    ap.add_argument("--strip-levels", type=int, default=2,
+                    help="how many of the finest levels are striped in --strip mode (the rest is replicated)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     # the CPU arm costs seconds per step: bound the run to a few minutes

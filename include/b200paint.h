@@ -92,20 +92,24 @@ typedef struct b200p_level_info {
 typedef struct b200p_plan b200p_plan;
 
 /* ---- strip mode (single frame over several GPUs; BASELINE config 4b) ----
- * The finest level is cut into horizontal strips, one per rank; all coarser levels are replicated.
- * A rank owns the pixel rows [own_lo, own_hi) (multiples of the block stride), solves the block rows
- * that cover them, and keeps a one-block-deep halo [ext_lo, ext_hi) of the iterate valid.  The
- * library calls `exchange` where data has to move between ranks; the callback works on `stream`
+ * The finest `levels` levels are cut into horizontal strips, one per rank; the coarser levels are
+ * replicated.  On a striped level a rank owns the pixel rows [own_lo, own_hi), solves the block
+ * rows that cover them (boundary block rows redundantly on both sides), and keeps the halo
+ * [ext_lo, ext_hi) of the level's iterate valid.  The library calls `exchange` where data has to
+ * move between ranks; kind = base + 16 * (level of the field).  The callback works on `stream`
  * (asynchronously or not) and returns 0 on success:
  *   B200P_XCHG_SUM_RS     d_ptr = (P) doubles: sum over ranks (partial ||r||^2 of the strips)
  *   B200P_XCHG_MAX_FLAGS  d_ptr = (P) ints:    max over ranks
- *   B200P_XCHG_HALO_U     d_ptr = level-0 iterate (P,H,W): rows [own_lo, own_hi) are new on every
- *                         rank; fill [ext_lo, own_lo) and [own_hi, ext_hi) from the owners
- *   B200P_XCHG_GATHER_RC  d_ptr = level-1 field (P,H1,W1): rows [own_lo/2, own_hi/2) are new on every
- *                         rank; make the whole field identical everywhere (all-gather)
+ *   B200P_XCHG_HALO_U     d_ptr = iterate of the level (P,h,w): rows [own_lo, own_hi) are new on
+ *                         every rank; fill [ext_lo, own_lo) and [own_hi, ext_hi) from their owners
+ *   B200P_XCHG_HALO_RC    the same for the restricted residual of a striped level >= 1
+ *   B200P_XCHG_GATHER_RC  d_ptr = restricted residual of the first REPLICATED level (P,h,w): every
+ *                         rank wrote the rows [own_lo/2, own_hi/2) of the level above; make the
+ *                         whole field identical everywhere (all-gather)
  * Inputs (mask, known) are given in full on every rank; the output holds the rank's rows (plus halo).
  * Strip plans run eagerly (use_graphs = 0).  Needs 32x32 blocks, width % 4 == 0, even block stride. */
-enum { B200P_XCHG_SUM_RS = 1, B200P_XCHG_MAX_FLAGS = 2, B200P_XCHG_HALO_U = 3, B200P_XCHG_GATHER_RC = 4 };
+enum { B200P_XCHG_SUM_RS = 1, B200P_XCHG_MAX_FLAGS = 2, B200P_XCHG_HALO_U = 3, B200P_XCHG_GATHER_RC = 4,
+       B200P_XCHG_HALO_RC = 5 };
 typedef int (*b200p_exchange_fn)(void *user, int kind, void *d_ptr, void *stream);
 
 const char *b200p_last_error(void);
@@ -142,14 +146,16 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out);
 void b200p_plan_destroy(b200p_plan *plan);
 int b200p_plan_num_levels(const b200p_plan *plan);
 int b200p_plan_level_info(const b200p_plan *plan, int level, b200p_level_info *out);
-/* Strip geometry of rank `rank` of `nranks` for this plan's finest level: block rows are dealt out
- * evenly; out = {own_lo, own_hi, ext_lo, ext_hi, iy_lo, iy_hi}.  Host-only. */
-int b200p_plan_strip_ranges(const b200p_plan *plan, int rank, int nranks, int out[6]);
+/* Strip geometry of rank `rank` of `nranks` on the `levels` finest levels of this plan: the rows are
+ * dealt out evenly (cuts at multiples of 2^levels); out[6 * l + ...] = {own_lo, own_hi, ext_lo, ext_hi,
+ * iy_lo, iy_hi} of level l.  Host-only. */
+int b200p_plan_strip_ranges(const b200p_plan *plan, int levels, int rank, int nranks, int *out);
 /* The same from the geometry alone (image height, block_size, overlap). */
-int b200p_strip_ranges(int height, int block, int overlap, int rank, int nranks, int out[6]);
-/* Puts the plan into strip mode with the given ranges (from b200p_plan_strip_ranges) and callback;
- * rank / nranks themselves are the callback's business.  own range (0, H) + NULL callback leaves it. */
-int b200p_plan_set_strip(b200p_plan *plan, const int ranges[6], b200p_exchange_fn exchange, void *user);
+int b200p_strip_ranges(int height, int block, int overlap, int levels, int rank, int nranks, int *out);
+/* Puts the plan into strip mode on its `levels` finest levels with the given ranges (from
+ * b200p_plan_strip_ranges) and callback; rank / nranks themselves are the callback's business.
+ * levels = 0 (and a NULL callback) leaves strip mode. */
+int b200p_plan_set_strip(b200p_plan *plan, int levels, const int *ranges, b200p_exchange_fn exchange, void *user);
 /* Device pointer of the level's restricted-residual field (P,h,w) (level >= 1), for the callback. */
 int b200p_plan_level_rc(const b200p_plan *plan, int level, double **d_rc);
 /* Bytes of device memory the plan holds. */

@@ -97,9 +97,9 @@ SIGNATURES = {
     "b200p_plan_destroy": (None, [_VP]),
     "b200p_plan_num_levels": (_I, [_VP]),
     "b200p_plan_level_info": (_I, [_VP, _I, C.POINTER(LevelInfo)]),
-    "b200p_plan_strip_ranges": (_I, [_VP, _I, _I, C.POINTER(_I * 6)]),
-    "b200p_strip_ranges": (_I, [_I, _I, _I, _I, _I, C.POINTER(_I * 6)]),
-    "b200p_plan_set_strip": (_I, [_VP, C.POINTER(_I * 6), _VP, _VP]),
+    "b200p_plan_strip_ranges": (_I, [_VP, _I, _I, _I, _VP]),
+    "b200p_strip_ranges": (_I, [_I, _I, _I, _I, _I, _I, _VP]),
+    "b200p_plan_set_strip": (_I, [_VP, _I, _VP, _VP, _VP]),
     "b200p_plan_level_rc": (_I, [_VP, _I, C.POINTER(_VP)]),
     "b200p_plan_device_bytes": (_I64, [_VP]),
     "b200p_plan_launch_count": (_I64, [_VP]),

@@ -169,6 +169,7 @@ struct LevelHost {
     unsigned *d_cell_cnt = nullptr;
     // strip mode (level 0 only): rows this rank owns / keeps valid, block rows it solves (default: all)
     int own_lo = 0, own_hi = 0, ext_lo = 0, ext_hi = 0, iy_lo = 0, iy_hi = 0;
+    bool is_strip = false;
     // fused sweep (K2F): ping-pong partner of the iterate, L2-resident ring, schedule tables
     bool fused = false;
     int fused_tile = 0;
@@ -471,10 +472,13 @@ static double field_bytes(const b200p_plan *pl, const LevelHost &L, double field
 static int rows_chunk(int h) { return h >= 1024 ? 32 : (h >= 256 ? 16 : 8); }
 
 // Strip mode: level 0 is cut into horizontal strips over ranks, coarser levels are replicated.
-static bool striped(const b200p_plan *pl, const LevelHost &L) { return pl->strip && &L == &pl->lev[0]; }
+static bool striped(const b200p_plan *pl, const LevelHost &L) { return pl->strip && L.is_strip; }
+static int level_of(const b200p_plan *pl, const LevelHost &L) { return (int)(&L - &pl->lev[0]); }
 
-static int strip_exchange(b200p_plan *pl, int kind, void *d_ptr, cudaStream_t st) {
+// kind = base + 16 * level of the field (include/b200paint.h)
+static int strip_exchange(b200p_plan *pl, int kind, void *d_ptr, cudaStream_t st, int level = 0) {
     if (!pl->exchange) return fail_arg(B200P_ERR_STATE, "strip mode needs an exchange callback");
+    kind += 16 * level;
     const int rc = pl->exchange(pl->exchange_user, kind, d_ptr, (void *)st);
     if (rc) return fail_arg(B200P_ERR_STATE, "strip exchange %d failed (%d)", kind, rc);
     return 0;
@@ -851,7 +855,7 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, UBuf &ub, cons
         CU(cudaGetLastError());
     }
     // strip mode: the rows the neighbours' block solves and stencils read from this strip
-    if (striped(pl, L)) return strip_exchange(pl, B200P_XCHG_HALO_U, u, st);
+    if (striped(pl, L)) return strip_exchange(pl, B200P_XCHG_HALO_U, u, st, level_of(pl, L));
     return 0;
 }
 
@@ -1071,9 +1075,11 @@ static int enqueue_vcycle(b200p_plan *pl, int level, UBuf &u, const double *b, b
         CU(cudaGetLastError());
     }
     if (striped(pl, L)) {
-        // every rank restricted its own rows: collect the replicated coarse right-hand side, and zero
-        // the whole coarse correction (K3 only zeroed this strip's rows)
-        if ((rc = strip_exchange(pl, B200P_XCHG_GATHER_RC, Cc.d_rc, st))) return rc;
+        // every rank restricted its own rows: the next level either is striped too (it needs the rows
+        // of its boundary blocks from the neighbours) or is replicated (all-gather); and the whole
+        // coarse correction is zeroed (K3 only zeroed this strip's rows)
+        if ((rc = strip_exchange(pl, Cc.is_strip ? B200P_XCHG_HALO_RC : B200P_XCHG_GATHER_RC, Cc.d_rc, st, level + 1)))
+            return rc;
         if (level + 1 != nl - 1)
             CU(cudaMemsetAsync(e.cur, 0, sizeof(double) * (size_t)pl->P * Cc.info.height * Cc.info.width, st));
     }
@@ -1916,67 +1922,97 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
 
 int b200p_plan_num_levels(const b200p_plan *pl) { return pl ? (int)pl->lev.size() : 0; }
 
-int b200p_plan_strip_ranges(const b200p_plan *pl, int rank, int nranks, int out[6]) {
+int b200p_plan_strip_ranges(const b200p_plan *pl, int levels, int rank, int nranks, int *out) {
     if (!pl || !out) return fail_arg(B200P_ERR_ARG, "null argument");
-    return b200p_strip_ranges(pl->cfg.height, pl->cfg.block_size, pl->cfg.overlap, rank, nranks, out);
+    return b200p_strip_ranges(pl->cfg.height, pl->cfg.block_size, pl->cfg.overlap, levels, rank, nranks, out);
 }
 
-int b200p_strip_ranges(int H, int block, int overlap, int rank, int nranks, int out[6]) {
+int b200p_strip_ranges(int H, int block, int overlap, int levels, int rank, int nranks, int *out) {
     if (!out) return fail_arg(B200P_ERR_ARG, "null argument");
     if (H < 1 || block <= overlap || overlap < 0)
         return fail_arg(B200P_ERR_ARG, "need height >= 1 and block_size > overlap >= 0");
-    const std::vector<int> ys = axis_starts(H, block, block - overlap);
-    const int ny = (int)ys.size(), bh = std::min(block, H);
+    if (levels < 1 || levels > 8) return fail_arg(B200P_ERR_ARG, "need 1 <= striped levels <= 8");
     if (nranks < 1 || rank < 0 || rank >= nranks)
         return fail_arg(B200P_ERR_ARG, "bad rank %d of %d", rank, nranks);
-    if (nranks > ny) return fail_arg(B200P_ERR_ARG, "%d ranks for %d block rows", nranks, ny);
-    std::vector<int> cyf, cyn;
-    axis_cover(ys, bh, H, cyf, cyn);
-    // block rows are dealt out evenly; a rank owns the pixel rows from its first block row's start to
-    // the next rank's
-    const int k0 = (int)((long long)rank * ny / nranks), k1 = (int)((long long)(rank + 1) * ny / nranks);
-    const int own_lo = k0 == 0 ? 0 : ys[k0], own_hi = k1 == ny ? H : ys[k1];
-    if (own_hi <= own_lo) return fail_arg(B200P_ERR_ARG, "empty strip for rank %d", rank);
-    if ((own_lo | own_hi) & 1) {
-        if (own_hi != H || (own_lo & 1))
-            return fail_arg(B200P_ERR_UNSUPPORTED, "strip mode needs even block-row starts");
+    // strip boundaries on the finest level: even shares of the rows, rounded down to a multiple of
+    // 2^levels so that they halve exactly on every striped level (2x2 cells never straddle a cut)
+    const int q = 1 << levels;
+    auto cut = [&](int k) { return k <= 0 ? 0 : (k >= nranks ? H : (int)(((long long)H * k / nranks) / q * q)); };
+    const int a0 = cut(rank), b0 = cut(rank + 1);
+    int h = H, need_lo = 0, need_hi = 0;  // rows of this level the finer level's prolongation reads
+    for (int l = 0; l < levels; ++l) {
+        const int own_lo = a0 >> l, own_hi = (rank + 1 == nranks) ? h : (b0 >> l);
+        if (own_hi <= own_lo)
+            return fail_arg(B200P_ERR_ARG, "empty strip on level %d for rank %d of %d (height %d)", l, rank, nranks, H);
+        const std::vector<int> ys = axis_starts(h, block, block - overlap);
+        const int ny = (int)ys.size(), bh = std::min(block, h);
+        std::vector<int> cyf, cyn;
+        axis_cover(ys, bh, h, cyf, cyn);
+        // block rows that cover an owned pixel row are solved here (boundary rows redundantly by both sides)
+        int iy_lo = ny, iy_hi = 0;
+        for (int y = own_lo; y < own_hi; ++y) {
+            iy_lo = std::min(iy_lo, cyf[y]);
+            iy_hi = std::max(iy_hi, cyf[y] + cyn[y]);
+        }
+        // rows those block solves (1-pixel gather halo) and the stencils of the owned rows read, plus
+        // what the finer level's prolongation onto ITS halo reads from this level
+        int ext_lo = std::max(0, ys[iy_lo] - 1), ext_hi = std::min(h, ys[iy_hi - 1] + bh + 1);
+        if (l > 0) {
+            ext_lo = std::min(ext_lo, std::max(0, need_lo));
+            ext_hi = std::max(ext_hi, std::min(h, need_hi));
+        }
+        ext_lo &= ~1;
+        if (ext_hi < h) ext_hi = std::min(h, (ext_hi + 1) & ~1);
+        int *o = out + 6 * l;
+        o[0] = own_lo; o[1] = own_hi; o[2] = ext_lo; o[3] = ext_hi; o[4] = iy_lo; o[5] = iy_hi;
+        need_lo = (ext_lo >> 1) - 1;
+        need_hi = ((ext_hi + 1) >> 1) + 1;
+        h = (h + 1) / 2;
     }
-    // block rows that cover an owned pixel row are solved here (boundary rows redundantly by both sides)
-    int iy_lo = ny, iy_hi = 0;
-    for (int y = own_lo; y < own_hi; ++y) {
-        iy_lo = std::min(iy_lo, cyf[y]);
-        iy_hi = std::max(iy_hi, cyf[y] + cyn[y]);
-    }
-    // rows those block solves (1-pixel gather halo) and the stencils of the owned rows read
-    int ext_lo = std::max(0, ys[iy_lo] - 1), ext_hi = std::min(H, ys[iy_hi - 1] + bh + 1);
-    ext_lo &= ~1;
-    if (ext_hi < H) ext_hi = std::min(H, (ext_hi + 1) & ~1);
-    out[0] = own_lo; out[1] = own_hi; out[2] = ext_lo; out[3] = ext_hi; out[4] = iy_lo; out[5] = iy_hi;
     return 0;
 }
 
-int b200p_plan_set_strip(b200p_plan *pl, const int r[6], b200p_exchange_fn exchange, void *user) {
-    if (!pl || !r) return fail_arg(B200P_ERR_ARG, "null argument");
-    LevelHost &L = pl->lev[0];
-    const int H = L.info.height;
+int b200p_plan_set_strip(b200p_plan *pl, int levels, const int *r, b200p_exchange_fn exchange, void *user) {
+    if (!pl) return fail_arg(B200P_ERR_ARG, "null argument");
     if (pl->pending) return fail_arg(B200P_ERR_STATE, "a solve is pending on this plan");
-    if (!exchange && r[0] == 0 && r[1] == H) {  // back to the whole image
+    if (levels == 0 || !exchange) {  // back to the whole image
+        if (levels != 0) return fail_arg(B200P_ERR_ARG, "strip mode needs an exchange callback");
         pl->strip = false;
         pl->exchange = nullptr;
-        L.own_lo = L.ext_lo = 0; L.own_hi = L.ext_hi = H; L.iy_lo = 0; L.iy_hi = L.info.ny;
+        for (LevelHost &L : pl->lev) {
+            L.is_strip = false;
+            L.own_lo = L.ext_lo = 0; L.own_hi = L.ext_hi = L.info.height; L.iy_lo = 0; L.iy_hi = L.info.ny;
+        }
         return 0;
     }
-    if (!exchange) return fail_arg(B200P_ERR_ARG, "strip mode needs an exchange callback");
+    if (!r) return fail_arg(B200P_ERR_ARG, "null argument");
     if (pl->cfg.use_graphs) return fail_arg(B200P_ERR_STATE, "strip plans run eagerly: create the plan with use_graphs = 0");
     if (pl->cfg.mode != 0 || pl->cfg.smoother != 0)
         return fail_arg(B200P_ERR_UNSUPPORTED, "strip mode covers the mg-oras path only");
-    if (pl->lev.size() < 2) return fail_arg(B200P_ERR_UNSUPPORTED, "strip mode needs at least two levels");
-    if (!L.d_mtab || L.info.width % 4 != 0)
-        return fail_arg(B200P_ERR_UNSUPPORTED, "strip mode needs 32x32 blocks with even starts and width % 4 == 0");
-    if (!(0 <= r[2] && r[2] <= r[0] && r[0] < r[1] && r[1] <= r[3] && r[3] <= H && 0 <= r[4] && r[4] < r[5] &&
-          r[5] <= L.info.ny) || (r[0] & 1) || (r[2] & 1) || ((r[1] & 1) && r[1] != H) || ((r[3] & 1) && r[3] != H))
-        return fail_arg(B200P_ERR_ARG, "inconsistent strip ranges");
-    L.own_lo = r[0]; L.own_hi = r[1]; L.ext_lo = r[2]; L.ext_hi = r[3]; L.iy_lo = r[4]; L.iy_hi = r[5];
+    if (levels < 1 || levels + 1 > (int)pl->lev.size())
+        return fail_arg(B200P_ERR_UNSUPPORTED, "need 1 <= striped levels < %d (the coarsest level stays replicated)",
+                        (int)pl->lev.size());
+    for (int l = 0; l < levels; ++l) {
+        const LevelHost &L = pl->lev[l];
+        const int H = L.info.height;
+        const int *q = r + 6 * l;
+        if (!L.d_mtab || L.info.width % 4 != 0 || L.nblocks < 2)
+            return fail_arg(B200P_ERR_UNSUPPORTED,
+                            "strip mode needs 32x32 blocks with even starts and width %% 4 == 0 (level %d)", l);
+        if (!(0 <= q[2] && q[2] <= q[0] && q[0] < q[1] && q[1] <= q[3] && q[3] <= H && 0 <= q[4] && q[4] < q[5] &&
+              q[5] <= L.info.ny) || (q[0] & 1) || (q[2] & 1) || ((q[1] & 1) && q[1] != H) || ((q[3] & 1) && q[3] != H))
+            return fail_arg(B200P_ERR_ARG, "inconsistent strip ranges on level %d", l);
+    }
+    for (int l = 0; l < (int)pl->lev.size(); ++l) {
+        LevelHost &L = pl->lev[l];
+        L.is_strip = l < levels;
+        if (L.is_strip) {
+            const int *q = r + 6 * l;
+            L.own_lo = q[0]; L.own_hi = q[1]; L.ext_lo = q[2]; L.ext_hi = q[3]; L.iy_lo = q[4]; L.iy_hi = q[5];
+        } else {
+            L.own_lo = L.ext_lo = 0; L.own_hi = L.ext_hi = L.info.height; L.iy_lo = 0; L.iy_hi = L.info.ny;
+        }
+    }
     pl->strip = true;
     pl->exchange = exchange;
     pl->exchange_user = user;

@@ -31,7 +31,7 @@ import torch
 from . import _dev, _lib
 from .multigrid import MultigridConfig, Plan
 
-XCHG_SUM_RS, XCHG_MAX_FLAGS, XCHG_HALO_U, XCHG_GATHER_RC = 1, 2, 3, 4
+XCHG_SUM_RS, XCHG_MAX_FLAGS, XCHG_HALO_U, XCHG_GATHER_RC, XCHG_HALO_RC = 1, 2, 3, 4, 5
 _EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p)
 
 
@@ -68,14 +68,17 @@ def halo_plan(ranges, rank):
     return recv, send
 
 
-def strip_ranges(height, block_size, overlap, nranks):
-    """[(own_lo, own_hi, ext_lo, ext_hi, iy_lo, iy_hi)] of all ranks (host-only geometry)."""
-    out = []
+def strip_ranges(height, block_size, overlap, nranks, levels=1):
+    """ranges[l][q] = (own_lo, own_hi, ext_lo, ext_hi, iy_lo, iy_hi) of rank q on striped level l
+    (host-only geometry).  With levels == 1 the list of level 0 is returned directly."""
+    per_rank = []
     for q in range(nranks):
-        r = (C.c_int * 6)()
-        _lib.check(_lib.lib().b200p_strip_ranges(int(height), int(block_size), int(overlap), q, nranks, C.byref(r)))
-        out.append(tuple(r))
-    return out
+        r = (C.c_int * (6 * levels))()
+        _lib.check(_lib.lib().b200p_strip_ranges(int(height), int(block_size), int(overlap), int(levels), q,
+                                                 nranks, C.cast(r, C.c_void_p)))
+        per_rank.append([tuple(r[6 * l:6 * l + 6]) for l in range(levels)])
+    by_level = [[per_rank[q][l] for q in range(nranks)] for l in range(levels)]
+    return by_level[0] if levels == 1 else by_level
 
 
 def coarse_rows(ranges, h1):
@@ -192,20 +195,31 @@ class StripSolver:
     solution (device tensor (C, own_hi - own_lo, W)), and the reports, identical on all ranks."""
 
     def __init__(self, width, height, channels, cfg: MultigridConfig | None, transport: Transport,
-                 spacing: float = 1.0):
+                 spacing: float = 1.0, levels: int = 1):
+        """levels: how many of the finest levels are striped (the rest is replicated); 1 keeps 25 % of the
+        work replicated, 2 about 6 %."""
         self.t = transport
         self.cfg = cfg or MultigridConfig()
         self.plan = Plan(width, height, channels, 1, self.cfg, spacing, use_graphs=False)
-        self.shape = (int(channels), int(height), int(width))
-        L = _lib.lib()
-        self.ranges = strip_ranges(height, self.cfg.block_size, self.cfg.overlap, transport.nranks)
-        info1 = self.plan.level_info(1)
-        self.shape1 = (int(channels), info1.height, info1.width)
-        self.rows1 = coarse_rows(self.ranges, info1.height)
+        self.levels = int(levels)
+        if not 1 <= self.levels < self.plan.num_levels:
+            raise ValueError(f"need 1 <= striped levels < {self.plan.num_levels}")
+        self.shapes = []
+        for l in range(self.levels + 1):
+            info = self.plan.level_info(l)
+            self.shapes.append((int(channels), info.height, info.width))
+        self.shape = self.shapes[0]
+        rg = strip_ranges(height, self.cfg.block_size, self.cfg.overlap, transport.nranks, self.levels)
+        self.ranges_by_level = [rg] if self.levels == 1 else rg
+        self.ranges = self.ranges_by_level[0]
+        # rows of the first replicated level that every rank restricted from the last striped level
+        self.gather_rows = coarse_rows(self.ranges_by_level[-1], self.shapes[self.levels][1])
         self.error = None
         self._cb = _EXCHANGE_FN(self._exchange)  # keep the callback object alive
-        mine = (C.c_int * 6)(*self.ranges[transport.rank])
-        _lib.check(L.b200p_plan_set_strip(self.plan.handle, C.byref(mine), C.cast(self._cb, C.c_void_p), None))
+        flat = [v for l in range(self.levels) for v in self.ranges_by_level[l][transport.rank]]
+        mine = (C.c_int * len(flat))(*flat)
+        _lib.check(_lib.lib().b200p_plan_set_strip(self.plan.handle, self.levels, C.cast(mine, C.c_void_p),
+                                                   C.cast(self._cb, C.c_void_p), None))
 
     @property
     def own(self):
@@ -215,16 +229,17 @@ class StripSolver:
     def _exchange(self, user, kind, d_ptr, stream):
         try:
             P = self.shape[0]
+            base, lvl = kind & 15, kind >> 4
             ext = torch.cuda.ExternalStream(int(stream or 0)) if stream else torch.cuda.default_stream()
             with torch.cuda.stream(ext):
-                if kind == XCHG_SUM_RS:
+                if base == XCHG_SUM_RS:
                     self.t.sum_(device_view(d_ptr, (P,), torch.float64))
-                elif kind == XCHG_MAX_FLAGS:
+                elif base == XCHG_MAX_FLAGS:
                     self.t.max_(device_view(d_ptr, (P,), torch.int32))
-                elif kind == XCHG_HALO_U:
-                    self.t.halo(device_view(d_ptr, self.shape, torch.float64), self.ranges)
-                elif kind == XCHG_GATHER_RC:
-                    self.t.gather_rows(device_view(d_ptr, self.shape1, torch.float64), self.rows1)
+                elif base in (XCHG_HALO_U, XCHG_HALO_RC):
+                    self.t.halo(device_view(d_ptr, self.shapes[lvl], torch.float64), self.ranges_by_level[lvl])
+                elif base == XCHG_GATHER_RC:
+                    self.t.gather_rows(device_view(d_ptr, self.shapes[lvl], torch.float64), self.gather_rows)
                 else:
                     return 1
             return 0

@@ -14,13 +14,13 @@ from paper_2401_06744_b200 import strip
 pytestmark = pytest.mark.gpu
 
 
-def _run_virtual(nranks, w, h, c, cfg, mask, known):
+def _run_virtual(nranks, w, h, c, cfg, mask, known, levels=1):
     group = strip.LocalGroup(nranks)
     out, errs = [None] * nranks, []
 
     def work(r):
         try:
-            s = strip.StripSolver(w, h, c, cfg, group.transport(r))
+            s = strip.StripSolver(w, h, c, cfg, group.transport(r), levels=levels)
             u, reps = s.solve(mask, known)
             out[r] = (s.own, u.cpu().numpy(), reps)
             s.close()
@@ -38,19 +38,23 @@ def _run_virtual(nranks, w, h, c, cfg, mask, known):
     return out
 
 
-@pytest.mark.parametrize("w,h,dens,seed,nranks", [
-    (640, 400, 0.02, 3, 2),
-    (640, 400, 0.02, 3, 3),
-    (512, 700, 0.05, 5, 4),      # clamped last block row, uneven strips
-    (1920, 1080, 0.04, 0, 4),
-    (3840, 2160, 0.02, 0, 8),    # the 8-GPU layout of BASELINE config 4 at 4K
+@pytest.mark.parametrize("w,h,dens,seed,nranks,levels", [
+    (640, 400, 0.02, 3, 2, 1),
+    (640, 400, 0.02, 3, 3, 1),
+    (512, 700, 0.05, 5, 4, 1),      # clamped last block row, uneven strips
+    (1920, 1080, 0.04, 0, 4, 1),
+    (3840, 2160, 0.02, 0, 8, 1),    # the 8-GPU layout of BASELINE config 4 at 4K
+    (640, 400, 0.02, 3, 2, 2),      # two striped levels: halo exchange of the restricted residual too
+    (1920, 1080, 0.04, 0, 4, 2),
+    (3840, 2160, 0.02, 0, 8, 2),
+    (3840, 2160, 0.02, 0, 4, 3),
 ])
-def test_strip_solve_matches_single_plan(w, h, dens, seed, nranks):
+def test_strip_solve_matches_single_plan(w, h, dens, seed, nranks, levels):
     c = 2
     m, k = oracle.seeded_problem(w, h, dens, seed, channels=c)
     cfg = bp.MultigridConfig(block_size=32, overlap=6)
     ref = bp.solve_image(bp.InpaintingProblem(m, k), "mg-oras", cfg)
-    parts = _run_virtual(nranks, w, h, c, cfg, m, k)
+    parts = _run_virtual(nranks, w, h, c, cfg, m, k, levels)
     full = np.empty_like(ref.fields)
     covered = 0
     for (lo, hi), u, reps in parts:
@@ -66,24 +70,15 @@ def test_strip_solve_matches_single_plan(w, h, dens, seed, nranks):
 
 
 def test_strip_geometry_and_halo_plan():
-    plan = bp.Plan(3840, 2160, 3, 1, bp.MultigridConfig(), use_graphs=False)
-    import ctypes as C
-    from paper_2401_06744_b200 import _lib
     n = 8
-    ranges = []
-    for q in range(n):
-        r = (C.c_int * 6)()
-        _lib.check(_lib.lib().b200p_plan_strip_ranges(plan.handle, q, n, C.byref(r)))
-        ranges.append(tuple(r))
-    plan.close()
+    ranges = strip.strip_ranges(2160, 32, 6, n)
     assert ranges[0][0] == 0 and ranges[-1][1] == 2160
     for a, b in zip(ranges, ranges[1:]):
         assert a[1] == b[0]                      # strips tile the image
-        assert b[4] == a[5] - 1                  # the boundary block row is solved on both sides
-    for r in ranges:
-        own_lo, own_hi, ext_lo, ext_hi, iy_lo, iy_hi = r
-        assert own_lo % 26 == 0 and ext_lo % 2 == 0 and ext_lo <= max(0, own_lo - 1) and ext_hi >= min(2160, own_hi + 1)
-        assert ext_hi - own_hi <= 34 and own_lo - ext_lo <= 28   # one-block-deep halos
+        assert b[4] <= a[5] - 1                  # the boundary block row is solved on both sides
+    for own_lo, own_hi, ext_lo, ext_hi, iy_lo, iy_hi in ranges:
+        assert own_lo % 2 == 0 and ext_lo % 2 == 0 and ext_lo <= max(0, own_lo - 1) and ext_hi >= min(2160, own_hi + 1)
+        assert ext_hi - own_hi <= 34 + 26 and own_lo - ext_lo <= 28 + 26   # one-block-deep halos
     # what rank 3 receives is exactly what its neighbours send to it
     recv, _ = strip.halo_plan(ranges, 3)
     sends = []
@@ -93,3 +88,9 @@ def test_strip_geometry_and_halo_plan():
     assert sorted(recv) == sorted(sends)
     rows = strip.coarse_rows(ranges, 1080)
     assert rows[0][0] == 0 and rows[-1][1] == 1080 and all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
+    # two striped levels: the cuts halve exactly, the level-1 halo covers what level 0's prolongation reads
+    r2 = strip.strip_ranges(2160, 32, 6, n, levels=2)
+    for q in range(n):
+        l0, l1 = r2[0][q], r2[1][q]
+        assert l1[0] == l0[0] // 2 and (l1[1] == l0[1] // 2 or q == n - 1)
+        assert l1[2] <= max(0, l0[2] // 2 - 1) and l1[3] >= min(1080, (l0[3] + 1) // 2 + 1)

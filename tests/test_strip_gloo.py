@@ -70,12 +70,15 @@ def test_strip_ranges_cover_and_overlap():
         rg = strip.strip_ranges(h, BLOCK, OVERLAP, n)
         assert rg[0][0] == 0 and rg[-1][1] == h
         for a, b in zip(rg, rg[1:]):
-            assert a[1] == b[0] and b[4] <= a[5] - 1      # strips tile the image; boundary block rows shared
+            assert a[1] == b[0] and b[4] <= a[5]          # strips tile the image; boundary block rows shared
         for own_lo, own_hi, ext_lo, ext_hi, iy_lo, iy_hi in rg:
             assert ext_lo <= own_lo < own_hi <= ext_hi and iy_lo < iy_hi
             assert own_lo % 2 == 0 and ext_lo % 2 == 0
     with pytest.raises(ValueError):
-        strip.strip_ranges(64, BLOCK, OVERLAP, 5)             # more ranks than block rows
+        strip.strip_ranges(8, BLOCK, OVERLAP, 5)              # more ranks than row pairs: an empty strip
+    two = strip.strip_ranges(2160, BLOCK, OVERLAP, 8, levels=2)
+    assert len(two) == 2 and all(len(lv) == 8 for lv in two)
+    assert all(two[1][q][0] == two[0][q][0] // 2 for q in range(8))
 
 
 def test_local_transport_threads():
