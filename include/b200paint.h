@@ -281,6 +281,12 @@ int b200p_prolongate_solution(const double *d_coarse_u, const uint8_t *d_fine_ma
 /* ---- small device-memory helpers for host languages without a CUDA binding */
 int b200p_malloc(void **d_ptr, int64_t bytes);
 int b200p_free(void *d_ptr);
+/* CUDA IPC for the strip mode's peer-memory transport: export a cudaMalloc'ed buffer (its BASE pointer),
+ * map a peer's buffer into this process (reads and writes then go over NVLink / peer memory), unmap it. */
+int b200p_ipc_export(const void *d_ptr, unsigned char handle[64]);
+int b200p_ipc_open(const unsigned char handle[64], void **d_ptr);
+int b200p_ipc_close(void *d_ptr);
+int b200p_memcpy_d2d_async(void *d_dst, const void *d_src, int64_t bytes, void *stream);
 int b200p_memcpy_h2d(void *d_dst, const void *h_src, int64_t bytes);
 int b200p_memcpy_d2h(void *h_dst, const void *d_src, int64_t bytes);
 int b200p_memset(void *d_ptr, int value, int64_t bytes);

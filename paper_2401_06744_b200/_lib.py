@@ -131,6 +131,10 @@ SIGNATURES = {
     "b200p_prolongate_solution": (_I, [_VP, _VP, _VP, _I, _I, _VP, _VP]),
     "b200p_malloc": (_I, [C.POINTER(_VP), _I64]),
     "b200p_free": (_I, [_VP]),
+    "b200p_ipc_export": (_I, [_VP, _VP]),
+    "b200p_ipc_open": (_I, [_VP, C.POINTER(_VP)]),
+    "b200p_ipc_close": (_I, [_VP]),
+    "b200p_memcpy_d2d_async": (_I, [_VP, _VP, _I64, _VP]),
     "b200p_memcpy_h2d": (_I, [_VP, _VP, _I64]),
     "b200p_memcpy_d2h": (_I, [_VP, _VP, _I64]),
     "b200p_memset": (_I, [_VP, _I, _I64]),

@@ -2608,6 +2608,33 @@ int b200p_free(void *d_ptr) {
     CU(cudaFree(d_ptr));
     return 0;
 }
+
+// ---- CUDA IPC: another process (one process per GPU, or several on one GPU) maps this buffer and
+// reads / writes it through NVLink / peer memory.  d_ptr must be the base of a cudaMalloc allocation
+// (b200p_malloc, or the plan-owned fields).
+int b200p_ipc_export(const void *d_ptr, unsigned char handle[64]) {
+    if (!d_ptr || !handle) return fail_arg(B200P_ERR_ARG, "null argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    cudaIpcMemHandle_t h;
+    CU(cudaIpcGetMemHandle(&h, const_cast<void *>(d_ptr)));
+    memcpy(handle, &h, 64);
+    return 0;
+}
+int b200p_ipc_open(const unsigned char handle[64], void **d_ptr) {
+    if (!d_ptr || !handle) return fail_arg(B200P_ERR_ARG, "null argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, 64);
+    CU(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return 0;
+}
+int b200p_ipc_close(void *d_ptr) {
+    CU(cudaIpcCloseMemHandle(d_ptr));
+    return 0;
+}
+int b200p_memcpy_d2d_async(void *d_dst, const void *d_src, int64_t bytes, void *stream) {
+    CU(cudaMemcpyAsync(d_dst, d_src, (size_t)bytes, cudaMemcpyDefault, (cudaStream_t)stream));
+    return 0;
+}
 int b200p_memcpy_h2d(void *d_dst, const void *h_src, int64_t bytes) {
     CU(cudaMemcpy(d_dst, h_src, (size_t)bytes, cudaMemcpyHostToDevice));
     return 0;

@@ -93,6 +93,10 @@ class Transport:
     rank = 0
     nranks = 1
 
+    def zeros_f64(self, shape):
+        """Device buffer for the solution (a transport may need a particular allocation)."""
+        return torch.zeros(tuple(shape), dtype=torch.float64, device=_dev.device())
+
     def sum_(self, t): raise NotImplementedError
     def max_(self, t): raise NotImplementedError
     def halo(self, u, ranges): raise NotImplementedError
@@ -134,6 +138,85 @@ class TorchDistTransport(Transport):
             self.dist.broadcast(chunk, src=q, group=self.group)
             if q != self.rank:
                 field[:, a:b].copy_(chunk)
+
+
+class IpcTransport(Transport):
+    """Peer-memory transport for one process per GPU (or several processes on one GPU): every rank
+    maps its peers' buffers with CUDA IPC and PULLS the halo rows / gathered rows it needs with
+    device-to-device copies over NVLink; no NCCL.  Control (handle exchange, barriers, the P-element
+    reductions) goes through a host process group (gloo).  Buffers must be cudaMalloc bases:
+    `zeros_f64` for the solution, the plan-owned level fields otherwise."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank, self.nranks = dist.get_rank(group), dist.get_world_size(group)
+        self._peers = {}     # local base pointer -> [peer tensor views]
+        self._owned = []
+
+    def zeros_f64(self, shape):
+        n = int(np.prod(shape)) * 8
+        p = C.c_void_p()
+        _lib.check(_lib.lib().b200p_malloc(C.byref(p), n))
+        _lib.check(_lib.lib().b200p_memset(p, 0, n))
+        self._owned.append(p)
+        return device_view(p.value, shape, torch.float64)
+
+    def _peer_views(self, t):
+        key = t.data_ptr()
+        if key not in self._peers:
+            h = (C.c_ubyte * 64)()
+            _lib.check(_lib.lib().b200p_ipc_export(C.c_void_p(key), C.cast(h, C.c_void_p)))
+            handles = [None] * self.nranks
+            self.dist.all_gather_object(handles, bytes(h), group=self.group)
+            views = []
+            for q, hb in enumerate(handles):
+                if q == self.rank:
+                    views.append(t)
+                    continue
+                buf = (C.c_ubyte * 64).from_buffer_copy(hb)
+                pp = C.c_void_p()
+                _lib.check(_lib.lib().b200p_ipc_open(C.cast(buf, C.c_void_p), C.byref(pp)))
+                views.append(device_view(pp.value, tuple(t.shape), t.dtype))
+            self._peers[key] = views
+        return self._peers[key]
+
+    def _fence(self):
+        torch.cuda.synchronize()
+        self.dist.barrier(group=self.group)
+
+    def _reduce(self, t, op):
+        h = t.detach().cpu()
+        self.dist.all_reduce(h, op=op, group=self.group)
+        t.copy_(h)
+
+    def sum_(self, t): self._reduce(t, self.dist.ReduceOp.SUM)
+    def max_(self, t): self._reduce(t, self.dist.ReduceOp.MAX)
+
+    def halo(self, u, ranges):
+        peers = self._peer_views(u)
+        self._fence()                       # everybody's strip is written
+        for q, a, b in halo_plan(ranges, self.rank)[0]:
+            u[:, a:b].copy_(peers[q][:, a:b])
+        self._fence()                       # nobody overwrites rows that are still being pulled
+
+    def gather_rows(self, field, rows):
+        peers = self._peer_views(field)
+        self._fence()
+        for q, (a, b) in enumerate(rows):
+            if q != self.rank:
+                field[:, a:b].copy_(peers[q][:, a:b])
+        self._fence()
+
+    def close(self):
+        for views in self._peers.values():
+            for q, v in enumerate(views):
+                if q != self.rank:
+                    _lib.lib().b200p_ipc_close(C.c_void_p(v.data_ptr()))
+        self._peers = {}
+        for p in self._owned:
+            _lib.lib().b200p_free(p)
+        self._owned = []
 
 
 class LocalGroup:
@@ -251,8 +334,7 @@ class StripSolver:
         c, h, w = self.shape
         d_mask = _dev.to_device_u8(np.ascontiguousarray(mask).view(np.uint8).reshape(1, h, w))
         d_known = _dev.to_device_f64(np.ascontiguousarray(known, dtype=np.float64).reshape(1, c, h, w))
-        d_out = _dev.empty_f64((1, c, h, w))
-        d_out.zero_()
+        d_out = self.t.zeros_f64((1, c, h, w))
         try:
             _, reports = self.plan.solve_device(d_mask, d_known, d_out)
         except Exception:
@@ -264,3 +346,5 @@ class StripSolver:
 
     def close(self):
         self.plan.close()
+        if hasattr(self.t, "close"):
+            self.t.close()

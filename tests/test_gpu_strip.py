@@ -94,3 +94,50 @@ def test_strip_geometry_and_halo_plan():
         l0, l1 = r2[0][q], r2[1][q]
         assert l1[0] == l0[0] // 2 and (l1[1] == l0[1] // 2 or q == n - 1)
         assert l1[2] <= max(0, l0[2] // 2 - 1) and l1[3] >= min(1080, (l0[3] + 1) // 2 + 1)
+
+
+# ---- two real PROCESSES on the one GPU: peer memory through CUDA IPC, control through gloo ----------
+
+def _ipc_worker(rank, world, port, w, h, c, levels, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    m, k = oracle.seeded_problem(w, h, 0.03, 7, channels=c)
+    s = strip.StripSolver(w, h, c, bp.MultigridConfig(), strip.IpcTransport(), levels=levels)
+    u, reps = s.solve(m, k)
+    q.put((rank, s.own, u.cpu().numpy(), [(r.iterations, r.final_rel_residual) for r in reps]))
+    dist.barrier()
+    s.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,levels", [(2, 1), (3, 2)])
+def test_strip_solve_over_cuda_ipc_processes(world, levels):
+    """One process per rank (all on this GPU), buffers mapped into each other with CUDA IPC, halo rows
+    pulled with device-to-device copies: the multi-process shape of the multi-GPU run."""
+    import socket
+    import torch.multiprocessing as mp
+    w, h, c = 768, 512, 2
+    m, k = oracle.seeded_problem(w, h, 0.03, 7, channels=c)
+    ref = bp.solve_image(bp.InpaintingProblem(m, k), "mg-oras", bp.MultigridConfig())
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, w, h, c, levels, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    full = np.empty_like(ref.fields)
+    for _ in range(world):
+        rank, (lo, hi), u, reps = q.get(timeout=300)
+        full[:, lo:hi] = u
+        assert [it for it, _ in reps] == [r.iterations for r in ref.reports]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    np.testing.assert_allclose(full, ref.fields, rtol=0, atol=1e-9)
