@@ -173,14 +173,16 @@ def run_strip(args, rank, world, local):
     if "RANK" in os.environ and not dist.is_initialized():  # torchrun with one rank: still exercise NCCL
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if dist.is_initialized():
+    if dist.is_initialized() and args.strip_transport == "ipc":
+        transport = strip.IpcTransport(dist.new_group(backend="gloo"))
+    elif dist.is_initialized():
         transport = strip.TorchDistTransport()
     else:
         transport = strip.LocalGroup(1).transport(0)
     solver = strip.StripSolver(W, H, C, cfg, transport, levels=args.strip_levels)
     d_mask = torch.from_numpy(mask.view(np.uint8)[None]).cuda()
     d_known = torch.from_numpy(known[None]).cuda()
-    d_out = torch.zeros_like(d_known)
+    d_out = transport.zeros_f64(tuple(d_known.shape))  # the IPC transport needs a cudaMalloc base
 
     def barrier():
         torch.cuda.synchronize()
@@ -212,7 +214,8 @@ def run_strip(args, rank, world, local):
                        "block_size": bs, "overlap": ov, "tol_rel": 1e-3, "frames": 1,
                        "v_cycles": [r.iterations for r in reports],
                        "parallelism": f"1 frame in {world} horizontal strip(s); rank 0 owns rows [{lo}, {hi}); "
-                                      f"halo exchange per sweep, {args.strip_levels} striped level(s), coarser levels replicated"}}), flush=True)
+                                      f"halo exchange per sweep ({type(transport).__name__}), {args.strip_levels} striped level(s), "
+                                      "coarser levels replicated"}}), flush=True)
     solver.close()
     if dist.is_initialized():
         dist.destroy_process_group()
@@ -233,6 +236,8 @@ def main():
     ap.add_argument("--strip", action="store_true",
                     help="single-frame strip mode: ONE frame cut into horizontal strips over the ranks "
                          "(halo exchange per sweep over NCCL); default workload 8k_rgb_2pct_b32o6")
+    ap.add_argument("--strip-transport", default="nccl", choices=["nccl", "ipc"],
+                    help="--strip exchange: torch.distributed NCCL, or CUDA-IPC peer memory + gloo control")
     ap.add_argument("--strip-levels", type=int, default=2,
                     help="how many of the finest levels are striped in --strip mode (the rest is replicated)")
     args = ap.parse_args()
