@@ -470,3 +470,41 @@ def test_async_api_state_and_streaming_pipeline():
     again, _ = pipe.run(masks[:2], known[:2])
     assert np.array_equal(again, ref_out[:2])
     pipe.close()
+
+
+def test_randomised_shapes_and_configs_match_oracle():
+    """Seeded sweep over image shapes (odd, tiny, non-square), block geometries, densities, channel counts
+    and tolerances: mg-oras through the C-ABI against the oracle (the reference's hypothesis-style checks,
+    tests/test_partition.py:56-67, applied to the whole path)."""
+    rng = np.random.default_rng(20240106)
+    geoms = [(32, 6), (16, 2), (8, 2), (24, 4), (32, 0), (16, 8), (10, 3), (40, 6), (64, 6)]
+    for case in range(40):
+        w, h = int(rng.integers(9, 260)), int(rng.integers(9, 200))
+        if case % 5 == 0:
+            w, h = 4 * (w // 4 + 1), 2 * (h // 2 + 1)          # eligible for the vector paths
+        bs, ov = geoms[int(rng.integers(len(geoms)))]
+        dens = float(rng.choice([0.01, 0.03, 0.1, 0.3, 0.8]))
+        dens = max(dens, 2.0 / (w * h))
+        c = int(rng.integers(1, 4))
+        kw = dict(tol_rel=float(rng.choice([1e-3, 1e-5])), alpha=float(rng.choice([0.5, 1.0, 0.2])))
+        mkw = dict(nu_pre=int(rng.integers(0, 3)), nu_post=int(rng.integers(1, 3)),
+                   value_downsampling=str(rng.choice(["modified", "naive"])))
+        m, k = oracle.seeded_problem(w, h, dens, 500 + case, channels=c)
+        cfg_o, cfg_b = _cfgs(bs, ov, **kw, **mkw)
+        spacing = float(rng.choice([1.0, 0.5, 2.0]))
+        try:
+            ref, reps_o = oracle.solve_image(m, k, spacing, cfg_o)
+            if not all(r.converged for r in reps_o):
+                # a few geometries (no overlap, small Robin weight) make the Schwarz iteration DIVERGE in
+                # the reference itself: the two implementations must then blow up alike (same counts,
+                # residuals equal to 1e-6 relative), absolute field differences mean nothing
+                res = bp.solve_image(bp.InpaintingProblem(m, k, spacing), "mg-oras", cfg_b)
+                for ro, rg in zip(reps_o, res.reports):
+                    assert rg.iterations == ro.iterations and rg.converged == ro.converged
+                    assert rg.final_rel_residual == pytest.approx(ro.final_rel_residual, rel=1e-5)
+                scale = max(1.0, float(np.abs(ref).max()))
+                assert np.abs(res.fields - ref).max() <= 1e-6 * scale
+                continue
+            _compare(m, k, cfg_o, cfg_b, spacing=spacing)
+        except AssertionError as e:
+            raise AssertionError(f"case {case}: {w}x{h}x{c} block {bs}/{ov} density {dens} {kw} {mkw}: {e}") from e
