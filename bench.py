@@ -332,7 +332,7 @@ def main():
         # D2H are inside the timed region, the pipeline is drained once, before the clock stops
         t0 = time.perf_counter()
         for i in range(k_e2e):
-            pipe.submit(h_mask.numpy(), h_known.numpy(), (h_out2 if i % 2 else h_out).numpy())
+            job = pipe.submit(h_mask.numpy(), h_known.numpy(), (h_out2 if i % 2 else h_out).numpy())
         pipe.flush()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
@@ -346,12 +346,23 @@ def main():
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = {"value": world * F * k_e2e / float(t.item()), "unit": UNIT,
-               "h2d_bytes_per_step": int(h_mask.numel() + h_known.numel() * 8),
-               "d2h_bytes_per_step": int(h_out.numel() * 8), "steps": k_e2e,
+               "h2d_bytes_per_step": int(job["h2d_bytes"]),
+               "d2h_bytes_per_step": int(job["d2h_bytes"]), "steps": k_e2e,
                "api": f"FramePipeline.submit/flush -> b200p_solve_host_async + b200p_solve_wait per frame on "
                       f"{lanes} lanes (float64 fields, pinned host buffers, H2D + D2H inside the timed region)",
                "bit_identical_to_device_path": e2e_same,
                "drained_every_step_value": world * F * 3 / dt_drained}
+        # the same pipeline with the sparse ingest (mask plane + known values at mask pixels only,
+        # fetched by the device from the pinned array): fewer bytes, but slower when lanes overlap
+        sp = bp.FramePipeline(W, H, C, cfg, lanes=lanes, frames_per_lane=1, sparse_ingest=True)
+        sp.run(h_mask.numpy(), h_known.numpy(), h_out.numpy())
+        t0 = time.perf_counter()
+        for i in range(k_e2e):
+            job = sp.submit(h_mask.numpy(), h_known.numpy(), (h_out2 if i % 2 else h_out).numpy())
+        sp.flush()
+        e2e["sparse_ingest_value"] = world * F * k_e2e / (time.perf_counter() - t0)
+        e2e["sparse_ingest_h2d_bytes_per_step"] = int(job["h2d_bytes"])
+        sp.close()
         # single plan, no overlap (H2D -> solve -> D2H back to back)
         t0 = time.perf_counter()
         for _ in range(3):

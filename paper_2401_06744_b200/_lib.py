@@ -103,6 +103,8 @@ SIGNATURES = {
     "b200p_plan_level_rc": (_I, [_VP, _I, C.POINTER(_VP)]),
     "b200p_plan_device_bytes": (_I64, [_VP]),
     "b200p_plan_launch_count": (_I64, [_VP]),
+    "b200p_plan_set_ingest": (_I, [_VP, _I]),
+    "b200p_plan_last_transfer_bytes": (_I, [_VP, C.POINTER(_I64), C.POINTER(_I64)]),
     "b200p_plan_profile": (_I, [_VP, _I]),
     "b200p_plan_profile_kinds": (_I, []),
     "b200p_plan_profile_name": (C.c_char_p, [_I]),

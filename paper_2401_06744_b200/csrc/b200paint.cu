@@ -250,6 +250,14 @@ struct b200p_plan {
     uint8_t *d_in_mask = nullptr;
     double *d_in_known = nullptr, *d_out = nullptr;
     uint8_t *d_io_u8 = nullptr;
+    // sparse ingest (host f64 entry point): pixel indices + values at mask pixels, pinned + device
+    uint32_t *h_sp_idx = nullptr, *d_sp_idx = nullptr;
+    double *h_sp_val = nullptr, *d_sp_val = nullptr;
+    size_t sp_cap = 0;
+    int64_t last_h2d = 0, last_d2h = 0;  // bytes the last host entry point copied each way
+    int ingest_mode = 0;                  // 0 auto (sparse when the mask is), 1 always the dense plane copy
+    bool last_h2d_counted = false;        // ... H2D side = mask planes + *h_cnt values (counted on the device)
+    unsigned long long *h_cnt = nullptr, *d_cnt = nullptr;
     void *h_pin = nullptr;  // pinned bounce buffer
     size_t h_pin_bytes = 0;
     cudaStream_t own_stream = nullptr;
@@ -1679,6 +1687,12 @@ void b200p_plan_destroy(b200p_plan *pl) {
     for (void *p : pl->owned) cudaFree(p);
     if (pl->h_any) cudaFreeHost(pl->h_any);
     if (pl->h_pin) cudaFreeHost(pl->h_pin);
+    if (pl->h_cnt) cudaFreeHost(pl->h_cnt);
+    if (pl->d_cnt) cudaFree(pl->d_cnt);
+    if (pl->h_sp_idx) cudaFreeHost(pl->h_sp_idx);
+    if (pl->h_sp_val) cudaFreeHost(pl->h_sp_val);
+    if (pl->d_sp_idx) cudaFree(pl->d_sp_idx);
+    if (pl->d_sp_val) cudaFree(pl->d_sp_val);
     if (pl->own_stream) cudaStreamDestroy(pl->own_stream);
     delete pl;
 }
@@ -2291,17 +2305,177 @@ static int check_masks(const b200p_plan *pl, const uint8_t *h_mask) {
     return 0;
 }
 
+// Known pixels of one frame: count, then indices (row-major order) -- the mask is ~98 % zeros at
+// the benchmark densities, so whole 8-byte words are skipped.
+static size_t count_nonzero(const uint8_t *m, size_t n) {
+    size_t cnt = 0, i = 0;
+    for (; i + 8 <= n; i += 8) {
+        uint64_t v;
+        memcpy(&v, m + i, 8);
+        if (!v) continue;
+        for (int k = 0; k < 8; ++k) cnt += m[i + k] != 0;
+    }
+    for (; i < n; ++i) cnt += m[i] != 0;
+    return cnt;
+}
+
+static size_t list_nonzero(const uint8_t *m, size_t n, uint32_t *idx) {
+    size_t cnt = 0, i = 0;
+    for (; i + 8 <= n; i += 8) {
+        uint64_t v;
+        memcpy(&v, m + i, 8);
+        if (!v) continue;
+        for (int k = 0; k < 8; ++k)
+            if (m[i + k]) idx[cnt++] = (uint32_t)(i + k);
+    }
+    for (; i < n; ++i)
+        if (m[i]) idx[cnt++] = (uint32_t)i;
+    return cnt;
+}
+
+static int ensure_sparse_staging(b200p_plan *pl, size_t entries) {
+    if (entries <= pl->sp_cap) return 0;
+    const size_t cap = entries + entries / 4 + 1024;
+    const int C = pl->cfg.channels;
+    if (pl->h_cnt) cudaFreeHost(pl->h_cnt);
+    if (pl->d_cnt) cudaFree(pl->d_cnt);
+    if (pl->h_sp_idx) cudaFreeHost(pl->h_sp_idx);
+    if (pl->h_sp_val) cudaFreeHost(pl->h_sp_val);
+    if (pl->d_sp_idx) cudaFree(pl->d_sp_idx);
+    if (pl->d_sp_val) cudaFree(pl->d_sp_val);
+    pl->h_sp_idx = pl->d_sp_idx = nullptr;
+    pl->h_sp_val = pl->d_sp_val = nullptr;
+    pl->sp_cap = 0;
+    CU(cudaMallocHost((void **)&pl->h_sp_idx, cap * sizeof(uint32_t)));
+    CU(cudaMallocHost((void **)&pl->h_sp_val, cap * C * sizeof(double)));
+    CU(cudaMalloc((void **)&pl->d_sp_idx, cap * sizeof(uint32_t)));
+    CU(cudaMalloc((void **)&pl->d_sp_val, cap * C * sizeof(double)));
+    pl->sp_cap = cap;
+    return 0;
+}
+
+// Host f64 entry point.  The path uses `known` only at mask pixels (rhs = where(mask, known, 0),
+// core.py:147-151), so when the mask is sparse the H2D side carries the mask plane plus the values
+// at mask pixels only: 4K RGB at 2 % moves 12 MB instead of 207 MB per frame.
+//   * `h_known` pinned (cudaHostAlloc / cudaHostRegister): a kernel reads those values straight
+//     from the caller's array over PCIe (zero copy) and writes the zero-filled known plane;
+//   * pageable `h_known`: this thread gathers a compacted (pixel index, C values) list into
+//     pinned staging, and a scatter kernel rebuilds the plane.
+// Dense masks (list larger than half the planes) and B200P_DENSE_INGEST=1 copy the planes as they
+// are.  The result is copied back in full.
 int b200p_solve_host_async(b200p_plan *pl, const uint8_t *h_mask, const double *h_known, double *h_out) {
     if (!pl || !h_mask || !h_known || !h_out) return fail_arg(B200P_ERR_ARG, "null argument");
+    if (pl->pending) return fail_arg(B200P_ERR_STATE, "a solve is already pending on this plan");
     int rc = check_masks(pl, h_mask);
     if (rc) return rc;
-    if ((rc = ensure_staging(pl, false))) return rc;
     const size_t plane = (size_t)pl->cfg.width * pl->cfg.height;
+    const int C = pl->cfg.channels;
+    const char *env_dense = getenv("B200P_DENSE_INGEST");  // read per call (A/B tests toggle it)
+    const bool force_dense = pl->ingest_mode == 1 || (env_dense && atoi(env_dense) != 0);
+    if ((rc = ensure_staging(pl, false))) return rc;
     cudaStream_t st = pl->own_stream;
+    const size_t dense_bytes = pl->P * plane * sizeof(double);
     CU(cudaMemcpyAsync(pl->d_in_mask, h_mask, pl->F * plane, cudaMemcpyHostToDevice, st));
-    CU(cudaMemcpyAsync(pl->d_in_known, h_known, pl->P * plane * sizeof(double), cudaMemcpyHostToDevice, st));
+    pl->last_h2d = (int64_t)(pl->F * plane + dense_bytes);
+    pl->last_h2d_counted = false;
+    // pinned source: the device fetches the mask pixels' values itself (no host pass over `known`)
+    const double *mapped = nullptr;
+    if (!force_dense) {
+        cudaPointerAttributes at;
+        if (cudaPointerGetAttributes(&at, h_known) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+            at.devicePointer)
+            mapped = static_cast<const double *>(at.devicePointer);
+        else
+            cudaGetLastError();
+    }
+    bool done = false;
+    if (mapped) {
+        // density from a strided sample of the mask words (the choice of path does not change results)
+        size_t seen = 0, hit = 0;
+        const size_t n = pl->F * plane;
+        for (size_t i = 0; i + 8 <= n; i += 8 * 61) {
+            for (int k = 0; k < 8; ++k) hit += h_mask[i + k] != 0;
+            seen += 8;
+        }
+        if (seen && hit * 4 <= seen) {  // <= 25 % known pixels: fetching them beats copying the planes
+            if (!pl->h_cnt) {
+                CU(cudaHostAlloc((void **)&pl->h_cnt, 64, cudaHostAllocMapped));
+                CU(cudaMalloc((void **)&pl->d_cnt, 64));
+            }
+            CU(cudaMemsetAsync(pl->d_cnt, 0, 8, st));
+            {
+                LaunchScope sc(pl, st, KK_CONVERT, (double)(n + dense_bytes));
+                gather_known_mapped_kernel<<<(unsigned)((n + ST_THREADS - 1) / ST_THREADS), ST_THREADS, 0, st>>>(
+                    pl->d_in_mask, mapped, n, C, plane, pl->d_in_known, pl->d_cnt);
+                CU(cudaGetLastError());
+            }
+            {
+                LaunchScope sc(pl, st, KK_CONVERT, 16.0);
+                publish_count_kernel<<<1, 1, 0, st>>>(pl->d_cnt, pl->h_cnt);
+                CU(cudaGetLastError());
+            }
+            pl->last_h2d_counted = true;  // F*plane + count*C*8, known once the stream has run
+            done = true;
+        }
+    } else if (!force_dense && plane < (1ull << 32)) {
+        // pageable source: gather on this thread into pinned staging
+        std::vector<size_t> cnt(pl->F);
+        size_t total = 0;
+        for (int f = 0; f < pl->F; ++f) total += cnt[f] = count_nonzero(h_mask + (size_t)f * plane, plane);
+        const size_t sparse_bytes = total * (sizeof(uint32_t) + C * sizeof(double));
+        if (sparse_bytes * 2 <= dense_bytes) {
+            if ((rc = ensure_sparse_staging(pl, total))) return rc;
+            CU(cudaMemsetAsync(pl->d_in_known, 0, dense_bytes, st));
+            size_t off = 0;
+            for (int f = 0; f < pl->F; ++f) {
+                uint32_t *idx = pl->h_sp_idx + off;
+                double *val = pl->h_sp_val + off * C;
+                list_nonzero(h_mask + (size_t)f * plane, plane, idx);
+                for (int c = 0; c < C; ++c) {
+                    const double *src = h_known + ((size_t)f * C + c) * plane;
+                    for (size_t k = 0; k < cnt[f]; ++k) val[k * C + c] = src[idx[k]];
+                }
+                // one frame's list travels while the next one is gathered
+                CU(cudaMemcpyAsync(pl->d_sp_idx + off, idx, cnt[f] * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+                CU(cudaMemcpyAsync(pl->d_sp_val + off * C, val, cnt[f] * C * sizeof(double),
+                                   cudaMemcpyHostToDevice, st));
+                {
+                    const size_t n = cnt[f] * C;
+                    LaunchScope sc(pl, st, KK_CONVERT, 20.0 * n);
+                    scatter_known_kernel<<<(unsigned)((n + ST_THREADS - 1) / ST_THREADS), ST_THREADS, 0, st>>>(
+                        pl->d_sp_idx + off, pl->d_sp_val + off * C, n, C, plane,
+                        pl->d_in_known + (size_t)f * C * plane);
+                    CU(cudaGetLastError());
+                }
+                off += cnt[f];
+            }
+            pl->last_h2d = (int64_t)(pl->F * plane + sparse_bytes);
+            done = true;
+        }
+    }
+    if (!done) CU(cudaMemcpyAsync(pl->d_in_known, h_known, dense_bytes, cudaMemcpyHostToDevice, st));
     if ((rc = b200p_solve_async(pl, pl->d_in_mask, pl->d_in_known, pl->d_out, st))) return rc;
-    CU(cudaMemcpyAsync(h_out, pl->d_out, pl->P * plane * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(h_out, pl->d_out, dense_bytes, cudaMemcpyDeviceToHost, st));
+    pl->last_d2h = (int64_t)dense_bytes;
+    return 0;
+}
+
+int b200p_plan_set_ingest(b200p_plan *pl, int mode) {
+    if (!pl) return fail_arg(B200P_ERR_ARG, "null plan");
+    if (mode != 0 && mode != 1) return fail_arg(B200P_ERR_ARG, "ingest mode must be 0 (auto) or 1 (dense), got %d", mode);
+    pl->ingest_mode = mode;
+    return 0;
+}
+
+int b200p_plan_last_transfer_bytes(const b200p_plan *pl, int64_t *h2d, int64_t *d2h) {
+    if (!pl) return fail_arg(B200P_ERR_ARG, "null plan");
+    if (pl->pending) return fail_arg(B200P_ERR_STATE, "a solve is pending on this plan: call b200p_solve_wait first");
+    if (h2d)
+        *h2d = pl->last_h2d_counted
+                   ? (int64_t)((size_t)pl->F * pl->cfg.width * pl->cfg.height +
+                               *pl->h_cnt * (size_t)pl->cfg.channels * sizeof(double))
+                   : pl->last_h2d;
+    if (d2h) *d2h = pl->last_d2h;
     return 0;
 }
 
@@ -2337,6 +2511,8 @@ int b200p_solve_host_u8_async(b200p_plan *pl, const uint8_t *h_mask, const uint8
         CU(cudaGetLastError());
     }
     CU(cudaMemcpyAsync(h_out_u8, pl->d_io_u8, n, cudaMemcpyDeviceToHost, st));
+    pl->last_h2d = (int64_t)(pl->F * plane + n);
+    pl->last_d2h = (int64_t)n;
     return 0;
 }
 

@@ -515,6 +515,39 @@ u8_to_f64_kernel(const uint8_t *__restrict__ in, size_t n, double *__restrict__ 
     if (i < n) out[i] = (double)in[i];
 }
 
+// Sparse ingest: entry e = k*C + c of the compacted list goes to channel plane c, pixel idx[k].
+__global__ void __launch_bounds__(ST_THREADS)
+scatter_known_kernel(const uint32_t *__restrict__ idx, const double *__restrict__ val, size_t n, int C,
+                     size_t plane, double *__restrict__ known) {
+    const size_t e = (size_t)blockIdx.x * ST_THREADS + threadIdx.x;
+    if (e < n) {
+        const size_t k = e / (unsigned)C;
+        const int c = (int)(e - k * (unsigned)C);
+        known[(size_t)c * plane + idx[k]] = val[e];
+    }
+}
+
+// Sparse ingest from PINNED host memory: `hk` is the caller's known array seen through its device
+// alias (zero copy).  Only mask pixels are fetched over PCIe; everything else is written as 0.
+__global__ void __launch_bounds__(ST_THREADS)
+gather_known_mapped_kernel(const uint8_t *__restrict__ mask, const double *__restrict__ hk, size_t n, int C,
+                           size_t plane, double *__restrict__ known, unsigned long long *__restrict__ count) {
+    const size_t i = (size_t)blockIdx.x * ST_THREADS + threadIdx.x;
+    const bool m = i < n && mask[i] != 0;
+    if (i < n) {
+        const size_t f = i / plane, pix = i - f * plane;
+        for (int c = 0; c < C; ++c) {
+            const size_t o = (f * C + c) * plane + pix;
+            known[o] = m ? __ldcs(hk + o) : 0.0;
+        }
+    }
+    const int k = __syncthreads_count(m);
+    if (threadIdx.x == 0 && k) atomicAdd(count, (unsigned long long)k);
+}
+
+// the number of values fetched, for b200p_plan_last_transfer_bytes (plain store into pinned host memory)
+__global__ void publish_count_kernel(const unsigned long long *count, unsigned long long *host) { *host = *count; }
+
 __global__ void __launch_bounds__(ST_THREADS)
 f64_to_u8_kernel(const double *__restrict__ in, size_t n, uint8_t *__restrict__ out) {
     const size_t i = (size_t)blockIdx.x * ST_THREADS + threadIdx.x;

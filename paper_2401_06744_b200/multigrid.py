@@ -120,6 +120,17 @@ class Plan:
     def launch_count(self) -> int:
         return int(_lib.lib().b200p_plan_launch_count(self.handle))
 
+    def set_ingest(self, dense: bool):
+        """Host f64 entry points: False = sparse ingest when the mask is sparse (default; lowest latency of a
+        single solve), True = always DMA the planes (what a multi-lane pipeline wants)."""
+        _lib.check(_lib.lib().b200p_plan_set_ingest(self.handle, 1 if dense else 0))
+
+    def last_transfer_bytes(self):
+        """(H2D, D2H) bytes copied by the last host entry point (the f64 ingest is sparse when the mask is)."""
+        a, b = C.c_int64(), C.c_int64()
+        _lib.check(_lib.lib().b200p_plan_last_transfer_bytes(self.handle, C.byref(a), C.byref(b)))
+        return int(a.value), int(b.value)
+
     def profile(self, enable: bool):
         _lib.check(_lib.lib().b200p_plan_profile(self.handle, 1 if enable else 0))
 

@@ -25,7 +25,7 @@ from .multigrid import MultigridConfig, Plan
 
 class FramePipeline:
     def __init__(self, width, height, channels, cfg: MultigridConfig | None = None, spacing=1.0,
-                 lanes: int = 5, frames_per_lane: int = 1):
+                 lanes: int = 5, frames_per_lane: int = 1, sparse_ingest: bool | None = None):
         if lanes < 1 or frames_per_lane < 1:
             raise ValueError("need lanes >= 1 and frames_per_lane >= 1")
         _dev.require_cuda()
@@ -36,6 +36,12 @@ class FramePipeline:
         _lib.check(_lib.lib().b200p_get_device(C.byref(dev)))
         self.device = dev.value
         self.plans = [Plan(width, height, channels, frames_per_lane, self.cfg, spacing) for _ in range(lanes)]
+        # with several lanes the copy engines run under the other lanes' kernels for free, while the
+        # zero-copy fetch of the sparse ingest queues behind their D2H traffic: DMA the planes
+        if sparse_ingest is None:
+            sparse_ingest = lanes == 1
+        for p in self.plans:
+            p.set_ingest(dense=not sparse_ingest)
         self._inflight = [None] * lanes  # (job, chunk index) pending on each lane
         self._next = 0
 
@@ -63,7 +69,7 @@ class FramePipeline:
     def submit(self, masks, known, out=None, u8: bool = False):
         """Enqueue a batch: masks (F,H,W) bool/uint8, known (F,C,H,W) float64 (uint8 with u8=True).
 
-        Returns a job dict {"out", "reports"}; its arrays are complete after `flush()` (or once
+        Returns a job dict {"out", "reports", "h2d_bytes", "d2h_bytes"}; its arrays are complete after `flush()` (or once
         later submits have recycled all of its lanes).  Batches submitted back to back keep the
         lanes busy across batch boundaries: only `flush()` drains the pipeline.  `out` may be a
         preallocated (pinned) array of known's shape and dtype.  reports[f] is the list of
@@ -80,7 +86,7 @@ class FramePipeline:
         self._check(masks, known, out)
         m8 = masks.view(np.uint8)
         k = self.frames_per_lane
-        job = {"out": out, "reports": [None] * masks.shape[0]}
+        job = {"out": out, "reports": [None] * masks.shape[0], "h2d_bytes": 0, "d2h_bytes": 0}
         try:
             for i in range(masks.shape[0] // k):
                 li = self._next % len(self.plans)
@@ -101,6 +107,9 @@ class FramePipeline:
         self._inflight[li] = None
         job, i = ent
         reps = self.plans[li].wait()
+        up, down = self.plans[li].last_transfer_bytes()
+        job["h2d_bytes"] += up
+        job["d2h_bytes"] += down
         k, c = self.frames_per_lane, self.shape[0]
         for j in range(k):
             job["reports"][i * k + j] = reps[j * c:(j + 1) * c]

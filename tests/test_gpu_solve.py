@@ -508,3 +508,54 @@ def test_randomised_shapes_and_configs_match_oracle():
             _compare(m, k, cfg_o, cfg_b, spacing=spacing)
         except AssertionError as e:
             raise AssertionError(f"case {case}: {w}x{h}x{c} block {bs}/{ov} density {dens} {kw} {mkw}: {e}") from e
+
+
+def test_sparse_ingest_matches_dense_ingest(monkeypatch):
+    """Host f64 entry point: the H2D side carries the mask plane + the known values at mask pixels only
+    (rhs = where(mask, known, 0), core.py:147-151).  Same bits as copying the planes in full; values off
+    the mask are never looked at; dense masks fall back to the plane copy."""
+    w, h, c = 200, 136, 3
+    cfg = bp.MultigridConfig(block_size=16, overlap=2)
+    ms, ks = zip(*(oracle.seeded_problem(w, h, 0.04, 70 + f, channels=c) for f in range(2)))
+    masks, known = np.stack(ms).view(np.uint8), np.stack(ks)
+    plan = bp.Plan(w, h, c, 2, cfg)
+    out_s, reps_s = plan.solve_host(masks, known)
+    up, down = plan.last_transfer_bytes()
+    nk = int(masks.sum())
+    assert up == masks.size + nk * (4 + 8 * c) and down == known.nbytes
+    monkeypatch.setenv("B200P_DENSE_INGEST", "1")
+    out_d, reps_d = plan.solve_host(masks, known)
+    assert plan.last_transfer_bytes() == (masks.size + known.nbytes, known.nbytes)
+    monkeypatch.delenv("B200P_DENSE_INGEST")
+    assert np.array_equal(out_s, out_d)
+    plan.set_ingest(dense=True)
+    out_d2, _ = plan.solve_host(masks, known)
+    assert plan.last_transfer_bytes() == (masks.size + known.nbytes, known.nbytes) and np.array_equal(out_d2, out_s)
+    plan.set_ingest(dense=False)
+    assert [r.final_rel_residual for r in reps_s] == [r.final_rel_residual for r in reps_d]
+    # garbage off the mask changes nothing (sparse: never copied; dense: never read)
+    junk = np.where(masks[:, None].astype(bool), known, 1e6 * np.random.default_rng(1).random(known.shape))
+    out_j, _ = plan.solve_host(masks, junk)
+    assert np.array_equal(out_j, out_s)
+    ref, _ = oracle.solve_image(ms[1], ks[1], 1.0, _cfgs(16, 2)[0])
+    assert np.abs(out_s[1] - ref).max() <= 1e-9
+    # pinned source: the device fetches the values at mask pixels in place (zero copy)
+    import torch
+    pk = torch.from_numpy(junk).pin_memory()
+    po = torch.empty_like(pk).pin_memory()
+    plan.solve_host_async(masks, pk.numpy(), po.numpy())
+    plan.wait()
+    assert plan.last_transfer_bytes() == (masks.size + nk * 8 * c, known.nbytes)
+    assert np.array_equal(po.numpy(), out_s)
+    plan.close()
+    # dense mask -> plane copy; a bigger list than the staging of an earlier call -> regrown staging
+    plan = bp.Plan(w, h, 1, 1, cfg)
+    for dens in (0.02, 0.3, 0.9):
+        m, k = oracle.seeded_problem(w, h, dens, 91, channels=1)
+        out, _ = plan.solve_host(m.view(np.uint8)[None], k[None])
+        up, _ = plan.last_transfer_bytes()
+        n_known = int(m.sum())
+        assert up == (m.size + n_known * 12 if n_known * 12 * 2 <= k.nbytes else m.size + k.nbytes)
+        ref, _ = oracle.solve_image(m, k, 1.0, _cfgs(16, 2)[0])
+        assert np.abs(out[0] - ref).max() <= 1e-9
+    plan.close()
