@@ -498,6 +498,14 @@ static bool rows4_ok(const LevelHost &L, const double *u, const double *b) {
            ((uintptr_t)b % 16) == 0 && ((uintptr_t)L.d_mask % 4) == 0;
 }
 
+// rm (right-hand side = where(mask, known, 0)) is only used by the solve drivers, where the iterate equals
+// `known` at mask pixels after every step (flat init, prolongate_solution, corrections that are exactly 0
+// there): the row walkers then skip the b - u evaluation at mask pixels.  B200P_TRUST_MASK=0 evaluates it.
+static bool trust_mask_enabled() {
+    const char *e = getenv("B200P_TRUST_MASK");
+    return !(e && *e == '0');
+}
+
 static RowsArgs rows_args(b200p_plan *pl, const LevelHost &L, const double *u, const double *b,
                           const int *pred) {
     RowsArgs R;
@@ -518,6 +526,7 @@ static RowsArgs rows_args(b200p_plan *pl, const LevelHost &L, const double *u, c
     R.counter = pl->d_counter;
     R.rs_out = pl->d_rs;
     R.flag_out = pl->d_mflag;
+    R.trust = 0;
     return R;
 }
 
@@ -532,6 +541,7 @@ static int launch_norm(b200p_plan *pl, const LevelHost &L, const double *u, cons
     if (rows4_ok(L, u, b)) {
         // four columns per thread, 16-byte loads (kernels_rows.cuh)
         RowsArgs R = rows_args(pl, L, u, b, pred);
+        R.trust = rm && trust_mask_enabled();
         dim3 g4((L.info.width / 4 + ROWS4_THREADS - 1) / ROWS4_THREADS,
                 (R.y_hi - R.y_lo + R.rows_per_cta - 1) / R.rows_per_cta, pl->P);
         if (um && rm) residual_sqnorm_rows4_kernel<true, true><<<g4, ROWS4_THREADS, 0, st>>>(R);
@@ -1059,6 +1069,7 @@ static int enqueue_vcycle(b200p_plan *pl, int level, UBuf &u, const double *b, b
         if (rows4_ok(L, u.cur, b) && ((uintptr_t)Cc.d_rc % 16) == 0 && ((uintptr_t)Cc.d_mask % 2) == 0) {
             RestrictArgs RA;
             RA.R = rows_args(pl, L, u.cur, b, pred);
+            RA.R.trust = rm && trust_mask_enabled();
             RA.cmask = Cc.d_mask;
             RA.rc = Cc.d_rc;
             RA.e_zero = ez;

@@ -21,6 +21,10 @@ constexpr int ROWS4_THREADS = 128;  // 512 columns per CTA
 #ifndef B200P_ROWS_UNROLL
 #define B200P_ROWS_UNROLL 1
 #endif
+// L2 prefetch distance (rows ahead of the row being fetched) of the row walkers; 0 = off.
+#ifndef B200P_ROWS_PF
+#define B200P_ROWS_PF 0
+#endif
 
 struct RowsArgs {
     const double *u, *b;
@@ -32,6 +36,8 @@ struct RowsArgs {
     const int *pred;
     int rows_per_cta;  // even
     int y_lo, y_hi;    // rows handled by this launch (strip mode; default 0 .. h)
+    int trust;         // RM only: the caller guarantees u == b at mask pixels (true throughout fmg_solve:
+                       // interpolation is exact after every step), so b is not read at all
     // reduction of the per-CTA partials (last CTA of a problem sums them in index order)
     double *partial;
     int *partial_flag;
@@ -86,7 +92,7 @@ struct Row4 {
 template <bool UM, bool RM, class Consumer>
 __device__ __forceinline__ void walk_rows4(const double *__restrict__ up, const double *__restrict__ bp,
                                            const uint8_t *__restrict__ mp, int h, int w, double hinv2,
-                                           int xc, int y0, int y1, Consumer &consume) {
+                                           int xc, int y0, int y1, bool trust, Consumer &consume) {
     const int lane = threadIdx.x & 31;
     const bool hasL = xc > 0, hasR = xc + 4 < w;
     const double cxL = 4.0 - (xc == 0 ? 1.0 : 0.0);
@@ -132,6 +138,11 @@ __device__ __forceinline__ void walk_rows4(const double *__restrict__ up, const 
             mn = load_mask(i + w);
             below = load_row(i + w, mn);
         }
+        if (B200P_ROWS_PF > 0 && !UM && y + 1 + B200P_ROWS_PF < y1 + 1 && y + 1 + B200P_ROWS_PF < h) {
+            // the thread's four columns are one 32-byte sector: pull it into L2 a few rows ahead
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(up + i + (size_t)(1 + B200P_ROWS_PF) * w));
+            if (!RM) asm volatile("prefetch.global.L2 [%0];" ::"l"(bp + i + (size_t)(1 + B200P_ROWS_PF) * w));
+        }
         double left = __shfl_up_sync(FULL_MASK, centre.v[3], 1);
         double right = __shfl_down_sync(FULL_MASK, centre.v[0], 1);
         if (lane == 0) left = hasL ? load_one(i - 1) : 0.0;
@@ -144,13 +155,13 @@ __device__ __forceinline__ void walk_rows4(const double *__restrict__ up, const 
         for (int k = 0; k < 4; ++k) {
             // branch-free: the stencil value is always formed, mask pixels select b - u
             const double c = centre.v[k];
-            const double bb = RM ? (m[k] ? bp[i + k] : 0.0) : bp[i + k];
+            const double bb = RM ? ((m[k] && !trust) ? bp[i + k] : 0.0) : bp[i + k];
             const double lf = k == 0 ? left : centre.v[k - 1];
             const double rt = k == 3 ? right : centre.v[k + 1];
             const double s = ((above.v[k] + below.v[k]) + lf) + rt;
             const double cnt = (k == 0 ? cxL : (k == 3 ? cxR : 4.0)) - cy;
             const double au = s * (-hinv2) + (cnt * hinv2) * c;
-            r[k] = bb - (m[k] ? c : au);
+            r[k] = (RM && trust && m[k]) ? 0.0 : bb - (m[k] ? c : au);
         }
         consume(y, r, m);
         above = centre;
@@ -184,7 +195,7 @@ residual_sqnorm_rows4_kernel(const RowsArgs A) {
             if (m[k] && r[k] != 0.0) flag = 1;
     };
     walk_rows4<UM, RM>(A.u + (size_t)p * A.plane, A.b + (size_t)p * A.plane,
-                       A.mask + (size_t)(p / A.channels) * A.plane, A.h, A.w, A.hinv2, xc, y0, y1, consume);
+                       A.mask + (size_t)(p / A.channels) * A.plane, A.h, A.w, A.hinv2, xc, y0, y1, A.trust != 0, consume);
     if (!live) { acc = 0.0; flag = 0; }
     publish_partial(acc, flag, p, A, red, &sflag, &is_last);
 }
@@ -250,7 +261,7 @@ residual_restrict_rows4_kernel(const RestrictArgs A) {
         }
     };
     walk_rows4<false, RM>(R.u + (size_t)p * R.plane, R.b + (size_t)p * R.plane,
-                          R.mask + (size_t)(p / R.channels) * R.plane, h, w, R.hinv2, xc, y0, y1, consume);
+                          R.mask + (size_t)(p / R.channels) * R.plane, h, w, R.hinv2, xc, y0, y1, R.trust != 0, consume);
     publish_partial(acc, 0, p, R, red, &sflag, &is_last);
 }
 

@@ -559,3 +559,26 @@ def test_sparse_ingest_matches_dense_ingest(monkeypatch):
         ref, _ = oracle.solve_image(m, k, 1.0, _cfgs(16, 2)[0])
         assert np.abs(out[0] - ref).max() <= 1e-9
     plan.close()
+
+
+def test_mask_residual_shortcut_agrees(monkeypatch):
+    """Inside the solve drivers the iterate equals `known` at mask pixels after every step, so the row
+    walkers (K1, K3) take b - u = 0 there without reading b (default); B200P_TRUST_MASK=0 evaluates it.
+    Same cycle counts, fields equal to rounding, and interpolation stays exact at the mask pixels."""
+    w, h, c = 512, 384, 3
+    m, k = oracle.seeded_problem(w, h, 0.03, 21, channels=c)
+    cfg = bp.MultigridConfig(block_size=32, overlap=6, solver=bp.SolverConfig(tol_rel=1e-6))
+    bp.clear_plan_cache()
+    a = bp.solve_image(bp.InpaintingProblem(m, k), "mg-oras", cfg)
+    monkeypatch.setenv("B200P_TRUST_MASK", "0")
+    bp.clear_plan_cache()
+    b = bp.solve_image(bp.InpaintingProblem(m, k), "mg-oras", cfg)
+    monkeypatch.delenv("B200P_TRUST_MASK")
+    bp.clear_plan_cache()
+    assert [r.iterations for r in a.reports] == [r.iterations for r in b.reports]
+    assert np.abs(a.fields - b.fields).max() <= 1e-9
+    for r1, r2 in zip(a.reports, b.reports):
+        assert r1.final_rel_residual == pytest.approx(r2.final_rel_residual, rel=1e-9)
+    assert np.array_equal(a.fields[:, m], k[:, m]) and np.array_equal(b.fields[:, m], k[:, m])
+    ref, _ = oracle.solve_image(m, k, 1.0, _cfgs(32, 6, tol_rel=1e-6)[0])
+    assert np.abs(a.fields - ref).max() <= 1e-9
