@@ -459,7 +459,25 @@ downsample_values_kernel(const uint8_t *__restrict__ fmask, const uint8_t *__res
     const size_t ci = (size_t)Y * wc + X;
     double wg[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
     bool has[4] = {false, false, false, false};
-    const bool known = cm[ci] != 0;
+    // the cell's own fine mask is fetched together with its coarse mask (one 2-byte load per row when
+    // w is even), so the dependent chain is masks -> neighbours / values
+    const uint8_t cmk = cm[ci];
+    bool fmk[4] = {false, false, false, false};
+    if ((w & 1) == 0) {
+        const uchar2 a = *reinterpret_cast<const uchar2 *>(fm + (size_t)(2 * Y) * w + 2 * X);
+        fmk[0] = a.x != 0; fmk[1] = a.y != 0;
+        if (2 * Y + 1 < h) {
+            const uchar2 b = *reinterpret_cast<const uchar2 *>(fm + (size_t)(2 * Y + 1) * w + 2 * X);
+            fmk[2] = b.x != 0; fmk[3] = b.y != 0;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int y = 2 * Y + (k >> 1), x = 2 * X + (k & 1);
+            if (y < h && x < w) fmk[k] = fm[(size_t)y * w + x] != 0;
+        }
+    }
+    const bool known = cmk != 0;
     if (known) {
 #pragma unroll
         for (int dy = 0; dy < 2; ++dy)
@@ -467,13 +485,13 @@ downsample_values_kernel(const uint8_t *__restrict__ fmask, const uint8_t *__res
             for (int dx = 0; dx < 2; ++dx) {
                 const int y = 2 * Y + dy, x = 2 * X + dx;
                 if (y >= h || x >= w) continue;
-                const size_t i = (size_t)y * w + x;
-                if (!fm[i]) continue;
+                if (!fmk[dy * 2 + dx]) continue;
                 double n = 0.0;
-                if (x >= 1) n += (x & 1) ? (double)(fm[i - 1] != 0) : (double)(cm[(size_t)Y * wc + (X - 1)] != 0);
-                if (x <= w - 2) n += !(x & 1) ? (double)(fm[i + 1] != 0) : (double)(cm[(size_t)Y * wc + (X + 1)] != 0);
-                if (y >= 1) n += (y & 1) ? (double)(fm[i - w] != 0) : (double)(cm[(size_t)(Y - 1) * wc + X] != 0);
-                if (y <= h - 2) n += !(y & 1) ? (double)(fm[i + w] != 0) : (double)(cm[(size_t)(Y + 1) * wc + X] != 0);
+                // in-cell neighbours: the cell's own fine mask; the others: the adjacent cell's coarse mask
+                if (x >= 1) n += dx ? (double)fmk[dy * 2] : (double)(cm[(size_t)Y * wc + (X - 1)] != 0);
+                if (x <= w - 2) n += !dx ? (double)fmk[dy * 2 + 1] : (double)(cm[(size_t)Y * wc + (X + 1)] != 0);
+                if (y >= 1) n += dy ? (double)fmk[dx] : (double)(cm[(size_t)(Y - 1) * wc + X] != 0);
+                if (y <= h - 2) n += !dy ? (double)fmk[2 + dx] : (double)(cm[(size_t)(Y + 1) * wc + X] != 0);
                 const int k = dy * 2 + dx;
                 wg[k] = 4.0 - n;
                 c1[k] = 1.0;
