@@ -394,6 +394,33 @@ prolongate_kernel(const double *__restrict__ c, const uint8_t *__restrict__ fmas
         rowR[k] = 0.75 * mid + 0.25 * row[Xp];  // fine x odd : far = near + 1
     }
     const int y0 = 2 * Y, x0 = 2 * X;
+    if ((w & 1) == 0 && ((uintptr_t)up & 15) == 0) {
+        // even width: the two fine pixels of a row are one 16-byte store (and one 2-byte mask load)
+#pragma unroll
+        for (int dy = 0; dy < 2; ++dy) {
+            const int y = y0 + dy;
+            if (y >= h) break;
+            const int kf = dy ? 2 : 0;
+            const size_t i = (size_t)y * w + x0;
+            const uchar2 m = *reinterpret_cast<const uchar2 *>(fm + i);
+            const double v0 = 0.75 * rowL[1] + 0.25 * rowL[kf];
+            const double v1 = 0.75 * rowR[1] + 0.25 * rowR[kf];
+            double2 *dst = reinterpret_cast<double2 *>(up + i);
+            if (SOLUTION) {
+                const double *fr = frhs + (size_t)p * fplane + i;
+                double2 o;
+                o.x = m.x ? fr[0] : v0;
+                o.y = m.y ? fr[1] : v1;
+                *dst = o;
+            } else {
+                double2 o = *dst;
+                if (!m.x) o.x += v0;
+                if (!m.y) o.y += v1;
+                *dst = o;
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int dy = 0; dy < 2; ++dy) {
         const int y = y0 + dy;
