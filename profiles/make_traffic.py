@@ -33,7 +33,9 @@ n_sweeps = sum(a[0] for k, a in agg.items() if 'oras_sweep' in k)
 traffic = {'oras_sweep': {'dram_bytes_per_launch': sum(a[2] + a[3] for a in sweep) / max(n_sweeps, 1),
                           'sweeps': n_sweeps, 'source': src.split('/')[-1],
                           'note': 'dram__bytes_read.sum + dram__bytes_write.sum of K2 + K2b, averaged over the '
-                                  'sweeps of one step (all levels), like roofline.alg_bytes_per_launch'}}
+                                  'sweeps of one step (all levels), like roofline.alg_bytes_per_launch',
+                          # frames per step of the profiled command (scripts/profile_round.sh: --frames 4)
+                          'frames': int(sys.argv[4]) if len(sys.argv) > 4 else 4}}
 json.dump(traffic, open(out_json, 'w'), indent=1)
 print(open(out_txt).read())
 print(traffic)
