@@ -464,15 +464,56 @@ def v_cycle(hier: LevelHierarchy, level: int, u, rhs, cfg: MultigridConfig | Non
     return u
 
 
+def _fmg_solve_stepwise(hier: LevelHierarchy, cfg: MultigridConfig, channel: int, callback):
+    """fmg_solve with a per-cycle `callback(u)` (multigrid.py:466-481): the reference's own loop, driven from
+    the host over the stage entry points (cascade, V-cycle, residual norm) instead of the one-graph solve,
+    so that the iterate can be handed out after every cycle.  Same kernels, same cycle counts."""
+    if cfg.mode != "full_multigrid" or cfg.smoother != "oras":
+        raise NotImplementedError("callbacks are available for the mg-oras pipeline on the CUDA path")
+    t0 = time.perf_counter()
+    p = hier.problem
+    h, w = p.shape
+    plan, d_mask, _ = _channel_plan(hier, cfg, channel)
+    d_b = _dev.to_device_f64(np.where(p.mask, p.known[channel], 0.0))
+    sq = np.zeros(1)
+
+    def norm(d_u):
+        _dev.call("b200p_residual_sqnorm", _dev.ptr(d_mask), h, w, float(p.spacing), _dev.ptr(d_b),
+                  _dev.ptr(d_u), 1, sq.ctypes.data, _dev.stream())
+        return float(np.sqrt(sq[0]))
+
+    baseline = norm(d_b)                                    # flat initialisation = rhs (multigrid.py:446)
+    d_u = _dev.empty_f64((h, w))
+    _dev.call("b200p_plan_cascade", plan.handle, _dev.ptr(d_u), _dev.stream())
+    rn = norm(d_u)
+    denom = baseline if baseline > 0.0 else (rn if rn > 0.0 else 1.0)
+    rel = rn / denom
+    history, cycles, fine_units = [rel], 0, 0
+    units = np.zeros(1, dtype=np.int32)
+    while rel > cfg.solver.tol_rel and cycles < cfg.v_cycles_max:
+        _dev.call("b200p_plan_vcycle", plan.handle, 0, _dev.ptr(d_u), _dev.ptr(d_b), units.ctypes.data,
+                  _dev.stream())
+        fine_units += int(units[0])
+        cycles += 1
+        rel = norm(d_u) / denom
+        history.append(rel)
+        callback(_dev.to_host(d_u))
+    name = "mg-" + cfg.smoother
+    return _dev.to_host(d_u), SolveReport(
+        solver=name, iterations=cycles, final_rel_residual=rel, wall_time=time.perf_counter() - t0,
+        history=history, converged=rel <= cfg.solver.tol_rel, baseline_residual=baseline,
+        init_residual=baseline, fine_smoother_iterations=fine_units)
+
+
 def fmg_solve(hier: LevelHierarchy, cfg: MultigridConfig | None = None, channel: int = 0, callback=None):
     """Full-multigrid solve of one channel (multigrid.py:425-487) -> (u, SolveReport)."""
     cfg = cfg or hier.cfg
     _require_hot_path(cfg)
-    if callback is not None:
-        raise NotImplementedError("per-cycle callbacks are not available on the CUDA path")
     p = hier.problem
     if not p.mask.any():
         raise EmptyMaskError("cannot solve without known pixels")
+    if callback is not None:
+        return _fmg_solve_stepwise(hier, cfg, channel, callback)
     h, w = p.shape
     plan = cached_plan(w, h, 1, 1, cfg, p.spacing)
     d_known = hier._d_known[channel:channel + 1].contiguous()

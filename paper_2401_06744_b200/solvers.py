@@ -90,11 +90,11 @@ def oras_sweeps(op, blocks: BlockSolver, b, u, *, max_sweeps: int, stop_norm: fl
     """Schwarz sweeps on u in place until ||b - A u|| <= stop_norm (solvers.py:393-424).
 
     ``workers`` is accepted for signature compatibility (block parallelism is
-    the CUDA grid).  ``on_state`` hooks are not supported on the device path.
+    the CUDA grid).  ``on_state(u, rn, sweeps)`` is called at every residual
+    evaluation like the reference's (solvers.py:418-419); with a hook the sweeps
+    are enqueued one at a time so that the iterate can be handed out in between.
     Returns (sweeps, final residual norm).
     """
-    if on_state is not None:
-        raise NotImplementedError("on_state hooks are not available on the CUDA path")
     u_arr = np.asarray(u)
     if u_arr.dtype != np.float64 or u_arr.shape != blocks.shape:
         raise ValueError("u must be a float64 field of the mask's shape")
@@ -102,10 +102,27 @@ def oras_sweeps(op, blocks: BlockSolver, b, u, *, max_sweeps: int, stop_norm: fl
     du, db = _dev.to_device_f64(u_arr), _dev.to_device_f64(b)
     sweeps = np.zeros(1, dtype=np.int32)
     rn = np.zeros(1)
-    _dev.call("b200p_plan_oras_sweeps", plan.handle, 0, _dev.ptr(db), _dev.ptr(du), int(max_sweeps),
-              float(stop_norm), int(path), sweeps.ctypes.data, rn.ctypes.data, _dev.stream())
+
+    def run(k):
+        _dev.call("b200p_plan_oras_sweeps", plan.handle, 0, _dev.ptr(db), _dev.ptr(du), int(k),
+                  float(stop_norm), int(path), sweeps.ctypes.data, rn.ctypes.data, _dev.stream())
+        return int(sweeps[0]), float(rn[0])
+
+    if on_state is None:
+        done, norm = run(max_sweeps)
+    else:
+        done, (_, norm) = 0, run(0)                      # the residual of the start iterate
+        while True:
+            u_arr[...] = _dev.to_host(du)
+            on_state(u_arr, norm, done)
+            if norm == 0.0 or norm <= stop_norm or done >= max_sweeps:   # solvers.py:420-421
+                break
+            step, norm = run(1)
+            if step == 0:
+                break
+            done += step
     u_arr[...] = _dev.to_host(du)
-    return int(sweeps[0]), float(rn[0])
+    return done, norm
 
 
 __all__ = ["SolverConfig", "SolveReport", "BlockSolver", "oras_sweeps",

@@ -582,3 +582,29 @@ def test_mask_residual_shortcut_agrees(monkeypatch):
     assert np.array_equal(a.fields[:, m], k[:, m]) and np.array_equal(b.fields[:, m], k[:, m])
     ref, _ = oracle.solve_image(m, k, 1.0, _cfgs(32, 6, tol_rel=1e-6)[0])
     assert np.abs(a.fields - ref).max() <= 1e-9
+
+
+def test_fmg_solve_callback_after_every_cycle():
+    """fmg_solve(..., callback=cb) (multigrid.py:480-481): the host-driven loop over the stage entry points
+    hands out the iterate after every V-cycle; cycle counts, history and fields as the one-graph solve."""
+    m, k = oracle.seeded_problem(200, 144, 0.03, 8, channels=2)
+    cfg_o, cfg_b = _cfgs(16, 2, tol_rel=1e-6)
+    prob = bp.InpaintingProblem(m, k)
+    hier = bp.build_hierarchy(prob, cfg_b)
+    ho = oracle.build_hierarchy(m, k, 1.0, cfg_o)
+    for c in range(2):
+        seen = []
+        u, rep = bp.fmg_solve(hier, cfg_b, channel=c, callback=lambda uu: seen.append(uu.copy()))
+        u0, rep0 = bp.fmg_solve(hier, cfg_b, channel=c)
+        uo, ro = oracle.fmg_solve(ho, cfg_o, channel=c)
+        assert rep.iterations == rep0.iterations == ro.iterations == len(seen) > 1
+        assert rep.fine_smoother_iterations == ro.fine_smoother_iterations
+        assert len(rep.history) == len(ro.history)
+        np.testing.assert_allclose(rep.history, ro.history, rtol=1e-6)
+        assert np.array_equal(seen[-1], u) and not np.array_equal(seen[0], seen[-1])
+        assert np.abs(u - u0).max() <= 1e-9 and np.abs(u - uo).max() <= 1e-9
+        assert rep.converged and rep.baseline_residual == pytest.approx(ro.baseline_residual, rel=1e-12)
+    u1, _ = bp.solve_channel(prob, "mg-oras", cfg_b, channel=1, hierarchy=hier, callback=lambda uu: None)
+    assert np.array_equal(u1, u)
+    with pytest.raises(NotImplementedError):
+        bp.solve_channel(prob, "ml-oras", cfg_b, channel=0, callback=lambda uu: None)

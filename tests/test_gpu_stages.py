@@ -271,3 +271,35 @@ def test_v_cycle(w, h, bs, ov, rng):
         oracle.v_cycle(ho, 1, e_o, rb)
         bp.v_cycle(hb, 1, e_g, rb)
         np.testing.assert_allclose(e_g, e_o, rtol=0, atol=1e-8)
+
+
+def test_oras_sweeps_on_state_hook(rng):
+    """on_state(u, rn, sweeps) fires once before any sweep and once after each completed sweep
+    (solvers.py:418-419; reference test_solvers.py:259-264: history length = sweeps + 1)."""
+    w, h, bs, ov = 96, 64, 16, 2
+    m, k = oracle.seeded_problem(w, h, 0.08, 5)
+    b = np.where(m, k[0], 0.0)
+    part = bp.build_partition(w, h, bs, ov)
+    blocks = bp.BlockSolver(m, 1.0, part, bp.build_weights(part), 0.5)
+    op = bp.StencilOperator(m, 1.0)
+    u_a, u_b = b.copy(), b.copy()
+    seen = []
+    s_a, rn_a = bp.oras_sweeps(op, blocks, b, u_a, max_sweeps=6, stop_norm=0.0, eta=1e-5, local_max_iters=None,
+                               on_state=lambda uu, rn, it: seen.append((uu.copy(), rn, it)))
+    s_b, rn_b = bp.oras_sweeps(op, blocks, b, u_b, max_sweeps=6, stop_norm=0.0, eta=1e-5, local_max_iters=None)
+    assert s_a == s_b == 6 and len(seen) == s_a + 1
+    assert [it for _, _, it in seen] == list(range(7))
+    assert rn_a == rn_b == seen[-1][1] and np.array_equal(u_a, u_b) and np.array_equal(seen[-1][0], u_a)
+    assert np.array_equal(seen[0][0], b) and seen[0][1] > seen[-1][1]
+    s_o, rn_o = oracle.oras_sweeps(m, 1.0, bs, ov, 0.5, b, b.copy(), max_sweeps=6, stop_norm=0.0, eta=1e-5)
+    assert rn_a == pytest.approx(rn_o, rel=1e-7)
+    # stop_norm exit: the hook sees the evaluation that stops the loop
+    seen.clear()
+    u_c = b.copy()
+    s_c, rn_c = bp.oras_sweeps(op, blocks, b, u_c, max_sweeps=50, stop_norm=seen_stop(rn_b), eta=1e-5,
+                               local_max_iters=None, on_state=lambda uu, rn, it: seen.append((None, rn, it)))
+    assert len(seen) == s_c + 1 and seen[-1][1] == rn_c <= seen_stop(rn_b) < seen[-2][1]
+
+
+def seen_stop(rn):
+    return 1.5 * rn
