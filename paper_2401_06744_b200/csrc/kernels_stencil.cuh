@@ -394,7 +394,7 @@ prolongate_kernel(const double *__restrict__ c, const uint8_t *__restrict__ fmas
         rowR[k] = 0.75 * mid + 0.25 * row[Xp];  // fine x odd : far = near + 1
     }
     const int y0 = 2 * Y, x0 = 2 * X;
-    if ((w & 1) == 0 && ((uintptr_t)up & 15) == 0) {
+    if ((w & 1) == 0 && ((uintptr_t)up & 15) == 0 && ((uintptr_t)fm & 1) == 0) {
         // even width: the two fine pixels of a row are one 16-byte store (and one 2-byte mask load)
 #pragma unroll
         for (int dy = 0; dy < 2; ++dy) {
@@ -490,7 +490,7 @@ downsample_values_kernel(const uint8_t *__restrict__ fmask, const uint8_t *__res
     // w is even), so the dependent chain is masks -> neighbours / values
     const uint8_t cmk = cm[ci];
     bool fmk[4] = {false, false, false, false};
-    if ((w & 1) == 0) {
+    if ((w & 1) == 0 && ((uintptr_t)fm & 1) == 0) {
         const uchar2 a = *reinterpret_cast<const uchar2 *>(fm + (size_t)(2 * Y) * w + 2 * X);
         fmk[0] = a.x != 0; fmk[1] = a.y != 0;
         if (2 * Y + 1 < h) {
