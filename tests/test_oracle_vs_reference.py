@@ -231,3 +231,22 @@ def test_cg_smoothed_pipelines(diffpaint, w, h, d, s, bs, ov, mode, kw):
     assert (ro.iterations, ro.converged) == (rep.iterations, rep.converged)
     np.testing.assert_allclose(ro.history, rep.history, rtol=1e-6)
     np.testing.assert_allclose(uo, u, rtol=0, atol=1e-9)
+
+
+def test_ill_conditioned_regime_agrees_to_the_north_star_bar(diffpaint):
+    """Weak Robin coupling (alpha * h = 0.1), small thinly overlapping blocks, tol 1e-5: the outcome of
+    the near-threshold local-CG stop decisions depends on the summation order of the dot products, so the
+    NumPy reference and the C restatement agree to the north star's bar (max-abs 1e-3, same cycle count),
+    not to 1e-9 -- measured: 2.8e-3 relative in the final residual, 2.2e-4 in the field.  The GPU parity
+    tests use the same bar in this regime (tests/test_gpu_solve.py)."""
+    w, h, bs, ov = 132, 104, 10, 3
+    m, k = oracle.seeded_problem(w, h, 0.01, 685)
+    kw = dict(tol_rel=1e-5, alpha=0.2)
+    mkw = dict(nu_pre=1, nu_post=2, value_downsampling="modified")
+    ref_o, rep_o = oracle.solve_image(m, k, 0.5, oracle.MultigridConfig(
+        block_size=bs, overlap=ov, solver=oracle.SolverConfig(**kw), **mkw))
+    res = diffpaint.solve_image(diffpaint.InpaintingProblem(m, k, 0.5), "mg-oras", diffpaint.MultigridConfig(
+        block_size=bs, overlap=ov, solver=diffpaint.SolverConfig(**kw), **mkw))
+    assert rep_o[0].iterations == res.reports[0].iterations and rep_o[0].converged
+    assert rep_o[0].final_rel_residual == pytest.approx(res.reports[0].final_rel_residual, rel=0.05)
+    assert np.abs(ref_o - res.fields).max() <= 1e-3
