@@ -87,18 +87,21 @@ def test_whole_path_vs_reference_vectors(gold, meta, name):
     assert np.abs(res.fields - gold[f"{name}_fields"]).max() <= 1e-7
 
 
-def test_1080p_anchor_vs_reference_vectors():
-    """BASELINE configs[1]: V-cycles, final residuals and a strided sample of the REFERENCE's field."""
+@pytest.mark.parametrize("name,bs,ov", [("1080p_4pct_16_2", 16, 2), ("4k_2pct_32_6", 32, 6), ("4k_0.5pct_32_6", 32, 6)])
+def test_full_size_anchors_vs_reference_vectors(name, bs, ov):
+    """BASELINE configs[1..3] at FULL size: V-cycles, final residuals and a strided sample of the field the
+    REFERENCE produced (tests/golden/anchors*.{json,npz}); max-abs bar 1e-3, measured ~1e-9."""
     with open(os.path.join(G, "anchors.json")) as f:
-        a = json.load(f)["1080p_4pct_16_2"]
+        a = json.load(f)[name]
     sample = np.load(os.path.join(G, "anchors_sample.npz"))
     m, k = synthetic.seeded_problem(a["w"], a["h"], a["density"], 0, a["channels"])
-    res = bp.solve_image(bp.InpaintingProblem(m, k), "mg-oras", bp.MultigridConfig(block_size=16, overlap=2))
+    res = bp.solve_image(bp.InpaintingProblem(m, k), "mg-oras", bp.MultigridConfig(block_size=bs, overlap=ov))
     for r, g in zip(res.reports, a["reports"]):
         assert r.iterations == g["iterations"]
         assert r.final_rel_residual == pytest.approx(g["final_rel"], rel=1e-6)
     got = res.fields.reshape(a["channels"], -1)[:, ::997]
-    assert np.abs(got - sample["1080p_4pct_16_2"]).max() <= 1e-6
+    assert got.shape == sample[name].shape
+    assert np.abs(got - sample[name]).max() <= 1e-6
 
 
 @pytest.mark.parametrize("solver", ["ml-oras", "oras", "mg-cg", "ml-cg", "cg"])
