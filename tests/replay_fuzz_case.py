@@ -1,6 +1,7 @@
-"""Probe: replay one case of test_randomised_shapes_and_configs_match_oracle and print both histories."""
+"""Test helper (not collected): replays one case of test_randomised_shapes_and_configs_match_oracle
+(python tests/replay_fuzz_case.py SEED CASE) and prints the histories of the oracle and of the CUDA path."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import oracle
 import paper_2401_06744_b200 as bp
