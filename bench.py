@@ -221,6 +221,71 @@ def run_strip(args, rank, world, local):
         dist.destroy_process_group()
 
 
+def _free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args, argv):
+    """`python bench.py --gpus N` without torchrun: start N ranks (one per GPU) ourselves by
+    re-executing this file under torch.distributed.run on 127.0.0.1 and pass its exit code on.
+    Refuses loudly when the box has fewer than N devices (no silent N = 1 run)."""
+    if not args.dry_launch and args.impl == "b200":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} requested but only {have} CUDA device(s) are "
+                             f"visible; refusing to report n_gpus={args.gpus} from fewer ranks")
+    env = dict(os.environ)
+    if not args.dry_launch:
+        # the communicator line ("... nranks N ...") of every rank goes to stderr, stdout keeps the JSON line
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", str(max(1, (os.cpu_count() or 1) // args.gpus)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + argv
+    return subprocess.run(cmd, env=env).returncode
+
+
+def run_dry_launch(args, rank, world):
+    """--dry-launch: the N-rank launcher / barrier / report-gather logic on CPU (gloo), no kernels.
+    Every rank reports which global frames it would decode; rank 0 checks that exactly `world`
+    distinct ranks answered and that the frames partition the batch, then prints the JSON line."""
+    import torch
+    import torch.distributed as dist
+    from paper_2401_06744_b200.sharding import frames_of_rank
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    if world > 1:
+        dist.init_process_group("gloo")
+    F = args.frames
+    mine = frames_of_rank(world * F, rank, world)
+    t = torch.tensor([1.0 + rank], dtype=torch.float64)
+    bucket = [None] * world
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_gather_object(bucket, (rank, os.getpid(), mine))
+    else:
+        bucket = [(rank, os.getpid(), mine)]
+    if rank == 0:
+        ranks = sorted(b[0] for b in bucket)
+        pids = {b[1] for b in bucket}
+        frames = sorted(f for b in bucket for f in b[2])
+        if ranks != list(range(world)) or len(pids) != world or frames != list(range(world * F)):
+            raise SystemExit(f"bench.py: launcher check failed: ranks {ranks}, {len(pids)} processes")
+        if world != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but {world} rank(s) ran")
+        print(json.dumps({"dry_launch": True, "n_gpus": world, "ranks": ranks, "processes": len(pids),
+                          "max_over_ranks": float(t.item()), "frames_per_rank": F,
+                          "frames": len(frames)}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -240,18 +305,30 @@ def main():
                     help="--strip exchange: torch.distributed NCCL, or CUDA-IPC peer memory + gloo control")
     ap.add_argument("--strip-levels", type=int, default=2,
                     help="how many of the finest levels are striped in --strip mode (the rest is replicated)")
+    ap.add_argument("--dry-launch", action="store_true",
+                    help="exercise the N-rank launcher and the report gather on CPU (gloo), no kernels")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     # the CPU arm costs seconds per step: bound the run to a few minutes
     args.steps_ref = max(1, min(args.steps, 5))
     args.warmup_ref = max(0, min(args.warmup, 1))
 
+    if args.gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "b200":
+        # no torchrun around us: start the N ranks ourselves (one process per GPU)
+        sys.exit(self_launch(args, sys.argv[1:]))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: refusing to report "
+                         f"n_gpus={args.gpus} from {world} rank(s)")
+    if args.dry_launch:
+        run_dry_launch(args, rank, world)
         return
 
     import torch
@@ -262,10 +339,20 @@ def main():
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device (the CUDA path has no CPU fallback)")
+    if local >= torch.cuda.device_count():
+        raise SystemExit(f"bench.py: rank {rank} has no device (LOCAL_RANK {local}, "
+                         f"{torch.cuda.device_count()} visible)")
     torch.cuda.set_device(local)
+    devices_seen = [str(torch.cuda.get_device_properties(local).uuid)]
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        bucket = [None] * world
+        dist.all_gather_object(bucket, (rank, devices_seen[0]))
+        devices_seen = sorted({d for _, d in bucket})
+        if sorted(r for r, _ in bucket) != list(range(world)) or len(devices_seen) != world:
+            raise SystemExit(f"bench.py: {world} ranks on {len(devices_seen)} distinct GPU(s); "
+                             "one process per GPU is required")
 
     if args.strip:
         run_strip(args, rank, world, local)
@@ -475,7 +562,8 @@ def main():
                    "channels": C, "mask_density": density, "block_size": bs, "overlap": ov, "tol_rel": 1e-3,
                    "v_cycles": cycles[:C], "l2_policy": "inputs larger than L2 (%.0f MB resident per step)"
                    % ((d_known.numel() * 8 * 2 + d_mask.numel()) / 1e6),
-                   "parallelism": f"frames sharded over {world} GPU(s), no data-path collective"},
+                   "parallelism": f"frames sharded over {world} GPU(s), no data-path collective",
+                   "ranks": world, "distinct_gpus": len(devices_seen)},
         "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
         "roofline": roofline, "frame_roofline": frame_roof, "kernels": kernels,
         "cpu_baseline": cpu, "parity": parity,

@@ -24,6 +24,7 @@
 #include "kernels_rows.cuh"
 #include "kernels_oras.cuh"
 #include "kernels_oras_tma.cuh"
+#include "kernels_oras_warp.cuh"
 #include "kernels_cg.cuh"
 
 using namespace b200p;
@@ -164,6 +165,7 @@ struct LevelHost {
     double *d_rc = nullptr;     // (P,h,w) restricted residual (levels >= 1)
     int tile = 0;               // K2 variant: 0 generic, else see launch_sweep
     unsigned *d_mtab = nullptr; // K2T: packed block-local masks (F, nblocks, 64); null = level not eligible
+    unsigned *d_mtabw = nullptr; // K2W: the same for the warp-per-block layout (F, nblocks, 32)
     // combine on arrival (FUSE variant of the lean kernel): cell tables and arrival counters
     const int *d_cell_need = nullptr, *d_lastx = nullptr, *d_lasty = nullptr;
     unsigned *d_cell_cnt = nullptr;
@@ -586,7 +588,8 @@ static int local_cap(const b200p_plan *pl, const LevelHost &L) {
 
 // Tile variants of K2 (block extent -> <TW,TH,NWARP>).
 enum { TILE_GENERIC = 0, TILE_32_A = 1, TILE_16 = 2, TILE_8 = 3, TILE_32_B = 4, TILE_32_C = 5,
-       TILE_32_S = 6, TILE_32_T = 7, TILE_32_U = 8, TILE_32_TMA = 9, TILE_32_L = 10 };
+       TILE_32_S = 6, TILE_32_T = 7, TILE_32_U = 8, TILE_32_TMA = 9, TILE_32_L = 10, TILE_32_W = 11,
+       TILE_32_WQ = 12 };
 
 static int tile_for(int bw, int bh) {
     if (bw == 32 && bh == 32) {
@@ -598,7 +601,9 @@ static int tile_for(int bw, int bh) {
         if (e && *e == 'U') return TILE_32_U;
         if (e && *e == 'M') return TILE_32_TMA;
         if (e && *e == 'B') return TILE_32_B;
-        return TILE_32_L;  // lean prologue + packed reduction; falls back to B where not eligible
+        if (e && *e == 'L') return TILE_32_L;  // two-warp register tile with the lean prologue
+        if (e && *e == 'Q') return TILE_32_WQ; // warp per block, v and q in tensor memory
+        return TILE_32_W;  // warp per block, v in tensor memory; falls back to B where not eligible
     }
     if (bw == 16 && bh == 16) return TILE_16;
     if (bw == 8 && bh == 8) return TILE_8;
@@ -786,6 +791,23 @@ static int launch_sweep_tma(b200p_plan *pl, const LevelHost &L, const SweepArgs 
     return 0;
 }
 
+// K2W is persistent: resident CTAs per SM (register-limited) x SMs.
+static int warp_sweep_grid() {
+    static int grid = 0;
+    if (!grid) {
+        int occ = 0, sms = 148, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, oras_sweep_warp_kernel<true, false>, KW_THREADS, 0) !=
+                cudaSuccess || occ < 2)
+            occ = 2;  // 2 x 128 threads x 256 registers = the whole register file (the query reports 1)
+        const char *e = getenv("B200P_KW_CTAS");
+        if (e && atoi(e) > 0) occ = atoi(e);
+        grid = sms * occ;
+    }
+    return grid;
+}
+
 // K2 + K2b: one ORAS sweep (in place on u.cur) using rs/mflag from the preceding K1.
 static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, UBuf &ub, const double *b, bool rm,
                               const int *pred, int *unit_counter, int tile, cudaStream_t st) {
@@ -794,13 +816,33 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, UBuf &ub, cons
     fill_sweep_args(pl, L, u, b, pred, A);
     A.iy0 = L.iy_lo;
     dim3 grid(L.nblocks, pl->P);
-    if (striped(pl, L) && !(tile == TILE_32_L && tma_eligible(L, u, b, rm)))
+    if (striped(pl, L) && !((tile == TILE_32_L || tile == TILE_32_W || tile == TILE_32_WQ) && tma_eligible(L, u, b, rm)))
         return fail_arg(B200P_ERR_UNSUPPORTED, "strip mode needs the 32x32 lean block-solve kernel");
     {
         // read u (+ b) + mask, write the weighted correction tiles
         LaunchScope sc(pl, st, KK_SWEEP_SPLIT, field_bytes(pl, L, rm ? 2.0 : 3.0, 1.0));
-        if ((tile == TILE_32_TMA || tile == TILE_32_L) && !tma_eligible(L, u, b, rm)) tile = TILE_32_B;
+        if ((tile == TILE_32_TMA || tile == TILE_32_L || tile == TILE_32_W || tile == TILE_32_WQ) &&
+            !tma_eligible(L, u, b, rm))
+            tile = TILE_32_B;
         switch (tile) {
+            case TILE_32_W:
+            case TILE_32_WQ: {
+                WarpSweepArgs WA;
+                WA.S = A;
+                WA.mtab = L.d_mtabw;
+                WA.nrows = L.iy_hi - L.iy_lo;  // strip mode: only the block rows of this rank
+                WA.items_per_problem = WA.nrows * L.info.nx;
+                WA.total = pl->P * WA.items_per_problem;
+                const int g = std::min((WA.total + KW_WARPS - 1) / KW_WARPS, warp_sweep_grid());
+                if (tile == TILE_32_W) {
+                    if (rm) oras_sweep_warp_kernel<true, false><<<g, KW_THREADS, 0, st>>>(WA);
+                    else oras_sweep_warp_kernel<false, false><<<g, KW_THREADS, 0, st>>>(WA);
+                } else {
+                    if (rm) oras_sweep_warp_kernel<true, true><<<g, KW_THREADS, 0, st>>>(WA);
+                    else oras_sweep_warp_kernel<false, true><<<g, KW_THREADS, 0, st>>>(WA);
+                }
+                break;
+            }
             case TILE_32_L: {
                 static const int cap = getenv("B200P_REGCAP") ? atoi(getenv("B200P_REGCAP")) : 168;
                 dim3 g3(L.info.nx, L.iy_hi - L.iy_lo, pl->P);  // strip mode: only the block rows of this rank
@@ -955,6 +997,9 @@ static int pack_masks(b200p_plan *pl, const LevelHost &L, cudaStream_t st) {
     LaunchScope sc(pl, st, KK_DOWN_MASK, (double)pl->F * L.nblocks * (32.0 * 32.0 + 4.0 * KT_THREADS));
     pack_block_masks_kernel<<<dim3(L.nblocks, pl->F), KT_THREADS, 0, st>>>(
         L.dev, L.d_mask, (size_t)L.info.height * L.info.width, L.d_mtab, 0);
+    CU(cudaGetLastError());
+    pack_block_masks_warp_kernel<<<dim3((L.nblocks + KW_WARPS - 1) / KW_WARPS, pl->F), KW_THREADS, 0, st>>>(
+        L.dev, L.d_mask, (size_t)L.info.height * L.info.width, L.d_mtabw);
     CU(cudaGetLastError());
     return 0;
 }
@@ -1839,7 +1884,10 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
         bool xs_even = true;
         for (int x : xs) xs_even = xs_even && (x % 2 == 0);
         if (D.bw == 32 && D.bh == 32 && w % 2 == 0 && xs_even)
+        {
             PTRY(dev_alloc(pl, &L.d_mtab, (size_t)pl->F * L.nblocks * KT_THREADS));
+            PTRY(dev_alloc(pl, &L.d_mtabw, (size_t)pl->F * L.nblocks * 32));
+        }
         if (L.d_mtab && L.nblocks > 1 && arrival_fusion_enabled()) {
             // cells = rectangles between consecutive block starts; a block overlaps the cells from its own
             // index to the last one starting inside its extent
@@ -2605,7 +2653,8 @@ int b200p_plan_oras_sweeps(b200p_plan *pl, int level, const double *d_b, double 
     } else if (path >= 10) {
         const int t = path - 10;
         const bool ok = (is32 && (t == TILE_32_A || t == TILE_32_B || t == TILE_32_C || t == TILE_32_S ||
-                                 t == TILE_32_T || t == TILE_32_U || t == TILE_32_TMA || t == TILE_32_L)) ||
+                                 t == TILE_32_T || t == TILE_32_U || t == TILE_32_TMA || t == TILE_32_L ||
+                                 t == TILE_32_W || t == TILE_32_WQ)) ||
                         (is16 && t == TILE_16) || (is8 && t == TILE_8);
         if (!ok) return fail_arg(B200P_ERR_UNSUPPORTED, "level %d is not eligible for tile variant %d", level, t);
         force = t;

@@ -1,0 +1,505 @@
+// kernels_oras_warp.cuh -- K2W: the 32x32 ORAS block solve with ONE WARP per block and the
+// write-mostly part of the CG state in TENSOR MEMORY.
+//
+// Why (measured on a B200, scripts/probe/fp64_probe.cu, tmem_probe.cu, profiles/oras_sweep_lean_r1.txt):
+//   * DFMA/DADD issue once per 2.03 cycles per SM sub-partition; a 64-bit shuffle is two SHFL
+//     instructions on a pipe that accepts ONE warp instruction per cycle per SM (shared with LDS/STS).
+//     The two-warp register tile of K2L (4x4 pixels per thread) needs ~150 of those per block CG step
+//     (halo exchange, two butterflies' worth of reduction, the cross-warp row pair and bar.sync)
+//     against ~200 SM cycles of FP64 issue: both pipes sit at 40-50 % because a block's warps spend
+//     most of a step in dependent exchange / reduction chains and only 12 warps fit per SM.
+//   * A warp that owns the whole block (8x4 pixels per thread) halves the halo per pixel, needs no
+//     cross-warp exchange, no bar.sync, no shared memory in the CG loop and one butterfly per 1024
+//     pixels: ~66 SHFL per block step.  Its state (v, r, p, q = 4 x 32 doubles per thread) does not
+//     fit 255 registers, so the iterate v -- touched once per CG step, never exchanged -- lives in
+//     tensor memory: a thread's 32 doubles are 64 TMEM columns of its own lane, moved with
+//     tcgen05.ld / tcgen05.st .32x32b (measured ~200 B/clk/SM each way next to the LSU pipe, which
+//     they do not use).  QT additionally parks q = A_i p there between the dot products and the
+//     residual update.
+//
+// A CTA is KW_WARPS independent warps (TMEM lane quarter = warp index) that walk the
+// (problem, block) items of the launch persistently; TMEM is allocated once per CTA.
+// Semantics are those of tile_block_solve / oras_sweep_lean_kernel (solvers.py:303-305 gather,
+// :328-370 _solve_range, :309-310 scatter weights); the weighted tile goes to the same scratch
+// layout, K2b is unchanged.
+// Requires: block 32x32, even level width, even block starts, 16-byte aligned u / b.
+#pragma once
+#include "kernels_oras.cuh"
+
+namespace b200p {
+
+constexpr int KW_WARPS = 4;
+constexpr int KW_THREADS = KW_WARPS * 32;
+
+struct WarpSweepArgs {
+    SweepArgs S;
+    const unsigned *mtab;  // (F, nblocks, 32): bit j*8+i of word `lane` = mask of that lane's pixel (i, j)
+    int nrows;             // block rows of this launch (strip mode: S.iy0 .. S.iy0 + nrows)
+    int items_per_problem; // nrows * nx
+    int total;             // P * items_per_problem
+};
+
+// Packs the block-local masks for K2W: grid (ceil(nblocks / 4), F), 128 threads, a warp per block.
+__global__ void __launch_bounds__(KW_THREADS)
+pack_block_masks_warp_kernel(const LevelDev L, const uint8_t *__restrict__ mask, size_t plane,
+                             unsigned *__restrict__ mtab) {
+    const int blk = blockIdx.x * KW_WARPS + (threadIdx.x >> 5), f = blockIdx.y, lane = threadIdx.x & 31;
+    if (blk >= L.nblocks) return;
+    const int iy = blk / L.nx, ix = blk - iy * L.nx;
+    const int gx0 = L.xs[ix] + (lane & 3) * 8, gy0 = L.ys[iy] + (lane >> 2) * 4;
+    const uint8_t *mp = mask + (size_t)f * plane;
+    unsigned bits = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (mp[(size_t)(gy0 + j) * L.w + gx0 + i]) bits |= 1u << (j * 8 + i);
+    mtab[((size_t)f * L.nblocks + blk) * 32 + lane] = bits;
+}
+
+// ---- tensor memory as a per-thread scratch: 8 doubles = 16 columns of the thread's own lane
+__device__ __forceinline__ void tm_st8(uint32_t taddr, const double (&d)[8]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+        ::"r"(taddr),
+        "r"(__double2loint(d[0])), "r"(__double2hiint(d[0])), "r"(__double2loint(d[1])), "r"(__double2hiint(d[1])),
+        "r"(__double2loint(d[2])), "r"(__double2hiint(d[2])), "r"(__double2loint(d[3])), "r"(__double2hiint(d[3])),
+        "r"(__double2loint(d[4])), "r"(__double2hiint(d[4])), "r"(__double2loint(d[5])), "r"(__double2hiint(d[5])),
+        "r"(__double2loint(d[6])), "r"(__double2hiint(d[6])), "r"(__double2loint(d[7])), "r"(__double2hiint(d[7])));
+}
+struct TmRow {
+    int w[16];
+    __device__ __forceinline__ double get(int i) const { return __hiloint2double(w[2 * i + 1], w[2 * i]); }
+};
+__device__ __forceinline__ void tm_ld8(uint32_t taddr, TmRow &t) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(t.w[0]), "=r"(t.w[1]), "=r"(t.w[2]), "=r"(t.w[3]), "=r"(t.w[4]), "=r"(t.w[5]), "=r"(t.w[6]), "=r"(t.w[7]),
+          "=r"(t.w[8]), "=r"(t.w[9]), "=r"(t.w[10]), "=r"(t.w[11]), "=r"(t.w[12]), "=r"(t.w[13]), "=r"(t.w[14]),
+          "=r"(t.w[15])
+        : "r"(taddr));
+}
+// tcgen05.wait::ld, tied to the registers of the loads it completes so that no consumer can be
+// scheduled above it.
+__device__ __forceinline__ void tm_wait_ld(TmRow &t) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(t.w[0]), "+r"(t.w[1]), "+r"(t.w[2]), "+r"(t.w[3]), "+r"(t.w[4]), "+r"(t.w[5]), "+r"(t.w[6]),
+                   "+r"(t.w[7]), "+r"(t.w[8]), "+r"(t.w[9]), "+r"(t.w[10]), "+r"(t.w[11]), "+r"(t.w[12]),
+                   "+r"(t.w[13]), "+r"(t.w[14]), "+r"(t.w[15]));
+}
+__device__ __forceinline__ void tm_wait_ld2(TmRow &a, TmRow &b) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(a.w[0]), "+r"(a.w[1]), "+r"(a.w[2]), "+r"(a.w[3]), "+r"(a.w[4]), "+r"(a.w[5]), "+r"(a.w[6]),
+                   "+r"(a.w[7]), "+r"(a.w[8]), "+r"(a.w[9]), "+r"(a.w[10]), "+r"(a.w[11]), "+r"(a.w[12]),
+                   "+r"(a.w[13]), "+r"(a.w[14]), "+r"(a.w[15]), "+r"(b.w[0]), "+r"(b.w[1]), "+r"(b.w[2]),
+                   "+r"(b.w[3]), "+r"(b.w[4]), "+r"(b.w[5]), "+r"(b.w[6]), "+r"(b.w[7]), "+r"(b.w[8]), "+r"(b.w[9]),
+                   "+r"(b.w[10]), "+r"(b.w[11]), "+r"(b.w[12]), "+r"(b.w[13]), "+r"(b.w[14]), "+r"(b.w[15]));
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// q = (mbits bit K) ? 0 : q as "test bit into a predicate, zero under the predicate" (2 instructions
+// per pixel; the select form costs a bit test and two FSELs, and ptxas tends to hoist and re-pack
+// the 32 predicates of a tile into a register every CG step).
+template <int K>
+__device__ __forceinline__ void mask_zero(double &q, unsigned mbits) {
+    asm("{\n\t.reg .pred z;\n\t.reg .b32 t;\n\tand.b32 t, %1, %2;\n\tsetp.ne.u32 z, t, 0;\n\t"
+        "@z mov.f64 %0, 0d0000000000000000;\n\t}"
+        : "+d"(q)
+        : "r"(mbits), "n"(1u << K));
+}
+// h = flag ? g * p : h as one predicated DMUL (ghost value of a cut block side)
+__device__ __forceinline__ void ghost_mul(double &h, double g, double p, unsigned flag) {
+    asm("{\n\t.reg .pred e;\n\tsetp.ne.u32 e, %3, 0;\n\t@e mul.f64 %0, %1, %2;\n\t}"
+        : "+d"(h)
+        : "d"(g), "d"(p), "r"(flag));
+}
+
+// One warp, 32x32 block, lane (lx = lane & 3, ly = lane >> 2) owns the 8 x 4 pixels at (8 lx, 4 ly).
+struct WarpCG {
+    static constexpr int TW = 8, TH = 4;
+    int lane;
+    unsigned eL, eR, eT, eB;  // tile touches the block's left / right / top / bottom side
+    double gL, gR, gT, gB;  // ghost factors of those sides (1 on the image border, 1 - alpha*h inside)
+    unsigned mbits;
+
+    // q' = 4 p - neighbours (scaled local Robin operator, solvers.py:316-326), 0 at mask pixels;
+    // rows are handed to `sink(j, qrow)` as they are produced.
+    template <class Sink>
+    __device__ __forceinline__ void apply(const double (&pc)[TH][TW], Sink sink) const {
+        double hT[TW], hB[TW];
+#pragma unroll
+        for (int i = 0; i < TW; ++i) {
+            hT[i] = __shfl_up_sync(FULL_MASK, pc[TH - 1][i], 4);
+            hB[i] = __shfl_down_sync(FULL_MASK, pc[0][i], 4);
+        }
+#pragma unroll
+        for (int i = 0; i < TW; ++i) {
+            ghost_mul(hT[i], gT, pc[0][i], eT);
+            ghost_mul(hB[i], gB, pc[TH - 1][i], eB);
+        }
+        apply_row<0>(pc, hT, hB, sink);
+        apply_row<1>(pc, hT, hB, sink);
+        apply_row<2>(pc, hT, hB, sink);
+        apply_row<3>(pc, hT, hB, sink);
+    }
+
+    template <int J, class Sink>
+    __device__ __forceinline__ void apply_row(const double (&pc)[TH][TW], const double (&hT)[TW],
+                                              const double (&hB)[TW], Sink &sink) const {
+        double hl = __shfl_up_sync(FULL_MASK, pc[J][TW - 1], 1);
+        double hr = __shfl_down_sync(FULL_MASK, pc[J][0], 1);
+        ghost_mul(hl, gL, pc[J][0], eL);
+        ghost_mul(hr, gR, pc[J][TW - 1], eR);
+        double qrow[TW];
+#define B200P_KW_PX(I)                                                          \
+        {                                                                       \
+            const double up = J == 0 ? hT[I] : pc[J == 0 ? 0 : J - 1][I];       \
+            const double dn = J == TH - 1 ? hB[I] : pc[J == TH - 1 ? J : J + 1][I]; \
+            const double lf = I == 0 ? hl : pc[J][I == 0 ? 0 : I - 1];          \
+            const double rt = I == TW - 1 ? hr : pc[J][I == TW - 1 ? I : I + 1]; \
+            const double s = ((up + dn) + lf) + rt;                             \
+            qrow[I] = fma(4.0, pc[J][I], -s);                                   \
+            mask_zero<J * TW + I>(qrow[I], mbits);                              \
+        }
+        B200P_KW_PX(0) B200P_KW_PX(1) B200P_KW_PX(2) B200P_KW_PX(3)
+        B200P_KW_PX(4) B200P_KW_PX(5) B200P_KW_PX(6) B200P_KW_PX(7)
+#undef B200P_KW_PX
+        sink(J, qrow);
+    }
+};
+
+// Three warp sums in one packed butterfly (6 exchanges + 3 broadcasts), fixed summation order.
+__device__ __forceinline__ void warp_sum3(int lane, double &a, double &b, double &c) {
+    const bool hi = lane & 16;
+    const double send = hi ? a : b;
+    double keep = hi ? b : a;
+    keep += __shfl_xor_sync(FULL_MASK, send, 16);
+    c += __shfl_xor_sync(FULL_MASK, c, 16);
+    const bool h8 = lane & 8;
+    const double send2 = h8 ? keep : c;
+    double w = h8 ? c : keep;
+    w += __shfl_xor_sync(FULL_MASK, send2, 8);
+    w += __shfl_xor_sync(FULL_MASK, w, 4);
+    w += __shfl_xor_sync(FULL_MASK, w, 2);
+    w += __shfl_xor_sync(FULL_MASK, w, 1);
+    a = __shfl_sync(FULL_MASK, w, 0);
+    b = __shfl_sync(FULL_MASK, w, 16);
+    c = __shfl_sync(FULL_MASK, w, 8);
+}
+
+struct WarpSmem {
+    alignas(16) double wx[KW_WARPS][32];
+    alignas(16) double wy[KW_WARPS][32];
+    uint32_t tm_base;
+};
+
+template <bool RM, bool QT>
+__global__ void __launch_bounds__(KW_THREADS, 2)
+oras_sweep_warp_kernel(const WarpSweepArgs A) {
+    constexpr int TW = 8, TH = 4, BW = 32, BH = 32;
+    constexpr int NCOL = QT ? 128 : 64;  // TMEM columns per CTA: v (64) [+ q (64)] per lane
+    __shared__ WarpSmem sm;
+    const SweepArgs &S = A.S;
+    const LevelDev &L = S.L;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (warp == 0) {
+        const uint32_t slot = (uint32_t)__cvta_generic_to_shared(&sm.tm_base);
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(slot), "r"(NCOL) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tv = sm.tm_base + ((uint32_t)(warp * 32) << 16);  // this warp's lane quarter
+    const uint32_t tq = tv + 64;
+
+    const int W = L.w, H = L.h;
+    const double hinv2 = L.hinv2, g_in = L.g_in;
+    const int lx = lane & 3, ly = lane >> 2;
+    const int bx = lx * TW, by = ly * TH;
+    double *swx = sm.wx[warp], *swy = sm.wy[warp];
+
+    for (int item = blockIdx.x * KW_WARPS + warp; item < A.total; item += gridDim.x * KW_WARPS) {
+        const int p = item / A.items_per_problem;
+        const int rem = item - p * A.items_per_problem;
+        const int iyl = rem / L.nx, ix = rem - iyl * L.nx, iy = iyl + S.iy0;
+        const int blk = iy * L.nx + ix;
+        if (S.pred && !S.pred[p]) continue;
+        const double rs_g = S.rs[p];
+        if (rs_g == 0.0) continue;  // oras_sweeps' rs == 0 exit (solvers.py:420)
+        const int frame = S.channels == 3 ? p / 3 : (S.channels == 1 ? p : p / S.channels);
+        const unsigned mbits = A.mtab[((size_t)frame * L.nblocks + blk) * 32 + lane];
+        __syncwarp();  // the previous item's weight rows have been consumed
+        swx[lane] = L.wx[ix * BW + lane];
+        swy[lane] = L.wy[iy * BH + lane];
+        const int x0 = L.xs[ix], y0 = L.ys[iy];
+        const double target = S.eta * rs_g;
+        const bool general = S.mflag[p] != 0;
+
+        WarpCG cg;
+        cg.lane = lane;
+        cg.eL = lx == 0 ? 1u : 0u;
+        cg.eR = lx == 3 ? 1u : 0u;
+        cg.eT = ly == 0 ? 1u : 0u;
+        cg.eB = ly == 7 ? 1u : 0u;
+        cg.gL = x0 > 0 ? g_in : 1.0;
+        cg.gR = x0 + BW < W ? g_in : 1.0;
+        cg.gT = y0 > 0 ? g_in : 1.0;
+        cg.gB = y0 + BH < H ? g_in : 1.0;
+        cg.mbits = mbits;
+
+        const int gx0 = x0 + bx, gy0 = y0 + by;
+        const bool border = x0 == 0 || y0 == 0 || x0 + BW >= W || y0 + BH >= H;  // warp-uniform
+
+        // ---- gather: global residual g = b - A u on the tile (core.py:100-110)
+        double r[TH][TW];
+        {
+            const double *urow = S.u + (size_t)p * S.plane + (size_t)(gy0 - 1) * W + gx0;
+            double uc[TH + 2][TW + 2];
+            if (!border) {
+#pragma unroll
+                for (int j = 0; j < TH + 2; ++j) {
+                    const double *rp = urow + (size_t)j * W;
+#pragma unroll
+                    for (int k = 0; k < TW / 2; ++k) {
+                        const double2 a = *reinterpret_cast<const double2 *>(rp + 2 * k);
+                        uc[j][1 + 2 * k] = a.x;
+                        uc[j][2 + 2 * k] = a.y;
+                    }
+                    if (j >= 1 && j <= TH) {
+                        uc[j][0] = rp[-1];
+                        uc[j][TW + 1] = rp[TW];
+                    } else {
+                        uc[j][0] = uc[j][TW + 1] = 0.0;
+                    }
+                }
+            } else {
+                const bool hasL = gx0 > 0, hasR = gx0 + TW < W, hasT = gy0 > 0, hasB = gy0 + TH < H;
+#pragma unroll
+                for (int j = 0; j < TH + 2; ++j) {
+                    const double *rp = urow + (size_t)j * W;
+                    const bool rowin = (j > 0 || hasT) && (j < TH + 1 || hasB);
+#pragma unroll
+                    for (int k = 0; k < TW / 2; ++k) {
+                        double2 a = make_double2(0.0, 0.0);
+                        if (rowin) a = *reinterpret_cast<const double2 *>(rp + 2 * k);
+                        uc[j][1 + 2 * k] = a.x;
+                        uc[j][2 + 2 * k] = a.y;
+                    }
+                    uc[j][0] = uc[j][TW + 1] = 0.0;
+                    if (j >= 1 && j <= TH) {
+                        if (hasL) uc[j][0] = rp[-1];
+                        if (hasR) uc[j][TW + 1] = rp[TW];
+                    }
+                }
+            }
+            const double nc4 = -4.0 * hinv2;
+#pragma unroll
+            for (int j = 0; j < TH; ++j) {
+                double bt[TW];
+                if (!RM) {
+                    const double *bp = S.b + (size_t)p * S.plane + (size_t)(gy0 + j) * W + gx0;
+#pragma unroll
+                    for (int k = 0; k < TW / 2; ++k) {
+                        const double2 a = *reinterpret_cast<const double2 *>(bp + 2 * k);
+                        bt[2 * k] = a.x;
+                        bt[2 * k + 1] = a.y;
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < TW; ++i) {
+                    const double s = ((uc[j][i + 1] + uc[j + 2][i + 1]) + uc[j + 1][i]) + uc[j + 1][i + 2];
+                    const double uu = uc[j + 1][i + 1];
+                    const double res = fma(hinv2, s, RM ? nc4 * uu : fma(nc4, uu, bt[i]));
+                    const bool m = (mbits >> (j * TW + i)) & 1u;
+                    // RM: rhs = where(mask, known, 0) and b - u == 0 at mask pixels unless `general`
+                    r[j][i] = m ? (RM ? 0.0 : bt[i] - uu) : res;
+                }
+            }
+            if (border) {
+                // image border: fewer in-image neighbours (reflecting boundary, core.py:59-67)
+#pragma unroll
+                for (int j = 0; j < TH; ++j)
+#pragma unroll
+                    for (int i = 0; i < TW; ++i) {
+                        const int gy = gy0 + j, gx = gx0 + i;
+                        const double miss = (gy == 0 ? 1.0 : 0.0) + (gy == H - 1 ? 1.0 : 0.0) +
+                                            (gx == 0 ? 1.0 : 0.0) + (gx == W - 1 ? 1.0 : 0.0);
+                        const bool m = (mbits >> (j * TW + i)) & 1u;
+                        if (!m && miss != 0.0) r[j][i] = fma(miss * hinv2, uc[j + 1][i + 1], r[j][i]);
+                    }
+            }
+            if (RM && general) {
+#pragma unroll
+                for (int j = 0; j < TH; ++j)
+#pragma unroll
+                    for (int i = 0; i < TW; ++i)
+                        if ((mbits >> (j * TW + i)) & 1u)
+                            r[j][i] = S.b[(size_t)p * S.plane + (size_t)(gy0 + j) * W + gx0 + i] - uc[j + 1][i + 1];
+            }
+        }
+
+        // ---- local start: v0 = where(mask, g, 0) -> TMEM, r0 = g - A_i v0 (solvers.py:331-333)
+        double pc[TH][TW];
+        if (general) {
+#pragma unroll
+            for (int j = 0; j < TH; ++j) {
+#pragma unroll
+                for (int i = 0; i < TW; ++i) pc[j][i] = ((mbits >> (j * TW + i)) & 1u) ? r[j][i] : 0.0;
+                tm_st8(tv + 16 * j, pc[j]);
+            }
+            cg.apply(pc, [&](int j, const double (&qrow)[TW]) {
+#pragma unroll
+                for (int i = 0; i < TW; ++i) {
+                    const bool m = (mbits >> (j * TW + i)) & 1u;
+                    r[j][i] = m ? 0.0 : fma(-hinv2, qrow[i], r[j][i]);
+                }
+            });
+        } else {
+            const double z[TW] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int j = 0; j < TH; ++j) tm_st8(tv + 16 * j, z);
+        }
+        double rs_k;
+        {
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int j = 0; j < TH; ++j)
+#pragma unroll
+                for (int i = 0; i < TW; ++i) acc[i & 3] = fma(r[j][i], r[j][i], acc[i & 3]);
+            rs_k = warp_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
+        }
+        tm_wait_st();
+
+        if (rs_k > target) {  // solvers.py:336 (strict)
+#pragma unroll
+            for (int j = 0; j < TH; ++j)
+#pragma unroll
+                for (int i = 0; i < TW; ++i) pc[j][i] = r[j][i];
+            double inv_rs = __drcp_rn(rs_k);
+            for (int it = 0; it < S.max_iters; ++it) {
+                double d_pq0 = 0.0, d_pq1 = 0.0, d_rq0 = 0.0, d_rq1 = 0.0, d_qq0 = 0.0, d_qq1 = 0.0;
+                double q[QT ? 1 : TH][TW];
+                cg.apply(pc, [&](int j, const double (&qrow)[TW]) {
+#pragma unroll
+                    for (int i = 0; i < TW; i += 2) {
+                        d_pq0 = fma(pc[j][i], qrow[i], d_pq0);
+                        d_rq0 = fma(r[j][i], qrow[i], d_rq0);
+                        d_qq0 = fma(qrow[i], qrow[i], d_qq0);
+                        d_pq1 = fma(pc[j][i + 1], qrow[i + 1], d_pq1);
+                        d_rq1 = fma(r[j][i + 1], qrow[i + 1], d_rq1);
+                        d_qq1 = fma(qrow[i + 1], qrow[i + 1], d_qq1);
+                    }
+                    if (QT) {
+                        tm_st8(tq + 16 * j, qrow);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < TW; ++i) q[QT ? 0 : j][i] = qrow[i];
+                    }
+                });
+                double d_pq = d_pq0 + d_pq1, d_rq = d_rq0 + d_rq1, d_qq = d_qq0 + d_qq1;
+                warp_sum3(lane, d_pq, d_rq, d_qq);
+                const double pq = hinv2 * d_pq;
+                const bool ok = pq > 0.0;                               // solvers.py:348
+                const double a = ok ? rs_k * __drcp_rn(pq) : 0.0;       // :349-350
+                const double ah = a * hinv2;
+                const double rs_new = fma(ah * ah, d_qq, fma(-2.0 * ah, d_rq, rs_k));
+                const bool stop = rs_new <= target || !ok;              // :354
+                const double beta = rs_new * inv_rs;
+                if (QT) {
+                    tm_wait_st();
+#pragma unroll
+                    for (int j = 0; j < TH; ++j) {
+                        TmRow tvr, tqr;
+                        tm_ld8(tv + 16 * j, tvr);
+                        tm_ld8(tq + 16 * j, tqr);
+                        tm_wait_ld2(tvr, tqr);
+                        double vrow[TW];
+#pragma unroll
+                        for (int i = 0; i < TW; ++i) {
+                            vrow[i] = fma(a, pc[j][i], tvr.get(i));
+                            r[j][i] = fma(-ah, tqr.get(i), r[j][i]);
+                        }
+                        tm_st8(tv + 16 * j, vrow);
+                        if (!stop) {
+#pragma unroll
+                            for (int i = 0; i < TW; ++i) pc[j][i] = fma(beta, pc[j][i], r[j][i]);
+                        }
+                    }
+                } else {
+                    // residual first (q dies), then ONE batch of v loads into the freed registers
+#pragma unroll
+                    for (int j = 0; j < TH; ++j)
+#pragma unroll
+                        for (int i = 0; i < TW; ++i) r[j][i] = fma(-ah, q[QT ? 0 : j][i], r[j][i]);
+                    TmRow t0, t1, t2, t3;
+                    tm_ld8(tv, t0);
+                    tm_ld8(tv + 16, t1);
+                    tm_ld8(tv + 32, t2);
+                    tm_ld8(tv + 48, t3);
+                    tm_wait_ld2(t0, t1);
+                    tm_wait_ld2(t2, t3);
+                    double vrow[TW];
+#define B200P_KW_V(J, T)                                                                     \
+    {                                                                                        \
+        _Pragma("unroll") for (int i = 0; i < TW; ++i) vrow[i] = fma(a, pc[J][i], T.get(i)); \
+        tm_st8(tv + 16 * J, vrow);                                                           \
+    }
+                    B200P_KW_V(0, t0) B200P_KW_V(1, t1) B200P_KW_V(2, t2) B200P_KW_V(3, t3)
+#undef B200P_KW_V
+                    if (!stop) {
+#pragma unroll
+                        for (int j = 0; j < TH; ++j)
+#pragma unroll
+                            for (int i = 0; i < TW; ++i) pc[j][i] = fma(beta, pc[j][i], r[j][i]);
+                    }
+                }
+                tm_wait_st();
+                if (stop) break;
+                rs_k = rs_new;
+                inv_rs = __drcp_rn(rs_k);
+            }
+        }
+
+        // ---- weighted correction (v * wy) * wx (solvers.py:309-310)
+        {
+            double *out = S.scratch + ((size_t)p * L.nblocks + blk) * (BW * BH);
+            __syncwarp();
+            double wxv[TW], wyv[TH];
+#pragma unroll
+            for (int k = 0; k < TW / 2; ++k) {
+                const double2 t = *reinterpret_cast<const double2 *>(&swx[bx + 2 * k]);
+                wxv[2 * k] = t.x;
+                wxv[2 * k + 1] = t.y;
+            }
+#pragma unroll
+            for (int k = 0; k < TH / 2; ++k) {
+                const double2 t = *reinterpret_cast<const double2 *>(&swy[by + 2 * k]);
+                wyv[2 * k] = t.x;
+                wyv[2 * k + 1] = t.y;
+            }
+#pragma unroll
+            for (int j = 0; j < TH; ++j) {
+                TmRow tvr;
+                tm_ld8(tv + 16 * j, tvr);
+                tm_wait_ld(tvr);
+                double2 *row = reinterpret_cast<double2 *>(out + (by + j) * BW + bx);
+#pragma unroll
+                for (int k = 0; k < TW / 2; ++k) {
+                    double2 o;
+                    o.x = (tvr.get(2 * k) * wyv[j]) * wxv[2 * k];
+                    o.y = (tvr.get(2 * k + 1) * wyv[j]) * wxv[2 * k + 1];
+                    row[k] = o;
+                }
+            }
+        }
+    }
+
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tm_base), "r"(NCOL) : "memory");
+}
+
+}  // namespace b200p

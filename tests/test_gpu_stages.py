@@ -194,7 +194,7 @@ def test_oras_sweeps_general_start_and_stop_norm(rng):
         np.testing.assert_allclose(u_g, u_o, rtol=0, atol=1e-8)
 
 
-@pytest.mark.parametrize("variant", [1, 4, 5, 6, 7, 8, 9, 10])
+@pytest.mark.parametrize("variant", [1, 4, 5, 6, 7, 8, 9, 10, 11, 12])
 def test_tile32_variants_match_oracle(variant, rng):
     """Every 32x32 register/shared-memory tile variant of K2 (path 10 + id), regular start and
     the general start (u violating the interpolation condition)."""
