@@ -791,6 +791,17 @@ static int launch_sweep_tma(b200p_plan *pl, const LevelHost &L, const SweepArgs 
     return 0;
 }
 
+static void launch_warp_sweep(const WarpSweepArgs &WA, bool rm, bool qt, int grid, cudaStream_t st) {
+    const size_t smem = kw_table_bytes(WA.P, WA.S.L.nx, WA.S.L.ny);  // a few KB (P <= a few hundred problems)
+    if (rm) {
+        if (qt) oras_sweep_warp_kernel<true, true><<<grid, KW_THREADS, smem, st>>>(WA);
+        else oras_sweep_warp_kernel<true, false><<<grid, KW_THREADS, smem, st>>>(WA);
+    } else {
+        if (qt) oras_sweep_warp_kernel<false, true><<<grid, KW_THREADS, smem, st>>>(WA);
+        else oras_sweep_warp_kernel<false, false><<<grid, KW_THREADS, smem, st>>>(WA);
+    }
+}
+
 // K2W is persistent: resident CTAs per SM (register-limited) x SMs.
 static int warp_sweep_grid() {
     static int grid = 0;
@@ -834,13 +845,10 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, UBuf &ub, cons
                 WA.items_per_problem = WA.nrows * L.info.nx;
                 WA.total = pl->P * WA.items_per_problem;
                 const int g = std::min((WA.total + KW_WARPS - 1) / KW_WARPS, warp_sweep_grid());
-                if (tile == TILE_32_W) {
-                    if (rm) oras_sweep_warp_kernel<true, false><<<g, KW_THREADS, 0, st>>>(WA);
-                    else oras_sweep_warp_kernel<false, false><<<g, KW_THREADS, 0, st>>>(WA);
-                } else {
-                    if (rm) oras_sweep_warp_kernel<true, true><<<g, KW_THREADS, 0, st>>>(WA);
-                    else oras_sweep_warp_kernel<false, true><<<g, KW_THREADS, 0, st>>>(WA);
-                }
+                WA.P = pl->P;
+                if (kw_table_bytes(WA.P, L.info.nx, L.info.ny) > 40 * 1024)
+                    return fail_arg(B200P_ERR_UNSUPPORTED, "too many problems / blocks per axis for the K2W tables");
+                launch_warp_sweep(WA, rm, tile == TILE_32_WQ, g, st);
                 break;
             }
             case TILE_32_L: {

@@ -28,7 +28,16 @@
 
 namespace b200p {
 
-constexpr int KW_WARPS = 4;
+#ifndef B200P_KW_PAIRSUM
+#define B200P_KW_PAIRSUM 0    // stencil sum as (up + dn) + (lf + rt) instead of ((up + dn) + lf) + rt
+#endif
+#ifndef B200P_KW_WARPS
+#define B200P_KW_WARPS 4      // independent warps (= blocks in flight) per CTA
+#endif
+#ifndef B200P_KW_MAXREG
+#define B200P_KW_MAXREG 255   // 2 CTAs x 4 warps x 256 registers = the register file of an SM
+#endif
+constexpr int KW_WARPS = B200P_KW_WARPS;
 constexpr int KW_THREADS = KW_WARPS * 32;
 
 struct WarpSweepArgs {
@@ -37,6 +46,7 @@ struct WarpSweepArgs {
     int nrows;             // block rows of this launch (strip mode: S.iy0 .. S.iy0 + nrows)
     int items_per_problem; // nrows * nx
     int total;             // P * items_per_problem
+    int P;                 // problems (frames x channels)
 };
 
 // Packs the block-local masks for K2W: grid (ceil(nblocks / 4), F), 128 threads, a warp per block.
@@ -157,7 +167,7 @@ struct WarpCG {
             const double dn = J == TH - 1 ? hB[I] : pc[J == TH - 1 ? J : J + 1][I]; \
             const double lf = I == 0 ? hl : pc[J][I == 0 ? 0 : I - 1];          \
             const double rt = I == TW - 1 ? hr : pc[J][I == TW - 1 ? I : I + 1]; \
-            const double s = ((up + dn) + lf) + rt;                             \
+            const double s = B200P_KW_PAIRSUM ? (up + dn) + (lf + rt) : ((up + dn) + lf) + rt; \
             qrow[I] = fma(4.0, pc[J][I], -s);                                   \
             mask_zero<J * TW + I>(qrow[I], mbits);                              \
         }
@@ -193,25 +203,53 @@ struct WarpSmem {
     uint32_t tm_base;
 };
 
+struct WarpItem {
+    int p, ix, iy;
+};
+
+#ifndef KW_PREFETCH
+#define KW_PREFETCH 1
+#endif
+
+// Dynamic shared memory: the per-problem scalars and the block-start tables of the level, staged once
+// per CTA so that decoding an item costs LDS latency instead of a chain of dependent L2 round trips
+// (ncu: 6 % of all stall samples sat on S.rs[p] / L.xs[ix] at the start of every block).
+//   double rs[P]; int live_general[P] (bit 0: live, bit 1: general start); int xs[nx]; int ys[ny]
+__host__ __device__ inline size_t kw_table_bytes(int P, int nx, int ny) {
+    return sizeof(double) * P + sizeof(int) * ((size_t)P + nx + ny);
+}
+
 template <bool RM, bool QT>
-__global__ void __launch_bounds__(KW_THREADS, 2)
+__global__ void __maxnreg__(B200P_KW_MAXREG)
 oras_sweep_warp_kernel(const WarpSweepArgs A) {
     constexpr int TW = 8, TH = 4, BW = 32, BH = 32;
-    constexpr int NCOL = QT ? 128 : 64;  // TMEM columns per CTA: v (64) [+ q (64)] per lane
+    constexpr int NCOLW = QT ? 128 : 64;                   // TMEM columns per warp: v (64) [+ q (64)] per lane
+    constexpr int NCOL = NCOLW * ((KW_WARPS + 3) / 4);     // warps w and w + 4 share a lane quarter
     __shared__ WarpSmem sm;
+    extern __shared__ __align__(16) unsigned char kw_dyn[];
     const SweepArgs &S = A.S;
     const LevelDev &L = S.L;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double *s_rs = reinterpret_cast<double *>(kw_dyn);
+    int *s_flag = reinterpret_cast<int *>(s_rs + A.P);
+    int *s_xs = s_flag + A.P, *s_ys = s_xs + L.nx;
 
     if (warp == 0) {
         const uint32_t slot = (uint32_t)__cvta_generic_to_shared(&sm.tm_base);
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(slot), "r"(NCOL) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
+    for (int t = threadIdx.x; t < A.P; t += KW_THREADS) {
+        const double rs = (!S.pred || S.pred[t]) ? S.rs[t] : 0.0;  // frozen problems and rs == 0 (solvers.py:420) are skipped
+        s_rs[t] = rs;
+        s_flag[t] = (rs != 0.0 ? 1 : 0) | (S.mflag[t] != 0 ? 2 : 0);
+    }
+    for (int t = threadIdx.x; t < L.nx; t += KW_THREADS) s_xs[t] = L.xs[t];
+    for (int t = threadIdx.x; t < L.ny; t += KW_THREADS) s_ys[t] = L.ys[t];
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tv = sm.tm_base + ((uint32_t)(warp * 32) << 16);  // this warp's lane quarter
+    const uint32_t tv = sm.tm_base + ((uint32_t)((warp & 3) * 32) << 16) + (warp >> 2) * NCOLW;  // lane quarter
     const uint32_t tq = tv + 64;
 
     const int W = L.w, H = L.h;
@@ -219,23 +257,132 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
     const int lx = lane & 3, ly = lane >> 2;
     const int bx = lx * TW, by = ly * TH;
     double *swx = sm.wx[warp], *swy = sm.wy[warp];
+    const int stride_items = gridDim.x * KW_WARPS;
 
-    for (int item = blockIdx.x * KW_WARPS + warp; item < A.total; item += gridDim.x * KW_WARPS) {
-        const int p = item / A.items_per_problem;
-        const int rem = item - p * A.items_per_problem;
-        const int iyl = rem / L.nx, ix = rem - iyl * L.nx, iy = iyl + S.iy0;
+    // next item at or after `it` whose problem is live
+    auto next_live = [&](int it, WarpItem &w) {
+        while (it < A.total) {
+            const int p = it / A.items_per_problem;
+            if (s_flag[p] & 1) {
+                const int rem = it - p * A.items_per_problem;
+                const int iyl = rem / L.nx;
+                w.p = p;
+                w.ix = rem - iyl * L.nx;
+                w.iy = iyl + S.iy0;
+                return it;
+            }
+            it += stride_items;
+        }
+        return it;
+    };
+
+    // The gather window of an item (6 x 10 values of u around the lane's tile, its tile of b, its mask
+    // word) is loaded into registers ONE ITEM AHEAD: the loads are issued in the tail of the previous
+    // item, when the CG state is dead, and complete under that item's epilogue.
+    double uc[TH + 2][TW + 2];
+    double bt[RM ? 1 : TH][TW];
+    unsigned mbits = 0;
+    auto load_window = [&](const WarpItem &w) {
+        const int x0 = s_xs[w.ix], y0 = s_ys[w.iy];
+        const int gx0 = x0 + bx, gy0 = y0 + by;
+        const int frame = S.channels == 3 ? w.p / 3 : (S.channels == 1 ? w.p : w.p / S.channels);
+        mbits = A.mtab[((size_t)frame * L.nblocks + w.iy * L.nx + w.ix) * 32 + lane];
+        const double *urow = S.u + (size_t)w.p * S.plane + (size_t)(gy0 - 1) * W + gx0;
+        if (!(x0 == 0 || y0 == 0 || x0 + BW >= W || y0 + BH >= H)) {
+#pragma unroll
+            for (int j = 0; j < TH + 2; ++j) {
+                const double *rp = urow + (size_t)j * W;
+#pragma unroll
+                for (int k = 0; k < TW / 2; ++k) {
+                    const double2 a = *reinterpret_cast<const double2 *>(rp + 2 * k);
+                    uc[j][1 + 2 * k] = a.x;
+                    uc[j][2 + 2 * k] = a.y;
+                }
+                if (j >= 1 && j <= TH) {
+                    uc[j][0] = rp[-1];
+                    uc[j][TW + 1] = rp[TW];
+                } else {
+                    uc[j][0] = uc[j][TW + 1] = 0.0;
+                }
+            }
+        } else {
+            const bool hasL = gx0 > 0, hasR = gx0 + TW < W, hasT = gy0 > 0, hasB = gy0 + TH < H;
+#pragma unroll
+            for (int j = 0; j < TH + 2; ++j) {
+                const double *rp = urow + (size_t)j * W;
+                const bool rowin = (j > 0 || hasT) && (j < TH + 1 || hasB);
+#pragma unroll
+                for (int k = 0; k < TW / 2; ++k) {
+                    double2 a = make_double2(0.0, 0.0);
+                    if (rowin) a = *reinterpret_cast<const double2 *>(rp + 2 * k);
+                    uc[j][1 + 2 * k] = a.x;
+                    uc[j][2 + 2 * k] = a.y;
+                }
+                uc[j][0] = uc[j][TW + 1] = 0.0;
+                if (j >= 1 && j <= TH) {
+                    if (hasL) uc[j][0] = rp[-1];
+                    if (hasR) uc[j][TW + 1] = rp[TW];
+                }
+            }
+        }
+        if (!RM) {
+#pragma unroll
+            for (int j = 0; j < TH; ++j) {
+                const double *bp = S.b + (size_t)w.p * S.plane + (size_t)(gy0 + j) * W + gx0;
+#pragma unroll
+                for (int k = 0; k < TW / 2; ++k) {
+                    const double2 a = *reinterpret_cast<const double2 *>(bp + 2 * k);
+                    bt[RM ? 0 : j][2 * k] = a.x;
+                    bt[RM ? 0 : j][2 * k + 1] = a.y;
+                }
+            }
+        }
+    };
+
+    // L1 prefetch of the NEXT item's window (34 rows x 3 lines) and mask word: no registers, ~4
+    // instructions per lane; the gather of that item then hits L1 instead of waiting for L2 / DRAM.
+    auto prefetch_window = [&](const WarpItem &w) {
+        const int x0 = s_xs[w.ix], y0 = s_ys[w.iy];
+        const int frame = S.channels == 3 ? w.p / 3 : (S.channels == 1 ? w.p : w.p / S.channels);
+        if (lane == 0)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(A.mtab + ((size_t)frame * L.nblocks + w.iy * L.nx + w.ix) * 32));
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int y = y0 - 1 + lane + 32 * h;
+            if (y >= 0 && y < H && (h == 0 || lane < 2)) {
+                const double *rp = S.u + (size_t)w.p * S.plane + (size_t)y * W;
+                const int xa = max(x0 - 1, 0), xb = min(x0 + BW, W - 1);
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + xa));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + (xa + xb) / 2));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + xb));
+                if (!RM && y >= y0 && y < y0 + BH) {
+                    const double *bp = S.b + (size_t)w.p * S.plane + (size_t)y * W;
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(bp + x0));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(bp + x0 + 16));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(bp + x0 + BW - 1));
+                }
+            }
+        }
+    };
+
+    WarpItem cur;
+    int item = next_live(blockIdx.x * KW_WARPS + warp, cur);
+
+    while (item < A.total) {
+        load_window(cur);
+        if (KW_PREFETCH) {
+            WarpItem nx;
+            if (next_live(item + stride_items, nx) < A.total) prefetch_window(nx);
+        }
+        const int p = cur.p, ix = cur.ix, iy = cur.iy;
         const int blk = iy * L.nx + ix;
-        if (S.pred && !S.pred[p]) continue;
-        const double rs_g = S.rs[p];
-        if (rs_g == 0.0) continue;  // oras_sweeps' rs == 0 exit (solvers.py:420)
-        const int frame = S.channels == 3 ? p / 3 : (S.channels == 1 ? p : p / S.channels);
-        const unsigned mbits = A.mtab[((size_t)frame * L.nblocks + blk) * 32 + lane];
+        const double rs_g = s_rs[p];
         __syncwarp();  // the previous item's weight rows have been consumed
         swx[lane] = L.wx[ix * BW + lane];
         swy[lane] = L.wy[iy * BH + lane];
-        const int x0 = L.xs[ix], y0 = L.ys[iy];
+        const int x0 = s_xs[ix], y0 = s_ys[iy];
         const double target = S.eta * rs_g;
-        const bool general = S.mflag[p] != 0;
+        const bool general = (s_flag[p] & 2) != 0;
 
         WarpCG cg;
         cg.lane = lane;
@@ -254,67 +401,19 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
 
         // ---- gather: global residual g = b - A u on the tile (core.py:100-110)
         double r[TH][TW];
+        double vm[TH][TW];  // general start only: v0 = where(mask, g, 0)
         {
-            const double *urow = S.u + (size_t)p * S.plane + (size_t)(gy0 - 1) * W + gx0;
-            double uc[TH + 2][TW + 2];
-            if (!border) {
-#pragma unroll
-                for (int j = 0; j < TH + 2; ++j) {
-                    const double *rp = urow + (size_t)j * W;
-#pragma unroll
-                    for (int k = 0; k < TW / 2; ++k) {
-                        const double2 a = *reinterpret_cast<const double2 *>(rp + 2 * k);
-                        uc[j][1 + 2 * k] = a.x;
-                        uc[j][2 + 2 * k] = a.y;
-                    }
-                    if (j >= 1 && j <= TH) {
-                        uc[j][0] = rp[-1];
-                        uc[j][TW + 1] = rp[TW];
-                    } else {
-                        uc[j][0] = uc[j][TW + 1] = 0.0;
-                    }
-                }
-            } else {
-                const bool hasL = gx0 > 0, hasR = gx0 + TW < W, hasT = gy0 > 0, hasB = gy0 + TH < H;
-#pragma unroll
-                for (int j = 0; j < TH + 2; ++j) {
-                    const double *rp = urow + (size_t)j * W;
-                    const bool rowin = (j > 0 || hasT) && (j < TH + 1 || hasB);
-#pragma unroll
-                    for (int k = 0; k < TW / 2; ++k) {
-                        double2 a = make_double2(0.0, 0.0);
-                        if (rowin) a = *reinterpret_cast<const double2 *>(rp + 2 * k);
-                        uc[j][1 + 2 * k] = a.x;
-                        uc[j][2 + 2 * k] = a.y;
-                    }
-                    uc[j][0] = uc[j][TW + 1] = 0.0;
-                    if (j >= 1 && j <= TH) {
-                        if (hasL) uc[j][0] = rp[-1];
-                        if (hasR) uc[j][TW + 1] = rp[TW];
-                    }
-                }
-            }
             const double nc4 = -4.0 * hinv2;
 #pragma unroll
             for (int j = 0; j < TH; ++j) {
-                double bt[TW];
-                if (!RM) {
-                    const double *bp = S.b + (size_t)p * S.plane + (size_t)(gy0 + j) * W + gx0;
-#pragma unroll
-                    for (int k = 0; k < TW / 2; ++k) {
-                        const double2 a = *reinterpret_cast<const double2 *>(bp + 2 * k);
-                        bt[2 * k] = a.x;
-                        bt[2 * k + 1] = a.y;
-                    }
-                }
 #pragma unroll
                 for (int i = 0; i < TW; ++i) {
                     const double s = ((uc[j][i + 1] + uc[j + 2][i + 1]) + uc[j + 1][i]) + uc[j + 1][i + 2];
                     const double uu = uc[j + 1][i + 1];
-                    const double res = fma(hinv2, s, RM ? nc4 * uu : fma(nc4, uu, bt[i]));
+                    const double res = fma(hinv2, s, RM ? nc4 * uu : fma(nc4, uu, bt[RM ? 0 : j][i]));
                     const bool m = (mbits >> (j * TW + i)) & 1u;
                     // RM: rhs = where(mask, known, 0) and b - u == 0 at mask pixels unless `general`
-                    r[j][i] = m ? (RM ? 0.0 : bt[i] - uu) : res;
+                    r[j][i] = m ? (RM ? 0.0 : bt[RM ? 0 : j][i] - uu) : res;
                 }
             }
             if (border) {
@@ -372,11 +471,14 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
         }
         tm_wait_st();
 
+        // The LAST CG step's update of v is folded into the weighted store below (v = v_tmem + a_last p):
+        // no TMEM round trip, and the residual / direction updates of that step are skipped.
+        double a_last = 0.0;
+#pragma unroll
+        for (int j = 0; j < TH; ++j)
+#pragma unroll
+            for (int i = 0; i < TW; ++i) pc[j][i] = r[j][i];
         if (rs_k > target) {  // solvers.py:336 (strict)
-#pragma unroll
-            for (int j = 0; j < TH; ++j)
-#pragma unroll
-                for (int i = 0; i < TW; ++i) pc[j][i] = r[j][i];
             double inv_rs = __drcp_rn(rs_k);
             for (int it = 0; it < S.max_iters; ++it) {
                 double d_pq0 = 0.0, d_pq1 = 0.0, d_rq0 = 0.0, d_rq1 = 0.0, d_qq0 = 0.0, d_qq1 = 0.0;
@@ -405,7 +507,8 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
                 const double a = ok ? rs_k * __drcp_rn(pq) : 0.0;       // :349-350
                 const double ah = a * hinv2;
                 const double rs_new = fma(ah * ah, d_qq, fma(-2.0 * ah, d_rq, rs_k));
-                const bool stop = rs_new <= target || !ok;              // :354
+                a_last = a;
+                if (rs_new <= target || !ok || it + 1 >= S.max_iters) break;   // :354, :338
                 const double beta = rs_new * inv_rs;
                 if (QT) {
                     tm_wait_st();
@@ -422,10 +525,8 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
                             r[j][i] = fma(-ah, tqr.get(i), r[j][i]);
                         }
                         tm_st8(tv + 16 * j, vrow);
-                        if (!stop) {
 #pragma unroll
-                            for (int i = 0; i < TW; ++i) pc[j][i] = fma(beta, pc[j][i], r[j][i]);
-                        }
+                        for (int i = 0; i < TW; ++i) pc[j][i] = fma(beta, pc[j][i], r[j][i]);
                     }
                 } else {
                     // residual first (q dies), then ONE batch of v loads into the freed registers
@@ -448,23 +549,26 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
     }
                     B200P_KW_V(0, t0) B200P_KW_V(1, t1) B200P_KW_V(2, t2) B200P_KW_V(3, t3)
 #undef B200P_KW_V
-                    if (!stop) {
 #pragma unroll
-                        for (int j = 0; j < TH; ++j)
+                    for (int j = 0; j < TH; ++j)
 #pragma unroll
-                            for (int i = 0; i < TW; ++i) pc[j][i] = fma(beta, pc[j][i], r[j][i]);
-                    }
+                        for (int i = 0; i < TW; ++i) pc[j][i] = fma(beta, pc[j][i], r[j][i]);
                 }
                 tm_wait_st();
-                if (stop) break;
                 rs_k = rs_new;
                 inv_rs = __drcp_rn(rs_k);
             }
         }
 
-        // ---- weighted correction (v * wy) * wx (solvers.py:309-310)
+        // ---- weighted correction (v * wy) * wx (solvers.py:309-310); the window of the warp's next
+        // item is requested first so that its latency runs under this epilogue
         {
             double *out = S.scratch + ((size_t)p * L.nblocks + blk) * (BW * BH);
+            TmRow t0, t1, t2, t3;
+            tm_ld8(tv, t0);
+            tm_ld8(tv + 16, t1);
+            tm_ld8(tv + 32, t2);
+            tm_ld8(tv + 48, t3);
             __syncwarp();
             double wxv[TW], wyv[TH];
 #pragma unroll
@@ -479,20 +583,28 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
                 wyv[2 * k] = t.x;
                 wyv[2 * k + 1] = t.y;
             }
+            tm_wait_ld2(t0, t1);
+            tm_wait_ld2(t2, t3);
+            double vf[TH][TW];
+#define B200P_KW_VF(J, T) \
+    _Pragma("unroll") for (int i = 0; i < TW; ++i) vf[J][i] = fma(a_last, pc[J][i], T.get(i));
+            B200P_KW_VF(0, t0) B200P_KW_VF(1, t1) B200P_KW_VF(2, t2) B200P_KW_VF(3, t3)
+#undef B200P_KW_VF
+            WarpItem nxt;
+            const int next = next_live(item + stride_items, nxt);
 #pragma unroll
             for (int j = 0; j < TH; ++j) {
-                TmRow tvr;
-                tm_ld8(tv + 16 * j, tvr);
-                tm_wait_ld(tvr);
                 double2 *row = reinterpret_cast<double2 *>(out + (by + j) * BW + bx);
 #pragma unroll
                 for (int k = 0; k < TW / 2; ++k) {
                     double2 o;
-                    o.x = (tvr.get(2 * k) * wyv[j]) * wxv[2 * k];
-                    o.y = (tvr.get(2 * k + 1) * wyv[j]) * wxv[2 * k + 1];
+                    o.x = (vf[j][2 * k] * wyv[j]) * wxv[2 * k];
+                    o.y = (vf[j][2 * k + 1] * wyv[j]) * wxv[2 * k + 1];
                     row[k] = o;
                 }
             }
+            item = next;
+            cur = nxt;
         }
     }
 
