@@ -166,6 +166,7 @@ struct LevelHost {
     int tile = 0;               // K2 variant: 0 generic, else see launch_sweep
     unsigned *d_mtab = nullptr; // K2T: packed block-local masks (F, nblocks, 64); null = level not eligible
     unsigned *d_mtabw = nullptr; // K2W: the same for the warp-per-block layout (F, nblocks, 32)
+    unsigned *d_claim = nullptr; // K2W: {next unclaimed item, finished CTAs}, zero between launches
     // combine on arrival (FUSE variant of the lean kernel): cell tables and arrival counters
     const int *d_cell_need = nullptr, *d_lastx = nullptr, *d_lasty = nullptr;
     unsigned *d_cell_cnt = nullptr;
@@ -846,6 +847,11 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, UBuf &ub, cons
                 WA.total = pl->P * WA.items_per_problem;
                 const int g = std::min((WA.total + KW_WARPS - 1) / KW_WARPS, warp_sweep_grid());
                 WA.P = pl->P;
+                WA.claim = L.d_claim;
+                kw_magic((unsigned)WA.items_per_problem, WA.m_ipp, WA.k_ipp);
+                kw_magic((unsigned)L.info.nx, WA.m_nx, WA.k_nx);
+                if ((unsigned)WA.total >= (1u << 30))
+                    return fail_arg(B200P_ERR_UNSUPPORTED, "too many block solves per launch for the K2W item decode");
                 if (kw_table_bytes(WA.P, L.info.nx, L.info.ny) > 40 * 1024)
                     return fail_arg(B200P_ERR_UNSUPPORTED, "too many problems / blocks per axis for the K2W tables");
                 launch_warp_sweep(WA, rm, tile == TILE_32_WQ, g, st);
@@ -1895,6 +1901,8 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
         {
             PTRY(dev_alloc(pl, &L.d_mtab, (size_t)pl->F * L.nblocks * KT_THREADS));
             PTRY(dev_alloc(pl, &L.d_mtabw, (size_t)pl->F * L.nblocks * 32));
+            PTRY(dev_alloc(pl, &L.d_claim, 4));
+            CU(cudaMemset(L.d_claim, 0, 4 * sizeof(unsigned)));
         }
         if (L.d_mtab && L.nblocks > 1 && arrival_fusion_enabled()) {
             // cells = rectangles between consecutive block starts; a block overlaps the cells from its own
@@ -2404,8 +2412,7 @@ static int ensure_sparse_staging(b200p_plan *pl, size_t entries) {
     if (entries <= pl->sp_cap) return 0;
     const size_t cap = entries + entries / 4 + 1024;
     const int C = pl->cfg.channels;
-    if (pl->h_cnt) cudaFreeHost(pl->h_cnt);
-    if (pl->d_cnt) cudaFree(pl->d_cnt);
+    // (h_cnt / d_cnt belong to the pinned zero-copy ingest and are not touched here)
     if (pl->h_sp_idx) cudaFreeHost(pl->h_sp_idx);
     if (pl->h_sp_val) cudaFreeHost(pl->h_sp_val);
     if (pl->d_sp_idx) cudaFree(pl->d_sp_idx);

@@ -28,8 +28,8 @@
 
 namespace b200p {
 
-#ifndef B200P_KW_PAIRSUM
-#define B200P_KW_PAIRSUM 0    // stencil sum as (up + dn) + (lf + rt) instead of ((up + dn) + lf) + rt
+#ifndef B200P_KW_PREDFMA
+#define B200P_KW_PREDFMA 1    // mask pixels: stencil FMA under a predicate on a zeroed register (else FMA + predicated zero)
 #endif
 #ifndef B200P_KW_WARPS
 #define B200P_KW_WARPS 4      // independent warps (= blocks in flight) per CTA
@@ -45,9 +45,24 @@ struct WarpSweepArgs {
     const unsigned *mtab;  // (F, nblocks, 32): bit j*8+i of word `lane` = mask of that lane's pixel (i, j)
     int nrows;             // block rows of this launch (strip mode: S.iy0 .. S.iy0 + nrows)
     int items_per_problem; // nrows * nx
-    int total;             // P * items_per_problem
+    int total;             // P * items_per_problem (upper bound; the kernel walks live problems only)
     int P;                 // problems (frames x channels)
+    unsigned *claim;       // [0] next unclaimed item, [1] CTAs that have finished; both 0 between launches
+    unsigned m_ipp, k_ipp; // n / items_per_problem == (n * m) >> k for n < 2^30 (kw_magic)
+    unsigned m_nx, k_nx;   // the same for n / nx
 };
+
+// Division by a launch constant as one wide multiply and a shift: k = 31 + floor(log2 d),
+// m = ceil(2^k / d) <= 2^31; exact for n < 2^30 (n * (m d - 2^k) < n d < 2^k).
+inline void kw_magic(unsigned d, unsigned &m, unsigned &k) {
+    unsigned fl = 0;
+    while ((2u << fl) <= d) ++fl;
+    k = 31 + fl;
+    m = (unsigned)((((unsigned long long)1 << k) + d - 1) / d);
+}
+__device__ __forceinline__ unsigned kw_div(unsigned n, unsigned m, unsigned k) {
+    return (unsigned)(((unsigned long long)n * m) >> k);
+}
 
 // Packs the block-local masks for K2W: grid (ceil(nblocks / 4), F), 128 threads, a warp per block.
 __global__ void __launch_bounds__(KW_THREADS)
@@ -107,33 +122,40 @@ __device__ __forceinline__ void tm_wait_ld2(TmRow &a, TmRow &b) {
 }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// q = (mbits bit K) ? 0 : q as "test bit into a predicate, zero under the predicate" (2 instructions
-// per pixel; the select form costs a bit test and two FSELs, and ptxas tends to hoist and re-pack
-// the 32 predicates of a tile into a register every CG step).
+// q = (mbits bit K) ? 0 : c * p - s: the bit test feeds a predicate, the stencil FMA runs under it
+// on a zeroed destination (no select; the 32 bit tests of a tile become a handful of R2P).
 template <int K>
-__device__ __forceinline__ void mask_zero(double &q, unsigned mbits) {
+__device__ __forceinline__ double stencil_q(double c, double p, double s, unsigned mbits) {
+    double q;
+#if B200P_KW_PREDFMA
+    asm("{\n\t.reg .pred z;\n\t.reg .b32 t;\n\t.reg .f64 ns;\n\tand.b32 t, %4, %5;\n\tsetp.ne.u32 z, t, 0;\n\t"
+        "neg.f64 ns, %3;\n\tmov.f64 %0, 0d0000000000000000;\n\t@!z fma.rn.f64 %0, %1, %2, ns;\n\t}"
+        : "=d"(q)
+        : "d"(c), "d"(p), "d"(s), "r"(mbits), "n"(1u << K));
+#else
+    q = fma(c, p, -s);
     asm("{\n\t.reg .pred z;\n\t.reg .b32 t;\n\tand.b32 t, %1, %2;\n\tsetp.ne.u32 z, t, 0;\n\t"
         "@z mov.f64 %0, 0d0000000000000000;\n\t}"
         : "+d"(q)
         : "r"(mbits), "n"(1u << K));
-}
-// h = flag ? g * p : h as one predicated DMUL (ghost value of a cut block side)
-__device__ __forceinline__ void ghost_mul(double &h, double g, double p, unsigned flag) {
-    asm("{\n\t.reg .pred e;\n\tsetp.ne.u32 e, %3, 0;\n\t@e mul.f64 %0, %1, %2;\n\t}"
-        : "+d"(h)
-        : "d"(g), "d"(p), "r"(flag));
+#endif
+    return q;
 }
 
 // One warp, 32x32 block, lane (lx = lane & 3, ly = lane >> 2) owns the 8 x 4 pixels at (8 lx, 4 ly).
+// Block sides: a neighbour cut off by a side is the ghost gamma * p_edge (gamma = 1 on the image border,
+// 1 - alpha h on an inner side, solvers.py:288-297), folded into the centre coefficient of the pixel
+// (4 - gamma per cut side); the value the halo shuffle delivers to such a lane is switched off by a
+// 0 / 1 factor inside the FMA that adds it, so block sides cost no selects and no extra multiplies.
 struct WarpCG {
     static constexpr int TW = 8, TH = 4;
-    int lane;
-    unsigned eL, eR, eT, eB;  // tile touches the block's left / right / top / bottom side
-    double gL, gR, gT, gB;  // ghost factors of those sides (1 on the image border, 1 - alpha*h inside)
+    double zL, zR, zT, zB;  // 0 where the tile touches that block side, else 1 (lane constants)
+    double cT, cB;          // centre coefficient of the tile's top / bottom row: 4 - gamma_T|B (4 inside)
+    double gLz, gRz;        // gamma of the left / right side where the tile touches it, else 0
     unsigned mbits;
 
-    // q' = 4 p - neighbours (scaled local Robin operator, solvers.py:316-326), 0 at mask pixels;
-    // rows are handed to `sink(j, qrow)` as they are produced.
+    // q' = c p - in-block neighbours (scaled local Robin operator, solvers.py:316-326), 0 at mask
+    // pixels; rows are handed to `sink(j, qrow)` as they are produced.
     template <class Sink>
     __device__ __forceinline__ void apply(const double (&pc)[TH][TW], Sink sink) const {
         double hT[TW], hB[TW];
@@ -141,11 +163,6 @@ struct WarpCG {
         for (int i = 0; i < TW; ++i) {
             hT[i] = __shfl_up_sync(FULL_MASK, pc[TH - 1][i], 4);
             hB[i] = __shfl_down_sync(FULL_MASK, pc[0][i], 4);
-        }
-#pragma unroll
-        for (int i = 0; i < TW; ++i) {
-            ghost_mul(hT[i], gT, pc[0][i], eT);
-            ghost_mul(hB[i], gB, pc[TH - 1][i], eB);
         }
         apply_row<0>(pc, hT, hB, sink);
         apply_row<1>(pc, hT, hB, sink);
@@ -156,20 +173,21 @@ struct WarpCG {
     template <int J, class Sink>
     __device__ __forceinline__ void apply_row(const double (&pc)[TH][TW], const double (&hT)[TW],
                                               const double (&hB)[TW], Sink &sink) const {
-        double hl = __shfl_up_sync(FULL_MASK, pc[J][TW - 1], 1);
-        double hr = __shfl_down_sync(FULL_MASK, pc[J][0], 1);
-        ghost_mul(hl, gL, pc[J][0], eL);
-        ghost_mul(hr, gR, pc[J][TW - 1], eR);
+        const double hl = __shfl_up_sync(FULL_MASK, pc[J][TW - 1], 1);
+        const double hr = __shfl_down_sync(FULL_MASK, pc[J][0], 1);
+        const double cJ = J == 0 ? cT : (J == TH - 1 ? cB : 4.0);
         double qrow[TW];
-#define B200P_KW_PX(I)                                                          \
-        {                                                                       \
-            const double up = J == 0 ? hT[I] : pc[J == 0 ? 0 : J - 1][I];       \
-            const double dn = J == TH - 1 ? hB[I] : pc[J == TH - 1 ? J : J + 1][I]; \
-            const double lf = I == 0 ? hl : pc[J][I == 0 ? 0 : I - 1];          \
-            const double rt = I == TW - 1 ? hr : pc[J][I == TW - 1 ? I : I + 1]; \
-            const double s = B200P_KW_PAIRSUM ? (up + dn) + (lf + rt) : ((up + dn) + lf) + rt; \
-            qrow[I] = fma(4.0, pc[J][I], -s);                                   \
-            mask_zero<J * TW + I>(qrow[I], mbits);                              \
+#define B200P_KW_PX(I)                                                                           \
+        {                                                                                        \
+            double s;                                                                            \
+            if (J == 0) s = fma(hT[I], zT, pc[1][I]);                                            \
+            else if (J == TH - 1) s = fma(hB[I], zB, pc[TH - 2][I]);                             \
+            else s = pc[J == 0 ? 0 : J - 1][I] + pc[J == TH - 1 ? J : J + 1][I];                 \
+            if (I == 0) s = fma(hl, zL, s); else s += pc[J][I == 0 ? 0 : I - 1];                 \
+            if (I == TW - 1) s = fma(hr, zR, s); else s += pc[J][I == TW - 1 ? I : I + 1];       \
+            if (I == 0) s = fma(gLz, pc[J][0], s);                                               \
+            if (I == TW - 1) s = fma(gRz, pc[J][TW - 1], s);                                     \
+            qrow[I] = stencil_q<J * TW + I>(cJ, pc[J][I], s, mbits);                             \
         }
         B200P_KW_PX(0) B200P_KW_PX(1) B200P_KW_PX(2) B200P_KW_PX(3)
         B200P_KW_PX(4) B200P_KW_PX(5) B200P_KW_PX(6) B200P_KW_PX(7)
@@ -201,6 +219,7 @@ struct WarpSmem {
     alignas(16) double wx[KW_WARPS][32];
     alignas(16) double wy[KW_WARPS][32];
     uint32_t tm_base;
+    int nlive;
 };
 
 struct WarpItem {
@@ -211,14 +230,18 @@ struct WarpItem {
 #define KW_PREFETCH 1
 #endif
 
-// Dynamic shared memory: the per-problem scalars and the block-start tables of the level, staged once
-// per CTA so that decoding an item costs LDS latency instead of a chain of dependent L2 round trips
-// (ncu: 6 % of all stall samples sat on S.rs[p] / L.xs[ix] at the start of every block).
-//   double rs[P]; int live_general[P] (bit 0: live, bit 1: general start); int xs[nx]; int ys[ny]
+// Dynamic shared memory: the per-problem scalars, the list of live problems and the block-start tables
+// of the level, staged once per CTA so that decoding an item costs LDS latency instead of a chain of
+// dependent L2 round trips.
+//   double rs[P]; int general[P]; int live[P]; int xs[nx]; int ys[ny]
 __host__ __device__ inline size_t kw_table_bytes(int P, int nx, int ny) {
-    return sizeof(double) * P + sizeof(int) * ((size_t)P + nx + ny);
+    return sizeof(double) * P + sizeof(int) * (2 * (size_t)P + nx + ny);
 }
 
+// Work distribution: the items (live problem, block) of a launch are claimed from a global counter,
+// one claim ahead of the block being solved (the atomic's round trip runs under the gather), so the
+// warps of the grid finish together whatever the spread of CG step counts; the first item of a warp
+// is its own index.  The last CTA to leave zeroes the counters for the next launch on the stream.
 template <bool RM, bool QT>
 __global__ void __maxnreg__(B200P_KW_MAXREG)
 oras_sweep_warp_kernel(const WarpSweepArgs A) {
@@ -231,21 +254,35 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
     const LevelDev &L = S.L;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double *s_rs = reinterpret_cast<double *>(kw_dyn);
-    int *s_flag = reinterpret_cast<int *>(s_rs + A.P);
-    int *s_xs = s_flag + A.P, *s_ys = s_xs + L.nx;
+    int *s_general = reinterpret_cast<int *>(s_rs + A.P);
+    int *s_live = s_general + A.P;
+    int *s_xs = s_live + A.P, *s_ys = s_xs + L.nx;
 
     if (warp == 0) {
         const uint32_t slot = (uint32_t)__cvta_generic_to_shared(&sm.tm_base);
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(slot), "r"(NCOL) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
-    for (int t = threadIdx.x; t < A.P; t += KW_THREADS) {
-        const double rs = (!S.pred || S.pred[t]) ? S.rs[t] : 0.0;  // frozen problems and rs == 0 (solvers.py:420) are skipped
-        s_rs[t] = rs;
-        s_flag[t] = (rs != 0.0 ? 1 : 0) | (S.mflag[t] != 0 ? 2 : 0);
+    if (warp == KW_WARPS - 1) {
+        // live problems in ascending order; frozen problems and rs == 0 (solvers.py:420) are skipped
+        int base = 0;
+        for (int t0 = 0; t0 < A.P; t0 += 32) {
+            const int t = t0 + lane;
+            double rs = 0.0;
+            if (t < A.P) {
+                rs = (!S.pred || S.pred[t]) ? S.rs[t] : 0.0;
+                s_rs[t] = rs;
+                s_general[t] = S.mflag[t] != 0;
+            }
+            const unsigned m = __ballot_sync(FULL_MASK, rs != 0.0);
+            if (rs != 0.0) s_live[base + __popc(m & ((1u << lane) - 1u))] = t;
+            base += __popc(m);
+        }
+        if (lane == 0) sm.nlive = base;
+    } else {
+        for (int t = threadIdx.x; t < L.nx; t += KW_THREADS - 32) s_xs[t] = L.xs[t];
+        for (int t = threadIdx.x; t < L.ny; t += KW_THREADS - 32) s_ys[t] = L.ys[t];
     }
-    for (int t = threadIdx.x; t < L.nx; t += KW_THREADS) s_xs[t] = L.xs[t];
-    for (int t = threadIdx.x; t < L.ny; t += KW_THREADS) s_ys[t] = L.ys[t];
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -257,28 +294,19 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
     const int lx = lane & 3, ly = lane >> 2;
     const int bx = lx * TW, by = ly * TH;
     double *swx = sm.wx[warp], *swy = sm.wy[warp];
-    const int stride_items = gridDim.x * KW_WARPS;
+    const unsigned grid_warps = gridDim.x * KW_WARPS;
+    const unsigned total = (unsigned)sm.nlive * (unsigned)A.items_per_problem;
 
-    // next item at or after `it` whose problem is live
-    auto next_live = [&](int it, WarpItem &w) {
-        while (it < A.total) {
-            const int p = it / A.items_per_problem;
-            if (s_flag[p] & 1) {
-                const int rem = it - p * A.items_per_problem;
-                const int iyl = rem / L.nx;
-                w.p = p;
-                w.ix = rem - iyl * L.nx;
-                w.iy = iyl + S.iy0;
-                return it;
-            }
-            it += stride_items;
-        }
-        return it;
+    auto decode = [&](unsigned it, WarpItem &w) {
+        const unsigned li = kw_div(it, A.m_ipp, A.k_ipp);
+        const unsigned rem = it - li * (unsigned)A.items_per_problem;
+        const unsigned iyl = kw_div(rem, A.m_nx, A.k_nx);
+        w.p = s_live[li];
+        w.ix = (int)(rem - iyl * (unsigned)L.nx);
+        w.iy = (int)iyl + S.iy0;
     };
 
-    // The gather window of an item (6 x 10 values of u around the lane's tile, its tile of b, its mask
-    // word) is loaded into registers ONE ITEM AHEAD: the loads are issued in the tail of the previous
-    // item, when the CG state is dead, and complete under that item's epilogue.
+    // The gather window of an item: 6 x 10 values of u around the lane's tile, its tile of b, its mask word.
     double uc[TH + 2][TW + 2];
     double bt[RM ? 1 : TH][TW];
     unsigned mbits = 0;
@@ -365,15 +393,21 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
         }
     };
 
-    WarpItem cur;
-    int item = next_live(blockIdx.x * KW_WARPS + warp, cur);
+    WarpCG cg;
+    cg.zL = lx == 0 ? 0.0 : 1.0;
+    cg.zR = lx == 3 ? 0.0 : 1.0;
+    cg.zT = ly == 0 ? 0.0 : 1.0;
+    cg.zB = ly == 7 ? 0.0 : 1.0;
 
-    while (item < A.total) {
+    WarpItem cur;
+    unsigned item = blockIdx.x * KW_WARPS + warp;
+    bool have = item < total;
+    if (have) decode(item, cur);
+
+    while (have) {
+        unsigned claimed = 0;
+        if (lane == 0) claimed = atomicAdd(A.claim, 1u);   // the next item; consumed after the gather
         load_window(cur);
-        if (KW_PREFETCH) {
-            WarpItem nx;
-            if (next_live(item + stride_items, nx) < A.total) prefetch_window(nx);
-        }
         const int p = cur.p, ix = cur.ix, iy = cur.iy;
         const int blk = iy * L.nx + ix;
         const double rs_g = s_rs[p];
@@ -382,26 +416,23 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
         swy[lane] = L.wy[iy * BH + lane];
         const int x0 = s_xs[ix], y0 = s_ys[iy];
         const double target = S.eta * rs_g;
-        const bool general = (s_flag[p] & 2) != 0;
+        const bool general = s_general[p] != 0;
 
-        WarpCG cg;
-        cg.lane = lane;
-        cg.eL = lx == 0 ? 1u : 0u;
-        cg.eR = lx == 3 ? 1u : 0u;
-        cg.eT = ly == 0 ? 1u : 0u;
-        cg.eB = ly == 7 ? 1u : 0u;
-        cg.gL = x0 > 0 ? g_in : 1.0;
-        cg.gR = x0 + BW < W ? g_in : 1.0;
-        cg.gT = y0 > 0 ? g_in : 1.0;
-        cg.gB = y0 + BH < H ? g_in : 1.0;
         cg.mbits = mbits;
+        {
+            const double gl = x0 > 0 ? g_in : 1.0, gr = x0 + BW < W ? g_in : 1.0;
+            const double gt = y0 > 0 ? g_in : 1.0, gb = y0 + BH < H ? g_in : 1.0;
+            cg.gLz = lx == 0 ? gl : 0.0;
+            cg.gRz = lx == 3 ? gr : 0.0;
+            cg.cT = ly == 0 ? 4.0 - gt : 4.0;
+            cg.cB = ly == 7 ? 4.0 - gb : 4.0;
+        }
 
         const int gx0 = x0 + bx, gy0 = y0 + by;
         const bool border = x0 == 0 || y0 == 0 || x0 + BW >= W || y0 + BH >= H;  // warp-uniform
 
         // ---- gather: global residual g = b - A u on the tile (core.py:100-110)
         double r[TH][TW];
-        double vm[TH][TW];  // general start only: v0 = where(mask, g, 0)
         {
             const double nc4 = -4.0 * hinv2;
 #pragma unroll
@@ -437,6 +468,15 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
                         if ((mbits >> (j * TW + i)) & 1u)
                             r[j][i] = S.b[(size_t)p * S.plane + (size_t)(gy0 + j) * W + gx0 + i] - uc[j + 1][i + 1];
             }
+        }
+
+        // ---- the warp's next item (claimed above): decode it and pull its window towards L1
+        WarpItem nxt;
+        const unsigned next = __shfl_sync(FULL_MASK, claimed, 0) + grid_warps;
+        const bool have_next = next < total;
+        if (have_next) {
+            decode(next, nxt);
+            if (KW_PREFETCH) prefetch_window(nxt);
         }
 
         // ---- local start: v0 = where(mask, g, 0) -> TMEM, r0 = g - A_i v0 (solvers.py:331-333)
@@ -560,8 +600,7 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
             }
         }
 
-        // ---- weighted correction (v * wy) * wx (solvers.py:309-310); the window of the warp's next
-        // item is requested first so that its latency runs under this epilogue
+        // ---- weighted correction (v * wy) * wx (solvers.py:309-310)
         {
             double *out = S.scratch + ((size_t)p * L.nblocks + blk) * (BW * BH);
             TmRow t0, t1, t2, t3;
@@ -590,8 +629,6 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
     _Pragma("unroll") for (int i = 0; i < TW; ++i) vf[J][i] = fma(a_last, pc[J][i], T.get(i));
             B200P_KW_VF(0, t0) B200P_KW_VF(1, t1) B200P_KW_VF(2, t2) B200P_KW_VF(3, t3)
 #undef B200P_KW_VF
-            WarpItem nxt;
-            const int next = next_live(item + stride_items, nxt);
 #pragma unroll
             for (int j = 0; j < TH; ++j) {
                 double2 *row = reinterpret_cast<double2 *>(out + (by + j) * BW + bx);
@@ -603,15 +640,24 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
                     row[k] = o;
                 }
             }
-            item = next;
-            cur = nxt;
         }
+        cur = nxt;
+        have = have_next;
     }
 
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(sm.tm_base), "r"(NCOL) : "memory");
+    if (threadIdx.x == 0) {
+        // every warp of this CTA has made its last claim; the last CTA re-arms the counters
+        __threadfence();
+        if (atomicAdd(A.claim + 1, 1u) == gridDim.x - 1) {
+            A.claim[0] = 0;
+            A.claim[1] = 0;
+            __threadfence();
+        }
+    }
 }
 
 }  // namespace b200p

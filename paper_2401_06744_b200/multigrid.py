@@ -10,6 +10,7 @@ validates arguments, owns plans and converts reports.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 import time
 from dataclasses import dataclass, field, replace
 
@@ -174,12 +175,29 @@ class Plan:
         wall = time.perf_counter() - t0
         return d_out, (self._reports(raw, wall) if raw is not None else None)
 
+    def _check_host(self, mask, known, out, dtype):
+        """The C side reads F*H*W mask bytes and P*H*W values and writes P*H*W values through raw host
+        pointers: element counts, dtypes and contiguity are checked here (the device path has
+        _dev.check_tensor for the same reason)."""
+        n = self.height * self.width
+        for a, name, dt, count in ((mask, "mask", np.uint8, self.frames * n),
+                                   (known, "known", dtype, self.problems * n),
+                                   (out, "out", dtype, self.problems * n)):
+            if not isinstance(a, np.ndarray) or a.dtype != dt or not a.flags.c_contiguous:
+                raise ValueError(f"{name} must be a C-contiguous {np.dtype(dt)} array")
+            if a.size != count:
+                raise ValueError(f"{name} has {a.size} elements, this plan needs {count} "
+                                 f"({self.frames} frame(s) x {self.channels} channel(s) x {self.height} x {self.width})")
+            if name == "out" and not a.flags.writeable:
+                raise ValueError("out must be writeable")
+
     def solve_host(self, mask, known, out=None):
         """Host buffers in and out (H2D + solve + D2H inside the call)."""
         mask = np.ascontiguousarray(mask, dtype=np.uint8)
         known = np.ascontiguousarray(known, dtype=np.float64)
         if out is None:
             out = np.empty((self.frames, self.channels, self.height, self.width))
+        self._check_host(mask, known, out, np.float64)
         raw = (_lib.Report * self.problems)()
         t0 = time.perf_counter()
         _dev.call("b200p_solve_host", self.handle, mask.ctypes.data, known.ctypes.data, out.ctypes.data,
@@ -190,10 +208,7 @@ class Plan:
     def solve_host_async(self, mask, known, out, u8: bool = False):
         """Enqueue H2D + solve + D2H on the plan's stream and return; `wait()` completes it.
         The arrays must be C-contiguous, of the exact dtypes, and stay alive until `wait()`."""
-        want = np.uint8 if u8 else np.float64
-        for a, n, dt in ((mask, "mask", np.uint8), (known, "known", want), (out, "out", want)):
-            if not isinstance(a, np.ndarray) or a.dtype != dt or not a.flags.c_contiguous:
-                raise ValueError(f"{n} must be a C-contiguous {np.dtype(dt)} array")
+        self._check_host(mask, known, out, np.uint8 if u8 else np.float64)
         self._t0 = time.perf_counter()
         _dev.call("b200p_solve_host_u8_async" if u8 else "b200p_solve_host_async", self.handle,
                   mask.ctypes.data, known.ctypes.data, out.ctypes.data)
@@ -211,6 +226,7 @@ class Plan:
         known_u8 = np.ascontiguousarray(known_u8, dtype=np.uint8)
         if out is None:
             out = np.empty((self.frames, self.channels, self.height, self.width), dtype=np.uint8)
+        self._check_host(mask, known_u8, out, np.uint8)
         raw = (_lib.Report * self.problems)()
         t0 = time.perf_counter()
         _dev.call("b200p_solve_host_u8", self.handle, mask.ctypes.data, known_u8.ctypes.data,
@@ -221,6 +237,7 @@ class Plan:
 
 _PLAN_CACHE: dict = {}
 _PLAN_CACHE_MAX = 4
+_PLAN_CACHE_LOCK = threading.Lock()
 
 
 def _cfg_key(cfg):
@@ -234,18 +251,22 @@ def _cfg_key(cfg):
 def cached_plan(width, height, channels, frames, cfg, spacing=1.0, single_level=False) -> Plan:
     """Plans are expensive (device scratch + graph capture); reuse by configuration."""
     key = (width, height, channels, frames, float(spacing), _cfg_key(cfg), bool(single_level))
-    plan = _PLAN_CACHE.pop(key, None)
-    if plan is None:
-        while len(_PLAN_CACHE) >= _PLAN_CACHE_MAX:
-            _PLAN_CACHE.pop(next(iter(_PLAN_CACHE))).close()
-        plan = Plan(width, height, channels, frames, cfg, spacing, single_level=single_level)
-    _PLAN_CACHE[key] = plan
-    return plan
+    with _PLAN_CACHE_LOCK:
+        plan = _PLAN_CACHE.pop(key, None)
+        if plan is None or not plan.handle:
+            # Eviction only drops the cache's reference: a LevelHierarchy (or any caller) may still hold the
+            # plan, so it is never closed here -- Plan.__del__ frees it with the last reference.
+            while len(_PLAN_CACHE) >= _PLAN_CACHE_MAX:
+                _PLAN_CACHE.pop(next(iter(_PLAN_CACHE)))
+            plan = Plan(width, height, channels, frames, cfg, spacing, single_level=single_level)
+        _PLAN_CACHE[key] = plan
+        return plan
 
 
 def clear_plan_cache():
-    while _PLAN_CACHE:
-        _PLAN_CACHE.popitem()[1].close()
+    """Drop the cache's references (plans still held elsewhere stay valid)."""
+    with _PLAN_CACHE_LOCK:
+        _PLAN_CACHE.clear()
 
 
 def _stage_plan(mask, spacing, block_size, overlap, alpha, eta, local_max_iters) -> Plan:

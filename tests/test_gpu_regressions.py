@@ -1,0 +1,98 @@
+"""Regression tests for defects found in review: staging lifetime of the host entry
+points, element-count checks in front of the raw-pointer calls, plan-cache eviction."""
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2401_06744_b200 as bp
+
+pytestmark = pytest.mark.gpu
+
+
+def test_pinned_then_pageable_regrow_then_pinned_on_one_plan():
+    """The zero-copy counters of the pinned ingest survive a regrow of the pageable path's sparse staging
+    (they used to be freed with it and left dangling)."""
+    import torch
+    w, h = 200, 136
+    cfg = bp.MultigridConfig(block_size=16, overlap=2)
+    plan = bp.Plan(w, h, 1, 1, cfg)
+    refs = {}
+
+    def problem(dens):
+        m, k = oracle.seeded_problem(w, h, dens, 33, channels=1)
+        if dens not in refs:
+            refs[dens] = oracle.solve_image(m, k, 1.0, oracle.MultigridConfig(block_size=16, overlap=2))[0]
+        return m.view(np.uint8)[None], k[None], refs[dens]
+
+    def pinned(dens):
+        m, k, ref = problem(dens)
+        pk = torch.from_numpy(k).pin_memory()
+        po = torch.empty_like(pk).pin_memory()
+        plan.solve_host_async(m, pk.numpy(), po.numpy())
+        plan.wait()
+        up, _ = plan.last_transfer_bytes()
+        assert up == m.size + int(m.sum()) * 8
+        assert np.abs(po.numpy()[0] - ref).max() <= 1e-9
+
+    def pageable(dens):
+        m, k, ref = problem(dens)
+        out, _ = plan.solve_host(m, k)
+        assert np.abs(out[0] - ref).max() <= 1e-9
+
+    pinned(0.02)
+    pageable(0.01)      # first sparse staging
+    pageable(0.2)       # larger list: staging regrown
+    pinned(0.02)        # counters must still be alive
+    pageable(0.3)
+    pinned(0.05)
+    plan.close()
+
+
+def test_host_entry_points_check_element_counts():
+    w, h, c, f = 64, 48, 3, 2
+    plan = bp.Plan(w, h, c, f, bp.MultigridConfig(block_size=16, overlap=2))
+    ms, ks = zip(*(oracle.seeded_problem(w, h, 0.05, s, channels=c) for s in range(f)))
+    masks, known = np.stack(ms).view(np.uint8), np.stack(ks)
+    out, _ = plan.solve_host(masks, known)
+    with pytest.raises(ValueError, match="known has"):
+        plan.solve_host(masks, known[0])                      # (C,H,W) on a 2-frame plan
+    with pytest.raises(ValueError, match="mask has"):
+        plan.solve_host(masks[0], known)                      # (H,W) mask
+    with pytest.raises(ValueError, match="out must be"):
+        plan.solve_host(masks, known, out=np.empty(known.shape, dtype=np.float32))
+    with pytest.raises(ValueError, match="out has"):
+        plan.solve_host(masks, known, out=np.empty(known[0].shape))
+    with pytest.raises(ValueError, match="out must be"):
+        plan.solve_host(masks, known, out=np.empty(known.shape + (2,))[..., 0])   # not contiguous
+    with pytest.raises(ValueError, match="known has"):
+        plan.solve_host_u8(masks, known[0].astype(np.uint8))
+    with pytest.raises(ValueError, match="out has"):
+        plan.solve_host_async(masks, known, np.empty(known[0].shape))
+    out2, _ = plan.solve_host(masks, known)                   # the plan is still usable
+    assert np.array_equal(out, out2)
+    plan.close()
+
+
+def test_plan_cache_eviction_keeps_live_hierarchies_valid():
+    """cached_plan evicts without closing: a hierarchy built before several other geometries went through
+    the cache still answers .levels / len() (they used to hit a destroyed handle)."""
+    bp.clear_plan_cache()
+    m0, k0 = oracle.seeded_problem(96, 80, 0.05, 1, channels=2)
+    cfg = bp.MultigridConfig(block_size=16, overlap=2)
+    hier = bp.build_hierarchy(bp.InpaintingProblem(m0, k0), cfg)
+    n = len(hier)
+    for i, (w, h) in enumerate([(64, 64), (72, 40), (50, 90), (120, 33), (88, 88)]):
+        m, k = oracle.seeded_problem(w, h, 0.05, 10 + i, channels=1)
+        bp.solve_image(bp.InpaintingProblem(m, k), "mg-oras", cfg)
+    assert len(hier) == n and n > 1
+    levels = hier.levels
+    ho = oracle.build_hierarchy(m0, k0, 1.0, oracle.MultigridConfig(block_size=16, overlap=2))
+    assert len(levels) == len(ho.levels)
+    for lv, lo in zip(levels, ho.levels):
+        assert np.array_equal(lv.mask, lo.mask) and np.array_equal(lv.rhs, lo.rhs)
+    u, rep = bp.fmg_solve(hier, cfg, channel=1)
+    uo, ro = oracle.fmg_solve(ho, oracle.MultigridConfig(block_size=16, overlap=2), channel=1)
+    assert rep.iterations == ro.iterations and np.abs(u - uo).max() <= 1e-9
+    bp.clear_plan_cache()
+    assert len(hier) == n        # clearing drops references only
