@@ -792,7 +792,7 @@ static int launch_sweep_tma(b200p_plan *pl, const LevelHost &L, const SweepArgs 
     return 0;
 }
 
-static void launch_warp_sweep(const WarpSweepArgs &WA, bool rm, bool qt, int grid, cudaStream_t st) {
+static int launch_warp_sweep(const WarpSweepArgs &WA, bool rm, bool qt, int grid, cudaStream_t st) {
     const size_t smem = kw_table_bytes(WA.P, WA.S.L.nx, WA.S.L.ny);  // a few KB (P <= a few hundred problems)
     if (rm) {
         if (qt) oras_sweep_warp_kernel<true, true><<<grid, KW_THREADS, smem, st>>>(WA);
@@ -801,6 +801,8 @@ static void launch_warp_sweep(const WarpSweepArgs &WA, bool rm, bool qt, int gri
         if (qt) oras_sweep_warp_kernel<false, true><<<grid, KW_THREADS, smem, st>>>(WA);
         else oras_sweep_warp_kernel<false, false><<<grid, KW_THREADS, smem, st>>>(WA);
     }
+    CU(cudaGetLastError());
+    return 0;
 }
 
 // K2W is persistent: resident CTAs per SM (register-limited) x SMs.
@@ -845,7 +847,11 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, UBuf &ub, cons
                 WA.nrows = L.iy_hi - L.iy_lo;  // strip mode: only the block rows of this rank
                 WA.items_per_problem = WA.nrows * L.info.nx;
                 WA.total = pl->P * WA.items_per_problem;
-                const int g = std::min((WA.total + KW_WARPS - 1) / KW_WARPS, warp_sweep_grid());
+                // runs of consecutive items per claim only where every warp still gets several runs
+                static const unsigned chunk_max = getenv("B200P_KW_CHUNK") ? (unsigned)atoi(getenv("B200P_KW_CHUNK")) : KW_CHUNK_MAX;
+                WA.chunk = (long long)WA.total >= 8ll * chunk_max * KW_WARPS * warp_sweep_grid() ? chunk_max : 1u;
+                const int per_cta = KW_WARPS * (int)WA.chunk;
+                const int g = std::min((WA.total + per_cta - 1) / per_cta, warp_sweep_grid());
                 WA.P = pl->P;
                 WA.claim = L.d_claim;
                 kw_magic((unsigned)WA.items_per_problem, WA.m_ipp, WA.k_ipp);
@@ -854,7 +860,8 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, UBuf &ub, cons
                     return fail_arg(B200P_ERR_UNSUPPORTED, "too many block solves per launch for the K2W item decode");
                 if (kw_table_bytes(WA.P, L.info.nx, L.info.ny) > 40 * 1024)
                     return fail_arg(B200P_ERR_UNSUPPORTED, "too many problems / blocks per axis for the K2W tables");
-                launch_warp_sweep(WA, rm, tile == TILE_32_WQ, g, st);
+                int rc = launch_warp_sweep(WA, rm, tile == TILE_32_WQ, g, st);
+                if (rc) return rc;
                 break;
             }
             case TILE_32_L: {

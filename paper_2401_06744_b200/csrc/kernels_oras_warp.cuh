@@ -50,6 +50,7 @@ struct WarpSweepArgs {
     unsigned *claim;       // [0] next unclaimed item, [1] CTAs that have finished; both 0 between launches
     unsigned m_ipp, k_ipp; // n / items_per_problem == (n * m) >> k for n < 2^30 (kw_magic)
     unsigned m_nx, k_nx;   // the same for n / nx
+    unsigned chunk;        // consecutive items per claim (1 on small launches, KW_CHUNK_MAX on large ones)
 };
 
 // Division by a launch constant as one wide multiply and a shift: k = 31 + floor(log2 d),
@@ -226,9 +227,13 @@ struct WarpItem {
     int p, ix, iy;
 };
 
-#ifndef KW_PREFETCH
-#define KW_PREFETCH 1
+#ifndef B200P_KW_STCS
+#define B200P_KW_STCS 1       // weighted tiles leave with streaming stores (they are read next by K2b, not here)
 #endif
+#ifndef B200P_KW_CHUNK
+#define B200P_KW_CHUNK 4      // consecutive items per claim (a warp walks along a block row: its windows overlap in L1)
+#endif
+constexpr unsigned KW_CHUNK_MAX = B200P_KW_CHUNK;
 
 // Dynamic shared memory: the per-problem scalars, the list of live problems and the block-start tables
 // of the level, staged once per CTA so that decoding an item costs LDS latency instead of a chain of
@@ -238,10 +243,11 @@ __host__ __device__ inline size_t kw_table_bytes(int P, int nx, int ny) {
     return sizeof(double) * P + sizeof(int) * (2 * (size_t)P + nx + ny);
 }
 
-// Work distribution: the items (live problem, block) of a launch are claimed from a global counter,
-// one claim ahead of the block being solved (the atomic's round trip runs under the gather), so the
-// warps of the grid finish together whatever the spread of CG step counts; the first item of a warp
-// is its own index.  The last CTA to leave zeroes the counters for the next launch on the stream.
+// Work distribution: the items (live problem, block) of a launch are claimed from a global counter in
+// runs of KW_CHUNK consecutive items, one claim ahead of the run being solved (the atomic's round trip
+// runs under a whole block solve), so the warps of the grid finish together whatever the spread of CG
+// step counts; the first run of a warp is its own index.  The last CTA to leave zeroes the counters
+// for the next launch on the stream.
 template <bool RM, bool QT>
 __global__ void __maxnreg__(B200P_KW_MAXREG)
 oras_sweep_warp_kernel(const WarpSweepArgs A) {
@@ -367,32 +373,6 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
         }
     };
 
-    // L1 prefetch of the NEXT item's window (34 rows x 3 lines) and mask word: no registers, ~4
-    // instructions per lane; the gather of that item then hits L1 instead of waiting for L2 / DRAM.
-    auto prefetch_window = [&](const WarpItem &w) {
-        const int x0 = s_xs[w.ix], y0 = s_ys[w.iy];
-        const int frame = S.channels == 3 ? w.p / 3 : (S.channels == 1 ? w.p : w.p / S.channels);
-        if (lane == 0)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(A.mtab + ((size_t)frame * L.nblocks + w.iy * L.nx + w.ix) * 32));
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int y = y0 - 1 + lane + 32 * h;
-            if (y >= 0 && y < H && (h == 0 || lane < 2)) {
-                const double *rp = S.u + (size_t)w.p * S.plane + (size_t)y * W;
-                const int xa = max(x0 - 1, 0), xb = min(x0 + BW, W - 1);
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + xa));
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + (xa + xb) / 2));
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(rp + xb));
-                if (!RM && y >= y0 && y < y0 + BH) {
-                    const double *bp = S.b + (size_t)w.p * S.plane + (size_t)y * W;
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(bp + x0));
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(bp + x0 + 16));
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(bp + x0 + BW - 1));
-                }
-            }
-        }
-    };
-
     WarpCG cg;
     cg.zL = lx == 0 ? 0.0 : 1.0;
     cg.zR = lx == 3 ? 0.0 : 1.0;
@@ -400,13 +380,18 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
     cg.zB = ly == 7 ? 0.0 : 1.0;
 
     WarpItem cur;
-    unsigned item = blockIdx.x * KW_WARPS + warp;
+    const unsigned KW_CHUNK = A.chunk;
+    unsigned item = (blockIdx.x * KW_WARPS + warp) * KW_CHUNK, run_end = item + KW_CHUNK;
     bool have = item < total;
-    if (have) decode(item, cur);
+    if (have) {
+        decode(item, cur);
+    }
+    unsigned claimed = 0;  // lane 0: start of the warp's next run, minus the statically assigned part
 
     while (have) {
-        unsigned claimed = 0;
-        if (lane == 0) claimed = atomicAdd(A.claim, 1u);   // the next item; consumed after the gather
+        if (item + KW_CHUNK == run_end && lane == 0)   // first item of a run: claim the next run (plain PTX:
+            asm volatile("atom.global.add.u32 %0, [%1], %2;"  // no warp-aggregation sequence, no wait here)
+                         : "=r"(claimed) : "l"(A.claim), "r"(KW_CHUNK));
         load_window(cur);
         const int p = cur.p, ix = cur.ix, iy = cur.iy;
         const int blk = iy * L.nx + ix;
@@ -472,11 +457,14 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
 
         // ---- the warp's next item (claimed above): decode it and pull its window towards L1
         WarpItem nxt;
-        const unsigned next = __shfl_sync(FULL_MASK, claimed, 0) + grid_warps;
+        unsigned next = item + 1;
+        if (next == run_end) {
+            next = __shfl_sync(FULL_MASK, claimed, 0) + grid_warps * KW_CHUNK;
+            run_end = next + KW_CHUNK;
+        }
         const bool have_next = next < total;
         if (have_next) {
             decode(next, nxt);
-            if (KW_PREFETCH) prefetch_window(nxt);
         }
 
         // ---- local start: v0 = where(mask, g, 0) -> TMEM, r0 = g - A_i v0 (solvers.py:331-333)
@@ -637,11 +625,16 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
                     double2 o;
                     o.x = (vf[j][2 * k] * wyv[j]) * wxv[2 * k];
                     o.y = (vf[j][2 * k + 1] * wyv[j]) * wxv[2 * k + 1];
+#if B200P_KW_STCS
+                    __stcs(row + k, o);   // streaming store: the tile is not read again by this kernel
+#else
                     row[k] = o;
+#endif
                 }
             }
         }
         cur = nxt;
+        item = next;
         have = have_next;
     }
 
