@@ -228,6 +228,22 @@ int b200p_solve_host_async(b200p_plan *plan, const uint8_t *h_mask, const double
 int b200p_solve_host_u8_async(b200p_plan *plan, const uint8_t *h_mask, const uint8_t *h_known_u8,
                               uint8_t *h_out_u8);
 
+/* 8-bit image files as they are on disk, replacing the host-side conversions around
+ * solve_image in cli._cmd_inpaint (cli.py:80-95):
+ *   h_pixels     (frames,H,W,C) uint8, interleaved as ImageFile.pixels holds them (fileio.py:27-37;
+ *                C = 1: (frames,H,W)) -- ImageFile.channel_fields (fileio.py:51-55) runs on the device;
+ *   h_mask_bits  (frames,H,ceil(W/8)) the P4 raster of read_mask / write_mask (fileio.py:181-230): rows
+ *                padded to whole bytes, most significant bit first, 1 = known pixel; padding bits ignored;
+ *   h_out        (frames,H,W,C) uint8 = image_from_fields(solve_image(...).fields).pixels
+ *                (fileio.py:58-65: round half to even, clip to [0,255], channels last).
+ * The rounding rides on the last post-smoothing combine pass of the finest level (no pass over the fp64
+ * result); problems that converge without a V-cycle, and the comparison pipelines, take a tail pass.
+ * Errors as b200p_solve_host; an all-zero raster is B200P_ERR_EMPTY_MASK. */
+int b200p_solve_host_image_u8(b200p_plan *plan, const uint8_t *h_mask_bits, const uint8_t *h_pixels,
+                              uint8_t *h_out, b200p_report *h_reports);
+int b200p_solve_host_image_u8_async(b200p_plan *plan, const uint8_t *h_mask_bits, const uint8_t *h_pixels,
+                                    uint8_t *h_out);
+
 /* ---- stage entry points (A/B tests against the reference functions) ---- */
 
 /* build_hierarchy's data half (multigrid.py:249-260): coarsen mask and known
@@ -276,6 +292,12 @@ int b200p_residual_sqnorm(const uint8_t *d_mask, int h, int w, double spacing, c
 
 /* Transfers (multigrid.py:98-186); coarse shapes are ceil(h/2) x ceil(w/2). */
 int b200p_downsample_mask(const uint8_t *d_fine, int h, int w, uint8_t *d_coarse, void *stream);
+/* image_from_fields (fileio.py:58-65): (frames,C,h,w) fp64 -> (frames,h,w,C) uint8, np.round (half to
+ * even) then clip to [0,255]; the quantiser the solve's 8-bit egress uses. */
+int b200p_image_from_fields(const double *d_fields, int frames, int channels, int h, int w, uint8_t *d_pixels,
+                            void *stream);
+/* read_mask's P4 branch (fileio.py:206-216): raster rows of ceil(w/8) bytes, MSB first -> (frames,h,w) bytes. */
+int b200p_unpack_mask_bits(const uint8_t *d_bits, int frames, int h, int w, uint8_t *d_mask, void *stream);
 int b200p_downsample_values(const uint8_t *d_fine_mask, const uint8_t *d_coarse_mask,
                             const double *d_fine_rhs, int h, int w, int modified,
                             double *d_coarse_rhs, void *stream);

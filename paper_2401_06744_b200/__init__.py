@@ -7,7 +7,7 @@ the arithmetic runs in ``libb200paint.so`` (hand-written CUDA, C-ABI in
 ``include/b200paint.h``).  No CPU fallback.
 """
 
-from . import _lib, strip, suites
+from . import _lib, fileio, strip, suites
 from .core import (EmptyMaskError, InpaintingProblem, Metrics, StencilOperator, apply_operator,
                    as_field, as_mask, compute_metrics, mask_density, residual)
 from .multigrid import (Level, LevelHierarchy, MultigridConfig, Plan, build_hierarchy, cached_plan,
@@ -17,8 +17,9 @@ from .multigrid import (Level, LevelHierarchy, MultigridConfig, Plan, build_hier
 from .partition import (BlockPartition, BlockRect, BlockWeights, build_partition, build_weights,
                         extend_add_weighted, restrict_to_block)
 from .pipeline import FramePipeline
-from .pipelines import (SOLVER_NAMES, SolveResult, join_solver_name, solve_channel, solve_frames,
-                        solve_image, split_solver_name)
+from .fileio import ImageFile, image_from_fields, pack_mask_raster, unpack_mask_raster
+from .pipelines import (SOLVER_NAMES, SolveResult, inpaint_image_u8, join_solver_name, solve_channel,
+                        solve_frames, solve_image, split_solver_name)
 from .solvers import BlockSolver, SolveReport, SolverConfig, oras_sweeps
 
 __version__ = "0.1.0"
@@ -35,6 +36,7 @@ __all__ = [
     "BlockPartition", "BlockRect", "BlockWeights", "build_partition", "build_weights",
     "extend_add_weighted", "restrict_to_block",
     "SOLVER_NAMES", "SolveResult", "join_solver_name", "solve_channel", "solve_frames", "solve_image",
-    "split_solver_name",
+    "split_solver_name", "inpaint_image_u8", "ImageFile", "image_from_fields", "pack_mask_raster",
+    "unpack_mask_raster", "fileio",
     "BlockSolver", "SolveReport", "SolverConfig", "oras_sweeps", "FramePipeline", "suites", "strip",
 ]

@@ -116,6 +116,8 @@ SIGNATURES = {
     "b200p_solve_host_async": (_I, [_VP, _VP, _VP, _VP]),
     "b200p_solve_host_u8_async": (_I, [_VP, _VP, _VP, _VP]),
     "b200p_solve_host_u8": (_I, [_VP, _VP, _VP, _VP, _VP]),
+    "b200p_solve_host_image_u8_async": (_I, [_VP, _VP, _VP, _VP]),
+    "b200p_solve_host_image_u8": (_I, [_VP, _VP, _VP, _VP, _VP]),
     "b200p_plan_build_hierarchy": (_I, [_VP, _VP, _VP, _VP]),
     "b200p_plan_level_ptrs": (_I, [_VP, _I, C.POINTER(_VP), C.POINTER(_VP)]),
     "b200p_plan_cascade": (_I, [_VP, _VP, _VP]),
@@ -126,6 +128,8 @@ SIGNATURES = {
     "b200p_residual": (_I, [_VP, _I, _I, _D, _VP, _VP, _VP, _VP]),
     "b200p_residual_sqnorm": (_I, [_VP, _I, _I, _D, _VP, _VP, _I, _VP, _VP]),
     "b200p_downsample_mask": (_I, [_VP, _I, _I, _VP, _VP]),
+    "b200p_image_from_fields": (_I, [_VP, _I, _I, _I, _I, _VP, _VP]),
+    "b200p_unpack_mask_bits": (_I, [_VP, _I, _I, _I, _VP, _VP]),
     "b200p_downsample_values": (_I, [_VP, _VP, _VP, _I, _I, _I, _VP, _VP]),
     "b200p_residual_restrict": (_I, [_VP, _VP, _I, _I, _D, _VP, _VP, _VP, _VP]),
     "b200p_restrict_residual": (_I, [_VP, _VP, _I, _I, _VP, _VP]),

@@ -201,7 +201,7 @@ struct ReportPack {
 
 struct GraphSlot {
     cudaGraphExec_t exec = nullptr;
-    const void *k0 = nullptr, *k1 = nullptr, *k2 = nullptr;  // pointers baked into the graph
+    const void *k0 = nullptr, *k1 = nullptr, *k2 = nullptr, *k3 = nullptr;  // pointers baked into the graph
     int64_t kernels = 0;
 };
 
@@ -253,6 +253,11 @@ struct b200p_plan {
     uint8_t *d_in_mask = nullptr;
     double *d_in_known = nullptr, *d_out = nullptr;
     uint8_t *d_io_u8 = nullptr;
+    uint8_t *d_mask_bits = nullptr;       // P4 raster of the image entry points (F, h, ceil(w / 8))
+    // 8-bit egress of the solve being enqueued: target image (F, h, w, C), the sweep that carries it
+    uint8_t *egress = nullptr, *egress_now = nullptr;
+    const double *egress_src = nullptr;   // the fp64 result the tail pass converts
+    bool egress_fused = false;            // a combine pass of the cycle body writes the image
     // sparse ingest (host f64 entry point): pixel indices + values at mask pixels, pinned + device
     uint32_t *h_sp_idx = nullptr, *d_sp_idx = nullptr;
     double *h_sp_val = nullptr, *d_sp_val = nullptr;
@@ -931,8 +936,12 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, UBuf &ub, cons
                (L.own_hi - L.own_lo + COMBINE_ROWS - 1) / COMBINE_ROWS, pl->P);
         // read corrections + u, write u
         LaunchScope sc(pl, st, KK_COMBINE, field_bytes(pl, L, 3.0, 0.0));
+        uint8_t *eg = pl->egress_now;   // set by enqueue_smooth for the last post-smoothing sweep of level 0
+        pl->egress_now = nullptr;
+        if (eg) pl->egress_fused = true;
         oras_combine_kernel<<<g, ST_THREADS_COMBINE, 0, st>>>(L.dev, pl->d_scratch, A.plane, pred,
-                                                              pl->d_rs, u, unit_counter, L.own_lo, L.own_hi);
+                                                              pl->d_rs, u, unit_counter, L.own_lo, L.own_hi,
+                                                              eg, pl->C);
         CU(cudaGetLastError());
     }
     // strip mode: the rows the neighbours' block solves and stencils read from this strip
@@ -952,13 +961,18 @@ static int launch_sweep(b200p_plan *pl, const LevelHost &L, UBuf &u, const doubl
 // have_norm is set, rs/mflag already describe (u, b) and the first K1 is skipped.
 static int enqueue_smooth(b200p_plan *pl, const LevelHost &L, UBuf &u, const double *b, bool rm,
                           int units, const int *pred, int *unit_counter, bool have_norm,
-                          cudaStream_t st) {
+                          cudaStream_t st, bool carries_egress = false) {
     for (int i = 0; i < units; ++i) {
         if (!(have_norm && i == 0)) {
             int rc = launch_norm(pl, L, u.cur, b, false, rm, pred, st);
             if (rc) return rc;
         }
+        // the last sweep of the finest level's post-smoothing leaves the iterate the V-cycle ends with:
+        // its combine pass also writes the 8-bit image (split path only; anything else takes the tail pass)
+        const bool split = !L.fused && !(L.d_cell_cnt && !striped(pl, L));
+        pl->egress_now = (carries_egress && i == units - 1 && split && !striped(pl, L)) ? pl->egress : nullptr;
         int rc = launch_sweep(pl, L, u, b, rm, pred, unit_counter, -1, st);
+        pl->egress_now = nullptr;
         if (rc) return rc;
     }
     return 0;
@@ -1184,7 +1198,8 @@ static int enqueue_vcycle(b200p_plan *pl, int level, UBuf &u, const double *b, b
             e.cur, L.d_mask, nullptr, L.info.height, L.info.width, pl->C, pred, u.cur, Ylo, Yhi);
         CU(cudaGetLastError());
     }
-    if ((rc = enqueue_smooth(pl, L, u, b, rm, cfg.nu_post, pred, uc, false, st))) return rc;
+    if ((rc = enqueue_smooth(pl, L, u, b, rm, cfg.nu_post, pred, uc, false, st, level == 0 && settle_home)))
+        return rc;
     // inner levels may end in the partner buffer (the caller prolongates from e.cur); the level
     // handed in from outside must end where it started
     return settle_home ? settle(pl, L, u, home, st) : 0;
@@ -2181,6 +2196,16 @@ static int ensure_report_block(b200p_plan *pl) {
 static int enqueue_reports(b200p_plan *pl, cudaStream_t st) {
     int rc = ensure_report_block(pl);
     if (rc) return rc;
+    if (pl->egress) {
+        // 8-bit decode: problems whose image bytes no combine pass has written (no V-cycle needed, or a
+        // pipeline / sweep variant without the fused egress) are converted here from the fp64 result
+        const size_t plane = (size_t)pl->cfg.width * pl->cfg.height, npix = pl->F * plane;
+        const int all = (pl->egress_fused && pl->cfg.mode == 0 && pl->cfg.smoother == 0) ? 0 : 1;
+        LaunchScope sc(pl, st, KK_CONVERT, all ? 9.0 * pl->P * plane : 0.0);
+        egress_u8_kernel<<<(unsigned)((npix + ST_THREADS - 1) / ST_THREADS), ST_THREADS, 0, st>>>(
+            pl->egress_src, npix, pl->C, plane, pl->d_cycles, all, pl->egress);
+        CU(cudaGetLastError());
+    }
     LaunchScope sc(pl, st, KK_CONTROL, 0.0);
     const int n = pl->P * B200P_MAX_HISTORY;
     pack_reports_kernel<<<(n + 255) / 256, 256, 0, st>>>(pl->P, pl->d_cycles, pl->d_units, pl->d_histlen,
@@ -2210,11 +2235,12 @@ static void read_reports(b200p_plan *pl, b200p_report *h_reports) {
 static int launch_solve_graph(b200p_plan *pl, const uint8_t *d_mask, const double *d_known, double *d_out,
                               cudaStream_t st) {
     GraphSlot &slot = pl->g_solve;
-    if (!slot.exec || slot.k0 != d_mask || slot.k1 != d_known || slot.k2 != d_out) {
+    if (!slot.exec || slot.k0 != d_mask || slot.k1 != d_known || slot.k2 != d_out || slot.k3 != pl->egress) {
         if (slot.exec) {
             cudaGraphExecDestroy(slot.exec);
             slot.exec = nullptr;
         }
+        pl->egress_fused = false;
         int rc = ensure_report_block(pl);
         if (rc) return rc;
         if (!pl->aux_stream) CU(cudaStreamCreateWithFlags(&pl->aux_stream, cudaStreamNonBlocking));
@@ -2276,17 +2302,30 @@ static int launch_solve_graph(b200p_plan *pl, const uint8_t *d_mask, const doubl
         slot.k0 = d_mask;
         slot.k1 = d_known;
         slot.k2 = d_out;
+        slot.k3 = pl->egress;
     }
     CU(cudaGraphLaunch(slot.exec, st));
     return 0;
 }
 
+static int solve_async_impl(b200p_plan *pl, const uint8_t *d_mask, const double *d_known, double *d_out,
+                            uint8_t *d_egress, void *stream);
+
 int b200p_solve_async(b200p_plan *pl, const uint8_t *d_mask, const double *d_known, double *d_out,
                       void *stream) {
+    return solve_async_impl(pl, d_mask, d_known, d_out, nullptr, stream);
+}
+
+// d_egress: optional (F, h, w, C) 8-bit image the solve also leaves its result in (image_from_fields)
+static int solve_async_impl(b200p_plan *pl, const uint8_t *d_mask, const double *d_known, double *d_out,
+                            uint8_t *d_egress, void *stream) {
     if (!pl || !d_mask || !d_known || !d_out) return fail_arg(B200P_ERR_ARG, "null argument");
     if (pl->pending) return fail_arg(B200P_ERR_STATE, "a solve is pending on this plan: call b200p_solve_wait first");
     cudaStream_t st = (cudaStream_t)stream;
     const bool graphs = pl->cfg.use_graphs && !pl->profiling;
+    pl->egress = d_egress;
+    pl->egress_src = d_out;
+    if (!graphs) pl->egress_fused = false;
     if (graphs && st == nullptr) {
         // stream capture is not allowed on the legacy default stream
         if (!pl->own_stream) CU(cudaStreamCreateWithFlags(&pl->own_stream, cudaStreamNonBlocking));
@@ -2604,6 +2643,67 @@ int b200p_solve_host_u8(b200p_plan *pl, const uint8_t *h_mask, const uint8_t *h_
     return b200p_solve_wait(pl, h_reports);
 }
 
+// 8-bit image files as they are on disk: interleaved pixels (F, h, w, C) as ImageFile holds
+// them (fileio.py:27-55) and the bit-packed P4 raster of write_mask / read_mask (fileio.py:181-230: rows
+// padded to bytes, MSB first, 1 = known).  Unpacking, channel_fields and image_from_fields run on the
+// device; the round / clip / interleave of the result rides on the last combine pass of the solve.
+static int check_mask_bits(const b200p_plan *pl, const uint8_t *bits) {
+    const int w = pl->cfg.width, h = pl->cfg.height, rb = (w + 7) / 8;
+    const uint8_t last = (w % 8) ? (uint8_t)(0xff00u >> (w % 8)) : 0xff;   // padding bits of a row are ignored
+    for (int f = 0; f < pl->F; ++f) {
+        bool any = false;
+        const uint8_t *fp = bits + (size_t)f * h * rb;
+        for (int y = 0; y < h && !any; ++y) {
+            const uint8_t *row = fp + (size_t)y * rb;
+            any = (rb > 1 && any_nonzero(row, rb - 1)) || (row[rb - 1] & last);
+        }
+        if (!any) return fail_arg(B200P_ERR_EMPTY_MASK, "cannot solve without known pixels");
+    }
+    return 0;
+}
+
+int b200p_solve_host_image_u8_async(b200p_plan *pl, const uint8_t *h_mask_bits, const uint8_t *h_pixels,
+                                    uint8_t *h_out) {
+    if (!pl || !h_mask_bits || !h_pixels || !h_out) return fail_arg(B200P_ERR_ARG, "null argument");
+    if (pl->pending) return fail_arg(B200P_ERR_STATE, "a solve is already pending on this plan");
+    int rc = check_mask_bits(pl, h_mask_bits);
+    if (rc) return rc;
+    if ((rc = ensure_staging(pl, true))) return rc;
+    const int w = pl->cfg.width, h = pl->cfg.height, rb = (w + 7) / 8;
+    const size_t plane = (size_t)w * h, npix = pl->F * plane, n = pl->P * plane;
+    const size_t nbits = (size_t)pl->F * h * rb;
+    if (!pl->d_mask_bits && (rc = dev_alloc(pl, &pl->d_mask_bits, nbits))) return rc;
+    cudaStream_t st = pl->own_stream;
+    CU(cudaMemcpyAsync(pl->d_mask_bits, h_mask_bits, nbits, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(pl->d_io_u8, h_pixels, n, cudaMemcpyHostToDevice, st));
+    {
+        LaunchScope sc(pl, st, KK_CONVERT, (double)(nbits + npix));
+        unpack_mask_bits_kernel<<<(unsigned)((nbits + ST_THREADS - 1) / ST_THREADS), ST_THREADS, 0, st>>>(
+            pl->d_mask_bits, nbits, w, rb, pl->d_in_mask);
+        CU(cudaGetLastError());
+    }
+    {
+        LaunchScope sc(pl, st, KK_CONVERT, 9.0 * n);
+        deinterleave_u8_kernel<<<(unsigned)((npix + ST_THREADS - 1) / ST_THREADS), ST_THREADS, 0, st>>>(
+            pl->d_io_u8, npix, pl->C, plane, pl->d_in_known);
+        CU(cudaGetLastError());
+    }
+    // the pixels have been consumed: the same buffer receives the decoded image
+    if ((rc = solve_async_impl(pl, pl->d_in_mask, pl->d_in_known, pl->d_out, pl->d_io_u8, st))) return rc;
+    CU(cudaMemcpyAsync(h_out, pl->d_io_u8, n, cudaMemcpyDeviceToHost, st));
+    pl->last_h2d = (int64_t)(nbits + n);
+    pl->last_h2d_counted = false;
+    pl->last_d2h = (int64_t)n;
+    return 0;
+}
+
+int b200p_solve_host_image_u8(b200p_plan *pl, const uint8_t *h_mask_bits, const uint8_t *h_pixels,
+                              uint8_t *h_out, b200p_report *h_reports) {
+    int rc = b200p_solve_host_image_u8_async(pl, h_mask_bits, h_pixels, h_out);
+    if (rc) return rc;
+    return b200p_solve_wait(pl, h_reports);
+}
+
 // ---- stage entry points -------------------------------------------------
 
 int b200p_plan_build_hierarchy(b200p_plan *pl, const uint8_t *d_mask, const double *d_known,
@@ -2791,6 +2891,27 @@ int b200p_residual_sqnorm(const uint8_t *d_mask, int h, int w, double spacing, c
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     cudaFree(d_partial); cudaFree(d_pf); cudaFree(d_cnt); cudaFree(d_rs); cudaFree(d_flag);
     if (e != cudaSuccess) return fail_cuda(e, "residual_sqnorm");
+    return 0;
+}
+
+int b200p_image_from_fields(const double *d_fields, int frames, int channels, int h, int w, uint8_t *d_pixels,
+                            void *stream) {
+    if (!d_fields || !d_pixels || frames < 1 || channels < 1 || h < 1 || w < 1)
+        return fail_arg(B200P_ERR_ARG, "bad argument");
+    const size_t plane = (size_t)h * w, npix = (size_t)frames * plane;
+    egress_u8_kernel<<<(unsigned)((npix + ST_THREADS - 1) / ST_THREADS), ST_THREADS, 0, (cudaStream_t)stream>>>(
+        d_fields, npix, channels, plane, nullptr, 1, d_pixels);
+    CU(cudaGetLastError());
+    return 0;
+}
+
+int b200p_unpack_mask_bits(const uint8_t *d_bits, int frames, int h, int w, uint8_t *d_mask, void *stream) {
+    if (!d_bits || !d_mask || frames < 1 || h < 1 || w < 1) return fail_arg(B200P_ERR_ARG, "bad argument");
+    const int rb = (w + 7) / 8;
+    const size_t nbits = (size_t)frames * h * rb;
+    unpack_mask_bits_kernel<<<(unsigned)((nbits + ST_THREADS - 1) / ST_THREADS), ST_THREADS, 0, (cudaStream_t)stream>>>(
+        d_bits, nbits, w, rb, d_mask);
+    CU(cudaGetLastError());
     return 0;
 }
 

@@ -22,6 +22,13 @@ struct LevelDev {
 
 constexpr unsigned FULL_MASK = 0xffffffffu;
 
+// np.clip(np.round(v), 0, 255).astype(np.uint8) (fileio.py:60): round half to even, then clip
+__device__ __forceinline__ uint8_t quantize_u8(double v) {
+    v = rint(v);
+    v = v < 0.0 ? 0.0 : (v > 255.0 ? 255.0 : v);
+    return (uint8_t)v;
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
     // xor butterfly: every lane ends with the bit-identical total
 #pragma unroll

@@ -1443,10 +1443,14 @@ oras_sweep_generic_kernel(const SweepArgs A) {
 constexpr int COMBINE_ROWS = 32;
 constexpr int COMBINE_G = 8;
 
+// `egress` (8-bit decode): the updated pixel is also written as clip(round(u)) into
+// the interleaved (F, h, w, C) image (image_from_fields, fileio.py:58-65) -- the last post-smoothing
+// combine of the finest level carries it, so an 8-bit decode needs no pass over the fp64 result.
 __global__ void __launch_bounds__(ST_THREADS_COMBINE)
 oras_combine_kernel(const LevelDev L, const double *__restrict__ scratch, size_t plane,
                     const int *__restrict__ pred, const double *__restrict__ rs,
-                    double *__restrict__ u, int *__restrict__ unit_counter, int y_lo, int y_hi) {
+                    double *__restrict__ u, int *__restrict__ unit_counter, int y_lo, int y_hi,
+                    uint8_t *__restrict__ egress, int channels) {
     __shared__ int s_rn[COMBINE_ROWS], s_rf[COMBINE_ROWS];
     __shared__ size_t s_roff[COMBINE_ROWS][2];
     const int p = blockIdx.z;
@@ -1510,7 +1514,12 @@ oras_combine_kernel(const LevelDev L, const double *__restrict__ scratch, size_t
                 acc += n > 1 ? v10[j] : 0.0;
                 acc += (n > 1 && two_x) ? v11[j] : 0.0;
             }
-            up[(size_t)(y0 + k) * L.w + x] = uu[j] + acc;
+            const double un = uu[j] + acc;
+            up[(size_t)(y0 + k) * L.w + x] = un;
+            if (egress) {
+                const int f = p / channels, c = p - f * channels;
+                egress[((size_t)f * plane + (size_t)(y0 + k) * L.w + x) * channels + c] = quantize_u8(un);
+            }
         }
     }
 }

@@ -596,10 +596,46 @@ __global__ void publish_count_kernel(const unsigned long long *count, unsigned l
 __global__ void __launch_bounds__(ST_THREADS)
 f64_to_u8_kernel(const double *__restrict__ in, size_t n, uint8_t *__restrict__ out) {
     const size_t i = (size_t)blockIdx.x * ST_THREADS + threadIdx.x;
-    if (i < n) {
-        double v = rint(in[i]);  // round half to even, like np.rint
-        v = v < 0.0 ? 0.0 : (v > 255.0 ? 255.0 : v);
-        out[i] = (uint8_t)v;
+    if (i < n) out[i] = quantize_u8(in[i]);
+}
+
+// ---- 8-bit image files as they are on disk ----
+// Mask: the P4 raster (fileio.py:214-216, :226): rows padded to whole bytes, most significant bit
+// first, bit 1 = known pixel -> the byte plane (F, h, w) every kernel reads.  One thread per raster byte.
+__global__ void __launch_bounds__(ST_THREADS)
+unpack_mask_bits_kernel(const uint8_t *__restrict__ bits, size_t nbytes, int w, int row_bytes,
+                        uint8_t *__restrict__ mask) {
+    const size_t i = (size_t)blockIdx.x * ST_THREADS + threadIdx.x;
+    if (i >= nbytes) return;
+    const size_t row = i / (unsigned)row_bytes;          // frame * h + y
+    const int x0 = (int)(i - row * (unsigned)row_bytes) * 8;
+    const unsigned b = bits[i];
+    uint8_t *mp = mask + row * (size_t)w + x0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (x0 + k < w) mp[k] = (b >> (7 - k)) & 1u;
+}
+
+// Pixels: (F, h, w, C) interleaved 8-bit -> (F, C, h, w) float64 (ImageFile.channel_fields, fileio.py:51-55).
+__global__ void __launch_bounds__(ST_THREADS)
+deinterleave_u8_kernel(const uint8_t *__restrict__ px, size_t npix, int C, size_t plane, double *__restrict__ out) {
+    const size_t i = (size_t)blockIdx.x * ST_THREADS + threadIdx.x;   // f * plane + pixel
+    if (i >= npix) return;
+    const size_t f = i / plane, pix = i - f * plane;
+    for (int c = 0; c < C; ++c) out[(f * C + c) * plane + pix] = (double)px[i * C + c];
+}
+
+// image_from_fields (fileio.py:58-65) for the problems whose 8-bit result has not been written by a
+// combine pass (K2b's egress): those that needed no V-cycle (cycles == 0), or all of them (`all`).
+__global__ void __launch_bounds__(ST_THREADS)
+egress_u8_kernel(const double *__restrict__ fields, size_t npix, int C, size_t plane,
+                 const int *__restrict__ cycles, int all, uint8_t *__restrict__ out) {
+    const size_t i = (size_t)blockIdx.x * ST_THREADS + threadIdx.x;
+    if (i >= npix) return;
+    const size_t f = i / plane, pix = i - f * plane;
+    for (int c = 0; c < C; ++c) {
+        const size_t p = f * C + c;
+        if (all || cycles[p] == 0) out[i * C + c] = quantize_u8(fields[p * plane + pix]);
     }
 }
 

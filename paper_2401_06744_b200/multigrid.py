@@ -175,12 +175,13 @@ class Plan:
         wall = time.perf_counter() - t0
         return d_out, (self._reports(raw, wall) if raw is not None else None)
 
-    def _check_host(self, mask, known, out, dtype):
-        """The C side reads F*H*W mask bytes and P*H*W values and writes P*H*W values through raw host
-        pointers: element counts, dtypes and contiguity are checked here (the device path has
-        _dev.check_tensor for the same reason)."""
+    def _check_host(self, mask, known, out, dtype, packed_mask=False):
+        """The C side reads F*H*W mask bytes (F*H*ceil(W/8) for a bit-packed raster) and P*H*W values and
+        writes P*H*W values through raw host pointers: element counts, dtypes and contiguity are checked
+        here (the device path has _dev.check_tensor for the same reason)."""
         n = self.height * self.width
-        for a, name, dt, count in ((mask, "mask", np.uint8, self.frames * n),
+        mask_count = self.frames * (self.height * ((self.width + 7) // 8) if packed_mask else n)
+        for a, name, dt, count in ((mask, "mask", np.uint8, mask_count),
                                    (known, "known", dtype, self.problems * n),
                                    (out, "out", dtype, self.problems * n)):
             if not isinstance(a, np.ndarray) or a.dtype != dt or not a.flags.c_contiguous:
@@ -205,13 +206,17 @@ class Plan:
         wall = time.perf_counter() - t0
         return out, self._reports(raw, wall)
 
-    def solve_host_async(self, mask, known, out, u8: bool = False):
+    def solve_host_async(self, mask, known, out, u8: bool = False, image: bool = False):
         """Enqueue H2D + solve + D2H on the plan's stream and return; `wait()` completes it.
-        The arrays must be C-contiguous, of the exact dtypes, and stay alive until `wait()`."""
-        self._check_host(mask, known, out, np.uint8 if u8 else np.float64)
+        The arrays must be C-contiguous, of the exact dtypes, and stay alive until `wait()`.
+        image=True: the 8-bit file layouts -- mask = P4 raster bits (F,H,ceil(W/8)), known / out =
+        interleaved pixels (F,H,W,C) (see solve_host_image_u8)."""
+        u8 = u8 or image
+        self._check_host(mask, known, out, np.uint8 if u8 else np.float64, packed_mask=image)
         self._t0 = time.perf_counter()
-        _dev.call("b200p_solve_host_u8_async" if u8 else "b200p_solve_host_async", self.handle,
-                  mask.ctypes.data, known.ctypes.data, out.ctypes.data)
+        entry = "b200p_solve_host_image_u8_async" if image else (
+            "b200p_solve_host_u8_async" if u8 else "b200p_solve_host_async")
+        _dev.call(entry, self.handle, mask.ctypes.data, known.ctypes.data, out.ctypes.data)
         self._keep = (mask, known, out)
 
     def wait(self):
@@ -230,6 +235,25 @@ class Plan:
         raw = (_lib.Report * self.problems)()
         t0 = time.perf_counter()
         _dev.call("b200p_solve_host_u8", self.handle, mask.ctypes.data, known_u8.ctypes.data,
+                  out.ctypes.data, C.cast(raw, C.c_void_p))
+        wall = time.perf_counter() - t0
+        return out, self._reports(raw, wall)
+
+
+    def solve_host_image_u8(self, mask_bits, pixels, out=None):
+        """8-bit images as they are on disk: `pixels` (F,H,W,C) uint8 interleaved (ImageFile.pixels,
+        fileio.py:27-37; C = 1 may be (F,H,W)), `mask_bits` (F,H,ceil(W/8)) the P4 raster of
+        read_mask / write_mask (fileio.py:181-230, = np.packbits(mask, axis=-1)).  Returns
+        (image_from_fields(fields).pixels per frame, reports): channel_fields, the rounding, the clip and
+        the interleave run on the device (fileio.py:51-65)."""
+        mask_bits = np.ascontiguousarray(mask_bits, dtype=np.uint8)
+        pixels = np.ascontiguousarray(pixels, dtype=np.uint8)
+        if out is None:
+            out = np.empty(pixels.shape, dtype=np.uint8)
+        self._check_host(mask_bits, pixels, out, np.uint8, packed_mask=True)
+        raw = (_lib.Report * self.problems)()
+        t0 = time.perf_counter()
+        _dev.call("b200p_solve_host_image_u8", self.handle, mask_bits.ctypes.data, pixels.ctypes.data,
                   out.ctypes.data, C.cast(raw, C.c_void_p))
         wall = time.perf_counter() - t0
         return out, self._reports(raw, wall)

@@ -51,14 +51,17 @@ class FramePipeline:
             p.close()
         self.plans = []
 
-    def _check(self, masks, known, out):
+    def _check(self, masks, known, out, image=False):
         c, h, w = self.shape
         if masks.dtype != np.uint8 and masks.dtype != np.bool_:
             raise ValueError("masks must be bool or uint8")
-        if masks.ndim != 3 or masks.shape[1:] != (h, w):
-            raise ValueError(f"masks must be (F,{h},{w}), got {masks.shape}")
-        if known.shape != (masks.shape[0], c, h, w):
-            raise ValueError(f"known must be (F,{c},{h},{w}), got {known.shape}")
+        mshape = (h, (w + 7) // 8) if image else (h, w)
+        if masks.ndim != 3 or masks.shape[1:] != mshape:
+            raise ValueError(f"masks must be (F,{mshape[0]},{mshape[1]}), got {masks.shape}")
+        kshapes = [(masks.shape[0], h, w, c)] + ([(masks.shape[0], h, w)] if c == 1 else []) if image \
+            else [(masks.shape[0], c, h, w)]
+        if known.shape not in kshapes:
+            raise ValueError(f"known must be {kshapes[0]}, got {known.shape}")
         for a, n in ((masks, "masks"), (known, "known"), (out, "out")):
             if a is not None and not a.flags.c_contiguous:
                 raise ValueError(f"{n} must be C-contiguous")
@@ -66,8 +69,10 @@ class FramePipeline:
             raise ValueError(f"frame count {masks.shape[0]} is not a multiple of frames_per_lane "
                              f"{self.frames_per_lane}")
 
-    def submit(self, masks, known, out=None, u8: bool = False):
+    def submit(self, masks, known, out=None, u8: bool = False, image: bool = False):
         """Enqueue a batch: masks (F,H,W) bool/uint8, known (F,C,H,W) float64 (uint8 with u8=True).
+        image=True takes the 8-bit file layouts: masks = P4 raster bits (F,H,ceil(W/8)) uint8, known = interleaved
+        pixels (F,H,W,C) uint8; `out` then holds image_from_fields(...).pixels of every frame (Plan.solve_host_image_u8).
 
         Returns a job dict {"out", "reports", "h2d_bytes", "d2h_bytes"}; its arrays are complete after `flush()` (or once
         later submits have recycled all of its lanes).  Batches submitted back to back keep the
@@ -76,6 +81,7 @@ class FramePipeline:
         per-channel SolveReports of frame f."""
         masks = np.asarray(masks)
         known = np.asarray(known)
+        u8 = u8 or image
         want = np.uint8 if u8 else np.float64
         if known.dtype != want:
             raise ValueError(f"known must have dtype {np.dtype(want)}")
@@ -83,7 +89,7 @@ class FramePipeline:
             out = np.empty(known.shape, dtype=want)
         elif out.dtype != want or out.shape != known.shape:
             raise ValueError("out must match known's shape and dtype")
-        self._check(masks, known, out)
+        self._check(masks, known, out, image=image)
         m8 = masks.view(np.uint8)
         k = self.frames_per_lane
         job = {"out": out, "reports": [None] * masks.shape[0], "h2d_bytes": 0, "d2h_bytes": 0}
@@ -93,7 +99,7 @@ class FramePipeline:
                 self._next += 1
                 self._retire(li)
                 sl = slice(i * k, (i + 1) * k)
-                self.plans[li].solve_host_async(m8[sl], known[sl], out[sl], u8=u8)
+                self.plans[li].solve_host_async(m8[sl], known[sl], out[sl], u8=u8, image=image)
                 self._inflight[li] = (job, i)
         except BaseException:
             self._drain_quietly()
@@ -130,8 +136,8 @@ class FramePipeline:
             self._drain_quietly()
             raise
 
-    def run(self, masks, known, out=None, u8: bool = False):
+    def run(self, masks, known, out=None, u8: bool = False, image: bool = False):
         """submit + flush: returns (out, reports)."""
-        job = self.submit(masks, known, out, u8=u8)
+        job = self.submit(masks, known, out, u8=u8, image=image)
         self.flush()
         return job["out"], job["reports"]

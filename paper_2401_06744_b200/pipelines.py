@@ -109,6 +109,42 @@ def solve_image(problem: InpaintingProblem, name: str = "mg-oras",
     return SolveResult(fields=out[0], reports=reports, elapsed=elapsed)
 
 
+def inpaint_image_u8(pixels, mask, name: str = "mg-oras", cfg: MultigridConfig | None = None,
+                     spacing: float = 1.0, packed: bool = False):
+    """8-bit decode of one image, the body of the reference's `inpaint` command (cli.py:80-95):
+
+        image_from_fields(solve_image(InpaintingProblem(mask, image.channel_fields()), name, cfg).fields).pixels
+
+    `pixels` is ImageFile.pixels -- (H,W) or (H,W,3) uint8 -- and `mask` the boolean known-pixel mask, or with
+    packed=True its P4 raster (H, ceil(W/8)) as read_mask / write_mask hold it on disk (fileio.py:181-230).
+    Returns (pixels_out uint8 of the same shape, reports): unpacking, channel_fields, rounding, clipping and
+    the interleave run on the device (fileio.py:51-65), only 8-bit data crosses PCIe."""
+    _require_built(name)
+    base, mode = split_solver_name(name)
+    single = mode == "single"
+    cfg = cfg or MultigridConfig()
+    cfg = replace(cfg, smoother=base) if single else replace(cfg, smoother=base, mode=mode)
+    px = np.asarray(pixels)
+    if px.dtype != np.uint8 or px.ndim not in (2, 3) or (px.ndim == 3 and px.shape[2] != 3):
+        raise ValueError("pixels must be uint8 with shape (h, w) or (h, w, 3)")     # fileio.py:34-37
+    h, w = px.shape[:2]
+    c = 1 if px.ndim == 2 else 3
+    if packed:
+        bits = np.ascontiguousarray(mask, dtype=np.uint8)
+        if bits.shape != (h, (w + 7) // 8):
+            raise ValueError(f"packed mask must be ({h}, {(w + 7) // 8}), got {bits.shape}")
+    else:
+        m = np.asarray(mask)
+        if m.shape != (h, w):
+            raise ValueError(f"mask shape {m.shape} does not match the image {(h, w)}")
+        bits = np.packbits(m.astype(bool), axis=1)
+    if not np.unpackbits(bits, axis=1)[:, :w].any():
+        raise EmptyMaskError("cannot solve without known pixels")
+    plan = cached_plan(w, h, c, 1, cfg, spacing, single_level=single)
+    out, reports = plan.solve_host_image_u8(bits[None], np.ascontiguousarray(px)[None])
+    return out[0], reports
+
+
 def solve_frames(masks, known, cfg: MultigridConfig | None = None, spacing: float = 1.0):
     """Batch of independent frames: masks (F,H,W), known (F,C,H,W) -> (fields, reports[F][C], elapsed)."""
     cfg = cfg or MultigridConfig()

@@ -5,6 +5,7 @@ container (the reference is not present on the GPU box):
     python tests/golden/make_golden.py            # small vectors  (seconds)
     python tests/golden/make_golden.py --anchors  # + 1080p / 4K anchors (~3 min)
     python tests/golden/make_golden.py --pipelines  # only golden_pipelines.* (comparison pipelines)
+    python tests/golden/make_golden.py --images     # only golden_images.* (8-bit decode, P4 raster, quantiser)
 
 Outputs: golden_small.npz (inputs are regenerated from seeds by the tests; only
 reference OUTPUTS are stored) and anchors.json / anchors_4k_sample.npz."""
@@ -131,6 +132,63 @@ def pipelines():
         json.dump(meta, f, indent=1)
 
 
+IMAGE_CASES = {
+    # name: (w, h, density, seed, channels, block, overlap)
+    "img_rgb_256x192": (256, 192, 0.03, 5, 3, 32, 6),      # warp-per-block sweep, fused 8-bit egress
+    "img_gray_203x131": (203, 131, 0.05, 4, 1, 16, 2),     # odd width (raster rows padded), 16x16 blocks
+    "img_gray_20x30": (20, 30, 0.20, 3, 1, 32, 6),         # single level: the tail pass writes the image
+    "img_rgb_dense_64x48": (64, 48, 0.97, 9, 3, 16, 2),    # nearly everything known
+    "img_rgb_loose_96x64": (96, 64, 0.10, 2, 3, 16, 2, dict(tol_rel=0.5)),  # multilevel, no V-cycle needed: tail pass
+}
+
+
+def images():
+    """8-bit file path: ImageFile.channel_fields -> solve_image -> image_from_fields
+    (fileio.py:51-65) and the P4 raster of write_mask (fileio.py:219-230), all by the reference."""
+    import tempfile
+    from diffpaint import fileio
+    out, meta = {}, {}
+    # quantiser known answers: ties (round half to even), out-of-range, exact integers
+    rng = np.random.default_rng(65)
+    special = np.array([0.5, 1.5, 2.5, 3.5, 126.5, 127.5, 253.5, 254.5, 255.5, -0.5, -0.4999, 255.4999, 1e6, -1e6,
+                        0.0, 255.0, 17.0, 0.49999999999, 254.50000000001, -0.0])
+    f3 = rng.uniform(-40.0, 300.0, size=(3, 16, 24))
+    f3.reshape(-1)[: special.size * 3 : 3] = special
+    f1 = np.floor(rng.uniform(-3.0, 259.0, size=(1, 9, 11))) + 0.5      # nothing but ties
+    out["quant_rgb_fields"], out["quant_rgb_pixels"] = f3, fileio.image_from_fields(f3).pixels
+    out["quant_gray_fields"], out["quant_gray_pixels"] = f1, fileio.image_from_fields(f1).pixels
+    # P4 raster known answer, width not a multiple of 8
+    m = rng.random((13, 21)) < 0.3
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "m.pbm")
+        fileio.write_mask(path, m)
+        raw = open(path, "rb").read()
+        assert np.array_equal(fileio.read_mask(path), m)
+    header = f"P4\n{m.shape[1]} {m.shape[0]}\n".encode()
+    assert raw.startswith(header)
+    out["raster_mask"] = m
+    out["raster_bytes"] = np.frombuffer(raw[len(header):], dtype=np.uint8).reshape(m.shape[0], -1)
+    # whole decodes
+    for name, case in IMAGE_CASES.items():
+        w, h, dens, seed, ch, bs, ov = case[:7]
+        skw = case[7] if len(case) > 7 else {}
+        prob = seeded(w, h, dens, seed, ch)
+        px = prob.known.astype(np.uint8)
+        image = fileio.ImageFile(px[0] if ch == 1 else np.moveaxis(px, 0, 2).copy())
+        assert np.array_equal(image.channel_fields(), prob.known)
+        cfg = dp.MultigridConfig(block_size=bs, overlap=ov, solver=dp.SolverConfig(**skw))
+        res = dp.solve_image(dp.InpaintingProblem(prob.mask, image.channel_fields()), "mg-oras", cfg)
+        out[f"{name}_pixels"] = fileio.image_from_fields(res.fields).pixels
+        # distance of every value to the nearest rounding boundary: pixels closer than 1e-9 may differ
+        out[f"{name}_margin_min"] = np.array(np.abs(res.fields - np.floor(res.fields) - 0.5).min())
+        meta[name] = dict(w=w, h=h, density=dens, seed=seed, channels=ch, block_size=bs, overlap=ov, solver=skw,
+                          iterations=[r.iterations for r in res.reports])
+    np.savez_compressed(os.path.join(HERE, "golden_images.npz"), **out)
+    with open(os.path.join(HERE, "golden_images.json"), "w") as f:
+        json.dump(meta, f, indent=1)
+    print({k: v["iterations"] for k, v in meta.items()})
+
+
 def anchors():
     os.environ["INPAINT_THREADS"] = "0"
     res = {}
@@ -159,11 +217,15 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--anchors", action="store_true")
     ap.add_argument("--pipelines", action="store_true", help="write only golden_pipelines.*")
+    ap.add_argument("--images", action="store_true", help="write only golden_images.* (8-bit file path)")
     a = ap.parse_args()
     if a.pipelines:
         pipelines()
+    elif a.images:
+        images()
     else:
         small()
         pipelines()
+        images()
         if a.anchors:
             anchors()

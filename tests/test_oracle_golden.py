@@ -155,3 +155,27 @@ def test_comparison_pipelines(pgold, pmeta, case, solver):
         assert rep["baseline"] == pytest.approx(want["baseline"], rel=1e-12)
         np.testing.assert_allclose(rep["history"], want["history"], rtol=1e-6, atol=1e-13)
         np.testing.assert_allclose(u, pgold[f"{case}_{solver}_fields"][ch], rtol=0, atol=1e-9)
+
+
+def test_eight_bit_decode_vectors_are_reproduced_by_the_oracle():
+    """golden_images.* (fileio.image_from_fields of the reference's mg-oras solve): the oracle's fields
+    quantise to the reference's bytes, and the stored P4 raster is np.packbits of the stored mask."""
+    g = np.load(os.path.join(G, "golden_images.npz"))
+    with open(os.path.join(G, "golden_images.json")) as f:
+        cases = json.load(f)
+    assert np.array_equal(np.packbits(g["raster_mask"], axis=1), g["raster_bytes"])
+    assert np.array_equal(np.unpackbits(g["raster_bytes"], axis=1)[:, : g["raster_mask"].shape[1]].astype(bool),
+                          g["raster_mask"])
+    for name in ("quant_rgb", "quant_gray"):
+        q = np.clip(np.round(g[f"{name}_fields"]), 0, 255).astype(np.uint8)
+        want = g[f"{name}_pixels"]
+        assert np.array_equal(q[0] if q.shape[0] == 1 else np.moveaxis(q, 0, 2), want)
+    for name, c in cases.items():
+        m, k = oracle.seeded_problem(c["w"], c["h"], c["density"], c["seed"], channels=c["channels"])
+        assert np.array_equal(k, k.astype(np.uint8).astype(np.float64))      # the inputs are 8-bit images
+        cfg = oracle.MultigridConfig(block_size=c["block_size"], overlap=c["overlap"],
+                                     solver=oracle.SolverConfig(**c.get("solver", {})))
+        fields, reps = oracle.solve_image(m, k, 1.0, cfg)
+        assert [r.iterations for r in reps] == c["iterations"]
+        q = np.clip(np.round(fields), 0, 255).astype(np.uint8)
+        assert np.array_equal(q[0] if c["channels"] == 1 else np.moveaxis(q, 0, 2), g[f"{name}_pixels"])
