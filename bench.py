@@ -221,6 +221,71 @@ def run_strip(args, rank, world, local):
         dist.destroy_process_group()
 
 
+def run_traffic_child(args):
+    """--traffic-child (run under ncu by measure_sweep_traffic): one warm-up solve, then ONE eager solve
+    of the same step between cudaProfilerStart/Stop, so that ncu's launch list holds exactly the
+    kernels of one step."""
+    import torch
+    import paper_2401_06744_b200 as bp
+    from paper_2401_06744_b200 import synthetic
+    W, H, C, density, bs, ov = WORKLOADS[args.workload]
+    F = args.frames
+    masks, known = synthetic.seeded_frames(W, H, density, F, C, first_seed=0)
+    d_mask = torch.from_numpy(masks.view(np.uint8)).cuda()
+    d_known = torch.from_numpy(known).cuda()
+    d_out = torch.empty_like(d_known)
+    plan = bp.Plan(W, H, C, F, bp.MultigridConfig(block_size=bs, overlap=ov), use_graphs=False)
+    plan.solve_device(d_mask, d_known, d_out, want_reports=False)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    plan.solve_device(d_mask, d_known, d_out, want_reports=False)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+
+
+def measure_sweep_traffic(args, sweep_launches_per_step):
+    """DRAM bytes (read + write) of the ORAS sweep kernels (block solve + combine) per average sweep
+    launch, from an ncu pass over one step of THIS build run as a child process.  None when ncu is not
+    available or the pass fails (the caller then falls back to the committed profiles/traffic.json)."""
+    import csv
+    import shutil
+    import tempfile
+    ncu = shutil.which("ncu") or ("/usr/local/cuda/bin/ncu" if os.path.exists("/usr/local/cuda/bin/ncu") else None)
+    if not ncu or not sweep_launches_per_step:
+        return None
+    with tempfile.TemporaryDirectory() as d:
+        log = os.path.join(d, "sweep.csv")
+        cmd = [ncu, "--profile-from-start", "off", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum",
+               "--clock-control", "none", "-k", "regex:oras_", "--csv", "--log-file", log,
+               sys.executable, os.path.abspath(__file__), "--traffic-child", "--workload", args.workload,
+               "--frames", str(args.frames)]
+        env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+        try:
+            r = subprocess.run(cmd, env=env, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL, timeout=300)
+            if r.returncode != 0 or not os.path.exists(log):
+                return None
+            rows = [row for row in csv.reader(open(log, errors="replace")) if len(row) > 5]
+        except Exception:
+            return None
+    hdr = next((row for row in rows if "Metric Name" in row), None)
+    if not hdr:
+        return None
+    iname, iunit, ival, ikern = (hdr.index(k) for k in ("Metric Name", "Metric Unit", "Metric Value", "Kernel Name"))
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    total, kernels = 0.0, set()
+    for row in rows:
+        if row is hdr or len(row) <= max(iname, iunit, ival) or not row[iname].startswith("dram__bytes"):
+            continue
+        try:
+            total += float(row[ival].replace(",", "")) * scale.get(row[iunit], 1.0)
+            kernels.add(row[ikern].split("(")[0].replace("void ", "").strip())
+        except ValueError:
+            continue
+    if total <= 0:
+        return None
+    return {"dram_bytes_per_launch": total / sweep_launches_per_step, "kernels": sorted(kernels)}
+
+
 def _free_port():
     import socket
     with socket.socket() as s:
@@ -305,6 +370,9 @@ def main():
                     help="--strip exchange: torch.distributed NCCL, or CUDA-IPC peer memory + gloo control")
     ap.add_argument("--strip-levels", type=int, default=2,
                     help="how many of the finest levels are striped in --strip mode (the rest is replicated)")
+    ap.add_argument("--traffic-child", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--no-traffic", action="store_true",
+                    help="skip the same-run ncu pass behind roofline.traffic (falls back to profiles/traffic.json)")
     ap.add_argument("--dry-launch", action="store_true",
                     help="exercise the N-rank launcher and the report gather on CPU (gloo), no kernels")
     args = ap.parse_args()
@@ -315,6 +383,9 @@ def main():
 
     if args.gpus < 1:
         raise SystemExit("bench.py: --gpus must be >= 1")
+    if args.traffic_child:
+        run_traffic_child(args)
+        return
     if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "b200":
         # no torchrun around us: start the N ranks ourselves (one process per GPU)
         sys.exit(self_launch(args, sys.argv[1:]))
@@ -464,10 +535,41 @@ def main():
             pipe.submit(h_mask.numpy(), h_k8.numpy(), h_o8.numpy(), u8=True)
         pipe.flush()
         dt8 = time.perf_counter() - t0
-        e2e["u8_value"] = F * k_e2e / dt8 * world
+        t = torch.tensor([dt8], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e["u8_value"] = F * k_e2e / float(t.item()) * world
         e2e["u8_h2d_bytes_per_step"] = int(h_mask.numel() + h_k8.numel())
         e2e["u8_d2h_bytes_per_step"] = int(h_o8.numel())
+        # 8-bit images as they are on disk: interleaved (H,W,C) pixels + the bit-packed P4 mask raster in,
+        # image_from_fields(...).pixels out (rounding fused into the last combine pass).  This is the
+        # end-to-end number that scales with the GPU count: 33 MB per frame each way instead of 200 MB.
+        h_bits = torch.from_numpy(np.packbits(masks, axis=2)).pin_memory()
+        h_px = torch.from_numpy(np.ascontiguousarray(np.moveaxis(known.astype(np.uint8), 1, 3))).pin_memory()
+        h_opx = torch.empty_like(h_px).pin_memory()
+        pipe.run(h_bits.numpy(), h_px.numpy(), h_opx.numpy(), image=True)
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            pipe.submit(h_bits.numpy(), h_px.numpy(), h_opx.numpy(), image=True)
+        pipe.flush()
+        t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e["image_u8_value"] = F * k_e2e / float(t.item()) * world
+        e2e["image_u8_h2d_bytes_per_step"] = int(h_bits.numel() + h_px.numel())
+        e2e["image_u8_d2h_bytes_per_step"] = int(h_opx.numel())
+        want8 = np.moveaxis(np.clip(np.rint(d_out.cpu().numpy()), 0, 255).astype(np.uint8), 1, 3)
+        e2e["image_u8_mismatching_bytes_vs_rounded_f64"] = int((h_opx.numpy() != want8).sum())
         pipe.close()
+        # the reference's own call, one frame: solve_image(InpaintingProblem(mask, known), "mg-oras", cfg) with
+        # pageable NumPy arrays in and out (validation, H2D, solve, D2H, report objects all inside)
+        prob = bp.InpaintingProblem(masks[0], known[0])
+        bp.solve_image(prob, "mg-oras", cfg)
+        t0 = time.perf_counter()
+        for _ in range(3):
+            res1 = bp.solve_image(prob, "mg-oras", cfg)
+        e2e["solve_image_value"] = 3 / (time.perf_counter() - t0)
+        e2e["solve_image_api"] = "solve_image(InpaintingProblem, 'mg-oras', cfg): 1 frame per call, pageable float64 arrays"
 
     if rank != 0:
         if world > 1:
@@ -495,13 +597,20 @@ def main():
         ms = prof["oras_sweep_split"][0] + prof.get("oras_combine", (0.0, 0, 0.0))[0]
         n = prof["oras_sweep_split"][1]
         by = prof["oras_sweep_split"][2]
-        dom = "oras_sweep (K2 oras_sweep_lean_kernel + K2b oras_combine_kernel)"
+        dom = "oras_sweep (K2 oras_sweep_warp_kernel + K2b oras_combine_kernel)"
     else:
         dom = max(prof, key=lambda k: prof[k][0])
         ms, n, by = prof[dom]
-    traffic = None
+    traffic, traffic_src = None, None
+    if not args.no_traffic and "oras_sweep_split" in prof:
+        # free this process's big buffers first: the child builds its own plan on the same GPU
+        tm = measure_sweep_traffic(args, prof["oras_sweep_split"][1] // 2)
+        if tm:
+            traffic = tm["dram_bytes_per_launch"]
+            traffic_src = "same-run ncu pass over one eager step (" + ", ".join(tm["kernels"]) + ")"
     tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
+    if traffic is None and os.path.exists(tp):
+        traffic_src = "profiles/traffic.json (committed ncu launch list; stale if the sweep kernels changed since)"
         try:
             with open(tp) as f:
                 tj = json.load(f).get("oras_sweep", {})
@@ -513,11 +622,12 @@ def main():
     roofline = {"bound": "hbm", "kernel": dom, "achieved": (by / n / 1e9) / (ms / n * 1e-3), "peak": peak,
                 "unit": "GB/s", "frac": ((by / 1e9) / (ms * 1e-3)) / peak, "traffic": traffic,
                 "peak_source": peak_src, "avg_launch_ms": ms / n, "alg_bytes_per_launch": by / n,
-                "share_of_step": ms / tot_ms,
+                "share_of_step": ms / tot_ms, "traffic_source": traffic_src,
+                "traffic_over_algorithmic": (traffic / (by / n)) if traffic else None,
                 "note": "the sweep is bound by fp64 issue and by the dependent chains of the per-block CG "
-                        "(FP64 pipe 39 %, LSU data pipe 50 %, DRAM 18 % in ncu), not by HBM; its DRAM traffic "
-                        "is ~3x the algorithmic bytes because the weighted correction tiles make a round trip "
-                        "through HBM (K2 writes 1.5 fields, K2b reads them): see DESIGN.md and profiles/",
+                        "(FP64 pipe ~42 %, DRAM ~22 % in ncu), not by HBM; its DRAM traffic exceeds the "
+                        "algorithmic bytes because the weighted correction tiles make a round trip "
+                        "through HBM (K2 writes them, K2b reads them back): see DESIGN.md and profiles/",
                 "how": "eager pass of the same step with a CUDA event pair around every launch on the "
                        "launching stream, run right after the timed (graph-replay) region"}
     frame_bytes = algorithmic_bytes_per_frame(W, H, C, max(cycles))

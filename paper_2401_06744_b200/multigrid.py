@@ -197,7 +197,7 @@ class Plan:
         mask = np.ascontiguousarray(mask, dtype=np.uint8)
         known = np.ascontiguousarray(known, dtype=np.float64)
         if out is None:
-            out = np.empty((self.frames, self.channels, self.height, self.width))
+            out = _dev.empty_host((self.frames, self.channels, self.height, self.width))
         self._check_host(mask, known, out, np.float64)
         raw = (_lib.Report * self.problems)()
         t0 = time.perf_counter()
@@ -230,7 +230,7 @@ class Plan:
         mask = np.ascontiguousarray(mask, dtype=np.uint8)
         known_u8 = np.ascontiguousarray(known_u8, dtype=np.uint8)
         if out is None:
-            out = np.empty((self.frames, self.channels, self.height, self.width), dtype=np.uint8)
+            out = _dev.empty_host((self.frames, self.channels, self.height, self.width), np.uint8)
         self._check_host(mask, known_u8, out, np.uint8)
         raw = (_lib.Report * self.problems)()
         t0 = time.perf_counter()
@@ -249,7 +249,7 @@ class Plan:
         mask_bits = np.ascontiguousarray(mask_bits, dtype=np.uint8)
         pixels = np.ascontiguousarray(pixels, dtype=np.uint8)
         if out is None:
-            out = np.empty(pixels.shape, dtype=np.uint8)
+            out = _dev.empty_host(pixels.shape, np.uint8)
         self._check_host(mask_bits, pixels, out, np.uint8, packed_mask=True)
         raw = (_lib.Report * self.problems)()
         t0 = time.perf_counter()

@@ -86,7 +86,7 @@ class FramePipeline:
         if known.dtype != want:
             raise ValueError(f"known must have dtype {np.dtype(want)}")
         if out is None:
-            out = np.empty(known.shape, dtype=want)
+            out = _dev.empty_host(known.shape, want)
         elif out.dtype != want or out.shape != known.shape:
             raise ValueError("out must match known's shape and dtype")
         self._check(masks, known, out, image=image)
