@@ -32,7 +32,8 @@ extern "C" {
 #endif
 
 #define B200P_MAX_LEVELS 32
-#define B200P_MAX_HISTORY 128  /* v_cycles_max + 1 entries are kept, capped here */
+#define B200P_ABI_VERSION 2    /* 2: b200p_config lost `spec_cycles`; history_len counts past the cap; image entry points */
+#define B200P_MAX_HISTORY 128  /* history entries STORED per report; history_len may be larger (see b200p_report) */
 #define B200P_MAX_BLOCK 64     /* largest supported block edge */
 
 enum {
@@ -61,7 +62,6 @@ typedef struct b200p_config {
     int local_max_iters;          /* SolverConfig.local_max_iters, 0 = None -> 4*bh*bw */
     int use_graphs;               /* 1: the whole solve is one CUDA graph (WHILE node for the V-cycle loop);
                                      0: eager launches, the host reads the loop condition after every cycle */
-    int spec_cycles;              /* unused since the single-graph solve (kept for ABI stability) */
     int mode;                     /* MultigridConfig.mode: 0 "full_multigrid" (mg-oras), 1 "multilevel" (ml-oras,
                                      cascade with every level smoothed to tol_rel, multigrid.py:412-418, :449-464),
                                      2 "single": oras_solve on the finest level only (solvers.py:427-485) */
@@ -76,7 +76,8 @@ typedef struct b200p_report {
     int iterations;               /* V-cycles */
     int converged;
     int fine_smoother_iterations;
-    int history_len;
+    int history_len;              /* values recorded (iterations + 1 for mg-*, one per sweep / step for the
+                                     comparison pipelines); only the first B200P_MAX_HISTORY are stored below */
     double final_rel_residual;
     double baseline_residual;
     double init_residual;
@@ -113,6 +114,8 @@ enum { B200P_XCHG_SUM_RS = 1, B200P_XCHG_MAX_FLAGS = 2, B200P_XCHG_HALO_U = 3, B
 typedef int (*b200p_exchange_fn)(void *user, int kind, void *d_ptr, void *stream);
 
 const char *b200p_last_error(void);
+/* B200P_ABI_VERSION of the built library (bindings compare it with the header they were written for). */
+int b200p_abi_version(void);
 int b200p_device_count(void);
 /* CUDA's current device is per host thread: worker threads that drive their own plan
  * (pipeline lanes) select the device of their process first. */

@@ -33,7 +33,7 @@ class Config(C.Structure):
         ("value_downsampling", C.c_int),
         ("coarse_tol", C.c_double), ("coarse_max_iters", C.c_int),
         ("tol_rel", C.c_double), ("alpha", C.c_double), ("eta", C.c_double),
-        ("local_max_iters", C.c_int), ("use_graphs", C.c_int), ("spec_cycles", C.c_int),
+        ("local_max_iters", C.c_int), ("use_graphs", C.c_int),
         ("mode", C.c_int), ("max_outer_iters", C.c_int),
         ("smoother", C.c_int), ("smoother_cg_iters", C.c_int),
     ]
@@ -145,7 +145,9 @@ SIGNATURES = {
     "b200p_memcpy_d2h": (_I, [_VP, _VP, _I64]),
     "b200p_memset": (_I, [_VP, _I, _I64]),
     "b200p_device_synchronize": (_I, []),
+    "b200p_abi_version": (_I, []),
 }
+ABI_VERSION = 2  # B200P_ABI_VERSION these bindings (struct layouts above) were written for
 
 
 def lib():
@@ -157,6 +159,10 @@ def lib():
                 f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
                 "(there is no CPU fallback)")
         L = C.CDLL(LIB_PATH)
+        got = L.b200p_abi_version() if hasattr(L, "b200p_abi_version") else 1
+        if got != ABI_VERSION:
+            raise ImportError(f"{LIB_PATH} has ABI version {got}, these bindings need {ABI_VERSION}: rebuild it "
+                              "(`make -C paper_2401_06744_b200/csrc`)")
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(L, name)
             fn.restype = res

@@ -379,11 +379,9 @@ __global__ void fmg_control_kernel(int P, int stage, const double *rs, double to
         cycles[p] = c;
         const double r = rn / denom[p];
         rel[p] = r;
-        const int hl = histlen[p];
-        if (hl < B200P_MAX_HISTORY) {
-            hist[(size_t)p * B200P_MAX_HISTORY + hl] = r;
-            histlen[p] = hl + 1;
-        }
+        const int hl = histlen[p];   // counts every recorded value; the first B200P_MAX_HISTORY are stored
+        if (hl < B200P_MAX_HISTORY) hist[(size_t)p * B200P_MAX_HISTORY + hl] = r;
+        histlen[p] = hl + 1;
         const int act = (r > tol && c < cycles_max) ? 1 : 0;
         active[p] = act;
         mine |= act;
@@ -459,11 +457,9 @@ __global__ void ml_gate_kernel(int P, const double *rs, double tol, int max_unit
     const double r = rn / d;
     rel[p] = r;
     if (record) {
-        const int hl = histlen[p];
-        if (hl < B200P_MAX_HISTORY) {
-            hist[(size_t)p * B200P_MAX_HISTORY + hl] = r;
-            histlen[p] = hl + 1;
-        }
+        const int hl = histlen[p];   // counts every recorded value; the first B200P_MAX_HISTORY are stored
+        if (hl < B200P_MAX_HISTORY) hist[(size_t)p * B200P_MAX_HISTORY + hl] = r;
+        histlen[p] = hl + 1;
     }
     if (r2 == 0.0 || rn <= tol * d || sweeps[p] >= max_units) gate[p] = 0;
     else atomicOr(any, 1);
@@ -1681,6 +1677,8 @@ extern "C" {
 
 const char *b200p_last_error(void) { return g_err.c_str(); }
 
+int b200p_abi_version(void) { return B200P_ABI_VERSION; }
+
 int b200p_device_count(void) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) {
@@ -1721,7 +1719,6 @@ void b200p_config_default(b200p_config *c, int width, int height, int channels) 
     c->eta = 1e-5;
     c->local_max_iters = 0;
     c->use_graphs = 1;
-    c->spec_cycles = 1;
     c->mode = 0;
     c->max_outer_iters = 10000;
     c->smoother = 0;
@@ -1826,7 +1823,6 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
 
     b200p_plan *pl = new b200p_plan();
     pl->cfg = c;
-    if (pl->cfg.spec_cycles < 1) pl->cfg.spec_cycles = 1;
     pl->F = c.frames;
     pl->C = c.channels;
     pl->P = c.frames * c.channels;

@@ -154,8 +154,8 @@ __global__ void cg_after_init_kernel(int P, CgState S, int denom_mode, double to
         S.denom[p] = d;
         stop = tol * d;
         S.rel[p] = d == 0.0 ? 0.0 : rn / d;
-        if (record && d != 0.0 && S.histlen[p] < S.hist_cap) {
-            S.hist[(size_t)p * S.hist_cap + S.histlen[p]] = rn / d;
+        if (record && d != 0.0) {
+            if (S.histlen[p] < S.hist_cap) S.hist[(size_t)p * S.hist_cap + S.histlen[p]] = rn / d;
             S.histlen[p] += 1;
         }
     }
@@ -188,8 +188,8 @@ __global__ void cg_after_update_kernel(int P, CgState S, int max_steps, int reco
     if (denom_mode != 0) {
         const double d = S.denom[p];
         S.rel[p] = rn / d;
-        if (record && S.histlen[p] < S.hist_cap) {
-            S.hist[(size_t)p * S.hist_cap + S.histlen[p]] = rn / d;
+        if (record) {
+            if (S.histlen[p] < S.hist_cap) S.hist[(size_t)p * S.hist_cap + S.histlen[p]] = rn / d;
             S.histlen[p] += 1;
         }
     }

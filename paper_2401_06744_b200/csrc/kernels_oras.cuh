@@ -1611,8 +1611,8 @@ coarse_solve_kernel(const CoarseArgs A) {
             if (rn == 0.0) break;  // denom == 0 -> (0, 0.0), multigrid.py:302-303
             stop = A.tol * rn;
         }
-        if (A.hist && tid == 0 && sweeps < A.hist_cap) {
-            A.hist[(size_t)p * A.hist_cap + sweeps] = rn / denom;
+        if (A.hist && tid == 0) {
+            if (sweeps < A.hist_cap) A.hist[(size_t)p * A.hist_cap + sweeps] = rn / denom;
             A.histlen[p] = sweeps + 1;
         }
         if (rs == 0.0 || rn <= stop || sweeps >= A.max_sweeps) break;

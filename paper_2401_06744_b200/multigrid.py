@@ -64,7 +64,7 @@ class Plan:
     """RAII wrapper of a ``b200p_plan`` (geometry, scratch, CUDA graphs)."""
 
     def __init__(self, width, height, channels=1, frames=1, cfg=None, spacing=1.0,
-                 use_graphs=True, spec_cycles=1, single_level=False):
+                 use_graphs=True, single_level=False):
         cfg = cfg or MultigridConfig()
         _require_hot_path(cfg)
         _dev.require_cuda()
@@ -80,7 +80,6 @@ class Plan:
         c.tol_rel, c.alpha, c.eta = float(s.tol_rel), float(s.alpha), float(s.local_tol_fraction)
         c.local_max_iters = int(s.local_max_iters or 0)
         c.use_graphs = 1 if use_graphs else 0
-        c.spec_cycles = int(spec_cycles)
         # single_level: oras_solve on the finest level only (the "oras" pipeline, solvers.py:427-485)
         c.mode = 2 if single_level else (1 if cfg.mode == "multilevel" else 0)
         self.single_level = bool(single_level)
@@ -154,11 +153,24 @@ class Plan:
         for r in raw:
             reps.append(SolveReport(
                 solver=name, iterations=r.iterations, final_rel_residual=r.final_rel_residual,
-                wall_time=wall, history=list(r.history[: r.history_len]) or [r.final_rel_residual],
+                wall_time=wall, history=self._history(r),
                 converged=bool(r.converged),
                 baseline_residual=r.baseline_residual, init_residual=r.init_residual,
                 fine_smoother_iterations=r.fine_smoother_iterations))
         return reps
+
+    @staticmethod
+    def _history(r):
+        """The report stores the first B200P_MAX_HISTORY values; a longer history (comparison pipelines that
+        record per sweep / step, v_cycles_max > 127) is returned as its stored head with the final value last,
+        so that history[-1] == final_rel_residual still holds, and a warning says how many were dropped."""
+        cap = len(r.history)
+        if r.history_len <= cap:
+            return list(r.history[: r.history_len]) or [r.final_rel_residual]
+        import warnings
+        warnings.warn(f"residual history truncated: {r.history_len} values recorded, the first {cap - 1} and "
+                      f"the last are kept (B200P_MAX_HISTORY = {cap})", RuntimeWarning, stacklevel=3)
+        return list(r.history[: cap - 1]) + [r.final_rel_residual]
 
     def solve_device(self, d_mask, d_known, d_out=None, want_reports=True):
         """Device-resident solve: mask (F,H,W) uint8, known (F,C,H,W) float64 CUDA tensors."""

@@ -115,9 +115,22 @@ def build_weights(partition: BlockPartition) -> BlockWeights:
                         _weights(p.height, p.block_size, p.overlap, p.ny))
 
 
+def _inside(field: np.ndarray, rect: BlockRect) -> tuple:
+    h, w = field.shape
+    if min(rect.x0, rect.y0) < 0 or rect.x0 + rect.w > w or rect.y0 + rect.h > h:
+        raise ValueError(f"block {rect} exceeds field bounds {h}x{w}")
+    return slice(rect.y0, rect.y0 + rect.h), slice(rect.x0, rect.x0 + rect.w)
+
+
 def restrict_to_block(field: np.ndarray, rect: BlockRect) -> np.ndarray:
-    return field[rect.y0:rect.y0 + rect.h, rect.x0:rect.x0 + rect.w]
+    """R_i u: a COPY of the block's sub-rectangle (partition.py:171-176); host-side helper, the kernels
+    gather straight from the level field."""
+    return np.array(field[_inside(field, rect)])
 
 
-def extend_add_weighted(target: np.ndarray, rect: BlockRect, local: np.ndarray, weights: np.ndarray):
-    target[rect.y0:rect.y0 + rect.h, rect.x0:rect.x0 + rect.w] += weights * local
+def extend_add_weighted(field: np.ndarray, rect: BlockRect, weights: np.ndarray, local: np.ndarray) -> None:
+    """field += R_i^T (weights * local), in place (partition.py:179-188; same argument order)."""
+    window = _inside(field, rect)
+    if local.shape != (rect.h, rect.w) or weights.shape != (rect.h, rect.w):
+        raise ValueError("local field / weights do not match the block extent")
+    field[window] += weights * local

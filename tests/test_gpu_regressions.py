@@ -96,3 +96,26 @@ def test_plan_cache_eviction_keeps_live_hierarchies_valid():
     assert rep.iterations == ro.iterations and np.abs(u - uo).max() <= 1e-9
     bp.clear_plan_cache()
     assert len(hier) == n        # clearing drops references only
+
+
+def test_long_histories_are_truncated_loudly():
+    """The report stores B200P_MAX_HISTORY = 128 values; the single-level Schwarz iteration records one per
+    sweep.  A longer history comes back as its first 127 values plus the final one (history[-1] ==
+    final_rel_residual, as in the reference) with a RuntimeWarning; short ones are unchanged."""
+    import warnings
+    m, k = oracle.seeded_problem(320, 240, 0.003, 3, channels=1)
+    cfg_b = bp.MultigridConfig(block_size=16, overlap=2, solver=bp.SolverConfig(tol_rel=1e-6, max_outer_iters=400))
+    with warnings.catch_warnings(record=True) as seen:
+        warnings.simplefilter("always")
+        res = bp.solve_image(bp.InpaintingProblem(m, k), "oras", cfg_b)
+    ref, ro = oracle.oras_solve(m, k[0], 1.0, 16, 2, oracle.SolverConfig(tol_rel=1e-6, max_outer_iters=400))
+    rep = res.reports[0]
+    assert rep.iterations == ro["iterations"] > 128
+    assert any(issubclass(w.category, RuntimeWarning) and "history truncated" in str(w.message) for w in seen)
+    assert len(rep.history) == 128 and rep.history[-1] == rep.final_rel_residual
+    np.testing.assert_allclose(rep.history[:127], ro["history"][:127], rtol=5e-3)  # 200+ sweeps: local stop decisions drift
+    assert np.abs(res.fields[0] - ref).max() <= 1e-3
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")
+        short = bp.solve_image(bp.InpaintingProblem(m, k), "mg-oras", cfg_b)
+    assert len(short.reports[0].history) == short.reports[0].iterations + 1

@@ -425,7 +425,9 @@ def test_bench_suites_on_the_cuda_path():
     leak = {r["solver"]: r["mse_vs_reference"] for r in suites.downsampling_suite(cfg)}
     assert leak["ml-oras+modified"] < leak["ml-oras+naive"]
     arows = suites.alpha_suite(img, cfg, alphas=(0.1, 0.5, 5.0))
-    assert [r["alpha"] for r in arows] == [0.1, 0.5, 5.0] and all(r["rel_residual"] <= 1e-3 for r in arows)
+    # the Schwarz-based solvers of the reference's sweep (bench.py:110): single-level oras and mg-oras per alpha
+    assert [(r["alpha"], r["solver"]) for r in arows] == [(a, s) for a in (0.1, 0.5, 5.0) for s in ("oras", "mg-oras")]
+    assert all(r["rel_residual"] <= 1e-3 for r in arows)
     sizes = ((240, 135), (960, 540), (1920, 1080))
     rrows = [r for r in suites.resolution_suite(bp.MultigridConfig(), sizes=sizes, solvers=("mg-oras",))]
     t = [r["wall_time_s"] for r in rrows]
@@ -434,6 +436,24 @@ def test_bench_suites_on_the_cuda_path():
     assert 0.0 < slope < 1.5  # sub-linear while the small sizes are launch-latency bound
     ranked = suites.compare_rows(bp.InpaintingProblem(synthetic.random_mask(192, 128, 0.05, 1), img), cfg)
     assert ranked[0]["mse_vs_reference"] <= ranked[-1]["mse_vs_reference"]
+    # batched cells == the reference's one-call-per-cell harness: same iterations, residuals and fields
+    for r in rows:
+        if r["solver"] == "mg-oras":
+            one = bp.solve_image(bp.InpaintingProblem(synthetic.random_mask(192, 128, r["density"], 0), img), "mg-oras", cfg)
+            assert r["iterations"] == one.iterations and r["rel_residual"] == one.final_rel_residual
+    # small images are measured against the exact discrete solution (the dense oracle's role, oracle.py:38-80)
+    small = bp.InpaintingProblem(synthetic.random_mask(96, 64, 0.08, 2), img[:, :64, :96])
+    truth = suites.direct_truth(small)
+    tight = bp.solve_image(small, "mg-oras", bp.MultigridConfig(block_size=16, overlap=2,
+                                                              solver=bp.SolverConfig(tol_rel=1e-12))).fields
+    assert np.abs(tight - truth).max() < 1e-7          # tests/test_multigrid.py:328-334 (MSE <= 1e-10)
+    sranked = suites.compare_rows(small, cfg)
+    assert [r["solver"] for r in sranked] != [] and sranked[0]["mse_vs_reference"] <= sranked[-1]["mse_vs_reference"]
+    assert all(r["mse_vs_reference"] < 1.0 for r in sranked)
+    text = suites.format_report_csv(sranked[:2] + allrows[:1])
+    lines = text.split("\r\n")
+    assert lines[0] == "solver,width,height,density,seed,alpha,tol,iterations,rel_residual,mse_vs_reference,psnr,wall_time_s"
+    assert lines[3].split(",")[9:11] == ["", ""] and len(lines) == 5 and lines[4] == ""
 
 
 def test_async_api_state_and_streaming_pipeline():

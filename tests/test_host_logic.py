@@ -180,3 +180,65 @@ def test_synthetic_inputs_match_oracle_recipe():
     ms, ks = synthetic.seeded_frames(32, 24, 0.2, 3, 2, first_seed=5)
     assert ms.shape == (3, 24, 32) and ks.shape == (3, 2, 24, 32)
     assert np.array_equal(ms[1], synthetic.random_mask(32, 24, 0.2, 6))
+
+
+def test_report_csv_matches_the_reference_writer(tmp_path, diffpaint):
+    """suites.format_report_csv == fileio.write_report_csv (fileio.py:233-275) byte for byte."""
+    from paper_2401_06744_b200 import suites
+    rows = [
+        {"solver": "mg-oras", "width": 3840, "height": 2160, "density": 0.02, "seed": 0, "alpha": 0.5, "tol": 1e-3,
+         "iterations": 2, "rel_residual": 1.2895951277968e-4, "mse_vs_reference": 3.25e-7, "psnr": 112.98765,
+         "wall_time_s": 0.0035801},
+        {"solver": "ml-oras+naive", "width": 256, "height": 256, "density": 0.0123456789, "seed": 3, "alpha": 2.0,
+         "tol": 1e-10, "iterations": 17, "rel_residual": 9.9e-11, "mse_vs_reference": None, "psnr": None,
+         "wall_time_s": 1.5},
+        {"solver": "cg", "width": 20, "height": 30, "density": 0.2, "seed": 1, "alpha": 0.5, "tol": 1e-6,
+         "iterations": 100, "rel_residual": 0.5, "mse_vs_reference": 0.0, "psnr": float("inf"), "wall_time_s": 2},
+    ]
+    from diffpaint import fileio
+    path = tmp_path / "ref.csv"
+    fileio.write_report_csv(path, rows)
+    assert suites.format_report_csv(rows) == open(path, newline="").read()
+    assert suites.CSV_HEADER == fileio.CSV_HEADER and suites.ROW_FIELDS == fileio.CSV_FIELDS
+    mine = tmp_path / "mine.csv"
+    suites.write_report_csv(mine, rows)
+    assert open(mine, "rb").read() == open(path, "rb").read()
+
+
+def test_direct_truth_matches_the_reference_dense_oracle(diffpaint):
+    """suites.direct_truth (sparse LU) == oracle.solve (dense LU, oracle.py:38-80) on small problems."""
+    from paper_2401_06744_b200 import suites
+    for (w, h, dens, seed, ch, spacing) in [(24, 17, 0.15, 1, 1, 1.0), (31, 40, 0.05, 2, 3, 0.5), (8, 8, 0.5, 3, 1, 2.0)]:
+        m, k = oracle.seeded_problem(w, h, dens, seed, channels=ch)
+        got = suites.direct_truth(bp.InpaintingProblem(m, k, spacing))
+        ref_prob = diffpaint.InpaintingProblem(m, k, spacing)
+        from diffpaint import oracle as dense
+        want = np.stack([dense.solve(ref_prob, c) for c in range(ch)])
+        assert np.abs(got - want).max() <= 1e-9
+    with pytest.raises(bp.EmptyMaskError):
+        suites.direct_truth(bp.InpaintingProblem(np.zeros((4, 4), bool), np.zeros((1, 4, 4))))
+    with pytest.raises(ValueError, match="refusing"):
+        suites.direct_truth(bp.InpaintingProblem(np.ones((200, 200), bool), np.zeros((1, 200, 200))))
+
+
+def test_block_restriction_and_weighted_extension_like_the_reference(diffpaint):
+    """partition.py:171-188: restrict_to_block copies, extend_add_weighted(field, rect, weights, local)
+    accumulates in place, both refuse blocks outside the field; sum_i R_i^T (w_i * R_i u) == u."""
+    from diffpaint import partition as rp
+    part, rpart = bp.build_partition(70, 45, 16, 4), rp.build_partition(70, 45, 16, 4)
+    wts, rw = bp.build_weights(part), rp.build_weights(rpart)
+    u = np.random.default_rng(3).normal(size=(45, 70))
+    acc, racc = np.zeros_like(u), np.zeros_like(u)
+    for i, (rect, rrect) in enumerate(zip(part.rects(), rpart.rects())):
+        loc, rloc = bp.restrict_to_block(u, rect), rp.restrict_to_block(u, rrect)
+        assert np.array_equal(loc, rloc) and loc.base is None          # a copy, not a view
+        bp.extend_add_weighted(field=acc, rect=rect, weights=wts.block(part, i), local=loc)
+        rp.extend_add_weighted(racc, rrect, rw.block(rpart, i), rloc)
+    assert np.array_equal(acc, racc) and np.abs(acc - u).max() <= 1e-12
+    bad = bp.BlockRect(60, 40, 16, 16, True, False, True, False)
+    with pytest.raises(ValueError, match="exceeds field bounds"):
+        bp.restrict_to_block(u, bad)
+    with pytest.raises(ValueError, match="exceeds field bounds"):
+        bp.extend_add_weighted(acc, bad, np.ones((16, 16)), np.ones((16, 16)))
+    with pytest.raises(ValueError, match="do not match the block extent"):
+        bp.extend_add_weighted(acc, part.rect(0), np.ones((3, 3)), np.ones((16, 16)))
