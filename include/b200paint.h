@@ -284,6 +284,11 @@ int b200p_plan_oras_sweeps(b200p_plan *plan, int level, const double *d_b, doubl
 int b200p_plan_solve_blocks(b200p_plan *plan, int level, const double *d_r, double target_sq,
                             double *d_v, void *stream);
 
+/* BlockSolver.scatter_weighted (solvers.py:307-314): d_v (frames*C, nblocks, bh, bw) UNWEIGHTED local
+ * corrections -> d_field (frames*C, h, w) = sum_i R_i^T ((v_i * wy_i) * wx_i), summed per pixel in ascending
+ * block order like np.bincount.  Runs the sweeps' own combine kernel (K2b) on a zero field, in isolation. */
+int b200p_plan_scatter_weighted(b200p_plan *plan, int level, const double *d_v, double *d_field, void *stream);
+
 /* StencilOperator.apply / residual (core.py:100-110) on one (h,w) field. */
 int b200p_apply(const uint8_t *d_mask, int h, int w, double spacing, const double *d_u,
                 double *d_out, void *stream);

@@ -123,6 +123,7 @@ SIGNATURES = {
     "b200p_plan_cascade": (_I, [_VP, _VP, _VP]),
     "b200p_plan_vcycle": (_I, [_VP, _I, _VP, _VP, _VP, _VP]),
     "b200p_plan_oras_sweeps": (_I, [_VP, _I, _VP, _VP, _I, _D, _I, _VP, _VP, _VP]),
+    "b200p_plan_scatter_weighted": (_I, [_VP, _I, _VP, _VP, _VP]),
     "b200p_plan_solve_blocks": (_I, [_VP, _I, _VP, _D, _VP, _VP]),
     "b200p_apply": (_I, [_VP, _I, _I, _D, _VP, _VP, _VP]),
     "b200p_residual": (_I, [_VP, _I, _I, _D, _VP, _VP, _VP, _VP]),

@@ -2786,6 +2786,24 @@ int b200p_plan_oras_sweeps(b200p_plan *pl, int level, const double *d_b, double 
     int rc;
     if ((rc = launch_set_int(pl, pl->d_gate, pl->P, 1, st))) return rc;
     if ((rc = launch_set_int(pl, pl->d_sweeps, pl->P, 0, st))) return rc;
+    if (path == 0 && stop_norm == 0.0 && L.nblocks == 1 && level == (int)pl->lev.size() - 1) {
+        // a single-block coarsest level is what the solve drivers hand to K7 (sweeps looped in one kernel,
+        // multigrid.py:264-279 with stop_norm = 0): the default path of the stage call runs the same kernel,
+        // so that a single-level V-cycle and its sweeps are the same arithmetic (tests/test_multigrid.py:218-233)
+        if ((rc = launch_coarse(pl, L, d_u, d_b, false, 2, 0.0, max_sweeps, nullptr, pl->d_sweeps, 0, st))) return rc;
+        if ((rc = launch_norm(pl, L, d_u, d_b, false, false, nullptr, st))) return rc;
+        {
+            LaunchScope sc(pl, st, KK_CONTROL, 0.0);
+            sweep_gate_kernel<<<(pl->P + 127) / 128, 128, 0, st>>>(pl->P, pl->d_rs, 0.0, 0, pl->d_gate,
+                                                                   pl->d_sweeps, pl->d_rn, pl->d_any);
+            CU(cudaGetLastError());
+        }
+        if (h_sweeps) CU(cudaMemcpyAsync(h_sweeps, pl->d_sweeps, pl->P * sizeof(int), cudaMemcpyDeviceToHost, st));
+        if (h_rn) CU(cudaMemcpyAsync(h_rn, pl->d_rn, pl->P * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        if (pl->profiling) prof_collect(pl);
+        return 0;
+    }
     int it = 0;
     for (;;) {
         const int chunk = 8;
@@ -2835,6 +2853,30 @@ int b200p_plan_solve_blocks(b200p_plan *pl, int level, const double *d_r, double
     LaunchScope sc(pl, st, KK_SWEEP, 0.0);
     oras_sweep_generic_kernel<false, 1><<<dim3(L.nblocks, pl->P), GEN_THREADS,
                                           smem_cg_bytes(L.info.block_w, L.info.block_h), st>>>(A);
+    CU(cudaGetLastError());
+    return 0;
+}
+
+int b200p_plan_scatter_weighted(b200p_plan *pl, int level, const double *d_v, double *d_field, void *stream) {
+    if (!pl || !d_v || !d_field) return fail_arg(B200P_ERR_ARG, "null argument");
+    if (level < 0 || level >= (int)pl->lev.size()) return fail_arg(B200P_ERR_ARG, "bad level %d", level);
+    LevelHost &L = pl->lev[level];
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t plane = (size_t)L.info.height * L.info.width;
+    const size_t n = (size_t)pl->P * L.nblocks * L.info.block_w * L.info.block_h;
+    // the plan's tile scratch receives (v * wy) * wx, then the combine pass of the sweeps (K2b) sums the
+    // covering tiles of every pixel in ascending block order onto a zero field (np.bincount order)
+    weight_tiles_kernel<<<(unsigned)((n + ST_THREADS_COMBINE - 1) / ST_THREADS_COMBINE), ST_THREADS_COMBINE, 0, st>>>(
+        L.dev, d_v, pl->d_scratch, n);
+    CU(cudaGetLastError());
+    fill_double_kernel<<<(pl->P + 127) / 128, 128, 0, st>>>(pl->d_rs, pl->P, 1.0);   // every problem is live
+    CU(cudaGetLastError());
+    CU(cudaMemsetAsync(d_field, 0, sizeof(double) * pl->P * plane, st));
+    dim3 g((L.info.width + ST_THREADS_COMBINE - 1) / ST_THREADS_COMBINE,
+           (L.info.height + COMBINE_ROWS - 1) / COMBINE_ROWS, pl->P);
+    LaunchScope sc(pl, st, KK_COMBINE, field_bytes(pl, L, 3.0, 0.0));
+    oras_combine_kernel<<<g, ST_THREADS_COMBINE, 0, st>>>(L.dev, pl->d_scratch, plane, nullptr, pl->d_rs, d_field,
+                                                          nullptr, 0, L.info.height, nullptr, pl->C);
     CU(cudaGetLastError());
     return 0;
 }

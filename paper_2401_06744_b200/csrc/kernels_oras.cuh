@@ -1443,6 +1443,24 @@ oras_sweep_generic_kernel(const SweepArgs A) {
 constexpr int COMBINE_ROWS = 32;
 constexpr int COMBINE_G = 8;
 
+// Stage helper: tiles[p][blk][j][i] *= wy[iy][j] * wx[ix][i] in the order of K2's epilogue, (v * wy) * wx
+// (solvers.py:309-310), so that an isolated combine pass can be fed UNWEIGHTED local corrections.
+__global__ void __launch_bounds__(ST_THREADS_COMBINE)
+weight_tiles_kernel(const LevelDev L, const double *__restrict__ v, double *__restrict__ tiles, size_t n) {
+    const size_t i = (size_t)blockIdx.x * ST_THREADS_COMBINE + threadIdx.x;
+    if (i >= n) return;
+    const size_t bsz = (size_t)L.bw * L.bh;
+    const int blk = (int)((i / bsz) % (size_t)L.nblocks);
+    const int r = (int)(i % bsz), jy = r / L.bw, jx = r - jy * L.bw;
+    const int iy = blk / L.nx, ix = blk - iy * L.nx;
+    tiles[i] = (v[i] * L.wy[iy * L.bh + jy]) * L.wx[ix * L.bw + jx];
+}
+
+__global__ void fill_double_kernel(double *p, int n, double v) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
 // `egress` (8-bit decode): the updated pixel is also written as clip(round(u)) into
 // the interleaved (F, h, w, C) image (image_from_fields, fileio.py:58-65) -- the last post-smoothing
 // combine of the finest level carries it, so an 8-bit decode needs no pass over the fp64 result.

@@ -55,8 +55,10 @@ class BlockSolver:
 
     The reference precomputes gather indices and per-block diagonals; the GPU
     kernels derive both analytically, so this object only validates and carries
-    the geometry.  ``solve_blocks`` / ``gather`` / ``scatter_weighted`` are
-    provided for A/B tests.
+    the geometry.  ``gather`` / ``solve_blocks`` / ``scatter_weighted`` are the
+    reference's stage calls for A/B tests: the block solve runs the generic
+    shared-memory kernel on its own, the scatter runs the sweeps' combine
+    kernel (K2b) on its own.
     """
 
     def __init__(self, mask, spacing: float, part: BlockPartition, weights: BlockWeights, alpha: float):
@@ -74,8 +76,46 @@ class BlockSolver:
         return _stage_plan(self.mask, self.spacing, self.part.block_size, self.part.overlap,
                            self.alpha, eta, local_max_iters)
 
-    def solve_blocks(self, rhs_field, target_sq: float, max_iters: int, workers: int = 1) -> np.ndarray:
-        """gather + solve_blocks on a global residual FIELD (solvers.py:303-305, :372-390)."""
+    def gather(self, r) -> np.ndarray:
+        """R_i r for every block: (h, w) -> (nblocks, bh, bw) (solvers.py:303-305).  Host-side indexing with
+        the library's block starts; inside the sweeps the gather is fused into the block-solve kernel."""
+        r = np.asarray(r, dtype=np.float64)
+        if r.shape != self.shape:
+            raise ValueError(f"field shape {r.shape} does not match the mask {self.shape}")
+        p = self.part
+        return np.stack([r[y:y + p.block_h, x:x + p.block_w] for y in p.ys for x in p.xs])
+
+    def _field_of(self, tiles) -> np.ndarray:
+        """The field whose gather is `tiles` (the device entry point takes a field)."""
+        p = self.part
+        if tiles.shape != (p.nblocks, p.block_h, p.block_w):
+            raise ValueError(f"expected gathered blocks {(p.nblocks, p.block_h, p.block_w)}, got {tiles.shape}")
+        f = np.zeros(self.shape)
+        for t, (y, x) in zip(tiles, ((y, x) for y in p.ys for x in p.xs)):
+            f[y:y + p.block_h, x:x + p.block_w] = t
+        if not np.array_equal(self.gather(f), tiles):
+            raise ValueError("blocks disagree on their overlaps: not the gather of a field")
+        return f
+
+    def scatter_weighted(self, v) -> np.ndarray:
+        """sum_i R_i^T (wy_i (x) wx_i * v_i) in block order (solvers.py:307-314): the combine kernel alone."""
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        p = self.part
+        if v.shape != (p.nblocks, p.block_h, p.block_w):
+            raise ValueError(f"expected local corrections {(p.nblocks, p.block_h, p.block_w)}, got {v.shape}")
+        plan = self._plan()
+        d_v = _dev.to_device_f64(v)
+        d_f = _dev.empty_f64(self.shape)
+        _dev.call("b200p_plan_scatter_weighted", plan.handle, 0, _dev.ptr(d_v), _dev.ptr(d_f), _dev.stream())
+        return _dev.to_host(d_f)
+
+    def solve_blocks(self, rhs, target_sq: float, max_iters: int, workers: int = 1) -> np.ndarray:
+        """Local Robin solves of all blocks (solvers.py:372-390) to `target_sq`.  `rhs` is the reference's
+        gathered residual (nblocks, bh, bw) -- `bs.solve_blocks(bs.gather(r), ...)` -- or the global residual
+        field itself (gather fused, as in the sweeps)."""
+        rhs_field = np.asarray(rhs, dtype=np.float64)
+        if rhs_field.ndim == 3:
+            rhs_field = self._field_of(rhs_field)
         plan = self._plan(local_max_iters=max_iters)
         r = _dev.to_device_f64(rhs_field)
         p = self.part

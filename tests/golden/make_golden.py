@@ -189,6 +189,50 @@ def images():
     print({k: v["iterations"] for k, v in meta.items()})
 
 
+def kats():
+    """Three known-answer tests of the reference's own suite, with the reference's outputs:
+    TestBlockSolver.test_matches_scalar_local_solve (tests/test_solvers.py:156-169),
+    TestVCycle.test_single_level_reduces_to_smoothing (tests/test_multigrid.py:218-233),
+    TestFmgSolve.test_fine_unit_accounting (tests/test_multigrid.py:298-302)."""
+    from diffpaint.partition import build_partition, build_weights
+    out = {}
+    # (a) batched block solve == scalar local solves, clamped blocks in both axes
+    prob = seeded(80, 56, 0.15, 8)
+    part = build_partition(80, 56, 32, 6)
+    bs = sv.BlockSolver(prob.mask, 1.0, part, build_weights(part), alpha=0.5)
+    r = np.random.default_rng(12345).normal(size=(56, 80))
+    r[prob.mask] = 0.0
+    target = 1e-5 * float(np.vdot(r, r))
+    batched = bs.solve_blocks(bs.gather(r), target, max_iters=4096)
+    for i, rect in enumerate(part.rects()):
+        local = sv.build_local_system(rect, prob.mask, 1.0, 0.5)
+        expected = sv.local_solve(local, r[rect.y0:rect.y0 + rect.h, rect.x0:rect.x0 + rect.w], target, 4096)
+        np.testing.assert_allclose(batched[i], expected, atol=1e-12)
+    out["kat_blocks_r"], out["kat_blocks_target"], out["kat_blocks_v"] = r, np.array(target), batched
+    out["kat_blocks_scatter"] = bs.scatter_weighted(batched)
+    # (b) a single-level V-cycle is nu_pre + nu_post Schwarz sweeps, bit for bit
+    prob = seeded(32, 32, 0.1, 4)
+    cfg = dp.MultigridConfig()
+    hier = dp.build_hierarchy(prob, cfg)
+    assert len(hier) == 1
+    lev = hier.levels[0]
+    u_cycle = prob.flat_init(0)
+    mg.v_cycle(hier, 0, u_cycle, lev.rhs[0], cfg)
+    u_manual = prob.flat_init(0)
+    sv.oras_sweeps(lev.op, lev.block_solver(cfg.solver.alpha), lev.rhs[0], u_manual,
+                   max_sweeps=cfg.nu_pre + cfg.nu_post, stop_norm=0.0, eta=cfg.solver.local_tol_fraction,
+                   local_max_iters=4096)
+    assert np.array_equal(u_cycle, u_manual)
+    out["kat_vcycle_u"] = u_cycle
+    # (c) fine-level work units = (nu_pre + nu_post) * cycles
+    prob = seeded(128, 128, 0.05, 1)
+    _, rep = dp.fmg_solve(dp.build_hierarchy(prob, cfg), cfg)
+    assert rep.fine_smoother_iterations == (cfg.nu_pre + cfg.nu_post) * rep.iterations
+    out["kat_units"] = np.array([rep.iterations, rep.fine_smoother_iterations])
+    np.savez_compressed(os.path.join(HERE, "golden_kats.npz"), **out)
+    print("kats:", out["kat_units"], batched.shape)
+
+
 def anchors():
     os.environ["INPAINT_THREADS"] = "0"
     res = {}
@@ -218,14 +262,18 @@ if __name__ == "__main__":
     ap.add_argument("--anchors", action="store_true")
     ap.add_argument("--pipelines", action="store_true", help="write only golden_pipelines.*")
     ap.add_argument("--images", action="store_true", help="write only golden_images.* (8-bit file path)")
+    ap.add_argument("--kats", action="store_true", help="write only golden_kats.npz (reference-suite known answers)")
     a = ap.parse_args()
     if a.pipelines:
         pipelines()
     elif a.images:
         images()
+    elif a.kats:
+        kats()
     else:
         small()
         pipelines()
         images()
+        kats()
         if a.anchors:
             anchors()
