@@ -114,6 +114,9 @@ enum { B200P_XCHG_SUM_RS = 1, B200P_XCHG_MAX_FLAGS = 2, B200P_XCHG_HALO_U = 3, B
 typedef int (*b200p_exchange_fn)(void *user, int kind, void *d_ptr, void *stream);
 
 const char *b200p_last_error(void);
+/* 1 when the library was built with -DB200P_EXPERIMENTS (block-solve variants that lost their A/B,
+ * selected by B200P_TILE32 / B200P_FUSED / B200P_ARRIVAL); the default build does not contain them. */
+int b200p_has_experiments(void);
 /* B200P_ABI_VERSION of the built library (bindings compare it with the header they were written for). */
 int b200p_abi_version(void);
 int b200p_device_count(void);

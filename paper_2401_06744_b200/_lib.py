@@ -147,6 +147,7 @@ SIGNATURES = {
     "b200p_memset": (_I, [_VP, _I, _I64]),
     "b200p_device_synchronize": (_I, []),
     "b200p_abi_version": (_I, []),
+    "b200p_has_experiments": (_I, []),
 }
 ABI_VERSION = 2  # B200P_ABI_VERSION these bindings (struct layouts above) were written for
 

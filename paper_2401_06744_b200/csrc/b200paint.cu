@@ -23,8 +23,16 @@
 #include "kernels_stencil.cuh"
 #include "kernels_rows.cuh"
 #include "kernels_oras.cuh"
-#include "kernels_oras_tma.cuh"
 #include "kernels_oras_warp.cuh"
+// Block-solve variants that lost their A/B are compiled only on request:
+//   make EXTRA=-DB200P_EXPERIMENTS
+#ifdef B200P_EXPERIMENTS
+#include "kernels_oras_lab.cuh"
+#include "kernels_oras_tma.cuh"
+#define B200P_LAB 1
+#else
+#define B200P_LAB 0
+#endif
 #include "kernels_cg.cuh"
 
 using namespace b200p;
@@ -595,6 +603,7 @@ enum { TILE_GENERIC = 0, TILE_32_A = 1, TILE_16 = 2, TILE_8 = 3, TILE_32_B = 4, 
 
 static int tile_for(int bw, int bh) {
     if (bw == 32 && bh == 32) {
+#if B200P_LAB
         const char *e = getenv("B200P_TILE32");
         if (e && *e == 'A') return TILE_32_A;
         if (e && *e == 'C') return TILE_32_C;
@@ -605,6 +614,7 @@ static int tile_for(int bw, int bh) {
         if (e && *e == 'B') return TILE_32_B;
         if (e && *e == 'L') return TILE_32_L;  // two-warp register tile with the lean prologue
         if (e && *e == 'Q') return TILE_32_WQ; // warp per block, v and q in tensor memory
+#endif
         return TILE_32_W;  // warp per block, v in tensor memory; falls back to B where not eligible
     }
     if (bw == 16 && bh == 16) return TILE_16;
@@ -618,6 +628,7 @@ static void launch_tile(const SweepArgs &A, bool rm, dim3 grid, cudaStream_t st)
     else oras_sweep_tile_kernel<TW, TH, NWARP, false, REGCAP><<<grid, NWARP * 32, 0, st>>>(A);
 }
 
+#if B200P_LAB
 template <int TW, int TH, int NWARP, bool SR>
 static void launch_tile_s(const SweepArgs &A, bool rm, dim3 grid, cudaStream_t st) {
     if (rm) oras_sweep_tile_s_kernel<TW, TH, NWARP, true, SR><<<grid, NWARP * 32, 0, st>>>(A);
@@ -640,6 +651,7 @@ static int fused_occupancy() {
         occ = 0;
     return occ;
 }
+#endif
 
 static void fill_sweep_args(b200p_plan *pl, const LevelHost &L, const double *u, const double *b,
                             const int *pred, SweepArgs &A) {
@@ -657,6 +669,13 @@ static void fill_sweep_args(b200p_plan *pl, const LevelHost &L, const double *u,
     A.scratch = pl->d_scratch;
 }
 
+#if !B200P_LAB
+static int launch_sweep_fused(b200p_plan *, const LevelHost &, UBuf &, const double *, bool, const int *, int *,
+                              cudaStream_t) {
+    return fail_arg(B200P_ERR_UNSUPPORTED, "the fused sweep is an experiment: build with -DB200P_EXPERIMENTS");
+}
+static bool arrival_fusion_enabled() { return false; }
+#else
 // K2F: fused solve + combine, u.cur -> u.alt, then swap.
 static int launch_sweep_fused(b200p_plan *pl, const LevelHost &L, UBuf &u, const double *b, bool rm,
                               const int *pred, int *unit_counter, cudaStream_t st) {
@@ -765,10 +784,6 @@ static void launch_tma_t(const SweepTmaArgs &A, const CUtensorMap &tu, const CUt
     oras_sweep_tma_kernel<RM, REGCAP><<<grid, KT_THREADS, 0, st>>>(A, tu, tb);
 }
 
-static bool tma_eligible(const LevelHost &L, const double *u, const double *b, bool rm) {
-    return L.d_mtab && L.info.width % 2 == 0 && ((uintptr_t)u % 16) == 0 && (rm || ((uintptr_t)b % 16) == 0);
-}
-
 static int launch_sweep_tma(b200p_plan *pl, const LevelHost &L, const SweepArgs &S, bool rm, cudaStream_t st) {
     SweepTmaArgs A;
     A.S = S;
@@ -792,16 +807,26 @@ static int launch_sweep_tma(b200p_plan *pl, const LevelHost &L, const SweepArgs 
 #undef KT_LAUNCH
     return 0;
 }
+#endif  // B200P_LAB
+
+// the 32x32 fast paths gather with 16-byte loads from a packed mask table: even width and starts, aligned fields
+static bool tma_eligible(const LevelHost &L, const double *u, const double *b, bool rm) {
+    return L.d_mtabw && L.info.width % 2 == 0 && ((uintptr_t)u % 16) == 0 && (rm || ((uintptr_t)b % 16) == 0);
+}
 
 static int launch_warp_sweep(const WarpSweepArgs &WA, bool rm, bool qt, int grid, cudaStream_t st) {
     const size_t smem = kw_table_bytes(WA.P, WA.S.L.nx, WA.S.L.ny);  // a few KB (P <= a few hundred problems)
-    if (rm) {
-        if (qt) oras_sweep_warp_kernel<true, true><<<grid, KW_THREADS, smem, st>>>(WA);
-        else oras_sweep_warp_kernel<true, false><<<grid, KW_THREADS, smem, st>>>(WA);
-    } else {
-        if (qt) oras_sweep_warp_kernel<false, true><<<grid, KW_THREADS, smem, st>>>(WA);
-        else oras_sweep_warp_kernel<false, false><<<grid, KW_THREADS, smem, st>>>(WA);
+#if B200P_LAB
+    if (qt) {   // q = A p parked in tensor memory as well (measured slower)
+        if (rm) oras_sweep_warp_kernel<true, true><<<grid, KW_THREADS, smem, st>>>(WA);
+        else oras_sweep_warp_kernel<false, true><<<grid, KW_THREADS, smem, st>>>(WA);
+        CU(cudaGetLastError());
+        return 0;
     }
+#endif
+    (void)qt;
+    if (rm) oras_sweep_warp_kernel<true, false><<<grid, KW_THREADS, smem, st>>>(WA);
+    else oras_sweep_warp_kernel<false, false><<<grid, KW_THREADS, smem, st>>>(WA);
     CU(cudaGetLastError());
     return 0;
 }
@@ -865,6 +890,7 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, UBuf &ub, cons
                 if (rc) return rc;
                 break;
             }
+#if B200P_LAB
             case TILE_32_L: {
                 static const int cap = getenv("B200P_REGCAP") ? atoi(getenv("B200P_REGCAP")) : 168;
                 dim3 g3(L.info.nx, L.iy_hi - L.iy_lo, pl->P);  // strip mode: only the block rows of this rank
@@ -904,19 +930,14 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, UBuf &ub, cons
                 break;
             }
             case TILE_32_A: launch_tile<4, 2, 4>(A, rm, grid, st); break;
-            case TILE_32_B: {
-                static const int cap = getenv("B200P_REGCAP") ? atoi(getenv("B200P_REGCAP")) : 168;
-                if (cap == 168) launch_tile<4, 4, 2, 168>(A, rm, grid, st);
-                else if (cap == 160) launch_tile<4, 4, 2, 160>(A, rm, grid, st);
-                else if (cap == 144) launch_tile<4, 4, 2, 144>(A, rm, grid, st);
-                else if (cap == 128) launch_tile<4, 4, 2, 128>(A, rm, grid, st);
-                else launch_tile<4, 4, 2>(A, rm, grid, st);
-                break;
-            }
             case TILE_32_C: launch_tile<4, 1, 8>(A, rm, grid, st); break;
             case TILE_32_S: launch_tile_s<4, 4, 2, false>(A, rm, grid, st); break;
             case TILE_32_T: launch_tile_s<4, 4, 2, true>(A, rm, grid, st); break;
             case TILE_32_U: launch_tile_s<4, 2, 4, false>(A, rm, grid, st); break;
+#endif
+            // two warps per 32x32 block, 4x4 pixels per thread: levels the warp-per-block kernel cannot take
+            // (odd width, unaligned fields)
+            case TILE_32_B: launch_tile<4, 4, 2, 168>(A, rm, grid, st); break;
             case TILE_16: launch_tile<2, 4, 1>(A, rm, grid, st); break;
             case TILE_8: launch_tile<1, 2, 1>(A, rm, grid, st); break;
             default: {
@@ -1024,11 +1045,13 @@ static int launch_set_int(b200p_plan *pl, int *p, int n, int v, cudaStream_t st)
 
 // build_hierarchy's data half (multigrid.py:249-260).
 static int pack_masks(b200p_plan *pl, const LevelHost &L, cudaStream_t st) {
-    if (!L.d_mtab) return 0;
-    LaunchScope sc(pl, st, KK_DOWN_MASK, (double)pl->F * L.nblocks * (32.0 * 32.0 + 4.0 * KT_THREADS));
+    if (!L.d_mtabw) return 0;
+    LaunchScope sc(pl, st, KK_DOWN_MASK, (double)pl->F * L.nblocks * (32.0 * 32.0 + 4.0 * 32));
+#if B200P_LAB
     pack_block_masks_kernel<<<dim3(L.nblocks, pl->F), KT_THREADS, 0, st>>>(
         L.dev, L.d_mask, (size_t)L.info.height * L.info.width, L.d_mtab, 0);
     CU(cudaGetLastError());
+#endif
     pack_block_masks_warp_kernel<<<dim3((L.nblocks + KW_WARPS - 1) / KW_WARPS, pl->F), KW_THREADS, 0, st>>>(
         L.dev, L.d_mask, (size_t)L.info.height * L.info.width, L.d_mtabw);
     CU(cudaGetLastError());
@@ -1659,6 +1682,7 @@ static int set_smem_attrs() {
                             cudaFuncAttributeMaxDynamicSharedMemorySize, big));
     CU(cudaFuncSetAttribute(oras_sweep_generic_kernel<false, 1>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+#if B200P_LAB
     // K2S keeps CG state in static shared memory: ask for the large carve-out so that
     // 8 blocks per SM are resident
     const int carve = cudaSharedmemCarveoutMaxShared;
@@ -1668,6 +1692,7 @@ static int set_smem_attrs() {
     CU(cudaFuncSetAttribute(oras_sweep_tile_s_kernel<4, 4, 2, false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     CU(cudaFuncSetAttribute(oras_sweep_tile_s_kernel<4, 2, 4, true, false>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     CU(cudaFuncSetAttribute(oras_sweep_tile_s_kernel<4, 2, 4, false, false>, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+#endif
     done = true;
     return 0;
 }
@@ -1678,6 +1703,8 @@ extern "C" {
 const char *b200p_last_error(void) { return g_err.c_str(); }
 
 int b200p_abi_version(void) { return B200P_ABI_VERSION; }
+
+int b200p_has_experiments(void) { return B200P_LAB; }
 
 int b200p_device_count(void) {
     int n = 0;
@@ -1876,6 +1903,7 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
         L.iy_lo = 0;
         L.iy_hi = L.info.ny;
         const size_t plane = (size_t)h * w;
+#if B200P_LAB
         {
             const char *e = getenv("B200P_FUSED");
             const bool want = e && *e == '1';  // experimental; the split sweep (K2 + K2b) is faster
@@ -1912,16 +1940,20 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
                 L.fused_grid = sms * occ;
             }
         }
-        // K2T: the TMA box starts at x0 - 2 and needs a 16-byte aligned start: even block starts
+#endif
+        // the 32x32 fast path loads pixel pairs (16 bytes): even width and even block starts
         bool xs_even = true;
         for (int x : xs) xs_even = xs_even && (x % 2 == 0);
         if (D.bw == 32 && D.bh == 32 && w % 2 == 0 && xs_even)
         {
+#if B200P_LAB
             PTRY(dev_alloc(pl, &L.d_mtab, (size_t)pl->F * L.nblocks * KT_THREADS));
+#endif
             PTRY(dev_alloc(pl, &L.d_mtabw, (size_t)pl->F * L.nblocks * 32));
             PTRY(dev_alloc(pl, &L.d_claim, 4));
             CU(cudaMemset(L.d_claim, 0, 4 * sizeof(unsigned)));
         }
+#if B200P_LAB
         if (L.d_mtab && L.nblocks > 1 && arrival_fusion_enabled()) {
             // cells = rectangles between consecutive block starts; a block overlaps the cells from its own
             // index to the last one starting inside its extent
@@ -1951,6 +1983,7 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
             PTRY(dev_alloc(pl, &L.d_cell_cnt, (size_t)pl->P * L.nblocks));
             if (!L.d_u_alt) PTRY(dev_alloc(pl, &L.d_u_alt, (size_t)pl->P * h * w));
         }
+#endif
         if (l > 0) {
             PTRY(dev_alloc(pl, &L.d_mask, pl->F * plane));
             PTRY(dev_alloc(pl, &L.d_rhs, pl->P * plane));
@@ -2103,7 +2136,7 @@ int b200p_plan_set_strip(b200p_plan *pl, int levels, const int *r, b200p_exchang
         const LevelHost &L = pl->lev[l];
         const int H = L.info.height;
         const int *q = r + 6 * l;
-        if (!L.d_mtab || L.info.width % 4 != 0 || L.nblocks < 2)
+        if (!L.d_mtabw || L.info.width % 4 != 0 || L.nblocks < 2)
             return fail_arg(B200P_ERR_UNSUPPORTED,
                             "strip mode needs 32x32 blocks with even starts and width %% 4 == 0 (level %d)", l);
         if (!(0 <= q[2] && q[2] <= q[0] && q[0] < q[1] && q[1] <= q[3] && q[3] <= H && 0 <= q[4] && q[4] < q[5] &&
@@ -2770,10 +2803,12 @@ int b200p_plan_oras_sweeps(b200p_plan *pl, int level, const double *d_b, double 
         force = -2;
     } else if (path >= 10) {
         const int t = path - 10;
-        const bool ok = (is32 && (t == TILE_32_A || t == TILE_32_B || t == TILE_32_C || t == TILE_32_S ||
-                                 t == TILE_32_T || t == TILE_32_U || t == TILE_32_TMA || t == TILE_32_L ||
-                                 t == TILE_32_W || t == TILE_32_WQ)) ||
-                        (is16 && t == TILE_16) || (is8 && t == TILE_8);
+        const bool lab32 = t == TILE_32_A || t == TILE_32_C || t == TILE_32_S || t == TILE_32_T || t == TILE_32_U ||
+                           t == TILE_32_TMA || t == TILE_32_L || t == TILE_32_WQ;
+        if (is32 && lab32 && !B200P_LAB)
+            return fail_arg(B200P_ERR_UNSUPPORTED, "tile variant %d is an experiment: build with -DB200P_EXPERIMENTS", t);
+        const bool ok = (is32 && (lab32 || t == TILE_32_B || t == TILE_32_W)) || (is16 && t == TILE_16) ||
+                        (is8 && t == TILE_8);
         if (!ok) return fail_arg(B200P_ERR_UNSUPPORTED, "level %d is not eligible for tile variant %d", level, t);
         force = t;
     } else if (path != 0) {

@@ -196,8 +196,20 @@ def test_oras_sweeps_general_start_and_stop_norm(rng):
 
 @pytest.mark.parametrize("variant", [1, 4, 5, 6, 7, 8, 9, 10, 11, 12])
 def test_tile32_variants_match_oracle(variant, rng):
-    """Every 32x32 register/shared-memory tile variant of K2 (path 10 + id), regular start and
-    the general start (u violating the interpolation condition)."""
+    """Every 32x32 block-solve variant of K2 (path 10 + id), regular start and the general start (u violating
+    the interpolation condition).  The default build ships 11 (warp per block, the fast path) and 4 (two warps
+    per block, the fallback for odd widths); the others are experiments (-DB200P_EXPERIMENTS)."""
+    from paper_2401_06744_b200 import _lib
+    if variant not in (4, 11) and not _lib.lib().b200p_has_experiments():
+        w, h = 150, 100
+        m, k = oracle.seeded_problem(w, h, 0.05, 21)
+        part = bp.build_partition(w, h, 32, 6)
+        blocks = bp.BlockSolver(m, 1.0, part, bp.build_weights(part), 0.5)
+        b = np.where(m, k[0], 0.0)
+        with pytest.raises(NotImplementedError, match="experiment"):     # refused loudly, not silently replaced
+            bp.oras_sweeps(bp.StencilOperator(m), blocks, b, b.copy(), max_sweeps=1, stop_norm=0.0, eta=1e-5,
+                           local_max_iters=None, path=10 + variant)
+        pytest.skip("experiment variant: not in the default build")
     w, h, bs, ov = 150, 100, 32, 6
     m, k = oracle.seeded_problem(w, h, 0.05, 21)
     part = bp.build_partition(w, h, bs, ov)
