@@ -9,6 +9,7 @@
 // There is no CPU fallback anywhere in this file: every compute entry point
 // launches CUDA kernels and returns the CUDA error if no device is present.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -175,6 +176,12 @@ struct LevelHost {
     unsigned *d_mtab = nullptr; // K2T: packed block-local masks (F, nblocks, 64); null = level not eligible
     unsigned *d_mtabw = nullptr; // K2W: the same for the warp-per-block layout (F, nblocks, 32)
     unsigned *d_claim = nullptr; // K2W: {next unclaimed item, finished CTAs}, zero between launches
+    // band combine (K2W DIRECT + oras_combine_band_kernel): per-axis writer tables, row / column lists
+    bool band = false;
+    const uint8_t *d_xflag = nullptr, *d_yflag = nullptr;
+    const int *d_nzxf = nullptr, *d_nzxn = nullptr, *d_nzyf = nullptr, *d_nzyn = nullptr;
+    const int *d_band_rows = nullptr, *d_core_rows = nullptr, *d_band_cols = nullptr;
+    int n_band_rows = 0, n_core_rows = 0, n_band_cols = 0;
     // combine on arrival (FUSE variant of the lean kernel): cell tables and arrival counters
     const int *d_cell_need = nullptr, *d_lastx = nullptr, *d_lasty = nullptr;
     unsigned *d_cell_cnt = nullptr;
@@ -188,6 +195,17 @@ struct LevelHost {
     double *d_ring = nullptr;   // (R, nx, bh*bw)
     int R = 0, lag = 0, nsx = 0, nc = 0, cw = 0, fused_grid = 0;
     const int *d_band_first_row = nullptr, *d_row_last_band = nullptr;
+};
+
+// NVTX range around the launches of one stage of one level ("cascade L3", "vcycle L0 pre", ...): shows up in
+// nsys / ncu timelines of eager runs and of graph capture; a no-op without a profiler attached.
+struct NvtxScope {
+    NvtxScope(const char *what, int level) {
+        char buf[48];
+        snprintf(buf, sizeof buf, "%s L%d", what, level);
+        nvtxRangePushA(buf);
+    }
+    ~NvtxScope() { nvtxRangePop(); }
 };
 
 // current iterate of a level + its ping-pong partner (fused sweeps swap them)
@@ -596,6 +614,51 @@ static int local_cap(const b200p_plan *pl, const LevelHost &L) {
                                        : 4 * L.info.block_h * L.info.block_w;
 }
 
+// Who writes a pixel?  Per axis: the block slots that cover it with a NON-ZERO weight (the ramp of
+// partition.py:137-154 starts at 0, so the outermost pixel of every cut side drops out).  Returns false when
+// those slots are not consecutive (never the case for the reference's ramps; the caller then keeps the
+// full combine).  flag[slot * extent + i]: bit 0 = non-zero weight, bit 1 = "direct": the pixel has a
+// single writer and (align > 1) so has every pixel of its aligned group of `align` pixels.
+static bool axis_writers(const std::vector<int> &starts, const std::vector<double> &wts, int extent, int dim, int align,
+                         std::vector<int> &first, std::vector<int> &count, std::vector<uint8_t> &flag,
+                         std::vector<int> &direct_px) {
+    first.assign(dim, -1);
+    count.assign(dim, 0);
+    flag.assign(starts.size() * (size_t)extent, 0);
+    for (size_t s = 0; s < starts.size(); ++s)
+        for (int i = 0; i < extent; ++i) {
+            if (wts[s * extent + i] == 0.0) continue;
+            const int x = starts[s] + i;
+            flag[s * extent + i] |= 1;
+            if (count[x] == 0) first[x] = (int)s;
+            else if (first[x] + count[x] != (int)s) return false;
+            count[x] += 1;
+        }
+    direct_px.assign(dim, 0);
+    for (int g0 = 0; g0 < dim; g0 += align) {
+        bool single = true;
+        for (int x = g0; x < std::min(dim, g0 + align); ++x) single = single && count[x] == 1;
+        for (int x = g0; x < std::min(dim, g0 + align); ++x) direct_px[x] = single ? 1 : 0;
+    }
+    for (int x = 0; x < dim; ++x) {
+        if (count[x] < 1) return false;   // partition of unity: somebody must write every pixel
+        if (direct_px[x] && wts[(size_t)first[x] * extent + (x - starts[first[x]])] != 1.0) return false;
+    }
+    for (size_t s = 0; s < starts.size(); ++s)
+        for (int i = 0; i < extent; ++i)
+            if (direct_px[starts[s] + i]) flag[s * extent + i] |= 2;
+    // the block solve decides per PAIR of pixels (even start) from the first pixel's flags
+    if (align > 1)
+        for (size_t s = 0; s < starts.size(); ++s) {
+            if (starts[s] & 1) return false;
+            for (int i = 0; i + 1 < extent; i += 2) {
+                const uint8_t a = flag[s * extent + i], b = flag[s * extent + i + 1];
+                if ((a & 2) != (b & 2) || ((a & 2) && (a & 1) != (b & 1))) return false;
+            }
+        }
+    return true;
+}
+
 // Tile variants of K2 (block extent -> <TW,TH,NWARP>).
 enum { TILE_GENERIC = 0, TILE_32_A = 1, TILE_16 = 2, TILE_8 = 3, TILE_32_B = 4, TILE_32_C = 5,
        TILE_32_S = 6, TILE_32_T = 7, TILE_32_U = 8, TILE_32_TMA = 9, TILE_32_L = 10, TILE_32_W = 11,
@@ -817,6 +880,14 @@ static bool tma_eligible(const LevelHost &L, const double *u, const double *b, b
 static int launch_warp_sweep(const WarpSweepArgs &WA, bool rm, bool qt, int grid, cudaStream_t st) {
     const size_t smem = kw_table_bytes(WA.P, WA.S.L.nx, WA.S.L.ny);  // a few KB (P <= a few hundred problems)
 #if B200P_LAB
+    if (WA.u_out) {   // band combine: single-writer pixels go straight to the partner iterate
+        if (rm) oras_sweep_warp_kernel<true, false, true><<<grid, KW_THREADS, smem, st>>>(WA);
+        else oras_sweep_warp_kernel<false, false, true><<<grid, KW_THREADS, smem, st>>>(WA);
+        CU(cudaGetLastError());
+        return 0;
+    }
+#endif
+#if B200P_LAB
     if (qt) {   // q = A p parked in tensor memory as well (measured slower)
         if (rm) oras_sweep_warp_kernel<true, true><<<grid, KW_THREADS, smem, st>>>(WA);
         else oras_sweep_warp_kernel<false, true><<<grid, KW_THREADS, smem, st>>>(WA);
@@ -856,6 +927,11 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, UBuf &ub, cons
     fill_sweep_args(pl, L, u, b, pred, A);
     A.iy0 = L.iy_lo;
     dim3 grid(L.nblocks, pl->P);
+    // band combine (experiment, B200P_BAND=1 in a -DB200P_EXPERIMENTS build): K2W updates the single-writer
+    // pixels itself, the combine pass visits the overlap bands only, u.cur -> u.alt.  Not in strip mode, and
+    // not for the sweep that carries the 8-bit egress (its full combine pass writes every pixel of the image).
+    const bool band = L.band && tile == TILE_32_W && tma_eligible(L, u, b, rm) && !striped(pl, L) && !pl->egress_now &&
+                      ub.alt && ub.alt != ub.cur && ((uintptr_t)ub.alt % 16) == 0;
     if (striped(pl, L) && !((tile == TILE_32_L || tile == TILE_32_W || tile == TILE_32_WQ) && tma_eligible(L, u, b, rm)))
         return fail_arg(B200P_ERR_UNSUPPORTED, "strip mode needs the 32x32 lean block-solve kernel");
     {
@@ -880,6 +956,9 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, UBuf &ub, cons
                 const int g = std::min((WA.total + per_cta - 1) / per_cta, warp_sweep_grid());
                 WA.P = pl->P;
                 WA.claim = L.d_claim;
+                WA.u_out = band ? ub.alt : nullptr;
+                WA.xflag = L.d_xflag;
+                WA.yflag = L.d_yflag;
                 kw_magic((unsigned)WA.items_per_problem, WA.m_ipp, WA.k_ipp);
                 kw_magic((unsigned)L.info.nx, WA.m_nx, WA.k_nx);
                 if ((unsigned)WA.total >= (1u << 30))
@@ -948,6 +1027,42 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, UBuf &ub, cons
         }
         CU(cudaGetLastError());
     }
+#if B200P_LAB
+    if (band) {
+        BandTables T;
+        T.nzxf = L.d_nzxf; T.nzxn = L.d_nzxn; T.nzyf = L.d_nzyf; T.nzyn = L.d_nzyn;
+        T.tp = KW_TP; T.tsz = KW_TSZ;
+        if (L.n_band_rows > 0) {
+            // band rows, every column: up to 2 x 2 tiles per pixel
+            T.rows = L.d_band_rows; T.nrows = L.n_band_rows; T.cols = nullptr; T.ncols = L.info.width;
+            dim3 g((T.ncols + ST_THREADS_COMBINE - 1) / ST_THREADS_COMBINE, (T.nrows + COMBINE_ROWS - 1) / COMBINE_ROWS, pl->P);
+            LaunchScope sc(pl, st, KK_COMBINE, field_bytes(pl, L, 3.0, 0.0));
+            oras_combine_band_kernel<2><<<g, ST_THREADS_COMBINE, 0, st>>>(L.dev, T, pl->d_scratch, A.plane, pred, pl->d_rs,
+                                                                         u, ub.alt, unit_counter);
+            CU(cudaGetLastError());
+        }
+        if (L.n_core_rows > 0 && L.n_band_cols > 0) {
+            // the other rows, band columns only: one row slot, up to 2 tiles per pixel
+            T.rows = L.d_core_rows; T.nrows = L.n_core_rows; T.cols = L.d_band_cols; T.ncols = L.n_band_cols;
+            dim3 g((T.ncols + ST_THREADS_COMBINE - 1) / ST_THREADS_COMBINE, (T.nrows + COMBINE_ROWS - 1) / COMBINE_ROWS, pl->P);
+            LaunchScope sc(pl, st, KK_COMBINE, 0.0);
+            oras_combine_band_kernel<1><<<g, ST_THREADS_COMBINE, 0, st>>>(L.dev, T, pl->d_scratch, A.plane, pred, pl->d_rs,
+                                                                         u, ub.alt, L.n_band_rows > 0 ? nullptr : unit_counter);
+            CU(cudaGetLastError());
+        }
+        {
+            // problems the sweep skipped keep their iterate across the buffer swap
+            const size_t plane2 = A.plane / 2;
+            dim3 g((unsigned)std::min<size_t>((plane2 + ST_THREADS_COMBINE - 1) / ST_THREADS_COMBINE, 148), pl->P);
+            LaunchScope sc(pl, st, KK_COMBINE, 0.0);
+            copy_skipped_problems_kernel<<<g, ST_THREADS_COMBINE, 0, st>>>(
+                plane2, pred, pl->d_rs, reinterpret_cast<const double2 *>(u), reinterpret_cast<double2 *>(ub.alt));
+            CU(cudaGetLastError());
+        }
+        std::swap(ub.cur, ub.alt);
+        return 0;
+    }
+#endif
     {
         dim3 g((L.info.width + ST_THREADS_COMBINE - 1) / ST_THREADS_COMBINE,
                (L.own_hi - L.own_lo + COMBINE_ROWS - 1) / COMBINE_ROWS, pl->P);
@@ -1120,6 +1235,7 @@ static int enqueue_cascade(b200p_plan *pl, double *d_u0, cudaStream_t st) {
     if (rc) return rc;
     const double *coarse_u = co.d_u;
     for (int l = nl - 2; l >= 0; --l) {
+        NvtxScope nv("cascade", l);
         LevelHost &f = pl->lev[l];
         const LevelHost &c = pl->lev[l + 1];
         UBuf uf = level_ubuf(pl, l, d_u0);
@@ -1156,7 +1272,11 @@ static int enqueue_vcycle(b200p_plan *pl, int level, UBuf &u, const double *b, b
         // single-level cycle: nu_pre + nu_post sweeps (always a single block here)
         return launch_coarse(pl, L, u.cur, b, rm, 2, 0.0, cfg.nu_pre + cfg.nu_post, pred, uc, 1, st);
     }
-    int rc = enqueue_smooth(pl, L, u, b, rm, cfg.nu_pre, pred, uc, have_norm, st);
+    int rc;
+    {
+        NvtxScope nv("vcycle pre-smooth", level);
+        rc = enqueue_smooth(pl, L, u, b, rm, cfg.nu_pre, pred, uc, have_norm, st);
+    }
     if (rc) return rc;
     LevelHost &Cc = pl->lev[level + 1];
     UBuf e = level_ubuf(pl, level + 1, nullptr);
@@ -1217,8 +1337,11 @@ static int enqueue_vcycle(b200p_plan *pl, int level, UBuf &u, const double *b, b
             e.cur, L.d_mask, nullptr, L.info.height, L.info.width, pl->C, pred, u.cur, Ylo, Yhi);
         CU(cudaGetLastError());
     }
-    if ((rc = enqueue_smooth(pl, L, u, b, rm, cfg.nu_post, pred, uc, false, st, level == 0 && settle_home)))
-        return rc;
+    {
+        NvtxScope nv("vcycle post-smooth", level);
+        if ((rc = enqueue_smooth(pl, L, u, b, rm, cfg.nu_post, pred, uc, false, st, level == 0 && settle_home)))
+            return rc;
+    }
     // inner levels may end in the partner buffer (the caller prolongates from e.cur); the level
     // handed in from outside must end where it started
     return settle_home ? settle(pl, L, u, home, st) : 0;
@@ -1952,6 +2075,32 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
             PTRY(dev_alloc(pl, &L.d_mtabw, (size_t)pl->F * L.nblocks * 32));
             PTRY(dev_alloc(pl, &L.d_claim, 4));
             CU(cudaMemset(L.d_claim, 0, 4 * sizeof(unsigned)));
+            // band combine (experiment): single-writer pixels are updated by the block solve itself
+            static const bool want_band = B200P_LAB && getenv("B200P_BAND") && atoi(getenv("B200P_BAND")) == 1;
+            std::vector<int> nzxf, nzxn, nzyf, nzyn, dpx, dpy;
+            std::vector<uint8_t> xflag, yflag;
+            if (want_band && L.nblocks > 1 && (size_t)h * w >= 400000 &&   // small levels: one combine launch is cheaper
+                axis_writers(xs, wx, D.bw, w, KW_ALIGN, nzxf, nzxn, xflag, dpx) &&
+                axis_writers(ys, wy, D.bh, h, 1, nzyf, nzyn, yflag, dpy)) {
+                std::vector<int> brows, crows, bcols;
+                for (int y = 0; y < h; ++y) (dpy[y] ? crows : brows).push_back(y);
+                for (int x = 0; x < w; ++x)
+                    if (!dpx[x]) bcols.push_back(x);
+                L.band = true;
+                L.n_band_rows = (int)brows.size();
+                L.n_core_rows = (int)crows.size();
+                L.n_band_cols = (int)bcols.size();
+                PTRY(dev_upload(pl, xflag, &L.d_xflag));
+                PTRY(dev_upload(pl, yflag, &L.d_yflag));
+                PTRY(dev_upload(pl, nzxf, &L.d_nzxf));
+                PTRY(dev_upload(pl, nzxn, &L.d_nzxn));
+                PTRY(dev_upload(pl, nzyf, &L.d_nzyf));
+                PTRY(dev_upload(pl, nzyn, &L.d_nzyn));
+                PTRY(dev_upload(pl, brows, &L.d_band_rows));
+                PTRY(dev_upload(pl, crows, &L.d_core_rows));
+                PTRY(dev_upload(pl, bcols, &L.d_band_cols));
+                if (!L.d_u_alt) PTRY(dev_alloc(pl, &L.d_u_alt, (size_t)pl->P * h * w));
+            }
         }
 #if B200P_LAB
         if (L.d_mtab && L.nblocks > 1 && arrival_fusion_enabled()) {
@@ -1991,7 +2140,7 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
             PTRY(dev_alloc(pl, &L.d_rc, pl->P * plane));
         }
         if (L.nblocks > 1 || shapes.size() == 1)
-            scratch = std::max(scratch, (size_t)pl->P * L.nblocks * D.bw * D.bh);
+            scratch = std::max(scratch, (size_t)pl->P * L.nblocks * (L.band ? (size_t)KW_TSZ : (size_t)D.bw * D.bh));
     }
     PTRY(dev_alloc(pl, &pl->d_scratch, scratch));
     PTRY(dev_alloc(pl, &pl->d_sched, std::max<size_t>(pl->sched_words, 4)));

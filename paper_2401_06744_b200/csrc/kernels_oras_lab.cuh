@@ -5,6 +5,7 @@
 //   K2L  oras_sweep_lean_kernel       two warps per 32x32 block, lean prologue (+ combine on arrival)
 //   K2S  oras_sweep_tile_s_kernel     CG state partly in shared memory
 //   K2F  oras_fused_sweep_kernel      solve + combine in one persistent kernel through an L2-resident ring
+//   K2b'  oras_combine_band_kernel    combine over the overlap bands only (with the DIRECT variant of K2W)
 #pragma once
 #include "kernels_oras.cuh"
 
@@ -880,5 +881,117 @@ oras_fused_sweep_kernel(const FusedArgs A) {
         __syncthreads();  // s_item[(it+1)&1] visible; shared staging free for the next item
     }
 }
+
+// ------------------------------------------------------------------ K2b' --
+// Band combine.  The partition-of-unity ramp starts at 0 on every cut side (partition.py:137-154), so the
+// outermost pixel ring of a block has weight 0 and most pixels of a level have exactly ONE writer with
+// weight exactly 1.  The warp-per-block solve (K2W, DIRECT) writes those straight into the partner
+// iterate u_out = u + v; only pixels of the overlap bands travel through tiles.  This kernel visits the
+// band pixels only -- launch 1: the band rows (every column), launch 2: the remaining rows x the band
+// columns -- and forms u_out = u + sum of the covering tiles with a non-zero weight, in ascending block
+// order (the zero-weight tiles the full combine adds are exact zeros, so the result is the same).
+// Tiles use the KW layout (rows of TP doubles, column = x - (x0 & ~7)).
+struct BandTables {
+    const int *nzxf, *nzxn;   // per pixel column: first block column with a non-zero weight, how many
+    const int *nzyf, *nzyn;   // per pixel row
+    const int *rows;          // the rows of this launch
+    const int *cols;          // the columns of this launch, or null = all columns
+    int nrows, ncols;
+    int tp, tsz;              // tile row pitch and tile size in doubles
+};
+
+template <int NY>   // rows of the launch have at most NY non-zero row slots (more: the generic loop)
+__global__ void __launch_bounds__(ST_THREADS_COMBINE)
+oras_combine_band_kernel(const LevelDev L, const BandTables T, const double *__restrict__ scratch, size_t plane,
+                         const int *__restrict__ pred, const double *__restrict__ rs,
+                         const double *__restrict__ u_in, double *__restrict__ u_out,
+                         int *__restrict__ unit_counter) {
+    __shared__ int s_y[COMBINE_ROWS], s_rn[COMBINE_ROWS], s_rf[COMBINE_ROWS];
+    __shared__ size_t s_roff[COMBINE_ROWS][2];
+    const int p = blockIdx.z;
+    if (pred && !pred[p]) return;
+    if (rs[p] == 0.0) return;
+    const int tid = threadIdx.x;
+    const int ci = blockIdx.x * ST_THREADS_COMBINE + tid;
+    const int k_lo = blockIdx.y * COMBINE_ROWS;
+    const int rows = min(COMBINE_ROWS, T.nrows - k_lo);
+    if (unit_counter && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) unit_counter[p] += 1;
+    if (tid < rows) {
+        const int y = T.rows[k_lo + tid];
+        const int iyf = T.nzyf[y], iyn = T.nzyn[y];
+        s_y[tid] = y;
+        s_rn[tid] = iyn;
+        s_rf[tid] = iyf;
+        for (int a = 0; a < 2; ++a) {
+            const int iy = iyf + (a < iyn ? a : 0);
+            s_roff[tid][a] = (size_t)iy * L.nx * T.tsz + (size_t)(y - L.ys[iy]) * T.tp;
+        }
+    }
+    __syncthreads();
+    if (ci >= T.ncols) return;
+    const int x = T.cols ? T.cols[ci] : ci;
+    const int ixf = T.nzxf[x], ixn = T.nzxn[x];
+    const size_t xo0 = (size_t)ixf * T.tsz + (x - (L.xs[ixf] & ~7));
+    const bool two_x = ixn > 1;
+    const size_t xo1 = two_x ? (size_t)(ixf + 1) * T.tsz + (x - (L.xs[ixf + 1] & ~7)) : xo0;
+    const bool wide = ixn > 2;
+    const double *sp = scratch + (size_t)p * L.nblocks * T.tsz;
+    const double *ui = u_in + (size_t)p * plane;
+    double *uo = u_out + (size_t)p * plane;
+    constexpr int G = COMBINE_G;
+    for (int k0 = 0; k0 < rows; k0 += G) {
+        double uu[G], v00[G], v01[G], v10[NY > 1 ? G : 1], v11[NY > 1 ? G : 1];
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+            const int k = k0 + j < rows ? k0 + j : rows - 1;
+            const size_t o0 = s_roff[k][0];
+            uu[j] = ui[(size_t)s_y[k] * L.w + x];
+            v00[j] = __ldcs(sp + o0 + xo0);
+            v01[j] = __ldcs(sp + o0 + xo1);
+            if (NY > 1) {
+                const size_t o1 = s_roff[k][1];
+                v10[j] = __ldcs(sp + o1 + xo0);
+                v11[j] = __ldcs(sp + o1 + xo1);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+            const int k = k0 + j;
+            if (k >= rows) break;
+            const int n = s_rn[k], y = s_y[k];
+            // ascending block order: (iy0,ix0), (iy0,ix1), (iy1,ix0), (iy1,ix1)
+            double acc = v00[j];
+            acc += two_x ? v01[j] : 0.0;
+            if (wide || n > NY) {
+                acc = 0.0;
+                for (int a = 0; a < n; ++a) {
+                    const int iy = s_rf[k] + a;
+                    const size_t oa = (size_t)iy * L.nx * T.tsz + (size_t)(y - L.ys[iy]) * T.tp;
+                    for (int c = 0; c < ixn; ++c)
+                        acc += sp[oa + (size_t)(ixf + c) * T.tsz + (x - (L.xs[ixf + c] & ~7))];
+                }
+            } else if (NY > 1) {
+                acc += n > 1 ? v10[NY > 1 ? j : 0] : 0.0;
+                acc += (n > 1 && two_x) ? v11[NY > 1 ? j : 0] : 0.0;
+            }
+            uo[(size_t)y * L.w + x] = uu[j] + acc;
+        }
+    }
+}
+
+// Problems the sweep skips (frozen, or zero residual) keep their iterate: copied to the partner buffer so that
+// the ping-pong swap after a band-combine sweep is valid for every problem of the plan.
+__global__ void __launch_bounds__(ST_THREADS_COMBINE)
+copy_skipped_problems_kernel(size_t plane2, const int *__restrict__ pred, const double *__restrict__ rs,
+                             const double2 *__restrict__ u_in, double2 *__restrict__ u_out) {
+    const int p = blockIdx.y;
+    if ((!pred || pred[p]) && rs[p] != 0.0) return;   // live: the sweep wrote it
+    const double2 *a = u_in + (size_t)p * plane2;
+    double2 *b = u_out + (size_t)p * plane2;
+    for (size_t i = (size_t)blockIdx.x * ST_THREADS_COMBINE + threadIdx.x; i < plane2;
+         i += (size_t)gridDim.x * ST_THREADS_COMBINE)
+        b[i] = a[i];
+}
+
 
 }  // namespace b200p

@@ -51,7 +51,19 @@ struct WarpSweepArgs {
     unsigned m_ipp, k_ipp; // n / items_per_problem == (n * m) >> k for n < 2^30 (kw_magic)
     unsigned m_nx, k_nx;   // the same for n / nx
     unsigned chunk;        // consecutive items per claim (1 on small launches, KW_CHUNK_MAX on large ones)
+    // DIRECT (band combine, see oras_combine_band_kernel): pixels that exactly one block updates are written
+    // to the partner iterate u_out = u + v by this kernel; only the overlap bands go through tiles
+    double *u_out;         // (P, h, w) partner buffer of S.u
+    const uint8_t *xflag;  // (nx, 32) per block column: bit 0 = non-zero weight, bit 1 = column of a single-writer 4-group
+    const uint8_t *yflag;  // (ny, 32) per block row:    bit 0 = non-zero weight, bit 1 = single-writer row
 };
+
+// Band-combine tile layout: rows of KW_TP doubles, pixel x of a block starting at x0 sits in column
+// x - (x0 & ~7), so that the 64-byte pixel groups of the level (the DRAM access granularity) stay aligned
+// 64-byte pieces inside the tile.
+constexpr int KW_TP = 40;
+constexpr int KW_ALIGN = 8;   // pixels per aligned group (64 bytes)
+constexpr int KW_TSZ = 32 * KW_TP;
 
 // Division by a launch constant as one wide multiply and a shift: k = 31 + floor(log2 d),
 // m = ceil(2^k / d) <= 2^31; exact for n < 2^30 (n * (m d - 2^k) < n d < 2^k).
@@ -219,6 +231,8 @@ __device__ __forceinline__ void warp_sum3(int lane, double &a, double &b, double
 struct WarpSmem {
     alignas(16) double wx[KW_WARPS][32];
     alignas(16) double wy[KW_WARPS][32];
+    alignas(8) uint8_t fx[KW_WARPS][32];
+    alignas(8) uint8_t fy[KW_WARPS][32];
     uint32_t tm_base;
     int nlive;
 };
@@ -248,11 +262,12 @@ __host__ __device__ inline size_t kw_table_bytes(int P, int nx, int ny) {
 // runs under a whole block solve), so the warps of the grid finish together whatever the spread of CG
 // step counts; the first run of a warp is its own index.  The last CTA to leave zeroes the counters
 // for the next launch on the stream.
-template <bool RM, bool QT>
+template <bool RM, bool QT, bool DIRECT = false>
 __global__ void __maxnreg__(B200P_KW_MAXREG)
 oras_sweep_warp_kernel(const WarpSweepArgs A) {
     constexpr int TW = 8, TH = 4, BW = 32, BH = 32;
-    constexpr int NCOLW = QT ? 128 : 64;                   // TMEM columns per warp: v (64) [+ q (64)] per lane
+    // TMEM columns per warp and lane: v (64) [+ q (64)] [+ the lane's tile of u (64), DIRECT]; a power of two
+    constexpr int NCOLW = DIRECT ? (QT ? 256 : 128) : (QT ? 128 : 64);
     constexpr int NCOL = NCOLW * ((KW_WARPS + 3) / 4);     // warps w and w + 4 share a lane quarter
     __shared__ WarpSmem sm;
     extern __shared__ __align__(16) unsigned char kw_dyn[];
@@ -294,6 +309,7 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tv = sm.tm_base + ((uint32_t)((warp & 3) * 32) << 16) + (warp >> 2) * NCOLW;  // lane quarter
     const uint32_t tq = tv + 64;
+    const uint32_t tu = tv + (QT ? 128 : 64);
 
     const int W = L.w, H = L.h;
     const double hinv2 = L.hinv2, g_in = L.g_in;
@@ -397,6 +413,10 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
         const int blk = iy * L.nx + ix;
         const double rs_g = s_rs[p];
         __syncwarp();  // the previous item's weight rows have been consumed
+        if (DIRECT) {
+            sm.fx[warp][lane] = A.xflag[ix * BW + lane];
+            sm.fy[warp][lane] = A.yflag[iy * BH + lane];
+        }
         swx[lane] = L.wx[ix * BW + lane];
         swy[lane] = L.wy[iy * BH + lane];
         const int x0 = s_xs[ix], y0 = s_ys[iy];
@@ -452,6 +472,17 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
                     for (int i = 0; i < TW; ++i)
                         if ((mbits >> (j * TW + i)) & 1u)
                             r[j][i] = S.b[(size_t)p * S.plane + (size_t)(gy0 + j) * W + gx0 + i] - uc[j + 1][i + 1];
+            }
+        }
+
+        if (DIRECT) {
+            // the lane's own pixels of u wait in tensor memory for the direct update u_out = u + v
+#pragma unroll
+            for (int j = 0; j < TH; ++j) {
+                double urow[TW];
+#pragma unroll
+                for (int i = 0; i < TW; ++i) urow[i] = uc[j + 1][i + 1];
+                tm_st8(tu + 16 * j, urow);
             }
         }
 
@@ -617,20 +648,56 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
     _Pragma("unroll") for (int i = 0; i < TW; ++i) vf[J][i] = fma(a_last, pc[J][i], T.get(i));
             B200P_KW_VF(0, t0) B200P_KW_VF(1, t1) B200P_KW_VF(2, t2) B200P_KW_VF(3, t3)
 #undef B200P_KW_VF
+            if (!DIRECT) {
 #pragma unroll
-            for (int j = 0; j < TH; ++j) {
-                double2 *row = reinterpret_cast<double2 *>(out + (by + j) * BW + bx);
+                for (int j = 0; j < TH; ++j) {
+                    double2 *row = reinterpret_cast<double2 *>(out + (by + j) * BW + bx);
 #pragma unroll
-                for (int k = 0; k < TW / 2; ++k) {
-                    double2 o;
-                    o.x = (vf[j][2 * k] * wyv[j]) * wxv[2 * k];
-                    o.y = (vf[j][2 * k + 1] * wyv[j]) * wxv[2 * k + 1];
+                    for (int k = 0; k < TW / 2; ++k) {
+                        double2 o;
+                        o.x = (vf[j][2 * k] * wyv[j]) * wxv[2 * k];
+                        o.y = (vf[j][2 * k + 1] * wyv[j]) * wxv[2 * k + 1];
 #if B200P_KW_STCS
-                    __stcs(row + k, o);   // streaming store: the tile is not read again by this kernel
+                        __stcs(row + k, o);   // streaming store: the tile is not read again by this kernel
 #else
-                    row[k] = o;
+                        row[k] = o;
 #endif
+                    }
                 }
+            } else {
+                // Pixels with one writer (weight exactly 1 here, 0 in every other block) in single-writer rows
+                // and sector-aligned single-writer column groups go straight to the partner iterate; pixels of
+                // the overlap bands with a non-zero weight go to the tile; zero-weight pixels go nowhere.
+                const uint2 fxw = *reinterpret_cast<const uint2 *>(&sm.fx[warp][bx]);
+                const unsigned fyw = *reinterpret_cast<const unsigned *>(&sm.fy[warp][by]);
+                TmRow u0, u1, u2, u3;
+                tm_ld8(tu, u0);
+                tm_ld8(tu + 16, u1);
+                tm_ld8(tu + 32, u2);
+                tm_ld8(tu + 48, u3);
+                tm_wait_ld2(u0, u1);
+                tm_wait_ld2(u2, u3);
+                double *tile = S.scratch + ((size_t)p * L.nblocks + blk) * KW_TSZ + (x0 & (KW_ALIGN - 1));
+                double *uo = A.u_out + (size_t)p * S.plane + (size_t)gy0 * W + gx0;
+#define B200P_KW_OUT(J, U)                                                                               \
+    {                                                                                                    \
+        const unsigned fy = (fyw >> (8 * J)) & 0xffu;                                                    \
+        _Pragma("unroll") for (int k = 0; k < TW / 2; ++k) {                                             \
+            /* pixel pairs are homogeneous (checked when the plan is built): one flag byte decides */    \
+            const unsigned fa = ((k < 2 ? fxw.x : fxw.y) >> (16 * (k & 1))) & 0xffu;                     \
+            const bool direct = (fa & fy & 2u) != 0;                                                     \
+            const bool mine = (fa & fy & 1u) != 0;                                                       \
+            const double ta = (vf[J][2 * k] * wyv[J]) * wxv[2 * k];                                      \
+            const double tb = (vf[J][2 * k + 1] * wyv[J]) * wxv[2 * k + 1];                              \
+            if (direct && mine)                                                                          \
+                *reinterpret_cast<double2 *>(uo + (size_t)J * W + 2 * k) =                               \
+                    make_double2(U.get(2 * k) + ta, U.get(2 * k + 1) + tb);                              \
+            if (!direct)   /* zero-weight pixels of a band pair are stored as the zeros they are */      \
+                __stcs(reinterpret_cast<double2 *>(tile + (by + J) * KW_TP + bx + 2 * k), make_double2(ta, tb)); \
+        }                                                                                                \
+    }
+                B200P_KW_OUT(0, u0) B200P_KW_OUT(1, u1) B200P_KW_OUT(2, u2) B200P_KW_OUT(3, u3)
+#undef B200P_KW_OUT
             }
         }
         cur = nxt;

@@ -665,3 +665,25 @@ def test_fmg_solve_callback_after_every_cycle():
     assert np.array_equal(u1, u)
     with pytest.raises(NotImplementedError):
         bp.solve_channel(prob, "ml-oras", cfg_b, channel=0, callback=lambda uu: None)
+
+
+def test_band_combine_variant_agrees():
+    """Experiment (B200P_BAND=1, -DB200P_EXPERIMENTS): the block solve writes the single-writer pixels itself,
+    the combine pass visits the overlap bands only.  Same bits as the full combine (the tiles it skips are
+    exact zeros), same reports; levels too small for it keep the full combine."""
+    import os
+    _needs_experiments()
+    m, k = oracle.seeded_problem(1280, 720, 0.02, 3, channels=3)
+    cfg = bp.MultigridConfig(block_size=32, overlap=6, solver=bp.SolverConfig(tol_rel=1e-5))
+    mk = m.view(np.uint8)[None]
+    a = bp.Plan(1280, 720, 3, 1, cfg)
+    os.environ["B200P_BAND"] = "1"
+    try:
+        b = bp.Plan(1280, 720, 3, 1, cfg)
+    finally:
+        del os.environ["B200P_BAND"]
+    oa, ra = a.solve_host(mk, k[None])
+    ob, rb = b.solve_host(mk, k[None])
+    assert [(r.iterations, r.fine_smoother_iterations) for r in ra] == [(r.iterations, r.fine_smoother_iterations) for r in rb]
+    assert np.array_equal(oa, ob)
+    a.close(); b.close()
