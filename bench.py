@@ -173,7 +173,10 @@ def run_strip(args, rank, world, local):
     if "RANK" in os.environ and not dist.is_initialized():  # torchrun with one rank: still exercise NCCL
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if dist.is_initialized() and args.strip_transport == "ipc":
+    if args.strip_transport == "native":
+        # the library issues the NCCL calls itself; the strip solve replays as CUDA graphs
+        transport = strip.NcclNative()
+    elif dist.is_initialized() and args.strip_transport == "ipc":
         transport = strip.IpcTransport(dist.new_group(backend="gloo"))
     elif dist.is_initialized():
         transport = strip.TorchDistTransport()
@@ -203,6 +206,20 @@ def run_strip(args, rank, world, local):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = float(t.item())
+    single = None
+    if rank == 0 and world == 1:
+        # the same frame on ONE whole-image plan (single solve graph): what strip mode costs on one GPU
+        plan1 = bp.Plan(W, H, C, 1, cfg)
+        for _ in range(2):
+            plan1.solve_device(d_mask, d_known, d_out, want_reports=False)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            plan1.solve_device(d_mask, d_known, d_out, want_reports=False)
+        e1.record()
+        torch.cuda.synchronize()
+        single = args.steps / (e0.elapsed_time(e1) * 1e-3)
+        plan1.close()
     if rank == 0:
         lo, hi = solver.own
         print(json.dumps({
@@ -212,7 +229,8 @@ def run_strip(args, rank, world, local):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": name, "width": W, "height": H, "channels": C, "mask_density": density,
                        "block_size": bs, "overlap": ov, "tol_rel": 1e-3, "frames": 1,
-                       "v_cycles": [r.iterations for r in reports],
+                       "v_cycles": [r.iterations for r in reports], "whole_image_plan_value": single,
+                       "strip_over_whole_image": (args.steps / (ms_total * 1e-3)) / single if single else None,
                        "parallelism": f"1 frame in {world} horizontal strip(s); rank 0 owns rows [{lo}, {hi}); "
                                       f"halo exchange per sweep ({type(transport).__name__}), {args.strip_levels} striped level(s), "
                                       "coarser levels replicated"}}), flush=True)
@@ -366,8 +384,9 @@ def main():
     ap.add_argument("--strip", action="store_true",
                     help="single-frame strip mode: ONE frame cut into horizontal strips over the ranks "
                          "(halo exchange per sweep over NCCL); default workload 8k_rgb_2pct_b32o6")
-    ap.add_argument("--strip-transport", default="nccl", choices=["nccl", "ipc"],
-                    help="--strip exchange: torch.distributed NCCL, or CUDA-IPC peer memory + gloo control")
+    ap.add_argument("--strip-transport", default="native", choices=["native", "nccl", "ipc"],
+                    help="--strip exchange: native = NCCL calls issued by libb200paint on the solve stream (graphs); "
+                         "nccl = torch.distributed NCCL from a host callback; ipc = CUDA-IPC peer memory + gloo control")
     ap.add_argument("--strip-levels", type=int, default=2,
                     help="how many of the finest levels are striped in --strip mode (the rest is replicated)")
     ap.add_argument("--traffic-child", action="store_true", help=argparse.SUPPRESS)

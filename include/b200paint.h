@@ -162,6 +162,26 @@ int b200p_strip_ranges(int height, int block, int overlap, int levels, int rank,
  * b200p_plan_strip_ranges) and callback; rank / nranks themselves are the callback's business.
  * levels = 0 (and a NULL callback) leaves strip mode. */
 int b200p_plan_set_strip(b200p_plan *plan, int levels, const int *ranges, b200p_exchange_fn exchange, void *user);
+/* Strip mode with the LIBRARY doing the exchanges: `nccl_comm` is an ncclComm_t of `nranks`
+ * ranks (this process = `rank`), `ranges_all` the 6 * levels ints of EVERY rank, rank-major, as
+ * b200p_strip_ranges writes them.  Per sweep of a striped level the library issues, on the solve's stream,
+ *   ncclAllReduce(sum, P doubles) + ncclAllReduce(max, P ints)   after every K1   (global ||r||^2, flags)
+ *   ncclGroupStart; ncclSend / ncclRecv of the halo rows; ncclGroupEnd   after every combine
+ * and per V-cycle the halo / all-gather of the restricted residual: no host code between the kernels.  With
+ * use_graphs = 1 the front part and one V-cycle are captured as two CUDA graphs (collectives included) after
+ * one eager warm-up solve; the host reads the loop condition between replays.  libnccl.so.2 is loaded with
+ * dlopen on first use (the copy already in the process wins).  levels = 0 leaves strip mode. */
+int b200p_plan_set_strip_nccl(b200p_plan *plan, int levels, const int *ranges_all, int rank, int nranks,
+                              void *nccl_comm);
+/* For hosts without NCCL bindings: ncclGetUniqueId (128 bytes, to be broadcast by the caller),
+ * ncclCommInitRank on the current device, ncclCommDestroy. */
+int b200p_nccl_unique_id(void *id128);
+int b200p_nccl_comm_create(const void *id128, int rank, int nranks, void **nccl_comm);
+int b200p_nccl_comm_destroy(void *nccl_comm);
+/* The row intervals rank `rank` receives into / sends out of striped level `level` in one halo exchange,
+ * as (peer, y0, y1) triples (peer -1 pads the shorter list); returns max(#recv, #send).  Host-only. */
+int b200p_strip_halo_plan(const int *ranges_all, int levels, int level, int rank, int nranks, int *recv, int *send,
+                          int cap);
 /* Device pointer of the level's restricted-residual field (P,h,w) (level >= 1), for the callback. */
 int b200p_plan_level_rc(const b200p_plan *plan, int level, double **d_rc);
 /* Bytes of device memory the plan holds. */

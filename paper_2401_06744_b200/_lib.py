@@ -97,6 +97,11 @@ SIGNATURES = {
     "b200p_plan_destroy": (None, [_VP]),
     "b200p_plan_num_levels": (_I, [_VP]),
     "b200p_plan_level_info": (_I, [_VP, _I, C.POINTER(LevelInfo)]),
+    "b200p_plan_set_strip_nccl": (_I, [_VP, _I, _VP, _I, _I, _VP]),
+    "b200p_nccl_unique_id": (_I, [_VP]),
+    "b200p_nccl_comm_create": (_I, [_VP, _I, _I, C.POINTER(_VP)]),
+    "b200p_nccl_comm_destroy": (_I, [_VP]),
+    "b200p_strip_halo_plan": (_I, [_VP, _I, _I, _I, _I, _VP, _VP, _I]),
     "b200p_plan_strip_ranges": (_I, [_VP, _I, _I, _I, _VP]),
     "b200p_strip_ranges": (_I, [_I, _I, _I, _I, _I, _I, _VP]),
     "b200p_plan_set_strip": (_I, [_VP, _I, _VP, _VP, _VP]),

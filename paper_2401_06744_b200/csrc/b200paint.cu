@@ -10,6 +10,8 @@
 // launches CUDA kernels and returns the CUDA error if no device is present.
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
+#include <dlfcn.h>
+#include <nccl.h>   // types only: the library is loaded with dlopen when a strip plan asks for it
 
 #include <algorithm>
 #include <cmath>
@@ -270,6 +272,11 @@ struct b200p_plan {
     bool strip = false;
     b200p_exchange_fn exchange = nullptr;
     void *exchange_user = nullptr;
+    // native strip exchange: NCCL calls issued by the library on the solve's stream (capturable)
+    ncclComm_t nccl_comm = nullptr;
+    int nccl_rank = 0, nccl_nranks = 1, strip_levels = 0;
+    bool nccl_warm = false;               // one eager solve has run (NCCL connects peers lazily, outside capture)
+    std::vector<int> ranges_all;          // [rank][level][6] as b200p_strip_ranges writes them
     // CG-smoothed pipelines (cg, ml-cg, mg-cg): CG vectors sized for level 0 + per-problem state
     double *cg_r = nullptr, *cg_p = nullptr, *cg_q = nullptr;
     CgState cgs = {};
@@ -513,8 +520,144 @@ static int rows_chunk(int h) { return h >= 1024 ? 32 : (h >= 256 ? 16 : 8); }
 static bool striped(const b200p_plan *pl, const LevelHost &L) { return pl->strip && L.is_strip; }
 static int level_of(const b200p_plan *pl, const LevelHost &L) { return (int)(&L - &pl->lev[0]); }
 
+// ---- NCCL, loaded on demand (no link-time dependency: frame sharding never needs it) ----
+struct NcclApi {
+    void *handle = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommCount)(const ncclComm_t, int *) = nullptr;
+    ncclResult_t (*CommUserRank)(const ncclComm_t, int *) = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi *nccl_api() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        // the copy already in the process (torch loads its own) wins, then the system library
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            bool ok = true;
+#define NCCL_SYM(field, name) ok = ok && ((*(void **)(&api.field) = dlsym(h, name)) != nullptr)
+            NCCL_SYM(GetUniqueId, "ncclGetUniqueId");
+            NCCL_SYM(CommInitRank, "ncclCommInitRank");
+            NCCL_SYM(CommDestroy, "ncclCommDestroy");
+            NCCL_SYM(CommCount, "ncclCommCount");
+            NCCL_SYM(CommUserRank, "ncclCommUserRank");
+            NCCL_SYM(AllReduce, "ncclAllReduce");
+            NCCL_SYM(Send, "ncclSend");
+            NCCL_SYM(Recv, "ncclRecv");
+            NCCL_SYM(GroupStart, "ncclGroupStart");
+            NCCL_SYM(GroupEnd, "ncclGroupEnd");
+            NCCL_SYM(GetErrorString, "ncclGetErrorString");
+#undef NCCL_SYM
+            if (ok) api.handle = h;
+        }
+    }
+    return api.handle ? &api : nullptr;
+}
+
+#define NC(x)                                                                                        \
+    do {                                                                                             \
+        ncclResult_t r__ = (x);                                                                      \
+        if (r__ != ncclSuccess) return fail_arg(B200P_ERR_STATE, "%s: %s", #x, N->GetErrorString(r__)); \
+    } while (0)
+
+// Row intervals of a halo exchange on one striped level, seen from rank `me`: what it receives into its halo
+// [ext_lo, own_lo) + [own_hi, ext_hi) from the owners of those rows, and what it sends out of its own rows into
+// the halos of the others.  Both sides enumerate a pair's intervals from the RECEIVER's ranges (halo above,
+// then halo below), so sends and receives of a pair match in order.
+struct RowMove {
+    int peer, y0, y1;
+};
+static void halo_moves(const int *ranges_all, int levels, int level, int me, int nranks, std::vector<RowMove> &recv,
+                       std::vector<RowMove> &send) {
+    auto rg = [&](int q) { return ranges_all + ((size_t)q * levels + level) * 6; };
+    auto cut = [](const int *to, const int *from, int peer, std::vector<RowMove> &out) {
+        // rows of `to`'s halo that `from` owns
+        const int parts[2][2] = {{to[2], to[0]}, {to[1], to[3]}};
+        for (const auto &pr : parts) {
+            const int a = std::max(pr[0], from[0]), b = std::min(pr[1], from[1]);
+            if (a < b) out.push_back({peer, a, b});
+        }
+    };
+    recv.clear();
+    send.clear();
+    for (int q = 0; q < nranks; ++q) {
+        if (q == me) continue;
+        cut(rg(me), rg(q), q, recv);
+        cut(rg(q), rg(me), q, send);
+    }
+}
+
+// The exchanges of include/b200paint.h (B200P_XCHG_*) as NCCL calls on `st`.
+static int strip_exchange_nccl(b200p_plan *pl, int base, int level, void *d_ptr, cudaStream_t st) {
+    NcclApi *N = nccl_api();
+    if (!N) return fail_arg(B200P_ERR_STATE, "libnccl.so.2 could not be loaded");
+    const int P = pl->P, me = pl->nccl_rank, nr = pl->nccl_nranks;
+    if (base == B200P_XCHG_SUM_RS) {
+        NC(N->AllReduce(d_ptr, d_ptr, (size_t)P, ncclDouble, ncclSum, pl->nccl_comm, st));
+        return 0;
+    }
+    if (base == B200P_XCHG_MAX_FLAGS) {
+        NC(N->AllReduce(d_ptr, d_ptr, (size_t)P, ncclInt32, ncclMax, pl->nccl_comm, st));
+        return 0;
+    }
+    if (nr == 1) return 0;
+    const LevelHost &L = pl->lev[level];
+    const size_t w = (size_t)L.info.width, plane = w * L.info.height;
+    double *f = static_cast<double *>(d_ptr);
+    if (base == B200P_XCHG_HALO_U || base == B200P_XCHG_HALO_RC) {
+        std::vector<RowMove> recv, send;
+        halo_moves(pl->ranges_all.data(), pl->strip_levels, level, me, nr, recv, send);
+        NC(N->GroupStart());
+        for (const RowMove &m : send)
+            for (int p = 0; p < P; ++p)
+                NC(N->Send(f + p * plane + (size_t)m.y0 * w, (size_t)(m.y1 - m.y0) * w, ncclDouble, m.peer, pl->nccl_comm, st));
+        for (const RowMove &m : recv)
+            for (int p = 0; p < P; ++p)
+                NC(N->Recv(f + p * plane + (size_t)m.y0 * w, (size_t)(m.y1 - m.y0) * w, ncclDouble, m.peer, pl->nccl_comm, st));
+        NC(N->GroupEnd());
+        return 0;
+    }
+    if (base == B200P_XCHG_GATHER_RC) {
+        // `level` is the first replicated level: rank q restricted the halves of its rows of the level above
+        const int h1 = L.info.height, up = pl->strip_levels - 1;
+        auto rows = [&](int q, int &a, int &b) {
+            const int *r = pl->ranges_all.data() + ((size_t)q * pl->strip_levels + up) * 6;
+            a = r[0] / 2;
+            b = q == nr - 1 ? h1 : r[1] / 2;
+        };
+        int a0, b0;
+        rows(me, a0, b0);
+        NC(N->GroupStart());
+        for (int q = 0; q < nr; ++q) {
+            if (q == me) continue;
+            int a, b;
+            rows(q, a, b);
+            for (int p = 0; p < P; ++p) {
+                NC(N->Send(f + p * plane + (size_t)a0 * w, (size_t)(b0 - a0) * w, ncclDouble, q, pl->nccl_comm, st));
+                NC(N->Recv(f + p * plane + (size_t)a * w, (size_t)(b - a) * w, ncclDouble, q, pl->nccl_comm, st));
+            }
+        }
+        NC(N->GroupEnd());
+        return 0;
+    }
+    return fail_arg(B200P_ERR_ARG, "unknown exchange %d", base);
+}
+
 // kind = base + 16 * level of the field (include/b200paint.h)
 static int strip_exchange(b200p_plan *pl, int kind, void *d_ptr, cudaStream_t st, int level = 0) {
+    if (pl->nccl_comm) return strip_exchange_nccl(pl, kind, level, d_ptr, st);
     if (!pl->exchange) return fail_arg(B200P_ERR_STATE, "strip mode needs an exchange callback");
     kind += 16 * level;
     const int rc = pl->exchange(pl->exchange_user, kind, d_ptr, (void *)st);
@@ -1760,7 +1903,7 @@ template <class F>
 static int run_graph(b200p_plan *pl, GraphSlot &slot, const void *k0, const void *k1, const void *k2,
                      cudaStream_t st, F &&enqueue) {
     if (!pl->cfg.use_graphs || pl->profiling) return enqueue(st);
-    if (!slot.exec || slot.k0 != k0 || slot.k1 != k1 || slot.k2 != k2) {
+    if (!slot.exec || slot.k0 != k0 || slot.k1 != k1 || slot.k2 != k2 || slot.k3 != pl->egress) {
         if (slot.exec) {
             cudaGraphExecDestroy(slot.exec);
             slot.exec = nullptr;
@@ -1783,6 +1926,7 @@ static int run_graph(b200p_plan *pl, GraphSlot &slot, const void *k0, const void
         slot.k0 = k0;
         slot.k1 = k1;
         slot.k2 = k2;
+        slot.k3 = pl->egress;
     }
     CU(cudaGraphLaunch(slot.exec, st));
     pl->launches += slot.kernels;
@@ -2261,21 +2405,120 @@ int b200p_strip_ranges(int H, int block, int overlap, int levels, int rank, int 
     return 0;
 }
 
+static void drop_graphs(b200p_plan *pl) {
+    for (GraphSlot *g : {&pl->g_solve, &pl->g_front, &pl->g_cycle})
+        if (g->exec) {
+            cudaGraphExecDestroy(g->exec);
+            g->exec = nullptr;
+        }
+}
+
+static void leave_strip_mode(b200p_plan *pl) {
+    pl->strip = false;
+    pl->exchange = nullptr;
+    pl->nccl_comm = nullptr;
+    pl->ranges_all.clear();
+    for (LevelHost &L : pl->lev) {
+        L.is_strip = false;
+        L.own_lo = L.ext_lo = 0; L.own_hi = L.ext_hi = L.info.height; L.iy_lo = 0; L.iy_hi = L.info.ny;
+    }
+    drop_graphs(pl);
+}
+
+static int enter_strip_mode(b200p_plan *pl, int levels, const int *r);
+
 int b200p_plan_set_strip(b200p_plan *pl, int levels, const int *r, b200p_exchange_fn exchange, void *user) {
     if (!pl) return fail_arg(B200P_ERR_ARG, "null argument");
     if (pl->pending) return fail_arg(B200P_ERR_STATE, "a solve is pending on this plan");
     if (levels == 0 || !exchange) {  // back to the whole image
         if (levels != 0) return fail_arg(B200P_ERR_ARG, "strip mode needs an exchange callback");
-        pl->strip = false;
-        pl->exchange = nullptr;
-        for (LevelHost &L : pl->lev) {
-            L.is_strip = false;
-            L.own_lo = L.ext_lo = 0; L.own_hi = L.ext_hi = L.info.height; L.iy_lo = 0; L.iy_hi = L.info.ny;
-        }
+        leave_strip_mode(pl);
         return 0;
     }
     if (!r) return fail_arg(B200P_ERR_ARG, "null argument");
-    if (pl->cfg.use_graphs) return fail_arg(B200P_ERR_STATE, "strip plans run eagerly: create the plan with use_graphs = 0");
+    if (pl->cfg.use_graphs) return fail_arg(B200P_ERR_STATE, "strip plans with a host callback run eagerly: create the plan with use_graphs = 0");
+    int rc = enter_strip_mode(pl, levels, r);
+    if (rc) return rc;
+    pl->nccl_comm = nullptr;
+    pl->exchange = exchange;
+    pl->exchange_user = user;
+    return 0;
+}
+
+int b200p_plan_set_strip_nccl(b200p_plan *pl, int levels, const int *ranges_all, int rank, int nranks, void *comm) {
+    if (!pl) return fail_arg(B200P_ERR_ARG, "null argument");
+    if (pl->pending) return fail_arg(B200P_ERR_STATE, "a solve is pending on this plan");
+    if (levels == 0) {
+        leave_strip_mode(pl);
+        return 0;
+    }
+    if (!ranges_all || !comm) return fail_arg(B200P_ERR_ARG, "null argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail_arg(B200P_ERR_ARG, "bad rank %d of %d", rank, nranks);
+    NcclApi *N = nccl_api();
+    if (!N) return fail_arg(B200P_ERR_STATE, "libnccl.so.2 could not be loaded");
+    int count = 0, urank = -1;
+    NC(N->CommCount((ncclComm_t)comm, &count));
+    NC(N->CommUserRank((ncclComm_t)comm, &urank));
+    if (count != nranks || urank != rank)
+        return fail_arg(B200P_ERR_ARG, "communicator is rank %d of %d, the strip layout says rank %d of %d", urank, count,
+                        rank, nranks);
+    int rc = enter_strip_mode(pl, levels, ranges_all + (size_t)rank * levels * 6);
+    if (rc) return rc;
+    pl->exchange = nullptr;
+    pl->nccl_comm = (ncclComm_t)comm;
+    pl->nccl_rank = rank;
+    pl->nccl_nranks = nranks;
+    pl->strip_levels = levels;
+    pl->ranges_all.assign(ranges_all, ranges_all + (size_t)nranks * levels * 6);
+    return 0;
+}
+
+int b200p_nccl_unique_id(void *id128) {
+    NcclApi *N = nccl_api();
+    if (!N) return fail_arg(B200P_ERR_STATE, "libnccl.so.2 could not be loaded");
+    if (!id128) return fail_arg(B200P_ERR_ARG, "null argument");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    NC(N->GetUniqueId(static_cast<ncclUniqueId *>(id128)));
+    return 0;
+}
+
+int b200p_nccl_comm_create(const void *id128, int rank, int nranks, void **comm) {
+    NcclApi *N = nccl_api();
+    if (!N) return fail_arg(B200P_ERR_STATE, "libnccl.so.2 could not be loaded");
+    if (!id128 || !comm) return fail_arg(B200P_ERR_ARG, "null argument");
+    ncclUniqueId id;
+    memcpy(&id, id128, sizeof id);
+    ncclComm_t c = nullptr;
+    NC(N->CommInitRank(&c, nranks, id, rank));
+    *comm = c;
+    return 0;
+}
+
+int b200p_nccl_comm_destroy(void *comm) {
+    NcclApi *N = nccl_api();
+    if (!N) return fail_arg(B200P_ERR_STATE, "libnccl.so.2 could not be loaded");
+    if (comm) NC(N->CommDestroy((ncclComm_t)comm));
+    return 0;
+}
+
+int b200p_strip_halo_plan(const int *ranges_all, int levels, int level, int rank, int nranks, int *recv, int *send,
+                          int cap) {
+    if (!ranges_all || levels < 1 || level < 0 || level >= levels || nranks < 1 || rank < 0 || rank >= nranks)
+        return fail_arg(B200P_ERR_ARG, "bad argument");
+    std::vector<RowMove> r, s;
+    halo_moves(ranges_all, levels, level, rank, nranks, r, s);
+    const int n = (int)std::max(r.size(), s.size());
+    if (recv && send)
+        for (int i = 0; i < std::min(cap, n); ++i) {
+            const RowMove none = {-1, 0, 0};
+            const RowMove &a = i < (int)r.size() ? r[i] : none, &b = i < (int)s.size() ? s[i] : none;
+            recv[3 * i] = a.peer; recv[3 * i + 1] = a.y0; recv[3 * i + 2] = a.y1;
+            send[3 * i] = b.peer; send[3 * i + 1] = b.y0; send[3 * i + 2] = b.y1;
+        }
+    return n;
+}
+
+static int enter_strip_mode(b200p_plan *pl, int levels, const int *r) {
     if (pl->cfg.mode != 0 || pl->cfg.smoother != 0)
         return fail_arg(B200P_ERR_UNSUPPORTED, "strip mode covers the mg-oras path only");
     if (levels < 1 || levels + 1 > (int)pl->lev.size())
@@ -2303,8 +2546,7 @@ int b200p_plan_set_strip(b200p_plan *pl, int levels, const int *r, b200p_exchang
         }
     }
     pl->strip = true;
-    pl->exchange = exchange;
-    pl->exchange_user = user;
+    drop_graphs(pl);
     return 0;
 }
 
@@ -2524,10 +2766,30 @@ static int solve_async_impl(b200p_plan *pl, const uint8_t *d_mask, const double 
         return 0;
     }
     pl->pending_eager = !graphs;
-    if (graphs) {
+    if (graphs && pl->strip && pl->nccl_comm && pl->nccl_warm) {
+        // Strip mode with the library's own NCCL exchange: kernels and collectives of the front part and of
+        // one V-cycle are two captured graphs; the host only reads the loop condition between replays.
+        pl->pending_eager = true;
+        if ((rc = run_graph(pl, pl->g_front, d_mask, d_known, d_out, st,
+                            [&](cudaStream_t s) { return enqueue_front(pl, d_out, s); })))
+            return rc;
+        pl->hierarchy_ready = true;
+        CU(cudaStreamSynchronize(st));
+        int done = 0;
+        while (*pl->h_any && done < pl->cfg.v_cycles_max) {
+            if ((rc = run_graph(pl, pl->g_cycle, d_mask, d_known, d_out, st,
+                                [&](cudaStream_t s) { return enqueue_cycle(pl, d_out, s); })))
+                return rc;
+            ++done;
+            CU(cudaStreamSynchronize(st));
+        }
+        if ((rc = enqueue_reports(pl, st))) return rc;
+    } else if (graphs && !pl->strip) {
         if ((rc = launch_solve_graph(pl, d_mask, d_known, d_out, st))) return rc;
         pl->hierarchy_ready = true;
     } else {
+        pl->pending_eager = true;
+        if (pl->strip && pl->nccl_comm) pl->nccl_warm = true;
         // eager: the host reads the loop condition after every cycle
         if ((rc = enqueue_front(pl, d_out, st))) return rc;
         pl->hierarchy_ready = true;

@@ -68,6 +68,22 @@ def halo_plan(ranges, rank):
     return recv, send
 
 
+def native_halo_plan(ranges_by_level, level, rank):
+    """The library's own halo plan (b200p_strip_halo_plan, what the NCCL exchange walks): (recv, send) lists of
+    (peer, y0, y1), for comparison with `halo_plan`."""
+    levels, nranks = len(ranges_by_level), len(ranges_by_level[0])
+    flat = [v for q in range(nranks) for l in range(levels) for v in ranges_by_level[l][q]]
+    every = (C.c_int * len(flat))(*flat)
+    cap = 4 * nranks
+    r, s = (C.c_int * (3 * cap))(), (C.c_int * (3 * cap))()
+    n = _lib.lib().b200p_strip_halo_plan(C.cast(every, C.c_void_p), levels, level, rank, nranks,
+                                         C.cast(r, C.c_void_p), C.cast(s, C.c_void_p), cap)
+    if n < 0:
+        _lib.check(n)
+    unpack = lambda a: [(a[3 * i], a[3 * i + 1], a[3 * i + 2]) for i in range(n) if a[3 * i] >= 0]
+    return unpack(r), unpack(s)
+
+
 def strip_ranges(height, block_size, overlap, nranks, levels=1):
     """ranges[l][q] = (own_lo, own_hi, ext_lo, ext_hi, iy_lo, iy_hi) of rank q on striped level l
     (host-only geometry).  With levels == 1 the list of level 0 is returned directly."""
@@ -138,6 +154,35 @@ class TorchDistTransport(Transport):
             self.dist.broadcast(chunk, src=q, group=self.group)
             if q != self.rank:
                 field[:, a:b].copy_(chunk)
+
+
+class NcclNative(Transport):
+    """The library's own exchange (b200p_plan_set_strip_nccl): an NCCL communicator created through the C-ABI
+    helpers, the unique id broadcast over `group` (any torch.distributed backend; none needed for one rank).
+    There are no per-exchange methods: halo send / recv, the norm all-reduces and the residual all-gather are
+    issued by libb200paint on the solve's stream, so a strip solve runs as captured CUDA graphs."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            self.rank, self.nranks = dist.get_rank(group), dist.get_world_size(group)
+        else:
+            self.rank, self.nranks = 0, 1
+        uid = (C.c_ubyte * 128)()
+        if self.rank == 0:
+            _lib.check(_lib.lib().b200p_nccl_unique_id(C.cast(uid, C.c_void_p)))
+        if self.nranks > 1:
+            box = [bytes(uid)]
+            dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+            uid = (C.c_ubyte * 128).from_buffer_copy(box[0])
+        comm = C.c_void_p()
+        _lib.check(_lib.lib().b200p_nccl_comm_create(C.cast(uid, C.c_void_p), self.rank, self.nranks, C.byref(comm)))
+        self.comm = comm
+
+    def close(self):
+        if getattr(self, "comm", None):
+            _lib.lib().b200p_nccl_comm_destroy(self.comm)
+            self.comm = None
 
 
 class IpcTransport(Transport):
@@ -283,7 +328,9 @@ class StripSolver:
         work replicated, 2 about 6 %."""
         self.t = transport
         self.cfg = cfg or MultigridConfig()
-        self.plan = Plan(width, height, channels, 1, self.cfg, spacing, use_graphs=False)
+        native = isinstance(transport, NcclNative)
+        # a host callback between the kernels forces eager launches; the native exchange is captured with them
+        self.plan = Plan(width, height, channels, 1, self.cfg, spacing, use_graphs=native)
         self.levels = int(levels)
         if not 1 <= self.levels < self.plan.num_levels:
             raise ValueError(f"need 1 <= striped levels < {self.plan.num_levels}")
@@ -298,6 +345,12 @@ class StripSolver:
         # rows of the first replicated level that every rank restricted from the last striped level
         self.gather_rows = coarse_rows(self.ranges_by_level[-1], self.shapes[self.levels][1])
         self.error = None
+        if native:
+            flat = [v for q in range(transport.nranks) for l in range(self.levels) for v in self.ranges_by_level[l][q]]
+            every = (C.c_int * len(flat))(*flat)
+            _lib.check(_lib.lib().b200p_plan_set_strip_nccl(self.plan.handle, self.levels, C.cast(every, C.c_void_p),
+                                                            transport.rank, transport.nranks, transport.comm))
+            return
         self._cb = _EXCHANGE_FN(self._exchange)  # keep the callback object alive
         flat = [v for l in range(self.levels) for v in self.ranges_by_level[l][transport.rank]]
         mine = (C.c_int * len(flat))(*flat)

@@ -141,3 +141,43 @@ def test_strip_solve_over_cuda_ipc_processes(world, levels):
         p.join(timeout=120)
         assert p.exitcode == 0
     np.testing.assert_allclose(full, ref.fields, rtol=0, atol=1e-9)
+
+
+def test_native_nccl_strip_one_rank_runs_as_graphs():
+    """b200p_plan_set_strip_nccl: the library issues the exchanges itself (ncclAllReduce of the partial norms on a
+    one-rank communicator here; halo send / recv have no peer) and the strip solve is captured as graphs.  Same
+    cycle counts and fields as the whole-image plan; the second solve (graph replay) equals the first (eager
+    warm-up) bit for bit."""
+    w, h, c = 640, 400, 3
+    m, k = oracle.seeded_problem(w, h, 0.02, 3, channels=c)
+    cfg = bp.MultigridConfig(block_size=32, overlap=6, solver=bp.SolverConfig(tol_rel=1e-6))
+    ref = bp.solve_image(bp.InpaintingProblem(m, k), "mg-oras", cfg)
+    for levels in (1, 2):
+        t = strip.NcclNative()
+        assert (t.rank, t.nranks) == (0, 1)
+        s = strip.StripSolver(w, h, c, cfg, t, levels=levels)
+        out1, reps1 = s.solve(m, k)
+        out1 = out1.cpu().numpy()
+        launches = s.plan.launch_count
+        out2, reps2 = s.solve(m, k)
+        out2 = out2.cpu().numpy()
+        assert s.plan.launch_count > launches
+        assert [r.iterations for r in reps1] == [r.iterations for r in reps2] == [r.iterations for r in ref.reports]
+        assert np.array_equal(out1, out2)
+        assert np.abs(out1 - ref.fields).max() <= 1e-9
+        for r1, r0 in zip(reps2, ref.reports):
+            assert r1.final_rel_residual == pytest.approx(r0.final_rel_residual, rel=1e-9)
+        s.close()
+    with pytest.raises(ValueError, match="communicator is rank"):
+        t = strip.NcclNative()
+        plan = bp.Plan(w, h, c, 1, cfg)
+        rg = strip.strip_ranges(h, 32, 6, 2, 1)
+        flat = [v for q in range(2) for v in rg[q]]
+        import ctypes as C
+        from paper_2401_06744_b200 import _lib
+        arr = (C.c_int * len(flat))(*flat)
+        try:
+            _lib.check(_lib.lib().b200p_plan_set_strip_nccl(plan.handle, 1, C.cast(arr, C.c_void_p), 0, 2, t.comm))
+        finally:
+            plan.close()
+            t.close()

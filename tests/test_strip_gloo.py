@@ -122,3 +122,28 @@ def test_gloo_transport_matches_local():
         u, rc, rs, fl = res[r]
         assert np.array_equal(u, exp[r][0].numpy()) and np.array_equal(rc, exp[r][1].numpy())
         assert rs.tolist() == [6.0, 3.0] and fl.tolist() == [1, 0]
+
+
+@pytest.mark.parametrize("height,nranks,levels", [(700, 3, 1), (2160, 8, 2), (4320, 8, 3), (1080, 2, 2), (333, 4, 1)])
+def test_native_halo_plan_matches_the_python_plan(height, nranks, levels):
+    """The row intervals the library's NCCL exchange walks (b200p_strip_halo_plan) are those of strip.halo_plan,
+    per pair of ranks in the same order on the sending and on the receiving side (NCCL matches the sends and
+    receives of a pair in issue order), and together they fill every halo exactly once."""
+    rg = strip.strip_ranges(height, BLOCK, OVERLAP, nranks, levels)
+    by_level = [rg] if levels == 1 else rg
+    for l in range(levels):
+        plans = [strip.native_halo_plan(by_level, l, r) for r in range(nranks)]
+        for r in range(nranks):
+            recv, send = plans[r]
+            want_recv, want_send = strip.halo_plan(by_level[l], r)
+            assert sorted(recv) == sorted(want_recv) and sorted(send) == sorted(want_send)
+            for q in range(nranks):
+                if q == r:
+                    continue
+                # what r sends to q, in order == what q expects from r, in order
+                assert [(a, b) for p, a, b in send if p == q] == [(a, b) for p, a, b in plans[q][0] if p == r]
+            own_lo, own_hi, ext_lo, ext_hi = by_level[l][r][:4]
+            covered = sorted((a, b) for _, a, b in recv)
+            halo_rows = (own_lo - ext_lo) + (ext_hi - own_hi)
+            assert sum(b - a for a, b in covered) == halo_rows
+            assert all(covered[i][1] <= covered[i + 1][0] for i in range(len(covered) - 1))
