@@ -47,13 +47,37 @@ def _require_built(name: str):
             f"pipeline {name!r} is outside the B200 hot path; only {BUILT} are built")
 
 
+HBM_PEAK_GBS = 6546.0   # measured copy bandwidth of the B200s this was built on (MEASURED_PEAKS.json)
+
+
+def algorithmic_bytes(width: int, height: int, channels: int, v_cycles: int) -> float:
+    """Compulsory HBM traffic of one mg-oras solve: every array of a fused stage touched once,
+    B = (6.67 + 15.33 V) C s N0 + (4.67 + 9.33 V) m N0 with s = 8 (fp64), m = 1 (mask byte), V = V-cycles."""
+    n0 = float(width) * float(height)
+    return (6.67 + 15.33 * v_cycles) * channels * 8.0 * n0 + (4.67 + 9.33 * v_cycles) * n0
+
+
 @dataclass
 class SolveResult:
-    """pipelines.py:75-93."""
+    """pipelines.py:75-93, plus the throughput view of the call: frames/s, algorithmic HBM GB/s and
+    its fraction of the measured HBM peak -- of the whole host-to-host call, copies included."""
 
     fields: np.ndarray
     reports: list
     elapsed: float
+
+    @property
+    def frames_per_s(self) -> float:
+        return 1.0 / self.elapsed if self.elapsed > 0 else float("inf")
+
+    @property
+    def hbm_gbs(self) -> float:
+        c, h, w = self.fields.shape
+        return algorithmic_bytes(w, h, c, self.iterations) / 1e9 / self.elapsed if self.elapsed > 0 else float("inf")
+
+    @property
+    def roofline_fraction(self) -> float:
+        return self.hbm_gbs / HBM_PEAK_GBS
 
     @property
     def converged(self) -> bool:

@@ -387,7 +387,13 @@ class StripSolver:
         c, h, w = self.shape
         d_mask = _dev.to_device_u8(np.ascontiguousarray(mask).view(np.uint8).reshape(1, h, w))
         d_known = _dev.to_device_f64(np.ascontiguousarray(known, dtype=np.float64).reshape(1, c, h, w))
-        d_out = self.t.zeros_f64((1, c, h, w))
+        # one output buffer per solver (a transport may hand out cudaMalloc'ed memory that peers map: allocating
+        # per solve would leak it and grow the peer-mapping cache); the caller gets a copy of the owned rows
+        if getattr(self, "_d_out", None) is None:
+            self._d_out = self.t.zeros_f64((1, c, h, w))
+        else:
+            self._d_out.zero_()
+        d_out = self._d_out
         try:
             _, reports = self.plan.solve_device(d_mask, d_known, d_out)
         except Exception:
@@ -395,9 +401,10 @@ class StripSolver:
                 raise self.error
             raise
         lo, hi = self.own
-        return d_out[0, :, lo:hi], reports
+        return d_out[0, :, lo:hi].clone(), reports
 
     def close(self):
+        self._d_out = None
         self.plan.close()
         if hasattr(self.t, "close"):
             self.t.close()

@@ -119,3 +119,31 @@ def test_long_histories_are_truncated_loudly():
         warnings.simplefilter("error")
         short = bp.solve_image(bp.InpaintingProblem(m, k), "mg-oras", cfg_b)
     assert len(short.reports[0].history) == short.reports[0].iterations + 1
+
+
+def test_solve_result_throughput_view_and_strip_output_ownership():
+    """SolveResult carries frames/s, algorithmic HBM GB/s and its roofline fraction; a strip solver
+    hands out a copy of its rows (its one output buffer is reused by the next solve)."""
+    from paper_2401_06744_b200 import strip
+    from paper_2401_06744_b200.pipelines import algorithmic_bytes
+    w, h, c = 640, 400, 3
+    m, k = oracle.seeded_problem(w, h, 0.02, 3, channels=c)
+    cfg = bp.MultigridConfig(block_size=32, overlap=6)
+    res = bp.solve_image(bp.InpaintingProblem(m, k), "mg-oras", cfg)
+    assert res.frames_per_s == pytest.approx(1.0 / res.elapsed)
+    assert res.hbm_gbs == pytest.approx(algorithmic_bytes(w, h, c, res.iterations) / 1e9 / res.elapsed)
+    assert 0.0 < res.roofline_fraction < 1.0
+    m2, k2 = oracle.seeded_problem(w, h, 0.05, 9, channels=c)
+    s = strip.StripSolver(w, h, c, cfg, strip.LocalGroup(1).transport(0))
+    a, _ = s.solve(m, k)
+    keep = a.clone()
+    b, _ = s.solve(m2, k2)
+    assert torch_equal(a, keep) and not torch_equal(a, b)
+    s.close()
+    assert torch_equal(a, keep)          # still valid after the solver is gone
+    assert np.abs(a.cpu().numpy() - res.fields).max() <= 1e-9
+
+
+def torch_equal(x, y):
+    import torch
+    return bool(torch.equal(x, y))
