@@ -99,7 +99,9 @@ def solve_channel(problem: InpaintingProblem, name: str, cfg: MultigridConfig | 
     base, mode = split_solver_name(name)
     if mode == "single":
         if callback is not None:
-            raise NotImplementedError("per-sweep callbacks are not available on the CUDA path")
+            if base != "oras":
+                raise NotImplementedError("per-step callbacks of the single-level CG solver are not built on the CUDA path")
+            return _oras_solve_stepwise(problem, (cfg or MultigridConfig()), channel, callback)
         sub = InpaintingProblem(problem.mask, problem.known[channel], problem.spacing)
         res = solve_image(sub, name, cfg)
         return res.fields[0], res.reports[0]
@@ -107,6 +109,41 @@ def solve_channel(problem: InpaintingProblem, name: str, cfg: MultigridConfig | 
     if hierarchy is None:
         hierarchy = build_hierarchy(problem, cfg)
     return fmg_solve(hierarchy, cfg, channel, callback=callback)
+
+
+def _oras_solve_stepwise(problem: InpaintingProblem, cfg: MultigridConfig, channel: int, callback):
+    """oras_solve with `callback(u)` after every sweep (solvers.py:427-485): the reference's own structure -- the
+    sweeps are driven one at a time through `oras_sweeps(..., on_state=)` (same kernels as the one-call solve), the
+    history is the relative residual at every residual evaluation."""
+    from .partition import build_partition, build_weights
+    from .solvers import BlockSolver, oras_sweeps
+    t0 = time.perf_counter()
+    s = cfg.solver
+    h, w = problem.shape
+    part = build_partition(w, h, cfg.block_size, cfg.overlap)
+    op = problem.operator()
+    blocks = BlockSolver(problem.mask, problem.spacing, part, build_weights(part), s.alpha)
+    b = problem.rhs(channel)
+    u = problem.flat_init(channel)
+    r0 = float(np.linalg.norm(op.residual(b, u)))
+    if r0 == 0.0:
+        return u, SolveReport(solver="oras", iterations=0, final_rel_residual=0.0, wall_time=time.perf_counter() - t0,
+                              history=[0.0], converged=True, baseline_residual=r0, init_residual=r0,
+                              fine_smoother_iterations=0)
+    history = []
+
+    def on_state(uu, rn_now, sweeps_done):
+        history.append(rn_now / r0)
+        if sweeps_done > 0:
+            callback(uu)
+
+    sweeps, rn = oras_sweeps(op, blocks, b, u, max_sweeps=s.max_outer_iters, stop_norm=s.tol_rel * r0,
+                             eta=s.local_tol_fraction, local_max_iters=s.local_max_iters or 4 * part.block_h * part.block_w,
+                             on_state=on_state)
+    rel = rn / r0
+    return u, SolveReport(solver="oras", iterations=sweeps, final_rel_residual=rel, wall_time=time.perf_counter() - t0,
+                          history=history, converged=rel <= s.tol_rel, baseline_residual=r0, init_residual=r0,
+                          fine_smoother_iterations=sweeps)
 
 
 def solve_image(problem: InpaintingProblem, name: str = "mg-oras",

@@ -687,3 +687,24 @@ def test_band_combine_variant_agrees():
     assert [(r.iterations, r.fine_smoother_iterations) for r in ra] == [(r.iterations, r.fine_smoother_iterations) for r in rb]
     assert np.array_equal(oa, ob)
     a.close(); b.close()
+
+
+def test_single_level_oras_callback_after_every_sweep():
+    """oras_solve(..., callback=cb) (solvers.py:469-472): the iterate after every sweep; sweeps, history and the
+    field as the one-call solve and the oracle."""
+    m, k = oracle.seeded_problem(120, 90, 0.08, 5, channels=2)
+    cfg = bp.MultigridConfig(block_size=16, overlap=2, solver=bp.SolverConfig(tol_rel=1e-4))
+    prob = bp.InpaintingProblem(m, k)
+    for c in range(2):
+        seen = []
+        u, rep = bp.solve_channel(prob, "oras", cfg, channel=c, callback=lambda uu: seen.append(uu.copy()))
+        u0, rep0 = bp.solve_channel(prob, "oras", cfg, channel=c)
+        uo, ro = oracle.oras_solve(m, k[c], 1.0, 16, 2, oracle.SolverConfig(tol_rel=1e-4))
+        assert rep.iterations == rep0.iterations == ro["iterations"] == len(seen) > 3
+        assert len(rep.history) == len(ro["history"]) == rep.iterations + 1
+        np.testing.assert_allclose(rep.history, ro["history"], rtol=1e-6)
+        assert np.array_equal(seen[-1], u) and not np.array_equal(seen[0], seen[-1])
+        assert np.abs(u - u0).max() <= 1e-9 and np.abs(u - uo).max() <= 1e-9
+        assert rep.converged and rep.fine_smoother_iterations == rep.iterations
+    with pytest.raises(NotImplementedError):
+        bp.solve_channel(prob, "cg", cfg, channel=0, callback=lambda uu: None)
