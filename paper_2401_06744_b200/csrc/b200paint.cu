@@ -288,6 +288,7 @@ struct b200p_plan {
     uint8_t *d_io_u8 = nullptr;
     uint8_t *d_mask_bits = nullptr;       // P4 raster of the image entry points (F, h, ceil(w / 8))
     // 8-bit egress of the solve being enqueued: target image (F, h, w, C), the sweep that carries it
+    bool u_zero_now = false;              // the next sweep's iterate is an implicit zero field (not to be read)
     uint8_t *egress = nullptr, *egress_now = nullptr;
     const double *egress_src = nullptr;   // the fp64 result the tail pass converts
     bool egress_fused = false;            // a combine pass of the cycle body writes the image
@@ -1069,6 +1070,11 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, UBuf &ub, cons
     SweepArgs A;
     fill_sweep_args(pl, L, u, b, pred, A);
     A.iy0 = L.iy_lo;
+    const bool u_zero = pl->u_zero_now;   // set by enqueue_vcycle for the first sweep on a fresh correction
+    pl->u_zero_now = false;
+    if (u_zero && !(tile == TILE_32_W && tma_eligible(L, u, b, rm)))
+        return fail_arg(B200P_ERR_STATE, "implicit zero iterate on a level without the warp-per-block kernel");
+    A.u_zero = u_zero ? 1 : 0;
     dim3 grid(L.nblocks, pl->P);
     // band combine (experiment, B200P_BAND=1 in a -DB200P_EXPERIMENTS build): K2W updates the single-writer
     // pixels itself, the combine pass visits the overlap bands only, u.cur -> u.alt.  Not in strip mode, and
@@ -1216,7 +1222,7 @@ static int launch_sweep_split(b200p_plan *pl, const LevelHost &L, UBuf &ub, cons
         if (eg) pl->egress_fused = true;
         oras_combine_kernel<<<g, ST_THREADS_COMBINE, 0, st>>>(L.dev, pl->d_scratch, A.plane, pred,
                                                               pl->d_rs, u, unit_counter, L.own_lo, L.own_hi,
-                                                              eg, pl->C);
+                                                              eg, pl->C, u_zero ? 1 : 0);
         CU(cudaGetLastError());
     }
     // strip mode: the rows the neighbours' block solves and stencils read from this strip
@@ -1405,7 +1411,7 @@ static int enqueue_cascade(b200p_plan *pl, double *d_u0, cudaStream_t st) {
 // The iterate enters and leaves in u.cur == its home buffer.
 static int enqueue_vcycle(b200p_plan *pl, int level, UBuf &u, const double *b, bool rm,
                           const int *pred, int *unit_counter, bool have_norm, cudaStream_t st,
-                          bool settle_home = true) {
+                          bool settle_home = true, bool u_is_zero = false) {
     const int nl = (int)pl->lev.size();
     LevelHost &L = pl->lev[level];
     const b200p_config &cfg = pl->cfg;
@@ -1418,17 +1424,26 @@ static int enqueue_vcycle(b200p_plan *pl, int level, UBuf &u, const double *b, b
     int rc;
     {
         NvtxScope nv("vcycle pre-smooth", level);
+        pl->u_zero_now = u_is_zero;   // the first sweep neither reads u nor needs it zeroed beforehand
         rc = enqueue_smooth(pl, L, u, b, rm, cfg.nu_pre, pred, uc, have_norm, st);
+        pl->u_zero_now = false;
     }
     if (rc) return rc;
     LevelHost &Cc = pl->lev[level + 1];
     UBuf e = level_ubuf(pl, level + 1, nullptr);
     bool coarse_norm = false;  // K3 also produced ||r_c||^2 = residual norm^2 of the coarse system at e = 0
+    bool e_implicit = false;   // the coarse correction starts as an implicit zero field
     {
         LaunchScope sc(pl, st, KK_RESTRICT, field_bytes(pl, L, rm ? 1.25 : 2.25, 1.25));
-        // e is zeroed by the coarse solve (init_mode 0) on the coarsest level, else here
-        double *ez = (level + 1 == nl - 1) ? nullptr : e.cur;
-        if (rows4_ok(L, u.cur, b) && ((uintptr_t)Cc.d_rc % 16) == 0 && ((uintptr_t)Cc.d_mask % 2) == 0) {
+        // e is zeroed by the coarse solve (init_mode 0) on the coarsest level; on a level whose first sweep runs
+        // the warp-per-block kernel it stays IMPLICITLY zero (that sweep does not read it, its combine pass
+        // writes every pixel): no zeroing pass, no first read; everywhere else it is zeroed here
+        const bool rows4 = rows4_ok(L, u.cur, b) && ((uintptr_t)Cc.d_rc % 16) == 0 && ((uintptr_t)Cc.d_mask % 2) == 0;
+        static const bool want_implicit = !(getenv("B200P_IMPLICIT_ZERO") && atoi(getenv("B200P_IMPLICIT_ZERO")) == 0);
+        e_implicit = want_implicit && level + 1 != nl - 1 && rows4 && !striped(pl, L) && !striped(pl, Cc) && cfg.nu_pre > 0 &&
+                     !Cc.fused && Cc.tile == TILE_32_W && tma_eligible(Cc, e.cur, Cc.d_rc, false) && Cc.nblocks > 1;
+        double *ez = (level + 1 == nl - 1 || e_implicit) ? nullptr : e.cur;
+        if (rows4) {
             RestrictArgs RA;
             RA.R = rows_args(pl, L, u.cur, b, pred);
             RA.R.trust = rm && trust_mask_enabled();
@@ -1469,7 +1484,8 @@ static int enqueue_vcycle(b200p_plan *pl, int level, UBuf &u, const double *b, b
         rc = launch_coarse(pl, Cc, e.cur, Cc.d_rc, false, 0, tol, cfg.coarse_max_iters, pred,
                            nullptr, 0, st);
     } else {
-        rc = enqueue_vcycle(pl, level + 1, e, Cc.d_rc, false, pred, nullptr, coarse_norm, st, false);
+        rc = enqueue_vcycle(pl, level + 1, e, Cc.d_rc, false, pred, nullptr, coarse_norm, st, false,
+                            e_implicit && coarse_norm);
     }
     if (rc) return rc;
     {

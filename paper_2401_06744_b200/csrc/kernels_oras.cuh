@@ -38,7 +38,9 @@ struct SweepArgs {
     double eta;            // local_tol_fraction
     int max_iters;         // local CG cap
     double *scratch;       // (P, nblocks, bh, bw) weighted corrections
-    int iy0;               // first block row of this launch (strip mode; default 0)
+    int iy0 = 0;           // first block row of this launch (strip mode; default 0)
+    int u_zero = 0;        // the iterate is identically 0 and must not be read (a V-cycle correction before its
+                           // first sweep, multigrid.py:361): the warp-per-block kernel and the combine honour it
 };
 
 // ------------------------------------------------------------------ K2 ----
@@ -597,12 +599,21 @@ __global__ void __launch_bounds__(ST_THREADS_COMBINE)
 oras_combine_kernel(const LevelDev L, const double *__restrict__ scratch, size_t plane,
                     const int *__restrict__ pred, const double *__restrict__ rs,
                     double *__restrict__ u, int *__restrict__ unit_counter, int y_lo, int y_hi,
-                    uint8_t *__restrict__ egress, int channels) {
+                    uint8_t *__restrict__ egress, int channels, int u_zero = 0) {
     __shared__ int s_rn[COMBINE_ROWS], s_rf[COMBINE_ROWS];
     __shared__ size_t s_roff[COMBINE_ROWS][2];
     const int p = blockIdx.z;
     if (pred && !pred[p]) return;
-    if (rs[p] == 0.0) return;
+    if (rs[p] == 0.0) {
+        // nothing to correct; an implicitly zero iterate (u_zero) has to become a real zero field now
+        if (u_zero) {
+            const int x = blockIdx.x * ST_THREADS_COMBINE + threadIdx.x;
+            const int ya = y_lo + blockIdx.y * COMBINE_ROWS, yb = min(ya + COMBINE_ROWS, y_hi);
+            if (x < L.w)
+                for (int y = ya; y < yb; ++y) u[(size_t)p * plane + (size_t)y * L.w + x] = 0.0;
+        }
+        return;
+    }
     const int tid = threadIdx.x;
     const int x = blockIdx.x * ST_THREADS_COMBINE + tid;
     const int y0 = y_lo + blockIdx.y * COMBINE_ROWS;  // rows [y_lo, y_hi): the whole level, or a strip
@@ -635,7 +646,7 @@ oras_combine_kernel(const LevelDev L, const double *__restrict__ scratch, size_t
         for (int j = 0; j < G; ++j) {
             const int k = k0 + j < rows ? k0 + j : rows - 1;
             const size_t o0 = s_roff[k][0], o1 = s_roff[k][1];
-            uu[j] = up[(size_t)(y0 + k) * L.w + x];
+            uu[j] = u_zero ? 0.0 : up[(size_t)(y0 + k) * L.w + x];
             v00[j] = sp[o0 + xo0];
             v01[j] = sp[o0 + (two_x ? xo1 : xo0)];
             v10[j] = sp[o1 + xo0];

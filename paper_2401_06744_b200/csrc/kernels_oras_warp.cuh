@@ -338,7 +338,13 @@ oras_sweep_warp_kernel(const WarpSweepArgs A) {
         const int frame = S.channels == 3 ? w.p / 3 : (S.channels == 1 ? w.p : w.p / S.channels);
         mbits = A.mtab[((size_t)frame * L.nblocks + w.iy * L.nx + w.ix) * 32 + lane];
         const double *urow = S.u + (size_t)w.p * S.plane + (size_t)(gy0 - 1) * W + gx0;
-        if (!(x0 == 0 || y0 == 0 || x0 + BW >= W || y0 + BH >= H)) {
+        if (S.u_zero) {
+            // a coarse correction before its first sweep: identically 0, never written, never read
+#pragma unroll
+            for (int j = 0; j < TH + 2; ++j)
+#pragma unroll
+                for (int i = 0; i < TW + 2; ++i) uc[j][i] = 0.0;
+        } else if (!(x0 == 0 || y0 == 0 || x0 + BW >= W || y0 + BH >= H)) {
 #pragma unroll
             for (int j = 0; j < TH + 2; ++j) {
                 const double *rp = urow + (size_t)j * W;
