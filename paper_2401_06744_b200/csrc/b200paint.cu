@@ -25,6 +25,7 @@
 #include "../../include/b200paint.h"
 #include "kernels_stencil.cuh"
 #include "kernels_rows.cuh"
+#include "kernels_rows_tma.cuh"
 #include "kernels_oras.cuh"
 #include "kernels_oras_warp.cuh"
 // Block-solve variants that lost their A/B are compiled only on request:
@@ -704,6 +705,44 @@ static RowsArgs rows_args(b200p_plan *pl, const LevelHost &L, const double *u, c
     return R;
 }
 
+// ---- tensor maps (cuTensorMapEncodeTiled through the runtime's driver entry point: no libcuda link)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn tensor_map_encoder() {
+    static EncodeTiledFn fn = []() -> EncodeTiledFn {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return nullptr;
+        return (EncodeTiledFn)p;
+    }();
+    return fn;
+}
+
+// (P, h, w) planes of fp64 (elem = 8) or bytes (elem = 1) as a 3-D tensor; box = bw x bh x 1 elements.
+static int encode_plane_map(CUtensorMap *tm, const void *base, int elem, int w, int h, int planes, int box_w, int box_h) {
+    EncodeTiledFn enc = tensor_map_encoder();
+    if (!enc) return fail_arg(B200P_ERR_STATE, "cuTensorMapEncodeTiled is not available in this driver");
+    cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)planes};
+    cuuint64_t strides[2] = {(cuuint64_t)w * elem, (cuuint64_t)w * h * elem};
+    cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(tm, elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 3,
+                     const_cast<void *>(base), dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail_arg(B200P_ERR_STATE, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return 0;
+}
+
+static int encode_field_map(CUtensorMap *tm, const double *base, int w, int h, int planes, int box_w, int box_h) {
+    return encode_plane_map(tm, base, 8, w, h, planes, box_w, box_h);
+}
+
 // K1: rs[p] = ||b - A u||^2, mflag[p].  UM/RM as in residual_px.
 static int launch_norm(b200p_plan *pl, const LevelHost &L, const double *u, const double *b,
                        bool um, bool rm, const int *pred, cudaStream_t st) {
@@ -712,6 +751,43 @@ static int launch_norm(b200p_plan *pl, const LevelHost &L, const double *u, cons
     LaunchScope sc(pl, st, KK_NORM, field_bytes(pl, L, rm ? 1.0 : 2.0, 1.0));
 #define NORM_ARGS u, b, L.d_mask, L.info.height, L.info.width, L.dev.hinv2, pl->C, plane, pred, \
                   pl->d_partial, pl->d_partial_flag, pl->d_counter, pl->d_rs, pl->d_mflag
+    static const bool want_tma = !(getenv("B200P_ROWS_TMA") && atoi(getenv("B200P_ROWS_TMA")) == 0);
+    if (want_tma && !um && rows4_ok(L, u, b) && L.info.width % 16 == 0 && L.info.width >= RT_W &&
+        L.info.height >= 4 * RT_R && ((uintptr_t)L.d_mask % 16) == 0) {
+        // TMA-fed tile pipeline (kernels_rows_tma.cuh): bytes in flight independent of registers
+        RowsArgs R = rows_args(pl, L, u, b, pred);
+        R.trust = rm && trust_mask_enabled();
+        const bool with_b = !(rm && R.trust);
+        {
+            // long strips amortise the pipeline fill (one DRAM latency per CTA); at least ~4 CTAs per SM slot overall
+            static const int tiles = getenv("B200P_ROWS_TMA_TILES") ? atoi(getenv("B200P_ROWS_TMA_TILES")) : 32;
+            R.rows_per_cta = std::max(4, tiles) * RT_R;
+        }
+        CUtensorMap tu, tm, tb;
+        int rc = encode_plane_map(&tu, u, 8, L.info.width, L.info.height, pl->P, RT_BOXW, RT_R + 2);
+        if (!rc) rc = encode_plane_map(&tm, L.d_mask, 1, L.info.width, L.info.height, pl->F, RT_W, RT_R);
+        if (!rc) rc = with_b ? encode_plane_map(&tb, b, 8, L.info.width, L.info.height, pl->P, RT_W, RT_R) : 0;
+        if (rc) return rc;
+        if (!with_b) tb = tu;
+        static bool attr = false;
+        if (!attr) {
+            CU(cudaFuncSetAttribute(residual_sqnorm_tma_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_tma_smem(false)));
+            CU(cudaFuncSetAttribute(residual_sqnorm_tma_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_tma_smem(true)));
+            CU(cudaFuncSetAttribute(residual_sqnorm_tma_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_tma_smem(true)));
+            attr = true;
+        }
+        dim3 g((L.info.width + RT_W - 1) / RT_W, (R.y_hi - R.y_lo + R.rows_per_cta - 1) / R.rows_per_cta, pl->P);
+        if (rm && !with_b) residual_sqnorm_tma_kernel<true, false><<<g, RT_THREADS, rows_tma_smem(false), st>>>(R, tu, tm, tb);
+        else if (rm) residual_sqnorm_tma_kernel<true, true><<<g, RT_THREADS, rows_tma_smem(true), st>>>(R, tu, tm, tb);
+        else residual_sqnorm_tma_kernel<false, true><<<g, RT_THREADS, rows_tma_smem(true), st>>>(R, tu, tm, tb);
+        CU(cudaGetLastError());
+        if (striped(pl, L)) {
+            int rc2 = strip_exchange(pl, B200P_XCHG_SUM_RS, pl->d_rs, st);
+            if (!rc2) rc2 = strip_exchange(pl, B200P_XCHG_MAX_FLAGS, pl->d_mflag, st);
+            return rc2;
+        }
+        return 0;
+    }
     if (rows4_ok(L, u, b)) {
         // four columns per thread, 16-byte loads (kernels_rows.cuh)
         RowsArgs R = rows_args(pl, L, u, b, pred);
@@ -922,38 +998,6 @@ static int launch_sweep_fused(b200p_plan *pl, const LevelHost &L, UBuf &u, const
 }
 
 // ---- K2T: TMA-fed persistent sweep kernel (kernels_oras_tma.cuh)
-typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
-                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
-                                  CUtensorMapFloatOOBfill);
-
-static EncodeTiledFn tensor_map_encoder() {
-    static EncodeTiledFn fn = []() -> EncodeTiledFn {
-        void *p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            return nullptr;
-        return (EncodeTiledFn)p;
-    }();
-    return fn;
-}
-
-// (P, h, w) fp64 planes as a 3-D tensor; box = bw x bh x 1 elements.
-static int encode_field_map(CUtensorMap *tm, const double *base, int w, int h, int planes, int box_w, int box_h) {
-    EncodeTiledFn enc = tensor_map_encoder();
-    if (!enc) return fail_arg(B200P_ERR_STATE, "cuTensorMapEncodeTiled is not available in this driver");
-    cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)planes};
-    cuuint64_t strides[2] = {(cuuint64_t)w * 8, (cuuint64_t)w * h * 8};
-    cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
-    cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(base), dims, strides, box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail_arg(B200P_ERR_STATE, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-    return 0;
-}
-
 // Combine on arrival inside K2 (no K2b launch, tiles consumed from L2): opt-in with B200P_ARRIVAL=1.
 // Parity-exact, but measured slower than K2 + K2b (193 vs 243 fps): the fence + arrival atomics + two
 // batches of L2 reads add ~5 k cycles of pure latency to every block in a kernel that is bound by

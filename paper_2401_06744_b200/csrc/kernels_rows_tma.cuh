@@ -1,0 +1,138 @@
+// kernels_rows_tma.cuh -- K1 as a TMA-fed pipeline: ||b - A u||^2 per problem (solvers.py:415-417,
+// core.py:100-110) for levels whose rows are 16-byte multiples in the mask plane too (w % 16 == 0).
+//
+// The register-window row walker (kernels_rows.cuh) keeps ONE row of 32 bytes per thread in flight; at the
+// measured DRAM latency that caps it near 4.8 TB/s (a plain read-only reduction reaches 6.7 TB/s on this
+// GPU).  Here the bytes in flight do not depend on registers: a CTA owns a strip of RT_W columns and streams
+// tiles of RT_R rows (+ one halo row above and below, + two halo columns on each side: the innermost TMA
+// coordinate must be 16-byte aligned) through a ring of RT_STAGES shared-memory stages filled by
+// cp.async.bulk.tensor; pixels outside the image arrive as zeros, which is exactly what the reflecting stencil
+// adds for them.  Thread (t, g) walks rows [g RT_R / RT_G, (g + 1) RT_R / RT_G) of column t of every tile with a
+// three-row register window (vertical neighbours) and reads its horizontal neighbours from the stage: consecutive
+// threads, consecutive words, no bank conflicts.  The arithmetic of a pixel is that of walk_rows4, operation by operation; the per-CTA partials
+// are reduced by the same deterministic last-CTA scheme (publish_partial).
+#pragma once
+#include "kernels_rows.cuh"
+#include "tma_utils.cuh"
+
+namespace b200p {
+
+constexpr int RT_W = 128;                 // columns per CTA
+constexpr int RT_G = 4;                   // row groups per tile: RT_W x RT_G threads per CTA
+constexpr int RT_THREADS = RT_W * RT_G;
+constexpr int RT_BOXW = RT_W + 4;         // box columns x0 - 2 .. x0 + RT_W + 1
+constexpr int RT_R = 16;                  // rows per tile
+constexpr int RT_STAGES = 4;
+constexpr int RT_U_BYTES = (RT_R + 2) * RT_BOXW * 8;            // 19008
+constexpr int RT_U_STRIDE = (RT_U_BYTES + 127) / 128 * 128;     // 19072: stages stay 128-byte aligned
+constexpr int RT_M_BYTES = RT_R * RT_W;                         // 2048
+constexpr int RT_B_BYTES = RT_R * RT_W * 8;                     // 16384
+__host__ __device__ inline size_t rows_tma_smem(bool with_b) {
+    return (size_t)RT_STAGES * (RT_U_STRIDE + RT_M_BYTES + (with_b ? RT_B_BYTES : 0)) + 128;
+}
+
+// RM: the right-hand side is where(mask, b, 0); with A.trust the caller guarantees u == b at mask pixels and b
+// is never read (WITH_B = false).  rows_per_cta comes in A.rows_per_cta (a multiple of RT_R).
+template <bool RM, bool WITH_B>
+__global__ void __launch_bounds__(RT_THREADS)
+residual_sqnorm_tma_kernel(const RowsArgs A, const __grid_constant__ CUtensorMap tm_u,
+                           const __grid_constant__ CUtensorMap tm_m, const __grid_constant__ CUtensorMap tm_b) {
+    extern __shared__ __align__(128) unsigned char rt_smem[];
+    __shared__ double red[34];
+    __shared__ int sflag;
+    __shared__ bool is_last;
+    __shared__ __align__(8) unsigned long long full[RT_STAGES];
+    const int p = blockIdx.z;
+    if (A.pred && !A.pred[p]) return;
+    const int t = threadIdx.x & (RT_W - 1), g = threadIdx.x / RT_W;
+    const bool leader = threadIdx.x == 0;
+    unsigned char *base = rt_smem;   // 128-byte aligned by declaration: the pointers stay in the shared window
+    unsigned char *su = base, *smk = base + RT_STAGES * RT_U_STRIDE, *sb = smk + RT_STAGES * RT_M_BYTES;
+    if (leader) {
+        sflag = 0;
+        for (int s = 0; s < RT_STAGES; ++s) mbar_init(smem_u32(&full[s]), 1);
+    }
+    __syncthreads();
+    const int h = A.h, w = A.w;
+    const int xs = blockIdx.x * RT_W;
+    const int x = xs + t;
+    const bool live = x < w;
+    const int y0 = A.y_lo + blockIdx.y * A.rows_per_cta;
+    const int y1 = min(A.y_hi, y0 + A.rows_per_cta);
+    const int ntiles = (y1 - y0 + RT_R - 1) / RT_R;
+    const int frame = p / A.channels;
+    auto issue = [&](int tile) {
+        const int s = tile % RT_STAGES;
+        const unsigned bar = smem_u32(&full[s]);
+        mbar_expect_tx(bar, RT_U_BYTES + RT_M_BYTES + (WITH_B ? RT_B_BYTES : 0));
+        const int ty = y0 + tile * RT_R;
+        tma_load_3d(smem_u32(su + s * RT_U_STRIDE), &tm_u, xs - 2, ty - 1, p, bar);
+        tma_load_3d(smem_u32(smk + s * RT_M_BYTES), &tm_m, xs, ty, frame, bar);
+        if (WITH_B) tma_load_3d(smem_u32(sb + s * RT_B_BYTES), &tm_b, xs, ty, p, bar);
+    };
+    if (leader)
+        for (int tile = 0; tile < min(RT_STAGES, ntiles); ++tile) issue(tile);
+    const double hinv2 = A.hinv2, nh = -hinv2;
+    const double cx = 4.0 - ((x == 0 ? 1.0 : 0.0) + (x == w - 1 ? 1.0 : 0.0));
+    const double cxh = cx * hinv2;
+    const bool trust = RM && A.trust != 0;
+    constexpr int RG = RT_R / RT_G;
+    double acc = 0.0;
+    int flag = 0;
+    for (int tile = 0; tile < ntiles; ++tile) {
+        const int s = tile % RT_STAGES;
+        mbar_wait(smem_u32(&full[s]), (tile / RT_STAGES) & 1);
+        const int ty = y0 + tile * RT_R;
+        const int rows = min(RT_R, y1 - ty);
+        const int r0 = g * RG;
+        const double *U = reinterpret_cast<const double *>(su + s * RT_U_STRIDE) + r0 * RT_BOXW + (t + 2);
+        const unsigned char *M = smk + s * RT_M_BYTES + r0 * RT_W + t;
+        const double *B = reinterpret_cast<const double *>(sb + s * RT_B_BYTES) + r0 * RT_W + t;
+        double above = U[0], centre = U[RT_BOXW];
+        if (!WITH_B && rows == RT_R && ty > 0 && ty + RT_R < h) {
+            // the common tile: all rows present, no image border row, b - u = 0 at mask pixels (trusted):
+            // r = -(A u) off the mask and 0 on it; only r^2 is needed, so the sign is dropped
+#pragma unroll
+            for (int rr = 0; rr < RG; ++rr) {
+                const double below = U[(rr + 2) * RT_BOXW];
+                const double lf = U[(rr + 1) * RT_BOXW - 1], rt = U[(rr + 1) * RT_BOXW + 1];
+                const unsigned char m = M[rr * RT_W];
+                const double sum = ((above + below) + lf) + rt;
+                double au = sum * nh + cxh * centre;
+                au = m ? 0.0 : au;
+                acc += au * au;
+                above = centre;
+                centre = below;
+            }
+        } else {
+            const int r1 = min(r0 + RG, rows);
+            for (int r = r0; r < r1; ++r) {
+                const int rr = r - r0, y = ty + r;
+                const double below = U[(rr + 2) * RT_BOXW];
+                const double lf = U[(rr + 1) * RT_BOXW - 1], rt = U[(rr + 1) * RT_BOXW + 1];
+                const unsigned char m = M[rr * RT_W];
+                const double cy = (y == 0 ? 1.0 : 0.0) + (y == h - 1 ? 1.0 : 0.0);
+                const double c = centre;
+                double bb;
+                if (RM) bb = (WITH_B && m && !trust) ? B[rr * RT_W] : 0.0;
+                else bb = WITH_B ? B[rr * RT_W] : 0.0;
+                const double sum = ((above + below) + lf) + rt;
+                const double au = sum * nh + ((cx - cy) * hinv2) * c;
+                const double res = (trust && m) ? 0.0 : bb - (m ? c : au);
+                acc += res * res;
+                if (m && res != 0.0) flag = 1;
+                above = centre;
+                centre = below;
+            }
+        }
+        __syncthreads();   // every thread is done with stage s
+        if (leader && tile + RT_STAGES < ntiles) issue(tile + RT_STAGES);
+    }
+    if (!live) {   // columns right of the image see the last column as a neighbour: not part of the sum
+        acc = 0.0;
+        flag = 0;
+    }
+    publish_partial(acc, flag, p, A, red, &sflag, &is_last);
+}
+
+}  // namespace b200p
