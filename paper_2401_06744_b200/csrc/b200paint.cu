@@ -1494,10 +1494,35 @@ static int enqueue_vcycle(b200p_plan *pl, int level, UBuf &u, const double *b, b
             RA.cmask = Cc.d_mask;
             RA.rc = Cc.d_rc;
             RA.e_zero = ez;
-            dim3 g4((L.info.width / 4 + ROWS4_THREADS - 1) / ROWS4_THREADS,
-                    (RA.R.y_hi - RA.R.y_lo + RA.R.rows_per_cta - 1) / RA.R.rows_per_cta, pl->P);
-            if (rm) residual_restrict_rows4_kernel<true><<<g4, ROWS4_THREADS, 0, st>>>(RA);
-            else residual_restrict_rows4_kernel<false><<<g4, ROWS4_THREADS, 0, st>>>(RA);
+            static const bool want_tma = !(getenv("B200P_ROWS_TMA") && atoi(getenv("B200P_ROWS_TMA")) != 1);   // 2: K1 only
+            if (want_tma && L.info.width % 16 == 0 && L.info.width >= RT_W && L.info.height >= 4 * RT_R &&
+                ((uintptr_t)L.d_mask % 16) == 0) {
+                // TMA-fed tile pipeline (kernels_rows_tma.cuh)
+                const bool with_b = !(rm && RA.R.trust);
+                RA.R.rows_per_cta = 32 * RT_R;
+                CUtensorMap tu, tm, tb;
+                int rc2 = encode_plane_map(&tu, u.cur, 8, L.info.width, L.info.height, pl->P, RT_BOXW, RT_R + 2);
+                if (!rc2) rc2 = encode_plane_map(&tm, L.d_mask, 1, L.info.width, L.info.height, pl->F, RT_W, RT_R);
+                if (!rc2) rc2 = with_b ? encode_plane_map(&tb, b, 8, L.info.width, L.info.height, pl->P, RT_W, RT_R) : 0;
+                if (rc2) return rc2;
+                if (!with_b) tb = tu;
+                static bool attr = false;
+                if (!attr) {
+                    CU(cudaFuncSetAttribute(residual_restrict_tma_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_tma_smem(false)));
+                    CU(cudaFuncSetAttribute(residual_restrict_tma_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_tma_smem(true)));
+                    CU(cudaFuncSetAttribute(residual_restrict_tma_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_tma_smem(true)));
+                    attr = true;
+                }
+                dim3 gt((L.info.width + RT_W - 1) / RT_W, (RA.R.y_hi - RA.R.y_lo + RA.R.rows_per_cta - 1) / RA.R.rows_per_cta, pl->P);
+                if (rm && !with_b) residual_restrict_tma_kernel<true, false><<<gt, RK_THREADS, rows_tma_smem(false), st>>>(RA, tu, tm, tb);
+                else if (rm) residual_restrict_tma_kernel<true, true><<<gt, RK_THREADS, rows_tma_smem(true), st>>>(RA, tu, tm, tb);
+                else residual_restrict_tma_kernel<false, true><<<gt, RK_THREADS, rows_tma_smem(true), st>>>(RA, tu, tm, tb);
+            } else {
+                dim3 g4((L.info.width / 4 + ROWS4_THREADS - 1) / ROWS4_THREADS,
+                        (RA.R.y_hi - RA.R.y_lo + RA.R.rows_per_cta - 1) / RA.R.rows_per_cta, pl->P);
+                if (rm) residual_restrict_rows4_kernel<true><<<g4, ROWS4_THREADS, 0, st>>>(RA);
+                else residual_restrict_rows4_kernel<false><<<g4, ROWS4_THREADS, 0, st>>>(RA);
+            }
             coarse_norm = !striped(pl, L);  // a strip only has its share of ||r_c||^2: the coarse level takes its own norm
         } else if (striped(pl, L)) {
             return fail_arg(B200P_ERR_UNSUPPORTED, "strip mode needs the row-walker kernels (width % 4 == 0)");

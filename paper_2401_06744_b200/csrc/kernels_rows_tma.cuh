@@ -135,4 +135,131 @@ residual_sqnorm_tma_kernel(const RowsArgs A, const __grid_constant__ CUtensorMap
     publish_partial(acc, flag, p, A, red, &sflag, &is_last);
 }
 
+// ---------------------------------------------------------------- K3 ------
+// Residual + 2x2 restriction + ||r_c||^2 (multigrid.py:358-361, :149-154) on the same tile pipeline.  Thread (t, g)
+// owns the coarse pixel (column t of the strip's 64 coarse columns, coarse row g of the tile's RT_R / 2): its
+// four fine pixels are two 16-byte words of the stage, their left / right neighbours two more 8-byte reads
+// per row.  Cell mean in NumPy's order (a00 + a01) + (a10 + a11), true constituent count (w % 4 == 0, so only
+// the last row of an odd-height level makes a one-row cell), 0 at coarse mask pixels; the coarse mask byte of
+// the NEXT tile's cell is fetched one tile ahead, so no global load sits in a tile's critical path.
+constexpr int RK_G = RT_R / 2;             // coarse rows per tile = row groups
+constexpr int RK_THREADS = (RT_W / 2) * RK_G;
+
+template <bool RM, bool WITH_B>
+__global__ void __launch_bounds__(RK_THREADS)
+residual_restrict_tma_kernel(const RestrictArgs A, const __grid_constant__ CUtensorMap tm_u,
+                             const __grid_constant__ CUtensorMap tm_m, const __grid_constant__ CUtensorMap tm_b) {
+    extern __shared__ __align__(128) unsigned char rt_smem[];
+    __shared__ double red[34];
+    __shared__ int sflag;
+    __shared__ bool is_last;
+    __shared__ __align__(8) unsigned long long full[RT_STAGES];
+    const RowsArgs &R = A.R;
+    const int p = blockIdx.z;
+    if (R.pred && !R.pred[p]) return;
+    const int t = threadIdx.x & (RT_W / 2 - 1), g = threadIdx.x / (RT_W / 2);
+    const bool leader = threadIdx.x == 0;
+    unsigned char *su = rt_smem, *smk = rt_smem + RT_STAGES * RT_U_STRIDE, *sb = smk + RT_STAGES * RT_M_BYTES;
+    if (leader) {
+        sflag = 0;
+        for (int s = 0; s < RT_STAGES; ++s) mbar_init(smem_u32(&full[s]), 1);
+    }
+    __syncthreads();
+    const int h = R.h, w = R.w;
+    const int hc = (h + 1) >> 1, wc = w >> 1;
+    const int xs = blockIdx.x * RT_W;
+    const int x = xs + 2 * t;                 // the thread's two fine columns x, x + 1
+    const bool live = x < w;
+    const int y0 = R.y_lo + blockIdx.y * R.rows_per_cta;   // even
+    const int y1 = min(R.y_hi, y0 + R.rows_per_cta);
+    const int ntiles = (y1 - y0 + RT_R - 1) / RT_R;
+    const int frame = p / R.channels;
+    const size_t cplane = (size_t)hc * wc;
+    const uint8_t *cm = A.cmask + (size_t)frame * cplane;
+    double *rc = A.rc + (size_t)p * cplane;
+    double *ez = A.e_zero ? A.e_zero + (size_t)p * cplane : nullptr;
+    auto issue = [&](int tile) {
+        const int s = tile % RT_STAGES;
+        const unsigned bar = smem_u32(&full[s]);
+        mbar_expect_tx(bar, RT_U_BYTES + RT_M_BYTES + (WITH_B ? RT_B_BYTES : 0));
+        const int ty = y0 + tile * RT_R;
+        tma_load_3d(smem_u32(su + s * RT_U_STRIDE), &tm_u, xs - 2, ty - 1, p, bar);
+        tma_load_3d(smem_u32(smk + s * RT_M_BYTES), &tm_m, xs, ty, frame, bar);
+        if (WITH_B) tma_load_3d(smem_u32(sb + s * RT_B_BYTES), &tm_b, xs, ty, p, bar);
+    };
+    if (leader)
+        for (int tile = 0; tile < min(RT_STAGES, ntiles); ++tile) issue(tile);
+    const double hinv2 = R.hinv2, nh = -hinv2;
+    const double cx0 = 4.0 - (x == 0 ? 1.0 : 0.0), cx1 = 4.0 - (x + 2 == w ? 1.0 : 0.0);
+    const double c0h = cx0 * hinv2, c1h = cx1 * hinv2;
+    const bool trust = RM && R.trust != 0;
+    double acc = 0.0;
+    auto coarse_mask_of = [&](int tile) -> uint8_t {
+        const int ya = y0 + tile * RT_R + 2 * g;
+        return (live && tile < ntiles && ya < y1) ? cm[(size_t)(ya >> 1) * wc + (x >> 1)] : (uint8_t)0;
+    };
+    uint8_t cmk_next = coarse_mask_of(0);
+    for (int tile = 0; tile < ntiles; ++tile) {
+        const int s = tile % RT_STAGES;
+        const int ty = y0 + tile * RT_R;
+        const int ya = ty + 2 * g;                         // the cell's fine rows ya, ya + 1
+        const bool cell = live && ya < y1;
+        const int Y = ya >> 1;
+        const uint8_t cmk = cmk_next;
+        cmk_next = coarse_mask_of(tile + 1);               // in flight during this tile
+        mbar_wait(smem_u32(&full[s]), (tile / RT_STAGES) & 1);
+        if (cell) {
+            const double *U = reinterpret_cast<const double *>(su + s * RT_U_STRIDE) + (2 * g) * RT_BOXW + (2 * t + 2);
+            const unsigned char *M = smk + s * RT_M_BYTES + (2 * g) * RT_W + 2 * t;
+            const double2 u0 = *reinterpret_cast<const double2 *>(U);                    // row ya - 1
+            const double2 u1 = *reinterpret_cast<const double2 *>(U + RT_BOXW);          // row ya
+            const double2 u2 = *reinterpret_cast<const double2 *>(U + 2 * RT_BOXW);      // row ya + 1
+            const double2 u3 = *reinterpret_cast<const double2 *>(U + 3 * RT_BOXW);      // row ya + 2
+            const double l1 = U[RT_BOXW - 1], r1 = U[RT_BOXW + 2], l2 = U[2 * RT_BOXW - 1], r2 = U[2 * RT_BOXW + 2];
+            const uchar2 m1 = *reinterpret_cast<const uchar2 *>(M), m2 = *reinterpret_cast<const uchar2 *>(M + RT_W);
+            const size_t ci = (size_t)Y * wc + (x >> 1);
+            double o;
+            if (!WITH_B && ya > 0 && ya + 2 < h) {
+                // the common cell: both rows inside the image, trusted mask pixels (r = 0 there, -(A u) elsewhere)
+                const double a00 = m1.x ? 0.0 : 0.0 - ((((u0.x + u2.x) + l1) + u1.y) * nh + c0h * u1.x);
+                const double a01 = m1.y ? 0.0 : 0.0 - ((((u0.y + u2.y) + u1.x) + r1) * nh + c1h * u1.y);
+                const double a10 = m2.x ? 0.0 : 0.0 - ((((u1.x + u3.x) + l2) + u2.y) * nh + c0h * u2.x);
+                const double a11 = m2.y ? 0.0 : 0.0 - ((((u1.y + u3.y) + u2.x) + r2) * nh + c1h * u2.y);
+                o = cmk ? 0.0 : ((a00 + a01) + (a10 + a11)) / 4.0;
+            } else {
+                const double *B = reinterpret_cast<const double *>(sb + s * RT_B_BYTES) + (2 * g) * RT_W + 2 * t;
+                const bool two = ya + 1 < h;               // odd height: the last cell has one row
+                const double cya = (ya == 0 ? 1.0 : 0.0) + (ya == h - 1 ? 1.0 : 0.0);
+                const double cyb = (ya + 1 == h - 1 ? 1.0 : 0.0);
+                auto res = [&](double c, double up, double dn, double lf, double rt, double cnt, uint8_t m, double b) {
+                    const double sum = ((up + dn) + lf) + rt;
+                    const double au = sum * nh + (cnt * hinv2) * c;
+                    const double bb = RM ? ((WITH_B && m && !trust) ? b : 0.0) : (WITH_B ? b : 0.0);
+                    return (trust && m) ? 0.0 : bb - (m ? c : au);
+                };
+                const double b00 = WITH_B ? B[0] : 0.0, b01 = WITH_B ? B[1] : 0.0;
+                const double b10 = WITH_B ? B[RT_W] : 0.0, b11 = WITH_B ? B[RT_W + 1] : 0.0;
+                const double a00 = res(u1.x, u0.x, u2.x, l1, u1.y, cx0 - cya, m1.x, b00);
+                const double a01 = res(u1.y, u0.y, u2.y, u1.x, r1, cx1 - cya, m1.y, b01);
+                double s0 = a00 + a01, cnt = 2.0;
+                if (two) {
+                    const double a10 = res(u2.x, u1.x, u3.x, l2, u2.y, cx0 - cyb, m2.x, b10);
+                    const double a11 = res(u2.y, u1.y, u3.y, u2.x, r2, cx1 - cyb, m2.y, b11);
+                    s0 = s0 + (a10 + a11);
+                    cnt = 4.0;
+                } else {
+                    s0 = s0 + 0.0;
+                }
+                o = cmk ? 0.0 : s0 / cnt;
+            }
+            rc[ci] = o;
+            if (ez) ez[ci] = 0.0;
+            acc += o * o;
+        }
+        __syncthreads();   // every thread is done with stage s
+        if (leader && tile + RT_STAGES < ntiles) issue(tile + RT_STAGES);
+    }
+    publish_partial(acc, 0, p, R, red, &sflag, &is_last);
+}
+
 }  // namespace b200p
