@@ -743,6 +743,38 @@ static int encode_field_map(CUtensorMap *tm, const double *base, int w, int h, i
     return encode_plane_map(tm, base, 8, w, h, planes, box_w, box_h);
 }
 
+// K4 / K5: fine rows of coarse rows [Ylo, Yhi) (strip mode passes a sub-range; the whole plane otherwise).  Whole planes
+// whose rows are 16-byte multiples in every array go through the TMA tile pipeline (kernels_rows_tma.cuh).
+template <bool SOLUTION>
+static int launch_prolongate(const double *coarse, const uint8_t *fmask, const double *frhs, int h, int w, int channels,
+                             int planes, const int *pred, double *u, int Ylo, int Yhi, cudaStream_t st) {
+    const int hc = (h + 1) >> 1, wc = (w + 1) >> 1;
+    static const int want_tma = getenv("B200P_PROLONG_TMA") ? atoi(getenv("B200P_PROLONG_TMA")) : 1;
+    if (want_tma && Ylo == 0 && Yhi >= hc && w % 16 == 0 && w >= RT_W && h >= 4 * RT_R && planes % channels == 0 &&
+        ((uintptr_t)fmask % 16) == 0 && ((uintptr_t)coarse % 16) == 0 && ((uintptr_t)u % 16) == 0) {
+        ProlongArgs A{h, w, channels, 32 * RT_R, pred, frhs, u};
+        CUtensorMap tc, tm, tu;
+        int rc = encode_plane_map(&tc, coarse, 8, wc, hc, planes, PT_CW, PT_CR);
+        if (!rc) rc = encode_plane_map(&tm, fmask, 1, w, h, planes / channels, RT_W, RT_R);
+        if (!rc) rc = SOLUTION ? 0 : encode_plane_map(&tu, u, 8, w, h, planes, RT_W, RT_R);
+        if (rc) return rc;
+        if (SOLUTION) tu = tc;
+        static bool attr = false;
+        if (!attr) {
+            CU(cudaFuncSetAttribute(prolongate_tma_kernel<SOLUTION>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)prolong_tma_smem(SOLUTION)));
+            attr = true;
+        }
+        dim3 g((w + RT_W - 1) / RT_W, (h + A.rows_per_cta - 1) / A.rows_per_cta, planes);
+        prolongate_tma_kernel<SOLUTION><<<g, PT_THREADS, prolong_tma_smem(SOLUTION), st>>>(A, tc, tm, tu);
+    } else {
+        prolongate_kernel<SOLUTION><<<grid2x(wc, min(Yhi, hc) - Ylo, planes), ST_THREADS, 0, st>>>(
+            coarse, fmask, frhs, h, w, channels, pred, u, Ylo, Yhi);
+    }
+    CU(cudaGetLastError());
+    return 0;
+}
+
 // K1: rs[p] = ||b - A u||^2, mflag[p].  UM/RM as in residual_px.
 static int launch_norm(b200p_plan *pl, const LevelHost &L, const double *u, const double *b,
                        bool um, bool rm, const int *pred, cudaStream_t st) {
@@ -1437,9 +1469,9 @@ static int enqueue_cascade(b200p_plan *pl, double *d_u0, cudaStream_t st) {
             // strip mode: the coarse level is replicated, so the strip and its halo rows are
             // prolongated locally (no exchange)
             const int Ylo = f.ext_lo >> 1, Yhi = (f.ext_hi + 1) >> 1;
-            prolongate_kernel<true><<<grid2x(c.info.width, Yhi - Ylo, pl->P), ST_THREADS, 0, st>>>(
-                coarse_u, f.d_mask, f.d_rhs, f.info.height, f.info.width, pl->C, nullptr, uf.cur, Ylo, Yhi);
-            CU(cudaGetLastError());
+            if ((rc = launch_prolongate<true>(coarse_u, f.d_mask, f.d_rhs, f.info.height, f.info.width, pl->C, pl->P, nullptr,
+                                              uf.cur, Ylo, Yhi, st)))
+                return rc;
         }
         if (l > 0) {
             rc = enqueue_smooth(pl, f, uf, f.d_rhs, true, 1, nullptr, nullptr, false, st);
@@ -1561,9 +1593,9 @@ static int enqueue_vcycle(b200p_plan *pl, int level, UBuf &u, const double *b, b
         LaunchScope sc(pl, st, KK_PROLONG_CORR, field_bytes(pl, L, 2.25, 1.0));
         // strip mode: e is replicated, the strip and its halo rows are corrected locally
         const int Ylo = L.ext_lo >> 1, Yhi = (L.ext_hi + 1) >> 1;
-        prolongate_kernel<false><<<grid2x(Cc.info.width, Yhi - Ylo, pl->P), ST_THREADS, 0, st>>>(
-            e.cur, L.d_mask, nullptr, L.info.height, L.info.width, pl->C, pred, u.cur, Ylo, Yhi);
-        CU(cudaGetLastError());
+        if ((rc = launch_prolongate<false>(e.cur, L.d_mask, nullptr, L.info.height, L.info.width, pl->C, pl->P, pred, u.cur,
+                                           Ylo, Yhi, st)))
+            return rc;
     }
     {
         NvtxScope nv("vcycle post-smooth", level);
@@ -1722,9 +1754,9 @@ static int cg_vcycle(b200p_plan *pl, int level, double *u, const double *b, bool
     if (rc) return rc;
     {
         LaunchScope sc(pl, st, KK_PROLONG_CORR, field_bytes(pl, L, 2.25, 1.0));
-        prolongate_kernel<false><<<grid2x(Cc.info.width, Cc.info.height, pl->P), ST_THREADS, 0, st>>>(
-            e, L.d_mask, nullptr, L.info.height, L.info.width, pl->C, pred, u);
-        CU(cudaGetLastError());
+        if ((rc = launch_prolongate<false>(e, L.d_mask, nullptr, L.info.height, L.info.width, pl->C, pl->P, pred, u, 0,
+                                           1 << 30, st)))
+            return rc;
     }
     return cg_smooth(pl, L, u, b, rm, cfg.nu_post, pred, uc, st);
 }
@@ -1776,9 +1808,9 @@ static int run_cg_pipeline(b200p_plan *pl, double *d_out, cudaStream_t st) {
         double *uf = l == 0 ? d_out : f.d_u;
         {
             LaunchScope sc(pl, st, KK_PROLONG_SOL, field_bytes(pl, f, 1.25, 1.0));
-            prolongate_kernel<true><<<grid2x(c.info.width, c.info.height, pl->P), ST_THREADS, 0, st>>>(
-                coarse_u, f.d_mask, f.d_rhs, f.info.height, f.info.width, pl->C, nullptr, uf);
-            CU(cudaGetLastError());
+            if ((rc = launch_prolongate<true>(coarse_u, f.d_mask, f.d_rhs, f.info.height, f.info.width, pl->C, pl->P, nullptr,
+                                              uf, 0, 1 << 30, st)))
+                return rc;
         }
         if (cfg.mode == 1) {
             // to_tol: denom = the level's flat-init defect (multigrid.py:413-417)
@@ -1938,9 +1970,9 @@ static int run_multilevel(b200p_plan *pl, double *d_out, cudaStream_t st) {
             double *home = uf.cur;
             {
                 LaunchScope sc(pl, st, KK_PROLONG_SOL, field_bytes(pl, f, 1.25, 1.0));
-                prolongate_kernel<true><<<grid2x(c.info.width, c.info.height, pl->P), ST_THREADS, 0, st>>>(
-                    coarse_u, f.d_mask, f.d_rhs, f.info.height, f.info.width, pl->C, nullptr, uf.cur);
-                CU(cudaGetLastError());
+                if ((rc = launch_prolongate<true>(coarse_u, f.d_mask, f.d_rhs, f.info.height, f.info.width, pl->C, pl->P,
+                                                  nullptr, uf.cur, 0, 1 << 30, st)))
+                    return rc;
             }
             if ((rc = smooth_level_to_tol(pl, f, uf, l == 0, st))) return rc;
             if ((rc = settle(pl, f, uf, home, st))) return rc;
@@ -3530,20 +3562,14 @@ int b200p_restrict_residual(const double *d_fine_r, const uint8_t *d_coarse_mask
 int b200p_prolongate_correct(const double *d_coarse_e, const uint8_t *d_fine_mask, int h, int w,
                              double *d_u, void *stream) {
     if (!d_coarse_e || !d_fine_mask || !d_u || h < 1 || w < 1) return fail_arg(B200P_ERR_ARG, "bad argument");
-    prolongate_kernel<false><<<grid2x((w + 1) / 2, (h + 1) / 2, 1), ST_THREADS, 0, (cudaStream_t)stream>>>(
-        d_coarse_e, d_fine_mask, nullptr, h, w, 1, nullptr, d_u);
-    CU(cudaGetLastError());
-    return 0;
+    return launch_prolongate<false>(d_coarse_e, d_fine_mask, nullptr, h, w, 1, 1, nullptr, d_u, 0, 1 << 30, (cudaStream_t)stream);
 }
 
 int b200p_prolongate_solution(const double *d_coarse_u, const uint8_t *d_fine_mask,
                               const double *d_fine_rhs, int h, int w, double *d_u, void *stream) {
     if (!d_coarse_u || !d_fine_mask || !d_fine_rhs || !d_u || h < 1 || w < 1)
         return fail_arg(B200P_ERR_ARG, "bad argument");
-    prolongate_kernel<true><<<grid2x((w + 1) / 2, (h + 1) / 2, 1), ST_THREADS, 0, (cudaStream_t)stream>>>(
-        d_coarse_u, d_fine_mask, d_fine_rhs, h, w, 1, nullptr, d_u);
-    CU(cudaGetLastError());
-    return 0;
+    return launch_prolongate<true>(d_coarse_u, d_fine_mask, d_fine_rhs, h, w, 1, 1, nullptr, d_u, 0, 1 << 30, (cudaStream_t)stream);
 }
 
 // ---- device-memory helpers -----------------------------------------------

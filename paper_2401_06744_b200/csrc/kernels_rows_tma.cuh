@@ -13,6 +13,7 @@
 // are reduced by the same deterministic last-CTA scheme (publish_partial).
 #pragma once
 #include "kernels_rows.cuh"
+#include "kernels_stencil.cuh"
 #include "tma_utils.cuh"
 
 namespace b200p {
@@ -260,6 +261,130 @@ residual_restrict_tma_kernel(const RestrictArgs A, const __grid_constant__ CUten
         if (leader && tile + RT_STAGES < ntiles) issue(tile + RT_STAGES);
     }
     publish_partial(acc, 0, p, R, red, &sflag, &is_last);
+}
+
+// ------------------------------------------------------------ K4 / K5 -----
+// Prolongation (multigrid.py:157-172, :364-366 / :398-400) on the tile pipeline.  A tile is RT_W x RT_R fine
+// pixels = 64 x 8 coarse cells; thread (t, g) owns one cell and writes its 2 x 2 fine pixels as two 16-byte
+// stores.  The stage holds the coarse box (cells Xs - 2 .. Xs + 65, rows Ys - 1 .. Ys + 8: the far neighbour of
+// every cell, zeros outside the grid, where the far index is clamped to the near one instead), the fine mask
+// tile and -- correction only -- the fine iterate tile.  The solution variant reads the right-hand side at mask
+// pixels only, straight from global memory, requested ONE TILE AHEAD (the mask of tile + 1 is already in its
+// stage), so no tile waits on that dependent load.  The arithmetic is prolong_pixel's, shared with the
+// generic kernel.
+constexpr int PT_CW = RT_W / 2 + 4;                    // coarse box columns
+constexpr int PT_CR = RT_R / 2 + 2;                    // coarse box rows
+constexpr int PT_C_BYTES = PT_CW * PT_CR * 8;          // 5440
+constexpr int PT_C_STRIDE = (PT_C_BYTES + 127) / 128 * 128;
+constexpr int PT_THREADS = (RT_W / 2) * (RT_R / 2);    // 512
+__host__ __device__ inline size_t prolong_tma_smem(bool solution) {
+    return (size_t)RT_STAGES * (PT_C_STRIDE + RT_M_BYTES + (solution ? 0 : RT_B_BYTES)) + 128;
+}
+struct ProlongArgs {
+    int h, w, channels, rows_per_cta;   // fine size; rows_per_cta a multiple of RT_R
+    const int *pred;
+    const double *frhs;                 // SOLUTION: fine right-hand side, read at mask pixels
+    double *u;
+};
+
+template <bool SOLUTION>
+__global__ void __launch_bounds__(PT_THREADS)
+prolongate_tma_kernel(const ProlongArgs A, const __grid_constant__ CUtensorMap tm_c,
+                      const __grid_constant__ CUtensorMap tm_m, const __grid_constant__ CUtensorMap tm_u) {
+    extern __shared__ __align__(128) unsigned char rt_smem[];
+    __shared__ __align__(8) unsigned long long full[RT_STAGES];
+    const int p = blockIdx.z;
+    if (A.pred && !A.pred[p]) return;
+    const int t = threadIdx.x & (RT_W / 2 - 1), g = threadIdx.x / (RT_W / 2);
+    const bool leader = threadIdx.x == 0;
+    unsigned char *sc = rt_smem, *smk = rt_smem + RT_STAGES * PT_C_STRIDE, *su = smk + RT_STAGES * RT_M_BYTES;
+    if (leader)
+        for (int s = 0; s < RT_STAGES; ++s) mbar_init(smem_u32(&full[s]), 1);
+    __syncthreads();
+    const int h = A.h, w = A.w;
+    const int hc = (h + 1) >> 1, wc = w >> 1;
+    const int xs = blockIdx.x * RT_W;
+    const int X = (xs >> 1) + t;
+    const bool live = X < wc;
+    const int y0 = blockIdx.y * A.rows_per_cta;
+    const int y1 = min(h, y0 + A.rows_per_cta);
+    const int ntiles = (y1 - y0 + RT_R - 1) / RT_R;
+    const int frame = p / A.channels;
+    const size_t fplane = (size_t)h * w;
+    double *up = A.u + (size_t)p * fplane;
+    const double *fr = SOLUTION ? A.frhs + (size_t)p * fplane : nullptr;
+    auto issue = [&](int tile) {
+        const int s = tile % RT_STAGES;
+        const unsigned bar = smem_u32(&full[s]);
+        mbar_expect_tx(bar, PT_C_BYTES + RT_M_BYTES + (SOLUTION ? 0 : RT_B_BYTES));
+        const int ty = y0 + tile * RT_R;
+        tma_load_3d(smem_u32(sc + s * PT_C_STRIDE), &tm_c, (xs >> 1) - 2, (ty >> 1) - 1, p, bar);
+        tma_load_3d(smem_u32(smk + s * RT_M_BYTES), &tm_m, xs, ty, frame, bar);
+        if (!SOLUTION) tma_load_3d(smem_u32(su + s * RT_B_BYTES), &tm_u, xs, ty, p, bar);
+    };
+    if (leader)
+        for (int tile = 0; tile < min(RT_STAGES, ntiles); ++tile) issue(tile);
+    // column offsets of the far neighbours in the coarse box (cell X sits at column t + 2): clamped at the borders
+    const int oL = X > 0 ? t + 1 : t + 2, oR = X < wc - 1 ? t + 3 : t + 2;
+    uchar2 m0n = make_uchar2(0, 0), m1n = make_uchar2(0, 0);
+    double2 f0n = make_double2(0.0, 0.0), f1n = make_double2(0.0, 0.0);
+    auto fetch_ahead = [&](int tile) {   // masks of `tile` from its stage; right-hand side at its mask pixels
+        const int s = tile % RT_STAGES;
+        mbar_wait(smem_u32(&full[s]), (tile / RT_STAGES) & 1);
+        const int ya = y0 + tile * RT_R + 2 * g;
+        m0n = m1n = make_uchar2(0, 0);
+        if (live && ya < y1) {
+            const unsigned char *M = smk + s * RT_M_BYTES + (2 * g) * RT_W + 2 * t;
+            m0n = *reinterpret_cast<const uchar2 *>(M);
+            if (ya + 1 < h) m1n = *reinterpret_cast<const uchar2 *>(M + RT_W);
+            if (SOLUTION) {
+                const size_t i0 = (size_t)ya * w + 2 * X;
+                if (m0n.x) f0n.x = fr[i0];
+                if (m0n.y) f0n.y = fr[i0 + 1];
+                if (m1n.x) f1n.x = fr[i0 + w];
+                if (m1n.y) f1n.y = fr[i0 + w + 1];
+            }
+        }
+    };
+    fetch_ahead(0);
+    for (int tile = 0; tile < ntiles; ++tile) {
+        const int s = tile % RT_STAGES;
+        const int ya = y0 + tile * RT_R + 2 * g;           // the cell's fine rows ya, ya + 1
+        const bool cell = live && ya < y1;
+        const uchar2 m0 = m0n, m1 = m1n;
+        double2 f0 = f0n, f1 = f1n;
+        if (tile + 1 < ntiles) fetch_ahead(tile + 1);      // waits for the next stage; this one landed before it
+        if (cell) {
+            const int Y = ya >> 1;
+            const bool two = ya + 1 < h;
+            const double *C = reinterpret_cast<const double *>(sc + s * PT_C_STRIDE);
+            const double *rowN = C + (g + 1) * PT_CW;                       // coarse row Y
+            const double *rowU = C + (Y > 0 ? g : g + 1) * PT_CW;          // Y - 1, clamped
+            const double *rowD = C + (Y < hc - 1 ? g + 2 : g + 1) * PT_CW; // Y + 1, clamped
+            const double nL = prolong_x(rowN[t + 2], rowN[oL]), nR = prolong_x(rowN[t + 2], rowN[oR]);
+            const double uL = prolong_x(rowU[t + 2], rowU[oL]), uR = prolong_x(rowU[t + 2], rowU[oR]);
+            const double v00 = prolong_x(nL, uL), v01 = prolong_x(nR, uR);
+            if (!SOLUTION) {
+                const double *U = reinterpret_cast<const double *>(su + s * RT_B_BYTES) + (2 * g) * RT_W + 2 * t;
+                f0 = *reinterpret_cast<const double2 *>(U);
+                if (two) f1 = *reinterpret_cast<const double2 *>(U + RT_W);
+            }
+            const size_t i0 = (size_t)ya * w + 2 * X;
+            double2 o;
+            o.x = SOLUTION ? (m0.x ? f0.x : v00) : (m0.x ? f0.x : f0.x + v00);
+            o.y = SOLUTION ? (m0.y ? f0.y : v01) : (m0.y ? f0.y : f0.y + v01);
+            *reinterpret_cast<double2 *>(up + i0) = o;
+            if (two) {
+                const double dL = prolong_x(rowD[t + 2], rowD[oL]), dR = prolong_x(rowD[t + 2], rowD[oR]);
+                const double v10 = prolong_x(nL, dL), v11 = prolong_x(nR, dR);
+                o.x = SOLUTION ? (m1.x ? f1.x : v10) : (m1.x ? f1.x : f1.x + v10);
+                o.y = SOLUTION ? (m1.y ? f1.y : v11) : (m1.y ? f1.y : f1.y + v11);
+                *reinterpret_cast<double2 *>(up + i0 + w) = o;
+            }
+        }
+        __syncthreads();   // every thread is done with stage s
+        if (leader && tile + RT_STAGES < ntiles) issue(tile + RT_STAGES);
+    }
 }
 
 }  // namespace b200p

@@ -367,6 +367,9 @@ restrict_field_kernel(const double *__restrict__ r, const uint8_t *__restrict__ 
 // far index clamped at the borders (multigrid.py:157-172).
 // SOLUTION = false:  u += P e, 0 at fine mask pixels  (prolongate_correction)
 // SOLUTION = true :  u  = P c, rhs at fine mask pixels (prolongate_solution)
+// 0.75 near + 0.25 far, written once so that every prolongation kernel rounds alike (0.25 far is exact).
+__device__ __forceinline__ double prolong_x(double nearv, double farv) { return __fma_rn(0.75, nearv, 0.25 * farv); }
+
 template <bool SOLUTION>
 __global__ void __launch_bounds__(ST_THREADS)
 prolongate_kernel(const double *__restrict__ c, const uint8_t *__restrict__ fmask,
@@ -390,8 +393,8 @@ prolongate_kernel(const double *__restrict__ c, const uint8_t *__restrict__ fmas
     for (int k = 0; k < 3; ++k) {
         const double *row = cp + (size_t)ys[k] * wc;
         const double mid = row[X];
-        rowL[k] = 0.75 * mid + 0.25 * row[Xm];  // fine x even: far = near - 1
-        rowR[k] = 0.75 * mid + 0.25 * row[Xp];  // fine x odd : far = near + 1
+        rowL[k] = prolong_x(mid, row[Xm]);  // fine x even: far = near - 1
+        rowR[k] = prolong_x(mid, row[Xp]);  // fine x odd : far = near + 1
     }
     const int y0 = 2 * Y, x0 = 2 * X;
     if ((w & 1) == 0 && ((uintptr_t)up & 15) == 0 && ((uintptr_t)fm & 1) == 0) {
@@ -403,8 +406,8 @@ prolongate_kernel(const double *__restrict__ c, const uint8_t *__restrict__ fmas
             const int kf = dy ? 2 : 0;
             const size_t i = (size_t)y * w + x0;
             const uchar2 m = *reinterpret_cast<const uchar2 *>(fm + i);
-            const double v0 = 0.75 * rowL[1] + 0.25 * rowL[kf];
-            const double v1 = 0.75 * rowR[1] + 0.25 * rowR[kf];
+            const double v0 = prolong_x(rowL[1], rowL[kf]);
+            const double v1 = prolong_x(rowR[1], rowR[kf]);
             double2 *dst = reinterpret_cast<double2 *>(up + i);
             if (SOLUTION) {
                 const double *fr = frhs + (size_t)p * fplane + i;
@@ -432,7 +435,7 @@ prolongate_kernel(const double *__restrict__ c, const uint8_t *__restrict__ fmas
             if (x >= w) break;
             const double nearv = dx ? rowR[1] : rowL[1];
             const double farv = dx ? rowR[kf] : rowL[kf];
-            const double val = 0.75 * nearv + 0.25 * farv;
+            const double val = prolong_x(nearv, farv);
             const size_t i = (size_t)y * w + x;
             const bool m = fm[i] != 0;
             if (SOLUTION) {
@@ -471,7 +474,7 @@ downsample_mask_kernel(const uint8_t *__restrict__ fine, int h, int w, uint8_t *
 // elsewhere; hierarchy values are 0 there).
 // One thread per coarse pixel of a FRAME: the neighbour-suppression weights depend on the masks
 // only, so they are formed once and applied to all channels of the frame (grid z = frame).
-__global__ void __launch_bounds__(ST_THREADS)
+__global__ void __launch_bounds__(ST_THREADS, 4)
 downsample_values_kernel(const uint8_t *__restrict__ fmask, const uint8_t *__restrict__ cmask,
                          const double *__restrict__ frhs, int h, int w, int channels, int modified,
                          double *__restrict__ crhs) {
@@ -505,51 +508,66 @@ downsample_values_kernel(const uint8_t *__restrict__ fmask, const uint8_t *__res
         }
     }
     const bool known = cmk != 0;
-    if (known) {
-#pragma unroll
-        for (int dy = 0; dy < 2; ++dy)
-#pragma unroll
-            for (int dx = 0; dx < 2; ++dx) {
-                const int y = 2 * Y + dy, x = 2 * X + dx;
-                if (y >= h || x >= w) continue;
-                if (!fmk[dy * 2 + dx]) continue;
-                double n = 0.0;
-                // in-cell neighbours: the cell's own fine mask; the others: the adjacent cell's coarse mask
-                if (x >= 1) n += dx ? (double)fmk[dy * 2] : (double)(cm[(size_t)Y * wc + (X - 1)] != 0);
-                if (x <= w - 2) n += !dx ? (double)fmk[dy * 2 + 1] : (double)(cm[(size_t)Y * wc + (X + 1)] != 0);
-                if (y >= 1) n += dy ? (double)fmk[dx] : (double)(cm[(size_t)(Y - 1) * wc + X] != 0);
-                if (y <= h - 2) n += !dy ? (double)fmk[2 + dx] : (double)(cm[(size_t)(Y + 1) * wc + X] != 0);
-                const int k = dy * 2 + dx;
-                wg[k] = 4.0 - n;
-                c1[k] = 1.0;
-                has[k] = true;
-            }
+    if (!known) {   // 0 off the coarse mask: nothing else to read
+        for (int c = 0; c < channels; ++c) crhs[((size_t)f * channels + c) * cplane + ci] = 0.0;
+        return;
     }
-    const double nden = (c1[0] + c1[1]) + (c1[2] + c1[3]);
-    const double den = (wg[0] + wg[1]) + (wg[2] + wg[3]);
-    for (int c = 0; c < channels; ++c) {
-        const size_t p = (size_t)f * channels + c;
-        double out = 0.0;
-        if (known) {
-            const double *fr = frhs + p * fplane;
-            double nv[4] = {0, 0, 0, 0}, wv[4] = {0, 0, 0, 0};
+    // All remaining requests go out together -- the four adjacent cells' coarse masks and the fine values at the
+    // cell's mask pixels, for every channel -- and are consumed afterwards: one memory latency behind the masks
+    // instead of one per step of the chain neighbours -> weights -> channel 0 -> channel 1 -> ...
+    const bool inL = X > 0, inR = 2 * X + 2 <= w - 1, inT = Y > 0, inB = 2 * Y + 2 <= h - 1;
+    const uint8_t nL = inL ? cm[ci - 1] : 0, nR = inR ? cm[ci + 1] : 0;
+    const uint8_t nT = inT ? cm[ci - wc] : 0, nB = inB ? cm[ci + wc] : 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) has[k] = fmk[k];   // fmk is false outside the image
+    constexpr int CB = 3;      // channels per batch of requests
+    for (int c0 = 0; c0 < channels; c0 += CB) {
+        double val[CB][4];
+#pragma unroll
+        for (int cc = 0; cc < CB; ++cc) {
+            const double *fr = frhs + ((size_t)f * channels + min(c0 + cc, channels - 1)) * fplane;
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                if (has[k]) {
-                    const double val = fr[(size_t)(2 * Y + (k >> 1)) * w + 2 * X + (k & 1)];
-                    nv[k] = val;
-                    wv[k] = wg[k] * val;
+                val[cc][k] = (has[k] && c0 + cc < channels) ? fr[(size_t)(2 * Y + (k >> 1)) * w + 2 * X + (k & 1)] : 0.0;
+        }
+        if (c0 == 0) {
+#pragma unroll
+            for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+                for (int dx = 0; dx < 2; ++dx) {
+                    const int k = dy * 2 + dx;
+                    if (!has[k]) continue;
+                    const int y = 2 * Y + dy, x = 2 * X + dx;
+                    double n = 0.0;
+                    // in-cell neighbours: the cell's own fine mask; the others: the adjacent cell's coarse mask
+                    if (x >= 1) n += dx ? (double)fmk[dy * 2] : (double)(nL != 0);
+                    if (x <= w - 2) n += !dx ? (double)fmk[dy * 2 + 1] : (double)(nR != 0);
+                    if (y >= 1) n += dy ? (double)fmk[dx] : (double)(nT != 0);
+                    if (y <= h - 2) n += !dy ? (double)fmk[2 + dx] : (double)(nB != 0);
+                    wg[k] = 4.0 - n;
+                    c1[k] = 1.0;
                 }
+        }
+        const double nden = (c1[0] + c1[1]) + (c1[2] + c1[3]);
+        const double den = (wg[0] + wg[1]) + (wg[2] + wg[3]);
+#pragma unroll
+        for (int cc = 0; cc < CB; ++cc) {
+            if (c0 + cc >= channels) break;
+            double nv[4], wv[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                nv[k] = has[k] ? val[cc][k] : 0.0;
+                wv[k] = has[k] ? wg[k] * val[cc][k] : 0.0;
+            }
             const double nnum = (nv[0] + nv[1]) + (nv[2] + nv[3]);
             const double naive = nnum / fmax(1.0, nden);
+            double out = naive;
             if (modified) {
                 const double num = (wv[0] + wv[1]) + (wv[2] + wv[3]);
                 out = den == 0.0 ? naive : num / fmax(1.0, den);
-            } else {
-                out = naive;
             }
+            crhs[((size_t)f * channels + c0 + cc) * cplane + ci] = out;
         }
-        crhs[p * cplane + ci] = out;
     }
 }
 

@@ -112,6 +112,19 @@ def test_prolongation(rng, shape):
         bp.prolongate_correction(np.zeros((cs[0] + 1, cs[1])), fm)
 
 
+@pytest.mark.parametrize("shape", [(64, 128), (135, 240), (560, 384), (513, 144), (1030, 256)])
+@pytest.mark.parametrize("density", [0.02, 0.6])
+def test_prolongation_tile_pipeline(rng, shape, density):
+    """Shapes the TMA tile pipeline takes (w % 16 == 0, w >= 128, h >= 64): ragged last tile, odd heights (a
+    one-row last cell), more rows than one CTA's 512, a strip narrower than the last tile column."""
+    cs = ((shape[0] + 1) // 2, (shape[1] + 1) // 2)
+    c = rng.normal(size=cs) * 50
+    fm = _mask(rng, shape, density)
+    rhs = rng.normal(size=shape)
+    np.testing.assert_allclose(bp.prolongate_correction(c, fm), oracle.prolongate_correction(c, fm), rtol=0, atol=1e-12)
+    np.testing.assert_allclose(bp.prolongate_solution(c, fm, rhs), oracle.prolongate_solution(c, fm, rhs), rtol=0, atol=1e-12)
+
+
 def test_prolongation_1d_weights():
     """(3a+b)/4 interior, border clamp (tests/test_multigrid.py:161-167 of the reference)."""
     c = np.array([[4.0, 8.0, 16.0]])
