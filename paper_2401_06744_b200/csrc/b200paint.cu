@@ -765,7 +765,7 @@ static int launch_prolongate(const double *coarse, const uint8_t *fmask, const d
                                     (int)prolong_tma_smem(SOLUTION)));
             attr = true;
         }
-        dim3 g((w + RT_W - 1) / RT_W, (h + A.rows_per_cta - 1) / A.rows_per_cta, planes);
+        dim3 g((w + RT_W - 1) / RT_W * channels, (h + A.rows_per_cta - 1) / A.rows_per_cta, planes / channels);
         prolongate_tma_kernel<SOLUTION><<<g, PT_THREADS, prolong_tma_smem(SOLUTION), st>>>(A, tc, tm, tu);
     } else {
         prolongate_kernel<SOLUTION><<<grid2x(wc, min(Yhi, hc) - Ylo, planes), ST_THREADS, 0, st>>>(
@@ -808,7 +808,7 @@ static int launch_norm(b200p_plan *pl, const LevelHost &L, const double *u, cons
             CU(cudaFuncSetAttribute(residual_sqnorm_tma_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_tma_smem(true)));
             attr = true;
         }
-        dim3 g((L.info.width + RT_W - 1) / RT_W, (R.y_hi - R.y_lo + R.rows_per_cta - 1) / R.rows_per_cta, pl->P);
+        dim3 g((L.info.width + RT_W - 1) / RT_W * pl->C, (R.y_hi - R.y_lo + R.rows_per_cta - 1) / R.rows_per_cta, pl->F);
         if (rm && !with_b) residual_sqnorm_tma_kernel<true, false><<<g, RT_THREADS, rows_tma_smem(false), st>>>(R, tu, tm, tb);
         else if (rm) residual_sqnorm_tma_kernel<true, true><<<g, RT_THREADS, rows_tma_smem(true), st>>>(R, tu, tm, tb);
         else residual_sqnorm_tma_kernel<false, true><<<g, RT_THREADS, rows_tma_smem(true), st>>>(R, tu, tm, tb);
@@ -1545,7 +1545,7 @@ static int enqueue_vcycle(b200p_plan *pl, int level, UBuf &u, const double *b, b
                     CU(cudaFuncSetAttribute(residual_restrict_tma_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rows_tma_smem(true)));
                     attr = true;
                 }
-                dim3 gt((L.info.width + RT_W - 1) / RT_W, (RA.R.y_hi - RA.R.y_lo + RA.R.rows_per_cta - 1) / RA.R.rows_per_cta, pl->P);
+                dim3 gt((L.info.width + RT_W - 1) / RT_W * pl->C, (RA.R.y_hi - RA.R.y_lo + RA.R.rows_per_cta - 1) / RA.R.rows_per_cta, pl->F);
                 if (rm && !with_b) residual_restrict_tma_kernel<true, false><<<gt, RK_THREADS, rows_tma_smem(false), st>>>(RA, tu, tm, tb);
                 else if (rm) residual_restrict_tma_kernel<true, true><<<gt, RK_THREADS, rows_tma_smem(true), st>>>(RA, tu, tm, tb);
                 else residual_restrict_tma_kernel<false, true><<<gt, RK_THREADS, rows_tma_smem(true), st>>>(RA, tu, tm, tb);

@@ -48,13 +48,12 @@ struct RowsArgs {
 
 // Deterministic two-stage reduction: every CTA stores its partial, the last one to
 // arrive (per problem) adds all partials in index order and publishes the total.
-__device__ __forceinline__ void publish_partial(double acc, int flag, int p, const RowsArgs &A,
-                                                double *red, int *sflag, bool *is_last) {
+// (nparts, me): the problem's CTA count and this CTA's index among them (the order the partials are added in).
+__device__ __forceinline__ void publish_partial_at(double acc, int flag, int p, unsigned nparts, unsigned me,
+                                                   const RowsArgs &A, double *red, int *sflag, bool *is_last) {
     const int T = blockDim.x;
     if (flag) *sflag = 1;
     const double tot = cta_sum(acc, red);
-    const unsigned nparts = gridDim.x * gridDim.y;
-    const unsigned me = blockIdx.y * gridDim.x + blockIdx.x;
     if (threadIdx.x == 0) {
         A.partial[(size_t)p * nparts + me] = tot;
         A.partial_flag[(size_t)p * nparts + me] = *sflag;
@@ -79,6 +78,11 @@ __device__ __forceinline__ void publish_partial(double acc, int flag, int p, con
             A.counter[p] = 0;
         }
     }
+}
+
+__device__ __forceinline__ void publish_partial(double acc, int flag, int p, const RowsArgs &A,
+                                                double *red, int *sflag, bool *is_last) {
+    publish_partial_at(acc, flag, p, gridDim.x * gridDim.y, blockIdx.y * gridDim.x + blockIdx.x, A, red, sflag, is_last);
 }
 
 struct Row4 {

@@ -28,6 +28,19 @@ constexpr int RT_U_BYTES = (RT_R + 2) * RT_BOXW * 8;            // 19008
 constexpr int RT_U_STRIDE = (RT_U_BYTES + 127) / 128 * 128;     // 19072: stages stay 128-byte aligned
 constexpr int RT_M_BYTES = RT_R * RT_W;                         // 2048
 constexpr int RT_B_BYTES = RT_R * RT_W * 8;                     // 16384
+// Grid of the tile pipelines: x = strip * channels + channel, y = row chunk, z = frame.  The channels of a frame
+// read the same mask tiles; launched side by side they find them in L2 (one DRAM read per frame, not per plane).
+struct TileCoord {
+    int p, frame, strip, nstrips;
+};
+__device__ __forceinline__ TileCoord tile_coord(int channels) {
+    TileCoord c;
+    c.frame = blockIdx.z;
+    c.strip = blockIdx.x / channels;
+    c.nstrips = gridDim.x / channels;
+    c.p = c.frame * channels + (blockIdx.x - c.strip * channels);
+    return c;
+}
 __host__ __device__ inline size_t rows_tma_smem(bool with_b) {
     return (size_t)RT_STAGES * (RT_U_STRIDE + RT_M_BYTES + (with_b ? RT_B_BYTES : 0)) + 128;
 }
@@ -43,7 +56,8 @@ residual_sqnorm_tma_kernel(const RowsArgs A, const __grid_constant__ CUtensorMap
     __shared__ int sflag;
     __shared__ bool is_last;
     __shared__ __align__(8) unsigned long long full[RT_STAGES];
-    const int p = blockIdx.z;
+    const TileCoord tc = tile_coord(A.channels);
+    const int p = tc.p;
     if (A.pred && !A.pred[p]) return;
     const int t = threadIdx.x & (RT_W - 1), g = threadIdx.x / RT_W;
     const bool leader = threadIdx.x == 0;
@@ -55,13 +69,13 @@ residual_sqnorm_tma_kernel(const RowsArgs A, const __grid_constant__ CUtensorMap
     }
     __syncthreads();
     const int h = A.h, w = A.w;
-    const int xs = blockIdx.x * RT_W;
+    const int xs = tc.strip * RT_W;
     const int x = xs + t;
     const bool live = x < w;
     const int y0 = A.y_lo + blockIdx.y * A.rows_per_cta;
     const int y1 = min(A.y_hi, y0 + A.rows_per_cta);
     const int ntiles = (y1 - y0 + RT_R - 1) / RT_R;
-    const int frame = p / A.channels;
+    const int frame = tc.frame;
     auto issue = [&](int tile) {
         const int s = tile % RT_STAGES;
         const unsigned bar = smem_u32(&full[s]);
@@ -133,7 +147,7 @@ residual_sqnorm_tma_kernel(const RowsArgs A, const __grid_constant__ CUtensorMap
         acc = 0.0;
         flag = 0;
     }
-    publish_partial(acc, flag, p, A, red, &sflag, &is_last);
+    publish_partial_at(acc, flag, p, tc.nstrips * gridDim.y, blockIdx.y * tc.nstrips + tc.strip, A, red, &sflag, &is_last);
 }
 
 // ---------------------------------------------------------------- K3 ------
@@ -156,7 +170,8 @@ residual_restrict_tma_kernel(const RestrictArgs A, const __grid_constant__ CUten
     __shared__ bool is_last;
     __shared__ __align__(8) unsigned long long full[RT_STAGES];
     const RowsArgs &R = A.R;
-    const int p = blockIdx.z;
+    const TileCoord tc = tile_coord(R.channels);
+    const int p = tc.p;
     if (R.pred && !R.pred[p]) return;
     const int t = threadIdx.x & (RT_W / 2 - 1), g = threadIdx.x / (RT_W / 2);
     const bool leader = threadIdx.x == 0;
@@ -168,13 +183,13 @@ residual_restrict_tma_kernel(const RestrictArgs A, const __grid_constant__ CUten
     __syncthreads();
     const int h = R.h, w = R.w;
     const int hc = (h + 1) >> 1, wc = w >> 1;
-    const int xs = blockIdx.x * RT_W;
+    const int xs = tc.strip * RT_W;
     const int x = xs + 2 * t;                 // the thread's two fine columns x, x + 1
     const bool live = x < w;
     const int y0 = R.y_lo + blockIdx.y * R.rows_per_cta;   // even
     const int y1 = min(R.y_hi, y0 + R.rows_per_cta);
     const int ntiles = (y1 - y0 + RT_R - 1) / RT_R;
-    const int frame = p / R.channels;
+    const int frame = tc.frame;
     const size_t cplane = (size_t)hc * wc;
     const uint8_t *cm = A.cmask + (size_t)frame * cplane;
     double *rc = A.rc + (size_t)p * cplane;
@@ -260,7 +275,7 @@ residual_restrict_tma_kernel(const RestrictArgs A, const __grid_constant__ CUten
         __syncthreads();   // every thread is done with stage s
         if (leader && tile + RT_STAGES < ntiles) issue(tile + RT_STAGES);
     }
-    publish_partial(acc, 0, p, R, red, &sflag, &is_last);
+    publish_partial_at(acc, 0, p, tc.nstrips * gridDim.y, blockIdx.y * tc.nstrips + tc.strip, R, red, &sflag, &is_last);
 }
 
 // ------------------------------------------------------------ K4 / K5 -----
@@ -293,7 +308,8 @@ prolongate_tma_kernel(const ProlongArgs A, const __grid_constant__ CUtensorMap t
                       const __grid_constant__ CUtensorMap tm_m, const __grid_constant__ CUtensorMap tm_u) {
     extern __shared__ __align__(128) unsigned char rt_smem[];
     __shared__ __align__(8) unsigned long long full[RT_STAGES];
-    const int p = blockIdx.z;
+    const TileCoord tc = tile_coord(A.channels);
+    const int p = tc.p;
     if (A.pred && !A.pred[p]) return;
     const int t = threadIdx.x & (RT_W / 2 - 1), g = threadIdx.x / (RT_W / 2);
     const bool leader = threadIdx.x == 0;
@@ -303,13 +319,13 @@ prolongate_tma_kernel(const ProlongArgs A, const __grid_constant__ CUtensorMap t
     __syncthreads();
     const int h = A.h, w = A.w;
     const int hc = (h + 1) >> 1, wc = w >> 1;
-    const int xs = blockIdx.x * RT_W;
+    const int xs = tc.strip * RT_W;
     const int X = (xs >> 1) + t;
     const bool live = X < wc;
     const int y0 = blockIdx.y * A.rows_per_cta;
     const int y1 = min(h, y0 + A.rows_per_cta);
     const int ntiles = (y1 - y0 + RT_R - 1) / RT_R;
-    const int frame = p / A.channels;
+    const int frame = tc.frame;
     const size_t fplane = (size_t)h * w;
     double *up = A.u + (size_t)p * fplane;
     const double *fr = SOLUTION ? A.frhs + (size_t)p * fplane : nullptr;
