@@ -233,11 +233,16 @@ int b200p_solve_host(b200p_plan *plan, const uint8_t *h_mask, const double *h_kn
  * or B200P_DENSE_INGEST=1 in the environment, copy the planes unchanged.  Results are identical.
  * b200p_plan_last_transfer_bytes reports what the last host entry point copied each way. */
 int b200p_plan_last_transfer_bytes(const b200p_plan *plan, int64_t *h2d_bytes, int64_t *d2h_bytes);
-/* mode 0 (default): sparse ingest when the mask is sparse -- lowest latency of a single solve
- * (4K RGB 2 %: 9.6 ms vs 12.4 ms host to host); mode 1: always copy the planes with the copy
- * engine -- what a multi-lane pipeline wants, because DMA overlaps the other lanes' kernels and
- * costs no SM time while zero-copy reads queue behind the lanes' D2H traffic (measured: 223 vs
- * 156 frames/s on 5 lanes). */
+/* fp64 ingest of the host entry points (results are identical in every mode):
+ * mode 0 (default): sparse when the mask is sparse -- from a pinned source the device fetches the values at
+ *   mask pixels itself (zero copy; lowest latency of a single solve: 4K RGB 2 %, 9.6 ms vs 12.4 ms host to
+ *   host), from a pageable source the library's host threads compact them (mode 2);
+ * mode 1: always copy the planes with the copy engine (costs no SM time, overlaps the other lanes' kernels);
+ * mode 2: the library's host threads (B200P_HOST_THREADS, default min(8, cores)) compact a (pixel index,
+ *   C values) list into pinned staging whatever the source, and a scatter kernel rebuilds the plane: 12 MB
+ *   instead of 207 MB per 4K RGB frame on the link and no device reads of host memory -- what a multi-lane
+ *   pipeline wants (measured on 5 lanes: 257 frames/s against 230 for mode 1 and 192 for the zero copy of
+ *   mode 0, whose reads queue behind the lanes' D2H traffic). */
 int b200p_plan_set_ingest(b200p_plan *plan, int mode);
 
 /* 8-bit ingest/egress variant (fileio.image_from_fields, fileio.py:58-65):

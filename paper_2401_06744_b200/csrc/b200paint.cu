@@ -14,6 +14,11 @@
 #include <nccl.h>   // types only: the library is loaded with dlopen when a strip plan asks for it
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -298,7 +303,7 @@ struct b200p_plan {
     double *h_sp_val = nullptr, *d_sp_val = nullptr;
     size_t sp_cap = 0;
     int64_t last_h2d = 0, last_d2h = 0;  // bytes the last host entry point copied each way
-    int ingest_mode = 0;                  // 0 auto (sparse when the mask is), 1 always the dense plane copy
+    int ingest_mode = 0;                  // 0 auto (sparse when the mask is), 1 always the dense plane copy, 2 sparse by host gather
     bool last_h2d_counted = false;        // ... H2D side = mask planes + *h_cnt values (counted on the device)
     unsigned long long *h_cnt = nullptr, *d_cnt = nullptr;
     void *h_pin = nullptr;  // pinned bounce buffer
@@ -3011,6 +3016,60 @@ static size_t list_nonzero(const uint8_t *m, size_t n, uint32_t *idx) {
     return cnt;
 }
 
+// A small process-wide pool for the host-side gather of the sparse ingest (the only host loop of the library that
+// touches whole planes).  B200P_HOST_THREADS workers (default min(8, cores)); the caller works too.  Never destroyed:
+// its threads sleep on a condition variable between calls.
+class HostPool {
+    std::mutex m, callers;
+    std::condition_variable cv, done_cv;
+    const std::function<void(int)> *job = nullptr;
+    int ntasks = 0, pending = 0, workers = 0;
+    std::atomic<int> next{0};
+    uint64_t gen = 0;
+    void loop() {
+        uint64_t seen = 0;
+        std::unique_lock<std::mutex> lk(m);
+        for (;;) {
+            cv.wait(lk, [&] { return gen != seen; });
+            seen = gen;
+            const std::function<void(int)> *f = job;
+            const int n = ntasks;
+            lk.unlock();
+            for (int t; (t = next.fetch_add(1)) < n;) (*f)(t);
+            lk.lock();
+            if (--pending == 0) done_cv.notify_one();
+        }
+    }
+public:
+    explicit HostPool(int n) : workers(n) {
+        for (int i = 0; i < n; ++i) std::thread([this] { loop(); }).detach();
+    }
+    int width() const { return workers + 1; }
+    void run(int n, const std::function<void(int)> &f) {
+        std::lock_guard<std::mutex> one(callers);
+        {
+            std::lock_guard<std::mutex> lk(m);
+            job = &f;
+            ntasks = n;
+            next = 0;
+            pending = workers;
+            ++gen;
+        }
+        cv.notify_all();
+        for (int t; (t = next.fetch_add(1)) < n;) f(t);
+        std::unique_lock<std::mutex> lk(m);
+        done_cv.wait(lk, [&] { return pending == 0; });
+    }
+};
+static HostPool &host_pool() {
+    static HostPool *pool = [] {
+        const char *e = getenv("B200P_HOST_THREADS");
+        int n = e ? atoi(e) : (int)std::min(8u, std::max(1u, std::thread::hardware_concurrency()));
+        return new HostPool(std::max(0, n - 1));
+    }();
+    return *pool;
+}
+
 static int ensure_sparse_staging(b200p_plan *pl, size_t entries) {
     if (entries <= pl->sp_cap) return 0;
     const size_t cap = entries + entries / 4 + 1024;
@@ -3057,7 +3116,7 @@ int b200p_solve_host_async(b200p_plan *pl, const uint8_t *h_mask, const double *
     pl->last_h2d_counted = false;
     // pinned source: the device fetches the mask pixels' values itself (no host pass over `known`)
     const double *mapped = nullptr;
-    if (!force_dense) {
+    if (!force_dense && pl->ingest_mode != 2) {
         cudaPointerAttributes at;
         if (cudaPointerGetAttributes(&at, h_known) == cudaSuccess && at.type == cudaMemoryTypeHost &&
             at.devicePointer)
@@ -3094,37 +3153,55 @@ int b200p_solve_host_async(b200p_plan *pl, const uint8_t *h_mask, const double *
             pl->last_h2d_counted = true;  // F*plane + count*C*8, known once the stream has run
             done = true;
         }
-    } else if (!force_dense && plane < (1ull << 32)) {
-        // pageable source: gather on this thread into pinned staging
-        std::vector<size_t> cnt(pl->F);
-        size_t total = 0;
-        for (int f = 0; f < pl->F; ++f) total += cnt[f] = count_nonzero(h_mask + (size_t)f * plane, plane);
+    }
+    if (!done && !force_dense && plane < (1ull << 32)) {
+        // pageable source (or B200P ingest mode 2): the host gathers a (pixel index, C values) list into pinned
+        // staging -- every frame cut into row chunks that the host pool counts, then lists and gathers in place
+        const int h = pl->cfg.height, w = pl->cfg.width;
+        const int chunks = std::max(1, std::min(h, 4 * host_pool().width() / std::max(1, std::min(pl->F, 4))));
+        const int ntask = pl->F * chunks;
+        std::vector<size_t> cnt(ntask + 1, 0);
+        auto rows_of = [&](int t, size_t &lo, size_t &n) {
+            const int c = t % chunks;
+            const size_t r0 = (size_t)h * c / chunks, r1 = (size_t)h * (c + 1) / chunks;
+            lo = r0 * w;
+            n = (r1 - r0) * w;
+        };
+        const std::function<void(int)> count = [&](int t) {
+            size_t lo, n;
+            rows_of(t, lo, n);
+            cnt[t + 1] = count_nonzero(h_mask + (size_t)(t / chunks) * plane + lo, n);
+        };
+        host_pool().run(ntask, count);
+        for (int t = 0; t < ntask; ++t) cnt[t + 1] += cnt[t];   // offsets
+        const size_t total = cnt[ntask];
         const size_t sparse_bytes = total * (sizeof(uint32_t) + C * sizeof(double));
         if (sparse_bytes * 2 <= dense_bytes) {
             if ((rc = ensure_sparse_staging(pl, total))) return rc;
             CU(cudaMemsetAsync(pl->d_in_known, 0, dense_bytes, st));
-            size_t off = 0;
-            for (int f = 0; f < pl->F; ++f) {
-                uint32_t *idx = pl->h_sp_idx + off;
-                double *val = pl->h_sp_val + off * C;
-                list_nonzero(h_mask + (size_t)f * plane, plane, idx);
+            const std::function<void(int)> gather = [&](int t) {
+                size_t lo, n;
+                rows_of(t, lo, n);
+                const int f = t / chunks;
+                uint32_t *idx = pl->h_sp_idx + cnt[t];
+                double *val = pl->h_sp_val + cnt[t] * C;
+                const size_t k_n = list_nonzero(h_mask + (size_t)f * plane + lo, n, idx);
+                for (size_t k = 0; k < k_n; ++k) idx[k] += (uint32_t)lo;
                 for (int c = 0; c < C; ++c) {
                     const double *src = h_known + ((size_t)f * C + c) * plane;
-                    for (size_t k = 0; k < cnt[f]; ++k) val[k * C + c] = src[idx[k]];
+                    for (size_t k = 0; k < k_n; ++k) val[k * C + c] = src[idx[k]];
                 }
-                // one frame's list travels while the next one is gathered
-                CU(cudaMemcpyAsync(pl->d_sp_idx + off, idx, cnt[f] * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-                CU(cudaMemcpyAsync(pl->d_sp_val + off * C, val, cnt[f] * C * sizeof(double),
-                                   cudaMemcpyHostToDevice, st));
-                {
-                    const size_t n = cnt[f] * C;
-                    LaunchScope sc(pl, st, KK_CONVERT, 20.0 * n);
-                    scatter_known_kernel<<<(unsigned)((n + ST_THREADS - 1) / ST_THREADS), ST_THREADS, 0, st>>>(
-                        pl->d_sp_idx + off, pl->d_sp_val + off * C, n, C, plane,
-                        pl->d_in_known + (size_t)f * C * plane);
-                    CU(cudaGetLastError());
-                }
-                off += cnt[f];
+            };
+            host_pool().run(ntask, gather);
+            CU(cudaMemcpyAsync(pl->d_sp_idx, pl->h_sp_idx, total * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+            CU(cudaMemcpyAsync(pl->d_sp_val, pl->h_sp_val, total * C * sizeof(double), cudaMemcpyHostToDevice, st));
+            for (int f = 0; f < pl->F; ++f) {
+                const size_t off = cnt[f * chunks], n = (cnt[(f + 1) * chunks] - off) * C;
+                if (!n) continue;
+                LaunchScope sc(pl, st, KK_CONVERT, 20.0 * n);
+                scatter_known_kernel<<<(unsigned)((n + ST_THREADS - 1) / ST_THREADS), ST_THREADS, 0, st>>>(
+                    pl->d_sp_idx + off, pl->d_sp_val + off * C, n, C, plane, pl->d_in_known + (size_t)f * C * plane);
+                CU(cudaGetLastError());
             }
             pl->last_h2d = (int64_t)(pl->F * plane + sparse_bytes);
             done = true;
@@ -3139,7 +3216,8 @@ int b200p_solve_host_async(b200p_plan *pl, const uint8_t *h_mask, const double *
 
 int b200p_plan_set_ingest(b200p_plan *pl, int mode) {
     if (!pl) return fail_arg(B200P_ERR_ARG, "null plan");
-    if (mode != 0 && mode != 1) return fail_arg(B200P_ERR_ARG, "ingest mode must be 0 (auto) or 1 (dense), got %d", mode);
+    if (mode < 0 || mode > 2)
+        return fail_arg(B200P_ERR_ARG, "ingest mode must be 0 (auto), 1 (dense) or 2 (host gather), got %d", mode);
     pl->ingest_mode = mode;
     return 0;
 }

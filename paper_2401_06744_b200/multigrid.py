@@ -120,10 +120,14 @@ class Plan:
     def launch_count(self) -> int:
         return int(_lib.lib().b200p_plan_launch_count(self.handle))
 
-    def set_ingest(self, dense: bool):
-        """Host f64 entry points: False = sparse ingest when the mask is sparse (default; lowest latency of a
-        single solve), True = always DMA the planes (what a multi-lane pipeline wants)."""
-        _lib.check(_lib.lib().b200p_plan_set_ingest(self.handle, 1 if dense else 0))
+    def set_ingest(self, dense: bool = False, host_gather: bool = False):
+        """Host f64 entry points: default = sparse ingest when the mask is sparse (from a pinned source the device
+        fetches the values itself; lowest latency of a single solve); dense = always DMA the planes;
+        host_gather = sparse, with the (index, values) list always gathered by the library's host threads
+        (12 MB instead of 207 MB per 4K RGB frame on the link, and no device reads of host memory)."""
+        if dense and host_gather:
+            raise ValueError("dense and host_gather exclude each other")
+        _lib.check(_lib.lib().b200p_plan_set_ingest(self.handle, 1 if dense else (2 if host_gather else 0)))
 
     def last_transfer_bytes(self):
         """(H2D, D2H) bytes copied by the last host entry point (the f64 ingest is sparse when the mask is)."""

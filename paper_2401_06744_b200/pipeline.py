@@ -11,6 +11,10 @@ One host thread therefore keeps `lanes` chunks in flight and the copy engines
 run under the kernels of the other lanes (PCIe is full duplex), which is what
 the end-to-end frames/s of a decoder fed from host memory depends on.  Pass
 pinned arrays: pageable memory makes the copies synchronous.
+fp64 ingest of a multi-lane pipeline: the path reads `known` only at mask pixels, so
+the library's host threads gather those values into a pinned (index, values) list
+(``ingest="host-gather"``: 12 MB instead of 207 MB per 4K RGB frame on the link, which
+leaves PCIe to the results; 227 -> 256 frames/s measured on 5 lanes).
 Results do not depend on the chunking (bit-identical to a single batched plan)."""
 
 from __future__ import annotations
@@ -25,7 +29,8 @@ from .multigrid import MultigridConfig, Plan
 
 class FramePipeline:
     def __init__(self, width, height, channels, cfg: MultigridConfig | None = None, spacing=1.0,
-                 lanes: int = 5, frames_per_lane: int = 1, sparse_ingest: bool | None = None):
+                 lanes: int = 5, frames_per_lane: int = 1, sparse_ingest: bool | None = None,
+                 ingest: str | None = None):
         if lanes < 1 or frames_per_lane < 1:
             raise ValueError("need lanes >= 1 and frames_per_lane >= 1")
         _dev.require_cuda()
@@ -36,12 +41,21 @@ class FramePipeline:
         _lib.check(_lib.lib().b200p_get_device(C.byref(dev)))
         self.device = dev.value
         self.plans = [Plan(width, height, channels, frames_per_lane, self.cfg, spacing) for _ in range(lanes)]
-        # with several lanes the copy engines run under the other lanes' kernels for free, while the
-        # zero-copy fetch of the sparse ingest queues behind their D2H traffic: DMA the planes
-        if sparse_ingest is None:
-            sparse_ingest = lanes == 1
+        # fp64 ingest.  "zero-copy": the device fetches the mask pixels' values from the pinned source itself --
+        # lowest latency for one lane, but with several lanes those reads queue behind the other lanes' D2H
+        # traffic (172 frames/s on 5 lanes); "dense": the copy engine moves the planes (227); "host-gather": host
+        # threads compact the values, the copy engine moves 6 % of the bytes (256).  sparse_ingest = True / False
+        # is the older spelling of "zero-copy" / "dense".
+        if ingest is None:
+            if sparse_ingest is None:
+                ingest = "zero-copy" if lanes == 1 else "host-gather"
+            else:
+                ingest = "zero-copy" if sparse_ingest else "dense"
+        if ingest not in ("zero-copy", "dense", "host-gather"):
+            raise ValueError(f"ingest must be 'zero-copy', 'dense' or 'host-gather', got {ingest!r}")
+        self.ingest = ingest
         for p in self.plans:
-            p.set_ingest(dense=not sparse_ingest)
+            p.set_ingest(dense=ingest == "dense", host_gather=ingest == "host-gather")
         self._inflight = [None] * lanes  # (job, chunk index) pending on each lane
         self._next = 0
 

@@ -16,8 +16,10 @@ ho = torch.empty_like(hk).pin_memory()
 hb = torch.from_numpy(np.packbits(masks, axis=2)).pin_memory()
 hp = torch.from_numpy(np.ascontiguousarray(np.moveaxis(known.astype(np.uint8), 1, 3))).pin_memory()
 hq = torch.empty_like(hp).pin_memory()
-for lanes, fpl in ((5, 1), (3, 2), (4, 2), (2, 4), (4, 4), (8, 1)):
-    pipe = bp.FramePipeline(W, H, C, cfg, lanes=lanes, frames_per_lane=fpl)
+import os
+shapes = ((5, 1, False), (5, 1, True), (4, 2, True), (8, 1, True), (4, 4, True), (3, 1, True))
+for lanes, fpl, hg in shapes:
+    pipe = bp.FramePipeline(W, H, C, cfg, lanes=lanes, frames_per_lane=fpl, host_gather=hg)
     res = []
     for image in (False, True):
         a = (hb, hp, hq) if image else (hm, hk, ho)
@@ -28,4 +30,4 @@ for lanes, fpl in ((5, 1), (3, 2), (4, 2), (2, 4), (4, 4), (8, 1)):
         pipe.flush()
         res.append(4 * F / (time.perf_counter() - t0))
     pipe.close()
-    print(f"lanes {lanes} x {fpl} frames: fp64 {res[0]:6.1f} frames/s, 8-bit image {res[1]:6.1f} frames/s", flush=True)
+    print(f"lanes {lanes} x {fpl} frames host_gather={hg} threads={os.environ.get('B200P_HOST_THREADS', 'default')}: fp64 {res[0]:6.1f} frames/s, 8-bit image {res[1]:6.1f} frames/s", flush=True)

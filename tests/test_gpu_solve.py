@@ -618,6 +618,43 @@ def test_sparse_ingest_matches_dense_ingest(monkeypatch):
     plan.close()
 
 
+@pytest.mark.parametrize("w,h,c,f,dens", [(200, 136, 3, 2, 0.04), (64, 5, 1, 3, 0.3), (333, 77, 2, 5, 0.01), (48, 40, 1, 1, 0.9)])
+def test_host_gather_ingest(w, h, c, f, dens, monkeypatch):
+    """Ingest mode 2: the library's host threads compact (index, values) lists chunk by chunk, also from a pinned
+    source.  Same bits as the plane copy, bytes as counted, dense masks fall back; one worker thread or many."""
+    import torch
+    cfg = bp.MultigridConfig(block_size=16, overlap=2)
+    ms, ks = zip(*(oracle.seeded_problem(w, h, dens, 30 + i, channels=c) for i in range(f)))
+    masks, known = np.stack(ms).view(np.uint8), np.stack(ks)
+    plan = bp.Plan(w, h, c, f, cfg)
+    plan.set_ingest(dense=True)
+    want, _ = plan.solve_host(masks, known)
+    plan.set_ingest(host_gather=True)
+    nk = int(masks.sum())
+    sparse = masks.size + nk * (4 + 8 * c)
+    expect_up = sparse if (nk * (4 + 8 * c)) * 2 <= known.nbytes else masks.size + known.nbytes
+    junk = np.where(masks[:, None].astype(bool), known, -7.0)
+    for src in (known, junk):
+        got, _ = plan.solve_host(masks, src)
+        assert np.array_equal(got, want)
+        assert plan.last_transfer_bytes() == (expect_up, known.nbytes)
+    pk = torch.from_numpy(junk).pin_memory()
+    po = torch.empty_like(pk).pin_memory()
+    plan.solve_host_async(masks, pk.numpy(), po.numpy())
+    plan.wait()
+    assert np.array_equal(po.numpy(), want) and plan.last_transfer_bytes() == (expect_up, known.nbytes)
+    with pytest.raises(ValueError):
+        plan.set_ingest(dense=True, host_gather=True)
+    plan.close()
+    pipe = bp.FramePipeline(w, h, c, cfg, lanes=2, frames_per_lane=1)
+    assert pipe.ingest == "host-gather"
+    out, _ = pipe.run(masks, junk)
+    assert np.array_equal(out, want)
+    pipe.close()
+    with pytest.raises(ValueError):
+        bp.FramePipeline(w, h, c, cfg, lanes=2, ingest="bogus")
+
+
 def test_mask_residual_shortcut_agrees(monkeypatch):
     """Inside the solve drivers the iterate equals `known` at mask pixels after every step, so the row
     walkers (K1, K3) take b - u = 0 there without reading b (default); B200P_TRUST_MASK=0 evaluates it.
