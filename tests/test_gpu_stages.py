@@ -328,3 +328,27 @@ def test_oras_sweeps_on_state_hook(rng):
 
 def seen_stop(rn):
     return 1.5 * rn
+
+
+@pytest.mark.parametrize("w,h", [(144, 65), (272, 135), (128, 1030), (400, 530)])
+def test_tile_pipelines_on_ragged_levels(w, h, rng):
+    """K1 / K3 / K4 / K5 as TMA tile pipelines (w % 16 == 0, w >= 128, h >= 64) where their tiling is ragged: a
+    last strip of 16 columns, odd heights (one-row last cells), a last tile of one row, more rows than one CTA's
+    512, levels that fall back to the walkers further down.  Explicit right-hand side (v_cycle on a general b)
+    and the solve driver's trusted-mask variants (solve_image), both against the oracle."""
+    m, k = oracle.seeded_problem(w, h, 0.04, 21, channels=2)
+    co, cb = oracle.MultigridConfig(block_size=16, overlap=2), bp.MultigridConfig(block_size=16, overlap=2)
+    ho = oracle.build_hierarchy(m, k, 1.0, co)
+    hb = bp.build_hierarchy(bp.InpaintingProblem(m, k), cb)
+    b = np.where(m, k[0], rng.normal(size=(h, w)))          # not the problem's own right-hand side
+    u_o = np.where(m, k[0], rng.normal(size=(h, w)))
+    u_g = u_o.copy()
+    oracle.v_cycle(ho, 0, u_o, b)
+    bp.v_cycle(hb, 0, u_g, b)
+    np.testing.assert_allclose(u_g, u_o, rtol=0, atol=1e-8)
+    res = bp.solve_image(bp.InpaintingProblem(m, k), "mg-oras", cb)
+    for c in range(2):
+        ref, rep = oracle.solve_image(m, k[c:c + 1], 1.0, co)
+        assert res.reports[c].iterations == rep[0].iterations
+        assert res.reports[c].final_rel_residual == pytest.approx(rep[0].final_rel_residual, rel=1e-6)
+        np.testing.assert_allclose(res.fields[c], ref[0], rtol=0, atol=1e-9)
