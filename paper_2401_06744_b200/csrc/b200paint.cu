@@ -788,6 +788,20 @@ static int launch_norm(b200p_plan *pl, const LevelHost &L, const double *u, cons
     LaunchScope sc(pl, st, KK_NORM, field_bytes(pl, L, rm ? 1.0 : 2.0, 1.0));
 #define NORM_ARGS u, b, L.d_mask, L.info.height, L.info.width, L.dev.hinv2, pl->C, plane, pred, \
                   pl->d_partial, pl->d_partial_flag, pl->d_counter, pl->d_rs, pl->d_mflag
+    static const bool want_flat = !(getenv("B200P_FLAT_NORM") && atoi(getenv("B200P_FLAT_NORM")) == 0);
+    if (want_flat && um && rm && u == b && L.info.width % 8 == 0 && ((uintptr_t)L.d_mask % 8) == 0) {
+        // the flat initialisation's norm: work only next to mask pixels (kernels_rows.cuh, K1f)
+        RowsArgs R = rows_args(pl, L, u, b, pred);
+        dim3 g((L.info.width / 8 + FLAT_THREADS - 1) / FLAT_THREADS, (R.y_hi - R.y_lo + FLAT_ROWS - 1) / FLAT_ROWS, pl->F);
+        flat_init_sqnorm_kernel<<<g, FLAT_THREADS, 0, st>>>(R);
+        CU(cudaGetLastError());
+        if (striped(pl, L)) {
+            int rc2 = strip_exchange(pl, B200P_XCHG_SUM_RS, pl->d_rs, st);
+            if (!rc2) rc2 = strip_exchange(pl, B200P_XCHG_MAX_FLAGS, pl->d_mflag, st);
+            return rc2;
+        }
+        return 0;
+    }
     static const bool want_tma = !(getenv("B200P_ROWS_TMA") && atoi(getenv("B200P_ROWS_TMA")) == 0);
     if (want_tma && !um && rows4_ok(L, u, b) && L.info.width % 16 == 0 && L.info.width >= RT_W &&
         L.info.height >= 4 * RT_R && ((uintptr_t)L.d_mask % 16) == 0) {

@@ -85,6 +85,74 @@ __device__ __forceinline__ void publish_partial(double acc, int flag, int p, con
     publish_partial_at(acc, flag, p, gridDim.x * gridDim.y, blockIdx.y * gridDim.x + blockIdx.x, A, red, sflag, is_last);
 }
 
+// ---------------------------------------------------------------- K1f -----
+// The baseline norm of the flat initialisation (multigrid.py:441-446, solvers.py:415-417 with u = b =
+// where(mask, known, 0)): the residual is 0 at mask pixels and hinv2 * (sum of the KNOWN direct neighbours)
+// elsewhere, i.e. non-zero only next to the 2 % of mask pixels.  A thread takes 8 pixels of a row as one
+// 8-byte mask word (+ the words above / below and the two edge bytes), finds the pixels that have a known
+// neighbour with byte arithmetic, and only for those fetches values -- for every channel of the frame, the
+// masks being shared (grid z = frame).  Same per-pixel arithmetic as residual_px (neighbour order
+// ((up + down) + left) + right, zeros for unknown neighbours); deterministic last-CTA reduction per problem.
+constexpr int FLAT_THREADS = 128;
+constexpr int FLAT_ROWS = 16;
+constexpr int FLAT_MAXC = 4;
+
+__device__ __forceinline__ unsigned long long bytes_nonzero(unsigned long long v) {  // every byte -> 0 / 1
+    v |= v >> 4;
+    v |= v >> 2;
+    v |= v >> 1;
+    return v & 0x0101010101010101ull;
+}
+
+__global__ void __launch_bounds__(FLAT_THREADS)
+flat_init_sqnorm_kernel(const RowsArgs A) {
+    __shared__ double red[34];
+    __shared__ int sflag;
+    __shared__ bool is_last;
+    const int frame = blockIdx.z;
+    const int C = A.channels;
+    if (threadIdx.x == 0) sflag = 0;
+    __syncthreads();
+    const int h = A.h, w = A.w;
+    const int x8 = 8 * (blockIdx.x * FLAT_THREADS + threadIdx.x);
+    const int y0 = A.y_lo + blockIdx.y * FLAT_ROWS, y1 = min(A.y_hi, y0 + FLAT_ROWS);
+    const uint8_t *mp = A.mask + (size_t)frame * A.plane;
+    for (int c0 = 0; c0 < C; c0 += FLAT_MAXC) {
+        double acc[FLAT_MAXC] = {0.0, 0.0, 0.0, 0.0};
+        if (x8 < w) {
+            for (int y = y0; y < y1; ++y) {
+                const uint8_t *row = mp + (size_t)y * w + x8;
+                const unsigned long long mc = bytes_nonzero(*reinterpret_cast<const unsigned long long *>(row));
+                const unsigned long long mu = y > 0 ? bytes_nonzero(*reinterpret_cast<const unsigned long long *>(row - w)) : 0ull;
+                const unsigned long long md = y + 1 < h ? bytes_nonzero(*reinterpret_cast<const unsigned long long *>(row + w)) : 0ull;
+                const unsigned long long lb = x8 > 0 ? (row[-1] != 0) : 0, rb = x8 + 8 < w ? (row[8] != 0) : 0;
+                const unsigned long long ml = (mc << 8) | lb, mr = (mc >> 8) | (rb << 56);
+                unsigned long long need = (mc ^ 0x0101010101010101ull) & (mu | md | ml | mr);
+                while (need) {
+                    const int k = (__ffsll((long long)need) - 1) >> 3;
+                    need &= need - 1;
+                    const bool up = (mu >> (8 * k)) & 1, dn = (md >> (8 * k)) & 1, lf = (ml >> (8 * k)) & 1, rt = (mr >> (8 * k)) & 1;
+                    const size_t i = (size_t)y * w + x8 + k;
+#pragma unroll
+                    for (int cc = 0; cc < FLAT_MAXC; ++cc) {
+                        if (c0 + cc >= C) break;
+                        const double *kp = A.u + ((size_t)frame * C + c0 + cc) * A.plane + i;
+                        const double vu = up ? kp[-w] : 0.0, vd = dn ? kp[w] : 0.0, vl = lf ? kp[-1] : 0.0, vr = rt ? kp[1] : 0.0;
+                        const double r = (((vu + vd) + vl) + vr) * A.hinv2;
+                        acc[cc] = fma(r, r, acc[cc]);
+                    }
+                }
+            }
+        }
+        for (int cc = 0; cc < FLAT_MAXC && c0 + cc < C; ++cc) {
+            const int p = frame * C + c0 + cc;
+            if (A.pred && !A.pred[p]) continue;     // block-uniform
+            __syncthreads();
+            publish_partial(acc[cc], 0, p, A, red, &sflag, &is_last);
+        }
+    }
+}
+
 struct Row4 {
     double v[4];
 };
