@@ -516,6 +516,12 @@ __global__ void ml_finish_kernel(int P, const int *sweeps, int *cycles, int *uni
 // ------------------------------------------------------ launch helpers -----
 static inline dim3 grid2x(int wc, int hc, int z) { return dim3((wc + 63) / 64, (hc + 3) / 4, z); }
 
+// K6a with 8 coarse cells per thread: fine rows are whole 16-byte words, coarse rows whole 8-byte words
+static bool words8_ok(int w, const void *fmask, const void *cmask) {
+    static const bool want = !(getenv("B200P_K6_WORDS") && atoi(getenv("B200P_K6_WORDS")) == 0);
+    return want && w % 16 == 0 && ((uintptr_t)fmask % 16) == 0 && ((uintptr_t)cmask % 8) == 0;
+}
+
 static double field_bytes(const b200p_plan *pl, const LevelHost &L, double fields, double masks) {
     const double n = (double)L.info.height * L.info.width;
     return fields * pl->P * 8.0 * n + masks * pl->F * n;
@@ -1429,8 +1435,10 @@ static int enqueue_hierarchy(b200p_plan *pl, cudaStream_t st) {
         const int h = f.info.height, w = f.info.width;
         {
             LaunchScope sc(pl, st, KK_DOWN_MASK, 1.25 * pl->F * (double)h * w);
-            downsample_mask_kernel<<<grid2x(c.info.width, c.info.height, pl->F), ST_THREADS, 0, st>>>(
-                f.d_mask, h, w, c.d_mask);
+            if (words8_ok(w, f.d_mask, c.d_mask))
+                downsample_mask8_kernel<<<grid2x(c.info.width / 8, c.info.height, pl->F), ST_THREADS, 0, st>>>(f.d_mask, h, w, c.d_mask);
+            else
+                downsample_mask_kernel<<<grid2x(c.info.width, c.info.height, pl->F), ST_THREADS, 0, st>>>(f.d_mask, h, w, c.d_mask);
             CU(cudaGetLastError());
         }
         {
@@ -3610,8 +3618,10 @@ int b200p_unpack_mask_bits(const uint8_t *d_bits, int frames, int h, int w, uint
 
 int b200p_downsample_mask(const uint8_t *d_fine, int h, int w, uint8_t *d_coarse, void *stream) {
     if (!d_fine || !d_coarse || h < 1 || w < 1) return fail_arg(B200P_ERR_ARG, "bad argument");
-    downsample_mask_kernel<<<grid2x((w + 1) / 2, (h + 1) / 2, 1), ST_THREADS, 0, (cudaStream_t)stream>>>(
-        d_fine, h, w, d_coarse);
+    if (words8_ok(w, d_fine, d_coarse))
+        downsample_mask8_kernel<<<grid2x(w / 16, (h + 1) / 2, 1), ST_THREADS, 0, (cudaStream_t)stream>>>(d_fine, h, w, d_coarse);
+    else
+        downsample_mask_kernel<<<grid2x((w + 1) / 2, (h + 1) / 2, 1), ST_THREADS, 0, (cudaStream_t)stream>>>(d_fine, h, w, d_coarse);
     CU(cudaGetLastError());
     return 0;
 }
