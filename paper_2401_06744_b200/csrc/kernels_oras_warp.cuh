@@ -78,6 +78,25 @@ __device__ __forceinline__ unsigned kw_div(unsigned n, unsigned m, unsigned k) {
 }
 
 // Packs the block-local masks for K2W: grid (ceil(nblocks / 4), F), 128 threads, a warp per block.
+// A lane's 8 mask bytes of a row are fetched with the widest loads their address allows (block starts are even:
+// 16-bit pieces at worst; one 8-byte load where the start is a multiple of 8) and squeezed to 8 bits by a multiply.
+__device__ __forceinline__ unsigned long long kw_load8(const uint8_t *p) {
+    const unsigned a = (unsigned)(uintptr_t)p & 7u;   // warp-uniform for a given row
+    if (a == 0) return *reinterpret_cast<const unsigned long long *>(p);
+    if ((a & 3u) == 0) {
+        const uint2 v = make_uint2(*reinterpret_cast<const unsigned *>(p), *reinterpret_cast<const unsigned *>(p + 4));
+        return ((unsigned long long)v.y << 32) | v.x;
+    }
+    unsigned long long r = 0;
+    if ((a & 1u) == 0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r |= (unsigned long long)*reinterpret_cast<const unsigned short *>(p + 2 * k) << (16 * k);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) r |= (unsigned long long)p[k] << (8 * k);
+    }
+    return r;
+}
 __global__ void __launch_bounds__(KW_THREADS)
 pack_block_masks_warp_kernel(const LevelDev L, const uint8_t *__restrict__ mask, size_t plane,
                              unsigned *__restrict__ mtab) {
@@ -88,10 +107,14 @@ pack_block_masks_warp_kernel(const LevelDev L, const uint8_t *__restrict__ mask,
     const uint8_t *mp = mask + (size_t)f * plane;
     unsigned bits = 0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-            if (mp[(size_t)(gy0 + j) * L.w + gx0 + i]) bits |= 1u << (j * 8 + i);
+    for (int j = 0; j < 4; ++j) {
+        unsigned long long v = kw_load8(mp + (size_t)(gy0 + j) * L.w + gx0);
+        v |= v >> 4;                          // every byte -> 0 / 1 ...
+        v |= v >> 2;
+        v |= v >> 1;
+        v &= 0x0101010101010101ull;
+        bits |= (unsigned)((v * 0x0102040810204080ull) >> 56) << (j * 8);   // ... -> bit i = byte i
+    }
     mtab[((size_t)f * L.nblocks + blk) * 32 + lane] = bits;
 }
 
