@@ -147,3 +147,45 @@ def test_solve_result_throughput_view_and_strip_output_ownership():
 def torch_equal(x, y):
     import torch
     return bool(torch.equal(x, y))
+
+
+_FALLBACK_SCRIPT = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import oracle
+import paper_2401_06744_b200 as bp
+out = {{}}
+for i, (w, h, c, bs, ov, dens) in enumerate({cases!r}):
+    m, k = oracle.seeded_problem(w, h, dens, 40 + i, channels=c)
+    res = bp.solve_image(bp.InpaintingProblem(m, k), "mg-oras", bp.MultigridConfig(block_size=bs, overlap=ov))
+    out[f"u{{i}}"] = res.fields
+    out[f"it{{i}}"] = np.array([r.iterations for r in res.reports])
+    out[f"rel{{i}}"] = np.array([r.final_rel_residual for r in res.reports])
+np.savez(sys.argv[1], **out)
+"""
+
+
+def test_fast_paths_agree_with_their_fallbacks(tmp_path):
+    """The TMA tile pipelines (K1 / K3 / K4 / K5), the sparse flat-init norm and the word-wise mask kernels against
+    the kernels they replaced (B200P_ROWS_TMA=0 B200P_PROLONG_TMA=0 B200P_FLAT_NORM=0 B200P_K6_WORDS=0, read once
+    per process: a second interpreter): same V-cycle counts, fields equal to rounding (the norms are summed in a
+    different order), on levels of every eligibility class."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cases = [(256, 144, 3, 32, 6, 0.03), (400, 530, 1, 16, 2, 0.02), (144, 65, 2, 16, 2, 0.05), (1040, 272, 1, 32, 6, 0.01)]
+    script = _FALLBACK_SCRIPT.format(root=root, cases=cases)
+    outs = []
+    for name, env in (("fast", {}), ("fallback", {"B200P_ROWS_TMA": "0", "B200P_PROLONG_TMA": "0",
+                                                  "B200P_FLAT_NORM": "0", "B200P_K6_WORDS": "0"})):
+        path = str(tmp_path / f"{name}.npz")
+        r = subprocess.run([sys.executable, "-c", script, path], env={**os.environ, **env}, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(path))
+    fast, slow = outs
+    for i in range(len(cases)):
+        assert np.array_equal(fast[f"it{i}"], slow[f"it{i}"])
+        np.testing.assert_allclose(fast[f"rel{i}"], slow[f"rel{i}"], rtol=1e-9)
+        np.testing.assert_allclose(fast[f"u{i}"], slow[f"u{i}"], rtol=0, atol=1e-10)
