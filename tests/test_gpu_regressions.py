@@ -189,3 +189,19 @@ def test_fast_paths_agree_with_their_fallbacks(tmp_path):
         assert np.array_equal(fast[f"it{i}"], slow[f"it{i}"])
         np.testing.assert_allclose(fast[f"rel{i}"], slow[f"rel{i}"], rtol=1e-9)
         np.testing.assert_allclose(fast[f"u{i}"], slow[f"u{i}"], rtol=0, atol=1e-10)
+
+
+def test_many_channels_and_frames_through_the_tile_pipelines():
+    """Grid x = strip * channels + channel, z = frame (tile pipelines), channel batches of 4 (flat-init norm) and 3
+    (K6b): 5 channels x 2 frames on a level the pipelines take, against the oracle frame by frame."""
+    w, h, c, f = 160, 96, 5, 2
+    cfg = bp.MultigridConfig(block_size=16, overlap=2)
+    ms, ks = zip(*(oracle.seeded_problem(w, h, 0.04, 60 + i, channels=c) for i in range(f)))
+    plan = bp.Plan(w, h, c, f, cfg)
+    out, reps = plan.solve_host(np.stack(ms).view(np.uint8), np.stack(ks))
+    plan.close()
+    for i in range(f):
+        ref, ro = oracle.solve_image(ms[i], ks[i], 1.0, oracle.MultigridConfig(block_size=16, overlap=2))
+        np.testing.assert_allclose(out[i], ref, rtol=0, atol=1e-9)
+        got = reps[i * c:(i + 1) * c] if not isinstance(reps[0], (list, tuple)) else reps[i]
+        assert [r.iterations for r in got] == [r.iterations for r in ro]
