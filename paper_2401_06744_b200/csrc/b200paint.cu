@@ -750,9 +750,11 @@ static int encode_plane_map(CUtensorMap *tm, const void *base, int elem, int w, 
     return 0;
 }
 
+#if B200P_LAB
 static int encode_field_map(CUtensorMap *tm, const double *base, int w, int h, int planes, int box_w, int box_h) {
     return encode_plane_map(tm, base, 8, w, h, planes, box_w, box_h);
 }
+#endif
 
 // K4 / K5: fine rows of coarse rows [Ylo, Yhi) (strip mode passes a sub-range; the whole plane otherwise).  Whole planes
 // whose rows are 16-byte multiples in every array go through the TMA tile pipeline (kernels_rows_tma.cuh).
@@ -1014,7 +1016,6 @@ static int launch_sweep_fused(b200p_plan *, const LevelHost &, UBuf &, const dou
                               cudaStream_t) {
     return fail_arg(B200P_ERR_UNSUPPORTED, "the fused sweep is an experiment: build with -DB200P_EXPERIMENTS");
 }
-static bool arrival_fusion_enabled() { return false; }
 #else
 // K2F: fused solve + combine, u.cur -> u.alt, then swap.
 static int launch_sweep_fused(b200p_plan *pl, const LevelHost &L, UBuf &u, const double *b, bool rm,
