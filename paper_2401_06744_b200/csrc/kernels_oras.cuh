@@ -571,8 +571,21 @@ oras_sweep_generic_kernel(const SweepArgs A) {
 // covering block columns are per-thread constants, and the (up to) four tile
 // reads per pixel are issued branch-free, COMBINE_G rows at a time, so that
 // ~40 independent loads per thread are in flight (HBM-bound streaming pass).
-constexpr int COMBINE_ROWS = 32;
-constexpr int COMBINE_G = 8;
+// K2b tuning (A/B builds): rows in flight per thread, resident CTAs per SM the register budget is cut for, rows
+// per CTA.  4 / 3 / 32 = 80 registers without spills, 768 threads per SM: 5.48 ms per 8-frame step; 8 rows in
+// flight at the compiler's own 128 registers (2 CTAs) 5.8, 4 at 114 registers 6.6, 3 at 64 registers 6.5, 5 at 80
+// (spills) 5.9, 16 at 242 registers 8.1
+#ifndef B200P_COMBINE_G
+#define B200P_COMBINE_G 4
+#endif
+#ifndef B200P_COMBINE_MINB
+#define B200P_COMBINE_MINB 3
+#endif
+#ifndef B200P_COMBINE_ROWS
+#define B200P_COMBINE_ROWS 32
+#endif
+constexpr int COMBINE_ROWS = B200P_COMBINE_ROWS;
+constexpr int COMBINE_G = B200P_COMBINE_G;
 
 // Stage helper: tiles[p][blk][j][i] *= wy[iy][j] * wx[ix][i] in the order of K2's epilogue, (v * wy) * wx
 // (solvers.py:309-310), so that an isolated combine pass can be fed UNWEIGHTED local corrections.
@@ -595,7 +608,7 @@ __global__ void fill_double_kernel(double *p, int n, double v) {
 // `egress` (8-bit decode): the updated pixel is also written as clip(round(u)) into
 // the interleaved (F, h, w, C) image (image_from_fields, fileio.py:58-65) -- the last post-smoothing
 // combine of the finest level carries it, so an 8-bit decode needs no pass over the fp64 result.
-__global__ void __launch_bounds__(ST_THREADS_COMBINE)
+__global__ void __launch_bounds__(ST_THREADS_COMBINE, B200P_COMBINE_MINB)
 oras_combine_kernel(const LevelDev L, const double *__restrict__ scratch, size_t plane,
                     const int *__restrict__ pred, const double *__restrict__ rs,
                     double *__restrict__ u, int *__restrict__ unit_counter, int y_lo, int y_hi,
