@@ -23,7 +23,10 @@ constexpr int RT_G = 4;                   // row groups per tile: RT_W x RT_G th
 constexpr int RT_THREADS = RT_W * RT_G;
 constexpr int RT_BOXW = RT_W + 4;         // box columns x0 - 2 .. x0 + RT_W + 1
 constexpr int RT_R = 16;                  // rows per tile
-constexpr int RT_STAGES = 4;
+#ifndef B200P_RT_STAGES
+#define B200P_RT_STAGES 3      // ring depth of K1 / K3: 3 stages = 3 CTAs per SM (2.31 / 1.35 ms per step; 4: 2.42 / 1.42; 2: 2.38 / 1.41)
+#endif
+constexpr int RT_STAGES = B200P_RT_STAGES;
 constexpr int RT_U_BYTES = (RT_R + 2) * RT_BOXW * 8;            // 19008
 constexpr int RT_U_STRIDE = (RT_U_BYTES + 127) / 128 * 128;     // 19072: stages stay 128-byte aligned
 constexpr int RT_M_BYTES = RT_R * RT_W;                         // 2048
@@ -292,8 +295,9 @@ constexpr int PT_CR = RT_R / 2 + 2;                    // coarse box rows
 constexpr int PT_C_BYTES = PT_CW * PT_CR * 8;          // 5440
 constexpr int PT_C_STRIDE = (PT_C_BYTES + 127) / 128 * 128;
 constexpr int PT_THREADS = (RT_W / 2) * (RT_R / 2);    // 512
+constexpr int PT_STAGES = 4;                           // ring depth of the prolongation pipelines (3: K4 1.62 vs 1.59 ms)
 __host__ __device__ inline size_t prolong_tma_smem(bool solution) {
-    return (size_t)RT_STAGES * (PT_C_STRIDE + RT_M_BYTES + (solution ? 0 : RT_B_BYTES)) + 128;
+    return (size_t)PT_STAGES * (PT_C_STRIDE + RT_M_BYTES + (solution ? 0 : RT_B_BYTES)) + 128;
 }
 struct ProlongArgs {
     int h, w, channels, rows_per_cta;   // fine size; rows_per_cta a multiple of RT_R
@@ -307,15 +311,15 @@ __global__ void __launch_bounds__(PT_THREADS)
 prolongate_tma_kernel(const ProlongArgs A, const __grid_constant__ CUtensorMap tm_c,
                       const __grid_constant__ CUtensorMap tm_m, const __grid_constant__ CUtensorMap tm_u) {
     extern __shared__ __align__(128) unsigned char rt_smem[];
-    __shared__ __align__(8) unsigned long long full[RT_STAGES];
+    __shared__ __align__(8) unsigned long long full[PT_STAGES];
     const TileCoord tc = tile_coord(A.channels);
     const int p = tc.p;
     if (A.pred && !A.pred[p]) return;
     const int t = threadIdx.x & (RT_W / 2 - 1), g = threadIdx.x / (RT_W / 2);
     const bool leader = threadIdx.x == 0;
-    unsigned char *sc = rt_smem, *smk = rt_smem + RT_STAGES * PT_C_STRIDE, *su = smk + RT_STAGES * RT_M_BYTES;
+    unsigned char *sc = rt_smem, *smk = rt_smem + PT_STAGES * PT_C_STRIDE, *su = smk + PT_STAGES * RT_M_BYTES;
     if (leader)
-        for (int s = 0; s < RT_STAGES; ++s) mbar_init(smem_u32(&full[s]), 1);
+        for (int s = 0; s < PT_STAGES; ++s) mbar_init(smem_u32(&full[s]), 1);
     __syncthreads();
     const int h = A.h, w = A.w;
     const int hc = (h + 1) >> 1, wc = w >> 1;
@@ -330,7 +334,7 @@ prolongate_tma_kernel(const ProlongArgs A, const __grid_constant__ CUtensorMap t
     double *up = A.u + (size_t)p * fplane;
     const double *fr = SOLUTION ? A.frhs + (size_t)p * fplane : nullptr;
     auto issue = [&](int tile) {
-        const int s = tile % RT_STAGES;
+        const int s = tile % PT_STAGES;
         const unsigned bar = smem_u32(&full[s]);
         mbar_expect_tx(bar, PT_C_BYTES + RT_M_BYTES + (SOLUTION ? 0 : RT_B_BYTES));
         const int ty = y0 + tile * RT_R;
@@ -339,14 +343,14 @@ prolongate_tma_kernel(const ProlongArgs A, const __grid_constant__ CUtensorMap t
         if (!SOLUTION) tma_load_3d(smem_u32(su + s * RT_B_BYTES), &tm_u, xs, ty, p, bar);
     };
     if (leader)
-        for (int tile = 0; tile < min(RT_STAGES, ntiles); ++tile) issue(tile);
+        for (int tile = 0; tile < min(PT_STAGES, ntiles); ++tile) issue(tile);
     // column offsets of the far neighbours in the coarse box (cell X sits at column t + 2): clamped at the borders
     const int oL = X > 0 ? t + 1 : t + 2, oR = X < wc - 1 ? t + 3 : t + 2;
     uchar2 m0n = make_uchar2(0, 0), m1n = make_uchar2(0, 0);
     double2 f0n = make_double2(0.0, 0.0), f1n = make_double2(0.0, 0.0);
     auto fetch_ahead = [&](int tile) {   // masks of `tile` from its stage; right-hand side at its mask pixels
-        const int s = tile % RT_STAGES;
-        mbar_wait(smem_u32(&full[s]), (tile / RT_STAGES) & 1);
+        const int s = tile % PT_STAGES;
+        mbar_wait(smem_u32(&full[s]), (tile / PT_STAGES) & 1);
         const int ya = y0 + tile * RT_R + 2 * g;
         m0n = m1n = make_uchar2(0, 0);
         if (live && ya < y1) {
@@ -364,7 +368,7 @@ prolongate_tma_kernel(const ProlongArgs A, const __grid_constant__ CUtensorMap t
     };
     fetch_ahead(0);
     for (int tile = 0; tile < ntiles; ++tile) {
-        const int s = tile % RT_STAGES;
+        const int s = tile % PT_STAGES;
         const int ya = y0 + tile * RT_R + 2 * g;           // the cell's fine rows ya, ya + 1
         const bool cell = live && ya < y1;
         const uchar2 m0 = m0n, m1 = m1n;
@@ -399,7 +403,7 @@ prolongate_tma_kernel(const ProlongArgs A, const __grid_constant__ CUtensorMap t
             }
         }
         __syncthreads();   // every thread is done with stage s
-        if (leader && tile + RT_STAGES < ntiles) issue(tile + RT_STAGES);
+        if (leader && tile + PT_STAGES < ntiles) issue(tile + PT_STAGES);
     }
 }
 
