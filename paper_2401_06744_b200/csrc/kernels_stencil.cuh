@@ -566,7 +566,10 @@ __device__ __forceinline__ void downsample_cell(const uint8_t *__restrict__ fmas
     }
 }
 
-__global__ void __launch_bounds__(ST_THREADS, 4)
+#ifndef B200P_K6_MINB
+#define B200P_K6_MINB 4
+#endif
+__global__ void __launch_bounds__(ST_THREADS, B200P_K6_MINB)
 downsample_values_kernel(const uint8_t *__restrict__ fmask, const uint8_t *__restrict__ cmask,
                          const double *__restrict__ frhs, int h, int w, int channels, int modified,
                          double *__restrict__ crhs) {
