@@ -19,7 +19,10 @@
 
 namespace b200p {
 
-constexpr int ST_THREADS_COMBINE = 256;
+#ifndef B200P_COMBINE_THREADS
+#define B200P_COMBINE_THREADS 128
+#endif
+constexpr int ST_THREADS_COMBINE = B200P_COMBINE_THREADS;
 
 #ifndef B200P_PACKED_RED
 #define B200P_PACKED_RED 1
@@ -572,14 +575,15 @@ oras_sweep_generic_kernel(const SweepArgs A) {
 // reads per pixel are issued branch-free, COMBINE_G rows at a time, so that
 // ~40 independent loads per thread are in flight (HBM-bound streaming pass).
 // K2b tuning (A/B builds): rows in flight per thread, resident CTAs per SM the register budget is cut for, rows
-// per CTA.  4 / 3 / 32 = 80 registers without spills, 768 threads per SM: 5.48 ms per 8-frame step; 8 rows in
+// per CTA (B200P_COMBINE_THREADS: threads per CTA).  4 rows, 80 registers without spills, 768 threads per SM as
+// 6 CTAs of 128: 5.36 ms per 8-frame step (3 CTAs of 256: 5.48; 12 of 64: 5.34; 7 of 128 at 72 registers: 5.52); 8 rows in
 // flight at the compiler's own 128 registers (2 CTAs) 5.8, 4 at 114 registers 6.6, 3 at 64 registers 6.5, 5 at 80
 // (spills) 5.9, 16 at 242 registers 8.1
 #ifndef B200P_COMBINE_G
 #define B200P_COMBINE_G 4
 #endif
 #ifndef B200P_COMBINE_MINB
-#define B200P_COMBINE_MINB 3
+#define B200P_COMBINE_MINB 6
 #endif
 #ifndef B200P_COMBINE_ROWS
 #define B200P_COMBINE_ROWS 32
