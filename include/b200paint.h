@@ -285,7 +285,9 @@ int b200p_plan_build_hierarchy(b200p_plan *plan, const uint8_t *d_mask, const do
  * bytes; rhs (frames*C,h,w) fp64 (level 0: NULL, rhs is where(mask,known,0)). */
 int b200p_plan_level_ptrs(const b200p_plan *plan, int level, const uint8_t **d_mask,
                           const double **d_rhs);
-/* cascadic_init (multigrid.py:374-386) after build_hierarchy; d_u (frames*C,H,W). */
+/* cascadic_init (multigrid.py:374-386) after build_hierarchy; d_u (frames*C,H,W).
+ * Both stage calls below smooth with config.smoother (ORAS sweeps or CG steps,
+ * multigrid.py:264-279). */
 int b200p_plan_cascade(b200p_plan *plan, double *d_u, void *stream);
 /* v_cycle(hier, level, u, rhs, cfg, counters) (multigrid.py:335-371): one
  * V-cycle at `level` on d_u/d_rhs (frames*C planes of that level's shape),

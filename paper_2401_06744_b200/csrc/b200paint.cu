@@ -1880,6 +1880,34 @@ static int run_cg_pipeline(b200p_plan *pl, double *d_out, cudaStream_t st) {
     return 0;
 }
 
+// _cascade(to_tol = False) with the CG smoother (multigrid.py:389-422), the stage form behind
+// b200p_plan_cascade: coarsest level to min(coarse_tol, tol_rel), then prolongate + one smoothing unit per
+// level (none on the finest).  No report state is touched.
+static int cg_cascade_stage(b200p_plan *pl, double *d_out, cudaStream_t st) {
+    const int nl = (int)pl->lev.size();
+    const b200p_config &cfg = pl->cfg;
+    const double ctol = std::min(cfg.coarse_tol, cfg.tol_rel);
+    LevelHost &co = pl->lev[nl - 1];
+    double *cu = nl == 1 ? d_out : co.d_u;
+    int rc;
+    if ((rc = launch_flat_init(pl, co, cu, st))) return rc;
+    if ((rc = cg_run(pl, co, cu, co.d_rhs, true, cfg.coarse_max_iters, 1, ctol, 0.0, false, nullptr, st))) return rc;
+    const double *coarse_u = cu;
+    for (int l = nl - 2; l >= 0; --l) {
+        LevelHost &f = pl->lev[l];
+        double *uf = l == 0 ? d_out : f.d_u;
+        {
+            LaunchScope sc(pl, st, KK_PROLONG_SOL, field_bytes(pl, f, 1.25, 1.0));
+            if ((rc = launch_prolongate<true>(coarse_u, f.d_mask, f.d_rhs, f.info.height, f.info.width, pl->C, pl->P,
+                                              nullptr, uf, 0, 1 << 30, st)))
+                return rc;
+        }
+        if (l > 0 && (rc = cg_smooth(pl, f, uf, f.d_rhs, true, 1, nullptr, nullptr, st))) return rc;
+        coarse_u = uf;
+    }
+    return 0;
+}
+
 // _smooth_to_tol with the ORAS smoother on a multi-block level (multigrid.py:282-322): sweeps until
 // ||r|| <= tol_rel * denom per problem, denom = the level's flat-init defect, at most max_outer_iters.
 static int smooth_level_to_tol(b200p_plan *pl, LevelHost &f, UBuf &uf, bool record, cudaStream_t st) {
@@ -3389,6 +3417,7 @@ int b200p_plan_cascade(b200p_plan *pl, double *d_u, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     int rc = launch_set_int(pl, pl->d_units, pl->P, 0, st);
     if (rc) return rc;
+    if (pl->cfg.smoother == 1) return cg_cascade_stage(pl, d_u, st);
     return enqueue_cascade(pl, d_u, st);
 }
 
@@ -3400,10 +3429,15 @@ int b200p_plan_vcycle(b200p_plan *pl, int level, double *d_u, const double *d_rh
     cudaStream_t st = (cudaStream_t)stream;
     int rc = launch_set_int(pl, pl->d_units, pl->P, 0, st);
     if (rc) return rc;
-    UBuf u;
-    u.cur = d_u;
-    u.alt = pl->lev[level].d_u_alt;
-    if ((rc = enqueue_vcycle(pl, level, u, d_rhs, false, nullptr, pl->d_units, false, st))) return rc;
+    if (pl->cfg.smoother == 1) {
+        // CG-smoothed cycle (multigrid.py:278-279, 335-371): in place on d_u, units counted at level 0
+        if ((rc = cg_vcycle(pl, level, d_u, d_rhs, false, nullptr, pl->d_units, st))) return rc;
+    } else {
+        UBuf u;
+        u.cur = d_u;
+        u.alt = pl->lev[level].d_u_alt;
+        if ((rc = enqueue_vcycle(pl, level, u, d_rhs, false, nullptr, pl->d_units, false, st))) return rc;
+    }
     if (h_fine_units) {
         CU(cudaMemcpyAsync(h_fine_units, pl->d_units, pl->P * sizeof(int), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));

@@ -529,8 +529,8 @@ def _fmg_solve_stepwise(hier: LevelHierarchy, cfg: MultigridConfig, channel: int
     """fmg_solve with a per-cycle `callback(u)` (multigrid.py:466-481): the reference's own loop, driven from
     the host over the stage entry points (cascade, V-cycle, residual norm) instead of the one-graph solve,
     so that the iterate can be handed out after every cycle.  Same kernels, same cycle counts."""
-    if cfg.mode != "full_multigrid" or cfg.smoother != "oras":
-        raise NotImplementedError("callbacks are available for the mg-oras pipeline on the CUDA path")
+    if cfg.mode != "full_multigrid":
+        raise NotImplementedError("callbacks are available for the mg-oras / mg-cg pipelines on the CUDA path")
     t0 = time.perf_counter()
     p = hier.problem
     h, w = p.shape

@@ -704,6 +704,53 @@ def test_fmg_solve_callback_after_every_cycle():
         bp.solve_channel(prob, "ml-oras", cfg_b, channel=0, callback=lambda uu: None)
 
 
+def test_cg_smoother_stage_calls_and_callback():
+    """The stage entry points follow cfg.smoother (multigrid.py:278-279): `cascadic_init` and `v_cycle` with the
+    CG smoother run the CG-smoothed cascade / cycle (they used to run the ORAS ones), and
+    fmg_solve(..., callback=cb) hands out the mg-cg iterate after every V-cycle (multigrid.py:480-481)."""
+    m, k = oracle.seeded_problem(97, 131, 0.03, 2, channels=2)
+    cfg_o, cfg_b = _cfgs(16, 2, tol_rel=1e-6, smoother="cg")
+    _, cfg_oras = _cfgs(16, 2, tol_rel=1e-6)
+    prob = bp.InpaintingProblem(m, k)
+    hier = bp.build_hierarchy(prob, cfg_b)
+    ho = oracle.build_hierarchy(m, k, 1.0, cfg_o)
+    # cascade
+    u_c = bp.cascadic_init(hier, cfg_b, channel=0)
+    u_co = oracle.cascadic_init(ho, cfg_o, channel=0)
+    assert np.abs(u_c - u_co).max() <= 1e-9
+    assert np.abs(u_c - bp.cascadic_init(hier, cfg_oras, channel=0)).max() > 1e-6     # not the ORAS cascade
+    # one V-cycle at level 0 and at level 1
+    b0 = np.where(m, k[0], 0.0)
+    u, uo = u_c.copy(), u_co.copy()
+    cnt = {}
+    bp.v_cycle(hier, 0, u, b0, cfg_b, cnt)
+    fu = oracle.v_cycle(ho, 0, uo, b0, cfg_o)
+    assert cnt["fine_units"] == fu == cfg_b.nu_pre + cfg_b.nu_post
+    assert np.abs(u - uo).max() <= 1e-9
+    h1, w1 = ho.levels[1].shape
+    rhs1 = np.random.default_rng(5).standard_normal((h1, w1))
+    e, eo = np.zeros((h1, w1)), np.zeros((h1, w1))
+    bp.v_cycle(hier, 1, e, rhs1, cfg_b)
+    oracle.v_cycle(ho, 1, eo, rhs1, cfg_o)
+    assert np.abs(e - eo).max() <= 1e-9 * max(1.0, np.abs(eo).max())
+    # callbacks of mg-cg
+    for c in range(2):
+        seen = []
+        u, rep = bp.fmg_solve(hier, cfg_b, channel=c, callback=lambda uu: seen.append(uu.copy()))
+        u0, rep0 = bp.fmg_solve(hier, cfg_b, channel=c)
+        uo, ro = oracle.fmg_solve(ho, cfg_o, channel=c)
+        assert rep.solver == "mg-cg"
+        assert rep.iterations == rep0.iterations == ro.iterations == len(seen) > 1
+        assert rep.fine_smoother_iterations == ro.fine_smoother_iterations
+        np.testing.assert_allclose(rep.history, ro.history, rtol=1e-6)
+        assert np.array_equal(seen[-1], u) and not np.array_equal(seen[0], seen[-1])
+        assert np.abs(u - u0).max() <= 1e-9 and np.abs(u - uo).max() <= 1e-9
+    u1, _ = bp.solve_channel(prob, "mg-cg", cfg_b, channel=1, hierarchy=hier, callback=lambda uu: None)
+    assert np.array_equal(u1, u)
+    with pytest.raises(NotImplementedError):
+        bp.solve_channel(prob, "ml-cg", cfg_b, channel=0, callback=lambda uu: None)
+
+
 def test_band_combine_variant_agrees():
     """Experiment (B200P_BAND=1, -DB200P_EXPERIMENTS): the block solve writes the single-writer pixels itself,
     the combine pass visits the overlap bands only.  Same bits as the full combine (the tiles it skips are
