@@ -65,7 +65,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "50",
                  "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._pump, daemon=True)
             self.t.start()
@@ -74,9 +74,13 @@ class ClockSampler:
 
     def _pump(self):
         for line in self.proc.stdout:
-            self.rows.append(line.strip())
+            self.rows.append((time.monotonic(), line.strip()))
 
-    def stop(self):
+    def stop(self, t0=None, t1=None):
+        """Statistics of the samples taken between the host times t0 and t1 (the timed region).  The sampler is
+        started before the warm-up steps (nvidia-smi needs ~0.1 s to deliver its first row); when the timed
+        region is too short for three samples, the warm-up steps (the same work) are counted as well and
+        `window` says so."""
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -86,7 +90,12 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
+        rows = [r for (t, r) in self.rows if (t0 is None or t >= t0) and (t1 is None or t <= t1 + 0.05)]
+        window = "timed region"
+        if len(rows) < 3:
+            rows = [r for (t, r) in self.rows if t1 is None or t <= t1 + 0.05]
+            window = "warm-up + timed region"
+        for r in rows:
             f = [x.strip() for x in r.split(",")]
             if len(f) < 9:
                 continue
@@ -99,7 +108,8 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "samples": len(sm), "reasons": sorted(reasons)}
+                "sm_max_mhz": max(mx) if mx else None, "samples": len(sm), "window": window,
+                "reasons": sorted(reasons)}
 
 
 def workload_config(args, world, cycles, distinct_gpus):
@@ -477,21 +487,22 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    sampler = ClockSampler(local)
+    if rank == 0:
+        sampler.start()
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             _, reports = plan.solve_device(d_mask, d_known, d_out)
         barrier()
         l0 = plan.launch_count
-        sampler = ClockSampler(local)
-        if rank == 0:
-            sampler.start()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t_host0 = time.monotonic()
         e0.record(stream)
         for _ in range(args.steps):
             plan.solve_device(d_mask, d_known, d_out, want_reports=False)
         e1.record(stream)
         barrier()
-        clocks = sampler.stop() if rank == 0 else None
+        clocks = sampler.stop(t_host0, time.monotonic()) if rank == 0 else None
         launches = plan.launch_count - l0
         ms_total = e0.elapsed_time(e1)
     t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
