@@ -525,12 +525,56 @@ def v_cycle(hier: LevelHierarchy, level: int, u, rhs, cfg: MultigridConfig | Non
     return u
 
 
+def _ml_oras_solve_stepwise(hier: LevelHierarchy, cfg: MultigridConfig, channel: int, callback):
+    """fmg_solve in "multilevel" mode with the ORAS smoother and a `callback(u)` after every finest-level
+    sweep (multigrid.py:449-464, on_fine_state): the levels below the finest ARE the multilevel solve of the
+    level-1 problem (the hierarchy is recursive: multigrid.py:236-261), which runs on the fast path; its
+    result is prolongated (multigrid.py:407-410) and the finest level is smoothed to tolerance one sweep at a
+    time through `oras_sweeps(..., on_state=)` (_smooth_to_tol, multigrid.py:282-322)."""
+    from .pipelines import solve_image
+    from .solvers import BlockSolver, oras_sweeps
+    t0 = time.perf_counter()
+    s = cfg.solver
+    levels = hier.levels
+    fine = levels[0]
+    b = fine.rhs[channel]
+    baseline = float(np.linalg.norm(b - fine.op.apply(fine.flat_init(channel))))
+    if len(levels) == 1:
+        u = fine.flat_init(channel)
+        tol, max_units, denom = min(cfg.coarse_tol, s.tol_rel), cfg.coarse_max_iters, 0.0
+    else:
+        below = levels[1]
+        sub = InpaintingProblem(below.mask, below.rhs[channel], below.spacing)
+        u = prolongate_solution(solve_image(sub, "ml-oras", cfg).fields[0], fine.mask, b)
+        tol, max_units, denom = s.tol_rel, s.max_outer_iters, baseline
+    if denom == 0.0:
+        denom = float(np.linalg.norm(b - fine.op.apply(u)))
+    history, units, rel = [], 0, 0.0
+    if denom > 0.0:
+        def on_state(uu, rn_now, sweeps_done):
+            history.append(rn_now / denom)
+            if sweeps_done > 0:
+                callback(uu)
+
+        blocks = BlockSolver(fine.mask, fine.spacing, fine.part, fine.weights, s.alpha)
+        cap = s.local_max_iters or 4 * fine.part.block_h * fine.part.block_w
+        units, rn = oras_sweeps(fine.op, blocks, b, u, max_sweeps=max_units, stop_norm=tol * denom,
+                                eta=s.local_tol_fraction, local_max_iters=cap, on_state=on_state)
+        rel = rn / denom
+    return u, SolveReport(
+        solver="ml-oras", iterations=units, final_rel_residual=rel, wall_time=time.perf_counter() - t0,
+        history=history or [rel], converged=rel <= s.tol_rel, baseline_residual=baseline,
+        init_residual=baseline, fine_smoother_iterations=units)
+
+
 def _fmg_solve_stepwise(hier: LevelHierarchy, cfg: MultigridConfig, channel: int, callback):
     """fmg_solve with a per-cycle `callback(u)` (multigrid.py:466-481): the reference's own loop, driven from
     the host over the stage entry points (cascade, V-cycle, residual norm) instead of the one-graph solve,
     so that the iterate can be handed out after every cycle.  Same kernels, same cycle counts."""
+    if cfg.mode == "multilevel" and cfg.smoother == "oras":
+        return _ml_oras_solve_stepwise(hier, cfg, channel, callback)
     if cfg.mode != "full_multigrid":
-        raise NotImplementedError("callbacks are available for the mg-oras / mg-cg pipelines on the CUDA path")
+        raise NotImplementedError("callbacks of ml-cg (one per CG step) are not built on the CUDA path")
     t0 = time.perf_counter()
     p = hier.problem
     h, w = p.shape

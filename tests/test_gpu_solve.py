@@ -700,8 +700,35 @@ def test_fmg_solve_callback_after_every_cycle():
         assert rep.converged and rep.baseline_residual == pytest.approx(ro.baseline_residual, rel=1e-12)
     u1, _ = bp.solve_channel(prob, "mg-oras", cfg_b, channel=1, hierarchy=hier, callback=lambda uu: None)
     assert np.array_equal(u1, u)
-    with pytest.raises(NotImplementedError):
-        bp.solve_channel(prob, "ml-oras", cfg_b, channel=0, callback=lambda uu: None)
+
+
+@pytest.mark.parametrize("w,h,bs,ov", [(200, 144, 16, 2), (97, 131, 32, 6), (20, 30, 32, 6)])
+def test_ml_oras_callback_after_every_fine_sweep(w, h, bs, ov):
+    """fmg_solve(mode="multilevel", callback=cb) (multigrid.py:449-464): the iterate after every sweep of the
+    finest level; units, history and field as the one-call ml-oras solve and as the oracle.  (20, 30) is a
+    single-level hierarchy: the 'coarse' solve is the finest level (multigrid.py:398-405)."""
+    m, k = oracle.seeded_problem(w, h, 0.05, 13, channels=2)
+    cfg_o, cfg_b = _cfgs(bs, ov, tol_rel=1e-5, mode="multilevel")
+    prob = bp.InpaintingProblem(m, k)
+    hier = bp.build_hierarchy(prob, cfg_b)
+    ho = oracle.build_hierarchy(m, k, 1.0, cfg_o)
+    for c in range(2):
+        seen = []
+        u, rep = bp.solve_channel(prob, "ml-oras", cfg_b, channel=c, hierarchy=hier,
+                                  callback=lambda uu: seen.append(uu.copy()))
+        u0, rep0 = bp.solve_channel(prob, "ml-oras", cfg_b, channel=c, hierarchy=hier)
+        uo, ro = oracle.fmg_solve(ho, cfg_o, channel=c)
+        assert rep.solver == "ml-oras"
+        assert rep.iterations == rep0.iterations == ro.iterations == len(seen) >= 1
+        assert rep.fine_smoother_iterations == ro.fine_smoother_iterations
+        assert len(rep.history) == len(ro.history) == rep.iterations + 1
+        # (relative residuals near 1e-11 of the single-level case sit at the rounding level of the norm)
+        np.testing.assert_allclose(rep.history, ro.history, rtol=1e-6, atol=1e-13)
+        assert rep.final_rel_residual == pytest.approx(ro.final_rel_residual, rel=1e-6, abs=1e-13)
+        assert np.array_equal(seen[-1], u)
+        assert np.abs(u - u0).max() <= 1e-9 and np.abs(u - uo).max() <= 1e-9
+        assert rep.converged == ro.converged
+        assert rep.baseline_residual == pytest.approx(ro.baseline_residual, rel=1e-12)
 
 
 def test_cg_smoother_stage_calls_and_callback():
