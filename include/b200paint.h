@@ -112,6 +112,11 @@ typedef struct b200p_plan b200p_plan;
 enum { B200P_XCHG_SUM_RS = 1, B200P_XCHG_MAX_FLAGS = 2, B200P_XCHG_HALO_U = 3, B200P_XCHG_GATHER_RC = 4,
        B200P_XCHG_HALO_RC = 5 };
 typedef int (*b200p_exchange_fn)(void *user, int kind, void *d_ptr, void *stream);
+/* Per-step hook of the CG solvers (the `callback` of cg_solve, solvers.py:171-174, and of the "multilevel"
+ * mode with the CG smoother, multigrid.py:449-464 / 316-321): called on the calling thread after every CG step
+ * of the finest level with the iterate d_u ((frames*C, h, w) fp64 on the device, complete: the solve's stream
+ * has been synchronised); a non-zero return aborts the solve. */
+typedef int (*b200p_step_fn)(void *user, const double *d_u, int height, int width);
 
 const char *b200p_last_error(void);
 /* 1 when the library was built with -DB200P_EXPERIMENTS (block-solve variants that lost their A/B,
@@ -285,6 +290,9 @@ int b200p_plan_build_hierarchy(b200p_plan *plan, const uint8_t *d_mask, const do
  * bytes; rhs (frames*C,h,w) fp64 (level 0: NULL, rhs is where(mask,known,0)). */
 int b200p_plan_level_ptrs(const b200p_plan *plan, int level, const uint8_t **d_mask,
                           const double **d_rhs);
+/* Installs (fn != NULL) or removes the per-step hook; it applies to the solves of `cg` and `ml-cg` plans
+ * (config.smoother 1, mode 2 / 1), which then check their stop test on the host after every step. */
+int b200p_plan_set_step_callback(b200p_plan *plan, b200p_step_fn fn, void *user);
 /* cascadic_init (multigrid.py:374-386) after build_hierarchy; d_u (frames*C,H,W).
  * Both stage calls below smooth with config.smoother (ORAS sweeps or CG steps,
  * multigrid.py:264-279). */

@@ -278,6 +278,8 @@ struct b200p_plan {
     bool strip = false;
     b200p_exchange_fn exchange = nullptr;
     void *exchange_user = nullptr;
+    b200p_step_fn step_cb = nullptr;      // per-step hook of the recording CG runs (cg / ml-cg callbacks)
+    void *step_user = nullptr;
     // native strip exchange: NCCL calls issued by the library on the solve's stream (capturable)
     ncclComm_t nccl_comm = nullptr;
     int nccl_rank = 0, nccl_nranks = 1, strip_levels = 0;
@@ -1689,10 +1691,18 @@ static int cg_run(b200p_plan *pl, const LevelHost &L, double *u, const double *b
         cg_after_init_kernel<<<nb, 128, 0, st>>>(pl->P, S, denom_mode, tol, stop_abs, record ? 1 : 0);
         CU(cudaGetLastError());
     }
-    const bool host_checks = max_steps > 16;
+    // on_step (solvers.py:120-121): with a step hook on a recording run, the host looks at the step counters
+    // after every update and hands out the iterate while they advance
+    const bool hook = record && pl->step_cb;
+    std::vector<int> seen, now;
+    if (hook) {
+        seen.assign(pl->P, 0);
+        now.assign(pl->P, 0);
+    }
+    const bool host_checks = max_steps > 16 && !hook;
     int done = 0;
     while (done < max_steps) {
-        const int chunk = std::min(host_checks ? 8 : max_steps, max_steps - done);
+        const int chunk = hook ? 1 : std::min(host_checks ? 8 : max_steps, max_steps - done);
         if (host_checks) {
             int rc = launch_set_int(pl, pl->d_any, 1, 0, st);
             if (rc) return rc;
@@ -1714,6 +1724,16 @@ static int cg_run(b200p_plan *pl, const LevelHost &L, double *u, const double *b
                 LaunchScope sc(pl, st, KK_CONTROL, 0.0);
                 cg_after_update_kernel<<<nb, 128, 0, st>>>(pl->P, S, max_steps, record ? 1 : 0, denom_mode,
                                                           host_checks ? pl->d_any : nullptr);
+            }
+            if (hook) {
+                CU(cudaMemcpyAsync(now.data(), S.steps, pl->P * sizeof(int), cudaMemcpyDeviceToHost, st));
+                CU(cudaStreamSynchronize(st));
+                bool advanced = false;
+                for (int p = 0; p < pl->P; ++p) advanced = advanced || now[p] != seen[p];
+                seen = now;
+                if (!advanced) return 0;                       // every problem stopped (tolerance, breakdown)
+                const int crc = pl->step_cb(pl->step_user, u, L.info.height, L.info.width);
+                if (crc) return fail_arg(B200P_ERR_STATE, "step callback returned %d", crc);
             }
             {
                 LaunchScope sc(pl, st, KK_CG, 3.0 * fb);
@@ -3408,6 +3428,13 @@ int b200p_plan_level_ptrs(const b200p_plan *pl, int level, const uint8_t **d_mas
     if (!pl->hierarchy_ready) return fail_arg(B200P_ERR_STATE, "build_hierarchy has not run");
     if (d_mask) *d_mask = pl->lev[level].d_mask;
     if (d_rhs) *d_rhs = level == 0 ? nullptr : pl->lev[level].d_rhs;
+    return 0;
+}
+
+int b200p_plan_set_step_callback(b200p_plan *pl, b200p_step_fn fn, void *user) {
+    if (!pl) return fail_arg(B200P_ERR_ARG, "null argument");
+    pl->step_cb = fn;
+    pl->step_user = fn ? user : nullptr;
     return 0;
 }
 

@@ -525,6 +525,45 @@ def v_cycle(hier: LevelHierarchy, level: int, u, rhs, cfg: MultigridConfig | Non
     return u
 
 
+_STEP_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int)
+
+
+def _cg_solve_with_step_hook(problem: InpaintingProblem, cfg: MultigridConfig, channel: int, callback,
+                             single_level: bool):
+    """`cg` / `ml-cg` with `callback(u)` after every CG step of the finest level (solvers.py:171-174,
+    multigrid.py:316-321, 449-464): the solve itself is the library's (same kernels and report as without a
+    callback); `b200p_plan_set_step_callback` makes it check the step counters on the host after every update
+    and call back with the device iterate, which is copied out here."""
+    if not 0 <= channel < problem.channels:
+        raise IndexError(f"channel {channel} out of range")
+    h, w = problem.shape
+    plan = cached_plan(w, h, 1, 1, cfg, problem.spacing, single_level=single_level)
+    u = np.empty((h, w))
+    raised = []
+
+    def hook(_user, d_u, hh, ww):
+        try:
+            assert (hh, ww) == (h, w)
+            _dev.call("b200p_memcpy_d2h", u.ctypes.data, d_u, u.nbytes)
+            callback(u)
+            return 0
+        except BaseException as exc:  # noqa: BLE001 -- carried across the C frame and re-raised below
+            raised.append(exc)
+            return 1
+
+    fn = _STEP_FN(hook)
+    _dev.call("b200p_plan_set_step_callback", plan.handle, C.cast(fn, C.c_void_p), None)
+    try:
+        out, reports = plan.solve_host(problem.mask.view(np.uint8)[None], np.ascontiguousarray(problem.known[channel], dtype=np.float64)[None, None])
+    except Exception:
+        if raised:
+            raise raised[0]
+        raise
+    finally:
+        _dev.call("b200p_plan_set_step_callback", plan.handle, None, None)
+    return out[0, 0], reports[0]
+
+
 def _ml_oras_solve_stepwise(hier: LevelHierarchy, cfg: MultigridConfig, channel: int, callback):
     """fmg_solve in "multilevel" mode with the ORAS smoother and a `callback(u)` after every finest-level
     sweep (multigrid.py:449-464, on_fine_state): the levels below the finest ARE the multilevel solve of the
@@ -573,8 +612,8 @@ def _fmg_solve_stepwise(hier: LevelHierarchy, cfg: MultigridConfig, channel: int
     so that the iterate can be handed out after every cycle.  Same kernels, same cycle counts."""
     if cfg.mode == "multilevel" and cfg.smoother == "oras":
         return _ml_oras_solve_stepwise(hier, cfg, channel, callback)
-    if cfg.mode != "full_multigrid":
-        raise NotImplementedError("callbacks of ml-cg (one per CG step) are not built on the CUDA path")
+    if cfg.mode == "multilevel":
+        return _cg_solve_with_step_hook(hier.problem, cfg, channel, callback, single_level=False)
     t0 = time.perf_counter()
     p = hier.problem
     h, w = p.shape

@@ -100,7 +100,11 @@ def solve_channel(problem: InpaintingProblem, name: str, cfg: MultigridConfig | 
     if mode == "single":
         if callback is not None:
             if base != "oras":
-                raise NotImplementedError("per-step callbacks of the single-level CG solver are not built on the CUDA path")
+                from .multigrid import _cg_solve_with_step_hook
+                if not problem.mask.any():
+                    raise EmptyMaskError("cannot solve without known pixels")
+                return _cg_solve_with_step_hook(problem, replace(cfg or MultigridConfig(), smoother=base), channel,
+                                                callback, single_level=True)
             return _oras_solve_stepwise(problem, (cfg or MultigridConfig()), channel, callback)
         sub = InpaintingProblem(problem.mask, problem.known[channel], problem.spacing)
         res = solve_image(sub, name, cfg)

@@ -774,8 +774,51 @@ def test_cg_smoother_stage_calls_and_callback():
         assert np.abs(u - u0).max() <= 1e-9 and np.abs(u - uo).max() <= 1e-9
     u1, _ = bp.solve_channel(prob, "mg-cg", cfg_b, channel=1, hierarchy=hier, callback=lambda uu: None)
     assert np.array_equal(u1, u)
-    with pytest.raises(NotImplementedError):
-        bp.solve_channel(prob, "ml-cg", cfg_b, channel=0, callback=lambda uu: None)
+
+
+@pytest.mark.parametrize("w,h,bs,ov", [(97, 131, 16, 2), (20, 30, 32, 6)])
+def test_cg_step_callbacks(w, h, bs, ov):
+    """`cg` and `ml-cg` with callback=cb (solvers.py:171-174; multigrid.py:316-321, 449-464): one call per CG
+    step of the finest level with the live iterate, through b200p_plan_set_step_callback; steps, history and
+    fields as the solve without a callback and as the oracle; an exception of the callback aborts the solve
+    and surfaces; the hook is removed afterwards."""
+    m, k = oracle.seeded_problem(w, h, 0.05, 17, channels=2)
+    cfg_o, cfg_b = _cfgs(bs, ov, tol_rel=1e-6, smoother="cg", mode="multilevel")
+    prob = bp.InpaintingProblem(m, k)
+    ho = oracle.build_hierarchy(m, k, 1.0, cfg_o)
+    for c in range(2):
+        # ml-cg
+        seen = []
+        u, rep = bp.solve_channel(prob, "ml-cg", cfg_b, channel=c, callback=lambda uu: seen.append(uu.copy()))
+        u0, rep0 = bp.solve_channel(prob, "ml-cg", cfg_b, channel=c)
+        uo, ro = oracle.fmg_solve(ho, cfg_o, channel=c)
+        assert rep.solver == "ml-cg" and rep.iterations == rep0.iterations == ro.iterations == len(seen) >= 1
+        assert rep.history == rep0.history and len(rep.history) == len(ro.history)
+        np.testing.assert_allclose(rep.history, ro.history, rtol=1e-6, atol=1e-13)
+        assert np.array_equal(u, u0) and np.array_equal(seen[-1], u) and np.abs(u - uo).max() <= 1e-9
+        assert all(np.array_equal(s[m], k[c][m]) for s in seen)
+        if len(seen) > 1:
+            assert not np.array_equal(seen[0], seen[-1])
+        # cg
+        seen = []
+        u, rep = bp.solve_channel(prob, "cg", cfg_b, channel=c, callback=lambda uu: seen.append(uu.copy()))
+        u0, rep0 = bp.solve_channel(prob, "cg", cfg_b, channel=c)
+        uo, ro = oracle.cg_solve(m, k[c], 1.0, cfg_o.solver)
+        assert rep.solver == "cg" and rep.iterations == rep0.iterations == ro.iterations == len(seen) > 1
+        assert rep.history == rep0.history and len(rep.history) == len(ro.history) == rep.iterations + 1
+        np.testing.assert_allclose(rep.history, ro.history, rtol=1e-6, atol=1e-13)
+        assert np.array_equal(u, u0) and np.array_equal(seen[-1], u) and np.abs(u - uo).max() <= 1e-9
+
+    class Stop(Exception):
+        pass
+
+    def bad(uu):
+        raise Stop()
+
+    with pytest.raises(Stop):
+        bp.solve_channel(prob, "cg", cfg_b, channel=0, callback=bad)
+    u2, rep2 = bp.solve_channel(prob, "cg", cfg_b, channel=1)            # hook gone, plan still usable
+    assert np.array_equal(u2, u) and rep2.iterations == rep.iterations
 
 
 def test_band_combine_variant_agrees():
@@ -817,5 +860,3 @@ def test_single_level_oras_callback_after_every_sweep():
         assert np.array_equal(seen[-1], u) and not np.array_equal(seen[0], seen[-1])
         assert np.abs(u - u0).max() <= 1e-9 and np.abs(u - uo).max() <= 1e-9
         assert rep.converged and rep.fine_smoother_iterations == rep.iterations
-    with pytest.raises(NotImplementedError):
-        bp.solve_channel(prob, "cg", cfg, channel=0, callback=lambda uu: None)
