@@ -141,6 +141,42 @@ def cpu_sample(W, H, C, density, bs, ov, threads=0):
     return dt, out, reps, oracle.max_threads()
 
 
+def numpy_reference_sample(W, H, C, density, bs, ov, port_fields, port_reports):
+    """One frame of the workload through the UNMODIFIED NumPy reference package, when it was installed into
+    baseline/_ref (`pip install --no-index --no-deps --target baseline/_ref <copy of /root/reference/pkg>`,
+    DESIGN.md 7): its own `solve_image(InpaintingProblem, "mg-oras", cfg)` with its own thread pool, on the
+    same seed-0 frame as the port, whose output it is compared with.  Returns None when it is not there."""
+    ref_dir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "diffpaint")):
+        return None
+    try:
+        sys.path.insert(0, ref_dir)
+        import diffpaint  # noqa: F401
+        from diffpaint.core import InpaintingProblem
+        from diffpaint.multigrid import MultigridConfig
+        from diffpaint.pipelines import solve_image
+        from diffpaint.solvers import worker_count
+        import oracle
+        m, k = oracle.seeded_problem(W, H, density, 0, C)
+        os.environ.setdefault("INPAINT_THREADS", "0")         # 0 = all host cpus (solvers.py:31-40)
+        t0 = time.perf_counter()
+        res = solve_image(InpaintingProblem(m.astype(bool), k), "mg-oras", MultigridConfig(block_size=bs, overlap=ov))
+        dt = time.perf_counter() - t0
+        return {"value": 1.0 / dt, "unit": UNIT, "seconds_per_frame": dt, "kind": "reference",
+                "cores": int(worker_count()),
+                "sample": "1 frame (seed 0), diffpaint.pipelines.solve_image(problem, 'mg-oras', cfg) from baseline/_ref",
+                "v_cycles": [int(r.iterations) for r in res.reports],
+                "port_v_cycles": [int(r.iterations) for r in port_reports],
+                "max_abs_port_vs_reference": float(np.abs(res.fields - port_fields).max()),
+                "final_rel_residual": [float(r.final_rel_residual) for r in res.reports],
+                "port_final_rel_residual": [float(r.final_rel_residual) for r in port_reports]}
+    except Exception as exc:  # the port's line must not depend on this leg
+        return {"unavailable": f"{type(exc).__name__}: {exc}"}
+    finally:
+        if ref_dir in sys.path:
+            sys.path.remove(ref_dir)
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference algorithm on the host CPU (oracle port; the
     pure-Python reference package cannot travel to the GPU box)."""
@@ -156,7 +192,7 @@ def run_reference(args, rank, world):
     times, reps = [], []
     for _ in range(args.steps_ref):
         t0 = time.perf_counter()
-        _, reps = oracle.solve_image(m, k, 1.0, cfg)
+        port_fields, reps = oracle.solve_image(m, k, 1.0, cfg)
         times.append(time.perf_counter() - t0)
     ms = 1e3 * float(np.mean(times))
     fps = 1e3 / ms
@@ -175,6 +211,14 @@ def run_reference(args, rank, world):
         "note": "C oracle port of the reference algorithm (oracle/fmg_oracle.c); the NumPy reference "
                 "itself measured 0.027 frames/s on 8 cores in the build container (BASELINE.md)",
     }
+    if not args.no_numpy_reference:
+        npref = numpy_reference_sample(W, H, C, density, bs, ov, port_fields, reps)
+        if npref is not None:
+            line["numpy_reference"] = npref
+            if "value" in npref:
+                line["note"] = ("value / cpu_baseline: C oracle port of the reference algorithm (oracle/fmg_oracle.c), "
+                                "the faster of the two CPU implementations; numpy_reference: the unmodified reference "
+                                "package from baseline/_ref on one frame of the same workload in this run")
     print(json.dumps(line), flush=True)
 
 
@@ -411,6 +455,8 @@ def main():
                          "nccl = torch.distributed NCCL from a host callback; ipc = CUDA-IPC peer memory + gloo control")
     ap.add_argument("--strip-levels", type=int, default=2,
                     help="how many of the finest levels are striped in --strip mode (the rest is replicated)")
+    ap.add_argument("--no-numpy-reference", action="store_true",
+                    help="--impl reference: skip the one-frame leg through the NumPy reference of baseline/_ref")
     ap.add_argument("--traffic-child", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--no-traffic", action="store_true",
                     help="skip the same-run ncu pass behind roofline.traffic (falls back to profiles/traffic.json)")

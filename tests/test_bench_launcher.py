@@ -56,3 +56,21 @@ def test_more_gpus_than_devices_fails_loudly():
     assert r.returncode != 0
     assert "refusing to report" in (r.stderr + r.stdout)
     assert not any(l.startswith("{") and '"n_gpus"' in l for l in r.stdout.splitlines())
+
+
+def test_reference_arm_line_and_numpy_reference_leg():
+    """`bench.py --impl reference` (CPU only): the port's line carries the keys of the contract; when the
+    unmodified reference package is installed under baseline/_ref (git-ignored) the same run
+    also times one frame through it and pins the port against it on that frame."""
+    r = _run("--impl", "reference", "--workload", "256_gray_5pct_b16o2", "--steps", "1", "--warmup", "0")
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["impl"] == "reference" and d["gpu_launches"] == 0 and d["cpu_baseline"]["kind"] == "port"
+    assert d["e2e"]["value"] == d["value"] and d["e2e"]["h2d_bytes_per_step"] == 0
+    if os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "diffpaint")):
+        n = d["numpy_reference"]
+        assert n["kind"] == "reference" and n["value"] > 0
+        assert n["v_cycles"] == n["port_v_cycles"]
+        assert n["max_abs_port_vs_reference"] <= 1e-9
+    else:
+        assert "numpy_reference" not in d
