@@ -33,7 +33,7 @@ extern "C" {
 
 #define B200P_MAX_LEVELS 32
 #define B200P_ABI_VERSION 2    /* 2: b200p_config lost `spec_cycles`; history_len counts past the cap; image entry points */
-#define B200P_MAX_HISTORY 128  /* history entries STORED per report; history_len may be larger (see b200p_report) */
+#define B200P_MAX_HISTORY 128  /* history entries STORED per report; history_len may be larger (b200p_plan_history has all) */
 #define B200P_MAX_BLOCK 64     /* largest supported block edge */
 
 enum {
@@ -290,6 +290,13 @@ int b200p_plan_build_hierarchy(b200p_plan *plan, const uint8_t *d_mask, const do
  * bytes; rhs (frames*C,h,w) fp64 (level 0: NULL, rhs is where(mask,known,0)). */
 int b200p_plan_level_ptrs(const b200p_plan *plan, int level, const uint8_t **d_mask,
                           const double **d_rhs);
+/* SolveReport.history of problem `problem` (frame * C + channel) of the plan's last completed solve, whole:
+ * the reference never truncates it (solvers.py:60-75), the b200p_report record keeps only its first
+ * B200P_MAX_HISTORY values.  The plan's device buffer is sized from the config's iteration caps
+ * (v_cycles_max + 2; max(max_outer_iters, coarse_max_iters) + 2 for the ml- and single-level pipelines).
+ * Copies min(cap, stored capacity) doubles to h_out and returns that count (< 0: error); the valid prefix
+ * is report.history_len long. */
+int b200p_plan_history(b200p_plan *plan, int problem, double *h_out, int cap);
 /* Installs (fn != NULL) or removes the per-step hook; it applies to the solves of `cg` and `ml-cg` plans
  * (config.smoother 1, mode 2 / 1), which then check their stop test on the host after every step. */
 int b200p_plan_set_step_callback(b200p_plan *plan, b200p_step_fn fn, void *user);

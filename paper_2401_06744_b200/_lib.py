@@ -106,6 +106,7 @@ SIGNATURES = {
     "b200p_strip_ranges": (_I, [_I, _I, _I, _I, _I, _I, _VP]),
     "b200p_plan_set_strip": (_I, [_VP, _I, _VP, _VP, _VP]),
     "b200p_plan_set_step_callback": (_I, [_VP, _VP, _VP]),
+    "b200p_plan_history": (_I, [_VP, _I, _VP, _I]),
     "b200p_plan_level_rc": (_I, [_VP, _I, C.POINTER(_VP)]),
     "b200p_plan_device_bytes": (_I64, [_VP]),
     "b200p_plan_launch_count": (_I64, [_VP]),

@@ -278,6 +278,7 @@ struct b200p_plan {
     bool strip = false;
     b200p_exchange_fn exchange = nullptr;
     void *exchange_user = nullptr;
+    int hist_cap = B200P_MAX_HISTORY;     // values per problem in d_hist (sized from the config's iteration caps)
     b200p_step_fn step_cb = nullptr;      // per-step hook of the recording CG runs (cg / ml-cg callbacks)
     void *step_user = nullptr;
     // native strip exchange: NCCL calls issued by the library on the solve's stream (capturable)
@@ -389,7 +390,7 @@ static void prof_collect(b200p_plan *pl) {
 __global__ void fmg_control_kernel(int P, int stage, const double *rs, double tol, int cycles_max,
                                    double *baseline, double *denom, double *rel, double *hist,
                                    int *histlen, int *active, int *cycles, int *units, int *any,
-                                   int use_cond, cudaGraphConditionalHandle cond) {
+                                   int use_cond, cudaGraphConditionalHandle cond, int hist_cap) {
     // one CTA, problems strided over its threads: the "is any problem still active" verdict is
     // a CTA-wide OR, written to `any` (eager host loop) or to the WHILE node of the solve graph
     int mine = 0;
@@ -409,7 +410,7 @@ __global__ void fmg_control_kernel(int P, int stage, const double *rs, double to
             denom[p] = d;
             const double r = rn / d;
             rel[p] = r;
-            hist[(size_t)p * B200P_MAX_HISTORY] = r;
+            hist[(size_t)p * hist_cap] = r;
             histlen[p] = 1;
             const int act = (r > tol && 0 < cycles_max) ? 1 : 0;
             active[p] = act;
@@ -421,8 +422,8 @@ __global__ void fmg_control_kernel(int P, int stage, const double *rs, double to
         cycles[p] = c;
         const double r = rn / denom[p];
         rel[p] = r;
-        const int hl = histlen[p];   // counts every recorded value; the first B200P_MAX_HISTORY are stored
-        if (hl < B200P_MAX_HISTORY) hist[(size_t)p * B200P_MAX_HISTORY + hl] = r;
+        const int hl = histlen[p];   // counts every recorded value; the plan sizes hist_cap for its config
+        if (hl < hist_cap) hist[(size_t)p * hist_cap + hl] = r;
         histlen[p] = hl + 1;
         const int act = (r > tol && c < cycles_max) ? 1 : 0;
         active[p] = act;
@@ -439,7 +440,7 @@ __global__ void fmg_control_kernel(int P, int stage, const double *rs, double to
 // SolveReport fields of all problems into one (mapped, pinned) host record.
 __global__ void pack_reports_kernel(int P, const int *cycles, const int *units, const int *histlen,
                                     const double *baseline, const double *rel, const double *hist,
-                                    ReportPack out) {
+                                    int hist_cap, ReportPack out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < P) {
         out.cycles[i] = cycles[i];
@@ -448,7 +449,9 @@ __global__ void pack_reports_kernel(int P, const int *cycles, const int *units, 
         out.baseline[i] = baseline[i];
         out.rel[i] = rel[i];
     }
-    if (i < P * B200P_MAX_HISTORY) out.hist[i] = hist[i];
+    // the report record keeps the first B200P_MAX_HISTORY values of each problem (b200p_plan_history: all)
+    if (i < P * B200P_MAX_HISTORY)
+        out.hist[i] = hist[(size_t)(i / B200P_MAX_HISTORY) * hist_cap + i % B200P_MAX_HISTORY];
 }
 
 __global__ void set_int_kernel(int *p, int n, int v) {
@@ -481,7 +484,7 @@ __global__ void ml_level_begin_kernel(int P, const double *rs_base, double *deno
 // records the relative norm (history on the finest level), closes the gate on exit.
 __global__ void ml_gate_kernel(int P, const double *rs, double tol, int max_units, double *denom, int *gate,
                                const int *sweeps, double *rel, double *hist, int *histlen, int record,
-                               int *any) {
+                               int *any, int hist_cap) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= P || !gate[p]) return;
     const double r2 = rs[p];
@@ -499,8 +502,8 @@ __global__ void ml_gate_kernel(int P, const double *rs, double tol, int max_unit
     const double r = rn / d;
     rel[p] = r;
     if (record) {
-        const int hl = histlen[p];   // counts every recorded value; the first B200P_MAX_HISTORY are stored
-        if (hl < B200P_MAX_HISTORY) hist[(size_t)p * B200P_MAX_HISTORY + hl] = r;
+        const int hl = histlen[p];   // counts every recorded value; the plan sizes hist_cap for its config
+        if (hl < hist_cap) hist[(size_t)p * hist_cap + hl] = r;
         histlen[p] = hl + 1;
     }
     if (r2 == 0.0 || rn <= tol * d || sweeps[p] >= max_units) gate[p] = 0;
@@ -1385,7 +1388,7 @@ static int launch_coarse(b200p_plan *pl, const LevelHost &L, double *u, const do
     A.rel_out = rel_out;
     A.hist = record_history ? pl->d_hist : nullptr;
     A.histlen = pl->d_histlen;
-    A.hist_cap = B200P_MAX_HISTORY;
+    A.hist_cap = pl->hist_cap;
     const size_t n = (size_t)L.info.block_w * L.info.block_h;
     const size_t smem = smem_cg_bytes(L.info.block_w, L.info.block_h) + 2 * n * sizeof(double);
     LaunchScope sc(pl, st, KK_COARSE, field_bytes(pl, L, 3.0, 1.0));
@@ -1399,7 +1402,7 @@ static int launch_control(b200p_plan *pl, int stage, cudaStream_t st) {
     fmg_control_kernel<<<1, 128, 0, st>>>(
         pl->P, stage, pl->d_rs, pl->cfg.tol_rel, pl->cfg.v_cycles_max, pl->d_baseline, pl->d_denom,
         pl->d_rel, pl->d_hist, pl->d_histlen, pl->d_active, pl->d_cycles, pl->d_units, pl->d_any,
-        pl->cond_capture ? 1 : 0, pl->cond);
+        pl->cond_capture ? 1 : 0, pl->cond, pl->hist_cap);
     CU(cudaGetLastError());
     return 0;
 }
@@ -1951,7 +1954,8 @@ static int smooth_level_to_tol(b200p_plan *pl, LevelHost &f, UBuf &uf, bool reco
                 LaunchScope sc(pl, st, KK_CONTROL, 0.0);
                 ml_gate_kernel<<<nb, 128, 0, st>>>(pl->P, pl->d_rs, cfg.tol_rel, cfg.max_outer_iters,
                                                   pl->d_denom, pl->d_gate, pl->d_sweeps, pl->d_rel,
-                                                  pl->d_hist, pl->d_histlen, record ? 1 : 0, pl->d_any);
+                                                  pl->d_hist, pl->d_histlen, record ? 1 : 0, pl->d_any,
+                                                  pl->hist_cap);
                 CU(cudaGetLastError());
             }
             if ((rc = launch_sweep(pl, f, uf, f.d_rhs, true, pl->d_gate, pl->d_sweeps, -1, st))) return rc;
@@ -2509,8 +2513,17 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
     PTRY(dev_alloc(pl, &pl->d_baseline, (size_t)pl->P));
     PTRY(dev_alloc(pl, &pl->d_denom, (size_t)pl->P));
     PTRY(dev_alloc(pl, &pl->d_rel, (size_t)pl->P));
-    PTRY(dev_alloc(pl, &pl->d_hist, (size_t)pl->P * B200P_MAX_HISTORY));
-    CU(cudaMemset(pl->d_hist, 0, sizeof(double) * (size_t)pl->P * B200P_MAX_HISTORY));  // entries past histlen are copied out too
+    {
+        // every value the configured pipeline can record (SolveReport.history is never truncated in the
+        // reference): V-cycles + 1 for mg-*, one per sweep / step (+ the start) for ml-* and the single-level
+        // solvers, whose single-level hierarchies run under coarse_max_iters
+        const b200p_config &hc = pl->cfg;
+        long long need = (long long)hc.v_cycles_max + 2;
+        if (hc.mode != 0) need = std::max(need, (long long)std::max(hc.max_outer_iters, hc.coarse_max_iters) + 2);
+        pl->hist_cap = (int)std::min<long long>(std::max<long long>(need, B200P_MAX_HISTORY), 1 << 22);
+    }
+    PTRY(dev_alloc(pl, &pl->d_hist, (size_t)pl->P * pl->hist_cap));
+    CU(cudaMemset(pl->d_hist, 0, sizeof(double) * (size_t)pl->P * pl->hist_cap));  // entries past histlen are copied out too
     PTRY(dev_alloc(pl, &pl->d_gate, (size_t)pl->P));
     PTRY(dev_alloc(pl, &pl->d_sweeps, (size_t)pl->P));
     PTRY(dev_alloc(pl, &pl->d_rn, (size_t)pl->P));
@@ -2532,7 +2545,7 @@ int b200p_plan_create(const b200p_config *cfg, b200p_plan **out) {
         S.gate = pl->d_gate;
         S.hist = pl->d_hist;
         S.histlen = pl->d_histlen;
-        S.hist_cap = B200P_MAX_HISTORY;
+        S.hist_cap = pl->hist_cap;
     }
     {
         cudaError_t e = cudaMallocHost((void **)&pl->h_any, 64);
@@ -2822,7 +2835,7 @@ static int enqueue_reports(b200p_plan *pl, cudaStream_t st) {
     LaunchScope sc(pl, st, KK_CONTROL, 0.0);
     const int n = pl->P * B200P_MAX_HISTORY;
     pack_reports_kernel<<<(n + 255) / 256, 256, 0, st>>>(pl->P, pl->d_cycles, pl->d_units, pl->d_histlen,
-                                                        pl->d_baseline, pl->d_rel, pl->d_hist, pl->rep);
+                                                        pl->d_baseline, pl->d_rel, pl->d_hist, pl->hist_cap, pl->rep);
     CU(cudaGetLastError());
     return 0;
 }
@@ -3429,6 +3442,16 @@ int b200p_plan_level_ptrs(const b200p_plan *pl, int level, const uint8_t **d_mas
     if (d_mask) *d_mask = pl->lev[level].d_mask;
     if (d_rhs) *d_rhs = level == 0 ? nullptr : pl->lev[level].d_rhs;
     return 0;
+}
+
+int b200p_plan_history(b200p_plan *pl, int problem, double *h_out, int cap) {
+    if (!pl || !h_out) return fail_arg(B200P_ERR_ARG, "null argument");
+    if (problem < 0 || problem >= pl->P) return fail_arg(B200P_ERR_ARG, "bad problem index %d", problem);
+    if (cap < 0) return fail_arg(B200P_ERR_ARG, "bad capacity %d", cap);
+    const int n = std::min(cap, pl->hist_cap);
+    CU(cudaMemcpy(h_out, pl->d_hist + (size_t)problem * pl->hist_cap, sizeof(double) * (size_t)n,
+                  cudaMemcpyDeviceToHost));
+    return n;
 }
 
 int b200p_plan_set_step_callback(b200p_plan *pl, b200p_step_fn fn, void *user) {

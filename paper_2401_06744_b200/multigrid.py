@@ -154,27 +154,33 @@ class Plan:
         reps = []
         base = self.cfg.smoother
         name = base if self.single_level else ("ml-" if self.cfg.mode == "multilevel" else "mg-") + base
-        for r in raw:
+        for p, r in enumerate(raw):
             reps.append(SolveReport(
                 solver=name, iterations=r.iterations, final_rel_residual=r.final_rel_residual,
-                wall_time=wall, history=self._history(r),
+                wall_time=wall, history=self._history(r, p),
                 converged=bool(r.converged),
                 baseline_residual=r.baseline_residual, init_residual=r.init_residual,
                 fine_smoother_iterations=r.fine_smoother_iterations))
         return reps
 
-    @staticmethod
-    def _history(r):
-        """The report stores the first B200P_MAX_HISTORY values; a longer history (comparison pipelines that
-        record per sweep / step, v_cycles_max > 127) is returned as its stored head with the final value last,
-        so that history[-1] == final_rel_residual still holds, and a warning says how many were dropped."""
+    def _history(self, r, p):
+        """The report record stores the first B200P_MAX_HISTORY values; a longer history (comparison pipelines
+        that record per sweep / step, v_cycles_max > 127) is fetched whole from the plan's device buffer, which
+        is sized from the config's iteration caps (`b200p_plan_history`): never truncated, like the reference's
+        list.  Only a history past even that buffer (more than 2^22 values) is cut, loudly."""
         cap = len(r.history)
         if r.history_len <= cap:
             return list(r.history[: r.history_len]) or [r.final_rel_residual]
+        full = np.empty(r.history_len)
+        got = _lib.lib().b200p_plan_history(self.handle, int(p), full.ctypes.data, int(r.history_len))
+        if got < 0:
+            _lib.check(got)
+        if got >= r.history_len:
+            return full.tolist()
         import warnings
-        warnings.warn(f"residual history truncated: {r.history_len} values recorded, the first {cap - 1} and "
-                      f"the last are kept (B200P_MAX_HISTORY = {cap})", RuntimeWarning, stacklevel=3)
-        return list(r.history[: cap - 1]) + [r.final_rel_residual]
+        warnings.warn(f"residual history truncated: {r.history_len} values recorded, the first {got} and the "
+                      f"last are kept", RuntimeWarning, stacklevel=3)
+        return full[:got].tolist() + [r.final_rel_residual]
 
     def solve_device(self, d_mask, d_known, d_out=None, want_reports=True):
         """Device-resident solve: mask (F,H,W) uint8, known (F,C,H,W) float64 CUDA tensors."""

@@ -98,27 +98,38 @@ def test_plan_cache_eviction_keeps_live_hierarchies_valid():
     assert len(hier) == n        # clearing drops references only
 
 
-def test_long_histories_are_truncated_loudly():
-    """The report stores B200P_MAX_HISTORY = 128 values; the single-level Schwarz iteration records one per
-    sweep.  A longer history comes back as its first 127 values plus the final one (history[-1] ==
-    final_rel_residual, as in the reference) with a RuntimeWarning; short ones are unchanged."""
+def test_long_histories_come_back_whole():
+    """The report record stores B200P_MAX_HISTORY = 128 values; the single-level solvers record one per sweep /
+    step.  A longer history is fetched whole from the plan (b200p_plan_history; the device buffer is sized
+    from the config's iteration caps): len(history) == iterations + 1 and history[-1] == final_rel_residual as
+    in the reference (solvers.py:60-75), without a warning; short ones are unchanged."""
     import warnings
-    m, k = oracle.seeded_problem(320, 240, 0.003, 3, channels=1)
+    m, k = oracle.seeded_problem(320, 240, 0.003, 3, channels=2)
     cfg_b = bp.MultigridConfig(block_size=16, overlap=2, solver=bp.SolverConfig(tol_rel=1e-6, max_outer_iters=400))
-    with warnings.catch_warnings(record=True) as seen:
-        warnings.simplefilter("always")
-        res = bp.solve_image(bp.InpaintingProblem(m, k), "oras", cfg_b)
-    ref, ro = oracle.oras_solve(m, k[0], 1.0, 16, 2, oracle.SolverConfig(tol_rel=1e-6, max_outer_iters=400))
-    rep = res.reports[0]
-    assert rep.iterations == ro["iterations"] > 128
-    assert any(issubclass(w.category, RuntimeWarning) and "history truncated" in str(w.message) for w in seen)
-    assert len(rep.history) == 128 and rep.history[-1] == rep.final_rel_residual
-    np.testing.assert_allclose(rep.history[:127], ro["history"][:127], rtol=5e-3)  # 200+ sweeps: local stop decisions drift
-    assert np.abs(res.fields[0] - ref).max() <= 1e-3
     with warnings.catch_warnings():
         warnings.simplefilter("error")
+        res = bp.solve_image(bp.InpaintingProblem(m, k), "oras", cfg_b)
+        res_cg = bp.solve_image(bp.InpaintingProblem(m, k), "cg", cfg_b)
         short = bp.solve_image(bp.InpaintingProblem(m, k), "mg-oras", cfg_b)
-    assert len(short.reports[0].history) == short.reports[0].iterations + 1
+    for c in range(2):
+        ref, ro = oracle.oras_solve(m, k[c], 1.0, 16, 2, oracle.SolverConfig(tol_rel=1e-6, max_outer_iters=400))
+        rep = res.reports[c]
+        # 200+ sweeps at a contraction of ~0.95 per sweep: local stop decisions drift in the last digits, and the
+        # sweep that crosses tol_rel may differ by one (DESIGN.md 5)
+        assert rep.iterations > 128 and abs(rep.iterations - ro["iterations"]) <= 1
+        assert len(rep.history) == rep.iterations + 1
+        assert rep.history[-1] == rep.final_rel_residual
+        n = min(len(rep.history), len(ro["history"]))
+        np.testing.assert_allclose(rep.history[:n], ro["history"][:n], rtol=5e-3)
+        assert np.abs(res.fields[c] - ref).max() <= 1e-3
+        uo, rc = oracle.cg_solve(m, k[c], 1.0, oracle.SolverConfig(tol_rel=1e-6, max_outer_iters=400))
+        rg = res_cg.reports[c]
+        assert rg.iterations == rc.iterations > 128 and len(rg.history) == rg.iterations + 1
+        assert rg.history[-1] == rg.final_rel_residual
+        n = len(rc.history)                              # the oracle's own record keeps 256 values
+        np.testing.assert_allclose(rg.history[:n], rc.history, rtol=1e-5, atol=1e-13)
+        assert np.abs(res_cg.fields[c] - uo).max() <= 1e-8
+        assert len(short.reports[c].history) == short.reports[c].iterations + 1
 
 
 def test_solve_result_throughput_view_and_strip_output_ownership():
