@@ -465,8 +465,10 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
     # the CPU arm costs seconds per step: bound the run to a few minutes
-    args.steps_ref = max(1, min(args.steps, 5))
-    args.warmup_ref = max(0, min(args.warmup, 1))
+    # (one 4K frame = 2.4-2.6 s on 16 host threads: the driver's K and W are honoured as given up to 40 + 3 steps,
+    #  i.e. two minutes, plus ~20 s for the one frame through the NumPy reference)
+    args.steps_ref = max(1, min(args.steps, 40))
+    args.warmup_ref = max(0, min(args.warmup, 3))
 
     if args.gpus < 1:
         raise SystemExit("bench.py: --gpus must be >= 1")
